@@ -1,0 +1,406 @@
+"""Benchmark of the hot path: iterative reconstruction frames/s on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
+
+A *step* is one complete reconstruction of one frame (BASELINE.json config 3 by default:
+512^2 image, 512 sensors x 2048 samples, 10 iterations).  The timed region replays the
+captured solver graph on inputs already resident in HBM; successive steps cycle through
+distinct synthetic frames whose measurements together exceed the 126 MB L2.  ``e2e``
+repeats the measurement through the C-ABI host-buffer entry (pk_reconstruct_host):
+pinned fp64 y in, H2D, solve, D2H of the fp64 image, every step.
+
+N > 1 (torchrun, NCCL): ``--shard sensors`` (default; one frame split by sensors with an
+all-reduce of the image-sized gradient per iteration, strong scaling) or
+``--shard frames`` (independent frames per GPU, no collective, weak scaling).
+
+``--impl reference`` times the reference's CPU algorithm (the matrix-free fp64 C oracle
+restatement, all host threads -- the dense reference cannot hold config 3's 2.2 TB K).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG_CHOICES = ["cfg1", "cfg2", "cfg3", "cfg5"]
+METRIC = "frames/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg3", choices=CFG_CHOICES)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--shard", default="sensors", choices=["sensors", "frames"])
+    ap.add_argument("--frames", type=int, default=40, help="distinct frames cycled (> L2)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port, test infrastructure; only here and in tests/)
+
+
+def cpu_iteration_time(cfg, budget_s: float, threads: int = 0):
+    """Seconds per solver iteration of the fp64 matrix-free C oracle at `cfg`, measured on
+    as many whole iterations as fit in `budget_s` (at least one after a warm-up)."""
+    from oracle import pyoracle as O
+
+    s = O.make_scene(cfg.n, cfg.sensors, cfg.samples, 0)
+    op = O.Operator.of(s, threads=threads)
+    y = op.forward(s.phantom)  # warm-up and input
+    alpha, beta = 1e-3 * 1.0, 1e-5
+    step = 1e-3
+    shape = (s.ny, s.nx)
+    x = np.zeros(s.P)
+    r = -y
+    done, t0 = 0, time.perf_counter()
+    while True:
+        grad = 2.0 * op.adjoint(r)
+        grad += beta * O.tv_gradient(x.reshape(shape), 1e-3).reshape(-1)
+        x = O.soft_threshold(x - step * grad, step * alpha)
+        r = op.forward(x) - y
+        O.objective_parts(r, x, shape, alpha, beta)
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or (done >= 1 and el * (done + 1) / done > 4 * budget_s):
+            break
+    return el / done, done, O.lib().or_max_threads() if threads <= 0 else threads
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    K, W = args.steps, args.warmup
+    per = []
+    from oracle import pyoracle as O
+
+    s = O.make_scene(cfg.n, cfg.sensors, cfg.samples, 0)
+    op = O.Operator.of(s)
+    y = op.forward(s.phantom)
+    shape = (s.ny, s.nx)
+    cores = O.lib().or_max_threads()
+    x = np.zeros(s.P)
+    r = -y
+    for k in range(W + K):
+        t0 = time.perf_counter()
+        grad = 2.0 * op.adjoint(r)
+        grad += 1e-5 * O.tv_gradient(x.reshape(shape), 1e-3).reshape(-1)
+        x = O.soft_threshold(x - 1e-3 * grad, 1e-6)
+        r = op.forward(x) - y
+        O.objective_parts(r, x, shape, 1e-3, 1e-5)
+        if k >= W:
+            per.append(time.perf_counter() - t0)
+    t_it = float(np.mean(per))
+    fps = 1.0 / (t_it * cfg.iterations)
+    sample = (f"{K} timed solver iterations of {cfg.name} (1 iteration per step; frames/s = "
+              f"1/(10 x mean iteration time)), fp64 matrix-free C oracle port, {cores} threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
+        "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": t_it * 1e3,
+        "ms_per_iteration": t_it * 1e3, "higher_is_better": True, "scaling": "none",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (make_scene vessel phantom, seed 0)",
+        "config": {"workload": cfg.name, "image": f"{cfg.n}x{cfg.n}", "sensors": cfg.sensors,
+                   "samples": cfg.samples, "iterations": cfg.iterations, "parallelism": "cpu threads"},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def main():
+    args = parse()
+    from paper_2404_10928_b200.workloads import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2404_10928_b200 as pk
+    from paper_2404_10928_b200 import _native as N
+    from paper_2404_10928_b200.sharded import DeviceShardOps, SensorShardedSolver, shard_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    grid, ring, ac, ph0 = pk.make_scene(cfg.n, cfg.sensors, cfg.samples, seed=0)
+    M, Q, P = cfg.sensors, cfg.samples, cfg.pixels
+    F = max(1, args.frames)
+    sensor_mode = world > 1 and args.shard == "sensors"
+
+    # synthetic frames: vessel phantoms (seeds = frame index), measurements by the fp64
+    # device projector; pinned regularisation from frame 0 (outside timing, bench.py:226)
+    op64 = pk.operator_for(grid, ring, ac, pk.CudaPool(local, "float64"))
+    Ys = []
+    for f in range(F):
+        phf = ph0 if f == 0 else pk.make_vessel_phantom(grid, f)
+        Ys.append(op64.matvec(phf.values).float())
+    Y = torch.stack(Ys)  # [F, M*Q] fp32 on the device
+    del Ys
+    K64 = pk.build_time_matrix(grid, ring, ac)
+    y0 = pk.SensorData("time", M, Q, Y[0].double().cpu().numpy())
+    pinned = pk.resolve_config(pk.ReconConfig(iterations=cfg.iterations), K64, y0,
+                               pool=pk.CudaPool(local, "float64"))
+    alpha, beta, step = pinned.alpha, pinned.beta, pinned.step
+    params = pk.solver.solver_params(pinned, alpha, beta, step)
+
+    if sensor_mode:
+        m0, m1 = shard_range(M, rank, world)
+        ops = DeviceShardOps(grid, ring, ac, pk.CudaPool(local, "float32"), m0, m1)
+        solver = SensorShardedSolver(ops)
+        Yl = Y[:, m0 * Q : m1 * Q].contiguous()
+
+        def one_step(f):
+            solver.solve(Yl[f], pinned, alpha, beta, step)
+        launches_per_step = 1 + 3 * cfg.iterations + 3 * cfg.iterations  # residual(3)/bp/update(2)
+    else:
+        op = pk.operator_for(grid, ring, ac, pk.CudaPool(local, "float32"))
+        x_out = torch.empty(P, device=dev, dtype=torch.float32)
+        hist = torch.zeros(4 * cfg.iterations, device=dev, dtype=torch.float64)
+        status = torch.zeros(2, device=dev, dtype=torch.int32)
+        stream_ptr = lambda: __import__("ctypes").c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        lib = N.load()
+        import ctypes
+
+        def one_step(f):
+            N.check(lib.pk_reconstruct(op.handle, ctypes.byref(params), Y[f].data_ptr(),
+                                       x_out.data_ptr(), hist.data_ptr(), status.data_ptr(),
+                                       stream_ptr()))
+        launches_per_step = 3 + 3 * cfg.iterations
+
+    frame_base = rank * 7919  # different frames per rank in frames mode
+
+    def frame(k):
+        return (frame_base + k) % F
+
+    for k in range(args.warmup):
+        one_step(frame(k))
+    torch.cuda.synchronize(dev)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    # keep the GPU busy while the sampler spins up, then time exactly K steps
+    t_spin = time.perf_counter()
+    while time.perf_counter() - t_spin < 0.3:
+        one_step(frame(0))
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(args.steps):
+        one_step(frame(args.warmup + k))
+    e1.record()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t[0])
+    frames_total = args.steps * (1 if sensor_mode else world)
+    fps = frames_total / (ms_max * 1e-3)
+    ms_step = ms_max / args.steps
+
+    # ---- roofline of the dominant kernel (CUDA events around each launch) ----
+    roof, kernels = None, None
+    if not sensor_mode:
+        fl = (ctypes.c_float * 3)()
+        nl = ctypes.c_int32()
+        prof_iters = cfg.iterations
+        reps = 5
+        tot = np.zeros(3)
+        for r_ in range(reps):
+            N.check(lib.pk_profile_iterations(op.handle, ctypes.byref(params), Y[frame(r_)].data_ptr(),
+                                              fl, ctypes.byref(nl), stream_ptr()))
+            tot += np.array(fl[:])
+        per_launch_ms = tot / (reps * prof_iters)
+        peak = ctypes.c_double()
+        N.check(lib.pk_measure_fp32_peak(local, ctypes.byref(peak)))
+        flops_per_launch = 12.0 * M * P  # 12 FP32 flops per sensor-pixel pair
+        names = ["K1 bp_update (back-projection + TV + prox)", "K2 projection (fixed-point scatter)",
+                 "K3 residual/objective"]
+        kernels = {}
+        for i, nm in enumerate(names):
+            ach = flops_per_launch / (per_launch_ms[i] * 1e-3) / 1e12 if i < 2 else None
+            kernels[nm] = {"ms_per_launch": float(per_launch_ms[i]),
+                           "achieved_tflops": ach, "frac": (ach / peak.value) if ach else None,
+                           "share_of_step": float(per_launch_ms[i] / per_launch_ms.sum())}
+        dom = int(np.argmax(per_launch_ms[:2]))
+        achieved = flops_per_launch / (per_launch_ms[dom] * 1e-3) / 1e12
+        traffic = None
+        prof_json = os.path.join(ROOT, "profiles", "ncu_summary.json")
+        if os.path.exists(prof_json):
+            try:
+                traffic = json.load(open(prof_json)).get("dram_bytes_per_launch", {}).get(
+                    ["bp_f32", "fp_f32"][dom])
+            except Exception:
+                traffic = None
+        roof = {"bound": "fp32", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
+                "frac": achieved / peak.value, "traffic": traffic,
+                "kernel": names[dom],
+                "peak_source": "measured live: FFMA microkernel (pk_measure_fp32_peak); "
+                               "MEASURED_PEAKS.json has no FP32 figure",
+                "work": f"12 flops x {M} sensors x {P} pixels per launch"}
+
+    # ---- end to end through the C-ABI host-buffer entry ----
+    e2e = None
+    if not args.no_e2e and not sensor_mode:
+        nF = min(F, 4)
+        yh = torch.empty((nF, M * Q), dtype=torch.float64, pin_memory=True)
+        yh.copy_(Y[:nF].double().cpu())
+        yh_np = yh.numpy()
+        xo = torch.empty(P, dtype=torch.float64, pin_memory=True).numpy()
+        hh = torch.empty(4 * cfg.iterations, dtype=torch.float64, pin_memory=True).numpy()
+        sh = torch.empty(2, dtype=torch.int32, pin_memory=True).numpy()
+        dp = ctypes.POINTER(ctypes.c_double)
+        ip = ctypes.POINTER(ctypes.c_int32)
+
+        def host_step(f):
+            N.check(lib.pk_reconstruct_host(op.handle, ctypes.byref(params),
+                                            yh_np[f].ctypes.data_as(dp), xo.ctypes.data_as(dp),
+                                            hh.ctypes.data_as(dp), sh.ctypes.data_as(ip), stream_ptr()))
+        for k in range(args.warmup):
+            host_step(k % nF)
+        torch.cuda.synchronize(dev)
+        ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ee0.record()
+        for k in range(args.steps):
+            host_step(k % nF)
+        ee1.record()
+        torch.cuda.synchronize(dev)
+        ms_e2e = ee0.elapsed_time(ee1)
+        e2e = {"value": args.steps / (ms_e2e * 1e-3) * world, "unit": "frames/s",
+               "h2d_bytes_per_step": M * Q * 8,
+               "d2h_bytes_per_step": P * 8 + 4 * cfg.iterations * 8 + 8,
+               "ms_per_step": ms_e2e / args.steps,
+               "path": "pk_reconstruct_host (C ABI, pinned fp64 host buffers)"}
+
+    # ---- CPU baseline (rank 0, N = 1) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        t_it, n_it, cores = cpu_iteration_time(cfg, args.cpu_seconds)
+        cpu = {"value": 1.0 / (t_it * cfg.iterations), "unit": "frames/s", "cores": cores,
+               "kind": "port",
+               "sample": f"{n_it} solver iteration(s) of {cfg.name}; frames/s = 1/({cfg.iterations} x "
+                         f"{t_it:.3f} s); fp64 matrix-free C oracle (oracle/pact_oracle.c)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "ms_per_iteration": ms_step / cfg.iterations,
+            "higher_is_better": True,
+            "scaling": "strong" if sensor_mode else ("weak" if world > 1 else "none"),
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: make_scene vessel phantoms (seed = frame), y = K x by the fp64 device projector",
+            "config": {"workload": cfg.name, "image": f"{cfg.n}x{cfg.n}", "sensors": M, "samples": Q,
+                       "iterations": cfg.iterations,
+                       "parallelism": (f"sensor-shard x{world} + NCCL all-reduce" if sensor_mode
+                                       else f"frames x{world}" if world > 1 else "single GPU"),
+                       "l2": f"{F} distinct frames cycled ({F * M * Q * 4 / 2**20:.0f} MiB of y > 126 MB L2)",
+                       "pinned": {"alpha": alpha, "beta": beta, "step": step}},
+            "clocks": clk,
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": roof,
+            "kernels": kernels,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

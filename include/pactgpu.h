@@ -1,0 +1,163 @@
+/*
+ * pactgpu.h -- C ABI of the B200-native iterative photoacoustic reconstruction
+ * hot path (arXiv 2404.10928's `pactkit`).
+ *
+ * The reference has no FFI: its hot products go through the Python seam
+ *   forward._matvec(K, x, pool)          pkg/src/pactkit/forward.py:237-241
+ *   forward._adjoint_matvec(K, y, pool)  pkg/src/pactkit/forward.py:244-250
+ * into numba GEMV cores (pkg/src/pactkit/kernels.py:185-225), driven by
+ *   recon.iterative_reconstruct          pkg/src/pactkit/recon.py:286-377.
+ * The entry points below are what a binding of that seam needs: an operator
+ * "plan" built from the geometry the reference's MeasurementMatrix carries in
+ * its provenance (grid / ring / acoustic, forward.py:70-121), the two
+ * products, the device-resident solver loop, and the sensor-sharded pieces.
+ *
+ * Conventions
+ *   - every call returns an int status: PK_OK (0) or a negative PK_ERR_*;
+ *     pk_last_error() gives a thread-local message for the last failure.
+ *   - no torch / C++ types: plain pointers and sizes.  `*_dev` pointers are
+ *     caller-owned device buffers on the plan's device; `stream` is a
+ *     cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - element type of every image / trace buffer is the plan's dtype
+ *     (PK_F32: float, PK_F64: double) unless stated otherwise.
+ *   - no host synchronisation and no allocation inside the hot calls
+ *     (pk_matvec, pk_adjoint_matvec, pk_reconstruct, pk_grad_update);
+ *     all workspace is owned by the plan.  One plan may be used by one stream
+ *     at a time.
+ *   - image layout: row-major, index j*nx + i (geometry.py:59-68).
+ *     trace layout: sensor-major, index (m - sensor_begin)*samples + s
+ *     (forward.py:124-128, MeasurementMatrix rows m*Q + s, forward.py:70-76).
+ */
+#ifndef PACTGPU_H
+#define PACTGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PK_OK 0
+#define PK_ERR_INVALID -1     /* bad argument (the reference raises ValueError) */
+#define PK_ERR_CUDA -2        /* CUDA runtime error */
+#define PK_ERR_UNSUPPORTED -3 /* geometry/config the kernels do not handle */
+#define PK_ERR_GEOMETRY -4    /* sensor coincides with a pixel (GeometryError, forward.py:161-163) */
+
+#define PK_F32 0
+#define PK_F64 1
+
+/* stopped_by codes (ReconResult.stopped_by, recon.py:82-93) */
+#define PK_STOP_MAX_ITERATIONS 0
+#define PK_STOP_TOLERANCE 1
+#define PK_STOP_DIVERGENCE 2
+
+typedef struct pk_geometry_desc {
+    int32_t nx, ny;          /* ImagingGrid.nx / .ny */
+    const double* pixel_x;   /* host [nx]: origin[0] + i*dx  (geometry.py:61-63) */
+    const double* pixel_y;   /* host [ny]: origin[1] + j*dx  (geometry.py:62-64) */
+    int32_t sensors;         /* TransducerRing.count */
+    const double* sensor_xy; /* host [sensors*2]: TransducerRing.positions (geometry.py:96-102) */
+    int32_t sensor_begin;    /* this plan's shard of sensors [begin, end) */
+    int32_t sensor_end;      /*   (whole ring: 0, sensors) */
+    int32_t samples;         /* AcousticConfig.q_s */
+    double c, dt;            /* AcousticConfig.c, .dt (forward.py:39-57) */
+    int32_t dtype;           /* PK_F32 or PK_F64 */
+    int32_t device;          /* CUDA device ordinal */
+} pk_geometry_desc;
+
+typedef struct pk_plan pk_plan;
+
+typedef struct pk_plan_info {
+    int32_t local_sensors;   /* sensor_end - sensor_begin */
+    int32_t pixels;          /* nx * ny */
+    int32_t dtype;
+    int32_t may_truncate;    /* 1 if some delay may leave the 1..q_s window (forward.py:196-205) */
+    double c_dt;             /* c*dt as the reference forms it (forward.py:180) */
+    double weight;           /* 1/(2*pi*c) (forward.py:183) */
+    int32_t bp_tile, bp_window, bp_chunk, bp_buffers; /* back-projector tiling */
+    int32_t fp_tile, fp_window, fp_bits;              /* projector tiling, fixed-point bits */
+    int64_t device_bytes;    /* workspace held by the plan */
+} pk_plan_info;
+
+typedef struct pk_solver_params {
+    double alpha, beta;      /* pinned ReconConfig.alpha / .beta (recon.py:46-79) */
+    double step;             /* pinned eta */
+    double tv_epsilon;
+    double tolerance;
+    int32_t iterations;
+    int32_t nonneg;
+} pk_solver_params;
+
+/* Build the operator for one geometry (replaces build_time_matrix, forward.py:167-215,
+ * without materialising K).  Uploads geometry, sizes tiles, allocates workspace. */
+int pk_plan_create(const pk_geometry_desc* desc, pk_plan** out);
+int pk_plan_destroy(pk_plan* plan);
+int pk_plan_get_info(const pk_plan* plan, pk_plan_info* out);
+
+/* out_dev[(m-begin)*Q + s] = (K x)[m*Q + s] for the plan's sensors.
+ * Replaces forward._matvec (forward.py:237-241) -> kernels.matvec_parallel. */
+int pk_matvec(pk_plan* plan, const void* x_dev, void* out_dev, void* stream);
+
+/* out_dev[p] = scale * sum_{m in shard} sum_s K[m*Q+s, p] * y[(m-begin)*Q + s].
+ * scale = 1 replaces forward._adjoint_matvec (forward.py:244-250); scale = 2 gives the
+ * data gradient 2 K^T r of recon.py:139-143 (summed over shards by the caller). */
+int pk_adjoint_matvec(pk_plan* plan, const void* y_dev, void* out_dev, double scale, void* stream);
+
+/* The whole proximal-gradient loop of iterative_reconstruct (recon.py:318-363) on the
+ * device, for a plan that owns all sensors: x0 = 0, r = -y, per iteration the fused
+ * back-projection + TV + soft-threshold (+ nonneg) update, the projection + residual,
+ * the objective and the stopping rules (non-finite, 5-streak, tolerance).
+ *   y_dev          [M*Q] measurements (plan dtype)
+ *   x_out_dev      [P] final image (plan dtype)
+ *   history_dev    [4*iterations] double: objective, data, l1, tv per accepted iteration
+ *   status_dev     [2] int32: iterations_run, stopped_by (PK_STOP_*)
+ * Asynchronous on `stream`; captured into a CUDA graph on first use per iteration count. */
+int pk_reconstruct(pk_plan* plan, const pk_solver_params* params, const void* y_dev,
+                   void* x_out_dev, double* history_dev, int32_t* status_dev, void* stream);
+
+/* Same with host buffers: y_host is double [M*Q] (SensorData.values), x_out_host double [P],
+ * history_host double [4*iterations], status_host int32 [2].  Copies in, solves, copies out,
+ * synchronises the stream.  Pinned host memory gives asynchronous copies. */
+int pk_reconstruct_host(pk_plan* plan, const pk_solver_params* params, const double* y_host,
+                        double* x_out_host, double* history_host, int32_t* status_host,
+                        void* stream);
+
+/* Sensor-sharded building block: given the globally reduced gradient
+ * grad_dev = 2 K^T r (summed over all shards), apply recon.py:330-338
+ *   x_out = S_{eta*alpha}(x - eta*(grad + beta*tv_grad(x)))   (+ max(.,0) if nonneg)
+ * and write sums_dev[3] (double): sum|x_out|, TV(x_out), non-finite count. */
+int pk_grad_update(pk_plan* plan, const pk_solver_params* params, const void* x_dev,
+                   const void* grad_dev, void* x_out_dev, double* sums_dev, void* stream);
+
+/* Residual of the shard: r_out = K_shard x - y_shard (trace layout) and
+ * sumsq_dev[0] = sum r^2 (double).  The plan keeps r for the next pk_adjoint_residual. */
+int pk_residual(pk_plan* plan, const void* x_dev, const void* y_dev, void* r_out_dev,
+                double* sumsq_dev, void* stream);
+/* out_dev = scale * K_shard^T r for the residual kept by the last pk_residual. */
+int pk_adjoint_residual(pk_plan* plan, void* out_dev, double scale, void* stream);
+
+/* Index dump (verification): for local sensors [ma, mb) (relative to sensor_begin),
+ * s0_dev[(m-ma)*P + p] = floor(hypot(px - sx, py - sy) / (c*dt)) and frac_dev likewise,
+ * evaluated in fp64 exactly as forward.py:157-182 (s0 int64, frac double; frac may be NULL). */
+int pk_index_dump(pk_plan* plan, int32_t ma, int32_t mb, int64_t* s0_dev, double* frac_dev,
+                  void* stream);
+
+/* Profiling hook (bench.py roofline): run the solver's kernels un-graphed on `stream`
+ * for params->iterations iterations, with CUDA events around every launch.
+ * ms_out[0..2] = summed device milliseconds of K1 (fused back-projection update),
+ * K2 (projection) and K3 (residual/objective); launches_out[0] = kernels launched.
+ * Synchronises the stream. */
+int pk_profile_iterations(pk_plan* plan, const pk_solver_params* params, const void* y_dev,
+                          float* ms_out, int32_t* launches_out, void* stream);
+
+/* FP32 roofline denominator: FFMA throughput of `device` measured with a dependent-chain
+ * microkernel (8 independent chains per thread, 148*4 CTAs), in TFLOP/s. */
+int pk_measure_fp32_peak(int32_t device, double* tflops_out);
+
+const char* pk_last_error(void);
+int pk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PACTGPU_H */

@@ -1,0 +1,53 @@
+"""B200-native iterative photoacoustic reconstruction (hot path of arXiv 2404.10928).
+
+Drop-in for the reference package ``pactkit``'s reconstruction / projection API
+(pkg/src/pactkit/__init__.py:10-78, hot-path subset): the same names, signatures and
+result types, with every product running matrix-free in sm_100a CUDA kernels behind the
+C ABI of include/pactgpu.h.  Pass ``pool=CudaPool(device, dtype)`` where the reference
+takes a ``WorkerPool``; ``pool=None`` uses ``CudaPool()`` (cuda:0, float32).
+"""
+
+from .device import CudaPool, DeviceOperator, clear_plan_cache, operator_for
+from .measurement import (
+    AcousticConfig,
+    DenseOperator,
+    MeasurementMatrix,
+    SensorData,
+    TruncationWarning,
+    add_noise,
+    build_time_matrix,
+    forward_project,
+)
+from .scene import (
+    GeometryError,
+    ImageField,
+    ImagingGrid,
+    TransducerRing,
+    centered_grid,
+    check_enclosure,
+    field_from_image,
+    make_grid,
+    make_point_phantom,
+    make_ring,
+    make_vessel_phantom,
+)
+from .solver import (
+    ObjectiveParts,
+    ReconConfig,
+    ReconResult,
+    back_project,
+    data_gradient,
+    estimate_lipschitz,
+    iterative_reconstruct,
+    objective,
+    psnr,
+    resolve_config,
+    resolve_regularization,
+    rmse,
+    soft_threshold,
+    tv_gradient,
+    tv_value,
+)
+from .workloads import CONFIGS, make_scene
+
+__version__ = "1.0.0"

@@ -1,0 +1,741 @@
+// pactgpu.cu -- C ABI (include/pactgpu.h) over the sm_100a kernels in pk_kernels.cuh.
+//
+// Host-side responsibilities: validate the geometry the reference's MeasurementMatrix
+// carries (forward.py:70-121), pick tile / window sizes, own the device workspace, and
+// sequence the kernels of each entry point on the caller's stream.  pk_reconstruct is
+// captured once per iteration count into a CUDA graph and replayed.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "pactgpu.h"
+#include "pk_kernels.cuh"
+
+using namespace pk;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+#define PK_CUDA(call)                                                                    \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return fail(PK_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                             \
+    } while (0)
+
+#define PK_CHECK_LAUNCH()                                                                 \
+    do {                                                                                  \
+        cudaError_t e_ = cudaGetLastError();                                              \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(PK_ERR_CUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                              \
+    } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int ceil_log2(double v) {
+    int b = 0;
+    while ((double)(1ull << b) < v && b < 62) ++b;
+    return b;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+int alloc(pk_plan* p, T** ptr, size_t count) {
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(ptr), count * sizeof(T));
+    if (e != cudaSuccess)
+        return fail(PK_ERR_CUDA, "cudaMalloc(%zu) failed: %s", count * sizeof(T),
+                    cudaGetErrorString(e));
+    p->device_bytes += (int64_t)(count * sizeof(T));
+    return PK_OK;
+}
+
+#define PK_TRY(x)               \
+    do {                        \
+        int rc_ = (x);          \
+        if (rc_ != PK_OK) return rc_; \
+    } while (0)
+
+void free_plan(pk_plan* p) {
+    if (!p) return;
+    DeviceGuard g(p->device);
+    if (p->graph_exec) cudaGraphExecDestroy(p->graph_exec);
+    if (p->graph) cudaGraphDestroy(p->graph);
+    void* ptrs[] = {p->pxs, p->pys, p->sxs, p->sys, p->px, p->py, p->sx, p->sy, p->table,
+                    p->acc, p->xbuf[0], p->xbuf[1], p->ydev, p->y64, p->x64, p->hist_dev,
+                    p->status_dev, p->part_bp, p->part_tv, p->part_r, p->part_misc, p->state,
+                    p->params, p->io, p->xout_dev};
+    for (void* q : ptrs)
+        if (q) cudaFree(q);
+    if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+    delete p;
+}
+
+size_t tsize(const pk_plan* p) { return p->dtype == PK_F32 ? 4 : 8; }
+
+// ---------------------------------------------------------------------------
+// kernel sequences
+
+int launch_maxabs(pk_plan* p, const void* x, cudaStream_t s) {
+    const int blocks = p->misc_blocks;
+    if (p->dtype == PK_F32)
+        maxabs_kernel<float><<<blocks, kThreads, 0, s>>>(static_cast<const float*>(x), p->P,
+                                                         p->part_misc, p->state, p->fp_bits);
+    else
+        maxabs_kernel<double><<<blocks, kThreads, 0, s>>>(static_cast<const double*>(x), p->P,
+                                                          p->part_misc, p->state, p->fp_bits);
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+// K2: x == nullptr -> solver mode (x from the iterate ring)
+int launch_fp(pk_plan* p, const void* x, int solver, cudaStream_t s) {
+    dim3 grid(p->fp_tiles_x * p->fp_tiles_y, p->fp_groups);
+    if (p->dtype == PK_F32) {
+        FpArgs a{};
+        a.x = static_cast<const float*>(x);
+        a.xb0 = static_cast<const float*>(p->xbuf[0]);
+        a.xb1 = static_cast<const float*>(p->xbuf[1]);
+        a.pxs = p->pxs; a.pys = p->pys; a.sxs = p->sxs; a.sys = p->sys;
+        a.acc = p->acc;
+        a.nx = p->nx; a.ny = p->ny; a.M = p->M; a.Q = p->Q; a.T = p->fp_T; a.L = p->fp_L;
+        a.tiles_x = p->fp_tiles_x;
+        a.qclamp = (float)p->Q + 1.5f;
+        a.st = p->state; a.part_tv = p->part_tv; a.solver = solver;
+        fp_f32_kernel<false><<<grid, kThreads, p->fp_smem, s>>>(a);
+    } else {
+        FpArgs64 a{};
+        a.x = static_cast<const double*>(x);
+        a.xb0 = static_cast<const double*>(p->xbuf[0]);
+        a.xb1 = static_cast<const double*>(p->xbuf[1]);
+        a.px = p->px; a.py = p->py; a.sx = p->sx; a.sy = p->sy; a.cdt = p->cdt;
+        a.acc = p->acc;
+        a.nx = p->nx; a.ny = p->ny; a.M = p->M; a.Q = p->Q; a.T = p->fp_T; a.L = p->fp_L;
+        a.tiles_x = p->fp_tiles_x;
+        a.st = p->state; a.part_tv = p->part_tv; a.solver = solver;
+        fp_f64_kernel<<<grid, kThreads, p->fp_smem, s>>>(a);
+    }
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+int launch_finalize(pk_plan* p, const void* y, void* trace_out, double* sumsq, int solver,
+                    cudaStream_t s) {
+    const size_t sm = (size_t)p->Q * tsize(p);
+    if (p->dtype == PK_F32) {
+        FinArgs<float> a{};
+        a.acc = p->acc; a.y = static_cast<const float*>(y);
+        a.trace_out = static_cast<float*>(trace_out);
+        a.table = static_cast<float2*>(p->table);
+        a.M = p->M; a.Q = p->Q; a.TS = p->TS; a.w = p->w;
+        a.st = p->state; a.prm = p->params; a.io = p->io; a.part_r = p->part_r;
+        a.part_tv = p->part_tv; a.ntv = p->fp_tiles_x * p->fp_tiles_y; a.sumsq_out = sumsq;
+        a.solver = solver;
+        finalize_kernel<float><<<p->M, kThreads, sm, s>>>(a);
+    } else {
+        FinArgs<double> a{};
+        a.acc = p->acc; a.y = static_cast<const double*>(y);
+        a.trace_out = static_cast<double*>(trace_out);
+        a.table = static_cast<double2*>(p->table);
+        a.M = p->M; a.Q = p->Q; a.TS = p->TS; a.w = p->w;
+        a.st = p->state; a.prm = p->params; a.io = p->io; a.part_r = p->part_r;
+        a.part_tv = p->part_tv; a.ntv = p->fp_tiles_x * p->fp_tiles_y; a.sumsq_out = sumsq;
+        a.solver = solver;
+        finalize_kernel<double><<<p->M, kThreads, sm, s>>>(a);
+    }
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+// K1: epi == 0 -> out = gscale_mult * w * K^T r; epi == 1 -> fused update (solver)
+int launch_bp(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_t s) {
+    const bool clamp = p->max_delay >= (double)p->Q + 0.5;
+    if (p->dtype == PK_F32) {
+        BpArgs a{};
+        a.table = static_cast<const float2*>(p->table);
+        a.pxs = p->pxs; a.pys = p->pys; a.sxs = p->sxs; a.sys = p->sys;
+        a.nx = p->nx; a.ny = p->ny; a.M = p->M; a.Q = p->Q; a.TS = p->TS; a.L = p->bp_L;
+        a.CS = p->bp_CS; a.nbuf = p->bp_nbuf; a.tiles_x = p->bp_tiles_x;
+        a.qclamp = (float)p->Q + 1.5f;
+        a.out = static_cast<float*>(out);
+        a.gscale = (float)(gscale_mult * p->w);
+        a.xb0 = static_cast<float*>(p->xbuf[0]);
+        a.xb1 = static_cast<float*>(p->xbuf[1]);
+        a.prm = p->params; a.st = p->state; a.part = p->part_bp; a.bits = p->fp_bits;
+        const int grid = p->bp_tiles_x * p->bp_tiles_y;
+        if (epi) {
+            if (clamp) bp_f32_kernel<true, true><<<grid, kThreads, p->bp_smem, s>>>(a);
+            else bp_f32_kernel<true, false><<<grid, kThreads, p->bp_smem, s>>>(a);
+        } else {
+            if (clamp) bp_f32_kernel<false, true><<<grid, kThreads, p->bp_smem, s>>>(a);
+            else bp_f32_kernel<false, false><<<grid, kThreads, p->bp_smem, s>>>(a);
+        }
+    } else {
+        BpArgs64 a{};
+        a.table = static_cast<const double2*>(p->table);
+        a.px = p->px; a.py = p->py; a.sx = p->sx; a.sy = p->sy; a.cdt = p->cdt;
+        a.nx = p->nx; a.ny = p->ny; a.M = p->M; a.Q = p->Q; a.TS = p->TS;
+        a.out = static_cast<double*>(out);
+        a.gscale = gscale_mult * p->w;
+        a.xb0 = static_cast<double*>(p->xbuf[0]);
+        a.xb1 = static_cast<double*>(p->xbuf[1]);
+        a.prm = p->params; a.st = p->state; a.part = p->part_bp; a.bits = p->fp_bits;
+        const int grid = (p->P + kThreads - 1) / kThreads;
+        if (epi) bp_f64_kernel<true><<<grid, kThreads, 0, s>>>(a);
+        else bp_f64_kernel<false><<<grid, kThreads, 0, s>>>(a);
+    }
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+int launch_table(pk_plan* p, const void* y, int init, cudaStream_t s) {
+    if (p->dtype == PK_F32)
+        table_kernel<float><<<p->M, kThreads, 0, s>>>(
+            static_cast<const float*>(y), p->io, static_cast<float2*>(p->table), p->M, p->Q, p->TS,
+            init ? -1.f : 1.f, p->part_r, p->state, init);
+    else
+        table_kernel<double><<<p->M, kThreads, 0, s>>>(
+            static_cast<const double*>(y), p->io, static_cast<double2*>(p->table), p->M, p->Q,
+            p->TS, init ? -1.0 : 1.0, p->part_r, p->state, init);
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+// the solver graph body: x0 = 0, r0 = -y, N x (K1 update, K2, K3), copy-out
+int record_solver(pk_plan* p, int iters, cudaStream_t s) {
+    const int pb = (p->P + kThreads - 1) / kThreads;
+    if (p->dtype == PK_F32)
+        init_kernel<float><<<pb, kThreads, 0, s>>>(static_cast<float*>(p->xbuf[0]), p->P, p->state,
+                                                   p->io);
+    else
+        init_kernel<double><<<pb, kThreads, 0, s>>>(static_cast<double*>(p->xbuf[0]), p->P,
+                                                    p->state, p->io);
+    PK_CHECK_LAUNCH();
+    PK_TRY(launch_table(p, nullptr, 1, s));
+    for (int it = 0; it < iters; ++it) {
+        PK_TRY(launch_bp(p, 1, nullptr, 2.0, s));
+        PK_TRY(launch_fp(p, nullptr, 1, s));
+        PK_TRY(launch_finalize(p, nullptr, nullptr, nullptr, 1, s));
+    }
+    const int cb = std::min(pb, 148 * 4);
+    if (p->dtype == PK_F32)
+        copy_out_kernel<float><<<cb, kThreads, 0, s>>>(static_cast<const float*>(p->xbuf[0]),
+                                                       static_cast<const float*>(p->xbuf[1]),
+                                                       p->state, p->io, p->P);
+    else
+        copy_out_kernel<double><<<cb, kThreads, 0, s>>>(static_cast<const double*>(p->xbuf[0]),
+                                                        static_cast<const double*>(p->xbuf[1]),
+                                                        p->state, p->io, p->P);
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+int check_params(const pk_solver_params* prm) {
+    if (!prm) return fail(PK_ERR_INVALID, "params is NULL");
+    if (prm->iterations < 1) return fail(PK_ERR_INVALID, "iterations must be >= 1");
+    if (!(prm->alpha >= 0) || !(prm->beta >= 0))
+        return fail(PK_ERR_INVALID, "alpha and beta must be >= 0");
+    if (!(prm->step > 0)) return fail(PK_ERR_INVALID, "step must be > 0");
+    if (!(prm->tv_epsilon > 0)) return fail(PK_ERR_INVALID, "tv_epsilon must be > 0");
+    if (!(prm->tolerance >= 0)) return fail(PK_ERR_INVALID, "tolerance must be >= 0");
+    return PK_OK;
+}
+
+int upload_params(pk_plan* p, const pk_solver_params* prm, cudaStream_t s) {
+    DevParams d{};
+    d.alpha = prm->alpha;
+    d.beta = prm->beta;
+    d.step = prm->step;
+    d.eps = prm->tv_epsilon;
+    d.tolerance = prm->tolerance;
+    d.eta_alpha = prm->step * prm->alpha;  // recon.py:336 passes eta * alpha
+    d.iterations = prm->iterations;
+    d.nonneg = prm->nonneg ? 1 : 0;
+    PK_CUDA(cudaMemcpyAsync(p->params, &d, sizeof(d), cudaMemcpyHostToDevice, s));
+    return PK_OK;
+}
+
+int ensure_hist(pk_plan* p, int iters) {
+    if (p->hist_cap >= iters) return PK_OK;
+    if (p->hist_dev) cudaFree(p->hist_dev);
+    p->hist_dev = nullptr;
+    PK_TRY(alloc(p, &p->hist_dev, (size_t)4 * iters));
+    p->hist_cap = iters;
+    return PK_OK;
+}
+
+}  // namespace
+
+namespace pk {
+// FP32 peak microkernel: 8 independent FFMA chains per thread, immediate-free operands
+__global__ void __launch_bounds__(kThreads) ffma_peak_kernel(float* out, int iters) {
+    float a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+          a6 = a0 + 6, a7 = a0 + 7;
+    const float b = 1.0001f + 1e-9f * blockIdx.x, c = 0.9999f;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            a0 = fmaf(a0, b, c); a1 = fmaf(a1, b, c); a2 = fmaf(a2, b, c); a3 = fmaf(a3, b, c);
+            a4 = fmaf(a4, b, c); a5 = fmaf(a5, b, c); a6 = fmaf(a6, b, c); a7 = fmaf(a7, b, c);
+        }
+    }
+    out[blockIdx.x * kThreads + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+}  // namespace pk
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* pk_last_error(void) { return g_err; }
+
+int pk_version(void) { return 10000; /* 1.0.0 */ }
+
+int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
+    if (!d || !out) return fail(PK_ERR_INVALID, "NULL argument");
+    *out = nullptr;
+    if (d->nx < 1 || d->ny < 1) return fail(PK_ERR_INVALID, "grid dimensions must be >= 1");
+    if (d->sensors < 1) return fail(PK_ERR_INVALID, "sensor count must be >= 1");
+    if (d->samples < 1) return fail(PK_ERR_INVALID, "samples must be >= 1");
+    if (!(d->c > 0) || !(d->dt > 0)) return fail(PK_ERR_INVALID, "c and dt must be > 0");
+    if (d->sensor_begin < 0 || d->sensor_end > d->sensors || d->sensor_begin >= d->sensor_end)
+        return fail(PK_ERR_INVALID, "bad sensor shard [%d, %d) of %d", d->sensor_begin,
+                    d->sensor_end, d->sensors);
+    if (d->dtype != PK_F32 && d->dtype != PK_F64) return fail(PK_ERR_INVALID, "bad dtype");
+    if (!d->pixel_x || !d->pixel_y || !d->sensor_xy) return fail(PK_ERR_INVALID, "NULL geometry");
+    if ((int64_t)d->nx * d->ny > (int64_t)1 << 30) return fail(PK_ERR_UNSUPPORTED, "grid too large");
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(PK_ERR_CUDA, "no CUDA device available (the B200 kernels have no CPU fallback)");
+    if (d->device < 0 || d->device >= ndev) return fail(PK_ERR_INVALID, "bad device %d", d->device);
+    DeviceGuard guard(d->device);
+
+    pk_plan* p = new pk_plan();
+    p->device = d->device;
+    p->dtype = d->dtype;
+    p->nx = d->nx; p->ny = d->ny; p->P = d->nx * d->ny;
+    p->Mall = d->sensors; p->m0 = d->sensor_begin; p->M = d->sensor_end - d->sensor_begin;
+    p->Q = d->samples;
+    p->c = d->c; p->dt = d->dt;
+    p->cdt = d->c * d->dt;                       // forward.py:180
+    p->w = 1.0 / (2.0 * 3.141592653589793 * d->c);  // forward.py:183
+
+    // pixel / sensor geometry; delay bounds per sensor from the grid rectangle
+    const double* X = d->pixel_x;
+    const double* Y = d->pixel_y;
+    const double* SP = d->sensor_xy + 2 * (size_t)d->sensor_begin;
+    for (int i = 1; i < p->nx; ++i)
+        if (!(X[i] > X[i - 1])) { free_plan(p); return fail(PK_ERR_INVALID, "pixel_x must increase"); }
+    for (int j = 1; j < p->ny; ++j)
+        if (!(Y[j] > Y[j - 1])) { free_plan(p); return fail(PK_ERR_INVALID, "pixel_y must increase"); }
+    const double xl = X[0], xh = X[p->nx - 1], yl = Y[0], yh = Y[p->ny - 1];
+    double dmin_all = 1e300, dmax_all = 0;
+    for (int m = 0; m < p->M; ++m) {
+        const double sx = SP[2 * m], sy = SP[2 * m + 1];
+        const double cx = std::min(std::max(sx, xl), xh), cy = std::min(std::max(sy, yl), yh);
+        const double dmin = std::hypot(cx - sx, cy - sy);
+        const double dmax = std::hypot(std::max(std::fabs(xl - sx), std::fabs(xh - sx)),
+                                       std::max(std::fabs(yl - sy), std::fabs(yh - sy)));
+        dmin_all = std::min(dmin_all, dmin);
+        dmax_all = std::max(dmax_all, dmax);
+        if (dmin == 0.0) {  // sensor inside the grid rectangle: exact coincidence check
+            const double* ix = std::find(X, X + p->nx, sx);
+            const double* iy = std::find(Y, Y + p->ny, sy);
+            if (ix != X + p->nx && iy != Y + p->ny) {
+                free_plan(p);
+                return fail(PK_ERR_GEOMETRY, "sensor %d coincides with pixel index %lld",
+                            m + d->sensor_begin,
+                            (long long)((iy - Y) * p->nx + (ix - X)));
+            }
+        }
+    }
+    p->min_delay = dmin_all / p->cdt;
+    p->max_delay = dmax_all / p->cdt;
+    p->may_truncate = (p->min_delay < 1.001 || p->max_delay > (double)p->Q - 1.001) ? 1 : 0;
+
+    // tiling.  h = pixel pitch in samples.
+    const double hx = p->nx > 1 ? (X[p->nx - 1] - X[0]) / (p->nx - 1) / p->cdt : 0.0;
+    const double hy = p->ny > 1 ? (Y[p->ny - 1] - Y[0]) / (p->ny - 1) / p->cdt : 0.0;
+    const double h = std::max(hx, hy);
+    auto tile_diag = [&](int T) {
+        const double ex = std::min(T - 1, p->nx - 1) * hx, ey = std::min(T - 1, p->ny - 1) * hy;
+        return std::sqrt(ex * ex + ey * ey);
+    };
+    p->TS = (p->Q + 2 + 1) & ~1;
+    // back-projector
+    p->bp_tiles_x = (p->nx + kBpTile - 1) / kBpTile;
+    p->bp_tiles_y = (p->ny + kBpTile - 1) / kBpTile;
+    p->bp_L = ((int)std::ceil(tile_diag(kBpTile)) + 6 + 1) & ~1;
+    if (p->bp_L > p->TS) p->bp_L = p->TS;
+    p->bp_nbuf = 3;
+    const int bp_budget = 72 * 1024;
+    p->bp_CS = std::max(1, std::min(32, bp_budget / (p->bp_nbuf * p->bp_L * 8)));
+    p->bp_smem = p->bp_nbuf * p->bp_CS * p->bp_L * 8 + p->bp_nbuf * p->bp_CS * 16 + p->bp_nbuf * 8;
+    if (p->dtype == PK_F32 && p->bp_smem > 200 * 1024) {
+        free_plan(p);
+        return fail(PK_ERR_UNSUPPORTED, "delay window per tile too long (%d samples)", p->bp_L);
+    }
+    // projector
+    p->fp_T = 32;
+    p->fp_tiles_x = (p->nx + p->fp_T - 1) / p->fp_T;
+    p->fp_tiles_y = (p->ny + p->fp_T - 1) / p->fp_T;
+    p->fp_groups = (p->M + 31) / 32;
+    p->fp_L = (int)std::ceil(tile_diag(p->fp_T)) + 6;
+    // contributions one window slot can receive: tile pixels in a band of 2 samples
+    double nc_tile = 1.5 * (p->fp_T * std::sqrt(2.0) + 2) * (2.0 / std::max(h, 1e-12) + 2);
+    if (p->min_delay < 8.0 * p->fp_T * std::max(h, 1.0)) nc_tile = (double)p->fp_T * p->fp_T;
+    nc_tile = std::min(nc_tile, (double)p->fp_T * p->fp_T);
+    if (p->dtype == PK_F32) {
+        p->fp_bits = std::min(22, 30 - ceil_log2(nc_tile));
+        p->fp_smem = p->fp_L * 32 * 4 + p->fp_T * p->fp_T * 16 + p->fp_T * 4;
+    } else {
+        double nc_glob = std::min((double)p->P, 4.0 * (p->nx + p->ny) * (2.0 / std::max(h, 1e-12) + 2));
+        if (p->min_delay < 8.0 * p->fp_T * std::max(h, 1.0)) nc_glob = (double)p->P;
+        p->fp_bits = std::min(62 - ceil_log2(nc_tile), 62 - ceil_log2(nc_glob));
+        p->fp_bits = std::min(p->fp_bits, 52);
+        p->fp_smem = p->fp_L * 32 * 8 + p->fp_T * p->fp_T * 24 + p->fp_T * 4;
+    }
+    if (p->fp_smem > 200 * 1024) {
+        free_plan(p);
+        return fail(PK_ERR_UNSUPPORTED, "projector window too long (%d samples)", p->fp_L);
+    }
+    p->misc_blocks = std::max(1, std::min(1024, (p->P + kThreads - 1) / kThreads));
+
+    // allocations
+    int rc = PK_OK;
+    auto A = [&](int r) { if (rc == PK_OK) rc = r; };
+    std::vector<float> fx(p->nx), fy(p->ny), fsx(p->M), fsy(p->M);
+    std::vector<double> dsx(p->M), dsy(p->M);
+    for (int i = 0; i < p->nx; ++i) fx[i] = (float)(X[i] / p->cdt);
+    for (int j = 0; j < p->ny; ++j) fy[j] = (float)(Y[j] / p->cdt);
+    for (int m = 0; m < p->M; ++m) {
+        dsx[m] = SP[2 * m];
+        dsy[m] = SP[2 * m + 1];
+        fsx[m] = (float)(SP[2 * m] / p->cdt);
+        fsy[m] = (float)(SP[2 * m + 1] / p->cdt);
+    }
+    A(alloc(p, &p->pxs, p->nx)); A(alloc(p, &p->pys, p->ny));
+    A(alloc(p, &p->sxs, p->M)); A(alloc(p, &p->sys, p->M));
+    A(alloc(p, &p->px, p->nx)); A(alloc(p, &p->py, p->ny));
+    A(alloc(p, &p->sx, p->M)); A(alloc(p, &p->sy, p->M));
+    const size_t ts = tsize(p);
+    A(alloc(p, reinterpret_cast<unsigned char**>(&p->table), (size_t)p->M * p->TS * 2 * ts));
+    A(alloc(p, &p->acc, (size_t)p->M * p->Q));
+    A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[0]), (size_t)p->P * ts));
+    A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[1]), (size_t)p->P * ts));
+    A(alloc(p, &p->part_bp, (size_t)4 * std::max(p->bp_tiles_x * p->bp_tiles_y,
+                                                 (p->P + kThreads - 1) / kThreads)));
+    A(alloc(p, &p->part_tv, (size_t)p->fp_tiles_x * p->fp_tiles_y));
+    A(alloc(p, &p->part_r, (size_t)p->M));
+    A(alloc(p, &p->part_misc, (size_t)4 * p->misc_blocks));
+    A(alloc(p, &p->state, 1));
+    A(alloc(p, &p->params, 1));
+    A(alloc(p, &p->io, 1));
+    if (rc != PK_OK) { free_plan(p); return rc; }
+    cudaError_t e = cudaSuccess;
+    auto up = [&](void* dst, const void* src, size_t n) {
+        if (e == cudaSuccess) e = cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
+    };
+    up(p->pxs, fx.data(), p->nx * 4); up(p->pys, fy.data(), p->ny * 4);
+    up(p->sxs, fsx.data(), p->M * 4); up(p->sys, fsy.data(), p->M * 4);
+    up(p->px, X, p->nx * 8); up(p->py, Y, p->ny * 8);
+    up(p->sx, dsx.data(), p->M * 8); up(p->sy, dsy.data(), p->M * 8);
+    if (e == cudaSuccess) e = cudaMemset(p->acc, 0, (size_t)p->M * p->Q * 8);
+    if (e == cudaSuccess) e = cudaMemset(p->state, 0, sizeof(DevState));
+    if (e == cudaSuccess) e = cudaMemset(p->table, 0, (size_t)p->M * p->TS * 2 * ts);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess && p->dtype == PK_F32) {
+        e = cudaFuncSetAttribute(bp_f32_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->bp_smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(bp_f32_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->bp_smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(bp_f32_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->bp_smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(bp_f32_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->bp_smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(fp_f32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->fp_smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(finalize_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->Q * 4);
+    } else if (e == cudaSuccess) {
+        e = cudaFuncSetAttribute(fp_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->fp_smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(finalize_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->Q * 8);
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        free_plan(p);
+        return fail(PK_ERR_CUDA, "plan setup failed: %s", cudaGetErrorString(e));
+    }
+    if ((size_t)p->Q * ts > 200 * 1024) {
+        free_plan(p);
+        return fail(PK_ERR_UNSUPPORTED, "trace of %d samples exceeds shared memory", p->Q);
+    }
+    *out = p;
+    return PK_OK;
+}
+
+int pk_plan_destroy(pk_plan* p) {
+    free_plan(p);
+    return PK_OK;
+}
+
+int pk_plan_get_info(const pk_plan* p, pk_plan_info* o) {
+    if (!p || !o) return fail(PK_ERR_INVALID, "NULL argument");
+    o->local_sensors = p->M;
+    o->pixels = p->P;
+    o->dtype = p->dtype;
+    o->may_truncate = p->may_truncate;
+    o->c_dt = p->cdt;
+    o->weight = p->w;
+    o->bp_tile = p->dtype == PK_F32 ? kBpTile : 1;
+    o->bp_window = p->bp_L;
+    o->bp_chunk = p->bp_CS;
+    o->bp_buffers = p->bp_nbuf;
+    o->fp_tile = p->fp_T;
+    o->fp_window = p->fp_L;
+    o->fp_bits = p->fp_bits;
+    o->device_bytes = p->device_bytes;
+    return PK_OK;
+}
+
+int pk_matvec(pk_plan* p, const void* x, void* out, void* stream) {
+    if (!p || !x || !out) return fail(PK_ERR_INVALID, "NULL argument");
+    DeviceGuard g(p->device);
+    cudaStream_t s = S(stream);
+    PK_TRY(launch_maxabs(p, x, s));
+    PK_TRY(launch_fp(p, x, 0, s));
+    PK_TRY(launch_finalize(p, nullptr, out, nullptr, 0, s));
+    return PK_OK;
+}
+
+int pk_adjoint_matvec(pk_plan* p, const void* y, void* out, double scale, void* stream) {
+    if (!p || !y || !out) return fail(PK_ERR_INVALID, "NULL argument");
+    DeviceGuard g(p->device);
+    cudaStream_t s = S(stream);
+    PK_TRY(launch_table(p, y, 0, s));
+    PK_TRY(launch_bp(p, 0, out, scale, s));
+    return PK_OK;
+}
+
+int pk_residual(pk_plan* p, const void* x, const void* y, void* r_out, double* sumsq,
+                void* stream) {
+    if (!p || !x || !y) return fail(PK_ERR_INVALID, "NULL argument");
+    DeviceGuard g(p->device);
+    cudaStream_t s = S(stream);
+    PK_TRY(launch_maxabs(p, x, s));
+    PK_TRY(launch_fp(p, x, 0, s));
+    PK_TRY(launch_finalize(p, y, r_out, sumsq, 0, s));
+    return PK_OK;
+}
+
+int pk_adjoint_residual(pk_plan* p, void* out, double scale, void* stream) {
+    if (!p || !out) return fail(PK_ERR_INVALID, "NULL argument");
+    DeviceGuard g(p->device);
+    PK_TRY(launch_bp(p, 0, out, scale, S(stream)));
+    return PK_OK;
+}
+
+int pk_grad_update(pk_plan* p, const pk_solver_params* prm, const void* x, const void* grad,
+                   void* x_out, double* sums, void* stream) {
+    if (!p || !x || !grad || !x_out || !sums) return fail(PK_ERR_INVALID, "NULL argument");
+    PK_TRY(check_params(prm));
+    DeviceGuard g(p->device);
+    cudaStream_t s = S(stream);
+    PK_TRY(upload_params(p, prm, s));
+    const int pb = (p->P + kThreads - 1) / kThreads;
+    if (p->dtype == PK_F32) {
+        grad_update_kernel<float><<<pb, kThreads, 0, s>>>(static_cast<const float*>(x),
+                                                          static_cast<const float*>(grad),
+                                                          static_cast<float*>(x_out), p->nx, p->ny,
+                                                          p->params);
+        image_sums_kernel<float><<<p->misc_blocks, kThreads, 0, s>>>(
+            static_cast<const float*>(x_out), p->nx, p->ny, p->part_misc, p->state, sums);
+    } else {
+        grad_update_kernel<double><<<pb, kThreads, 0, s>>>(static_cast<const double*>(x),
+                                                           static_cast<const double*>(grad),
+                                                           static_cast<double*>(x_out), p->nx,
+                                                           p->ny, p->params);
+        image_sums_kernel<double><<<p->misc_blocks, kThreads, 0, s>>>(
+            static_cast<const double*>(x_out), p->nx, p->ny, p->part_misc, p->state, sums);
+    }
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+int pk_reconstruct(pk_plan* p, const pk_solver_params* prm, const void* y, void* x_out,
+                   double* hist, int32_t* status, void* stream) {
+    if (!p || !y || !x_out || !hist || !status) return fail(PK_ERR_INVALID, "NULL argument");
+    PK_TRY(check_params(prm));
+    if (p->M != p->Mall)
+        return fail(PK_ERR_INVALID, "pk_reconstruct needs a plan over all sensors (use the sharded pieces)");
+    DeviceGuard g(p->device);
+    cudaStream_t s = S(stream);
+    PK_TRY(upload_params(p, prm, s));
+    DevIo io{y, x_out, hist, status};
+    PK_CUDA(cudaMemcpyAsync(p->io, &io, sizeof(io), cudaMemcpyHostToDevice, s));
+    if (p->graph_iters != prm->iterations) {
+        if (p->graph_exec) { cudaGraphExecDestroy(p->graph_exec); p->graph_exec = nullptr; }
+        if (p->graph) { cudaGraphDestroy(p->graph); p->graph = nullptr; }
+        p->graph_iters = -1;
+        PK_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+        int rc = record_solver(p, prm->iterations, p->cap_stream);
+        cudaGraph_t gr = nullptr;
+        cudaError_t e = cudaStreamEndCapture(p->cap_stream, &gr);
+        if (rc != PK_OK) { if (gr) cudaGraphDestroy(gr); return rc; }
+        if (e != cudaSuccess) return fail(PK_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+        p->graph = gr;
+        PK_CUDA(cudaGraphInstantiate(&p->graph_exec, p->graph, 0));
+        p->graph_iters = prm->iterations;
+    }
+    PK_CUDA(cudaGraphLaunch(p->graph_exec, s));
+    return PK_OK;
+}
+
+int pk_reconstruct_host(pk_plan* p, const pk_solver_params* prm, const double* y_host,
+                        double* x_out_host, double* hist_host, int32_t* status_host,
+                        void* stream) {
+    if (!p || !y_host || !x_out_host || !hist_host || !status_host)
+        return fail(PK_ERR_INVALID, "NULL argument");
+    PK_TRY(check_params(prm));
+    DeviceGuard g(p->device);
+    cudaStream_t s = S(stream);
+    const size_t ny = (size_t)p->M * p->Q;
+    if (!p->y64) { PK_TRY(alloc(p, &p->y64, ny)); }
+    if (!p->x64) { PK_TRY(alloc(p, &p->x64, p->P)); }
+    if (!p->status_dev) { PK_TRY(alloc(p, &p->status_dev, 2)); }
+    if (p->dtype == PK_F32 && !p->ydev) {
+        PK_TRY(alloc(p, reinterpret_cast<float**>(&p->ydev), ny));
+        PK_TRY(alloc(p, reinterpret_cast<float**>(&p->xout_dev), p->P));
+    }
+    PK_TRY(ensure_hist(p, prm->iterations));
+    PK_CUDA(cudaMemcpyAsync(p->y64, y_host, ny * 8, cudaMemcpyHostToDevice, s));
+    const int cb = 148 * 4;
+    if (p->dtype == PK_F32) {
+        convert_kernel<float><<<cb, kThreads, 0, s>>>(p->y64, static_cast<float*>(p->ydev), ny);
+        PK_CHECK_LAUNCH();
+        PK_TRY(pk_reconstruct(p, prm, p->ydev, p->xout_dev, p->hist_dev, p->status_dev, stream));
+        widen_kernel<float><<<cb, kThreads, 0, s>>>(static_cast<const float*>(p->xout_dev), p->x64,
+                                                    (size_t)p->P);
+        PK_CHECK_LAUNCH();
+    } else {
+        PK_TRY(pk_reconstruct(p, prm, p->y64, p->x64, p->hist_dev, p->status_dev, stream));
+    }
+    PK_CUDA(cudaMemcpyAsync(x_out_host, p->x64, (size_t)p->P * 8, cudaMemcpyDeviceToHost, s));
+    PK_CUDA(cudaMemcpyAsync(hist_host, p->hist_dev, (size_t)4 * prm->iterations * 8,
+                            cudaMemcpyDeviceToHost, s));
+    PK_CUDA(cudaMemcpyAsync(status_host, p->status_dev, 8, cudaMemcpyDeviceToHost, s));
+    PK_CUDA(cudaStreamSynchronize(s));
+    return PK_OK;
+}
+
+int pk_index_dump(pk_plan* p, int32_t ma, int32_t mb, int64_t* s0, double* frac, void* stream) {
+    if (!p || !s0) return fail(PK_ERR_INVALID, "NULL argument");
+    if (ma < 0 || mb > p->M || ma >= mb) return fail(PK_ERR_INVALID, "bad sensor range");
+    DeviceGuard g(p->device);
+    index_dump_kernel<<<148 * 8, kThreads, 0, S(stream)>>>(
+        p->px, p->py, p->sx, p->sy, p->cdt, p->nx, p->P, ma, mb,
+        reinterpret_cast<long long*>(s0), frac);
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+int pk_profile_iterations(pk_plan* p, const pk_solver_params* prm, const void* y, float* ms,
+                          int32_t* launches, void* stream) {
+    if (!p || !y || !ms) return fail(PK_ERR_INVALID, "NULL argument");
+    PK_TRY(check_params(prm));
+    if (p->M != p->Mall) return fail(PK_ERR_INVALID, "profiling needs a plan over all sensors");
+    DeviceGuard g(p->device);
+    cudaStream_t s = S(stream);
+    PK_TRY(ensure_hist(p, prm->iterations));
+    if (!p->status_dev) { PK_TRY(alloc(p, &p->status_dev, 2)); }
+    if (!p->xout_dev) { PK_TRY(alloc(p, reinterpret_cast<unsigned char**>(&p->xout_dev), (size_t)p->P * tsize(p))); }
+    PK_TRY(upload_params(p, prm, s));
+    DevIo io{y, p->xout_dev, p->hist_dev, p->status_dev};
+    PK_CUDA(cudaMemcpyAsync(p->io, &io, sizeof(io), cudaMemcpyHostToDevice, s));
+    const int pb = (p->P + kThreads - 1) / kThreads;
+    if (p->dtype == PK_F32)
+        init_kernel<float><<<pb, kThreads, 0, s>>>(static_cast<float*>(p->xbuf[0]), p->P, p->state, p->io);
+    else
+        init_kernel<double><<<pb, kThreads, 0, s>>>(static_cast<double*>(p->xbuf[0]), p->P, p->state, p->io);
+    PK_CHECK_LAUNCH();
+    PK_TRY(launch_table(p, nullptr, 1, s));
+    const int n = prm->iterations;
+    std::vector<cudaEvent_t> ev(3 * n + 1);
+    for (auto& e : ev) PK_CUDA(cudaEventCreate(&e));
+    PK_CUDA(cudaEventRecord(ev[0], s));
+    for (int it = 0; it < n; ++it) {
+        PK_TRY(launch_bp(p, 1, nullptr, 2.0, s));
+        PK_CUDA(cudaEventRecord(ev[3 * it + 1], s));
+        PK_TRY(launch_fp(p, nullptr, 1, s));
+        PK_CUDA(cudaEventRecord(ev[3 * it + 2], s));
+        PK_TRY(launch_finalize(p, nullptr, nullptr, nullptr, 1, s));
+        PK_CUDA(cudaEventRecord(ev[3 * it + 3], s));
+    }
+    PK_CUDA(cudaStreamSynchronize(s));
+    ms[0] = ms[1] = ms[2] = 0.f;
+    for (int it = 0; it < n; ++it)
+        for (int k = 0; k < 3; ++k) {
+            float t = 0.f;
+            PK_CUDA(cudaEventElapsedTime(&t, ev[3 * it + k], ev[3 * it + k + 1]));
+            ms[k] += t;
+        }
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (launches) launches[0] = 2 + 3 * n;
+    return PK_OK;
+}
+
+int pk_measure_fp32_peak(int32_t device, double* tflops) {
+    if (!tflops) return fail(PK_ERR_INVALID, "NULL argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return fail(PK_ERR_CUDA, "no CUDA device %d", device);
+    DeviceGuard g(device);
+    int sms = 0;
+    PK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    float* out = nullptr;
+    const int blocks = sms * 4, iters = 4096;
+    PK_CUDA(cudaMalloc(&out, (size_t)blocks * kThreads * sizeof(float)));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    ffma_peak_kernel<<<blocks, kThreads>>>(out, iters);  // warm-up
+    cudaEventRecord(e0);
+    ffma_peak_kernel<<<blocks, kThreads>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaError_t e = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    if (e != cudaSuccess) return fail(PK_ERR_CUDA, "peak kernel failed: %s", cudaGetErrorString(e));
+    const double flops = 2.0 * 8.0 * 16.0 * iters * (double)blocks * kThreads;
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    return PK_OK;
+}
+
+}  // extern "C"

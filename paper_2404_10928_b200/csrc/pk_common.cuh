@@ -1,0 +1,240 @@
+// pk_common.cuh -- shared device helpers, the plan object and device state.
+//
+// Naming follows the reference's domain (pactkit, arXiv 2404.10928): pixels,
+// sensors, samples, traces, delays.  The "table" is the per-sensor residual
+// trace laid out for the back-projector's two-sample interpolation (one
+// 8-byte load per sensor-pixel interaction).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pactgpu.h"
+
+namespace pk {
+
+// ---------------------------------------------------------------------------
+// constants of the fp32 delay / fixed-point tricks
+constexpr float kTwo23 = 8388608.0f;     // 2^23: floor via round-down add
+constexpr uint32_t kTwo23Bits = 0x4B000000u;
+constexpr float kMagic = 12582912.0f;    // 1.5 * 2^23: round-to-int via add
+constexpr int32_t kMagicBits = 0x4B400000;
+
+constexpr int kThreads = 256;  // every kernel uses 8 warps
+constexpr int kBpTile = 32;    // back-projector pixel tile (32 x 32, 4 pixels/thread)
+constexpr int kDivergenceStreak = 5;  // recon.py:42-43
+
+// ---------------------------------------------------------------------------
+// device state of one solve (single frame)
+struct DevState {
+    // written by the update (back-projection) kernel's last block
+    double maxabs;     // max |x'| of the new iterate
+    double l1sum;      // sum |x'|
+    double scale64;    // fixed-point scale for the projector (2^bits / maxabs)
+    float scale32;
+    int32_t nonfinite; // any non-finite x'
+    // solver bookkeeping, written by the residual kernel's last block
+    double f_prev;
+    int32_t iter;      // iterations attempted so far
+    int32_t accepted;  // iterations accepted (== iterations_run)
+    int32_t stopped;
+    int32_t stopped_by;
+    int32_t grow;
+    int32_t pad0;
+    // last-block counters (reset by the last block itself)
+    uint32_t cnt_bp, cnt_fp, cnt_fin, cnt_misc;
+    // scalars of the sharded / standalone entry points
+    double sums[4];
+};
+
+// device copy of the solver parameters (read by the graph's kernels)
+struct DevParams {
+    double alpha, beta, step, eps, tolerance;
+    double eta_alpha;  // step * alpha (soft-threshold level)
+    int32_t iterations, nonneg;
+};
+
+// I/O pointers of pk_reconstruct, read from device memory so that one captured graph
+// serves any caller buffers.
+struct DevIo {
+    const void* y;
+    void* x_out;
+    double* hist;
+    int32_t* status;
+};
+
+// ---------------------------------------------------------------------------
+// small PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float2 lds_f2(uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ void red_smem_s32(uint32_t addr, int32_t v) {
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+
+// 1-D bulk copy global -> shared (TMA engine), completion counted on an mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// deterministic block reductions (fixed shuffle tree + fixed warp order)
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// sum over the 256-thread block; result valid in every thread
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    T s = red[0];
+#pragma unroll
+    for (int w = 1; w < kThreads / 32; ++w) s += red[w];
+    return s;
+}
+template <typename T>
+__device__ __forceinline__ T block_max(T v, T* red) {
+    v = warp_max(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    T s = red[0];
+#pragma unroll
+    for (int w = 1; w < kThreads / 32; ++w) s = fmax(s, red[w]);
+    return s;
+}
+
+// "last block done" detection; every thread gets the answer.  The counter is reset
+// by the last block so the kernel can be relaunched (and graph-replayed).
+__device__ __forceinline__ bool last_block(uint32_t* counter, uint32_t total, int* flag_smem) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t prev = atomicAdd(counter, 1u);
+        *flag_smem = (prev == total - 1) ? 1 : 0;
+        if (prev == total - 1) atomicExch(counter, 0u);
+    }
+    __syncthreads();
+    const bool last = *flag_smem != 0;
+    if (last) __threadfence();
+    return last;
+}
+
+// fp64 delay exactly as forward.py:157-182 evaluates it (no FMA contraction)
+__device__ __forceinline__ double delay_f64(double px, double py, double sx, double sy,
+                                            double cdt) {
+    const double ex = __dsub_rn(px, sx);
+    const double ey = __dsub_rn(py, sy);
+    const double d = __dsqrt_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)));
+    return __ddiv_rn(d, cdt);
+}
+
+}  // namespace pk
+
+// ---------------------------------------------------------------------------
+// the plan (opaque to C callers)
+struct pk_plan {
+    int device = 0, dtype = PK_F32;
+    int nx = 0, ny = 0, P = 0, Mall = 0, m0 = 0, M = 0, Q = 0;
+    double c = 0, dt = 0, cdt = 0, w = 0;
+    int may_truncate = 0;
+    double min_delay = 0, max_delay = 0;  // in samples, host-computed bounds
+
+    // geometry on the device
+    float *pxs = nullptr, *pys = nullptr, *sxs = nullptr, *sys = nullptr;  // scaled by 1/cdt
+    double *px = nullptr, *py = nullptr, *sx = nullptr, *sy = nullptr;    // original fp64
+
+    // residual pair table [M][TS] (float2 / double2) and fixed-point accumulator [M][Q]
+    int TS = 0;
+    void* table = nullptr;
+    long long* acc = nullptr;
+
+    // iterates and scratch
+    void* xbuf[2] = {nullptr, nullptr};
+    void* ydev = nullptr;        // device copy of y for pk_reconstruct_host
+    double* y64 = nullptr;       // fp64 staging of y (host API)
+    double* x64 = nullptr;       // fp64 staging of the image (host API)
+    void* xout_dev = nullptr;    // image in plan dtype (host API)
+    double* hist_dev = nullptr;  // history for the host API
+    int hist_cap = 0;
+    int32_t* status_dev = nullptr;
+    double* part_bp = nullptr;   // [bp blocks * 4]
+    double* part_tv = nullptr;   // [fp tiles]
+    double* part_r = nullptr;    // [M]
+    double* part_misc = nullptr; // [generic blocks * 4]
+    pk::DevState* state = nullptr;
+    pk::DevParams* params = nullptr;
+    pk::DevIo* io = nullptr;
+
+    // back-projector tiling
+    int bp_tiles_x = 0, bp_tiles_y = 0, bp_L = 0, bp_CS = 0, bp_nbuf = 0, bp_smem = 0;
+    // projector tiling
+    int fp_T = 0, fp_tiles_x = 0, fp_tiles_y = 0, fp_groups = 0, fp_L = 0, fp_bits = 0,
+        fp_smem = 0;
+    int misc_blocks = 0;
+
+    // graph cache of pk_reconstruct
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    cudaStream_t cap_stream = nullptr;
+    int graph_iters = -1;
+
+    int64_t device_bytes = 0;
+};

@@ -1,0 +1,872 @@
+// pk_kernels.cuh -- sm_100a kernels of the iterative reconstruction hot path.
+//
+//   K1 bp_f32 / bp_f64     back-projection K^T r (recon.py:327), optionally fused with the
+//                          TV gradient, soft threshold and non-negativity (recon.py:330-338)
+//   K2 fp_f32 / fp_f64     projection K x (recon.py:342) into a fixed-point accumulator
+//   K3 finalize            r = K x - y, the residual pair table for the next K1, sum r^2,
+//                          and (solver mode) the objective + stopping rules (recon.py:346-363)
+//   misc                   table-from-trace, max|x| scale, update for sharded runs, index dump
+//
+// See DESIGN.md for the data layout and the per-interaction instruction budget.
+#pragma once
+#include <type_traits>
+
+#include "pk_common.cuh"
+
+namespace pk {
+
+// ===========================================================================
+// K1 -- back-projector, fp32.  CTA = 32x32 pixel tile, 256 threads, thread owns the
+// pixels (i0 + lx + 8k, j0 + 4*warp + ly), k = 0..3, so every warp instruction covers a
+// compact 8x4 pixel footprint (delay span <= ~32 samples -> broadcast-friendly LDS.64).
+// Sensors are processed in chunks of CS; for each chunk the per-(tile, sensor) window of
+// the residual pair table is brought into shared memory by the TMA engine
+// (cp.async.bulk + mbarrier), NBUF-deep ring.
+//
+// pair table entry s of sensor m: {r[s-1], r[s] - r[s-1]} (r[-1] = r[Q] = r[Q+1] = 0), so
+// one interaction is  acc += r[s0-1] + f*(r[s0]-r[s0-1])  == (1-f) r[s0-1] + f r[s0],
+// the two weights of build_time_matrix (forward.py:189-194) without the w factor.
+// ===========================================================================
+struct BpArgs {
+    const float2* table;  // [M][TS]
+    const float* pxs;     // [nx] scaled pixel x
+    const float* pys;     // [ny]
+    const float* sxs;     // [M]
+    const float* sys;     // [M]
+    int nx, ny, M, Q, TS, L, CS, nbuf, tiles_x;
+    float qclamp;         // Q + 1.5 (truncation clamp of the delay)
+    // EPI == 0: out[p] = gscale * acc
+    float* out;
+    float gscale;
+    // EPI == 1: fused update, x from xb[iter & 1] to xb[(iter+1) & 1]
+    float* xb0;
+    float* xb1;
+    const DevParams* prm;
+    DevState* st;
+    double* part;         // [blocks * 4]
+    int bits;             // projector fixed-point bits (scale = 2^bits / max|x'|)
+};
+
+template <bool EPI, bool CLAMP>
+__global__ void __launch_bounds__(kThreads, 2) bp_f32_kernel(BpArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ float red_f[kThreads / 32];
+    __shared__ int last_flag;
+
+    int iter = 0;
+    if (EPI) {
+        if (a.st->stopped) return;
+        iter = a.st->iter;
+    }
+    const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
+    const int i0 = tx * kBpTile, j0 = ty * kBpTile;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = lane & 7, ly = lane >> 3;
+    const int j = j0 + warp * 4 + ly;
+
+    float px[4], acc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        px[k] = __ldg(a.pxs + min(i0 + lx + 8 * k, a.nx - 1));
+        acc[k] = 0.f;
+    }
+    const float py = __ldg(a.pys + min(j, a.ny - 1));
+
+    // shared layout: windows [nbuf][CS][L] float2 | sconst [nbuf][CS] float4 | bars [nbuf] u64
+    float2* win = reinterpret_cast<float2*>(smem);
+    float4* sconst = reinterpret_cast<float4*>(smem + (size_t)a.nbuf * a.CS * a.L * 8);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)a.nbuf * a.CS * a.L * 8 +
+                                                 (size_t)a.nbuf * a.CS * 16);
+    const uint32_t win_s = smem_u32(win);
+    const uint32_t bar_s = smem_u32(bars);
+
+    // tile rectangle in scaled coordinates (for the per-sensor delay windows)
+    const float X0 = __ldg(a.pxs + i0), X1 = __ldg(a.pxs + min(i0 + kBpTile - 1, a.nx - 1));
+    const float Y0 = __ldg(a.pys + j0), Y1 = __ldg(a.pys + min(j0 + kBpTile - 1, a.ny - 1));
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < a.nbuf; ++b) mbar_init(bar_s + 8 * b, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    const int nchunks = (a.M + a.CS - 1) / a.CS;
+    // warp 0 computes the windows of a chunk and launches its bulk copies
+    auto issue = [&](int c, int b) {
+        const int m = c * a.CS + lane;
+        const int n = min(a.CS, a.M - c * a.CS);
+        if (lane < n) {
+            const float sx = __ldg(a.sxs + m), sy = __ldg(a.sys + m);
+            const float cx = fminf(fmaxf(sx, X0), X1), cy = fminf(fmaxf(sy, Y0), Y1);
+            float dmin = sqrtf((cx - sx) * (cx - sx) + (cy - sy) * (cy - sy));
+            if (CLAMP) dmin = fminf(dmin, a.qclamp);
+            int lo = (int)floorf(dmin) - 1;
+            lo = max(lo, 0) & ~1;
+            lo = min(lo, a.TS - a.L);
+            const uint32_t dst = win_s + (uint32_t)((b * a.CS + lane) * a.L) * 8u;
+            const uint32_t adj = dst - 8u * (uint32_t)lo - 8u * kTwo23Bits;
+            sconst[b * a.CS + lane] = make_float4(sx, sy, __uint_as_float(adj), 0.f);
+            __syncwarp(__activemask());
+            if (lane == 0) mbar_expect_tx(bar_s + 8 * b, (uint32_t)(n * a.L * 8));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp(__activemask());
+            bulk_g2s(dst, a.table + (size_t)m * a.TS + lo, (uint32_t)(a.L * 8), bar_s + 8 * b);
+        }
+    };
+    if (warp == 0) {
+        for (int c = 0; c < min(a.nbuf, nchunks); ++c) issue(c, c);
+    }
+
+    for (int c = 0; c < nchunks; ++c) {
+        const int b = c % a.nbuf;
+        mbar_wait(bar_s + 8 * b, (uint32_t)((c / a.nbuf) & 1));
+        const int n = min(a.CS, a.M - c * a.CS);
+        const float4* sc = sconst + b * a.CS;
+#pragma unroll 2
+        for (int s = 0; s < n; ++s) {
+            const float4 q = sc[s];
+            const float ey = py - q.y;
+            const float ey2 = ey * ey;
+            const uint32_t adj = __float_as_uint(q.z);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float ex = px[k] - q.x;
+                float u = sqrt_approx(fmaf(ex, ex, ey2));
+                if (CLAMP) u = fminf(u, a.qclamp);
+                const float tb = __fadd_rd(u, kTwo23);      // 2^23 + floor(u)
+                const float f = u - (tb - kTwo23);          // exact fraction
+                const float2 v = lds_f2(adj + (__float_as_uint(tb) << 3));
+                acc[k] += fmaf(f, v.y, v.x);
+            }
+        }
+        __syncthreads();  // everyone is done with buffer b
+        if (warp == 0 && c + a.nbuf < nchunks) issue(c + a.nbuf, b);
+    }
+
+    if (!EPI) {
+        if (j < a.ny) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = i0 + lx + 8 * k;
+                if (i < a.nx) a.out[(size_t)j * a.nx + i] = a.gscale * acc[k];
+            }
+        }
+        return;
+    }
+
+    // ---- fused update epilogue (recon.py:327-338) ----
+    const float* x = (iter & 1) ? a.xb1 : a.xb0;
+    float* xo = (iter & 1) ? a.xb0 : a.xb1;
+    const float eta = (float)a.prm->step, lam = (float)a.prm->eta_alpha;
+    const float beta = (float)a.prm->beta, eps = (float)a.prm->eps;
+    const float gsc = a.gscale;
+    const bool nonneg = a.prm->nonneg != 0;
+    float mx = 0.f, l1 = 0.f;
+    int bad = 0;
+    if (j < a.ny) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = i0 + lx + 8 * k;
+            if (i >= a.nx) continue;
+            const size_t p = (size_t)j * a.nx + i;
+            const float x0 = x[p];
+            float g = gsc * acc[k];
+            if (beta > 0.f) {
+                // recon.py:178-189, same accumulation order
+                const float e2 = eps * eps;
+                float t = 0.f;
+                if (i < a.nx - 1) { const float d = x[p + 1] - x0; t -= d / sqrtf(d * d + e2); }
+                if (i > 0) { const float d = x0 - x[p - 1]; t += d / sqrtf(d * d + e2); }
+                if (j < a.ny - 1) { const float d = x[p + a.nx] - x0; t -= d / sqrtf(d * d + e2); }
+                if (j > 0) { const float d = x0 - x[p - a.nx]; t += d / sqrtf(d * d + e2); }
+                g += beta * t;
+            }
+            const float v = x0 - eta * g;
+            float mag = fabsf(v) - lam;
+            mag = (mag != mag) ? mag : fmaxf(mag, 0.f);     // np.maximum keeps NaN
+            float xn = (v > 0.f) ? mag : ((v < 0.f) ? -mag : (v != v ? v : 0.f));
+            if (nonneg) xn = (xn != xn) ? xn : fmaxf(xn, 0.f);
+            xo[p] = xn;
+            if (!isfinite(xn)) bad = 1;
+            mx = fmaxf(mx, fabsf(xn));
+            l1 += fabsf(xn);
+        }
+    }
+    mx = block_max(mx, red_f);
+    const float l1b = block_sum(l1, red_f);
+    const int badb = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+        double* pp = a.part + 4 * (size_t)blockIdx.x;
+        pp[0] = mx;
+        pp[1] = l1b;
+        pp[2] = badb;
+    }
+    if (last_block(&a.st->cnt_bp, gridDim.x, &last_flag)) {
+        __shared__ double red_d[kThreads / 32];
+        double m2 = 0.0, s2 = 0.0, b2 = 0.0;
+        for (int q = threadIdx.x; q < (int)gridDim.x; q += kThreads) {
+            const double* pp = a.part + 4 * (size_t)q;
+            m2 = fmax(m2, pp[0]);
+            s2 += pp[1];
+            b2 += pp[2];
+        }
+        m2 = block_max(m2, red_d);
+        s2 = block_sum(s2, red_d);
+        b2 = block_sum(b2, red_d);
+        if (threadIdx.x == 0) {
+            a.st->maxabs = m2;
+            a.st->l1sum = s2;
+            a.st->nonfinite = b2 > 0.0 ? 1 : 0;
+            const double sc = (m2 > 0.0 && isfinite(m2)) ? ldexp(1.0, a.bits) / m2 : 0.0;
+            a.st->scale64 = sc;
+            a.st->scale32 = (float)sc;
+        }
+    }
+}
+
+// ===========================================================================
+// K1 -- back-projector, fp64 validation mode: one pixel per thread, fp64 delay evaluated
+// exactly as the reference (forward.py:157-182), table read through the L1/L2 path.
+// ===========================================================================
+struct BpArgs64 {
+    const double2* table;
+    const double *px, *py, *sx, *sy;
+    double cdt;
+    int nx, ny, M, Q, TS;
+    double* out;
+    double gscale;
+    double *xb0, *xb1;
+    const DevParams* prm;
+    DevState* st;
+    double* part;
+    int bits;
+};
+
+template <bool EPI>
+__global__ void __launch_bounds__(kThreads) bp_f64_kernel(BpArgs64 a) {
+    __shared__ double red_d[kThreads / 32];
+    __shared__ int last_flag;
+    int iter = 0;
+    if (EPI) {
+        if (a.st->stopped) return;
+        iter = a.st->iter;
+    }
+    const int p = blockIdx.x * kThreads + threadIdx.x;
+    const int P = a.nx * a.ny;
+    const bool valid = p < P;
+    const int i = valid ? p % a.nx : 0, j = valid ? p / a.nx : 0;
+    const double pxv = a.px[i], pyv = a.py[j];
+    double acc = 0.0;
+    if (valid) {
+        for (int m = 0; m < a.M; ++m) {
+            const double u = delay_f64(pxv, pyv, __ldg(a.sx + m), __ldg(a.sy + m), a.cdt);
+            double fl = floor(u);
+            if (fl > (double)(a.Q + 1)) fl = (double)(a.Q + 1);
+            const int s0 = (int)fl;
+            const double f = u - fl;
+            const double2 v = __ldg(a.table + (size_t)m * a.TS + s0);
+            acc += fma(f, v.y, v.x);
+        }
+    }
+    if (!EPI) {
+        if (valid) a.out[p] = a.gscale * acc;
+        return;
+    }
+    const double* x = (iter & 1) ? a.xb1 : a.xb0;
+    double* xo = (iter & 1) ? a.xb0 : a.xb1;
+    const double eta = a.prm->step, lam = a.prm->eta_alpha, beta = a.prm->beta, eps = a.prm->eps;
+    double mx = 0.0, l1 = 0.0;
+    int bad = 0;
+    if (valid) {
+        const double x0 = x[p];
+        double g = a.gscale * acc;
+        if (beta > 0.0) {
+            const double e2 = eps * eps;
+            double t = 0.0;
+            if (i < a.nx - 1) { const double d = x[p + 1] - x0; t -= d / sqrt(d * d + e2); }
+            if (i > 0) { const double d = x0 - x[p - 1]; t += d / sqrt(d * d + e2); }
+            if (j < a.ny - 1) { const double d = x[p + a.nx] - x0; t -= d / sqrt(d * d + e2); }
+            if (j > 0) { const double d = x0 - x[p - a.nx]; t += d / sqrt(d * d + e2); }
+            g += beta * t;
+        }
+        const double v = x0 - eta * g;
+        double mag = fabs(v) - lam;
+        mag = (mag != mag) ? mag : fmax(mag, 0.0);
+        double xn = (v > 0.0) ? mag : ((v < 0.0) ? -mag : (v != v ? v : 0.0));
+        if (a.prm->nonneg) xn = (xn != xn) ? xn : fmax(xn, 0.0);
+        xo[p] = xn;
+        bad = !isfinite(xn);
+        mx = fabs(xn);
+        l1 = fabs(xn);
+    }
+    mx = block_max(mx, red_d);
+    const double l1b = block_sum(l1, red_d);
+    const int badb = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+        double* pp = a.part + 4 * (size_t)blockIdx.x;
+        pp[0] = mx;
+        pp[1] = l1b;
+        pp[2] = badb;
+    }
+    if (last_block(&a.st->cnt_bp, gridDim.x, &last_flag)) {
+        double m2 = 0.0, s2 = 0.0, b2 = 0.0;
+        for (int q = threadIdx.x; q < (int)gridDim.x; q += kThreads) {
+            const double* pp = a.part + 4 * (size_t)q;
+            m2 = fmax(m2, pp[0]);
+            s2 += pp[1];
+            b2 += pp[2];
+        }
+        m2 = block_max(m2, red_d);
+        s2 = block_sum(s2, red_d);
+        b2 = block_sum(b2, red_d);
+        if (threadIdx.x == 0) {
+            a.st->maxabs = m2;
+            a.st->l1sum = s2;
+            a.st->nonfinite = b2 > 0.0 ? 1 : 0;
+            const double sc = (m2 > 0.0 && isfinite(m2)) ? ldexp(1.0, a.bits) / m2 : 0.0;
+            a.st->scale64 = sc;
+            a.st->scale32 = (float)sc;
+        }
+    }
+}
+
+// ===========================================================================
+// K2 -- projector, fp32 with an exact fixed-point accumulator (deterministic).
+// CTA = (T x T pixel tile, 32 consecutive sensors); lane l of every warp owns sensor
+// g*32 + l, so a warp instruction is 1 pixel x 32 sensors.  Each lane scatters into its own
+// sensor's window with native 32-bit shared atomics; the window is stored slot-major
+// ([slot][32 lanes]) so lane l always hits bank l: conflict-free by construction.
+// Contributions are integers:  xq = rint(x*scale),  a = rint(x*scale*f),  b = xq - a,
+// added at trace index s0 (weight f) and s0-1 (weight 1-f) -- forward.py:189-194.
+// Zero pixels (soft-threshold zeros) are skipped, warp-uniformly.
+// Each window is flushed into the int64 trace accumulator with coalescing-free RED.64.
+// ===========================================================================
+struct FpArgs {
+    const float* x;       // [P] (nullptr: solver mode, use xb[(iter+1)&1])
+    const float* xb0;
+    const float* xb1;
+    const float* pxs;
+    const float* pys;
+    const float* sxs;
+    const float* sys;
+    long long* acc;       // [M][Q]
+    int nx, ny, M, Q, T, L, tiles_x;
+    float qclamp;
+    DevState* st;
+    double* part_tv;      // solver mode: per-tile TV(x) partials (group 0 only)
+    int solver;
+};
+
+template <bool CLAMP>
+__global__ void __launch_bounds__(kThreads) fp_f32_kernel(FpArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ float red_f[kThreads / 32];
+    int iter = 0;
+    if (a.solver) {
+        if (a.st->stopped) return;
+        iter = a.st->iter;
+    }
+    const float* x = a.x ? a.x : ((iter & 1) ? a.xb0 : a.xb1);  // bp wrote xb[(iter+1)&1]
+    const float scale = a.st->scale32;
+    const int T = a.T;
+    const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
+    const int i0 = tx * T, j0 = ty * T;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int m = blockIdx.y * 32 + lane;
+    const bool sensor_ok = m < a.M;
+    const float sx = __ldg(a.sxs + min(m, a.M - 1)), sy = __ldg(a.sys + min(m, a.M - 1));
+
+    // shared layout: win int32 [L][32] | rec float4 [T*T] | rowcnt int [T]
+    int32_t* win = reinterpret_cast<int32_t*>(smem);
+    float4* rec = reinterpret_cast<float4*>(smem + (size_t)a.L * 32 * 4);
+    int* rowcnt = reinterpret_cast<int*>(smem + (size_t)a.L * 32 * 4 + (size_t)T * T * 16);
+
+    for (int q = threadIdx.x; q < a.L * 32; q += kThreads) win[q] = 0;
+
+    // compact the tile's non-zero pixels per row: {px, x*scale, bits(rint(x*scale)+magic)}
+    float tv = 0.f;
+    const bool do_tv = a.solver && blockIdx.y == 0;
+    for (int r = warp; r < T; r += kThreads / 32) {
+        const int jj = j0 + r;
+        int base = 0;
+        for (int cc = 0; cc < T; cc += 32) {
+            const int ii = i0 + cc + lane;
+            const bool in = ii < a.nx && jj < a.ny;
+            const float xv = in ? x[(size_t)jj * a.nx + ii] : 0.f;
+            if (do_tv && in) {  // exact anisotropic TV partial, recon.py:169-170
+                if (ii + 1 < a.nx) tv += fabsf(x[(size_t)jj * a.nx + ii + 1] - xv);
+                if (jj + 1 < a.ny) tv += fabsf(x[(size_t)(jj + 1) * a.nx + ii] - xv);
+            }
+            const bool nz = xv != 0.f;
+            const uint32_t bal = __ballot_sync(0xffffffffu, nz);
+            if (nz) {
+                const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                const float xs = xv * scale;
+                rec[r * T + pos] =
+                    make_float4(__ldg(a.pxs + ii), xs, __int_as_float(__float_as_int(xs + kMagic)), 0.f);
+            }
+            base += __popc(bal);
+        }
+        if (lane == 0) rowcnt[r] = base;
+    }
+    if (do_tv) {
+        const float tvb = block_sum(tv, red_f);
+        if (threadIdx.x == 0) a.part_tv[blockIdx.x] = tvb;
+    }
+
+    // this lane's window: trace indices [lo, lo + L)
+    const float X0 = __ldg(a.pxs + i0), X1 = __ldg(a.pxs + min(i0 + T - 1, a.nx - 1));
+    const float Y0 = __ldg(a.pys + j0), Y1 = __ldg(a.pys + min(j0 + T - 1, a.ny - 1));
+    const float cx = fminf(fmaxf(sx, X0), X1), cy = fminf(fmaxf(sy, Y0), Y1);
+    float dmin = sqrtf((cx - sx) * (cx - sx) + (cy - sy) * (cy - sy));
+    if (CLAMP) dmin = fminf(dmin, a.qclamp);
+    const int lo = (int)floorf(dmin) - 2;
+    // word address of trace index t: win + 4*(32*(t - lo) + lane);  t = s0 -> tb bits
+    const uint32_t adj = smem_u32(win) + 4u * (uint32_t)lane - 128u * (uint32_t)lo -
+                         128u * kTwo23Bits;
+    __syncthreads();
+
+    if (sensor_ok) {
+        for (int r = warp; r < T; r += kThreads / 32) {
+            const int cnt = rowcnt[r];
+            if (cnt == 0) continue;
+            const float ey = __ldg(a.pys + min(j0 + r, a.ny - 1)) - sy;
+            const float ey2 = ey * ey;
+            const float4* rr = rec + r * T;
+#pragma unroll 4
+            for (int k = 0; k < cnt; ++k) {
+                const float4 q = rr[k];
+                const float ex = q.x - sx;
+                float u = sqrt_approx(fmaf(ex, ex, ey2));
+                if (CLAMP) u = fminf(u, a.qclamp);
+                const float tb = __fadd_rd(u, kTwo23);
+                const float f = u - (tb - kTwo23);
+                const float fb = fmaf(q.y, f, kMagic);
+                const int32_t ia = __float_as_int(fb) - kMagicBits;       // weight f   -> s0
+                const int32_t ib = __float_as_int(q.z) - __float_as_int(fb); // weight 1-f -> s0-1
+                const uint32_t addr = adj + (__float_as_uint(tb) << 7);
+                red_smem_s32(addr - 128u, ib);
+                red_smem_s32(addr, ia);
+            }
+        }
+    }
+    __syncthreads();
+
+    // flush: slot-major rows, lane = sensor; only real trace indices 0..Q-1
+    if (sensor_ok) {
+        long long* accm = a.acc + (size_t)m * a.Q;
+        for (int k = warp; k < a.L; k += kThreads / 32) {
+            const int32_t v = win[k * 32 + lane];
+            const int t = lo + k;
+            if (v != 0 && t >= 0 && t < a.Q)
+                atomicAdd(reinterpret_cast<unsigned long long*>(accm + t),
+                          (unsigned long long)(long long)v);
+        }
+    }
+}
+
+// ===========================================================================
+// K2 -- projector, fp64 validation mode (same structure, int64 fixed point, CAS atomics)
+// ===========================================================================
+struct FpArgs64 {
+    const double* x;
+    const double* xb0;
+    const double* xb1;
+    const double *px, *py, *sx, *sy;
+    double cdt;
+    long long* acc;
+    int nx, ny, M, Q, T, L, tiles_x;
+    DevState* st;
+    double* part_tv;
+    int solver;
+};
+
+__global__ void __launch_bounds__(kThreads) fp_f64_kernel(FpArgs64 a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ double red_d[kThreads / 32];
+    int iter = 0;
+    if (a.solver) {
+        if (a.st->stopped) return;
+        iter = a.st->iter;
+    }
+    const double* x = a.x ? a.x : ((iter & 1) ? a.xb0 : a.xb1);
+    const double scale = a.st->scale64;
+    const int T = a.T;
+    const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
+    const int i0 = tx * T, j0 = ty * T;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int m = blockIdx.y * 32 + lane;
+    const bool sensor_ok = m < a.M;
+    const double sxv = a.sx[min(m, a.M - 1)], syv = a.sy[min(m, a.M - 1)];
+
+    unsigned long long* win = reinterpret_cast<unsigned long long*>(smem);
+    double2* rec = reinterpret_cast<double2*>(smem + (size_t)a.L * 32 * 8);  // {px, xs}
+    long long* recq = reinterpret_cast<long long*>(smem + (size_t)a.L * 32 * 8 + (size_t)T * T * 16);
+    int* rowcnt = reinterpret_cast<int*>(smem + (size_t)a.L * 32 * 8 + (size_t)T * T * 24);
+
+    for (int q = threadIdx.x; q < a.L * 32; q += kThreads) win[q] = 0ull;
+    double tv = 0.0;
+    const bool do_tv = a.solver && blockIdx.y == 0;
+    for (int r = warp; r < T; r += kThreads / 32) {
+        const int jj = j0 + r;
+        int base = 0;
+        for (int cc = 0; cc < T; cc += 32) {
+            const int ii = i0 + cc + lane;
+            const bool in = ii < a.nx && jj < a.ny && (cc + lane) < T;
+            const double xv = in ? x[(size_t)jj * a.nx + ii] : 0.0;
+            if (do_tv && in) {
+                if (ii + 1 < a.nx) tv += fabs(x[(size_t)jj * a.nx + ii + 1] - xv);
+                if (jj + 1 < a.ny) tv += fabs(x[(size_t)(jj + 1) * a.nx + ii] - xv);
+            }
+            const bool nz = xv != 0.0;
+            const uint32_t bal = __ballot_sync(0xffffffffu, nz);
+            if (nz) {
+                const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                const double xs = xv * scale;
+                rec[r * T + pos] = make_double2(a.px[ii], xs);
+                recq[r * T + pos] = __double2ll_rn(xs);
+            }
+            base += __popc(bal);
+        }
+        if (lane == 0) rowcnt[r] = base;
+    }
+    if (do_tv) {
+        const double tvb = block_sum(tv, red_d);
+        if (threadIdx.x == 0) a.part_tv[blockIdx.x] = tvb;
+    }
+    const double X0 = a.px[i0], X1 = a.px[min(i0 + T - 1, a.nx - 1)];
+    const double Y0 = a.py[j0], Y1 = a.py[min(j0 + T - 1, a.ny - 1)];
+    const double cx = fmin(fmax(sxv, X0), X1), cy = fmin(fmax(syv, Y0), Y1);
+    double dmin = sqrt((cx - sxv) * (cx - sxv) + (cy - syv) * (cy - syv)) / a.cdt;
+    dmin = fmin(dmin, (double)a.Q + 1.5);
+    const int lo = (int)floor(dmin) - 2;
+    __syncthreads();
+
+    if (sensor_ok) {
+        for (int r = warp; r < T; r += kThreads / 32) {
+            const int cnt = rowcnt[r];
+            if (cnt == 0) continue;
+            const double pyv = a.py[min(j0 + r, a.ny - 1)];
+            for (int k = 0; k < cnt; ++k) {
+                const double2 q = rec[r * T + k];
+                const long long xq = recq[r * T + k];
+                const double u = delay_f64(q.x, pyv, sxv, syv, a.cdt);
+                double fl = floor(u);
+                if (fl > (double)(a.Q + 1)) fl = (double)(a.Q + 1);
+                const int s0 = (int)fl;
+                const double f = u - fl;
+                const long long qa = __double2ll_rn(q.y * f);
+                const long long qb = xq - qa;
+                const int slot = s0 - lo;  // window slot of trace index s0
+                atomicAdd(win + (size_t)(slot - 1) * 32 + lane, (unsigned long long)qb);
+                atomicAdd(win + (size_t)slot * 32 + lane, (unsigned long long)qa);
+            }
+        }
+    }
+    __syncthreads();
+    if (sensor_ok) {
+        long long* accm = a.acc + (size_t)m * a.Q;
+        for (int k = warp; k < a.L; k += kThreads / 32) {
+            const long long v = (long long)win[k * 32 + lane];
+            const int t = lo + k;
+            if (v != 0 && t >= 0 && t < a.Q)
+                atomicAdd(reinterpret_cast<unsigned long long*>(accm + t), (unsigned long long)v);
+        }
+    }
+}
+
+// ===========================================================================
+// K3 -- residual / finalize: one CTA per sensor.  r = w*acc/scale - y, acc := 0, pair table,
+// sum r^2; solver mode: last CTA evaluates the objective and the stopping rules.
+// ===========================================================================
+template <typename T>
+struct FinArgs {
+    long long* acc;
+    const T* y;          // may be null (plain projection); solver mode reads io->y
+    T* trace_out;        // may be null
+    typename std::conditional<sizeof(T) == 4, float2, double2>::type* table;
+    int M, Q, TS;
+    double w;
+    int wscale_mode;     // unused
+    DevState* st;
+    const DevParams* prm;
+    const DevIo* io;
+    double* part_r;      // [M]
+    const double* part_tv;
+    int ntv;
+    double* sumsq_out;   // optional (pk_residual)
+    int solver;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
+    using T2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
+    extern __shared__ __align__(128) unsigned char smem[];
+    T* tr = reinterpret_cast<T*>(smem);
+    __shared__ double red_d[kThreads / 32];
+    __shared__ int last_flag;
+    if (a.solver && a.st->stopped) return;
+    const int m = blockIdx.x;
+    const double sc = sizeof(T) == 4 ? (double)a.st->scale32 : a.st->scale64;
+    const double wq = sc > 0.0 ? a.w / sc : 0.0;
+    const T* y = a.solver ? reinterpret_cast<const T*>(a.io->y) : a.y;
+    long long* accm = a.acc + (size_t)m * a.Q;
+    double ss = 0.0;
+    for (int s = threadIdx.x; s < a.Q; s += kThreads) {
+        const long long v = accm[s];
+        accm[s] = 0;
+        // K x rounded to the working type first, then the residual in that type, so that
+        // y produced by the same projection gives r == 0 exactly (recon.py:75-79 semantics)
+        const T kx = (T)((double)v * wq);
+        const T rv = y ? (T)(kx - y[(size_t)m * a.Q + s]) : kx;
+        tr[s] = rv;
+        if (a.trace_out) a.trace_out[(size_t)m * a.Q + s] = rv;
+        ss += (double)rv * (double)rv;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < a.TS; e += kThreads) {
+        const T rp = (e >= 1 && e - 1 < a.Q) ? tr[e - 1] : (T)0;
+        const T rc = (e < a.Q) ? tr[e] : (T)0;
+        T2 v;
+        v.x = rp;
+        v.y = rc - rp;
+        a.table[(size_t)m * a.TS + e] = v;
+    }
+    ss = block_sum(ss, red_d);
+    if (threadIdx.x == 0) a.part_r[m] = ss;
+    if (!last_block(&a.st->cnt_fin, gridDim.x, &last_flag)) return;
+
+    double data = 0.0, tvs = 0.0;
+    for (int q = threadIdx.x; q < a.M; q += kThreads) data += a.part_r[q];
+    data = block_sum(data, red_d);
+    if (a.solver) {
+        for (int q = threadIdx.x; q < a.ntv; q += kThreads) tvs += a.part_tv[q];
+        tvs = block_sum(tvs, red_d);
+    }
+    if (threadIdx.x != 0) return;
+    if (a.sumsq_out) a.sumsq_out[0] = data;
+    if (!a.solver) return;
+    // objective and stopping (recon.py:346-363)
+    DevState* st = a.st;
+    const DevParams* prm = a.prm;
+    const int it = st->iter;
+    const double l1 = prm->alpha * st->l1sum;
+    const double tv = prm->beta * tvs;
+    const double total = data + l1 + tv;
+    if (!isfinite(total) || st->nonfinite) {
+        st->stopped = 1;
+        st->stopped_by = PK_STOP_DIVERGENCE;
+    } else {
+        double* h = a.io->hist;
+        h[it] = total;
+        h[prm->iterations + it] = data;
+        h[2 * prm->iterations + it] = l1;
+        h[3 * prm->iterations + it] = tv;
+        st->accepted = it + 1;
+        st->grow = total > st->f_prev ? st->grow + 1 : 0;
+        if (st->grow >= kDivergenceStreak) {
+            st->stopped = 1;
+            st->stopped_by = PK_STOP_DIVERGENCE;
+        } else {
+            const double rel = fabs(total - st->f_prev) / fmax(fabs(st->f_prev), 1e-300);
+            st->f_prev = total;
+            if (prm->tolerance > 0.0 && rel < prm->tolerance) {
+                st->stopped = 1;
+                st->stopped_by = PK_STOP_TOLERANCE;
+            }
+        }
+    }
+    st->iter = it + 1;
+    if (st->iter >= prm->iterations) st->stopped = 1;
+    a.io->status[0] = st->accepted;
+    a.io->status[1] = st->stopped_by;
+}
+
+// ===========================================================================
+// pair table from a trace: table[m][s] = {sign*y[s-1], sign*(y[s]-y[s-1])}.
+// Solver init mode (sign = -1, r0 = -y): last block writes f_prev = sum y^2 and resets state.
+// ===========================================================================
+template <typename T>
+__global__ void __launch_bounds__(kThreads) table_kernel(
+    const T* y_direct, const DevIo* io, typename std::conditional<sizeof(T) == 4, float2, double2>::type* table,
+    int M, int Q, int TS, T sign, double* part, DevState* st, int init) {
+    using T2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
+    __shared__ double red_d[kThreads / 32];
+    __shared__ int last_flag;
+    const T* y = y_direct ? y_direct : reinterpret_cast<const T*>(io->y);
+    const int m = blockIdx.x;
+    const T* ym = y + (size_t)m * Q;
+    double ss = 0.0;
+    for (int e = threadIdx.x; e < TS; e += kThreads) {
+        const T rp = (e >= 1 && e - 1 < Q) ? sign * ym[e - 1] : (T)0;
+        const T rc = (e < Q) ? sign * ym[e] : (T)0;
+        T2 v;
+        v.x = rp;
+        v.y = rc - rp;
+        table[(size_t)m * TS + e] = v;
+        if (e < Q) ss += (double)rc * (double)rc;
+    }
+    if (!init) return;
+    ss = block_sum(ss, red_d);
+    if (threadIdx.x == 0) part[m] = ss;
+    if (!last_block(&st->cnt_misc, gridDim.x, &last_flag)) return;
+    double tot = 0.0;
+    for (int q = threadIdx.x; q < M; q += kThreads) tot += part[q];
+    tot = block_sum(tot, red_d);
+    if (threadIdx.x == 0) st->f_prev = tot;
+}
+
+// solver state reset + x0 = 0 (recon.py:318-320)
+template <typename T>
+__global__ void init_kernel(T* xb0, int P, DevState* st, const DevIo* io) {
+    const int p = blockIdx.x * kThreads + threadIdx.x;
+    if (p < P) xb0[p] = (T)0;
+    if (p == 0) {
+        st->iter = 0;
+        st->accepted = 0;
+        st->stopped = 0;
+        st->stopped_by = PK_STOP_MAX_ITERATIONS;
+        st->grow = 0;
+        st->nonfinite = 0;
+        io->status[0] = 0;
+        io->status[1] = PK_STOP_MAX_ITERATIONS;
+    }
+}
+
+// x_out := the last accepted iterate
+template <typename T>
+__global__ void copy_out_kernel(const T* xb0, const T* xb1, const DevState* st, const DevIo* io,
+                                int P) {
+    const T* src = (st->accepted & 1) ? xb1 : xb0;
+    T* dst = reinterpret_cast<T*>(io->x_out);
+    for (int p = blockIdx.x * kThreads + threadIdx.x; p < P; p += gridDim.x * kThreads)
+        dst[p] = src[p];
+}
+
+// max|x| -> fixed-point scale of the projector (standalone products)
+template <typename T>
+__global__ void __launch_bounds__(kThreads) maxabs_kernel(const T* x, int P, double* part,
+                                                          DevState* st, int bits) {
+    __shared__ double red_d[kThreads / 32];
+    __shared__ int last_flag;
+    double mx = 0.0;
+    for (int p = blockIdx.x * kThreads + threadIdx.x; p < P; p += gridDim.x * kThreads)
+        mx = fmax(mx, fabs((double)x[p]));
+    mx = block_max(mx, red_d);
+    if (threadIdx.x == 0) part[blockIdx.x] = mx;
+    if (!last_block(&st->cnt_misc, gridDim.x, &last_flag)) return;
+    double m2 = 0.0;
+    for (int q = threadIdx.x; q < (int)gridDim.x; q += kThreads) m2 = fmax(m2, part[q]);
+    m2 = block_max(m2, red_d);
+    if (threadIdx.x == 0) {
+        st->maxabs = m2;
+        const double sc = (m2 > 0.0 && isfinite(m2)) ? ldexp(1.0, bits) / m2 : 0.0;
+        st->scale64 = sc;
+        st->scale32 = (float)sc;
+    }
+}
+
+// ===========================================================================
+// sharded update (recon.py:330-338 on an all-reduced gradient) and its sums
+// ===========================================================================
+template <typename T>
+__global__ void __launch_bounds__(kThreads) grad_update_kernel(const T* x, const T* grad, T* xo,
+                                                               int nx, int ny,
+                                                               const DevParams* prm) {
+    const int p = blockIdx.x * kThreads + threadIdx.x;
+    if (p >= nx * ny) return;
+    const int i = p % nx, j = p / nx;
+    const T x0 = x[p];
+    T g = grad[p];
+    const T beta = (T)prm->beta, eps = (T)prm->eps, eta = (T)prm->step, lam = (T)prm->eta_alpha;
+    if (beta > (T)0) {
+        const T e2 = eps * eps;
+        T t = 0;
+        if (i < nx - 1) { const T d = x[p + 1] - x0; t -= d / sqrt(d * d + e2); }
+        if (i > 0) { const T d = x0 - x[p - 1]; t += d / sqrt(d * d + e2); }
+        if (j < ny - 1) { const T d = x[p + nx] - x0; t -= d / sqrt(d * d + e2); }
+        if (j > 0) { const T d = x0 - x[p - nx]; t += d / sqrt(d * d + e2); }
+        g += beta * t;
+    }
+    const T v = x0 - eta * g;
+    T mag = fabs(v) - lam;
+    mag = (mag != mag) ? mag : fmax(mag, (T)0);
+    T xn = (v > (T)0) ? mag : ((v < (T)0) ? -mag : (v != v ? v : (T)0));
+    if (prm->nonneg) xn = (xn != xn) ? xn : fmax(xn, (T)0);
+    xo[p] = xn;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) image_sums_kernel(const T* x, int nx, int ny,
+                                                              double* part, DevState* st,
+                                                              double* out) {
+    __shared__ double red_d[kThreads / 32];
+    __shared__ int last_flag;
+    double l1 = 0.0, tv = 0.0, bad = 0.0;
+    const int P = nx * ny;
+    for (int p = blockIdx.x * kThreads + threadIdx.x; p < P; p += gridDim.x * kThreads) {
+        const int i = p % nx, j = p / nx;
+        const double v = (double)x[p];
+        l1 += fabs(v);
+        if (i + 1 < nx) tv += fabs((double)x[p + 1] - v);
+        if (j + 1 < ny) tv += fabs((double)x[p + nx] - v);
+        if (!isfinite(v)) bad += 1.0;
+    }
+    l1 = block_sum(l1, red_d);
+    tv = block_sum(tv, red_d);
+    bad = block_sum(bad, red_d);
+    if (threadIdx.x == 0) {
+        part[3 * blockIdx.x] = l1;
+        part[3 * blockIdx.x + 1] = tv;
+        part[3 * blockIdx.x + 2] = bad;
+    }
+    if (!last_block(&st->cnt_misc, gridDim.x, &last_flag)) return;
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int q = threadIdx.x; q < (int)gridDim.x; q += kThreads) {
+        a += part[3 * q];
+        b += part[3 * q + 1];
+        c += part[3 * q + 2];
+    }
+    a = block_sum(a, red_d);
+    b = block_sum(b, red_d);
+    c = block_sum(c, red_d);
+    if (threadIdx.x == 0) {
+        out[0] = a;
+        out[1] = b;
+        out[2] = c;
+    }
+}
+
+// ===========================================================================
+// index dump (verification, fp64, forward.py:157-182)
+// ===========================================================================
+__global__ void index_dump_kernel(const double* px, const double* py, const double* sx,
+                                  const double* sy, double cdt, int nx, int P, int ma, int mb,
+                                  long long* s0_out, double* frac_out) {
+    const size_t n = (size_t)(mb - ma) * P;
+    for (size_t q = (size_t)blockIdx.x * kThreads + threadIdx.x; q < n;
+         q += (size_t)gridDim.x * kThreads) {
+        const int m = ma + (int)(q / P);
+        const int p = (int)(q % P);
+        const double u = delay_f64(px[p % nx], py[p / nx], sx[m], sy[m], cdt);
+        const double fl = floor(u);
+        s0_out[q] = (long long)fl;
+        if (frac_out) frac_out[q] = u - fl;
+    }
+}
+
+// fp64 -> plan dtype conversion and back (host API)
+template <typename T>
+__global__ void convert_kernel(const double* src, T* dst, size_t n) {
+    for (size_t q = (size_t)blockIdx.x * kThreads + threadIdx.x; q < n;
+         q += (size_t)gridDim.x * kThreads)
+        dst[q] = (T)src[q];
+}
+template <typename T>
+__global__ void widen_kernel(const T* src, double* dst, size_t n) {
+    for (size_t q = (size_t)blockIdx.x * kThreads + threadIdx.x; q < n;
+         q += (size_t)gridDim.x * kThreads)
+        dst[q] = (double)src[q];
+}
+
+}  // namespace pk

@@ -1,0 +1,263 @@
+"""Device policy and the geometry-backed operator (one ``pk_plan`` per geometry).
+
+``CudaPool`` takes the place of the reference's ``kernels.WorkerPool`` in the ``pool``
+slot of every public function (pkg/src/pactkit/kernels.py:55-73): it names the CUDA
+device and the arithmetic type.  ``DeviceOperator`` wraps the C ABI plan built from the
+provenance a reference ``MeasurementMatrix`` carries (grid / ring / acoustic,
+forward.py:70-121) -- the dense matrix is never formed.
+
+Host buffers cross the boundary as torch tensors (device memory, streams); torch is
+plumbing here, the arithmetic is in libpactgpu.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+__all__ = ["CudaPool", "DeviceOperator", "operator_for", "clear_plan_cache"]
+
+
+@dataclass(frozen=True)
+class CudaPool:
+    """Execution policy for the device path.
+
+    dtype "float32" is the production mode (fp32 storage and arithmetic, fp64 reductions);
+    "float64" is the validation mode (fp64 delays evaluated exactly like the reference).
+    """
+
+    device: int = 0
+    dtype: str = "float32"
+
+    def __post_init__(self):
+        if self.dtype not in ("float32", "float64"):
+            raise ValueError(f"dtype must be 'float32' or 'float64', got {self.dtype!r}")
+        if self.device < 0:
+            raise ValueError(f"device must be >= 0, got {self.device}")
+
+    @property
+    def pk_dtype(self) -> int:
+        return N.PK_F32 if self.dtype == "float32" else N.PK_F64
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _require_cuda(device: int):
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise N.NativeUnavailable("no CUDA device visible: the device path has no CPU fallback")
+    if device >= torch.cuda.device_count():
+        raise ValueError(f"CUDA device {device} not present")
+
+
+class DeviceOperator:
+    """K restricted to sensors [sensor_begin, sensor_end) of a ring, on one device."""
+
+    def __init__(self, grid, ring, acoustic, pool: CudaPool, sensor_begin=0, sensor_end=None):
+        _require_cuda(pool.device)
+        lib = N.load()
+        self.grid, self.ring, self.acoustic, self.pool = grid, ring, acoustic, pool
+        M = int(ring.count)
+        self.sensor_begin = int(sensor_begin)
+        self.sensor_end = M if sensor_end is None else int(sensor_end)
+        xx = np.ascontiguousarray(grid.origin[0] + np.arange(grid.nx) * grid.dx, dtype=np.float64)
+        yy = np.ascontiguousarray(grid.origin[1] + np.arange(grid.ny) * grid.dx, dtype=np.float64)
+        pos = np.ascontiguousarray(ring.positions, dtype=np.float64)
+        self._keep = (xx, yy, pos)
+        dp = ctypes.POINTER(ctypes.c_double)
+        desc = N.GeometryDesc(
+            nx=grid.nx, ny=grid.ny,
+            pixel_x=xx.ctypes.data_as(dp), pixel_y=yy.ctypes.data_as(dp),
+            sensors=M, sensor_xy=pos.ctypes.data_as(dp),
+            sensor_begin=self.sensor_begin, sensor_end=self.sensor_end,
+            samples=int(acoustic.q_s), c=float(acoustic.c), dt=float(acoustic.dt),
+            dtype=pool.pk_dtype, device=pool.device,
+        )
+        handle = ctypes.c_void_p()
+        N.check(lib.pk_plan_create(ctypes.byref(desc), ctypes.byref(handle)))
+        self._h = handle
+        self._lib = lib
+        info = N.PlanInfo()
+        N.check(lib.pk_plan_get_info(self._h, ctypes.byref(info)))
+        self.info = info
+        torch = _torch()
+        self.device = torch.device("cuda", pool.device)
+        self.tdtype = torch.float32 if pool.dtype == "float32" else torch.float64
+
+    # -- bookkeeping --------------------------------------------------------------
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def sensors(self) -> int:
+        return self.sensor_end - self.sensor_begin
+
+    @property
+    def samples(self) -> int:
+        return int(self.acoustic.q_s)
+
+    @property
+    def pixels(self) -> int:
+        return self.grid.size
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.pk_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown ordering
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def stream(self):
+        torch = _torch()
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def tensor(self, a) -> "object":
+        """Upload a host array (or move a tensor) to this operator's device and dtype."""
+        torch = _torch()
+        if isinstance(a, torch.Tensor):
+            return a.to(device=self.device, dtype=self.tdtype).contiguous()
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(
+            device=self.device, dtype=self.tdtype
+        ).contiguous()
+
+    def empty(self, n: int):
+        torch = _torch()
+        return torch.empty(n, device=self.device, dtype=self.tdtype)
+
+    # -- the seam: forward._matvec / forward._adjoint_matvec ----------------------
+    def matvec(self, x):
+        """(K x) restricted to this operator's sensors, as a device tensor."""
+        xt = self.tensor(x)
+        if xt.numel() != self.pixels:
+            raise ValueError(f"matrix has {self.pixels} columns but vector has {xt.numel()}")
+        out = self.empty(self.sensors * self.samples)
+        with _torch().cuda.device(self.device):
+            N.check(self._lib.pk_matvec(self._h, xt.data_ptr(), out.data_ptr(), self.stream()))
+        return out
+
+    def adjoint(self, y, scale: float = 1.0):
+        """scale * K^T y for y on this operator's sensors, as a device tensor."""
+        yt = self.tensor(y)
+        if yt.numel() != self.sensors * self.samples:
+            raise ValueError(
+                f"matrix has {self.sensors * self.samples} rows but signal has {yt.numel()} values"
+            )
+        out = self.empty(self.pixels)
+        with _torch().cuda.device(self.device):
+            N.check(self._lib.pk_adjoint_matvec(self._h, yt.data_ptr(), out.data_ptr(),
+                                                float(scale), self.stream()))
+        return out
+
+    def residual(self, x, y):
+        """(r = K x - y, sum r^2 as a 1-element fp64 device tensor); keeps r for adjoint_residual."""
+        torch = _torch()
+        xt, yt = self.tensor(x), self.tensor(y)
+        r = self.empty(self.sensors * self.samples)
+        ss = torch.empty(1, device=self.device, dtype=torch.float64)
+        with torch.cuda.device(self.device):
+            N.check(self._lib.pk_residual(self._h, xt.data_ptr(), yt.data_ptr(), r.data_ptr(),
+                                          ss.data_ptr(), self.stream()))
+        return r, ss
+
+    def adjoint_residual(self, scale: float = 1.0):
+        out = self.empty(self.pixels)
+        with _torch().cuda.device(self.device):
+            N.check(self._lib.pk_adjoint_residual(self._h, out.data_ptr(), float(scale),
+                                                  self.stream()))
+        return out
+
+    def grad_update(self, params: "N.SolverParams", x, grad):
+        """x_out = prox(x - eta*(grad + beta*tv_grad(x))) and [sum|x_out|, TV(x_out), #nonfinite]."""
+        torch = _torch()
+        xo = self.empty(self.pixels)
+        sums = torch.zeros(4, device=self.device, dtype=torch.float64)
+        with torch.cuda.device(self.device):
+            N.check(self._lib.pk_grad_update(self._h, ctypes.byref(params), x.data_ptr(),
+                                             grad.data_ptr(), xo.data_ptr(), sums.data_ptr(),
+                                             self.stream()))
+        return xo, sums
+
+    def reconstruct(self, y, params: "N.SolverParams"):
+        """Device-resident iterative_reconstruct; returns (x, history[4, N], status[2]) tensors."""
+        torch = _torch()
+        yt = self.tensor(y)
+        x = self.empty(self.pixels)
+        hist = torch.zeros(4 * params.iterations, device=self.device, dtype=torch.float64)
+        status = torch.zeros(2, device=self.device, dtype=torch.int32)
+        with torch.cuda.device(self.device):
+            N.check(self._lib.pk_reconstruct(self._h, ctypes.byref(params), yt.data_ptr(),
+                                             x.data_ptr(), hist.data_ptr(), status.data_ptr(),
+                                             self.stream()))
+        return x, hist.view(4, params.iterations), status
+
+    def reconstruct_host(self, y_host: np.ndarray, params: "N.SolverParams"):
+        """The C-ABI host-buffer entry (pk_reconstruct_host): fp64 in, fp64 out, synchronous."""
+        y = np.ascontiguousarray(y_host, dtype=np.float64)
+        x = np.empty(self.pixels)
+        hist = np.empty(4 * params.iterations)
+        status = np.zeros(2, dtype=np.int32)
+        dp = ctypes.POINTER(ctypes.c_double)
+        with _torch().cuda.device(self.device):
+            N.check(self._lib.pk_reconstruct_host(
+                self._h, ctypes.byref(params), y.ctypes.data_as(dp), x.ctypes.data_as(dp),
+                hist.ctypes.data_as(dp), status.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                self.stream()))
+        return x, hist.reshape(4, params.iterations), status
+
+    def index_dump(self, ma: int = 0, mb: int | None = None):
+        """fp64 (s0, frac) for local sensors [ma, mb) as device tensors [(mb-ma), P]."""
+        torch = _torch()
+        mb = self.sensors if mb is None else mb
+        n = (mb - ma) * self.pixels
+        s0 = torch.empty(n, device=self.device, dtype=torch.int64)
+        fr = torch.empty(n, device=self.device, dtype=torch.float64)
+        with torch.cuda.device(self.device):
+            N.check(self._lib.pk_index_dump(self._h, ma, mb, s0.data_ptr(), fr.data_ptr(),
+                                            self.stream()))
+        return s0.view(mb - ma, self.pixels), fr.view(mb - ma, self.pixels)
+
+
+_cache: dict = {}
+_cache_lock = threading.Lock()
+
+
+def _key(grid, ring, acoustic, pool, m0, m1):
+    return (
+        int(grid.nx), int(grid.ny), float(grid.dx), tuple(float(v) for v in grid.origin),
+        int(ring.count), float(ring.radius), tuple(float(v) for v in ring.center),
+        float(acoustic.c), float(acoustic.dt), int(acoustic.q_s),
+        pool.device, pool.dtype, int(m0), int(m1),
+    )
+
+
+def operator_for(grid, ring, acoustic, pool: CudaPool, sensor_begin=0, sensor_end=None):
+    """Cached DeviceOperator for a geometry (plans are reused across calls and frames)."""
+    m1 = int(ring.count) if sensor_end is None else int(sensor_end)
+    k = _key(grid, ring, acoustic, pool, sensor_begin, m1)
+    with _cache_lock:
+        op = _cache.get(k)
+        if op is None:
+            op = DeviceOperator(grid, ring, acoustic, pool, sensor_begin, m1)
+            _cache[k] = op
+        return op
+
+
+def clear_plan_cache():
+    with _cache_lock:
+        for op in _cache.values():
+            op.close()
+        _cache.clear()

@@ -1,0 +1,364 @@
+"""Acoustics, the (lazy) measurement operator, sensor data and projection.
+
+Mirror of the reference's ``pactkit.forward`` public surface (pkg/src/pactkit/forward.py)
+for the hot path.  The difference is the operator: ``build_time_matrix`` returns a
+geometry-backed ``MeasurementMatrix`` whose products run matrix-free on the B200
+(``DeviceOperator``); the dense (M*Q, P) array of forward.py:185-194 -- 2.2 TB at
+512^2 x 512 x 2048 -- is only formed if ``.entries`` is explicitly requested.
+
+Explicit matrices (``MeasurementMatrix(domain, entries)`` without provenance, e.g. read
+from a PACTMAT file) are supported through ``DenseOperator`` -- a cuBLAS GEMV on the
+device.
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .device import CudaPool, operator_for
+from .scene import GeometryError, ImageField, check_enclosure
+
+__all__ = [
+    "AcousticConfig",
+    "MeasurementMatrix",
+    "SensorData",
+    "TruncationWarning",
+    "DenseOperator",
+    "build_time_matrix",
+    "forward_project",
+    "add_noise",
+    "device_operator",
+]
+
+DEFAULT_SOUND_SPEED = 1500.0  # m/s (forward.py:32)
+
+
+class TruncationWarning(UserWarning):
+    """Some acoustic delays fall outside the acquisition window (forward.py:35-36)."""
+
+
+@dataclass(frozen=True)
+class AcousticConfig:
+    """Sound speed c, sample spacing dt, q_s time samples, q_n wavenumbers (forward.py:39-67)."""
+
+    c: float = DEFAULT_SOUND_SPEED
+    dt: float = 1e-7
+    q_s: int = 64
+    q_n: int = 64
+
+    def __post_init__(self):
+        if not (self.c > 0 and self.dt > 0):
+            raise ValueError(f"c and dt must be > 0, got c={self.c}, dt={self.dt}")
+        if self.q_s < 1 or self.q_n < 1:
+            raise ValueError(f"sample counts must be >= 1, got q_s={self.q_s}, q_n={self.q_n}")
+
+    @property
+    def k_values(self) -> np.ndarray:
+        n = np.arange(1, self.q_n + 1, dtype=np.float64)
+        return 2.0 * np.pi * n / (self.q_s * self.dt) / self.c
+
+    @property
+    def window(self) -> float:
+        return self.q_s * self.dt
+
+
+@dataclass(frozen=True)
+class SensorData:
+    """Stacked per-sensor traces; sensor m owns [m*samples, (m+1)*samples) (forward.py:124-150)."""
+
+    domain: str
+    sensors: int
+    samples: int
+    values: np.ndarray
+
+    def __post_init__(self):
+        if self.domain not in ("time", "frequency"):
+            raise ValueError(f"unknown domain {self.domain!r}")
+        want = np.complex128 if self.domain == "frequency" else np.float64
+        v = np.ascontiguousarray(np.asarray(self.values).ravel(), dtype=want)
+        if v.size != self.sensors * self.samples:
+            raise ValueError(
+                f"signal length {v.size} != sensors*samples = {self.sensors * self.samples}"
+            )
+        if not np.all(np.isfinite(v.view(np.float64))):
+            raise ValueError("sensor data must be finite")
+        v.setflags(write=False)
+        object.__setattr__(self, "values", v)
+
+    @property
+    def length(self) -> int:
+        return self.values.size
+
+
+@dataclass(frozen=True, eq=False)
+class MeasurementMatrix:
+    """The discretised operator K.
+
+    Geometry-backed (``provenance`` holds grid / ring / acoustic, as build_time_matrix
+    records them, forward.py:207-215): products run matrix-free on the device and
+    ``entries`` is materialised only on request.  Explicit (``entries`` given): the dense
+    array is the operator.
+    """
+
+    domain: str
+    entries_: np.ndarray | None = None
+    provenance: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        if self.domain not in ("time", "frequency"):
+            raise ValueError(f"unknown domain {self.domain!r}")
+        if self.entries_ is not None:
+            want = np.complex128 if self.domain == "frequency" else np.float64
+            e = np.ascontiguousarray(np.asarray(self.entries_), dtype=want)
+            if e.ndim != 2:
+                raise ValueError("matrix entries must be 2-D")
+            e.setflags(write=False)
+            object.__setattr__(self, "entries_", e)
+        elif not self.geometry_backed:
+            raise ValueError("a MeasurementMatrix needs entries or grid/ring/acoustic provenance")
+
+    @property
+    def geometry_backed(self) -> bool:
+        p = self.provenance
+        return self.entries_ is None and all(p.get(k) is not None for k in ("grid", "ring", "acoustic"))
+
+    @property
+    def grid(self):
+        return self.provenance.get("grid")
+
+    @property
+    def ring(self):
+        return self.provenance.get("ring")
+
+    @property
+    def acoustic(self):
+        return self.provenance.get("acoustic")
+
+    @property
+    def rows(self) -> int:
+        if self.entries_ is not None:
+            return self.entries_.shape[0]
+        q = self.acoustic.q_s if self.domain == "time" else self.acoustic.q_n
+        return self.ring.count * q
+
+    @property
+    def cols(self) -> int:
+        if self.entries_ is not None:
+            return self.entries_.shape[1]
+        return self.grid.size
+
+    def layout(self) -> tuple[int, int]:
+        """(sensor count, samples per sensor); needs builder provenance (forward.py:114-121)."""
+        ring, ac = self.ring, self.acoustic
+        if ring is None or ac is None:
+            raise ValueError("matrix has no builder provenance; pass the layout explicitly")
+        return ring.count, (ac.q_s if self.domain == "time" else ac.q_n)
+
+    @property
+    def entries(self) -> np.ndarray:
+        """Dense K.  Geometry-backed matrices materialise it from the device's fp64 index
+        dump (pk_index_dump, the same s0/frac the reference computes) -- small scenes only."""
+        if self.entries_ is not None:
+            return self.entries_
+        M, Q = self.ring.count, self.acoustic.q_s
+        P = self.grid.size
+        if M * Q * P > 64 * 1024 * 1024:
+            raise MemoryError(f"refusing to materialise a {M * Q} x {P} dense matrix")
+        op = operator_for(self.grid, self.ring, self.acoustic, CudaPool(dtype="float64"))
+        s0, fr = op.index_dump()
+        s0 = s0.cpu().numpy()
+        fr = fr.cpu().numpy()
+        w = 1.0 / (2.0 * np.pi * self.acoustic.c)
+        K = np.zeros((M * Q, P))
+        cols = np.broadcast_to(np.arange(P), s0.shape)
+        m_idx = np.arange(M)[:, None]
+        lo_ok = (s0 >= 1) & (s0 <= Q)
+        hi_ok = (s0 >= 0) & (s0 <= Q - 1)
+        K[(m_idx * Q + s0 - 1)[lo_ok], cols[lo_ok]] = (1.0 - fr[lo_ok]) * w
+        K[(m_idx * Q + s0)[hi_ok], cols[hi_ok]] = fr[hi_ok] * w
+        K.setflags(write=False)
+        object.__setattr__(self, "entries_", K)
+        return K
+
+
+# ---------------------------------------------------------------------------
+# operators
+
+
+class DenseOperator:
+    """Explicit matrix on the device; products are cuBLAS GEMV (torch.mv)."""
+
+    def __init__(self, entries: np.ndarray, pool: CudaPool):
+        import torch
+
+        from .device import _require_cuda
+
+        _require_cuda(pool.device)
+        self.pool = pool
+        self.device = torch.device("cuda", pool.device)
+        cplx = np.iscomplexobj(entries)
+        if pool.dtype == "float32":
+            self.tdtype = torch.complex64 if cplx else torch.float32
+        else:
+            self.tdtype = torch.complex128 if cplx else torch.float64
+        self.A = torch.from_numpy(np.ascontiguousarray(entries)).to(self.device, self.tdtype)
+        self.rows, self.cols = entries.shape
+
+    def tensor(self, a):
+        import torch
+
+        if isinstance(a, torch.Tensor):
+            return a.to(device=self.device, dtype=self.tdtype)
+        return torch.from_numpy(np.ascontiguousarray(a)).to(self.device, self.tdtype)
+
+    def matvec(self, x):
+        return self.A @ self.tensor(x)
+
+    def adjoint(self, y, scale: float = 1.0):
+        out = self.A.conj().T @ self.tensor(y)
+        return out * scale if scale != 1.0 else out
+
+
+_dense_cache: dict = {}
+
+
+def _as_pool(pool) -> CudaPool:
+    """The device policy for a ``pool`` argument.  None or a reference WorkerPool select the
+    default device pool -- every product runs on the GPU (no CPU path)."""
+    if isinstance(pool, CudaPool):
+        return pool
+    return CudaPool()
+
+
+def device_operator(K, pool=None):
+    """DeviceOperator (geometry-backed) or DenseOperator (explicit) for K.
+
+    Accepts this package's MeasurementMatrix and the reference's own
+    ``pactkit.forward.MeasurementMatrix`` (duck-typed on .provenance / .entries).
+    """
+    pool = _as_pool(pool)
+    prov = getattr(K, "provenance", {}) or {}
+    has_geo = all(prov.get(k) is not None for k in ("grid", "ring", "acoustic"))
+    explicit = getattr(K, "entries_", None) if isinstance(K, MeasurementMatrix) else None
+    if has_geo and explicit is None and K.domain == "time":
+        return operator_for(prov["grid"], prov["ring"], prov["acoustic"], pool)
+    entries = K.entries if not isinstance(K, np.ndarray) else K
+    key = (id(entries), pool)
+    op = _dense_cache.get(key)
+    if op is None or op[0] is not entries:
+        op = (entries, DenseOperator(entries, pool))
+        _dense_cache.clear()
+        _dense_cache[key] = op
+    return op[1]
+
+
+# ---------------------------------------------------------------------------
+# building the operator
+
+
+def _pair_bounds(grid, ring, acoustic):
+    """Per-sensor min/max delay in samples over the grid rectangle (host, O(M))."""
+    xs, ys = grid.axis_vectors() if hasattr(grid, "axis_vectors") else (
+        grid.origin[0] + np.arange(grid.nx) * grid.dx, grid.origin[1] + np.arange(grid.ny) * grid.dx)
+    pos = np.asarray(ring.positions)
+    cx = np.clip(pos[:, 0], xs[0], xs[-1])
+    cy = np.clip(pos[:, 1], ys[0], ys[-1])
+    dmin = np.hypot(cx - pos[:, 0], cy - pos[:, 1])
+    fx = np.maximum(np.abs(xs[0] - pos[:, 0]), np.abs(xs[-1] - pos[:, 0]))
+    fy = np.maximum(np.abs(ys[0] - pos[:, 1]), np.abs(ys[-1] - pos[:, 1]))
+    cdt = acoustic.c * acoustic.dt
+    return dmin / cdt, np.hypot(fx, fy) / cdt
+
+
+def _count_truncated(grid, ring, acoustic) -> int:
+    """Exact truncated-pair count of forward.py:196-198.  Only evaluated when the O(M)
+    bounds say truncation is possible; uses the reference's own arithmetic (np.hypot)."""
+    lo, hi = _pair_bounds(grid, ring, acoustic)
+    q = acoustic.q_s
+    if lo.min() >= 1.0 + 1e-9 and hi.max() < q - 1 - 1e-9:
+        return 0
+    pix = grid.pixel_coords()
+    cdt = acoustic.c * acoustic.dt
+    total = 0
+    for m0 in range(0, ring.count, 64):
+        pos = ring.positions[m0 : m0 + 64]
+        d = np.hypot(pix[None, :, 0] - pos[:, 0:1], pix[None, :, 1] - pos[:, 1:2])
+        u = d / cdt
+        s0 = np.floor(u).astype(np.int64)
+        frac = u - s0
+        in0 = (s0 >= 1) & (s0 <= q)
+        in1 = (s0 + 1 >= 1) & (s0 + 1 <= q)
+        total += int(np.count_nonzero(~in0 | (~in1 & (frac > 0.0))))
+    return total
+
+
+def build_time_matrix(grid, ring, acoustic) -> MeasurementMatrix:
+    """Time-domain operator of forward.py:167-215, without forming the dense matrix.
+
+    Same validation (ring must enclose the grid, no sensor on a pixel centre) and the same
+    TruncationWarning / ``truncated_pairs`` provenance.
+    """
+    check_enclosure(grid, ring)
+    xs = grid.origin[0] + np.arange(grid.nx) * grid.dx
+    ys = grid.origin[1] + np.arange(grid.ny) * grid.dx
+    pos = np.asarray(ring.positions)
+    hit = np.isin(pos[:, 0], xs) & np.isin(pos[:, 1], ys)
+    if hit.any():
+        m = int(np.flatnonzero(hit)[0])
+        i = int(np.flatnonzero(xs == pos[m, 0])[0])
+        j = int(np.flatnonzero(ys == pos[m, 1])[0])
+        raise GeometryError(f"sensor {m} coincides with pixel index {j * grid.nx + i}")
+    truncated = _count_truncated(grid, ring, acoustic)
+    if truncated:
+        warnings.warn(
+            f"{truncated} pixel-sensor delays fall (partly) outside the "
+            f"{acoustic.window:g} s acquisition window; their weights are dropped",
+            TruncationWarning,
+            stacklevel=2,
+        )
+    return MeasurementMatrix(
+        "time",
+        None,
+        provenance={"grid": grid, "ring": ring, "acoustic": acoustic, "truncated_pairs": truncated},
+    )
+
+
+def _grid_values(x):
+    return np.asarray(getattr(x, "values", x))
+
+
+def forward_project(K, x, pool=None) -> SensorData:
+    """y = K vec(x) on the device (forward.py:253-261)."""
+    grid = getattr(x, "grid", None)
+    if grid is not None and K.cols != grid.size:
+        raise ValueError(f"matrix has {K.cols} columns but field has {grid.size} pixels")
+    sensors, samples = K.layout()
+    op = device_operator(K, pool)
+    y = op.matvec(_grid_values(x))
+    yv = y.detach().cpu().numpy()
+    if K.domain == "time":
+        yv = yv.astype(np.float64)
+    else:
+        yv = yv.astype(np.complex128)
+    return SensorData(K.domain, sensors, samples, yv)
+
+
+def add_noise(y: SensorData, sigma: float, seed: int) -> SensorData:
+    """Seeded i.i.d. Gaussian noise (forward.py:264-275); host-side input preparation."""
+    if sigma < 0:
+        raise ValueError(f"sigma must be >= 0, got {sigma}")
+    if sigma == 0:
+        return y
+    rng = np.random.default_rng(seed)
+    if y.domain == "frequency":
+        noise = rng.normal(0.0, sigma, y.length) + 1j * rng.normal(0.0, sigma, y.length)
+    else:
+        noise = rng.normal(0.0, sigma, y.length)
+    return SensorData(y.domain, y.sensors, y.samples, y.values + noise)
+
+
+def make_image(grid, values) -> ImageField:
+    return ImageField(grid, values)

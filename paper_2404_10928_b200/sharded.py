@@ -1,0 +1,142 @@
+"""Multi-GPU drivers: one process per GPU, torch.distributed (NCCL) for the plumbing.
+
+Two natural shardings of the hot path:
+
+* ``SensorShardedSolver`` -- one large frame, sensors split across ranks.  Rank g owns
+  sensors [g*M/G, (g+1)*M/G) and its slice of y and r; x is replicated.  Per iteration:
+  local back-projection (partial 2 K_g^T r_g) -> all-reduce(sum) of the image-sized
+  gradient -> identical update on every rank -> local projection and residual ->
+  all-reduce of the data-term scalar.  This is the only exchange the algorithm has.
+* ``FrameShardedSolver`` -- a dynamic sequence: independent frames per rank, no
+  collective at all (weak scaling).
+
+The per-rank compute goes through an ``ops`` object; the production one is
+``DeviceShardOps`` (C ABI kernels on the rank's GPU).  Tests substitute a CPU
+implementation to exercise the sharding / reduction / stopping logic with gloo.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .device import CudaPool, operator_for
+from .solver import DIVERGENCE_STREAK, ReconConfig, solver_params
+
+__all__ = ["shard_range", "DeviceShardOps", "SensorShardedSolver", "FrameShardedSolver"]
+
+
+def shard_range(count: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced split of [0, count) -- sizes differ by at most one."""
+    if not (0 <= rank < world):
+        raise ValueError(f"rank {rank} outside world of {world}")
+    if count < world:
+        raise ValueError(f"cannot split {count} sensors over {world} ranks")
+    base, extra = divmod(count, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+class DeviceShardOps:
+    """Per-rank kernels (C ABI) for a sensor shard."""
+
+    def __init__(self, grid, ring, acoustic, pool: CudaPool, m0: int, m1: int):
+        self.op = operator_for(grid, ring, acoustic, pool, m0, m1)
+        self.pixels = grid.size
+
+    def zeros_image(self):
+        import torch
+
+        return torch.zeros(self.pixels, device=self.op.device, dtype=self.op.tdtype)
+
+    def residual(self, x, y_local):
+        """r = K_g x - y_g kept on the device for the next back-projection; returns sum r^2
+        as a 1-element fp64 tensor."""
+        _, ss = self.op.residual(x, y_local)
+        return ss
+
+    def backproject(self):
+        """2 K_g^T r_g (partial data gradient)."""
+        return self.op.adjoint_residual(2.0)
+
+    def update(self, params, x, grad):
+        """x' = prox(x - eta (grad + beta tv_grad x)); returns (x', [sum|x'|, TV(x'), #nonfinite])."""
+        return self.op.grad_update(params, x, grad)
+
+
+@dataclass
+class ShardResult:
+    image: np.ndarray
+    history: np.ndarray  # (n, 4): total, data, l1, tv
+    iterations_run: int
+    stopped_by: str
+
+
+class SensorShardedSolver:
+    """iterative_reconstruct (recon.py:286-377) over sensor shards with an all-reduce."""
+
+    def __init__(self, ops, group=None):
+        self.ops = ops
+        self.group = group
+
+    def _allreduce(self, t):
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            dist.all_reduce(t, group=self.group)
+        return t
+
+    def solve(self, y_local, config: ReconConfig, alpha: float, beta: float, step: float) -> ShardResult:
+        import torch
+
+        params = solver_params(config, alpha, beta, step)
+        x = self.ops.zeros_image()
+        ss = self.ops.residual(x, y_local)  # r0 = -y
+        f_prev = float(self._allreduce(ss.clone())[0])
+        hist = []
+        stopped_by = "max_iterations"
+        grow = 0
+        for _ in range(config.iterations):
+            grad = self.ops.backproject()
+            self._allreduce(grad)
+            x_new, sums = self.ops.update(params, x, grad)
+            ss = self.ops.residual(x_new, y_local)
+            data = float(self._allreduce(ss.clone())[0])
+            s = sums.double().cpu().numpy()
+            l1, tvv, bad = alpha * float(s[0]), beta * float(s[1]), float(s[2])
+            total = data + l1 + tvv
+            if not math.isfinite(total) or bad > 0:
+                stopped_by = "divergence"
+                # the residual kept by the device is r(x_new); x stays the last accepted one
+                break
+            hist.append((total, data, l1, tvv))
+            x = x_new
+            grow = grow + 1 if total > f_prev else 0
+            if grow >= DIVERGENCE_STREAK:
+                stopped_by = "divergence"
+                break
+            rel = abs(total - f_prev) / max(abs(f_prev), 1e-300)
+            f_prev = total
+            if config.tolerance > 0 and rel < config.tolerance:
+                stopped_by = "tolerance"
+                break
+        img = x.double().cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x, dtype=np.float64)
+        return ShardResult(img, np.array(hist, dtype=np.float64).reshape(-1, 4), len(hist), stopped_by)
+
+
+class FrameShardedSolver:
+    """Independent frames of a dynamic sequence on this rank (no collective)."""
+
+    def __init__(self, grid, ring, acoustic, pool: CudaPool):
+        self.op = operator_for(grid, ring, acoustic, pool)
+
+    @staticmethod
+    def frames_of(total: int, rank: int, world: int) -> range:
+        lo, hi = shard_range(total, rank, world)
+        return range(lo, hi)
+
+    def solve(self, y, config: ReconConfig, alpha: float, beta: float, step: float):
+        params = solver_params(config, alpha, beta, step)
+        return self.op.reconstruct(y, params)

@@ -1,0 +1,59 @@
+"""Synthetic scenes of the benchmark configurations (BASELINE.json ``configs``).
+
+``make_scene`` restates the reference's scene builder (pkg/src/pactkit/bench.py:193-203):
+a centred 1e-4 m grid, a ring at 1.8x the farthest pixel, c = 1500 m/s and dt chosen so
+every delay fits the window.  ``CONFIGS`` names the five BASELINE configurations.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .measurement import AcousticConfig
+from .scene import centered_grid, make_ring, make_vessel_phantom
+
+__all__ = ["make_scene", "Workload", "CONFIGS"]
+
+
+def make_scene(grid_size: int, sensors: int, samples: int, seed: int = 0, branches: int = 5):
+    """(grid, ring, acoustic, phantom), bit-identical to the reference's make_scene."""
+    grid = centered_grid(grid_size, grid_size, 1e-4)
+    max_pix = np.hypot((grid_size - 1) / 2, (grid_size - 1) / 2) * grid.dx
+    radius = 1.8 * max_pix
+    c = 1500.0
+    dt = 1.05 * (radius + max_pix) / c / samples
+    ring = make_ring(sensors, radius, (0.0, 0.0), grid)
+    acoustic = AcousticConfig(c=c, dt=dt, q_s=samples, q_n=samples)
+    phantom = make_vessel_phantom(grid, seed, branches)
+    return grid, ring, acoustic, phantom
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    n: int          # image n x n
+    sensors: int
+    samples: int
+    iterations: int
+    frames: int = 1
+
+    @property
+    def pixels(self) -> int:
+        return self.n * self.n
+
+    @property
+    def interactions_per_projection(self) -> int:
+        """Sensor-pixel pairs per projection (the algorithmic work unit)."""
+        return self.sensors * self.pixels
+
+
+CONFIGS = {
+    "cfg1": Workload("cfg1: 128^2, 128 sensors x 1024 samples, 10 it", 128, 128, 1024, 10),
+    "cfg2": Workload("cfg2: 256^2, 256 sensors x 2048 samples, 20 it", 256, 256, 2048, 20),
+    "cfg3": Workload("cfg3: 512^2, 512 sensors x 2048 samples, 10 it", 512, 512, 2048, 10),
+    "cfg4": Workload("cfg4: 1024 frames of 256^2, 256 sensors x 2048 samples, 20 it",
+                     256, 256, 2048, 20, frames=1024),
+    "cfg5": Workload("cfg5: 1024^2, 1024 sensors x 4096 samples, 50 it", 1024, 1024, 4096, 50),
+}

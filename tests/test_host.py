@@ -1,0 +1,134 @@
+"""Host-side logic of the drop-in package (no GPU): geometry mirror bit-exactness, config
+validation, operator construction and the C-ABI library's symbol table."""
+
+import ctypes
+import hashlib
+import json
+import os
+import re
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_2404_10928_b200 as pk
+from paper_2404_10928_b200 import _native
+from conftest import GOLDEN, ROOT
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_scene_geometry_bit_exact_with_reference():
+    for rec in json.load(open(os.path.join(GOLDEN, "geometry.json"))):
+        if rec.get("custom"):
+            g = pk.make_grid(24, 20, 2e-4, (1e-3, -2e-3))
+            ring = pk.make_ring(12, 9e-3, (3.3e-3, -0.1e-3), g)
+            assert sha(g.pixel_coords()) == rec["pixel_coords"]
+            assert sha(ring.positions) == rec["positions"]
+            assert sha(pk.make_vessel_phantom(g, 5, 3).values) == rec["phantom"]
+            continue
+        g, ring, ac, ph = pk.make_scene(rec["n"], rec["M"], rec["Q"], seed=rec["seed"])
+        assert ac.dt.hex() == rec["dt"]
+        assert ring.radius.hex() == rec["radius"]
+        assert [v.hex() for v in g.origin] == rec["origin"]
+        assert sha(g.pixel_coords()) == rec["pixel_coords"]
+        assert sha(ring.positions) == rec["positions"]
+        assert sha(ph.values) == rec["phantom"]
+
+
+def test_recon_config_validation():
+    with pytest.raises(ValueError):
+        pk.ReconConfig(alpha=-1.0)
+    with pytest.raises(ValueError):
+        pk.ReconConfig(iterations=0)
+    with pytest.raises(ValueError):
+        pk.ReconConfig(step=0.0)
+    with pytest.raises(ValueError):
+        pk.ReconConfig(step="fast")
+    with pytest.raises(ValueError):
+        pk.ReconConfig(tv_epsilon=0.0)
+
+
+def test_build_time_matrix_is_lazy_and_validates():
+    g, ring, ac, _ = pk.make_scene(512, 512, 2048)
+    K = pk.build_time_matrix(g, ring, ac)  # 2.2 TB dense -- must not be formed
+    assert K.rows == 512 * 2048 and K.cols == 512 * 512
+    assert K.provenance["truncated_pairs"] == 0
+    assert K.layout() == (512, 2048)
+    bad = pk.TransducerRing(8, 1e-3)
+    with pytest.raises(pk.GeometryError):
+        pk.build_time_matrix(pk.centered_grid(64, 64, 1e-4), bad, pk.AcousticConfig())
+
+
+def test_truncation_warning_count_matches_reference():
+    t = json.load(open(os.path.join(GOLDEN, "kat.json")))["truncation"]
+    g = pk.centered_grid(16, 16, 1e-4)
+    ring = pk.make_ring(4, 5e-3, (0, 0), g)
+    with pytest.warns(pk.TruncationWarning):
+        K = pk.build_time_matrix(g, ring, pk.AcousticConfig(c=1500.0, dt=1e-7, q_s=8, q_n=8))
+    assert K.provenance["truncated_pairs"] == t["truncated_pairs"]
+
+
+def test_sensor_data_and_field_validation():
+    with pytest.raises(ValueError):
+        pk.SensorData("time", 2, 3, np.zeros(5))
+    with pytest.raises(ValueError):
+        pk.SensorData("time", 1, 2, np.array([0.0, np.nan]))
+    g = pk.make_grid(2, 2, 1.0)
+    with pytest.raises(ValueError):
+        pk.ImageField(g, np.zeros(3))
+    with pytest.raises(ValueError):
+        pk.CudaPool(dtype="float16")
+
+
+def _header_symbols():
+    txt = open(os.path.join(ROOT, "include", "pactgpu.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(pk_\w+)\s*\(", txt, re.M)))
+
+
+def test_abi_library_exports_every_header_symbol():
+    """The C-ABI library loads without a GPU and exports what include/pactgpu.h declares."""
+    _native.build()
+    lib = _native.load()
+    syms = _header_symbols()
+    assert len(syms) >= 12
+    bound = {name for name, _, _ in _native.SYMBOLS}
+    for s in syms:
+        assert hasattr(lib, s), s
+        assert s in bound, f"{s} not bound in _native.SYMBOLS"
+    assert lib.pk_version() >= 10000
+
+
+def test_abi_rejects_bad_arguments_without_gpu():
+    lib = _native.load()
+    h = ctypes.c_void_p()
+    assert lib.pk_plan_create(None, ctypes.byref(h)) == _native.PK_ERR_INVALID
+    xx = np.zeros(1)
+    dp = ctypes.POINTER(ctypes.c_double)
+    desc = _native.GeometryDesc(nx=0, ny=1, pixel_x=xx.ctypes.data_as(dp), pixel_y=xx.ctypes.data_as(dp),
+                                sensors=1, sensor_xy=xx.ctypes.data_as(dp), sensor_begin=0,
+                                sensor_end=1, samples=4, c=1.0, dt=1.0, dtype=0, device=0)
+    assert lib.pk_plan_create(ctypes.byref(desc), ctypes.byref(h)) == _native.PK_ERR_INVALID
+    assert b"grid" in lib.pk_last_error()
+
+
+def test_no_cpu_fallback_when_no_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    g, ring, ac, ph = pk.make_scene(16, 8, 40)
+    K = pk.build_time_matrix(g, ring, ac)
+    with pytest.raises(_native.NativeUnavailable):
+        pk.forward_project(K, ph)
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2404_10928_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*", "", src).replace("oracle/", ""), f
