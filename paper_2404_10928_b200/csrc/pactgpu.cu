@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -92,7 +93,7 @@ void free_plan(pk_plan* p) {
     void* ptrs[] = {p->pxs, p->pys, p->sxs, p->sys, p->px, p->py, p->sx, p->sy, p->table,
                     p->acc, p->xbuf[0], p->xbuf[1], p->ydev, p->y64, p->x64, p->hist_dev,
                     p->status_dev, p->part_bp, p->part_tv, p->part_r, p->part_misc, p->state,
-                    p->params, p->io, p->xout_dev};
+                    p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
@@ -100,6 +101,25 @@ void free_plan(pk_plan* p) {
 }
 
 size_t tsize(const pk_plan* p) { return p->dtype == PK_F32 ? 4 : 8; }
+
+cudaError_t opt_in_smem(int device) {
+    static bool done[64] = {};
+    if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
+    if (done[device]) return cudaSuccess;
+    int mx = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    mx -= 1024;  // headroom for the kernels' static shared memory
+    const void* ks[] = {(const void*)bp_f32_kernel<true, true, true>, (const void*)bp_f32_kernel<true, false, true>,
+                        (const void*)bp_f32_kernel<false, true, true>, (const void*)bp_f32_kernel<false, false, true>,
+                        (const void*)bp_f32_kernel<true, true, false>, (const void*)bp_f32_kernel<true, false, false>,
+                        (const void*)bp_f32_kernel<false, true, false>, (const void*)bp_f32_kernel<false, false, false>,
+                        (const void*)fp_f32_kernel<false>, (const void*)fp_f64_kernel,
+                        (const void*)finalize_kernel<float>, (const void*)finalize_kernel<double>};
+    for (const void* k : ks)
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    if (e == cudaSuccess) done[device] = true;
+    return e;
+}
 
 // ---------------------------------------------------------------------------
 // kernel sequences
@@ -159,6 +179,7 @@ int launch_finalize(pk_plan* p, const void* y, void* trace_out, double* sumsq, i
         a.st = p->state; a.prm = p->params; a.io = p->io; a.part_r = p->part_r;
         a.part_tv = p->part_tv; a.ntv = p->fp_tiles_x * p->fp_tiles_y; a.sumsq_out = sumsq;
         a.solver = solver;
+        a.atrick = p->bp_atrick;
         finalize_kernel<float><<<p->M, kThreads, sm, s>>>(a);
     } else {
         FinArgs<double> a{};
@@ -190,14 +211,17 @@ int launch_bp(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_t s
         a.xb0 = static_cast<float*>(p->xbuf[0]);
         a.xb1 = static_cast<float*>(p->xbuf[1]);
         a.prm = p->params; a.st = p->state; a.part = p->part_bp; a.bits = p->fp_bits;
-        const int grid = p->bp_tiles_x * p->bp_tiles_y;
-        if (epi) {
-            if (clamp) bp_f32_kernel<true, true><<<grid, kThreads, p->bp_smem, s>>>(a);
-            else bp_f32_kernel<true, false><<<grid, kThreads, p->bp_smem, s>>>(a);
+        a.split = p->bp_split; a.ms = p->bp_ms; a.gpart = p->bp_gpart; a.tile_cnt = p->bp_tile_cnt;
+        const dim3 grid(p->bp_tiles_x * p->bp_tiles_y, p->bp_split);
+#define PK_BP(E, C, A) bp_f32_kernel<E, C, A><<<grid, kThreads, p->bp_smem, s>>>(a)
+        if (p->bp_atrick) {
+            if (epi) { if (clamp) PK_BP(true, true, true); else PK_BP(true, false, true); }
+            else { if (clamp) PK_BP(false, true, true); else PK_BP(false, false, true); }
         } else {
-            if (clamp) bp_f32_kernel<false, true><<<grid, kThreads, p->bp_smem, s>>>(a);
-            else bp_f32_kernel<false, false><<<grid, kThreads, p->bp_smem, s>>>(a);
+            if (epi) { if (clamp) PK_BP(true, true, false); else PK_BP(true, false, false); }
+            else { if (clamp) PK_BP(false, true, false); else PK_BP(false, false, false); }
         }
+#undef PK_BP
     } else {
         BpArgs64 a{};
         a.table = static_cast<const double2*>(p->table);
@@ -220,11 +244,11 @@ int launch_table(pk_plan* p, const void* y, int init, cudaStream_t s) {
     if (p->dtype == PK_F32)
         table_kernel<float><<<p->M, kThreads, 0, s>>>(
             static_cast<const float*>(y), p->io, static_cast<float2*>(p->table), p->M, p->Q, p->TS,
-            init ? -1.f : 1.f, p->part_r, p->state, init);
+            init ? -1.f : 1.f, p->part_r, p->state, init, p->bp_atrick);
     else
         table_kernel<double><<<p->M, kThreads, 0, s>>>(
             static_cast<const double*>(y), p->io, static_cast<double2*>(p->table), p->M, p->Q,
-            p->TS, init ? -1.0 : 1.0, p->part_r, p->state, init);
+            p->TS, init ? -1.0 : 1.0, p->part_r, p->state, init, 0);
     PK_CHECK_LAUNCH();
     return PK_OK;
 }
@@ -392,6 +416,10 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         return std::sqrt(ex * ex + ey * ey);
     };
     p->TS = (p->Q + 2 + 1) & ~1;
+    {
+        const char* ev = getenv("PK_BP_ATRICK");
+        p->bp_atrick = (p->dtype == PK_F32) ? (ev ? atoi(ev) != 0 : 1) : 0;
+    }
     // back-projector
     p->bp_tiles_x = (p->nx + kBpTile - 1) / kBpTile;
     p->bp_tiles_y = (p->ny + kBpTile - 1) / kBpTile;
@@ -401,15 +429,29 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     const int bp_budget = 72 * 1024;
     p->bp_CS = std::max(1, std::min(32, bp_budget / (p->bp_nbuf * p->bp_L * 8)));
     p->bp_smem = p->bp_nbuf * p->bp_CS * p->bp_L * 8 + p->bp_nbuf * p->bp_CS * 16 + p->bp_nbuf * 8;
+    {   // sensor split so that tiles x split >= ~4 CTAs per SM, each split >= 64 sensors
+        const int tiles = p->bp_tiles_x * p->bp_tiles_y;
+        int sp = 1;
+        while (tiles * sp < 4 * 148 && p->M / (2 * sp) >= 64) sp *= 2;
+        p->bp_split = sp;
+        p->bp_ms = (p->M + sp - 1) / sp;
+        p->bp_ms = ((p->bp_ms + p->bp_CS - 1) / p->bp_CS) * p->bp_CS;  // whole chunks
+        p->bp_split = (p->M + p->bp_ms - 1) / p->bp_ms;
+    }
     if (p->dtype == PK_F32 && p->bp_smem > 200 * 1024) {
         free_plan(p);
         return fail(PK_ERR_UNSUPPORTED, "delay window per tile too long (%d samples)", p->bp_L);
     }
     // projector
-    p->fp_T = 32;
+    // projector tile: 64 x 64 when that still gives >= 4 CTAs per SM (halves the window
+    // flush traffic per interaction), else 32 x 32
+    p->fp_groups = (p->M + 31) / 32;
+    {
+        const int t64 = ((p->nx + 63) / 64) * ((p->ny + 63) / 64);
+        p->fp_T = (p->dtype == PK_F32 && (int64_t)t64 * p->fp_groups >= 4 * 148) ? 64 : 32;
+    }
     p->fp_tiles_x = (p->nx + p->fp_T - 1) / p->fp_T;
     p->fp_tiles_y = (p->ny + p->fp_T - 1) / p->fp_T;
-    p->fp_groups = (p->M + 31) / 32;
     p->fp_L = (int)std::ceil(tile_diag(p->fp_T)) + 6;
     // contributions one window slot can receive: tile pixels in a band of 2 samples
     double nc_tile = 1.5 * (p->fp_T * std::sqrt(2.0) + 2) * (2.0 / std::max(h, 1e-12) + 2);
@@ -417,7 +459,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     nc_tile = std::min(nc_tile, (double)p->fp_T * p->fp_T);
     if (p->dtype == PK_F32) {
         p->fp_bits = std::min(22, 30 - ceil_log2(nc_tile));
-        p->fp_smem = p->fp_L * 32 * 4 + p->fp_T * p->fp_T * 16 + p->fp_T * 4;
+        p->fp_smem = p->fp_L * 32 * 4 + (kThreads / 32) * (p->fp_T + kFpBatch) * 16;
     } else {
         double nc_glob = std::min((double)p->P, 4.0 * (p->nx + p->ny) * (2.0 / std::max(h, 1e-12) + 2));
         if (p->min_delay < 8.0 * p->fp_T * std::max(h, 1.0)) nc_glob = (double)p->P;
@@ -456,6 +498,8 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     A(alloc(p, &p->part_bp, (size_t)4 * std::max(p->bp_tiles_x * p->bp_tiles_y,
                                                  (p->P + kThreads - 1) / kThreads)));
     A(alloc(p, &p->part_tv, (size_t)p->fp_tiles_x * p->fp_tiles_y));
+    if (p->bp_split > 1) A(alloc(p, &p->bp_gpart, (size_t)p->bp_split * p->P));
+    A(alloc(p, &p->bp_tile_cnt, (size_t)p->bp_tiles_x * p->bp_tiles_y));
     A(alloc(p, &p->part_r, (size_t)p->M));
     A(alloc(p, &p->part_misc, (size_t)4 * p->misc_blocks));
     A(alloc(p, &p->state, 1));
@@ -472,19 +516,13 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     up(p->sx, dsx.data(), p->M * 8); up(p->sy, dsy.data(), p->M * 8);
     if (e == cudaSuccess) e = cudaMemset(p->acc, 0, (size_t)p->M * p->Q * 8);
     if (e == cudaSuccess) e = cudaMemset(p->state, 0, sizeof(DevState));
+    if (e == cudaSuccess)
+        e = cudaMemset(p->bp_tile_cnt, 0, sizeof(uint32_t) * p->bp_tiles_x * p->bp_tiles_y);
     if (e == cudaSuccess) e = cudaMemset(p->table, 0, (size_t)p->M * p->TS * 2 * ts);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);
-    if (e == cudaSuccess && p->dtype == PK_F32) {
-        e = cudaFuncSetAttribute(bp_f32_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->bp_smem);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(bp_f32_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->bp_smem);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(bp_f32_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->bp_smem);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(bp_f32_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->bp_smem);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(fp_f32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->fp_smem);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(finalize_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->Q * 4);
-    } else if (e == cudaSuccess) {
-        e = cudaFuncSetAttribute(fp_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->fp_smem);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(finalize_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->Q * 8);
-    }
+    // opt every dynamic-smem kernel into the device maximum once per device (a per-plan
+    // value would shrink the limit under plans created earlier with larger windows)
+    if (e == cudaSuccess) e = opt_in_smem(p->device);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         free_plan(p);

@@ -43,12 +43,17 @@ struct BpArgs {
     float* xb1;
     const DevParams* prm;
     DevState* st;
-    double* part;         // [blocks * 4]
+    double* part;         // [tiles * 4]
     int bits;             // projector fixed-point bits (scale = 2^bits / max|x'|)
+    // sensor split: CTA (tile, s) sums sensors [s*ms, min(M, (s+1)*ms)); the last CTA of a
+    // tile to finish adds the S partials in split order (deterministic) and runs the epilogue
+    int split, ms;
+    float* gpart;         // [split][P]
+    uint32_t* tile_cnt;   // [tiles]
 };
 
-template <bool EPI, bool CLAMP>
-__global__ void __launch_bounds__(kThreads, 2) bp_f32_kernel(BpArgs a) {
+template <bool EPI, bool CLAMP, bool ATRICK>
+__global__ void __launch_bounds__(kThreads, 3) bp_f32_kernel(BpArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ float red_f[kThreads / 32];
     __shared__ int last_flag;
@@ -58,11 +63,14 @@ __global__ void __launch_bounds__(kThreads, 2) bp_f32_kernel(BpArgs a) {
         if (a.st->stopped) return;
         iter = a.st->iter;
     }
-    const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
+    const int tile = blockIdx.x;
+    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     const int i0 = tx * kBpTile, j0 = ty * kBpTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int lx = lane & 7, ly = lane >> 3;
     const int j = j0 + warp * 4 + ly;
+    const int mbase = blockIdx.y * a.ms;
+    const int mcount = min(a.ms, a.M - mbase);
 
     float px[4], acc[4];
 #pragma unroll
@@ -84,17 +92,21 @@ __global__ void __launch_bounds__(kThreads, 2) bp_f32_kernel(BpArgs a) {
     const float X0 = __ldg(a.pxs + i0), X1 = __ldg(a.pxs + min(i0 + kBpTile - 1, a.nx - 1));
     const float Y0 = __ldg(a.pys + j0), Y1 = __ldg(a.pys + min(j0 + kBpTile - 1, a.ny - 1));
 
+    __shared__ uint32_t done_cnt[8];  // per-buffer count of warps finished with it
     if (threadIdx.x == 0) {
-        for (int b = 0; b < a.nbuf; ++b) mbar_init(bar_s + 8 * b, 1);
+        for (int b = 0; b < a.nbuf; ++b) {
+            mbar_init(bar_s + 8 * b, 1);
+            done_cnt[b] = 0;
+        }
         fence_barrier_init();
     }
     __syncthreads();
 
-    const int nchunks = (a.M + a.CS - 1) / a.CS;
-    // warp 0 computes the windows of a chunk and launches its bulk copies
+    const int nchunks = (mcount + a.CS - 1) / a.CS;
+    // the calling warp computes the windows of a chunk and launches its bulk copies
     auto issue = [&](int c, int b) {
-        const int m = c * a.CS + lane;
-        const int n = min(a.CS, a.M - c * a.CS);
+        const int m = mbase + c * a.CS + lane;
+        const int n = min(a.CS, mcount - c * a.CS);
         if (lane < n) {
             const float sx = __ldg(a.sxs + m), sy = __ldg(a.sys + m);
             const float cx = fminf(fmaxf(sx, X0), X1), cy = fminf(fmaxf(sy, Y0), Y1);
@@ -120,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, 2) bp_f32_kernel(BpArgs a) {
     for (int c = 0; c < nchunks; ++c) {
         const int b = c % a.nbuf;
         mbar_wait(bar_s + 8 * b, (uint32_t)((c / a.nbuf) & 1));
-        const int n = min(a.CS, a.M - c * a.CS);
+        const int n = min(a.CS, mcount - c * a.CS);
         const float4* sc = sconst + b * a.CS;
 #pragma unroll 2
         for (int s = 0; s < n; ++s) {
@@ -134,13 +146,51 @@ __global__ void __launch_bounds__(kThreads, 2) bp_f32_kernel(BpArgs a) {
                 float u = sqrt_approx(fmaf(ex, ex, ey2));
                 if (CLAMP) u = fminf(u, a.qclamp);
                 const float tb = __fadd_rd(u, kTwo23);      // 2^23 + floor(u)
-                const float f = u - (tb - kTwo23);          // exact fraction
                 const float2 v = lds_f2(adj + (__float_as_uint(tb) << 3));
-                acc[k] += fmaf(f, v.y, v.x);
+                if (ATRICK) {
+                    // table {r[s-1] - s*D, D}:  value = (1-f) r[s0-1] + f r[s0] = fma(u, D, A)
+                    acc[k] += fmaf(u, v.y, v.x);
+                } else {
+                    const float f = u - (tb - kTwo23);      // exact fraction
+                    acc[k] += fmaf(f, v.y, v.x);
+                }
             }
         }
-        __syncthreads();  // everyone is done with buffer b
-        if (warp == 0 && c + a.nbuf < nchunks) issue(c + a.nbuf, b);
+        // no CTA barrier: the last warp to finish with buffer b refills it (acq_rel counter)
+        __syncwarp();
+        uint32_t prev = 0;
+        if (lane == 0) {
+            const uint32_t addr = smem_u32(&done_cnt[b]);
+            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(prev) : "r"(addr) : "memory");
+        }
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == kThreads / 32 - 1) {
+            if (lane == 0) done_cnt[b] = 0;
+            if (c + a.nbuf < nchunks) issue(c + a.nbuf, b);
+        }
+    }
+
+    if (a.split > 1) {
+        // publish this split's partial sums; the tile's last CTA combines them in order
+        if (j < a.ny) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = i0 + lx + 8 * k;
+                if (i < a.nx) a.gpart[(size_t)blockIdx.y * a.nx * a.ny + (size_t)j * a.nx + i] = acc[k];
+            }
+        }
+        if (!last_block(a.tile_cnt + tile, a.split, &last_flag)) return;
+        if (j < a.ny) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = i0 + lx + 8 * k;
+                float sum = 0.f;
+                if (i < a.nx)
+                    for (int q = 0; q < a.split; ++q)
+                        sum += __ldcg(a.gpart + (size_t)q * a.nx * a.ny + (size_t)j * a.nx + i);
+                acc[k] = sum;
+            }
+        }
     }
 
     if (!EPI) {
@@ -196,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 2) bp_f32_kernel(BpArgs a) {
     const float l1b = block_sum(l1, red_f);
     const int badb = __syncthreads_or(bad);
     if (threadIdx.x == 0) {
-        double* pp = a.part + 4 * (size_t)blockIdx.x;
+        double* pp = a.part + 4 * (size_t)tile;
         pp[0] = mx;
         pp[1] = l1b;
         pp[2] = badb;
@@ -338,8 +388,11 @@ __global__ void __launch_bounds__(kThreads) bp_f64_kernel(BpArgs64 a) {
 // ([slot][32 lanes]) so lane l always hits bank l: conflict-free by construction.
 // Contributions are integers:  xq = rint(x*scale),  a = rint(x*scale*f),  b = xq - a,
 // added at trace index s0 (weight f) and s0-1 (weight 1-f) -- forward.py:189-194.
-// Zero pixels (soft-threshold zeros) are skipped, warp-uniformly.
-// Each window is flushed into the int64 trace accumulator with coalescing-free RED.64.
+// Warps own whole image rows: a warp compacts its row's non-zero pixels (soft-threshold
+// zeros are skipped warp-uniformly) into a private record buffer, pads it to a multiple of
+// 8 with zero-weight records, and scatters 8 pixels per batch (8 independent chains: all
+// arithmetic first, then the 16 atomics).  Windows are flushed into the int64 trace
+// accumulator with RED.64 (integer adds commute: bitwise deterministic).
 // ===========================================================================
 struct FpArgs {
     const float* x;       // [P] (nullptr: solver mode, use xb[(iter+1)&1])
@@ -356,6 +409,8 @@ struct FpArgs {
     double* part_tv;      // solver mode: per-tile TV(x) partials (group 0 only)
     int solver;
 };
+
+constexpr int kFpBatch = 8;
 
 template <bool CLAMP>
 __global__ void __launch_bounds__(kThreads) fp_f32_kernel(FpArgs a) {
@@ -376,43 +431,12 @@ __global__ void __launch_bounds__(kThreads) fp_f32_kernel(FpArgs a) {
     const bool sensor_ok = m < a.M;
     const float sx = __ldg(a.sxs + min(m, a.M - 1)), sy = __ldg(a.sys + min(m, a.M - 1));
 
-    // shared layout: win int32 [L][32] | rec float4 [T*T] | rowcnt int [T]
+    // shared layout: win int32 [L][32] | per-warp row records float4 [8][T + kFpBatch]
     int32_t* win = reinterpret_cast<int32_t*>(smem);
-    float4* rec = reinterpret_cast<float4*>(smem + (size_t)a.L * 32 * 4);
-    int* rowcnt = reinterpret_cast<int*>(smem + (size_t)a.L * 32 * 4 + (size_t)T * T * 16);
+    float4* rows = reinterpret_cast<float4*>(smem + (size_t)a.L * 32 * 4);
+    float4* rec = rows + (size_t)warp * (T + kFpBatch);
 
     for (int q = threadIdx.x; q < a.L * 32; q += kThreads) win[q] = 0;
-
-    // compact the tile's non-zero pixels per row: {px, x*scale, bits(rint(x*scale)+magic)}
-    float tv = 0.f;
-    const bool do_tv = a.solver && blockIdx.y == 0;
-    for (int r = warp; r < T; r += kThreads / 32) {
-        const int jj = j0 + r;
-        int base = 0;
-        for (int cc = 0; cc < T; cc += 32) {
-            const int ii = i0 + cc + lane;
-            const bool in = ii < a.nx && jj < a.ny;
-            const float xv = in ? x[(size_t)jj * a.nx + ii] : 0.f;
-            if (do_tv && in) {  // exact anisotropic TV partial, recon.py:169-170
-                if (ii + 1 < a.nx) tv += fabsf(x[(size_t)jj * a.nx + ii + 1] - xv);
-                if (jj + 1 < a.ny) tv += fabsf(x[(size_t)(jj + 1) * a.nx + ii] - xv);
-            }
-            const bool nz = xv != 0.f;
-            const uint32_t bal = __ballot_sync(0xffffffffu, nz);
-            if (nz) {
-                const int pos = base + __popc(bal & ((1u << lane) - 1u));
-                const float xs = xv * scale;
-                rec[r * T + pos] =
-                    make_float4(__ldg(a.pxs + ii), xs, __int_as_float(__float_as_int(xs + kMagic)), 0.f);
-            }
-            base += __popc(bal);
-        }
-        if (lane == 0) rowcnt[r] = base;
-    }
-    if (do_tv) {
-        const float tvb = block_sum(tv, red_f);
-        if (threadIdx.x == 0) a.part_tv[blockIdx.x] = tvb;
-    }
 
     // this lane's window: trace indices [lo, lo + L)
     const float X0 = __ldg(a.pxs + i0), X1 = __ldg(a.pxs + min(i0 + T - 1, a.nx - 1));
@@ -421,34 +445,71 @@ __global__ void __launch_bounds__(kThreads) fp_f32_kernel(FpArgs a) {
     float dmin = sqrtf((cx - sx) * (cx - sx) + (cy - sy) * (cy - sy));
     if (CLAMP) dmin = fminf(dmin, a.qclamp);
     const int lo = (int)floorf(dmin) - 2;
-    // word address of trace index t: win + 4*(32*(t - lo) + lane);  t = s0 -> tb bits
+    // word address of trace index t: win + 4*(32*(t - lo) + lane);  t = s0 <-> bits(tb)
     const uint32_t adj = smem_u32(win) + 4u * (uint32_t)lane - 128u * (uint32_t)lo -
                          128u * kTwo23Bits;
     __syncthreads();
 
-    if (sensor_ok) {
-        for (int r = warp; r < T; r += kThreads / 32) {
-            const int cnt = rowcnt[r];
-            if (cnt == 0) continue;
-            const float ey = __ldg(a.pys + min(j0 + r, a.ny - 1)) - sy;
+    float tv = 0.f;
+    const bool do_tv = a.solver && blockIdx.y == 0;
+    const int jend = min(T, a.ny - j0);
+    for (int r = warp; r < jend; r += kThreads / 32) {
+        const int jj = j0 + r;
+        // compact the row's non-zero pixels: {px, x*scale, bits(rint(x*scale) + magic)}
+        int cnt = 0;
+        for (int cc = 0; cc < T; cc += 32) {
+            const int ii = i0 + cc + lane;
+            const bool in = ii < a.nx;
+            const float xv = in ? x[(size_t)jj * a.nx + ii] : 0.f;
+            if (do_tv && in) {  // exact anisotropic TV partial, recon.py:169-170
+                if (ii + 1 < a.nx) tv += fabsf(x[(size_t)jj * a.nx + ii + 1] - xv);
+                if (jj + 1 < a.ny) tv += fabsf(x[(size_t)(jj + 1) * a.nx + ii] - xv);
+            }
+            const bool nz = xv != 0.f;
+            const uint32_t bal = __ballot_sync(0xffffffffu, nz);
+            if (nz) {
+                const float xs = xv * scale;
+                rec[cnt + __popc(bal & ((1u << lane) - 1u))] =
+                    make_float4(__ldg(a.pxs + ii), xs, __int_as_float(__float_as_int(xs + kMagic)), 0.f);
+            }
+            cnt += __popc(bal);
+        }
+        if (cnt == 0) continue;  // warp-uniform
+        const int cnt8 = (cnt + kFpBatch - 1) & ~(kFpBatch - 1);
+        if (lane < cnt8 - cnt)  // zero-weight padding (adds 0 at a valid window address)
+            rec[cnt + lane] = make_float4(X0, 0.f, __int_as_float(kMagicBits), 0.f);
+        __syncwarp();
+        if (sensor_ok) {
+            const float ey = __ldg(a.pys + jj) - sy;
             const float ey2 = ey * ey;
-            const float4* rr = rec + r * T;
-#pragma unroll 4
-            for (int k = 0; k < cnt; ++k) {
-                const float4 q = rr[k];
-                const float ex = q.x - sx;
-                float u = sqrt_approx(fmaf(ex, ex, ey2));
-                if (CLAMP) u = fminf(u, a.qclamp);
-                const float tb = __fadd_rd(u, kTwo23);
-                const float f = u - (tb - kTwo23);
-                const float fb = fmaf(q.y, f, kMagic);
-                const int32_t ia = __float_as_int(fb) - kMagicBits;       // weight f   -> s0
-                const int32_t ib = __float_as_int(q.z) - __float_as_int(fb); // weight 1-f -> s0-1
-                const uint32_t addr = adj + (__float_as_uint(tb) << 7);
-                red_smem_s32(addr - 128u, ib);
-                red_smem_s32(addr, ia);
+            for (int k = 0; k < cnt8; k += kFpBatch) {
+                uint32_t ad[kFpBatch];
+                int32_t va[kFpBatch], vb[kFpBatch];
+#pragma unroll
+                for (int b = 0; b < kFpBatch; ++b) {
+                    const float4 q = rec[k + b];
+                    const float ex = q.x - sx;
+                    float u = sqrt_approx(fmaf(ex, ex, ey2));
+                    if (CLAMP) u = fminf(u, a.qclamp);
+                    const float tb = __fadd_rd(u, kTwo23);
+                    const float f = u - (tb - kTwo23);
+                    const float fb = fmaf(q.y, f, kMagic);
+                    va[b] = __float_as_int(fb) - kMagicBits;        // weight f   -> s0
+                    vb[b] = __float_as_int(q.z) - __float_as_int(fb); // weight 1-f -> s0-1
+                    ad[b] = adj + (__float_as_uint(tb) << 7);
+                }
+#pragma unroll
+                for (int b = 0; b < kFpBatch; ++b) {
+                    red_smem_s32(ad[b] - 128u, vb[b]);
+                    red_smem_s32(ad[b], va[b]);
+                }
             }
         }
+        __syncwarp();  // rec is rewritten by the next row
+    }
+    if (do_tv) {
+        const float tvb = block_sum(tv, red_f);
+        if (threadIdx.x == 0) a.part_tv[blockIdx.x] = tvb;
     }
     __syncthreads();
 
@@ -575,6 +636,20 @@ __global__ void __launch_bounds__(kThreads) fp_f64_kernel(FpArgs64 a) {
     }
 }
 
+// Pair-table entry s from r[s-1] (rp) and r[s] (rc).  Plain layout {r[s-1], D}; the fp32
+// back-projector's "A-trick" layout {r[s-1] - s*D, D} lets it use the delay u directly
+// (value = fma(u, D, A)) instead of the fraction f = u - s0, saving two FADDs per pair.
+// A is formed in fp64 and rounded once.
+template <typename T>
+__device__ __forceinline__ typename std::conditional<sizeof(T) == 4, float2, double2>::type
+pair_entry(T rp, T rc, int s, int atrick) {
+    typename std::conditional<sizeof(T) == 4, float2, double2>::type v;
+    const T d = rc - rp;
+    v.y = d;
+    v.x = atrick ? (T)((double)rp - (double)s * (double)d) : rp;
+    return v;
+}
+
 // ===========================================================================
 // K3 -- residual / finalize: one CTA per sensor.  r = w*acc/scale - y, acc := 0, pair table,
 // sum r^2; solver mode: last CTA evaluates the objective and the stopping rules.
@@ -596,6 +671,7 @@ struct FinArgs {
     int ntv;
     double* sumsq_out;   // optional (pk_residual)
     int solver;
+    int atrick;          // fp32 table layout {r[s-1] - s*D, D} (see pair_entry)
 };
 
 template <typename T>
@@ -627,10 +703,7 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
     for (int e = threadIdx.x; e < a.TS; e += kThreads) {
         const T rp = (e >= 1 && e - 1 < a.Q) ? tr[e - 1] : (T)0;
         const T rc = (e < a.Q) ? tr[e] : (T)0;
-        T2 v;
-        v.x = rp;
-        v.y = rc - rp;
-        a.table[(size_t)m * a.TS + e] = v;
+        a.table[(size_t)m * a.TS + e] = pair_entry<T>(rp, rc, e, a.atrick);
     }
     ss = block_sum(ss, red_d);
     if (threadIdx.x == 0) a.part_r[m] = ss;
@@ -689,7 +762,7 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
 template <typename T>
 __global__ void __launch_bounds__(kThreads) table_kernel(
     const T* y_direct, const DevIo* io, typename std::conditional<sizeof(T) == 4, float2, double2>::type* table,
-    int M, int Q, int TS, T sign, double* part, DevState* st, int init) {
+    int M, int Q, int TS, T sign, double* part, DevState* st, int init, int atrick) {
     using T2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
     __shared__ double red_d[kThreads / 32];
     __shared__ int last_flag;
@@ -700,10 +773,7 @@ __global__ void __launch_bounds__(kThreads) table_kernel(
     for (int e = threadIdx.x; e < TS; e += kThreads) {
         const T rp = (e >= 1 && e - 1 < Q) ? sign * ym[e - 1] : (T)0;
         const T rc = (e < Q) ? sign * ym[e] : (T)0;
-        T2 v;
-        v.x = rp;
-        v.y = rc - rp;
-        table[(size_t)m * TS + e] = v;
+        table[(size_t)m * TS + e] = pair_entry<T>(rp, rc, e, atrick);
         if (e < Q) ss += (double)rc * (double)rc;
     }
     if (!init) return;

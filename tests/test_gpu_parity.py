@@ -63,7 +63,7 @@ def test_products_vs_golden(sc, pool):
     g, ring, ac, ph, K = scene(*sc)
     gold = golden(*sc)
     y = pk.forward_project(K, ph, pool=pool)
-    tol = 1e-6 if pool.dtype == "float32" else 1e-13
+    tol = 1e-5 if pool.dtype == "float32" else 1e-13
     assert rel(y.values, gold["y"]) <= tol
     op = pk.operator_for(g, ring, ac, pool)
     kt = op.adjoint(gold["r"]).double().cpu().numpy()
@@ -80,7 +80,7 @@ def test_products_vs_oracle_large(oracle, cfg, pool):
     rng = np.random.default_rng(5)
     x = ph.values + 0.1 * rng.standard_normal(g.size)
     op = pk.operator_for(g, ring, ac, pool)
-    tol = 2e-6 if pool.dtype == "float32" else 1e-12
+    tol = 5e-6 if pool.dtype == "float32" else 1e-12
     y_dev = op.matvec(x).double().cpu().numpy()
     assert rel(y_dev, o.forward(x)) <= tol
     r = rng.standard_normal(M * Q)

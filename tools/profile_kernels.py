@@ -1,0 +1,41 @@
+"""Launch the solver kernels of one configuration un-graphed (for ncu).
+
+    python tools/profile_kernels.py [--config cfg3] [--iterations 2] [--dtype float32]
+
+Runs pk_profile_iterations once (init, table, then iterations x (K1, K2, K3)) after a
+warm-up, so `ncu -k regex:bp_f32|fp_f32 -s <skip> -c <n>` can select single launches.
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2404_10928_b200 as pk  # noqa: E402
+from paper_2404_10928_b200 import _native as N  # noqa: E402
+from paper_2404_10928_b200.workloads import CONFIGS  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg3")
+ap.add_argument("--iterations", type=int, default=2)
+ap.add_argument("--dtype", default="float32")
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+cfg = CONFIGS[a.config]
+grid, ring, ac, ph = pk.make_scene(cfg.n, cfg.sensors, cfg.samples, seed=0)
+op = pk.operator_for(grid, ring, ac, pk.CudaPool(0, a.dtype))
+y = op.matvec(ph.values)
+params = N.SolverParams(alpha=8.8e-8, beta=8.8e-10, step=333.0, tv_epsilon=1e-3, tolerance=0.0,
+                        iterations=a.iterations, nonneg=0)
+lib = N.load()
+ms = (ctypes.c_float * 3)()
+n = ctypes.c_int32()
+s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+for _ in range(a.reps):
+    N.check(lib.pk_profile_iterations(op.handle, ctypes.byref(params), y.data_ptr(), ms, ctypes.byref(n), s))
+torch.cuda.synchronize()
+print("per-kernel ms over", a.iterations, "iterations:", list(ms), "launches", n.value)
