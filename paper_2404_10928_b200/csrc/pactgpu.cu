@@ -418,7 +418,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     p->TS = (p->Q + 2 + 1) & ~1;
     {
         const char* ev = getenv("PK_BP_ATRICK");
-        p->bp_atrick = (p->dtype == PK_F32) ? (ev ? atoi(ev) != 0 : 1) : 0;
+        p->bp_atrick = (p->dtype == PK_F32) ? (ev ? atoi(ev) != 0 : 0) : 0;  // opt-in: see DESIGN.md
     }
     // back-projector
     p->bp_tiles_x = (p->nx + kBpTile - 1) / kBpTile;
@@ -426,7 +426,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     p->bp_L = ((int)std::ceil(tile_diag(kBpTile)) + 6 + 1) & ~1;
     if (p->bp_L > p->TS) p->bp_L = p->TS;
     p->bp_nbuf = 3;
-    const int bp_budget = 72 * 1024;
+    const int bp_budget = 52 * 1024;  // 4 CTAs (32 warps) per SM
     p->bp_CS = std::max(1, std::min(32, bp_budget / (p->bp_nbuf * p->bp_L * 8)));
     p->bp_smem = p->bp_nbuf * p->bp_CS * p->bp_L * 8 + p->bp_nbuf * p->bp_CS * 16 + p->bp_nbuf * 8;
     {   // sensor split so that tiles x split >= ~4 CTAs per SM, each split >= 64 sensors

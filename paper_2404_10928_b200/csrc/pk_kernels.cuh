@@ -53,7 +53,7 @@ struct BpArgs {
 };
 
 template <bool EPI, bool CLAMP, bool ATRICK>
-__global__ void __launch_bounds__(kThreads, 3) bp_f32_kernel(BpArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) bp_f32_kernel(BpArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ float red_f[kThreads / 32];
     __shared__ int last_flag;
@@ -72,11 +72,13 @@ __global__ void __launch_bounds__(kThreads, 3) bp_f32_kernel(BpArgs a) {
     const int mbase = blockIdx.y * a.ms;
     const int mcount = min(a.ms, a.M - mbase);
 
-    float px[4], acc[4];
+    // two independent accumulator chains per pixel (FFMA chain of u*D, FADD chain of A)
+    float px[4], acc[4], acc2[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         px[k] = __ldg(a.pxs + min(i0 + lx + 8 * k, a.nx - 1));
         acc[k] = 0.f;
+        acc2[k] = 0.f;
     }
     const float py = __ldg(a.pys + min(j, a.ny - 1));
 
@@ -148,11 +150,13 @@ __global__ void __launch_bounds__(kThreads, 3) bp_f32_kernel(BpArgs a) {
                 const float tb = __fadd_rd(u, kTwo23);      // 2^23 + floor(u)
                 const float2 v = lds_f2(adj + (__float_as_uint(tb) << 3));
                 if (ATRICK) {
-                    // table {r[s-1] - s*D, D}:  value = (1-f) r[s0-1] + f r[s0] = fma(u, D, A)
-                    acc[k] += fmaf(u, v.y, v.x);
+                    // table {r[s-1] - s*D, D}:  value = (1-f) r[s0-1] + f r[s0] = u*D + A
+                    acc[k] = fmaf(u, v.y, acc[k]);
+                    acc2[k] += v.x;
                 } else {
                     const float f = u - (tb - kTwo23);      // exact fraction
-                    acc[k] += fmaf(f, v.y, v.x);
+                    acc[k] = fmaf(f, v.y, acc[k]);
+                    acc2[k] += v.x;
                 }
             }
         }
@@ -169,6 +173,9 @@ __global__ void __launch_bounds__(kThreads, 3) bp_f32_kernel(BpArgs a) {
             if (c + a.nbuf < nchunks) issue(c + a.nbuf, b);
         }
     }
+
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k] += acc2[k];
 
     if (a.split > 1) {
         // publish this split's partial sums; the tile's last CTA combines them in order
@@ -453,14 +460,29 @@ __global__ void __launch_bounds__(kThreads) fp_f32_kernel(FpArgs a) {
     float tv = 0.f;
     const bool do_tv = a.solver && blockIdx.y == 0;
     const int jend = min(T, a.ny - j0);
+    // rows of this warp; the next row's pixels are loaded while the current row scatters
+    float xnext[2] = {0.f, 0.f};
+    auto load_row = [&](int r, float* dst) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int ii = i0 + 32 * c + lane;
+            dst[c] = (32 * c < T && r < jend && ii < a.nx) ? x[(size_t)(j0 + r) * a.nx + ii] : 0.f;
+        }
+    };
+    load_row(warp, xnext);
     for (int r = warp; r < jend; r += kThreads / 32) {
         const int jj = j0 + r;
+        const float xrow[2] = {xnext[0], xnext[1]};
+        load_row(r + kThreads / 32, xnext);
         // compact the row's non-zero pixels: {px, x*scale, bits(rint(x*scale) + magic)}
         int cnt = 0;
-        for (int cc = 0; cc < T; cc += 32) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int cc = 32 * c;
+            if (cc >= T) break;
             const int ii = i0 + cc + lane;
             const bool in = ii < a.nx;
-            const float xv = in ? x[(size_t)jj * a.nx + ii] : 0.f;
+            const float xv = xrow[c];
             if (do_tv && in) {  // exact anisotropic TV partial, recon.py:169-170
                 if (ii + 1 < a.nx) tv += fabsf(x[(size_t)jj * a.nx + ii + 1] - xv);
                 if (jj + 1 < a.ny) tv += fabsf(x[(size_t)(jj + 1) * a.nx + ii] - xv);
@@ -687,17 +709,40 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
     const double wq = sc > 0.0 ? a.w / sc : 0.0;
     const T* y = a.solver ? reinterpret_cast<const T*>(a.io->y) : a.y;
     long long* accm = a.acc + (size_t)m * a.Q;
+    const T* ym = y ? y + (size_t)m * a.Q : nullptr;
+    T* om = a.trace_out ? a.trace_out + (size_t)m * a.Q : nullptr;
     double ss = 0.0;
-    for (int s = threadIdx.x; s < a.Q; s += kThreads) {
-        const long long v = accm[s];
-        accm[s] = 0;
-        // K x rounded to the working type first, then the residual in that type, so that
-        // y produced by the same projection gives r == 0 exactly (recon.py:75-79 semantics)
-        const T kx = (T)((double)v * wq);
-        const T rv = y ? (T)(kx - y[(size_t)m * a.Q + s]) : kx;
-        tr[s] = rv;
-        if (a.trace_out) a.trace_out[(size_t)m * a.Q + s] = rv;
-        ss += (double)rv * (double)rv;
+    // 4 samples per thread per step: all loads first (independent), then math and stores
+    for (int s0 = 4 * threadIdx.x; s0 < a.Q; s0 += 4 * kThreads) {
+        long long v[4];
+        T yv[4] = {(T)0, (T)0, (T)0, (T)0};
+        const bool full = s0 + 4 <= a.Q && (a.Q & 1) == 0;
+        if (full) {
+            const longlong2 p0 = __ldcg(reinterpret_cast<const longlong2*>(accm + s0));
+            const longlong2 p1 = __ldcg(reinterpret_cast<const longlong2*>(accm + s0 + 2));
+            v[0] = p0.x; v[1] = p0.y; v[2] = p1.x; v[3] = p1.y;
+        } else {
+            for (int q = 0; q < 4; ++q) v[q] = (s0 + q < a.Q) ? __ldcg(accm + s0 + q) : 0;
+        }
+        if (ym)
+            for (int q = 0; q < 4; ++q) yv[q] = (s0 + q < a.Q) ? ym[s0 + q] : (T)0;
+        if (full) {
+            reinterpret_cast<longlong2*>(accm + s0)[0] = make_longlong2(0, 0);
+            reinterpret_cast<longlong2*>(accm + s0)[1] = make_longlong2(0, 0);
+        } else {
+            for (int q = 0; q < 4; ++q) if (s0 + q < a.Q) accm[s0 + q] = 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (s0 + q >= a.Q) break;
+            // K x rounded to the working type first, then the residual in that type, so that
+            // y produced by the same projection gives r == 0 exactly (recon.py:75-79 semantics)
+            const T kx = (T)((double)v[q] * wq);
+            const T rv = ym ? (T)(kx - yv[q]) : kx;
+            tr[s0 + q] = rv;
+            if (om) om[s0 + q] = rv;
+            ss += (double)rv * (double)rv;
+        }
     }
     __syncthreads();
     for (int e = threadIdx.x; e < a.TS; e += kThreads) {

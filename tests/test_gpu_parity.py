@@ -63,7 +63,7 @@ def test_products_vs_golden(sc, pool):
     g, ring, ac, ph, K = scene(*sc)
     gold = golden(*sc)
     y = pk.forward_project(K, ph, pool=pool)
-    tol = 1e-5 if pool.dtype == "float32" else 1e-13
+    tol = 1e-4 if pool.dtype == "float32" else 1e-13  # random r: see test_products_vs_oracle_large
     assert rel(y.values, gold["y"]) <= tol
     op = pk.operator_for(g, ring, ac, pool)
     kt = op.adjoint(gold["r"]).double().cpu().numpy()
@@ -80,7 +80,9 @@ def test_products_vs_oracle_large(oracle, cfg, pool):
     rng = np.random.default_rng(5)
     x = ph.values + 0.1 * rng.standard_normal(g.size)
     op = pk.operator_for(g, ring, ac, pool)
-    tol = 5e-6 if pool.dtype == "float32" else 1e-12
+    # fp32: the delay u ~ 1e3 samples carries ~1 ulp (1e-4 samples) of rounding, which for
+    # noise-like inputs shows up directly as ~5e-5 relative product error (images: SURVEY 6e-6..2e-5)
+    tol = 2e-4 if pool.dtype == "float32" else 1e-12
     y_dev = op.matvec(x).double().cpu().numpy()
     assert rel(y_dev, o.forward(x)) <= tol
     r = rng.standard_normal(M * Q)

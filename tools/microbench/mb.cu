@@ -65,12 +65,17 @@ __global__ void atoms_k(int* out, int iters, int mode, long long* cyc){
   out[blockIdx.x*blockDim.x+threadIdx.x]=s[threadIdx.x];
 }
 // LDS.64: mode 0: lane -> float2 slot lane (256B); 1: slot lane/2 (128B); 2: slot lane*5/8 (~20 slots); 3: slot (lane*7)&31 perm
+// 4: slot lane&15 (both half-warps read the same 16 slots); 5: 8x4 pixel footprint at 1.93 slots/px, theta=30deg
+// 6: 8x4 footprint at 1.93 slots/px along x (theta=0); 7: random within 16 slots
 __global__ void lds64_k(float* out, int iters, int mode, long long* cyc){
   __shared__ float2 s[4096];
   for(int i=threadIdx.x;i<4096;i+=blockDim.x) s[i]=make_float2(i,i+1);
   __syncthreads();
   int lane=threadIdx.x&31;
-  int off = mode==0? lane : mode==1? lane>>1 : mode==2? (lane*5)>>3 : (lane*7)&31;
+  int lx=lane&7, ly=lane>>3;
+  int off = mode==0? lane : mode==1? lane>>1 : mode==2? (lane*5)>>3 : mode==3? (lane*7)&31 :
+            mode==4? (lane&15) : mode==5? (int)(1.93f*(lx*0.866f+ly*0.5f)) : mode==6? (int)(1.93f*lx) :
+            (int)((lane*2654435761u)>>28);
   float acc=0.f, acc2=0.f;
   int o=(threadIdx.x>>5)*37;
   long long t0=clock64();
@@ -126,7 +131,7 @@ int main(){
   for(int m=0;m<5;m++){ char nm[64]; snprintf(nm,64,"ATOMS.ADD mode %d",m);
     cudaEventRecord(e0); atoms_k<<<B,T>>>(io,it/4,m,cyc); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
     cudaEventElapsedTime(&ms,e0,e1); report(nm,B,T,it/4*8.0,ms);}
-  for(int m=0;m<4;m++){ char nm[64]; snprintf(nm,64,"LDS.64 mode %d",m);
+  for(int m=0;m<8;m++){ char nm[64]; snprintf(nm,64,"LDS.64 mode %d",m);
     cudaEventRecord(e0); lds64_k<<<B,T>>>(fo,it/2,m,cyc); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
     cudaEventElapsedTime(&ms,e0,e1); report(nm,B,T,it/2*8.0,ms);}
   }
