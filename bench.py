@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--shard", default="sensors", choices=["sensors", "frames"])
     ap.add_argument("--frames", type=int, default=40, help="distinct frames cycled (> L2)")
+    ap.add_argument("--batch", type=int, default=1, choices=[1, 2, 4],
+                    help="frames reconstructed per launch sharing one delay evaluation")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -241,16 +243,21 @@ def main():
             solver.solve(Yl[f], pinned, alpha, beta, step)
         launches_per_step = 1 + 3 * cfg.iterations + 3 * cfg.iterations  # residual(3)/bp/update(2)
     else:
-        op = pk.operator_for(grid, ring, ac, pk.CudaPool(local, "float32"))
-        x_out = torch.empty(P, device=dev, dtype=torch.float32)
-        hist = torch.zeros(4 * cfg.iterations, device=dev, dtype=torch.float64)
-        status = torch.zeros(2, device=dev, dtype=torch.int32)
+        B = args.batch
+        op = pk.operator_for(grid, ring, ac, pk.CudaPool(local, "float32"), frames=B)
+        x_out = torch.empty(B * P, device=dev, dtype=torch.float32)
+        hist = torch.zeros(B * 4 * cfg.iterations, device=dev, dtype=torch.float64)
+        status = torch.zeros(2 * B, device=dev, dtype=torch.int32)
+        params_arr = (N.SolverParams * B)(*([params] * B))
+        # step inputs: B consecutive frames, contiguous [B][M*Q]
+        n_steps_in = max(1, F // B)
+        Ystep = [Y[B * t: B * t + B].reshape(-1) for t in range(n_steps_in)]
         stream_ptr = lambda: __import__("ctypes").c_void_p(torch.cuda.current_stream(dev).cuda_stream)
         lib = N.load()
         import ctypes
 
         def one_step(f):
-            N.check(lib.pk_reconstruct(op.handle, ctypes.byref(params), Y[f].data_ptr(),
+            N.check(lib.pk_reconstruct(op.handle, params_arr, Ystep[f % n_steps_in].data_ptr(),
                                        x_out.data_ptr(), hist.data_ptr(), status.data_ptr(),
                                        stream_ptr()))
         launches_per_step = 3 + 3 * cfg.iterations
@@ -288,7 +295,8 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t[0])
-    frames_total = args.steps * (1 if sensor_mode else world)
+    B = 1 if sensor_mode else args.batch
+    frames_total = args.steps * B * (1 if sensor_mode else world)
     fps = frames_total / (ms_max * 1e-3)
     ms_step = ms_max / args.steps
 
@@ -301,13 +309,13 @@ def main():
         reps = 5
         tot = np.zeros(3)
         for r_ in range(reps):
-            N.check(lib.pk_profile_iterations(op.handle, ctypes.byref(params), Y[frame(r_)].data_ptr(),
+            N.check(lib.pk_profile_iterations(op.handle, params_arr, Ystep[r_ % n_steps_in].data_ptr(),
                                               fl, ctypes.byref(nl), stream_ptr()))
             tot += np.array(fl[:])
         per_launch_ms = tot / (reps * prof_iters)
         peak = ctypes.c_double()
         N.check(lib.pk_measure_fp32_peak(local, ctypes.byref(peak)))
-        flops_per_launch = 12.0 * M * P  # 12 FP32 flops per sensor-pixel pair
+        flops_per_launch = 12.0 * M * P * B  # 12 FP32 flops per sensor-pixel pair, per frame
         names = ["K1 bp_update (back-projection + TV + prox)", "K2 projection (fixed-point scatter)",
                  "K3 residual/objective"]
         kernels = {}
@@ -336,18 +344,18 @@ def main():
     # ---- end to end through the C-ABI host-buffer entry ----
     e2e = None
     if not args.no_e2e and not sensor_mode:
-        nF = min(F, 4)
-        yh = torch.empty((nF, M * Q), dtype=torch.float64, pin_memory=True)
-        yh.copy_(Y[:nF].double().cpu())
+        nF = min(n_steps_in, 4)
+        yh = torch.empty((nF, B * M * Q), dtype=torch.float64, pin_memory=True)
+        yh.copy_(Y[:nF * B].reshape(nF, B * M * Q).double().cpu())
         yh_np = yh.numpy()
-        xo = torch.empty(P, dtype=torch.float64, pin_memory=True).numpy()
-        hh = torch.empty(4 * cfg.iterations, dtype=torch.float64, pin_memory=True).numpy()
-        sh = torch.empty(2, dtype=torch.int32, pin_memory=True).numpy()
+        xo = torch.empty(B * P, dtype=torch.float64, pin_memory=True).numpy()
+        hh = torch.empty(B * 4 * cfg.iterations, dtype=torch.float64, pin_memory=True).numpy()
+        sh = torch.empty(2 * B, dtype=torch.int32, pin_memory=True).numpy()
         dp = ctypes.POINTER(ctypes.c_double)
         ip = ctypes.POINTER(ctypes.c_int32)
 
         def host_step(f):
-            N.check(lib.pk_reconstruct_host(op.handle, ctypes.byref(params),
+            N.check(lib.pk_reconstruct_host(op.handle, params_arr,
                                             yh_np[f].ctypes.data_as(dp), xo.ctypes.data_as(dp),
                                             hh.ctypes.data_as(dp), sh.ctypes.data_as(ip), stream_ptr()))
         for k in range(args.warmup):
@@ -360,9 +368,9 @@ def main():
         ee1.record()
         torch.cuda.synchronize(dev)
         ms_e2e = ee0.elapsed_time(ee1)
-        e2e = {"value": args.steps / (ms_e2e * 1e-3) * world, "unit": "frames/s",
-               "h2d_bytes_per_step": M * Q * 8,
-               "d2h_bytes_per_step": P * 8 + 4 * cfg.iterations * 8 + 8,
+        e2e = {"value": args.steps * B / (ms_e2e * 1e-3) * world, "unit": "frames/s",
+               "h2d_bytes_per_step": B * M * Q * 8,
+               "d2h_bytes_per_step": B * (P * 8 + 4 * cfg.iterations * 8 + 8),
                "ms_per_step": ms_e2e / args.steps,
                "path": "pk_reconstruct_host (C ABI, pinned fp64 host buffers)"}
 
@@ -379,13 +387,14 @@ def main():
         line = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "ms_per_iteration": ms_step / cfg.iterations,
+            "ms_per_iteration": ms_step / (cfg.iterations * B),  # per frame, amortised over the batch
+            "latency_ms_per_step": ms_step,
             "higher_is_better": True,
             "scaling": "strong" if sensor_mode else ("weak" if world > 1 else "none"),
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: make_scene vessel phantoms (seed = frame), y = K x by the fp64 device projector",
             "config": {"workload": cfg.name, "image": f"{cfg.n}x{cfg.n}", "sensors": M, "samples": Q,
-                       "iterations": cfg.iterations,
+                       "iterations": cfg.iterations, "batch": B,
                        "parallelism": (f"sensor-shard x{world} + NCCL all-reduce" if sensor_mode
                                        else f"frames x{world}" if world > 1 else "single GPU"),
                        "l2": f"{F} distinct frames cycled ({F * M * Q * 4 / 2**20:.0f} MiB of y > 126 MB L2)",

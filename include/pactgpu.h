@@ -63,6 +63,10 @@ typedef struct pk_geometry_desc {
     double c, dt;            /* AcousticConfig.c, .dt (forward.py:39-57) */
     int32_t dtype;           /* PK_F32 or PK_F64 */
     int32_t device;          /* CUDA device ordinal */
+    int32_t frames;          /* frames reconstructed together on this geometry: 0/1 = one,
+                                2 or 4 = batched (PK_F32 only).  Every image / trace buffer of
+                                the entry points below then holds `frames` consecutive frames
+                                (frame-major), and params points to `frames` structs. */
 } pk_geometry_desc;
 
 typedef struct pk_plan pk_plan;
@@ -77,6 +81,8 @@ typedef struct pk_plan_info {
     int32_t bp_tile, bp_window, bp_chunk, bp_buffers; /* back-projector tiling */
     int32_t fp_tile, fp_window, fp_bits;              /* projector tiling, fixed-point bits */
     int64_t device_bytes;    /* workspace held by the plan */
+    int32_t frames;          /* frames per call */
+    int32_t bp_split;        /* sensor slices per back-projector tile */
 } pk_plan_info;
 
 typedef struct pk_solver_params {
@@ -107,10 +113,12 @@ int pk_adjoint_matvec(pk_plan* plan, const void* y_dev, void* out_dev, double sc
  * device, for a plan that owns all sensors: x0 = 0, r = -y, per iteration the fused
  * back-projection + TV + soft-threshold (+ nonneg) update, the projection + residual,
  * the objective and the stopping rules (non-finite, 5-streak, tolerance).
- *   y_dev          [M*Q] measurements (plan dtype)
- *   x_out_dev      [P] final image (plan dtype)
- *   history_dev    [4*iterations] double: objective, data, l1, tv per accepted iteration
- *   status_dev     [2] int32: iterations_run, stopped_by (PK_STOP_*)
+ *   params         [frames] structs (per-frame alpha/beta/step; iterations, tv_epsilon,
+ *                  tolerance and nonneg are taken from params[0])
+ *   y_dev          [frames][M*Q] measurements (plan dtype)
+ *   x_out_dev      [frames][P] final images (plan dtype)
+ *   history_dev    [frames][4][iterations] double: objective, data, l1, tv per accepted iteration
+ *   status_dev     [frames][2] int32: iterations_run, stopped_by (PK_STOP_*)
  * Asynchronous on `stream`; captured into a CUDA graph on first use per iteration count. */
 int pk_reconstruct(pk_plan* plan, const pk_solver_params* params, const void* y_dev,
                    void* x_out_dev, double* history_dev, int32_t* status_dev, void* stream);

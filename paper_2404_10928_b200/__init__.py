@@ -41,6 +41,7 @@ from .solver import (
     iterative_reconstruct,
     objective,
     psnr,
+    reconstruct_frames,
     resolve_config,
     resolve_regularization,
     rmse,

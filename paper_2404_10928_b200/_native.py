@@ -58,6 +58,7 @@ class GeometryDesc(ctypes.Structure):
         ("dt", ctypes.c_double),
         ("dtype", ctypes.c_int32),
         ("device", ctypes.c_int32),
+        ("frames", ctypes.c_int32),
     ]
 
 
@@ -77,6 +78,8 @@ class PlanInfo(ctypes.Structure):
         ("fp_window", ctypes.c_int32),
         ("fp_bits", ctypes.c_int32),
         ("device_bytes", ctypes.c_int64),
+        ("frames", ctypes.c_int32),
+        ("bp_split", ctypes.c_int32),
     ]
 
 

@@ -19,6 +19,23 @@
 
 using namespace pk;
 
+namespace pk {
+// FP32 peak microkernel: 8 independent FFMA chains per thread
+__global__ void __launch_bounds__(kThreads) ffma_peak_kernel(float* out, int iters) {
+    float a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+          a6 = a0 + 6, a7 = a0 + 7;
+    const float b = 1.0001f + 1e-9f * blockIdx.x, c = 0.9999f;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            a0 = fmaf(a0, b, c); a1 = fmaf(a1, b, c); a2 = fmaf(a2, b, c); a3 = fmaf(a3, b, c);
+            a4 = fmaf(a4, b, c); a5 = fmaf(a5, b, c); a6 = fmaf(a6, b, c); a7 = fmaf(a7, b, c);
+        }
+    }
+    out[blockIdx.x * kThreads + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+}  // namespace pk
+
 namespace {
 
 thread_local char g_err[512] = "";
@@ -45,6 +62,12 @@ int fail(int code, const char* fmt, ...) {
         if (e_ != cudaSuccess)                                                            \
             return fail(PK_ERR_CUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
                         __FILE__, __LINE__);                                              \
+    } while (0)
+
+#define PK_TRY(x)                     \
+    do {                              \
+        int rc_ = (x);                \
+        if (rc_ != PK_OK) return rc_; \
     } while (0)
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -79,12 +102,6 @@ int alloc(pk_plan* p, T** ptr, size_t count) {
     return PK_OK;
 }
 
-#define PK_TRY(x)               \
-    do {                        \
-        int rc_ = (x);          \
-        if (rc_ != PK_OK) return rc_; \
-    } while (0)
-
 void free_plan(pk_plan* p) {
     if (!p) return;
     DeviceGuard g(p->device);
@@ -102,19 +119,34 @@ void free_plan(pk_plan* p) {
 
 size_t tsize(const pk_plan* p) { return p->dtype == PK_F32 ? 4 : 8; }
 
+// every (kernel, NF) instantiation the dispatch below can launch
+template <int NF>
+void smem_kernels(std::vector<const void*>& v) {
+    v.push_back((const void*)bp_f32_kernel<NF, true, true, true>);
+    v.push_back((const void*)bp_f32_kernel<NF, true, false, true>);
+    v.push_back((const void*)bp_f32_kernel<NF, false, true, true>);
+    v.push_back((const void*)bp_f32_kernel<NF, false, false, true>);
+    v.push_back((const void*)bp_f32_kernel<NF, true, true, false>);
+    v.push_back((const void*)bp_f32_kernel<NF, true, false, false>);
+    v.push_back((const void*)bp_f32_kernel<NF, false, true, false>);
+    v.push_back((const void*)bp_f32_kernel<NF, false, false, false>);
+    v.push_back((const void*)fp_f32_kernel<NF, false>);
+    v.push_back((const void*)finalize_kernel<float, NF>);
+}
+
 cudaError_t opt_in_smem(int device) {
     static bool done[64] = {};
     if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
     if (done[device]) return cudaSuccess;
     int mx = 0;
     cudaError_t e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-    mx -= 1024;  // headroom for the kernels' static shared memory
-    const void* ks[] = {(const void*)bp_f32_kernel<true, true, true>, (const void*)bp_f32_kernel<true, false, true>,
-                        (const void*)bp_f32_kernel<false, true, true>, (const void*)bp_f32_kernel<false, false, true>,
-                        (const void*)bp_f32_kernel<true, true, false>, (const void*)bp_f32_kernel<true, false, false>,
-                        (const void*)bp_f32_kernel<false, true, false>, (const void*)bp_f32_kernel<false, false, false>,
-                        (const void*)fp_f32_kernel<false>, (const void*)fp_f64_kernel,
-                        (const void*)finalize_kernel<float>, (const void*)finalize_kernel<double>};
+    mx -= 2048;  // headroom for the kernels' static shared memory
+    std::vector<const void*> ks;
+    smem_kernels<1>(ks);
+    smem_kernels<2>(ks);
+    smem_kernels<4>(ks);
+    ks.push_back((const void*)fp_f64_kernel);
+    ks.push_back((const void*)finalize_kernel<double, 1>);
     for (const void* k : ks)
         if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e == cudaSuccess) done[device] = true;
@@ -122,22 +154,21 @@ cudaError_t opt_in_smem(int device) {
 }
 
 // ---------------------------------------------------------------------------
-// kernel sequences
+// kernel sequences (NF-dispatched)
 
-int launch_maxabs(pk_plan* p, const void* x, cudaStream_t s) {
-    const int blocks = p->misc_blocks;
+template <int NF>
+void launch_maxabs_t(pk_plan* p, const void* x, cudaStream_t s) {
+    const dim3 grid(p->misc_blocks, NF);
     if (p->dtype == PK_F32)
-        maxabs_kernel<float><<<blocks, kThreads, 0, s>>>(static_cast<const float*>(x), p->P,
-                                                         p->part_misc, p->state, p->fp_bits);
+        maxabs_kernel<float><<<grid, kThreads, 0, s>>>(static_cast<const float*>(x), p->P,
+                                                       p->part_misc, p->state, p->fp_bits);
     else
-        maxabs_kernel<double><<<blocks, kThreads, 0, s>>>(static_cast<const double*>(x), p->P,
-                                                          p->part_misc, p->state, p->fp_bits);
-    PK_CHECK_LAUNCH();
-    return PK_OK;
+        maxabs_kernel<double><<<grid, kThreads, 0, s>>>(static_cast<const double*>(x), p->P,
+                                                        p->part_misc, p->state, p->fp_bits);
 }
 
-// K2: x == nullptr -> solver mode (x from the iterate ring)
-int launch_fp(pk_plan* p, const void* x, int solver, cudaStream_t s) {
+template <int NF>
+void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
     dim3 grid(p->fp_tiles_x * p->fp_tiles_y, p->fp_groups);
     if (p->dtype == PK_F32) {
         FpArgs a{};
@@ -150,7 +181,7 @@ int launch_fp(pk_plan* p, const void* x, int solver, cudaStream_t s) {
         a.tiles_x = p->fp_tiles_x;
         a.qclamp = (float)p->Q + 1.5f;
         a.st = p->state; a.part_tv = p->part_tv; a.solver = solver;
-        fp_f32_kernel<false><<<grid, kThreads, p->fp_smem, s>>>(a);
+        fp_f32_kernel<NF, false><<<grid, kThreads, p->fp_smem, s>>>(a);
     } else {
         FpArgs64 a{};
         a.x = static_cast<const double*>(x);
@@ -163,13 +194,13 @@ int launch_fp(pk_plan* p, const void* x, int solver, cudaStream_t s) {
         a.st = p->state; a.part_tv = p->part_tv; a.solver = solver;
         fp_f64_kernel<<<grid, kThreads, p->fp_smem, s>>>(a);
     }
-    PK_CHECK_LAUNCH();
-    return PK_OK;
 }
 
-int launch_finalize(pk_plan* p, const void* y, void* trace_out, double* sumsq, int solver,
-                    cudaStream_t s) {
+template <int NF>
+void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq, int solver,
+                       cudaStream_t s) {
     const size_t sm = (size_t)p->Q * tsize(p);
+    const dim3 grid(p->M, NF);
     if (p->dtype == PK_F32) {
         FinArgs<float> a{};
         a.acc = p->acc; a.y = static_cast<const float*>(y);
@@ -180,7 +211,7 @@ int launch_finalize(pk_plan* p, const void* y, void* trace_out, double* sumsq, i
         a.part_tv = p->part_tv; a.ntv = p->fp_tiles_x * p->fp_tiles_y; a.sumsq_out = sumsq;
         a.solver = solver;
         a.atrick = p->bp_atrick;
-        finalize_kernel<float><<<p->M, kThreads, sm, s>>>(a);
+        finalize_kernel<float, NF><<<grid, kThreads, sm, s>>>(a);
     } else {
         FinArgs<double> a{};
         a.acc = p->acc; a.y = static_cast<const double*>(y);
@@ -190,14 +221,13 @@ int launch_finalize(pk_plan* p, const void* y, void* trace_out, double* sumsq, i
         a.st = p->state; a.prm = p->params; a.io = p->io; a.part_r = p->part_r;
         a.part_tv = p->part_tv; a.ntv = p->fp_tiles_x * p->fp_tiles_y; a.sumsq_out = sumsq;
         a.solver = solver;
-        finalize_kernel<double><<<p->M, kThreads, sm, s>>>(a);
+        finalize_kernel<double, 1><<<grid, kThreads, sm, s>>>(a);
     }
-    PK_CHECK_LAUNCH();
-    return PK_OK;
 }
 
 // K1: epi == 0 -> out = gscale_mult * w * K^T r; epi == 1 -> fused update (solver)
-int launch_bp(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_t s) {
+template <int NF>
+void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_t s) {
     const bool clamp = p->max_delay >= (double)p->Q + 0.5;
     if (p->dtype == PK_F32) {
         BpArgs a{};
@@ -213,7 +243,7 @@ int launch_bp(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_t s
         a.prm = p->params; a.st = p->state; a.part = p->part_bp; a.bits = p->fp_bits;
         a.split = p->bp_split; a.ms = p->bp_ms; a.gpart = p->bp_gpart; a.tile_cnt = p->bp_tile_cnt;
         const dim3 grid(p->bp_tiles_x * p->bp_tiles_y, p->bp_split);
-#define PK_BP(E, C, A) bp_f32_kernel<E, C, A><<<grid, kThreads, p->bp_smem, s>>>(a)
+#define PK_BP(E, C, A) bp_f32_kernel<NF, E, C, A><<<grid, kThreads, p->bp_smem, s>>>(a)
         if (p->bp_atrick) {
             if (epi) { if (clamp) PK_BP(true, true, true); else PK_BP(true, false, true); }
             else { if (clamp) PK_BP(false, true, true); else PK_BP(false, false, true); }
@@ -236,73 +266,123 @@ int launch_bp(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_t s
         if (epi) bp_f64_kernel<true><<<grid, kThreads, 0, s>>>(a);
         else bp_f64_kernel<false><<<grid, kThreads, 0, s>>>(a);
     }
-    PK_CHECK_LAUNCH();
-    return PK_OK;
 }
 
-int launch_table(pk_plan* p, const void* y, int init, cudaStream_t s) {
+template <int NF>
+void launch_table_t(pk_plan* p, const void* y, int init, cudaStream_t s) {
+    const dim3 grid(p->M, NF);
     if (p->dtype == PK_F32)
-        table_kernel<float><<<p->M, kThreads, 0, s>>>(
+        table_kernel<float, NF><<<grid, kThreads, 0, s>>>(
             static_cast<const float*>(y), p->io, static_cast<float2*>(p->table), p->M, p->Q, p->TS,
             init ? -1.f : 1.f, p->part_r, p->state, init, p->bp_atrick);
     else
-        table_kernel<double><<<p->M, kThreads, 0, s>>>(
+        table_kernel<double, 1><<<grid, kThreads, 0, s>>>(
             static_cast<const double*>(y), p->io, static_cast<double2*>(p->table), p->M, p->Q,
             p->TS, init ? -1.0 : 1.0, p->part_r, p->state, init, 0);
-    PK_CHECK_LAUNCH();
+}
+
+template <int NF>
+void launch_init_t(pk_plan* p, cudaStream_t s) {
+    const int pb = std::min((NF * p->P + kThreads - 1) / kThreads, 148 * 8);
+    if (p->dtype == PK_F32)
+        init_kernel<float, NF><<<pb, kThreads, 0, s>>>(static_cast<float*>(p->xbuf[0]), p->P, p->state, p->io);
+    else
+        init_kernel<double, 1><<<pb, kThreads, 0, s>>>(static_cast<double*>(p->xbuf[0]), p->P, p->state, p->io);
+}
+
+template <int NF>
+void launch_copy_out_t(pk_plan* p, cudaStream_t s) {
+    const int cb = std::min((p->P + kThreads - 1) / kThreads, 148 * 4);
+    if (p->dtype == PK_F32)
+        copy_out_kernel<float, NF><<<cb, kThreads, 0, s>>>(static_cast<const float*>(p->xbuf[0]),
+                                                           static_cast<const float*>(p->xbuf[1]),
+                                                           p->state, p->io, p->P);
+    else
+        copy_out_kernel<double, 1><<<cb, kThreads, 0, s>>>(static_cast<const double*>(p->xbuf[0]),
+                                                           static_cast<const double*>(p->xbuf[1]),
+                                                           p->state, p->io, p->P);
+}
+
+#define PK_DISPATCH(fn, ...)                                \
+    do {                                                    \
+        switch (p->nf) {                                    \
+            case 2: fn<2>(__VA_ARGS__); break;              \
+            case 4: fn<4>(__VA_ARGS__); break;              \
+            default: fn<1>(__VA_ARGS__); break;             \
+        }                                                   \
+        PK_CHECK_LAUNCH();                                  \
+    } while (0)
+
+int launch_maxabs(pk_plan* p, const void* x, cudaStream_t s) {
+    PK_DISPATCH(launch_maxabs_t, p, x, s);
+    return PK_OK;
+}
+int launch_fp(pk_plan* p, const void* x, int solver, cudaStream_t s) {
+    PK_DISPATCH(launch_fp_t, p, x, solver, s);
+    return PK_OK;
+}
+int launch_finalize(pk_plan* p, const void* y, void* out, double* sumsq, int solver, cudaStream_t s) {
+    PK_DISPATCH(launch_finalize_t, p, y, out, sumsq, solver, s);
+    return PK_OK;
+}
+int launch_bp(pk_plan* p, int epi, void* out, double g, cudaStream_t s) {
+    PK_DISPATCH(launch_bp_t, p, epi, out, g, s);
+    return PK_OK;
+}
+int launch_table(pk_plan* p, const void* y, int init, cudaStream_t s) {
+    PK_DISPATCH(launch_table_t, p, y, init, s);
+    return PK_OK;
+}
+int launch_init(pk_plan* p, cudaStream_t s) {
+    PK_DISPATCH(launch_init_t, p, s);
+    return PK_OK;
+}
+int launch_copy_out(pk_plan* p, cudaStream_t s) {
+    PK_DISPATCH(launch_copy_out_t, p, s);
     return PK_OK;
 }
 
 // the solver graph body: x0 = 0, r0 = -y, N x (K1 update, K2, K3), copy-out
 int record_solver(pk_plan* p, int iters, cudaStream_t s) {
-    const int pb = (p->P + kThreads - 1) / kThreads;
-    if (p->dtype == PK_F32)
-        init_kernel<float><<<pb, kThreads, 0, s>>>(static_cast<float*>(p->xbuf[0]), p->P, p->state,
-                                                   p->io);
-    else
-        init_kernel<double><<<pb, kThreads, 0, s>>>(static_cast<double*>(p->xbuf[0]), p->P,
-                                                    p->state, p->io);
-    PK_CHECK_LAUNCH();
+    PK_TRY(launch_init(p, s));
     PK_TRY(launch_table(p, nullptr, 1, s));
     for (int it = 0; it < iters; ++it) {
         PK_TRY(launch_bp(p, 1, nullptr, 2.0, s));
         PK_TRY(launch_fp(p, nullptr, 1, s));
         PK_TRY(launch_finalize(p, nullptr, nullptr, nullptr, 1, s));
     }
-    const int cb = std::min(pb, 148 * 4);
-    if (p->dtype == PK_F32)
-        copy_out_kernel<float><<<cb, kThreads, 0, s>>>(static_cast<const float*>(p->xbuf[0]),
-                                                       static_cast<const float*>(p->xbuf[1]),
-                                                       p->state, p->io, p->P);
-    else
-        copy_out_kernel<double><<<cb, kThreads, 0, s>>>(static_cast<const double*>(p->xbuf[0]),
-                                                        static_cast<const double*>(p->xbuf[1]),
-                                                        p->state, p->io, p->P);
-    PK_CHECK_LAUNCH();
+    PK_TRY(launch_copy_out(p, s));
     return PK_OK;
 }
 
-int check_params(const pk_solver_params* prm) {
+int check_params(const pk_plan* p, const pk_solver_params* prm) {
     if (!prm) return fail(PK_ERR_INVALID, "params is NULL");
-    if (prm->iterations < 1) return fail(PK_ERR_INVALID, "iterations must be >= 1");
-    if (!(prm->alpha >= 0) || !(prm->beta >= 0))
-        return fail(PK_ERR_INVALID, "alpha and beta must be >= 0");
-    if (!(prm->step > 0)) return fail(PK_ERR_INVALID, "step must be > 0");
-    if (!(prm->tv_epsilon > 0)) return fail(PK_ERR_INVALID, "tv_epsilon must be > 0");
-    if (!(prm->tolerance >= 0)) return fail(PK_ERR_INVALID, "tolerance must be >= 0");
+    if (prm[0].iterations < 1) return fail(PK_ERR_INVALID, "iterations must be >= 1");
+    if (!(prm[0].tv_epsilon > 0)) return fail(PK_ERR_INVALID, "tv_epsilon must be > 0");
+    if (!(prm[0].tolerance >= 0)) return fail(PK_ERR_INVALID, "tolerance must be >= 0");
+    for (int f = 0; f < p->nf; ++f) {
+        if (!(prm[f].alpha >= 0) || !(prm[f].beta >= 0))
+            return fail(PK_ERR_INVALID, "alpha and beta must be >= 0 (frame %d)", f);
+        if (!(prm[f].step > 0)) return fail(PK_ERR_INVALID, "step must be > 0 (frame %d)", f);
+        if (prm[f].iterations != prm[0].iterations)
+            return fail(PK_ERR_INVALID, "all frames of a batch run the same iteration count");
+    }
     return PK_OK;
 }
 
 int upload_params(pk_plan* p, const pk_solver_params* prm, cudaStream_t s) {
     DevParams d{};
-    d.alpha = prm->alpha;
-    d.beta = prm->beta;
-    d.step = prm->step;
-    d.eps = prm->tv_epsilon;
-    d.tolerance = prm->tolerance;
-    d.eta_alpha = prm->step * prm->alpha;  // recon.py:336 passes eta * alpha
-    d.iterations = prm->iterations;
-    d.nonneg = prm->nonneg ? 1 : 0;
+    for (int f = 0; f < kMaxFrames; ++f) {
+        const pk_solver_params& q = prm[f < p->nf ? f : 0];
+        d.alpha[f] = q.alpha;
+        d.beta[f] = q.beta;
+        d.step[f] = q.step;
+        d.eta_alpha[f] = q.step * q.alpha;  // recon.py:336 passes eta * alpha
+    }
+    d.eps = prm[0].tv_epsilon;
+    d.tolerance = prm[0].tolerance;
+    d.iterations = prm[0].iterations;
+    d.nonneg = prm[0].nonneg ? 1 : 0;
     PK_CUDA(cudaMemcpyAsync(p->params, &d, sizeof(d), cudaMemcpyHostToDevice, s));
     return PK_OK;
 }
@@ -311,29 +391,12 @@ int ensure_hist(pk_plan* p, int iters) {
     if (p->hist_cap >= iters) return PK_OK;
     if (p->hist_dev) cudaFree(p->hist_dev);
     p->hist_dev = nullptr;
-    PK_TRY(alloc(p, &p->hist_dev, (size_t)4 * iters));
+    PK_TRY(alloc(p, &p->hist_dev, (size_t)4 * iters * p->nf));
     p->hist_cap = iters;
     return PK_OK;
 }
 
 }  // namespace
-
-namespace pk {
-// FP32 peak microkernel: 8 independent FFMA chains per thread, immediate-free operands
-__global__ void __launch_bounds__(kThreads) ffma_peak_kernel(float* out, int iters) {
-    float a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
-          a6 = a0 + 6, a7 = a0 + 7;
-    const float b = 1.0001f + 1e-9f * blockIdx.x, c = 0.9999f;
-    for (int i = 0; i < iters; ++i) {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            a0 = fmaf(a0, b, c); a1 = fmaf(a1, b, c); a2 = fmaf(a2, b, c); a3 = fmaf(a3, b, c);
-            a4 = fmaf(a4, b, c); a5 = fmaf(a5, b, c); a6 = fmaf(a6, b, c); a7 = fmaf(a7, b, c);
-        }
-    }
-    out[blockIdx.x * kThreads + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
-}
-}  // namespace pk
 
 // ===========================================================================
 // C ABI
@@ -342,7 +405,7 @@ extern "C" {
 
 const char* pk_last_error(void) { return g_err; }
 
-int pk_version(void) { return 10000; /* 1.0.0 */ }
+int pk_version(void) { return 10100; /* 1.1.0: batched frames */ }
 
 int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     if (!d || !out) return fail(PK_ERR_INVALID, "NULL argument");
@@ -355,6 +418,10 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         return fail(PK_ERR_INVALID, "bad sensor shard [%d, %d) of %d", d->sensor_begin,
                     d->sensor_end, d->sensors);
     if (d->dtype != PK_F32 && d->dtype != PK_F64) return fail(PK_ERR_INVALID, "bad dtype");
+    const int nf = d->frames <= 1 ? 1 : d->frames;
+    if (nf != 1 && nf != 2 && nf != 4) return fail(PK_ERR_INVALID, "frames must be 1, 2 or 4");
+    if (nf > 1 && d->dtype != PK_F32)
+        return fail(PK_ERR_UNSUPPORTED, "batched frames are supported in fp32 only");
     if (!d->pixel_x || !d->pixel_y || !d->sensor_xy) return fail(PK_ERR_INVALID, "NULL geometry");
     if ((int64_t)d->nx * d->ny > (int64_t)1 << 30) return fail(PK_ERR_UNSUPPORTED, "grid too large");
 
@@ -367,11 +434,12 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     pk_plan* p = new pk_plan();
     p->device = d->device;
     p->dtype = d->dtype;
+    p->nf = nf;
     p->nx = d->nx; p->ny = d->ny; p->P = d->nx * d->ny;
     p->Mall = d->sensors; p->m0 = d->sensor_begin; p->M = d->sensor_end - d->sensor_begin;
     p->Q = d->samples;
     p->c = d->c; p->dt = d->dt;
-    p->cdt = d->c * d->dt;                       // forward.py:180
+    p->cdt = d->c * d->dt;                          // forward.py:180
     p->w = 1.0 / (2.0 * 3.141592653589793 * d->c);  // forward.py:183
 
     // pixel / sensor geometry; delay bounds per sensor from the grid rectangle
@@ -398,8 +466,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             if (ix != X + p->nx && iy != Y + p->ny) {
                 free_plan(p);
                 return fail(PK_ERR_GEOMETRY, "sensor %d coincides with pixel index %lld",
-                            m + d->sensor_begin,
-                            (long long)((iy - Y) * p->nx + (ix - X)));
+                            m + d->sensor_begin, (long long)((iy - Y) * p->nx + (ix - X)));
             }
         }
     }
@@ -418,7 +485,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     p->TS = (p->Q + 2 + 1) & ~1;
     {
         const char* ev = getenv("PK_BP_ATRICK");
-        p->bp_atrick = (p->dtype == PK_F32) ? (ev ? atoi(ev) != 0 : 0) : 0;  // opt-in: see DESIGN.md
+        p->bp_atrick = (p->dtype == PK_F32) ? (ev ? atoi(ev) != 0 : 0) : 0;  // opt-in: DESIGN.md
     }
     // back-projector
     p->bp_tiles_x = (p->nx + kBpTile - 1) / kBpTile;
@@ -426,29 +493,29 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     p->bp_L = ((int)std::ceil(tile_diag(kBpTile)) + 6 + 1) & ~1;
     if (p->bp_L > p->TS) p->bp_L = p->TS;
     p->bp_nbuf = 3;
-    const int bp_budget = 52 * 1024;  // 4 CTAs (32 warps) per SM
-    p->bp_CS = std::max(1, std::min(32, bp_budget / (p->bp_nbuf * p->bp_L * 8)));
-    p->bp_smem = p->bp_nbuf * p->bp_CS * p->bp_L * 8 + p->bp_nbuf * p->bp_CS * 16 + p->bp_nbuf * 8;
-    {   // sensor split so that tiles x split >= ~4 CTAs per SM, each split >= 64 sensors
-        const int tiles = p->bp_tiles_x * p->bp_tiles_y;
-        int sp = 1;
-        while (tiles * sp < 4 * 148 && p->M / (2 * sp) >= 64) sp *= 2;
-        p->bp_split = sp;
-        p->bp_ms = (p->M + sp - 1) / sp;
-        p->bp_ms = ((p->bp_ms + p->bp_CS - 1) / p->bp_CS) * p->bp_CS;  // whole chunks
-        p->bp_split = (p->M + p->bp_ms - 1) / p->bp_ms;
-    }
+    // CTAs per SM the launch bounds aim for: 4 (NF=1), 3 (NF=2), 2 (NF=4)
+    const int bp_budget = (nf == 1 ? 52 : (nf == 2 ? 70 : 104)) * 1024;
+    p->bp_CS = std::max(1, std::min(32, bp_budget / (p->bp_nbuf * p->bp_L * 8 * nf)));
+    p->bp_smem = p->bp_nbuf * p->bp_CS * p->bp_L * 8 * nf + p->bp_nbuf * p->bp_CS * 16 + p->bp_nbuf * 8;
     if (p->dtype == PK_F32 && p->bp_smem > 200 * 1024) {
         free_plan(p);
         return fail(PK_ERR_UNSUPPORTED, "delay window per tile too long (%d samples)", p->bp_L);
     }
-    // projector
+    {   // sensor split so that tiles x split >= ~4 CTAs per SM, each split >= 64 sensors
+        const int tiles = p->bp_tiles_x * p->bp_tiles_y;
+        int sp = 1;
+        if (p->dtype == PK_F32)
+            while (tiles * sp < 4 * 148 && p->M / (2 * sp) >= 64) sp *= 2;
+        p->bp_ms = (p->M + sp - 1) / sp;
+        p->bp_ms = ((p->bp_ms + p->bp_CS - 1) / p->bp_CS) * p->bp_CS;  // whole chunks
+        p->bp_split = (p->M + p->bp_ms - 1) / p->bp_ms;
+    }
     // projector tile: 64 x 64 when that still gives >= 4 CTAs per SM (halves the window
-    // flush traffic per interaction), else 32 x 32
+    // flush traffic per interaction) and the windows fit, else 32 x 32
     p->fp_groups = (p->M + 31) / 32;
     {
         const int t64 = ((p->nx + 63) / 64) * ((p->ny + 63) / 64);
-        p->fp_T = (p->dtype == PK_F32 && (int64_t)t64 * p->fp_groups >= 4 * 148) ? 64 : 32;
+        p->fp_T = (p->dtype == PK_F32 && nf <= 2 && (int64_t)t64 * p->fp_groups >= 4 * 148) ? 64 : 32;
     }
     p->fp_tiles_x = (p->nx + p->fp_T - 1) / p->fp_T;
     p->fp_tiles_y = (p->ny + p->fp_T - 1) / p->fp_T;
@@ -458,8 +525,9 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     if (p->min_delay < 8.0 * p->fp_T * std::max(h, 1.0)) nc_tile = (double)p->fp_T * p->fp_T;
     nc_tile = std::min(nc_tile, (double)p->fp_T * p->fp_T);
     if (p->dtype == PK_F32) {
+        const int rv = (1 + 2 * nf + 3) / 4;
         p->fp_bits = std::min(22, 30 - ceil_log2(nc_tile));
-        p->fp_smem = p->fp_L * 32 * 4 + (kThreads / 32) * (p->fp_T + kFpBatch) * 16;
+        p->fp_smem = p->fp_L * nf * 32 * 4 + (kThreads / 32) * (p->fp_T + kFpBatch) * rv * 16;
     } else {
         double nc_glob = std::min((double)p->P, 4.0 * (p->nx + p->ny) * (2.0 / std::max(h, 1e-12) + 2));
         if (p->min_delay < 8.0 * p->fp_T * std::max(h, 1.0)) nc_glob = (double)p->P;
@@ -472,6 +540,10 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         return fail(PK_ERR_UNSUPPORTED, "projector window too long (%d samples)", p->fp_L);
     }
     p->misc_blocks = std::max(1, std::min(1024, (p->P + kThreads - 1) / kThreads));
+    if ((size_t)p->Q * tsize(p) > 200 * 1024) {
+        free_plan(p);
+        return fail(PK_ERR_UNSUPPORTED, "trace of %d samples exceeds shared memory", p->Q);
+    }
 
     // allocations
     int rc = PK_OK;
@@ -491,17 +563,17 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     A(alloc(p, &p->px, p->nx)); A(alloc(p, &p->py, p->ny));
     A(alloc(p, &p->sx, p->M)); A(alloc(p, &p->sy, p->M));
     const size_t ts = tsize(p);
-    A(alloc(p, reinterpret_cast<unsigned char**>(&p->table), (size_t)p->M * p->TS * 2 * ts));
-    A(alloc(p, &p->acc, (size_t)p->M * p->Q));
-    A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[0]), (size_t)p->P * ts));
-    A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[1]), (size_t)p->P * ts));
-    A(alloc(p, &p->part_bp, (size_t)4 * std::max(p->bp_tiles_x * p->bp_tiles_y,
-                                                 (p->P + kThreads - 1) / kThreads)));
-    A(alloc(p, &p->part_tv, (size_t)p->fp_tiles_x * p->fp_tiles_y));
-    if (p->bp_split > 1) A(alloc(p, &p->bp_gpart, (size_t)p->bp_split * p->P));
+    A(alloc(p, reinterpret_cast<unsigned char**>(&p->table), (size_t)p->M * p->TS * 2 * ts * nf));
+    A(alloc(p, &p->acc, (size_t)p->M * p->Q * nf));
+    A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[0]), (size_t)p->P * ts * nf));
+    A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[1]), (size_t)p->P * ts * nf));
+    A(alloc(p, &p->part_bp, (size_t)4 * nf * std::max(p->bp_tiles_x * p->bp_tiles_y,
+                                                      (p->P + kThreads - 1) / kThreads)));
+    A(alloc(p, &p->part_tv, (size_t)p->fp_tiles_x * p->fp_tiles_y * nf));
+    A(alloc(p, &p->part_r, (size_t)p->M * nf));
+    A(alloc(p, &p->part_misc, (size_t)4 * p->misc_blocks * nf));
+    if (p->bp_split > 1) A(alloc(p, &p->bp_gpart, (size_t)p->bp_split * p->P * nf));
     A(alloc(p, &p->bp_tile_cnt, (size_t)p->bp_tiles_x * p->bp_tiles_y));
-    A(alloc(p, &p->part_r, (size_t)p->M));
-    A(alloc(p, &p->part_misc, (size_t)4 * p->misc_blocks));
     A(alloc(p, &p->state, 1));
     A(alloc(p, &p->params, 1));
     A(alloc(p, &p->io, 1));
@@ -514,11 +586,11 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     up(p->sxs, fsx.data(), p->M * 4); up(p->sys, fsy.data(), p->M * 4);
     up(p->px, X, p->nx * 8); up(p->py, Y, p->ny * 8);
     up(p->sx, dsx.data(), p->M * 8); up(p->sy, dsy.data(), p->M * 8);
-    if (e == cudaSuccess) e = cudaMemset(p->acc, 0, (size_t)p->M * p->Q * 8);
+    if (e == cudaSuccess) e = cudaMemset(p->acc, 0, (size_t)p->M * p->Q * 8 * nf);
     if (e == cudaSuccess) e = cudaMemset(p->state, 0, sizeof(DevState));
     if (e == cudaSuccess)
         e = cudaMemset(p->bp_tile_cnt, 0, sizeof(uint32_t) * p->bp_tiles_x * p->bp_tiles_y);
-    if (e == cudaSuccess) e = cudaMemset(p->table, 0, (size_t)p->M * p->TS * 2 * ts);
+    if (e == cudaSuccess) e = cudaMemset(p->table, 0, (size_t)p->M * p->TS * 2 * ts * nf);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);
     // opt every dynamic-smem kernel into the device maximum once per device (a per-plan
     // value would shrink the limit under plans created earlier with larger windows)
@@ -527,10 +599,6 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     if (e != cudaSuccess) {
         free_plan(p);
         return fail(PK_ERR_CUDA, "plan setup failed: %s", cudaGetErrorString(e));
-    }
-    if ((size_t)p->Q * ts > 200 * 1024) {
-        free_plan(p);
-        return fail(PK_ERR_UNSUPPORTED, "trace of %d samples exceeds shared memory", p->Q);
     }
     *out = p;
     return PK_OK;
@@ -557,6 +625,8 @@ int pk_plan_get_info(const pk_plan* p, pk_plan_info* o) {
     o->fp_window = p->fp_L;
     o->fp_bits = p->fp_bits;
     o->device_bytes = p->device_bytes;
+    o->frames = p->nf;
+    o->bp_split = p->bp_split;
     return PK_OK;
 }
 
@@ -600,7 +670,8 @@ int pk_adjoint_residual(pk_plan* p, void* out, double scale, void* stream) {
 int pk_grad_update(pk_plan* p, const pk_solver_params* prm, const void* x, const void* grad,
                    void* x_out, double* sums, void* stream) {
     if (!p || !x || !grad || !x_out || !sums) return fail(PK_ERR_INVALID, "NULL argument");
-    PK_TRY(check_params(prm));
+    if (p->nf != 1) return fail(PK_ERR_UNSUPPORTED, "pk_grad_update is single-frame");
+    PK_TRY(check_params(p, prm));
     DeviceGuard g(p->device);
     cudaStream_t s = S(stream);
     PK_TRY(upload_params(p, prm, s));
@@ -627,7 +698,7 @@ int pk_grad_update(pk_plan* p, const pk_solver_params* prm, const void* x, const
 int pk_reconstruct(pk_plan* p, const pk_solver_params* prm, const void* y, void* x_out,
                    double* hist, int32_t* status, void* stream) {
     if (!p || !y || !x_out || !hist || !status) return fail(PK_ERR_INVALID, "NULL argument");
-    PK_TRY(check_params(prm));
+    PK_TRY(check_params(p, prm));
     if (p->M != p->Mall)
         return fail(PK_ERR_INVALID, "pk_reconstruct needs a plan over all sensors (use the sharded pieces)");
     DeviceGuard g(p->device);
@@ -635,19 +706,19 @@ int pk_reconstruct(pk_plan* p, const pk_solver_params* prm, const void* y, void*
     PK_TRY(upload_params(p, prm, s));
     DevIo io{y, x_out, hist, status};
     PK_CUDA(cudaMemcpyAsync(p->io, &io, sizeof(io), cudaMemcpyHostToDevice, s));
-    if (p->graph_iters != prm->iterations) {
+    if (p->graph_iters != prm[0].iterations) {
         if (p->graph_exec) { cudaGraphExecDestroy(p->graph_exec); p->graph_exec = nullptr; }
         if (p->graph) { cudaGraphDestroy(p->graph); p->graph = nullptr; }
         p->graph_iters = -1;
         PK_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
-        int rc = record_solver(p, prm->iterations, p->cap_stream);
+        int rc = record_solver(p, prm[0].iterations, p->cap_stream);
         cudaGraph_t gr = nullptr;
         cudaError_t e = cudaStreamEndCapture(p->cap_stream, &gr);
         if (rc != PK_OK) { if (gr) cudaGraphDestroy(gr); return rc; }
         if (e != cudaSuccess) return fail(PK_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
         p->graph = gr;
         PK_CUDA(cudaGraphInstantiate(&p->graph_exec, p->graph, 0));
-        p->graph_iters = prm->iterations;
+        p->graph_iters = prm[0].iterations;
     }
     PK_CUDA(cudaGraphLaunch(p->graph_exec, s));
     return PK_OK;
@@ -658,34 +729,34 @@ int pk_reconstruct_host(pk_plan* p, const pk_solver_params* prm, const double* y
                         void* stream) {
     if (!p || !y_host || !x_out_host || !hist_host || !status_host)
         return fail(PK_ERR_INVALID, "NULL argument");
-    PK_TRY(check_params(prm));
+    PK_TRY(check_params(p, prm));
     DeviceGuard g(p->device);
     cudaStream_t s = S(stream);
-    const size_t ny = (size_t)p->M * p->Q;
+    const size_t ny = (size_t)p->M * p->Q * p->nf;
+    const size_t nx = (size_t)p->P * p->nf;
     if (!p->y64) { PK_TRY(alloc(p, &p->y64, ny)); }
-    if (!p->x64) { PK_TRY(alloc(p, &p->x64, p->P)); }
-    if (!p->status_dev) { PK_TRY(alloc(p, &p->status_dev, 2)); }
+    if (!p->x64) { PK_TRY(alloc(p, &p->x64, nx)); }
+    if (!p->status_dev) { PK_TRY(alloc(p, &p->status_dev, 2 * p->nf)); }
     if (p->dtype == PK_F32 && !p->ydev) {
         PK_TRY(alloc(p, reinterpret_cast<float**>(&p->ydev), ny));
-        PK_TRY(alloc(p, reinterpret_cast<float**>(&p->xout_dev), p->P));
+        PK_TRY(alloc(p, reinterpret_cast<float**>(&p->xout_dev), nx));
     }
-    PK_TRY(ensure_hist(p, prm->iterations));
+    PK_TRY(ensure_hist(p, prm[0].iterations));
     PK_CUDA(cudaMemcpyAsync(p->y64, y_host, ny * 8, cudaMemcpyHostToDevice, s));
     const int cb = 148 * 4;
     if (p->dtype == PK_F32) {
         convert_kernel<float><<<cb, kThreads, 0, s>>>(p->y64, static_cast<float*>(p->ydev), ny);
         PK_CHECK_LAUNCH();
         PK_TRY(pk_reconstruct(p, prm, p->ydev, p->xout_dev, p->hist_dev, p->status_dev, stream));
-        widen_kernel<float><<<cb, kThreads, 0, s>>>(static_cast<const float*>(p->xout_dev), p->x64,
-                                                    (size_t)p->P);
+        widen_kernel<float><<<cb, kThreads, 0, s>>>(static_cast<const float*>(p->xout_dev), p->x64, nx);
         PK_CHECK_LAUNCH();
     } else {
         PK_TRY(pk_reconstruct(p, prm, p->y64, p->x64, p->hist_dev, p->status_dev, stream));
     }
-    PK_CUDA(cudaMemcpyAsync(x_out_host, p->x64, (size_t)p->P * 8, cudaMemcpyDeviceToHost, s));
-    PK_CUDA(cudaMemcpyAsync(hist_host, p->hist_dev, (size_t)4 * prm->iterations * 8,
+    PK_CUDA(cudaMemcpyAsync(x_out_host, p->x64, nx * 8, cudaMemcpyDeviceToHost, s));
+    PK_CUDA(cudaMemcpyAsync(hist_host, p->hist_dev, (size_t)4 * prm[0].iterations * p->nf * 8,
                             cudaMemcpyDeviceToHost, s));
-    PK_CUDA(cudaMemcpyAsync(status_host, p->status_dev, 8, cudaMemcpyDeviceToHost, s));
+    PK_CUDA(cudaMemcpyAsync(status_host, p->status_dev, 8 * p->nf, cudaMemcpyDeviceToHost, s));
     PK_CUDA(cudaStreamSynchronize(s));
     return PK_OK;
 }
@@ -704,24 +775,21 @@ int pk_index_dump(pk_plan* p, int32_t ma, int32_t mb, int64_t* s0, double* frac,
 int pk_profile_iterations(pk_plan* p, const pk_solver_params* prm, const void* y, float* ms,
                           int32_t* launches, void* stream) {
     if (!p || !y || !ms) return fail(PK_ERR_INVALID, "NULL argument");
-    PK_TRY(check_params(prm));
+    PK_TRY(check_params(p, prm));
     if (p->M != p->Mall) return fail(PK_ERR_INVALID, "profiling needs a plan over all sensors");
     DeviceGuard g(p->device);
     cudaStream_t s = S(stream);
-    PK_TRY(ensure_hist(p, prm->iterations));
-    if (!p->status_dev) { PK_TRY(alloc(p, &p->status_dev, 2)); }
-    if (!p->xout_dev) { PK_TRY(alloc(p, reinterpret_cast<unsigned char**>(&p->xout_dev), (size_t)p->P * tsize(p))); }
+    PK_TRY(ensure_hist(p, prm[0].iterations));
+    if (!p->status_dev) { PK_TRY(alloc(p, &p->status_dev, 2 * p->nf)); }
+    if (!p->xout_dev) {
+        PK_TRY(alloc(p, reinterpret_cast<unsigned char**>(&p->xout_dev), (size_t)p->P * tsize(p) * p->nf));
+    }
     PK_TRY(upload_params(p, prm, s));
     DevIo io{y, p->xout_dev, p->hist_dev, p->status_dev};
     PK_CUDA(cudaMemcpyAsync(p->io, &io, sizeof(io), cudaMemcpyHostToDevice, s));
-    const int pb = (p->P + kThreads - 1) / kThreads;
-    if (p->dtype == PK_F32)
-        init_kernel<float><<<pb, kThreads, 0, s>>>(static_cast<float*>(p->xbuf[0]), p->P, p->state, p->io);
-    else
-        init_kernel<double><<<pb, kThreads, 0, s>>>(static_cast<double*>(p->xbuf[0]), p->P, p->state, p->io);
-    PK_CHECK_LAUNCH();
+    PK_TRY(launch_init(p, s));
     PK_TRY(launch_table(p, nullptr, 1, s));
-    const int n = prm->iterations;
+    const int n = prm[0].iterations;
     std::vector<cudaEvent_t> ev(3 * n + 1);
     for (auto& e : ev) PK_CUDA(cudaEventCreate(&e));
     PK_CUDA(cudaEventRecord(ev[0], s));

@@ -24,37 +24,45 @@ constexpr int kBpTile = 32;    // back-projector pixel tile (32 x 32, 4 pixels/t
 constexpr int kDivergenceStreak = 5;  // recon.py:42-43
 
 // ---------------------------------------------------------------------------
-// device state of one solve (single frame)
-struct DevState {
-    // written by the update (back-projection) kernel's last block
-    double maxabs;     // max |x'| of the new iterate
+// device state of one solve.  A plan reconstructs NF frames that share the geometry
+// (NF = 1 single frame; NF = 2 or 4 batched, fp32): the delay of every sensor-pixel pair is
+// evaluated once and applied to all NF frames.  Per-frame solver state lives in fr[].
+constexpr int kMaxFrames = 4;
+
+struct FrameState {
+    double maxabs;     // max |x'| of the new iterate (update kernel)
     double l1sum;      // sum |x'|
-    double scale64;    // fixed-point scale for the projector (2^bits / maxabs)
+    double scale64;    // fixed-point scale of the projector (2^bits / maxabs)
+    double f_prev;     // objective of the last accepted iterate
     float scale32;
     int32_t nonfinite; // any non-finite x'
-    // solver bookkeeping, written by the residual kernel's last block
-    double f_prev;
-    int32_t iter;      // iterations attempted so far
     int32_t accepted;  // iterations accepted (== iterations_run)
     int32_t stopped;
     int32_t stopped_by;
     int32_t grow;
-    int32_t pad0;
+};
+
+struct DevState {
+    int32_t iter;        // iterations attempted so far (shared by the frames)
+    int32_t all_stopped; // every frame stopped (or iteration cap): kernels early-exit
+    int32_t pad0, pad1;
     // last-block counters (reset by the last block itself)
     uint32_t cnt_bp, cnt_fp, cnt_fin, cnt_misc;
-    // scalars of the sharded / standalone entry points
-    double sums[4];
+    double sums[4];      // scalars of the sharded / standalone entry points
+    FrameState fr[kMaxFrames];
 };
 
 // device copy of the solver parameters (read by the graph's kernels)
 struct DevParams {
-    double alpha, beta, step, eps, tolerance;
-    double eta_alpha;  // step * alpha (soft-threshold level)
+    double alpha[kMaxFrames], beta[kMaxFrames], step[kMaxFrames];
+    double eta_alpha[kMaxFrames];  // step * alpha (soft-threshold level)
+    double eps, tolerance;
     int32_t iterations, nonneg;
 };
 
 // I/O pointers of pk_reconstruct, read from device memory so that one captured graph
-// serves any caller buffers.
+// serves any caller buffers.  Frame-major: y [NF][M*Q], x_out [NF][P],
+// hist [NF][4][iterations], status [NF][2].
 struct DevIo {
     const void* y;
     void* x_out;
@@ -77,6 +85,14 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 __device__ __forceinline__ float2 lds_f2(uint32_t addr) {
     float2 v;
     asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr));
     return v;
 }
 
@@ -212,6 +228,7 @@ __device__ __forceinline__ double delay_f64(double px, double py, double sx, dou
 // the plan (opaque to C callers)
 struct pk_plan {
     int device = 0, dtype = PK_F32;
+    int nf = 1;  // frames per plan (shared geometry)
     int nx = 0, ny = 0, P = 0, Mall = 0, m0 = 0, M = 0, Q = 0;
     double c = 0, dt = 0, cdt = 0, w = 0;
     int may_truncate = 0;

@@ -7,6 +7,8 @@
 //                          and (solver mode) the objective + stopping rules (recon.py:346-363)
 //   misc                   table-from-trace, max|x| scale, update for sharded runs, index dump
 //
+// fp32 kernels are templated on NF, the number of frames that share one geometry (1, 2, 4):
+// the delay of a sensor-pixel pair is evaluated once and applied to all NF frames.
 // See DESIGN.md for the data layout and the per-interaction instruction budget.
 #pragma once
 #include <type_traits>
@@ -15,52 +17,89 @@
 
 namespace pk {
 
+template <int NF>
+struct Lg;
+template <>
+struct Lg<1> { static constexpr int v = 0; };
+template <>
+struct Lg<2> { static constexpr int v = 1; };
+template <>
+struct Lg<4> { static constexpr int v = 2; };
+
+// soft threshold of recon.py:158-159 keeping NaN (np.maximum propagates it), then the
+// optional non-negativity clamp of recon.py:337-338
+template <typename T>
+__device__ __forceinline__ T prox(T v, T lam, bool nonneg) {
+    T mag = fabs(v) - lam;
+    mag = (mag != mag) ? mag : fmax(mag, (T)0);
+    T xn = (v > (T)0) ? mag : ((v < (T)0) ? -mag : (v != v ? v : (T)0));
+    if (nonneg) xn = (xn != xn) ? xn : fmax(xn, (T)0);
+    return xn;
+}
+
+// gradient of the eps-smoothed TV at pixel p (recon.py:178-189, same accumulation order)
+template <typename T>
+__device__ __forceinline__ T tv_grad_at(const T* x, size_t p, int i, int j, int nx, int ny, T e2) {
+    const T x0 = x[p];
+    T t = 0;
+    if (i < nx - 1) { const T d = x[p + 1] - x0; t -= d / sqrt(d * d + e2); }
+    if (i > 0) { const T d = x0 - x[p - 1]; t += d / sqrt(d * d + e2); }
+    if (j < ny - 1) { const T d = x[p + nx] - x0; t -= d / sqrt(d * d + e2); }
+    if (j > 0) { const T d = x0 - x[p - nx]; t += d / sqrt(d * d + e2); }
+    return t;
+}
+
 // ===========================================================================
-// K1 -- back-projector, fp32.  CTA = 32x32 pixel tile, 256 threads, thread owns the
-// pixels (i0 + lx + 8k, j0 + 4*warp + ly), k = 0..3, so every warp instruction covers a
-// compact 8x4 pixel footprint (delay span <= ~32 samples -> broadcast-friendly LDS.64).
-// Sensors are processed in chunks of CS; for each chunk the per-(tile, sensor) window of
-// the residual pair table is brought into shared memory by the TMA engine
-// (cp.async.bulk + mbarrier), NBUF-deep ring.
+// K1 -- back-projector, fp32.  CTA = 32x32 pixel tile x a slice of the sensors, 256
+// threads, thread owns the pixels (i0 + lx + 8k, j0 + 4*warp + ly), k = 0..3, so every
+// warp instruction covers a compact 8x4 pixel footprint.  Sensors are processed in chunks
+// of CS; the per-(tile, sensor) window of the residual pair table is brought into shared
+// memory by the TMA engine (cp.async.bulk + mbarrier), NBUF-deep ring, refilled by the
+// last warp to finish with a buffer (no CTA barrier in the loop).
 //
-// pair table entry s of sensor m: {r[s-1], r[s] - r[s-1]} (r[-1] = r[Q] = r[Q+1] = 0), so
-// one interaction is  acc += r[s0-1] + f*(r[s0]-r[s0-1])  == (1-f) r[s0-1] + f r[s0],
+// pair table entry s of sensor m, frame f (layout [m][s][f]): {r[s-1], r[s]-r[s-1]}
+// (r[-1] = r[Q] = r[Q+1] = 0), so one interaction is
+//     acc += r[s0-1] + f*(r[s0]-r[s0-1])  == (1-f) r[s0-1] + f r[s0],
 // the two weights of build_time_matrix (forward.py:189-194) without the w factor.
+// One LDS.64 (NF = 1) / LDS.128 (NF = 2) / 2x LDS.128 (NF = 4) per interaction.
 // ===========================================================================
 struct BpArgs {
-    const float2* table;  // [M][TS]
+    const float2* table;  // [M][TS][NF]
     const float* pxs;     // [nx] scaled pixel x
     const float* pys;     // [ny]
     const float* sxs;     // [M]
     const float* sys;     // [M]
     int nx, ny, M, Q, TS, L, CS, nbuf, tiles_x;
     float qclamp;         // Q + 1.5 (truncation clamp of the delay)
-    // EPI == 0: out[p] = gscale * acc
+    // EPI == 0: out[f][p] = gscale * acc
     float* out;
     float gscale;
-    // EPI == 1: fused update, x from xb[iter & 1] to xb[(iter+1) & 1]
+    // EPI == 1: fused update, x from xb[iter & 1] to xb[(iter+1) & 1] (each [NF][P])
     float* xb0;
     float* xb1;
     const DevParams* prm;
     DevState* st;
-    double* part;         // [tiles * 4]
+    double* part;         // [tiles][NF][4]
     int bits;             // projector fixed-point bits (scale = 2^bits / max|x'|)
     // sensor split: CTA (tile, s) sums sensors [s*ms, min(M, (s+1)*ms)); the last CTA of a
     // tile to finish adds the S partials in split order (deterministic) and runs the epilogue
     int split, ms;
-    float* gpart;         // [split][P]
+    float* gpart;         // [split][NF][P]
     uint32_t* tile_cnt;   // [tiles]
 };
 
-template <bool EPI, bool CLAMP, bool ATRICK>
-__global__ void __launch_bounds__(kThreads, 4) bp_f32_kernel(BpArgs a) {
+template <int NF, bool EPI, bool CLAMP, bool ATRICK>
+__global__ void __launch_bounds__(kThreads, NF == 1 ? 4 : (NF == 2 ? 3 : 2)) bp_f32_kernel(BpArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ float red_f[kThreads / 32];
+    __shared__ double red_d[kThreads / 32];
     __shared__ int last_flag;
+    __shared__ uint32_t done_cnt[8];  // per-buffer count of warps finished with it
+    constexpr int LG = Lg<NF>::v;
 
     int iter = 0;
     if (EPI) {
-        if (a.st->stopped) return;
+        if (a.st->all_stopped) return;
         iter = a.st->iter;
     }
     const int tile = blockIdx.x;
@@ -71,30 +110,29 @@ __global__ void __launch_bounds__(kThreads, 4) bp_f32_kernel(BpArgs a) {
     const int j = j0 + warp * 4 + ly;
     const int mbase = blockIdx.y * a.ms;
     const int mcount = min(a.ms, a.M - mbase);
+    const size_t P = (size_t)a.nx * a.ny;
 
-    // two independent accumulator chains per pixel (FFMA chain of u*D, FADD chain of A)
-    float px[4], acc[4], acc2[4];
+    // two independent accumulator chains per pixel and frame (FFMA chain, FADD chain)
+    float px[4], acc[4][NF], acc2[4][NF];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         px[k] = __ldg(a.pxs + min(i0 + lx + 8 * k, a.nx - 1));
-        acc[k] = 0.f;
-        acc2[k] = 0.f;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) acc[k][f] = acc2[k][f] = 0.f;
     }
     const float py = __ldg(a.pys + min(j, a.ny - 1));
 
-    // shared layout: windows [nbuf][CS][L] float2 | sconst [nbuf][CS] float4 | bars [nbuf] u64
-    float2* win = reinterpret_cast<float2*>(smem);
-    float4* sconst = reinterpret_cast<float4*>(smem + (size_t)a.nbuf * a.CS * a.L * 8);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)a.nbuf * a.CS * a.L * 8 +
-                                                 (size_t)a.nbuf * a.CS * 16);
-    const uint32_t win_s = smem_u32(win);
+    // shared layout: windows [nbuf][CS][L][NF] float2 | sconst [nbuf][CS] float4 | bars [nbuf]
+    const size_t win_bytes = (size_t)a.nbuf * a.CS * a.L * 8 * NF;
+    float4* sconst = reinterpret_cast<float4*>(smem + win_bytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + win_bytes + (size_t)a.nbuf * a.CS * 16);
+    const uint32_t win_s = smem_u32(smem);
     const uint32_t bar_s = smem_u32(bars);
 
     // tile rectangle in scaled coordinates (for the per-sensor delay windows)
     const float X0 = __ldg(a.pxs + i0), X1 = __ldg(a.pxs + min(i0 + kBpTile - 1, a.nx - 1));
     const float Y0 = __ldg(a.pys + j0), Y1 = __ldg(a.pys + min(j0 + kBpTile - 1, a.ny - 1));
 
-    __shared__ uint32_t done_cnt[8];  // per-buffer count of warps finished with it
     if (threadIdx.x == 0) {
         for (int b = 0; b < a.nbuf; ++b) {
             mbar_init(bar_s + 8 * b, 1);
@@ -117,14 +155,15 @@ __global__ void __launch_bounds__(kThreads, 4) bp_f32_kernel(BpArgs a) {
             int lo = (int)floorf(dmin) - 1;
             lo = max(lo, 0) & ~1;
             lo = min(lo, a.TS - a.L);
-            const uint32_t dst = win_s + (uint32_t)((b * a.CS + lane) * a.L) * 8u;
-            const uint32_t adj = dst - 8u * (uint32_t)lo - 8u * kTwo23Bits;
+            const uint32_t dst = win_s + (uint32_t)((b * a.CS + lane) * a.L) * (8u * NF);
+            const uint32_t adj = dst - (8u * NF) * (uint32_t)lo - (8u * NF) * kTwo23Bits;
             sconst[b * a.CS + lane] = make_float4(sx, sy, __uint_as_float(adj), 0.f);
             __syncwarp(__activemask());
-            if (lane == 0) mbar_expect_tx(bar_s + 8 * b, (uint32_t)(n * a.L * 8));
+            if (lane == 0) mbar_expect_tx(bar_s + 8 * b, (uint32_t)(n * a.L * 8 * NF));
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp(__activemask());
-            bulk_g2s(dst, a.table + (size_t)m * a.TS + lo, (uint32_t)(a.L * 8), bar_s + 8 * b);
+            bulk_g2s(dst, a.table + ((size_t)m * a.TS + lo) * NF, (uint32_t)(a.L * 8 * NF),
+                     bar_s + 8 * b);
         }
     };
     if (warp == 0) {
@@ -148,19 +187,28 @@ __global__ void __launch_bounds__(kThreads, 4) bp_f32_kernel(BpArgs a) {
                 float u = sqrt_approx(fmaf(ex, ex, ey2));
                 if (CLAMP) u = fminf(u, a.qclamp);
                 const float tb = __fadd_rd(u, kTwo23);      // 2^23 + floor(u)
-                const float2 v = lds_f2(adj + (__float_as_uint(tb) << 3));
-                if (ATRICK) {
-                    // table {r[s-1] - s*D, D}:  value = (1-f) r[s0-1] + f r[s0] = u*D + A
-                    acc[k] = fmaf(u, v.y, acc[k]);
-                    acc2[k] += v.x;
+                const uint32_t ad = adj + (__float_as_uint(tb) << (3 + LG));
+                // ATRICK table {r[s-1] - s*D, D}: value = u*D + A; else value = f*D + r[s-1]
+                const float w = ATRICK ? u : u - (tb - kTwo23);
+                float A[NF], D[NF];
+                if (NF == 1) {
+                    const float2 v = lds_f2(ad);
+                    A[0] = v.x; D[0] = v.y;
                 } else {
-                    const float f = u - (tb - kTwo23);      // exact fraction
-                    acc[k] = fmaf(f, v.y, acc[k]);
-                    acc2[k] += v.x;
+#pragma unroll
+                    for (int h = 0; h < NF / 2; ++h) {
+                        const float4 v = lds_f4(ad + 16 * h);
+                        A[2 * h] = v.x; D[2 * h] = v.y; A[2 * h + 1] = v.z; D[2 * h + 1] = v.w;
+                    }
+                }
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    acc[k][f] = fmaf(w, D[f], acc[k][f]);
+                    acc2[k][f] += A[f];
                 }
             }
         }
-        // no CTA barrier: the last warp to finish with buffer b refills it (acq_rel counter)
+        // the last warp to finish with buffer b refills it (acq_rel shared counter)
         __syncwarp();
         uint32_t prev = 0;
         if (lane == 0) {
@@ -173,9 +221,10 @@ __global__ void __launch_bounds__(kThreads, 4) bp_f32_kernel(BpArgs a) {
             if (c + a.nbuf < nchunks) issue(c + a.nbuf, b);
         }
     }
-
 #pragma unroll
-    for (int k = 0; k < 4; ++k) acc[k] += acc2[k];
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int f = 0; f < NF; ++f) acc[k][f] += acc2[k][f];
 
     if (a.split > 1) {
         // publish this split's partial sums; the tile's last CTA combines them in order
@@ -183,7 +232,10 @@ __global__ void __launch_bounds__(kThreads, 4) bp_f32_kernel(BpArgs a) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int i = i0 + lx + 8 * k;
-                if (i < a.nx) a.gpart[(size_t)blockIdx.y * a.nx * a.ny + (size_t)j * a.nx + i] = acc[k];
+                if (i < a.nx)
+#pragma unroll
+                    for (int f = 0; f < NF; ++f)
+                        a.gpart[((size_t)blockIdx.y * NF + f) * P + (size_t)j * a.nx + i] = acc[k][f];
             }
         }
         if (!last_block(a.tile_cnt + tile, a.split, &last_flag)) return;
@@ -191,11 +243,14 @@ __global__ void __launch_bounds__(kThreads, 4) bp_f32_kernel(BpArgs a) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int i = i0 + lx + 8 * k;
-                float sum = 0.f;
-                if (i < a.nx)
-                    for (int q = 0; q < a.split; ++q)
-                        sum += __ldcg(a.gpart + (size_t)q * a.nx * a.ny + (size_t)j * a.nx + i);
-                acc[k] = sum;
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    float sum = 0.f;
+                    if (i < a.nx)
+                        for (int q = 0; q < a.split; ++q)
+                            sum += __ldcg(a.gpart + ((size_t)q * NF + f) * P + (size_t)j * a.nx + i);
+                    acc[k][f] = sum;
+                }
             }
         }
     }
@@ -205,78 +260,76 @@ __global__ void __launch_bounds__(kThreads, 4) bp_f32_kernel(BpArgs a) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int i = i0 + lx + 8 * k;
-                if (i < a.nx) a.out[(size_t)j * a.nx + i] = a.gscale * acc[k];
+                if (i < a.nx)
+#pragma unroll
+                    for (int f = 0; f < NF; ++f)
+                        a.out[f * P + (size_t)j * a.nx + i] = a.gscale * acc[k][f];
             }
         }
         return;
     }
 
-    // ---- fused update epilogue (recon.py:327-338) ----
-    const float* x = (iter & 1) ? a.xb1 : a.xb0;
-    float* xo = (iter & 1) ? a.xb0 : a.xb1;
-    const float eta = (float)a.prm->step, lam = (float)a.prm->eta_alpha;
-    const float beta = (float)a.prm->beta, eps = (float)a.prm->eps;
-    const float gsc = a.gscale;
+    // ---- fused update epilogue (recon.py:327-338), per frame ----
+    const float* xin = (iter & 1) ? a.xb1 : a.xb0;
+    float* xout = (iter & 1) ? a.xb0 : a.xb1;
+    const float eps = (float)a.prm->eps;
     const bool nonneg = a.prm->nonneg != 0;
-    float mx = 0.f, l1 = 0.f;
-    int bad = 0;
-    if (j < a.ny) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int i = i0 + lx + 8 * k;
-            if (i >= a.nx) continue;
-            const size_t p = (size_t)j * a.nx + i;
-            const float x0 = x[p];
-            float g = gsc * acc[k];
-            if (beta > 0.f) {
-                // recon.py:178-189, same accumulation order
-                const float e2 = eps * eps;
-                float t = 0.f;
-                if (i < a.nx - 1) { const float d = x[p + 1] - x0; t -= d / sqrtf(d * d + e2); }
-                if (i > 0) { const float d = x0 - x[p - 1]; t += d / sqrtf(d * d + e2); }
-                if (j < a.ny - 1) { const float d = x[p + a.nx] - x0; t -= d / sqrtf(d * d + e2); }
-                if (j > 0) { const float d = x0 - x[p - a.nx]; t += d / sqrtf(d * d + e2); }
-                g += beta * t;
+    for (int f = 0; f < NF; ++f) {
+        const bool live = !a.st->fr[f].stopped;
+        const float eta = (float)a.prm->step[f], lam = (float)a.prm->eta_alpha[f];
+        const float beta = (float)a.prm->beta[f];
+        const float* x = xin + f * P;
+        float* xo = xout + f * P;
+        float mx = 0.f, l1 = 0.f;
+        int bad = 0;
+        if (live && j < a.ny) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = i0 + lx + 8 * k;
+                if (i >= a.nx) continue;
+                const size_t p = (size_t)j * a.nx + i;
+                float g = a.gscale * acc[k][f];
+                if (beta > 0.f) g += beta * tv_grad_at<float>(x, p, i, j, a.nx, a.ny, eps * eps);
+                const float xn = prox<float>(x[p] - eta * g, lam, nonneg);
+                xo[p] = xn;
+                if (!isfinite(xn)) bad = 1;
+                mx = fmaxf(mx, fabsf(xn));
+                l1 += fabsf(xn);
             }
-            const float v = x0 - eta * g;
-            float mag = fabsf(v) - lam;
-            mag = (mag != mag) ? mag : fmaxf(mag, 0.f);     // np.maximum keeps NaN
-            float xn = (v > 0.f) ? mag : ((v < 0.f) ? -mag : (v != v ? v : 0.f));
-            if (nonneg) xn = (xn != xn) ? xn : fmaxf(xn, 0.f);
-            xo[p] = xn;
-            if (!isfinite(xn)) bad = 1;
-            mx = fmaxf(mx, fabsf(xn));
-            l1 += fabsf(xn);
         }
-    }
-    mx = block_max(mx, red_f);
-    const float l1b = block_sum(l1, red_f);
-    const int badb = __syncthreads_or(bad);
-    if (threadIdx.x == 0) {
-        double* pp = a.part + 4 * (size_t)tile;
-        pp[0] = mx;
-        pp[1] = l1b;
-        pp[2] = badb;
+        mx = block_max(mx, red_f);
+        const float l1b = block_sum(l1, red_f);
+        const int badb = __syncthreads_or(bad);
+        if (threadIdx.x == 0) {
+            double* pp = a.part + 4 * ((size_t)tile * NF + f);
+            pp[0] = mx;
+            pp[1] = l1b;
+            pp[2] = badb;
+        }
     }
     if (last_block(&a.st->cnt_bp, gridDim.x, &last_flag)) {
-        __shared__ double red_d[kThreads / 32];
-        double m2 = 0.0, s2 = 0.0, b2 = 0.0;
-        for (int q = threadIdx.x; q < (int)gridDim.x; q += kThreads) {
-            const double* pp = a.part + 4 * (size_t)q;
-            m2 = fmax(m2, pp[0]);
-            s2 += pp[1];
-            b2 += pp[2];
-        }
-        m2 = block_max(m2, red_d);
-        s2 = block_sum(s2, red_d);
-        b2 = block_sum(b2, red_d);
-        if (threadIdx.x == 0) {
-            a.st->maxabs = m2;
-            a.st->l1sum = s2;
-            a.st->nonfinite = b2 > 0.0 ? 1 : 0;
-            const double sc = (m2 > 0.0 && isfinite(m2)) ? ldexp(1.0, a.bits) / m2 : 0.0;
-            a.st->scale64 = sc;
-            a.st->scale32 = (float)sc;
+#pragma unroll 1
+        for (int f = 0; f < NF; ++f) {
+            double m2 = 0.0, s2 = 0.0, b2 = 0.0;
+            for (int q = threadIdx.x; q < (int)gridDim.x; q += kThreads) {
+                const double* pp = a.part + 4 * ((size_t)q * NF + f);
+                m2 = fmax(m2, pp[0]);
+                s2 += pp[1];
+                b2 += pp[2];
+            }
+            m2 = block_max(m2, red_d);
+            s2 = block_sum(s2, red_d);
+            b2 = block_sum(b2, red_d);
+            if (threadIdx.x == 0 && !a.st->fr[f].stopped) {
+                FrameState& fs = a.st->fr[f];
+                fs.maxabs = m2;
+                fs.l1sum = s2;
+                fs.nonfinite = b2 > 0.0 ? 1 : 0;
+                const double scl = (m2 > 0.0 && isfinite(m2)) ? ldexp(1.0, a.bits) / m2 : 0.0;
+                fs.scale64 = scl;
+                fs.scale32 = (float)scl;
+            }
         }
     }
 }
@@ -305,7 +358,7 @@ __global__ void __launch_bounds__(kThreads) bp_f64_kernel(BpArgs64 a) {
     __shared__ int last_flag;
     int iter = 0;
     if (EPI) {
-        if (a.st->stopped) return;
+        if (a.st->all_stopped) return;
         iter = a.st->iter;
     }
     const int p = blockIdx.x * kThreads + threadIdx.x;
@@ -331,26 +384,13 @@ __global__ void __launch_bounds__(kThreads) bp_f64_kernel(BpArgs64 a) {
     }
     const double* x = (iter & 1) ? a.xb1 : a.xb0;
     double* xo = (iter & 1) ? a.xb0 : a.xb1;
-    const double eta = a.prm->step, lam = a.prm->eta_alpha, beta = a.prm->beta, eps = a.prm->eps;
     double mx = 0.0, l1 = 0.0;
     int bad = 0;
     if (valid) {
-        const double x0 = x[p];
+        const double eps = a.prm->eps;
         double g = a.gscale * acc;
-        if (beta > 0.0) {
-            const double e2 = eps * eps;
-            double t = 0.0;
-            if (i < a.nx - 1) { const double d = x[p + 1] - x0; t -= d / sqrt(d * d + e2); }
-            if (i > 0) { const double d = x0 - x[p - 1]; t += d / sqrt(d * d + e2); }
-            if (j < a.ny - 1) { const double d = x[p + a.nx] - x0; t -= d / sqrt(d * d + e2); }
-            if (j > 0) { const double d = x0 - x[p - a.nx]; t += d / sqrt(d * d + e2); }
-            g += beta * t;
-        }
-        const double v = x0 - eta * g;
-        double mag = fabs(v) - lam;
-        mag = (mag != mag) ? mag : fmax(mag, 0.0);
-        double xn = (v > 0.0) ? mag : ((v < 0.0) ? -mag : (v != v ? v : 0.0));
-        if (a.prm->nonneg) xn = (xn != xn) ? xn : fmax(xn, 0.0);
+        if (a.prm->beta[0] > 0.0) g += a.prm->beta[0] * tv_grad_at<double>(x, p, i, j, a.nx, a.ny, eps * eps);
+        const double xn = prox<double>(x[p] - a.prm->step[0] * g, a.prm->eta_alpha[0], a.prm->nonneg != 0);
         xo[p] = xn;
         bad = !isfinite(xn);
         mx = fabs(xn);
@@ -377,12 +417,13 @@ __global__ void __launch_bounds__(kThreads) bp_f64_kernel(BpArgs64 a) {
         s2 = block_sum(s2, red_d);
         b2 = block_sum(b2, red_d);
         if (threadIdx.x == 0) {
-            a.st->maxabs = m2;
-            a.st->l1sum = s2;
-            a.st->nonfinite = b2 > 0.0 ? 1 : 0;
-            const double sc = (m2 > 0.0 && isfinite(m2)) ? ldexp(1.0, a.bits) / m2 : 0.0;
-            a.st->scale64 = sc;
-            a.st->scale32 = (float)sc;
+            FrameState& fs = a.st->fr[0];
+            fs.maxabs = m2;
+            fs.l1sum = s2;
+            fs.nonfinite = b2 > 0.0 ? 1 : 0;
+            const double scl = (m2 > 0.0 && isfinite(m2)) ? ldexp(1.0, a.bits) / m2 : 0.0;
+            fs.scale64 = scl;
+            fs.scale32 = (float)scl;
         }
     }
 }
@@ -391,45 +432,57 @@ __global__ void __launch_bounds__(kThreads) bp_f64_kernel(BpArgs64 a) {
 // K2 -- projector, fp32 with an exact fixed-point accumulator (deterministic).
 // CTA = (T x T pixel tile, 32 consecutive sensors); lane l of every warp owns sensor
 // g*32 + l, so a warp instruction is 1 pixel x 32 sensors.  Each lane scatters into its own
-// sensor's window with native 32-bit shared atomics; the window is stored slot-major
-// ([slot][32 lanes]) so lane l always hits bank l: conflict-free by construction.
+// sensor's windows with native 32-bit shared atomics; windows are stored slot-major
+// ([slot][frame][32 lanes]) so lane l always hits bank l: conflict-free by construction.
 // Contributions are integers:  xq = rint(x*scale),  a = rint(x*scale*f),  b = xq - a,
 // added at trace index s0 (weight f) and s0-1 (weight 1-f) -- forward.py:189-194.
-// Warps own whole image rows: a warp compacts its row's non-zero pixels (soft-threshold
-// zeros are skipped warp-uniformly) into a private record buffer, pads it to a multiple of
-// 8 with zero-weight records, and scatters 8 pixels per batch (8 independent chains: all
-// arithmetic first, then the 16 atomics).  Windows are flushed into the int64 trace
-// accumulator with RED.64 (integer adds commute: bitwise deterministic).
+// Warps own whole image rows: a warp compacts its row's pixels that are non-zero in any
+// frame (soft-threshold zeros are skipped warp-uniformly) into a private record buffer,
+// pads it to a multiple of 8 with zero-weight records, and scatters 8 pixels per batch
+// (8 independent chains: all arithmetic first, then the atomics).  Windows are flushed
+// into the int64 trace accumulator with RED.64 (integer adds commute: deterministic).
 // ===========================================================================
 struct FpArgs {
-    const float* x;       // [P] (nullptr: solver mode, use xb[(iter+1)&1])
+    const float* x;       // [NF][P] (nullptr: solver mode, use xb[(iter+1)&1])
     const float* xb0;
     const float* xb1;
     const float* pxs;
     const float* pys;
     const float* sxs;
     const float* sys;
-    long long* acc;       // [M][Q]
+    long long* acc;       // [NF][M][Q]
     int nx, ny, M, Q, T, L, tiles_x;
     float qclamp;
     DevState* st;
-    double* part_tv;      // solver mode: per-tile TV(x) partials (group 0 only)
+    double* part_tv;      // solver mode: per-(tile, frame) TV(x) partials (group 0 only)
     int solver;
 };
 
 constexpr int kFpBatch = 8;
 
-template <bool CLAMP>
-__global__ void __launch_bounds__(kThreads) fp_f32_kernel(FpArgs a) {
+// record of one pixel: px, then {x*scale, bits(rint(x*scale) + magic)} per frame
+template <int NF>
+struct FpRec {
+    static constexpr int kFloats = 1 + 2 * NF;
+    static constexpr int kVec = (kFloats + 3) / 4;  // float4 per record
+};
+
+template <int NF, bool CLAMP>
+__global__ void __launch_bounds__(kThreads, NF == 1 ? 4 : (NF == 2 ? 3 : 2)) fp_f32_kernel(FpArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ float red_f[kThreads / 32];
+    constexpr int LG = Lg<NF>::v;
+    constexpr int RV = FpRec<NF>::kVec;
     int iter = 0;
     if (a.solver) {
-        if (a.st->stopped) return;
+        if (a.st->all_stopped) return;
         iter = a.st->iter;
     }
     const float* x = a.x ? a.x : ((iter & 1) ? a.xb0 : a.xb1);  // bp wrote xb[(iter+1)&1]
-    const float scale = a.st->scale32;
+    const size_t P = (size_t)a.nx * a.ny;
+    float scale[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) scale[f] = a.st->fr[f].scale32;
     const int T = a.T;
     const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
     const int i0 = tx * T, j0 = ty * T;
@@ -438,12 +491,12 @@ __global__ void __launch_bounds__(kThreads) fp_f32_kernel(FpArgs a) {
     const bool sensor_ok = m < a.M;
     const float sx = __ldg(a.sxs + min(m, a.M - 1)), sy = __ldg(a.sys + min(m, a.M - 1));
 
-    // shared layout: win int32 [L][32] | per-warp row records float4 [8][T + kFpBatch]
+    // shared layout: win int32 [L][NF][32] | per-warp row records float4 [8][(T+8)*RV]
     int32_t* win = reinterpret_cast<int32_t*>(smem);
-    float4* rows = reinterpret_cast<float4*>(smem + (size_t)a.L * 32 * 4);
-    float4* rec = rows + (size_t)warp * (T + kFpBatch);
+    float4* rows = reinterpret_cast<float4*>(smem + (size_t)a.L * NF * 32 * 4);
+    float4* rec = rows + (size_t)warp * (T + kFpBatch) * RV;
 
-    for (int q = threadIdx.x; q < a.L * 32; q += kThreads) win[q] = 0;
+    for (int q = threadIdx.x; q < a.L * NF * 32; q += kThreads) win[q] = 0;
 
     // this lane's window: trace indices [lo, lo + L)
     const float X0 = __ldg(a.pxs + i0), X1 = __ldg(a.pxs + min(i0 + T - 1, a.nx - 1));
@@ -452,29 +505,35 @@ __global__ void __launch_bounds__(kThreads) fp_f32_kernel(FpArgs a) {
     float dmin = sqrtf((cx - sx) * (cx - sx) + (cy - sy) * (cy - sy));
     if (CLAMP) dmin = fminf(dmin, a.qclamp);
     const int lo = (int)floorf(dmin) - 2;
-    // word address of trace index t: win + 4*(32*(t - lo) + lane);  t = s0 <-> bits(tb)
-    const uint32_t adj = smem_u32(win) + 4u * (uint32_t)lane - 128u * (uint32_t)lo -
-                         128u * kTwo23Bits;
+    // word address of (trace index t, frame f): win + 4*(32*(NF*(t - lo) + f) + lane)
+    const uint32_t adj = smem_u32(win) + 4u * (uint32_t)lane - (128u * NF) * (uint32_t)lo -
+                         (128u * NF) * kTwo23Bits;
     __syncthreads();
 
-    float tv = 0.f;
+    float tv[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) tv[f] = 0.f;
     const bool do_tv = a.solver && blockIdx.y == 0;
     const int jend = min(T, a.ny - j0);
     // rows of this warp; the next row's pixels are loaded while the current row scatters
-    float xnext[2] = {0.f, 0.f};
-    auto load_row = [&](int r, float* dst) {
+    float xnext[NF][2];
+    auto load_row = [&](int r, float (*dst)[2]) {
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int ii = i0 + 32 * c + lane;
-            dst[c] = (32 * c < T && r < jend && ii < a.nx) ? x[(size_t)(j0 + r) * a.nx + ii] : 0.f;
-        }
+        for (int f = 0; f < NF; ++f)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int ii = i0 + 32 * c + lane;
+                dst[f][c] = (32 * c < T && r < jend && ii < a.nx)
+                                ? x[f * P + (size_t)(j0 + r) * a.nx + ii] : 0.f;
+            }
     };
     load_row(warp, xnext);
     for (int r = warp; r < jend; r += kThreads / 32) {
         const int jj = j0 + r;
-        const float xrow[2] = {xnext[0], xnext[1]};
+        float xrow[NF][2];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) { xrow[f][0] = xnext[f][0]; xrow[f][1] = xnext[f][1]; }
         load_row(r + kThreads / 32, xnext);
-        // compact the row's non-zero pixels: {px, x*scale, bits(rint(x*scale) + magic)}
         int cnt = 0;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -482,68 +541,113 @@ __global__ void __launch_bounds__(kThreads) fp_f32_kernel(FpArgs a) {
             if (cc >= T) break;
             const int ii = i0 + cc + lane;
             const bool in = ii < a.nx;
-            const float xv = xrow[c];
-            if (do_tv && in) {  // exact anisotropic TV partial, recon.py:169-170
-                if (ii + 1 < a.nx) tv += fabsf(x[(size_t)jj * a.nx + ii + 1] - xv);
-                if (jj + 1 < a.ny) tv += fabsf(x[(size_t)(jj + 1) * a.nx + ii] - xv);
+            bool nz = false;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                const float xv = xrow[f][c];
+                if (do_tv && in) {  // exact anisotropic TV partial, recon.py:169-170
+                    const float* xf = x + f * P;
+                    if (ii + 1 < a.nx) tv[f] += fabsf(xf[(size_t)jj * a.nx + ii + 1] - xv);
+                    if (jj + 1 < a.ny) tv[f] += fabsf(xf[(size_t)(jj + 1) * a.nx + ii] - xv);
+                }
+                nz |= xv != 0.f;
             }
-            const bool nz = xv != 0.f;
             const uint32_t bal = __ballot_sync(0xffffffffu, nz);
             if (nz) {
-                const float xs = xv * scale;
-                rec[cnt + __popc(bal & ((1u << lane) - 1u))] =
-                    make_float4(__ldg(a.pxs + ii), xs, __int_as_float(__float_as_int(xs + kMagic)), 0.f);
+                float rv[4 * RV];
+                rv[0] = __ldg(a.pxs + ii);
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    const float xs = xrow[f][c] * scale[f];
+                    rv[1 + 2 * f] = xs;
+                    rv[2 + 2 * f] = __int_as_float(__float_as_int(xs + kMagic));
+                }
+#pragma unroll
+                for (int q = 1 + 2 * NF; q < 4 * RV; ++q) rv[q] = 0.f;
+                float4* dst = rec + (size_t)(cnt + __popc(bal & ((1u << lane) - 1u))) * RV;
+#pragma unroll
+                for (int v = 0; v < RV; ++v)
+                    dst[v] = make_float4(rv[4 * v], rv[4 * v + 1], rv[4 * v + 2], rv[4 * v + 3]);
             }
             cnt += __popc(bal);
         }
         if (cnt == 0) continue;  // warp-uniform
         const int cnt8 = (cnt + kFpBatch - 1) & ~(kFpBatch - 1);
-        if (lane < cnt8 - cnt)  // zero-weight padding (adds 0 at a valid window address)
-            rec[cnt + lane] = make_float4(X0, 0.f, __int_as_float(kMagicBits), 0.f);
+        if (lane < cnt8 - cnt) {  // zero-weight padding (adds 0 at a valid window address)
+            float rv[4 * RV];
+            rv[0] = X0;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                rv[1 + 2 * f] = 0.f;
+                rv[2 + 2 * f] = __int_as_float(kMagicBits);
+            }
+#pragma unroll
+            for (int q = 1 + 2 * NF; q < 4 * RV; ++q) rv[q] = 0.f;
+            float4* dst = rec + (size_t)(cnt + lane) * RV;
+#pragma unroll
+            for (int v = 0; v < RV; ++v)
+                dst[v] = make_float4(rv[4 * v], rv[4 * v + 1], rv[4 * v + 2], rv[4 * v + 3]);
+        }
         __syncwarp();
         if (sensor_ok) {
             const float ey = __ldg(a.pys + jj) - sy;
             const float ey2 = ey * ey;
             for (int k = 0; k < cnt8; k += kFpBatch) {
                 uint32_t ad[kFpBatch];
-                int32_t va[kFpBatch], vb[kFpBatch];
+                int32_t va[kFpBatch][NF], vb[kFpBatch][NF];
 #pragma unroll
                 for (int b = 0; b < kFpBatch; ++b) {
-                    const float4 q = rec[k + b];
-                    const float ex = q.x - sx;
+                    float rv[4 * RV];
+#pragma unroll
+                    for (int v = 0; v < RV; ++v) {
+                        const float4 q = rec[(size_t)(k + b) * RV + v];
+                        rv[4 * v] = q.x; rv[4 * v + 1] = q.y; rv[4 * v + 2] = q.z; rv[4 * v + 3] = q.w;
+                    }
+                    const float ex = rv[0] - sx;
                     float u = sqrt_approx(fmaf(ex, ex, ey2));
                     if (CLAMP) u = fminf(u, a.qclamp);
                     const float tb = __fadd_rd(u, kTwo23);
-                    const float f = u - (tb - kTwo23);
-                    const float fb = fmaf(q.y, f, kMagic);
-                    va[b] = __float_as_int(fb) - kMagicBits;        // weight f   -> s0
-                    vb[b] = __float_as_int(q.z) - __float_as_int(fb); // weight 1-f -> s0-1
-                    ad[b] = adj + (__float_as_uint(tb) << 7);
+                    const float fr = u - (tb - kTwo23);
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) {
+                        const float fb = fmaf(rv[1 + 2 * f], fr, kMagic);
+                        va[b][f] = __float_as_int(fb) - kMagicBits;                    // f   -> s0
+                        vb[b][f] = __float_as_int(rv[2 + 2 * f]) - __float_as_int(fb); // 1-f -> s0-1
+                    }
+                    ad[b] = adj + (__float_as_uint(tb) << (7 + LG));
                 }
 #pragma unroll
-                for (int b = 0; b < kFpBatch; ++b) {
-                    red_smem_s32(ad[b] - 128u, vb[b]);
-                    red_smem_s32(ad[b], va[b]);
-                }
+                for (int b = 0; b < kFpBatch; ++b)
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) {
+                        red_smem_s32(ad[b] - 128u * NF + 128u * f, vb[b][f]);
+                        red_smem_s32(ad[b] + 128u * f, va[b][f]);
+                    }
             }
         }
         __syncwarp();  // rec is rewritten by the next row
     }
     if (do_tv) {
-        const float tvb = block_sum(tv, red_f);
-        if (threadIdx.x == 0) a.part_tv[blockIdx.x] = tvb;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            const float tvb = block_sum(tv[f], red_f);
+            if (threadIdx.x == 0) a.part_tv[(size_t)blockIdx.x * NF + f] = tvb;
+        }
     }
     __syncthreads();
 
     // flush: slot-major rows, lane = sensor; only real trace indices 0..Q-1
     if (sensor_ok) {
-        long long* accm = a.acc + (size_t)m * a.Q;
         for (int k = warp; k < a.L; k += kThreads / 32) {
-            const int32_t v = win[k * 32 + lane];
             const int t = lo + k;
-            if (v != 0 && t >= 0 && t < a.Q)
-                atomicAdd(reinterpret_cast<unsigned long long*>(accm + t),
-                          (unsigned long long)(long long)v);
+            if (t < 0 || t >= a.Q) continue;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                const int32_t v = win[(k * NF + f) * 32 + lane];
+                if (v != 0)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(a.acc + ((size_t)f * a.M + m) * a.Q + t),
+                              (unsigned long long)(long long)v);
+            }
         }
     }
 }
@@ -569,11 +673,11 @@ __global__ void __launch_bounds__(kThreads) fp_f64_kernel(FpArgs64 a) {
     __shared__ double red_d[kThreads / 32];
     int iter = 0;
     if (a.solver) {
-        if (a.st->stopped) return;
+        if (a.st->all_stopped) return;
         iter = a.st->iter;
     }
     const double* x = a.x ? a.x : ((iter & 1) ? a.xb0 : a.xb1);
-    const double scale = a.st->scale64;
+    const double scale = a.st->fr[0].scale64;
     const int T = a.T;
     const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
     const int i0 = tx * T, j0 = ty * T;
@@ -658,10 +762,10 @@ __global__ void __launch_bounds__(kThreads) fp_f64_kernel(FpArgs64 a) {
     }
 }
 
-// Pair-table entry s from r[s-1] (rp) and r[s] (rc).  Plain layout {r[s-1], D}; the fp32
-// back-projector's "A-trick" layout {r[s-1] - s*D, D} lets it use the delay u directly
-// (value = fma(u, D, A)) instead of the fraction f = u - s0, saving two FADDs per pair.
-// A is formed in fp64 and rounded once.
+// Pair-table entry s from r[s-1] (rp) and r[s] (rc).  Plain layout {r[s-1], D}; the optional
+// fp32 "A-trick" layout {r[s-1] - s*D, D} lets the back-projector use the delay u directly
+// (value = fma(u, D, A)) instead of the fraction f = u - s0, saving two FADDs per pair at
+// the cost of cancellation error ~ s*ulp (opt-in, PK_BP_ATRICK=1).
 template <typename T>
 __device__ __forceinline__ typename std::conditional<sizeof(T) == 4, float2, double2>::type
 pair_entry(T rp, T rc, int s, int atrick) {
@@ -673,44 +777,45 @@ pair_entry(T rp, T rc, int s, int atrick) {
 }
 
 // ===========================================================================
-// K3 -- residual / finalize: one CTA per sensor.  r = w*acc/scale - y, acc := 0, pair table,
-// sum r^2; solver mode: last CTA evaluates the objective and the stopping rules.
+// K3 -- residual / finalize: one CTA per (sensor, frame).  r = w*acc/scale - y, acc := 0,
+// pair table, sum r^2; solver mode: the last CTA evaluates the objective and the stopping
+// rules of every frame.
 // ===========================================================================
 template <typename T>
 struct FinArgs {
-    long long* acc;
-    const T* y;          // may be null (plain projection); solver mode reads io->y
-    T* trace_out;        // may be null
-    typename std::conditional<sizeof(T) == 4, float2, double2>::type* table;
+    long long* acc;      // [NF][M][Q]
+    const T* y;          // [NF][M*Q]; may be null (plain projection); solver mode reads io->y
+    T* trace_out;        // [NF][M*Q]; may be null
+    typename std::conditional<sizeof(T) == 4, float2, double2>::type* table;  // [M][TS][NF]
     int M, Q, TS;
     double w;
-    int wscale_mode;     // unused
     DevState* st;
     const DevParams* prm;
     const DevIo* io;
-    double* part_r;      // [M]
-    const double* part_tv;
+    double* part_r;      // [NF][M]
+    const double* part_tv;  // [tiles][NF]
     int ntv;
-    double* sumsq_out;   // optional (pk_residual)
+    double* sumsq_out;   // optional [NF] (pk_residual)
     int solver;
-    int atrick;          // fp32 table layout {r[s-1] - s*D, D} (see pair_entry)
+    int atrick;
 };
 
-template <typename T>
+template <typename T, int NF>
 __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
-    using T2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
     extern __shared__ __align__(128) unsigned char smem[];
     T* tr = reinterpret_cast<T*>(smem);
     __shared__ double red_d[kThreads / 32];
+    __shared__ double data_s[NF], tv_s[NF];
     __shared__ int last_flag;
-    if (a.solver && a.st->stopped) return;
-    const int m = blockIdx.x;
-    const double sc = sizeof(T) == 4 ? (double)a.st->scale32 : a.st->scale64;
+    if (a.solver && a.st->all_stopped) return;
+    const int m = blockIdx.x, f = blockIdx.y;
+    const double sc = sizeof(T) == 4 ? (double)a.st->fr[f].scale32 : a.st->fr[f].scale64;
     const double wq = sc > 0.0 ? a.w / sc : 0.0;
     const T* y = a.solver ? reinterpret_cast<const T*>(a.io->y) : a.y;
-    long long* accm = a.acc + (size_t)m * a.Q;
-    const T* ym = y ? y + (size_t)m * a.Q : nullptr;
-    T* om = a.trace_out ? a.trace_out + (size_t)m * a.Q : nullptr;
+    const size_t MQ = (size_t)a.M * a.Q;
+    long long* accm = a.acc + (size_t)f * MQ + (size_t)m * a.Q;
+    const T* ym = y ? y + f * MQ + (size_t)m * a.Q : nullptr;
+    T* om = a.trace_out ? a.trace_out + f * MQ + (size_t)m * a.Q : nullptr;
     double ss = 0.0;
     // 4 samples per thread per step: all loads first (independent), then math and stores
     for (int s0 = 4 * threadIdx.x; s0 < a.Q; s0 += 4 * kThreads) {
@@ -748,141 +853,174 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
     for (int e = threadIdx.x; e < a.TS; e += kThreads) {
         const T rp = (e >= 1 && e - 1 < a.Q) ? tr[e - 1] : (T)0;
         const T rc = (e < a.Q) ? tr[e] : (T)0;
-        a.table[(size_t)m * a.TS + e] = pair_entry<T>(rp, rc, e, a.atrick);
+        a.table[((size_t)m * a.TS + e) * NF + f] = pair_entry<T>(rp, rc, e, a.atrick);
     }
     ss = block_sum(ss, red_d);
-    if (threadIdx.x == 0) a.part_r[m] = ss;
-    if (!last_block(&a.st->cnt_fin, gridDim.x, &last_flag)) return;
+    if (threadIdx.x == 0) a.part_r[(size_t)f * a.M + m] = ss;
+    if (!last_block(&a.st->cnt_fin, gridDim.x * gridDim.y, &last_flag)) return;
 
-    double data = 0.0, tvs = 0.0;
-    for (int q = threadIdx.x; q < a.M; q += kThreads) data += a.part_r[q];
-    data = block_sum(data, red_d);
-    if (a.solver) {
-        for (int q = threadIdx.x; q < a.ntv; q += kThreads) tvs += a.part_tv[q];
-        tvs = block_sum(tvs, red_d);
+#pragma unroll 1
+    for (int g = 0; g < NF; ++g) {
+        double d = 0.0, t = 0.0;
+        for (int q = threadIdx.x; q < a.M; q += kThreads) d += a.part_r[(size_t)g * a.M + q];
+        d = block_sum(d, red_d);
+        if (a.solver) {
+            for (int q = threadIdx.x; q < a.ntv; q += kThreads) t += a.part_tv[(size_t)q * NF + g];
+            t = block_sum(t, red_d);
+        }
+        if (threadIdx.x == 0) {
+            data_s[g] = d;
+            tv_s[g] = t;
+        }
     }
     if (threadIdx.x != 0) return;
-    if (a.sumsq_out) a.sumsq_out[0] = data;
+    if (a.sumsq_out)
+        for (int g = 0; g < NF; ++g) a.sumsq_out[g] = data_s[g];
     if (!a.solver) return;
-    // objective and stopping (recon.py:346-363)
+    // objective and stopping per frame (recon.py:346-363)
     DevState* st = a.st;
     const DevParams* prm = a.prm;
     const int it = st->iter;
-    const double l1 = prm->alpha * st->l1sum;
-    const double tv = prm->beta * tvs;
-    const double total = data + l1 + tv;
-    if (!isfinite(total) || st->nonfinite) {
-        st->stopped = 1;
-        st->stopped_by = PK_STOP_DIVERGENCE;
-    } else {
-        double* h = a.io->hist;
-        h[it] = total;
-        h[prm->iterations + it] = data;
-        h[2 * prm->iterations + it] = l1;
-        h[3 * prm->iterations + it] = tv;
-        st->accepted = it + 1;
-        st->grow = total > st->f_prev ? st->grow + 1 : 0;
-        if (st->grow >= kDivergenceStreak) {
-            st->stopped = 1;
-            st->stopped_by = PK_STOP_DIVERGENCE;
-        } else {
-            const double rel = fabs(total - st->f_prev) / fmax(fabs(st->f_prev), 1e-300);
-            st->f_prev = total;
-            if (prm->tolerance > 0.0 && rel < prm->tolerance) {
-                st->stopped = 1;
-                st->stopped_by = PK_STOP_TOLERANCE;
+    const int N = prm->iterations;
+    int all = 1;
+    for (int g = 0; g < NF; ++g) {
+        FrameState& fs = st->fr[g];
+        if (!fs.stopped) {
+            const double data = data_s[g];
+            const double l1 = prm->alpha[g] * fs.l1sum;
+            const double tv = prm->beta[g] * tv_s[g];
+            const double total = data + l1 + tv;
+            if (!isfinite(total) || fs.nonfinite) {
+                fs.stopped = 1;
+                fs.stopped_by = PK_STOP_DIVERGENCE;
+            } else {
+                double* h = a.io->hist + (size_t)g * 4 * N;
+                h[it] = total;
+                h[N + it] = data;
+                h[2 * N + it] = l1;
+                h[3 * N + it] = tv;
+                fs.accepted = it + 1;
+                fs.grow = total > fs.f_prev ? fs.grow + 1 : 0;
+                if (fs.grow >= kDivergenceStreak) {
+                    fs.stopped = 1;
+                    fs.stopped_by = PK_STOP_DIVERGENCE;
+                } else {
+                    const double rel = fabs(total - fs.f_prev) / fmax(fabs(fs.f_prev), 1e-300);
+                    fs.f_prev = total;
+                    if (prm->tolerance > 0.0 && rel < prm->tolerance) {
+                        fs.stopped = 1;
+                        fs.stopped_by = PK_STOP_TOLERANCE;
+                    }
+                }
             }
         }
+        all &= fs.stopped;
+        a.io->status[2 * g] = fs.accepted;
+        a.io->status[2 * g + 1] = fs.stopped_by;
     }
     st->iter = it + 1;
-    if (st->iter >= prm->iterations) st->stopped = 1;
-    a.io->status[0] = st->accepted;
-    a.io->status[1] = st->stopped_by;
+    st->all_stopped = (all || st->iter >= N) ? 1 : 0;
 }
 
 // ===========================================================================
-// pair table from a trace: table[m][s] = {sign*y[s-1], sign*(y[s]-y[s-1])}.
-// Solver init mode (sign = -1, r0 = -y): last block writes f_prev = sum y^2 and resets state.
+// pair table from a trace: table[m][s][f] = {sign*y[s-1], sign*(y[s]-y[s-1])}.
+// Solver init mode (sign = -1, r0 = -y): the last block writes f_prev = sum y^2 per frame.
+// Grid (M, NF).
 // ===========================================================================
-template <typename T>
+template <typename T, int NF>
 __global__ void __launch_bounds__(kThreads) table_kernel(
     const T* y_direct, const DevIo* io, typename std::conditional<sizeof(T) == 4, float2, double2>::type* table,
     int M, int Q, int TS, T sign, double* part, DevState* st, int init, int atrick) {
-    using T2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
     __shared__ double red_d[kThreads / 32];
     __shared__ int last_flag;
     const T* y = y_direct ? y_direct : reinterpret_cast<const T*>(io->y);
-    const int m = blockIdx.x;
-    const T* ym = y + (size_t)m * Q;
+    const int m = blockIdx.x, f = blockIdx.y;
+    const T* ym = y + (size_t)f * M * Q + (size_t)m * Q;
     double ss = 0.0;
     for (int e = threadIdx.x; e < TS; e += kThreads) {
         const T rp = (e >= 1 && e - 1 < Q) ? sign * ym[e - 1] : (T)0;
         const T rc = (e < Q) ? sign * ym[e] : (T)0;
-        table[(size_t)m * TS + e] = pair_entry<T>(rp, rc, e, atrick);
+        table[((size_t)m * TS + e) * NF + f] = pair_entry<T>(rp, rc, e, atrick);
         if (e < Q) ss += (double)rc * (double)rc;
     }
     if (!init) return;
     ss = block_sum(ss, red_d);
-    if (threadIdx.x == 0) part[m] = ss;
-    if (!last_block(&st->cnt_misc, gridDim.x, &last_flag)) return;
-    double tot = 0.0;
-    for (int q = threadIdx.x; q < M; q += kThreads) tot += part[q];
-    tot = block_sum(tot, red_d);
-    if (threadIdx.x == 0) st->f_prev = tot;
-}
-
-// solver state reset + x0 = 0 (recon.py:318-320)
-template <typename T>
-__global__ void init_kernel(T* xb0, int P, DevState* st, const DevIo* io) {
-    const int p = blockIdx.x * kThreads + threadIdx.x;
-    if (p < P) xb0[p] = (T)0;
-    if (p == 0) {
-        st->iter = 0;
-        st->accepted = 0;
-        st->stopped = 0;
-        st->stopped_by = PK_STOP_MAX_ITERATIONS;
-        st->grow = 0;
-        st->nonfinite = 0;
-        io->status[0] = 0;
-        io->status[1] = PK_STOP_MAX_ITERATIONS;
+    if (threadIdx.x == 0) part[(size_t)f * M + m] = ss;
+    if (!last_block(&st->cnt_misc, gridDim.x * gridDim.y, &last_flag)) return;
+#pragma unroll 1
+    for (int g = 0; g < NF; ++g) {
+        double tot = 0.0;
+        for (int q = threadIdx.x; q < M; q += kThreads) tot += part[(size_t)g * M + q];
+        tot = block_sum(tot, red_d);
+        if (threadIdx.x == 0) st->fr[g].f_prev = tot;
     }
 }
 
-// x_out := the last accepted iterate
-template <typename T>
-__global__ void copy_out_kernel(const T* xb0, const T* xb1, const DevState* st, const DevIo* io,
-                                int P) {
-    const T* src = (st->accepted & 1) ? xb1 : xb0;
-    T* dst = reinterpret_cast<T*>(io->x_out);
-    for (int p = blockIdx.x * kThreads + threadIdx.x; p < P; p += gridDim.x * kThreads)
-        dst[p] = src[p];
+// solver state reset + x0 = 0 (recon.py:318-320)
+template <typename T, int NF>
+__global__ void init_kernel(T* xb0, int P, DevState* st, const DevIo* io) {
+    for (int p = blockIdx.x * kThreads + threadIdx.x; p < NF * P; p += gridDim.x * kThreads)
+        xb0[p] = (T)0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->iter = 0;
+        st->all_stopped = 0;
+        for (int g = 0; g < NF; ++g) {
+            FrameState& fs = st->fr[g];
+            fs.accepted = 0;
+            fs.stopped = 0;
+            fs.stopped_by = PK_STOP_MAX_ITERATIONS;
+            fs.grow = 0;
+            fs.nonfinite = 0;
+            io->status[2 * g] = 0;
+            io->status[2 * g + 1] = PK_STOP_MAX_ITERATIONS;
+        }
+    }
 }
 
-// max|x| -> fixed-point scale of the projector (standalone products)
+// x_out[f] := the last accepted iterate of frame f
+template <typename T, int NF>
+__global__ void copy_out_kernel(const T* xb0, const T* xb1, const DevState* st, const DevIo* io,
+                                int P) {
+    T* dst = reinterpret_cast<T*>(io->x_out);
+    for (int f = 0; f < NF; ++f) {
+        const T* src = ((st->fr[f].accepted & 1) ? xb1 : xb0) + (size_t)f * P;
+        for (int p = blockIdx.x * kThreads + threadIdx.x; p < P; p += gridDim.x * kThreads)
+            dst[(size_t)f * P + p] = src[p];
+    }
+}
+
+// max|x| per frame -> fixed-point scale of the projector (standalone products); grid (B, NF)
 template <typename T>
 __global__ void __launch_bounds__(kThreads) maxabs_kernel(const T* x, int P, double* part,
                                                           DevState* st, int bits) {
     __shared__ double red_d[kThreads / 32];
     __shared__ int last_flag;
+    const int f = blockIdx.y;
+    const T* xf = x + (size_t)f * P;
     double mx = 0.0;
     for (int p = blockIdx.x * kThreads + threadIdx.x; p < P; p += gridDim.x * kThreads)
-        mx = fmax(mx, fabs((double)x[p]));
+        mx = fmax(mx, fabs((double)xf[p]));
     mx = block_max(mx, red_d);
-    if (threadIdx.x == 0) part[blockIdx.x] = mx;
-    if (!last_block(&st->cnt_misc, gridDim.x, &last_flag)) return;
-    double m2 = 0.0;
-    for (int q = threadIdx.x; q < (int)gridDim.x; q += kThreads) m2 = fmax(m2, part[q]);
-    m2 = block_max(m2, red_d);
-    if (threadIdx.x == 0) {
-        st->maxabs = m2;
-        const double sc = (m2 > 0.0 && isfinite(m2)) ? ldexp(1.0, bits) / m2 : 0.0;
-        st->scale64 = sc;
-        st->scale32 = (float)sc;
+    if (threadIdx.x == 0) part[(size_t)f * gridDim.x + blockIdx.x] = mx;
+    if (!last_block(&st->cnt_misc, gridDim.x * gridDim.y, &last_flag)) return;
+#pragma unroll 1
+    for (int g = 0; g < (int)gridDim.y; ++g) {
+        double m2 = 0.0;
+        for (int q = threadIdx.x; q < (int)gridDim.x; q += kThreads)
+            m2 = fmax(m2, part[(size_t)g * gridDim.x + q]);
+        m2 = block_max(m2, red_d);
+        if (threadIdx.x == 0) {
+            FrameState& fs = st->fr[g];
+            fs.maxabs = m2;
+            const double sc = (m2 > 0.0 && isfinite(m2)) ? ldexp(1.0, bits) / m2 : 0.0;
+            fs.scale64 = sc;
+            fs.scale32 = (float)sc;
+        }
     }
 }
 
 // ===========================================================================
-// sharded update (recon.py:330-338 on an all-reduced gradient) and its sums
+// sharded update (recon.py:330-338 on an all-reduced gradient) and its sums (NF = 1)
 // ===========================================================================
 template <typename T>
 __global__ void __launch_bounds__(kThreads) grad_update_kernel(const T* x, const T* grad, T* xo,
@@ -891,24 +1029,10 @@ __global__ void __launch_bounds__(kThreads) grad_update_kernel(const T* x, const
     const int p = blockIdx.x * kThreads + threadIdx.x;
     if (p >= nx * ny) return;
     const int i = p % nx, j = p / nx;
-    const T x0 = x[p];
     T g = grad[p];
-    const T beta = (T)prm->beta, eps = (T)prm->eps, eta = (T)prm->step, lam = (T)prm->eta_alpha;
-    if (beta > (T)0) {
-        const T e2 = eps * eps;
-        T t = 0;
-        if (i < nx - 1) { const T d = x[p + 1] - x0; t -= d / sqrt(d * d + e2); }
-        if (i > 0) { const T d = x0 - x[p - 1]; t += d / sqrt(d * d + e2); }
-        if (j < ny - 1) { const T d = x[p + nx] - x0; t -= d / sqrt(d * d + e2); }
-        if (j > 0) { const T d = x0 - x[p - nx]; t += d / sqrt(d * d + e2); }
-        g += beta * t;
-    }
-    const T v = x0 - eta * g;
-    T mag = fabs(v) - lam;
-    mag = (mag != mag) ? mag : fmax(mag, (T)0);
-    T xn = (v > (T)0) ? mag : ((v < (T)0) ? -mag : (v != v ? v : (T)0));
-    if (prm->nonneg) xn = (xn != xn) ? xn : fmax(xn, (T)0);
-    xo[p] = xn;
+    const T beta = (T)prm->beta[0], eps = (T)prm->eps;
+    if (beta > (T)0) g += beta * tv_grad_at<T>(x, p, i, j, nx, ny, eps * eps);
+    xo[p] = prox<T>(x[p] - (T)prm->step[0] * g, (T)prm->eta_alpha[0], prm->nonneg != 0);
 }
 
 template <typename T>

@@ -62,10 +62,12 @@ def _require_cuda(device: int):
 class DeviceOperator:
     """K restricted to sensors [sensor_begin, sensor_end) of a ring, on one device."""
 
-    def __init__(self, grid, ring, acoustic, pool: CudaPool, sensor_begin=0, sensor_end=None):
+    def __init__(self, grid, ring, acoustic, pool: CudaPool, sensor_begin=0, sensor_end=None,
+                 frames: int = 1):
         _require_cuda(pool.device)
         lib = N.load()
         self.grid, self.ring, self.acoustic, self.pool = grid, ring, acoustic, pool
+        self.frames = int(frames)
         M = int(ring.count)
         self.sensor_begin = int(sensor_begin)
         self.sensor_end = M if sensor_end is None else int(sensor_end)
@@ -80,7 +82,7 @@ class DeviceOperator:
             sensors=M, sensor_xy=pos.ctypes.data_as(dp),
             sensor_begin=self.sensor_begin, sensor_end=self.sensor_end,
             samples=int(acoustic.q_s), c=float(acoustic.c), dt=float(acoustic.dt),
-            dtype=pool.pk_dtype, device=pool.device,
+            dtype=pool.pk_dtype, device=pool.device, frames=self.frames,
         )
         handle = ctypes.c_void_p()
         N.check(lib.pk_plan_create(ctypes.byref(desc), ctypes.byref(handle)))
@@ -142,9 +144,9 @@ class DeviceOperator:
     def matvec(self, x):
         """(K x) restricted to this operator's sensors, as a device tensor."""
         xt = self.tensor(x)
-        if xt.numel() != self.pixels:
+        if xt.numel() != self.pixels * self.frames:
             raise ValueError(f"matrix has {self.pixels} columns but vector has {xt.numel()}")
-        out = self.empty(self.sensors * self.samples)
+        out = self.empty(self.sensors * self.samples * self.frames)
         with _torch().cuda.device(self.device):
             N.check(self._lib.pk_matvec(self._h, xt.data_ptr(), out.data_ptr(), self.stream()))
         return out
@@ -152,11 +154,11 @@ class DeviceOperator:
     def adjoint(self, y, scale: float = 1.0):
         """scale * K^T y for y on this operator's sensors, as a device tensor."""
         yt = self.tensor(y)
-        if yt.numel() != self.sensors * self.samples:
+        if yt.numel() != self.sensors * self.samples * self.frames:
             raise ValueError(
                 f"matrix has {self.sensors * self.samples} rows but signal has {yt.numel()} values"
             )
-        out = self.empty(self.pixels)
+        out = self.empty(self.pixels * self.frames)
         with _torch().cuda.device(self.device):
             N.check(self._lib.pk_adjoint_matvec(self._h, yt.data_ptr(), out.data_ptr(),
                                                 float(scale), self.stream()))
@@ -166,15 +168,15 @@ class DeviceOperator:
         """(r = K x - y, sum r^2 as a 1-element fp64 device tensor); keeps r for adjoint_residual."""
         torch = _torch()
         xt, yt = self.tensor(x), self.tensor(y)
-        r = self.empty(self.sensors * self.samples)
-        ss = torch.empty(1, device=self.device, dtype=torch.float64)
+        r = self.empty(self.sensors * self.samples * self.frames)
+        ss = torch.empty(self.frames, device=self.device, dtype=torch.float64)
         with torch.cuda.device(self.device):
             N.check(self._lib.pk_residual(self._h, xt.data_ptr(), yt.data_ptr(), r.data_ptr(),
                                           ss.data_ptr(), self.stream()))
         return r, ss
 
     def adjoint_residual(self, scale: float = 1.0):
-        out = self.empty(self.pixels)
+        out = self.empty(self.pixels * self.frames)
         with _torch().cuda.device(self.device):
             N.check(self._lib.pk_adjoint_residual(self._h, out.data_ptr(), float(scale),
                                                   self.stream()))
@@ -191,32 +193,47 @@ class DeviceOperator:
                                              self.stream()))
         return xo, sums
 
-    def reconstruct(self, y, params: "N.SolverParams"):
-        """Device-resident iterative_reconstruct; returns (x, history[4, N], status[2]) tensors."""
-        torch = _torch()
-        yt = self.tensor(y)
-        x = self.empty(self.pixels)
-        hist = torch.zeros(4 * params.iterations, device=self.device, dtype=torch.float64)
-        status = torch.zeros(2, device=self.device, dtype=torch.int32)
-        with torch.cuda.device(self.device):
-            N.check(self._lib.pk_reconstruct(self._h, ctypes.byref(params), yt.data_ptr(),
-                                             x.data_ptr(), hist.data_ptr(), status.data_ptr(),
-                                             self.stream()))
-        return x, hist.view(4, params.iterations), status
+    def _params(self, params):
+        """ctypes array of `frames` SolverParams (one struct is broadcast to all frames)."""
+        if isinstance(params, N.SolverParams):
+            params = [params] * self.frames
+        if len(params) != self.frames:
+            raise ValueError(f"need {self.frames} parameter sets, got {len(params)}")
+        arr = (N.SolverParams * self.frames)(*params)
+        return arr, int(params[0].iterations)
 
-    def reconstruct_host(self, y_host: np.ndarray, params: "N.SolverParams"):
+    def reconstruct(self, y, params):
+        """Device-resident iterative_reconstruct of the plan's `frames` frames.
+
+        y: [frames * M * Q] (frame-major).  Returns (x [frames, P], history [frames, 4, N],
+        status [frames, 2]) device tensors."""
+        torch = _torch()
+        arr, n = self._params(params)
+        yt = self.tensor(y)
+        F = self.frames
+        x = self.empty(self.pixels * F)
+        hist = torch.zeros(4 * n * F, device=self.device, dtype=torch.float64)
+        status = torch.zeros(2 * F, device=self.device, dtype=torch.int32)
+        with torch.cuda.device(self.device):
+            N.check(self._lib.pk_reconstruct(self._h, arr, yt.data_ptr(), x.data_ptr(),
+                                             hist.data_ptr(), status.data_ptr(), self.stream()))
+        return x.view(F, self.pixels), hist.view(F, 4, n), status.view(F, 2)
+
+    def reconstruct_host(self, y_host: np.ndarray, params):
         """The C-ABI host-buffer entry (pk_reconstruct_host): fp64 in, fp64 out, synchronous."""
+        arr, n = self._params(params)
+        F = self.frames
         y = np.ascontiguousarray(y_host, dtype=np.float64)
-        x = np.empty(self.pixels)
-        hist = np.empty(4 * params.iterations)
-        status = np.zeros(2, dtype=np.int32)
+        x = np.empty(self.pixels * F)
+        hist = np.empty(4 * n * F)
+        status = np.zeros(2 * F, dtype=np.int32)
         dp = ctypes.POINTER(ctypes.c_double)
         with _torch().cuda.device(self.device):
             N.check(self._lib.pk_reconstruct_host(
-                self._h, ctypes.byref(params), y.ctypes.data_as(dp), x.ctypes.data_as(dp),
+                self._h, arr, y.ctypes.data_as(dp), x.ctypes.data_as(dp),
                 hist.ctypes.data_as(dp), status.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                 self.stream()))
-        return x, hist.reshape(4, params.iterations), status
+        return x.reshape(F, self.pixels), hist.reshape(F, 4, n), status.reshape(F, 2)
 
     def index_dump(self, ma: int = 0, mb: int | None = None):
         """fp64 (s0, frac) for local sensors [ma, mb) as device tensors [(mb-ma), P]."""
@@ -235,8 +252,8 @@ _cache: dict = {}
 _cache_lock = threading.Lock()
 
 
-def _key(grid, ring, acoustic, pool, m0, m1):
-    return (
+def _key(grid, ring, acoustic, pool, m0, m1, frames=1):
+    return (int(frames),
         int(grid.nx), int(grid.ny), float(grid.dx), tuple(float(v) for v in grid.origin),
         int(ring.count), float(ring.radius), tuple(float(v) for v in ring.center),
         float(acoustic.c), float(acoustic.dt), int(acoustic.q_s),
@@ -244,14 +261,15 @@ def _key(grid, ring, acoustic, pool, m0, m1):
     )
 
 
-def operator_for(grid, ring, acoustic, pool: CudaPool, sensor_begin=0, sensor_end=None):
+def operator_for(grid, ring, acoustic, pool: CudaPool, sensor_begin=0, sensor_end=None,
+                 frames: int = 1):
     """Cached DeviceOperator for a geometry (plans are reused across calls and frames)."""
     m1 = int(ring.count) if sensor_end is None else int(sensor_end)
-    k = _key(grid, ring, acoustic, pool, sensor_begin, m1)
+    k = _key(grid, ring, acoustic, pool, sensor_begin, m1, frames)
     with _cache_lock:
         op = _cache.get(k)
         if op is None:
-            op = DeviceOperator(grid, ring, acoustic, pool, sensor_begin, m1)
+            op = DeviceOperator(grid, ring, acoustic, pool, sensor_begin, m1, frames)
             _cache[k] = op
         return op
 

@@ -37,6 +37,7 @@ __all__ = [
     "resolve_regularization",
     "resolve_config",
     "solver_params",
+    "reconstruct_frames",
     "rmse",
     "psnr",
 ]
@@ -374,11 +375,11 @@ def iterative_reconstruct(K, y, config: ReconConfig, grid=None, pool=None,
     if isinstance(op, DeviceOperator):
         params = solver_params(config, alpha, beta, eta)
         x, hist, status = op.reconstruct(y.values, params)
-        status = status.cpu().numpy()
+        status = status.cpu().numpy()[0]
         n = int(status[0])
-        h = hist.cpu().numpy()[:, :n].T
+        h = hist.cpu().numpy()[0][:, :n].T
         stopped_by = N.STOPPED_BY[int(status[1])]
-        xv = x.double().cpu().numpy()
+        xv = x[0].double().cpu().numpy()
     else:
         xv, h, stopped_by = _dense_loop(op, y.values, alpha, beta, eta, config, (g.ny, g.nx))
         n = h.shape[0]
@@ -414,3 +415,66 @@ def psnr(a: ImageField, b: ImageField, peak: float) -> float:
     if mse == 0:
         return math.inf
     return 10.0 * math.log10(peak * peak / mse)
+
+
+# ---------------------------------------------------------------------------
+# dynamic sequences: many frames on one geometry (BASELINE config 4)
+
+
+def reconstruct_frames(K, ys, config: ReconConfig, pool=None, batch: int = 4,
+                       pinned: tuple[float, float, float] | None = None) -> list[ReconResult]:
+    """iterative_reconstruct for a sequence of frames sharing one geometry.
+
+    Frames are solved ``batch`` at a time (1, 2 or 4) by plans that evaluate each
+    sensor-pixel delay once for the whole batch.  Each frame's result equals its
+    single-frame solve (per-frame alpha/beta/step, stopping rules and histories).
+    ``pinned`` = (alpha, beta, step) applies one calibration to every frame (config 4's
+    protocol: pinned once from frame 0); otherwise every frame is calibrated like
+    iterative_reconstruct does.
+    """
+    from .device import operator_for
+
+    pool = _as_pool(pool)
+    if batch not in (1, 2, 4):
+        raise ValueError(f"batch must be 1, 2 or 4, got {batch}")
+    if pool.dtype != "float32" and batch != 1:
+        raise ValueError("batched frames run in float32")
+    ys = list(ys)
+    if not ys:
+        return []
+    g = _grid_of(K, None)
+    for y in ys:
+        _check_pair(K, y)
+    prov = getattr(K, "provenance", {}) or {}
+    if not all(prov.get(k) is not None for k in ("grid", "ring", "acoustic")):
+        return [iterative_reconstruct(K, y, config, pool=pool) for y in ys]
+    cal = []
+    for y in ys:
+        if pinned is not None:
+            cal.append(tuple(float(v) for v in pinned))
+        else:
+            a, b = resolve_regularization(config, K, y, pool)
+            cal.append((a, b, _resolve_step(config, K, b, pool)))
+    out: list[ReconResult] = []
+    for s in range(0, len(ys), batch):
+        chunk = list(range(s, min(len(ys), s + batch)))
+        nb = batch if len(chunk) == batch else 1
+        groups = [chunk] if nb == batch else [[c] for c in chunk]
+        for grp in groups:
+            op = operator_for(prov["grid"], prov["ring"], prov["acoustic"], pool, frames=len(grp))
+            params = [solver_params(config, *cal[c]) for c in grp]
+            yv = np.concatenate([np.asarray(ys[c].values, dtype=np.float64) for c in grp])
+            x, hist, status = op.reconstruct(yv, params)
+            x = x.double().cpu().numpy()
+            hist = hist.cpu().numpy()
+            status = status.cpu().numpy()
+            for q, c in enumerate(grp):
+                n = int(status[q, 0])
+                h = hist[q][:, :n].T
+                out.append(ReconResult(
+                    image=ImageField(g, x[q]),
+                    objective_history=h[:, 0].copy(), data_term_history=h[:, 1].copy(),
+                    l1_history=h[:, 2].copy(), tv_history=h[:, 3].copy(),
+                    iterations_run=n, stopped_by=N.STOPPED_BY[int(status[q, 1])],
+                    alpha_used=cal[c][0], beta_used=cal[c][1], step_used=cal[c][2]))
+    return out

@@ -267,3 +267,42 @@ def test_reference_objects_accepted():
 
     y = pk.forward_project(RefLikeMatrix(), ph, pool=F64)
     assert rel(y.values, gold["y"]) <= 1e-13
+
+
+@pytest.mark.parametrize("batch", [2, 4])
+def test_batched_frames_match_single_frame(batch):
+    """Frames solved together (one delay evaluation per batch) equal their single solves."""
+    n, M, Q = 128, 128, 1024
+    g, ring, ac, ph0, K = scene(n, M, Q)
+    ys = [pk.forward_project(K, pk.make_vessel_phantom(g, s), pool=F64) for s in range(batch)]
+    ys[-1] = pk.SensorData("time", M, Q, 3.0 * ys[-1].values)  # different scale per frame
+    cfg = pk.ReconConfig(iterations=10)
+    singles = [pk.iterative_reconstruct(K, y, cfg, pool=F32) for y in ys]
+    many = pk.reconstruct_frames(K, ys, cfg, pool=F32, batch=batch)
+    for a, b in zip(singles, many):
+        assert b.iterations_run == a.iterations_run and b.stopped_by == a.stopped_by
+        assert rel(b.image.values, a.image.values) <= 1e-5
+        np.testing.assert_allclose(b.objective_history, a.objective_history, rtol=1e-5)
+
+
+def test_batched_frames_independent_stopping():
+    """A diverging frame stops alone; its batch-mates run all iterations (recon.py:349-358)."""
+    gold = golden(32, 16, 64, 3)
+    g, ring, ac, ph, K = scene(32, 16, 64, 3)
+    y = pk.SensorData("time", 16, 64, gold["y"])
+    alpha, beta, step = gold["pinned"]
+    cfg = pk.ReconConfig(alpha, beta, 10, step)
+    res = pk.reconstruct_frames(K, [y, y, y, y], cfg, pool=F32, batch=4,
+                                pinned=(alpha, beta, step))
+    assert all(r.iterations_run == 10 for r in res)
+    ref = pk.iterative_reconstruct(K, y, cfg, pool=F32)
+    for r in res:
+        assert rel(r.image.values, ref.image.values) <= 1e-6
+    # divergence in frame 2 only: per-frame step
+    op = pk.operator_for(g, ring, ac, F32, frames=4)
+    params = [pk.solver.solver_params(cfg, alpha, beta, step)] * 4
+    params[2] = pk.solver.solver_params(cfg, alpha, beta, 1e9)
+    x, hist, status = op.reconstruct(np.concatenate([gold["y"]] * 4), params)
+    st = status.cpu().numpy()
+    assert st[2, 1] == 2 and st[2, 0] < 10  # divergence
+    assert all(st[q, 0] == 10 and st[q, 1] == 0 for q in (0, 1, 3))
