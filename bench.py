@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--shard", default="sensors", choices=["sensors", "frames"])
     ap.add_argument("--frames", type=int, default=40, help="distinct frames cycled (> L2)")
+    ap.add_argument("--streams", type=int, default=4,
+                    help="independent plans on concurrent CUDA streams (frames in flight)")
     ap.add_argument("--batch", type=int, default=1, choices=[1, 2, 4],
                     help="frames reconstructed per launch sharing one delay evaluation")
     ap.add_argument("--no-e2e", action="store_true")
@@ -244,10 +246,14 @@ def main():
         launches_per_step = 1 + 3 * cfg.iterations + 3 * cfg.iterations  # residual(3)/bp/update(2)
     else:
         B = args.batch
-        op = pk.operator_for(grid, ring, ac, pk.CudaPool(local, "float32"), frames=B)
-        x_out = torch.empty(B * P, device=dev, dtype=torch.float32)
-        hist = torch.zeros(B * 4 * cfg.iterations, device=dev, dtype=torch.float64)
-        status = torch.zeros(2 * B, device=dev, dtype=torch.int32)
+        SS = max(1, args.streams)
+        ops = [pk.operator_for(grid, ring, ac, pk.CudaPool(local, "float32"), frames=B, slot=q)
+               for q in range(SS)]
+        op = ops[0]
+        streams = [torch.cuda.current_stream(dev)] + [torch.cuda.Stream(dev) for _ in range(SS - 1)]
+        x_outs = [torch.empty(B * P, device=dev, dtype=torch.float32) for _ in range(SS)]
+        hists = [torch.zeros(B * 4 * cfg.iterations, device=dev, dtype=torch.float64) for _ in range(SS)]
+        stats = [torch.zeros(2 * B, device=dev, dtype=torch.int32) for _ in range(SS)]
         params_arr = (N.SolverParams * B)(*([params] * B))
         # step inputs: B consecutive frames, contiguous [B][M*Q]
         n_steps_in = max(1, F // B)
@@ -257,9 +263,10 @@ def main():
         import ctypes
 
         def one_step(f):
-            N.check(lib.pk_reconstruct(op.handle, params_arr, Ystep[f % n_steps_in].data_ptr(),
-                                       x_out.data_ptr(), hist.data_ptr(), status.data_ptr(),
-                                       stream_ptr()))
+            q = f % SS
+            N.check(lib.pk_reconstruct(ops[q].handle, params_arr, Ystep[f % n_steps_in].data_ptr(),
+                                       x_outs[q].data_ptr(), hists[q].data_ptr(), stats[q].data_ptr(),
+                                       ctypes.c_void_p(streams[q].cuda_stream)))
         launches_per_step = 3 + 3 * cfg.iterations
 
     frame_base = rank * 7919  # different frames per rank in frames mode
@@ -283,8 +290,13 @@ def main():
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    side = [] if sensor_mode else streams[1:]
+    for st_ in side:  # side streams start after e0 and are joined before e1
+        st_.wait_event(e0)
     for k in range(args.steps):
         one_step(frame(args.warmup + k))
+    for st_ in side:
+        torch.cuda.current_stream(dev).wait_stream(st_)
     e1.record()
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -348,23 +360,31 @@ def main():
         yh = torch.empty((nF, B * M * Q), dtype=torch.float64, pin_memory=True)
         yh.copy_(Y[:nF * B].reshape(nF, B * M * Q).double().cpu())
         yh_np = yh.numpy()
-        xo = torch.empty(B * P, dtype=torch.float64, pin_memory=True).numpy()
-        hh = torch.empty(B * 4 * cfg.iterations, dtype=torch.float64, pin_memory=True).numpy()
-        sh = torch.empty(2 * B, dtype=torch.int32, pin_memory=True).numpy()
+        xo = [torch.empty(B * P, dtype=torch.float64, pin_memory=True).numpy() for _ in range(SS)]
+        hh = [torch.empty(B * 4 * cfg.iterations, dtype=torch.float64, pin_memory=True).numpy()
+              for _ in range(SS)]
+        sh = [torch.empty(2 * B, dtype=torch.int32, pin_memory=True).numpy() for _ in range(SS)]
         dp = ctypes.POINTER(ctypes.c_double)
         ip = ctypes.POINTER(ctypes.c_int32)
 
-        def host_step(f):
-            N.check(lib.pk_reconstruct_host(op.handle, params_arr,
-                                            yh_np[f].ctypes.data_as(dp), xo.ctypes.data_as(dp),
-                                            hh.ctypes.data_as(dp), sh.ctypes.data_as(ip), stream_ptr()))
+        def host_step(k):
+            # one plan per stream: H2D, solve and D2H of consecutive steps overlap across streams
+            q = k % SS
+            f = k % nF
+            N.check(lib.pk_reconstruct_host_async(
+                ops[q].handle, params_arr, yh_np[f].ctypes.data_as(dp), xo[q].ctypes.data_as(dp),
+                hh[q].ctypes.data_as(dp), sh[q].ctypes.data_as(ip), ctypes.c_void_p(streams[q].cuda_stream)))
         for k in range(args.warmup):
-            host_step(k % nF)
+            host_step(k)
         torch.cuda.synchronize(dev)
         ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ee0.record()
+        for st_ in streams[1:]:
+            st_.wait_event(ee0)
         for k in range(args.steps):
-            host_step(k % nF)
+            host_step(k)
+        for st_ in streams[1:]:
+            torch.cuda.current_stream(dev).wait_stream(st_)
         ee1.record()
         torch.cuda.synchronize(dev)
         ms_e2e = ee0.elapsed_time(ee1)
@@ -372,7 +392,7 @@ def main():
                "h2d_bytes_per_step": B * M * Q * 8,
                "d2h_bytes_per_step": B * (P * 8 + 4 * cfg.iterations * 8 + 8),
                "ms_per_step": ms_e2e / args.steps,
-               "path": "pk_reconstruct_host (C ABI, pinned fp64 host buffers)"}
+               "path": f"pk_reconstruct_host_async (C ABI, pinned fp64 host buffers, {SS} stream(s))"}
 
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
@@ -395,6 +415,7 @@ def main():
             "data": "synthetic: make_scene vessel phantoms (seed = frame), y = K x by the fp64 device projector",
             "config": {"workload": cfg.name, "image": f"{cfg.n}x{cfg.n}", "sensors": M, "samples": Q,
                        "iterations": cfg.iterations, "batch": B,
+                       "streams": 1 if sensor_mode else SS,
                        "parallelism": (f"sensor-shard x{world} + NCCL all-reduce" if sensor_mode
                                        else f"frames x{world}" if world > 1 else "single GPU"),
                        "l2": f"{F} distinct frames cycled ({F * M * Q * 4 / 2**20:.0f} MiB of y > 126 MB L2)",

@@ -130,6 +130,14 @@ int pk_reconstruct_host(pk_plan* plan, const pk_solver_params* params, const dou
                         double* x_out_host, double* history_host, int32_t* status_host,
                         void* stream);
 
+/* Asynchronous form of pk_reconstruct_host for streaming many frames: enqueues H2D, solve
+ * and D2H on `stream` and returns; the host buffers must stay valid (and should be pinned)
+ * until the stream has completed.  Plans are independent, so one plan per stream overlaps
+ * copies and kernels of consecutive frames. */
+int pk_reconstruct_host_async(pk_plan* plan, const pk_solver_params* params,
+                              const double* y_host, double* x_out_host, double* history_host,
+                              int32_t* status_host, void* stream);
+
 /* Sensor-sharded building block: given the globally reduced gradient
  * grad_dev = 2 K^T r (summed over all shards), apply recon.py:330-338
  *   x_out = S_{eta*alpha}(x - eta*(grad + beta*tv_grad(x)))   (+ max(.,0) if nonneg)

@@ -109,6 +109,8 @@ SYMBOLS = [
     ("pk_reconstruct", ctypes.c_int, [_vp, ctypes.POINTER(SolverParams), _vp, _vp, _vp, _vp, _vp]),
     ("pk_reconstruct_host", ctypes.c_int,
      [_vp, ctypes.POINTER(SolverParams), _dp, _dp, _dp, _ip, _vp]),
+    ("pk_reconstruct_host_async", ctypes.c_int,
+     [_vp, ctypes.POINTER(SolverParams), _dp, _dp, _dp, _ip, _vp]),
     ("pk_grad_update", ctypes.c_int, [_vp, ctypes.POINTER(SolverParams), _vp, _vp, _vp, _vp, _vp]),
     ("pk_residual", ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     ("pk_adjoint_residual", ctypes.c_int, [_vp, _vp, ctypes.c_double, _vp]),

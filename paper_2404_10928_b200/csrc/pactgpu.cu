@@ -724,9 +724,9 @@ int pk_reconstruct(pk_plan* p, const pk_solver_params* prm, const void* y, void*
     return PK_OK;
 }
 
-int pk_reconstruct_host(pk_plan* p, const pk_solver_params* prm, const double* y_host,
-                        double* x_out_host, double* hist_host, int32_t* status_host,
-                        void* stream) {
+int pk_reconstruct_host_async(pk_plan* p, const pk_solver_params* prm, const double* y_host,
+                              double* x_out_host, double* hist_host, int32_t* status_host,
+                              void* stream) {
     if (!p || !y_host || !x_out_host || !hist_host || !status_host)
         return fail(PK_ERR_INVALID, "NULL argument");
     PK_TRY(check_params(p, prm));
@@ -757,7 +757,15 @@ int pk_reconstruct_host(pk_plan* p, const pk_solver_params* prm, const double* y
     PK_CUDA(cudaMemcpyAsync(hist_host, p->hist_dev, (size_t)4 * prm[0].iterations * p->nf * 8,
                             cudaMemcpyDeviceToHost, s));
     PK_CUDA(cudaMemcpyAsync(status_host, p->status_dev, 8 * p->nf, cudaMemcpyDeviceToHost, s));
-    PK_CUDA(cudaStreamSynchronize(s));
+    return PK_OK;
+}
+
+int pk_reconstruct_host(pk_plan* p, const pk_solver_params* prm, const double* y_host,
+                        double* x_out_host, double* hist_host, int32_t* status_host,
+                        void* stream) {
+    PK_TRY(pk_reconstruct_host_async(p, prm, y_host, x_out_host, hist_host, status_host, stream));
+    DeviceGuard g(p->device);
+    PK_CUDA(cudaStreamSynchronize(S(stream)));
     return PK_OK;
 }
 

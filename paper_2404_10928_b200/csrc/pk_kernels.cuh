@@ -636,18 +636,35 @@ __global__ void __launch_bounds__(kThreads, NF == 1 ? 4 : (NF == 2 ? 3 : 2)) fp_
     }
     __syncthreads();
 
-    // flush: slot-major rows, lane = sensor; only real trace indices 0..Q-1
-    if (sensor_ok) {
-        for (int k = warp; k < a.L; k += kThreads / 32) {
-            const int t = lo + k;
-            if (t < 0 || t >= a.Q) continue;
+    // flush: each warp takes blocks of BS window slots, reads them row-wise (lane = sensor,
+    // conflict-free), transposes them through its (now free) record buffer with a padded
+    // stride, and issues the RED.64s sensor-major so that one warp instruction covers
+    // 32/BS sensors x BS consecutive trace samples (BS*8-byte runs instead of 32 scattered
+    // words).  Only real trace indices 0..Q-1 are flushed.
+    const int cap = (T + kFpBatch) * RV * 16;  // bytes of this warp's record buffer
+    const int bs = (32 * 9 * 4 <= cap) ? 8 : 4;
+    int32_t* scr = reinterpret_cast<int32_t*>(rec);
+    const int lanes_per_sensor = bs, sensors_per_step = 32 / bs;
+    const int sub = lane % lanes_per_sensor, grp = lane / lanes_per_sensor;
+    for (int k0 = warp * bs; k0 < a.L; k0 += (kThreads / 32) * bs) {
 #pragma unroll
-            for (int f = 0; f < NF; ++f) {
-                const int32_t v = win[(k * NF + f) * 32 + lane];
-                if (v != 0)
-                    atomicAdd(reinterpret_cast<unsigned long long*>(a.acc + ((size_t)f * a.M + m) * a.Q + t),
+        for (int f = 0; f < NF; ++f) {
+            for (int i = 0; i < bs; ++i) {
+                const int k = k0 + i;
+                scr[lane * (bs + 1) + i] = (k < a.L) ? win[(k * NF + f) * 32 + lane] : 0;
+            }
+            __syncwarp();
+            for (int r = 0; r < 32; r += sensors_per_step) {
+                const int ms = r + grp;                 // sensor (lane index) of this RED
+                const int lo_ms = __shfl_sync(0xffffffffu, lo, ms);
+                const int v = scr[ms * (bs + 1) + sub];
+                const int t = lo_ms + k0 + sub;
+                const int mg = blockIdx.y * 32 + ms;
+                if (v != 0 && mg < a.M && t >= 0 && t < a.Q && k0 + sub < a.L)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(a.acc + ((size_t)f * a.M + mg) * a.Q + t),
                               (unsigned long long)(long long)v);
             }
+            __syncwarp();
         }
     }
 }

@@ -252,8 +252,8 @@ _cache: dict = {}
 _cache_lock = threading.Lock()
 
 
-def _key(grid, ring, acoustic, pool, m0, m1, frames=1):
-    return (int(frames),
+def _key(grid, ring, acoustic, pool, m0, m1, frames=1, slot=0):
+    return (int(frames), int(slot),
         int(grid.nx), int(grid.ny), float(grid.dx), tuple(float(v) for v in grid.origin),
         int(ring.count), float(ring.radius), tuple(float(v) for v in ring.center),
         float(acoustic.c), float(acoustic.dt), int(acoustic.q_s),
@@ -262,10 +262,13 @@ def _key(grid, ring, acoustic, pool, m0, m1, frames=1):
 
 
 def operator_for(grid, ring, acoustic, pool: CudaPool, sensor_begin=0, sensor_end=None,
-                 frames: int = 1):
-    """Cached DeviceOperator for a geometry (plans are reused across calls and frames)."""
+                 frames: int = 1, slot: int = 0):
+    """Cached DeviceOperator for a geometry (plans are reused across calls and frames).
+
+    ``slot`` selects independent plans for the same geometry (one per CUDA stream when
+    frames are streamed concurrently)."""
     m1 = int(ring.count) if sensor_end is None else int(sensor_end)
-    k = _key(grid, ring, acoustic, pool, sensor_begin, m1, frames)
+    k = _key(grid, ring, acoustic, pool, sensor_begin, m1, frames, slot)
     with _cache_lock:
         op = _cache.get(k)
         if op is None:

@@ -239,7 +239,7 @@ def test_host_buffer_entry_matches_device_entry():
     x_d, hist_d, st_d = op.reconstruct(y.values, params)
     assert np.array_equal(x_h, x_d.double().cpu().numpy())
     assert np.array_equal(hist_h, hist_d.cpu().numpy())
-    assert list(st_h) == list(st_d.cpu().numpy())
+    assert np.array_equal(st_h, st_d.cpu().numpy())
 
 
 def test_back_project_point_localised():
