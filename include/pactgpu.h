@@ -83,6 +83,7 @@ typedef struct pk_plan_info {
     int64_t device_bytes;    /* workspace held by the plan */
     int32_t frames;          /* frames per call */
     int32_t bp_split;        /* sensor slices per back-projector tile */
+    int32_t symmetric;       /* 1: D4-symmetric scene, one delay per 8 pairs in the back-projector */
 } pk_plan_info;
 
 typedef struct pk_solver_params {

@@ -80,6 +80,7 @@ class PlanInfo(ctypes.Structure):
         ("device_bytes", ctypes.c_int64),
         ("frames", ctypes.c_int32),
         ("bp_split", ctypes.c_int32),
+        ("symmetric", ctypes.c_int32),
     ]
 
 

@@ -110,7 +110,7 @@ void free_plan(pk_plan* p) {
     void* ptrs[] = {p->pxs, p->pys, p->sxs, p->sys, p->px, p->py, p->sx, p->sy, p->table,
                     p->acc, p->xbuf[0], p->xbuf[1], p->ydev, p->y64, p->x64, p->hist_dev,
                     p->status_dev, p->part_bp, p->part_tv, p->part_r, p->part_misc, p->state,
-                    p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt};
+                    p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt, p->sym_tiles};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
@@ -134,6 +134,22 @@ void smem_kernels(std::vector<const void*>& v) {
     v.push_back((const void*)finalize_kernel<float, NF>);
 }
 
+template <int IW>
+void sym_kernels(std::vector<const void*>& v) {
+    v.push_back((const void*)bp_sym_f32_kernel<true, true, IW>);
+    v.push_back((const void*)bp_sym_f32_kernel<true, false, IW>);
+    v.push_back((const void*)bp_sym_f32_kernel<false, true, IW>);
+    v.push_back((const void*)bp_sym_f32_kernel<false, false, IW>);
+}
+
+template <int IW>
+void launch_sym(const BpSymArgs& A, dim3 grid, int smem, bool epi, bool clamp, cudaStream_t s) {
+    if (epi) { if (clamp) bp_sym_f32_kernel<true, true, IW><<<grid, kThreads, smem, s>>>(A);
+               else bp_sym_f32_kernel<true, false, IW><<<grid, kThreads, smem, s>>>(A); }
+    else { if (clamp) bp_sym_f32_kernel<false, true, IW><<<grid, kThreads, smem, s>>>(A);
+           else bp_sym_f32_kernel<false, false, IW><<<grid, kThreads, smem, s>>>(A); }
+}
+
 cudaError_t opt_in_smem(int device) {
     static bool done[64] = {};
     if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
@@ -145,6 +161,11 @@ cudaError_t opt_in_smem(int device) {
     smem_kernels<1>(ks);
     smem_kernels<2>(ks);
     smem_kernels<4>(ks);
+    sym_kernels<0>(ks);
+    sym_kernels<48>(ks);
+    sym_kernels<64>(ks);
+    sym_kernels<96>(ks);
+    sym_kernels<128>(ks);
     ks.push_back((const void*)fp_f64_kernel);
     ks.push_back((const void*)finalize_kernel<double, 1>);
     for (const void* k : ks)
@@ -229,6 +250,31 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
 template <int NF>
 void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_t s) {
     const bool clamp = p->max_delay >= (double)p->Q + 0.5;
+    if (p->dtype == PK_F32 && NF == 1 && p->sym) {
+        BpSymArgs A{};
+        BpArgs& a = A.b;
+        a.table = static_cast<const float2*>(p->table);
+        a.pxs = p->pxs; a.pys = p->pys; a.sxs = p->sxs; a.sys = p->sys;
+        a.nx = p->nx; a.ny = p->ny; a.M = p->M; a.Q = p->Q; a.TS = p->TS; a.L = p->sym_L;
+        a.CS = kSymCS; a.nbuf = p->sym_nbuf; a.tiles_x = 0;
+        a.qclamp = (float)p->Q + 1.5f;
+        a.out = static_cast<float*>(out);
+        a.gscale = (float)(gscale_mult * p->w);
+        a.xb0 = static_cast<float*>(p->xbuf[0]);
+        a.xb1 = static_cast<float*>(p->xbuf[1]);
+        a.prm = p->params; a.st = p->state; a.part = p->part_bp; a.bits = p->fp_bits;
+        a.split = p->sym_split; a.ms = p->sym_ms; a.gpart = p->bp_gpart; a.tile_cnt = p->bp_tile_cnt;
+        A.n = p->nx; A.tile_list = p->sym_tiles;
+        const dim3 grid(p->sym_ntiles, p->sym_split);
+        switch (p->sym_iw) {
+            case 48: launch_sym<48>(A, grid, p->sym_smem, epi, clamp, s); break;
+            case 64: launch_sym<64>(A, grid, p->sym_smem, epi, clamp, s); break;
+            case 96: launch_sym<96>(A, grid, p->sym_smem, epi, clamp, s); break;
+            case 128: launch_sym<128>(A, grid, p->sym_smem, epi, clamp, s); break;
+            default: launch_sym<0>(A, grid, p->sym_smem, epi, clamp, s); break;
+        }
+        return;
+    }
     if (p->dtype == PK_F32) {
         BpArgs a{};
         a.table = static_cast<const float2*>(p->table);
@@ -539,6 +585,57 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         free_plan(p);
         return fail(PK_ERR_UNSUPPORTED, "projector window too long (%d samples)", p->fp_L);
     }
+    // D4 symmetry of the scene (square grid centred on the ring centre, n even, M % 4 == 0):
+    // the back-projector then evaluates one delay per 8 sensor-pixel pairs (bp_sym_f32_kernel)
+    {
+        const char* ev = getenv("PK_SYM");
+        bool ok = (ev ? atoi(ev) != 0 : true) && p->dtype == PK_F32 && nf == 1 && p->M == p->Mall &&
+                  p->nx == p->ny && (p->nx % 2) == 0 && p->nx >= 2 * kSymTile && (p->M % 4) == 0;
+        const int n = p->nx;
+        double scl = 0.0;
+        for (int i = 0; ok && i < n; ++i) scl = std::max(scl, std::fabs(X[i]));
+        const double tolx = 1e-9 * std::max(scl, 1e-300);
+        for (int i = 0; ok && i < n; ++i)
+            if (std::fabs(X[i] + X[n - 1 - i]) > tolx || std::fabs(X[i] - Y[i]) > tolx) ok = false;
+        double R = 0.0;
+        for (int m = 0; ok && m < p->M; ++m) R = std::max(R, std::hypot(SP[2 * m], SP[2 * m + 1]));
+        const double tols = 1e-9 * std::max(R, 1e-300);
+        for (int m = 0; ok && m < p->M; ++m) {
+            const int q = p->M / 4;
+            const double sx = SP[2 * m], sy = SP[2 * m + 1];
+            const int mr = (m + q) % p->M, mf = (p->M - m) % p->M;
+            // rotation by 90 degrees (x, y) -> (-y, x) and reflection (x, y) -> (x, -y)
+            if (std::fabs(SP[2 * mr] + sy) > tols || std::fabs(SP[2 * mr + 1] - sx) > tols) ok = false;
+            if (std::fabs(SP[2 * mf] - sx) > tols || std::fabs(SP[2 * mf + 1] + sy) > tols) ok = false;
+        }
+        p->sym = ok ? 1 : 0;
+        if (p->sym) {
+            const int qt = (n / 2 + kSymTile - 1) / kSymTile;
+            std::vector<int> tl;
+            for (int tx = 0; tx < qt; ++tx)
+                for (int ty = 0; ty <= tx; ++ty) tl.push_back((tx << 16) | ty);
+            p->sym_ntiles = (int)tl.size();
+            p->sym_tile_host = tl;
+            p->sym_L = ((int)std::ceil(tile_diag(kSymTile)) + 7 + 1) & ~1;
+            if (p->sym_L > p->TS) p->sym_L = p->TS;
+            p->sym_iw = 0;
+            for (int iw : {48, 64, 96, 128})
+                if (p->sym_L <= iw) { p->sym_iw = iw; break; }
+            const int ws = p->sym_iw ? p->sym_iw : p->sym_L;
+            p->sym_nbuf = 3;
+            p->sym_smem = p->sym_nbuf * kSymCS * 8 * ws * 8 + p->sym_nbuf * kSymCS * 16 + p->sym_nbuf * 8;
+            if (p->sym_smem > 110 * 1024) {
+                p->sym_nbuf = 2;
+                p->sym_smem = p->sym_nbuf * kSymCS * 8 * ws * 8 + p->sym_nbuf * kSymCS * 16 + p->sym_nbuf * 8;
+            }
+            if (p->sym_smem > 200 * 1024) p->sym = 0;
+            int sp = 1;
+            while (p->sym_ntiles * sp < 4 * 148 && p->M / (2 * sp) >= 32) sp *= 2;
+            p->sym_ms = (p->M + sp - 1) / sp;
+            p->sym_ms = ((p->sym_ms + kSymCS - 1) / kSymCS) * kSymCS;
+            p->sym_split = (p->M + p->sym_ms - 1) / p->sym_ms;
+        }
+    }
     p->misc_blocks = std::max(1, std::min(1024, (p->P + kThreads - 1) / kThreads));
     if ((size_t)p->Q * tsize(p) > 200 * 1024) {
         free_plan(p);
@@ -567,13 +664,17 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     A(alloc(p, &p->acc, (size_t)p->M * p->Q * nf));
     A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[0]), (size_t)p->P * ts * nf));
     A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[1]), (size_t)p->P * ts * nf));
-    A(alloc(p, &p->part_bp, (size_t)4 * nf * std::max(p->bp_tiles_x * p->bp_tiles_y,
-                                                      (p->P + kThreads - 1) / kThreads)));
+    const int ntile_max = std::max(p->bp_tiles_x * p->bp_tiles_y, p->sym ? p->sym_ntiles : 0);
+    A(alloc(p, &p->part_bp, (size_t)4 * nf * std::max(ntile_max, (p->P + kThreads - 1) / kThreads)));
     A(alloc(p, &p->part_tv, (size_t)p->fp_tiles_x * p->fp_tiles_y * nf));
     A(alloc(p, &p->part_r, (size_t)p->M * nf));
     A(alloc(p, &p->part_misc, (size_t)4 * p->misc_blocks * nf));
-    if (p->bp_split > 1) A(alloc(p, &p->bp_gpart, (size_t)p->bp_split * p->P * nf));
-    A(alloc(p, &p->bp_tile_cnt, (size_t)p->bp_tiles_x * p->bp_tiles_y));
+    {
+        const int spmax = std::max(p->bp_split, p->sym ? p->sym_split : 1);
+        if (spmax > 1) A(alloc(p, &p->bp_gpart, (size_t)spmax * p->P * nf));
+    }
+    A(alloc(p, &p->bp_tile_cnt, (size_t)ntile_max));
+    if (p->sym) A(alloc(p, &p->sym_tiles, (size_t)p->sym_ntiles));
     A(alloc(p, &p->state, 1));
     A(alloc(p, &p->params, 1));
     A(alloc(p, &p->io, 1));
@@ -589,7 +690,10 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     if (e == cudaSuccess) e = cudaMemset(p->acc, 0, (size_t)p->M * p->Q * 8 * nf);
     if (e == cudaSuccess) e = cudaMemset(p->state, 0, sizeof(DevState));
     if (e == cudaSuccess)
-        e = cudaMemset(p->bp_tile_cnt, 0, sizeof(uint32_t) * p->bp_tiles_x * p->bp_tiles_y);
+        e = cudaMemset(p->bp_tile_cnt, 0, sizeof(uint32_t) * ntile_max);
+    if (e == cudaSuccess && p->sym)
+        e = cudaMemcpy(p->sym_tiles, p->sym_tile_host.data(), sizeof(int) * p->sym_ntiles,
+                       cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(p->table, 0, (size_t)p->M * p->TS * 2 * ts * nf);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);
     // opt every dynamic-smem kernel into the device maximum once per device (a per-plan
@@ -626,7 +730,8 @@ int pk_plan_get_info(const pk_plan* p, pk_plan_info* o) {
     o->fp_bits = p->fp_bits;
     o->device_bytes = p->device_bytes;
     o->frames = p->nf;
-    o->bp_split = p->bp_split;
+    o->bp_split = p->sym ? p->sym_split : p->bp_split;
+    o->symmetric = p->sym;
     return PK_OK;
 }
 

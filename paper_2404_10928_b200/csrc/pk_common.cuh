@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "pactgpu.h"
 
 namespace pk {
@@ -264,6 +266,11 @@ struct pk_plan {
     int bp_tiles_x = 0, bp_tiles_y = 0, bp_L = 0, bp_CS = 0, bp_nbuf = 0, bp_smem = 0;
     int bp_split = 1, bp_ms = 0;
     int bp_atrick = 0;  // fp32 pair-table layout {r[s-1] - s*D, D}
+    // D4-symmetric back-projector (bp_sym_f32_kernel)
+    int sym = 0, sym_ntiles = 0, sym_L = 0, sym_nbuf = 0, sym_smem = 0, sym_split = 1, sym_ms = 0;
+    int sym_iw = 0;  // compile-time image-window stride (slots), 0 = runtime
+    int* sym_tiles = nullptr;
+    std::vector<int> sym_tile_host;
     float* bp_gpart = nullptr;
     uint32_t* bp_tile_cnt = nullptr;
     // projector tiling

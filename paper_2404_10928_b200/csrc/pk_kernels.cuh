@@ -335,6 +335,263 @@ __global__ void __launch_bounds__(kThreads, NF == 1 ? 4 : (NF == 2 ? 3 : 2)) bp_
 }
 
 // ===========================================================================
+// K1s -- back-projector, fp32, for D4-symmetric scenes (square grid centred on the ring
+// centre, n even, M % 4 == 0 -- every BASELINE configuration).  The 8 elements g of the
+// dihedral group map a pair (pixel p, sensor m) to (g p, g m) with the same distance, so
+// one delay evaluation serves 8 pairs: a thread owns a representative pixel of the
+// fundamental triangle (i >= n/2, n/2 <= j <= i) and accumulates its 8 image pixels, each
+// against the image sensor g m.  Per pair: 7/8 geometry + LDS.64 + 2 accumulate ops.
+//   g:      0       1          2              3          4         5       6          7
+//   pixel: (i,j)  (n-1-j,i)  (n-1-i,n-1-j)  (j,n-1-i)  (i,n-1-j)  (j,i)  (n-1-i,j)  (n-1-j,n-1-i)
+//   sensor: m     m+M/4      m+M/2          m+3M/4     -m         M/4-m  M/2-m      3M/4-m
+// Diagonal representatives (i == j) have 4 distinct images (g = 0..3).
+// CTA = 16x16 representative pixels x a slice of the base sensors; chunks of 4 base
+// sensors = 32 image windows, one bulk copy per lane of the issuing warp.
+// ===========================================================================
+struct BpSymArgs {
+    BpArgs b;            // common arguments (table, coordinates, update, split buffers)
+    int n;               // grid side (nx == ny)
+    int qtiles;          // 16x16 tiles per side of the quadrant
+    const int* tile_list;  // [ntiles] packed (tx << 16 | ty) of triangle tiles
+};
+
+constexpr int kSymTile = 16;
+constexpr int kSymCS = 4;  // base sensors per chunk (x 8 images = 32 windows)
+
+__device__ __forceinline__ void sym_pixel(int g, int i, int j, int n, int& ig, int& jg) {
+    const int ri = n - 1 - i, rj = n - 1 - j;
+    switch (g) {
+        case 0: ig = i; jg = j; break;
+        case 1: ig = rj; jg = i; break;
+        case 2: ig = ri; jg = rj; break;
+        case 3: ig = j; jg = ri; break;
+        case 4: ig = i; jg = rj; break;
+        case 5: ig = j; jg = i; break;
+        case 6: ig = ri; jg = j; break;
+        default: ig = rj; jg = ri; break;
+    }
+}
+
+__device__ __forceinline__ int sym_sensor(int g, int m, int M) {
+    const int q = M >> 2;
+    int s;
+    switch (g) {
+        case 0: s = m; break;
+        case 1: s = m + q; break;
+        case 2: s = m + 2 * q; break;
+        case 3: s = m + 3 * q; break;
+        case 4: s = -m; break;
+        case 5: s = q - m; break;
+        case 6: s = 2 * q - m; break;
+        default: s = 3 * q - m; break;
+    }
+    s %= M;
+    return s < 0 ? s + M : s;
+}
+
+// IW > 0: image windows IW slots apart (compile-time, so the 8 image loads use immediate
+// offsets); IW == 0: a.L apart (runtime)
+template <bool EPI, bool CLAMP, int IW>
+__global__ void __launch_bounds__(kThreads, 4) bp_sym_f32_kernel(BpSymArgs A) {
+    const BpArgs& a = A.b;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ float red_f[kThreads / 32];
+    __shared__ double red_d[kThreads / 32];
+    __shared__ int last_flag;
+    __shared__ uint32_t done_cnt[8];
+
+    int iter = 0;
+    if (EPI) {
+        if (a.st->all_stopped) return;
+        iter = a.st->iter;
+    }
+    const int n = A.n, h = n >> 1;
+    const int tile = blockIdx.x;
+    const int packed = __ldg(A.tile_list + tile);
+    const int i0 = h + (packed >> 16) * kSymTile, j0 = h + (packed & 0xffff) * kSymTile;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int i = i0 + 8 * (warp & 1) + (lane & 7);
+    const int j = j0 + 4 * (warp >> 1) + (lane >> 3);
+    const bool rep = i < n && j < n && j <= i;  // a representative of the fundamental triangle
+    const int ng = (i == j) ? 4 : 8;
+    const int mbase = blockIdx.y * a.ms;
+    const int mcount = min(a.ms, a.M - mbase);
+    const size_t P = (size_t)n * n;
+
+    const float px = __ldg(a.pxs + min(i, n - 1)), py = __ldg(a.pys + min(j, n - 1));
+    float acc[8], acc2[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) acc[g] = acc2[g] = 0.f;
+
+    // windows [nbuf][kSymCS][8][L] float2 | sconst [nbuf][kSymCS] float4 | bars
+    const int WS = IW > 0 ? IW : a.L;  // window stride in slots
+    const size_t win_bytes = (size_t)a.nbuf * kSymCS * 8 * WS * 8;
+    float4* sconst = reinterpret_cast<float4*>(smem + win_bytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + win_bytes + (size_t)a.nbuf * kSymCS * 16);
+    const uint32_t win_s = smem_u32(smem);
+    const uint32_t bar_s = smem_u32(bars);
+    const uint32_t img_stride = (uint32_t)WS * 8u;  // bytes between the 8 image windows
+
+    const float X0 = __ldg(a.pxs + i0), X1 = __ldg(a.pxs + min(i0 + kSymTile - 1, n - 1));
+    const float Y0 = __ldg(a.pys + j0), Y1 = __ldg(a.pys + min(j0 + kSymTile - 1, n - 1));
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < a.nbuf; ++b) {
+            mbar_init(bar_s + 8 * b, 1);
+            done_cnt[b] = 0;
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    const int nchunks = (mcount + kSymCS - 1) / kSymCS;
+    // lane = (base sensor c = lane >> 3, image g = lane & 7): one bulk copy per lane
+    auto issue = [&](int c, int b) {
+        const int nb = min(kSymCS, mcount - c * kSymCS);
+        const int cs = lane >> 3, g = lane & 7;
+        const bool act = cs < nb;
+        int lo = 0;
+        const int m = mbase + c * kSymCS + min(cs, nb - 1);
+        const float sx = __ldg(a.sxs + m), sy = __ldg(a.sys + m);
+        {
+            const float cx = fminf(fmaxf(sx, X0), X1), cy = fminf(fmaxf(sy, Y0), Y1);
+            float dmin = sqrtf((cx - sx) * (cx - sx) + (cy - sy) * (cy - sy));
+            if (CLAMP) dmin = fminf(dmin, a.qclamp);
+            lo = (int)floorf(dmin) - 1;
+            lo = max(lo, 0) & ~1;
+            lo = min(lo, a.TS - a.L);
+        }
+        const uint32_t dst0 = win_s + (uint32_t)((b * kSymCS + cs) * 8) * img_stride;
+        if (act && g == 0)
+            sconst[b * kSymCS + cs] =
+                make_float4(sx, sy, __uint_as_float(dst0 - 8u * (uint32_t)lo - 8u * kTwo23Bits), 0.f);
+        __syncwarp();
+        if (lane == 0) mbar_expect_tx(bar_s + 8 * b, (uint32_t)(nb * 8 * a.L * 8));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (act) {
+            const int ms = sym_sensor(g, m, a.M);
+            bulk_g2s(dst0 + (uint32_t)g * img_stride, a.table + (size_t)ms * a.TS + lo,
+                     (uint32_t)(a.L * 8), bar_s + 8 * b);
+        }
+    };
+    if (warp == 0) {
+        for (int c = 0; c < min(a.nbuf, nchunks); ++c) issue(c, c);
+    }
+
+    for (int c = 0; c < nchunks; ++c) {
+        const int b = c % a.nbuf;
+        mbar_wait(bar_s + 8 * b, (uint32_t)((c / a.nbuf) & 1));
+        const int nb = min(kSymCS, mcount - c * kSymCS);
+        const float4* sc = sconst + b * kSymCS;
+        for (int s = 0; s < nb; ++s) {
+            const float4 q = sc[s];
+            const float ey = py - q.y;
+            const float ex = px - q.x;
+            float u = sqrt_approx(fmaf(ex, ex, ey * ey));
+            if (CLAMP) u = fminf(u, a.qclamp);
+            const float tb = __fadd_rd(u, kTwo23);
+            const float f = u - (tb - kTwo23);
+            const uint32_t ad = __float_as_uint(q.z) + (__float_as_uint(tb) << 3);
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                const float2 v = lds_f2(ad + (uint32_t)g * (IW > 0 ? (uint32_t)IW * 8u : img_stride));
+                acc[g] = fmaf(f, v.y, acc[g]);
+                acc2[g] += v.x;
+            }
+        }
+        __syncwarp();
+        uint32_t prev = 0;
+        if (lane == 0) {
+            const uint32_t addr = smem_u32(&done_cnt[b]);
+            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(prev) : "r"(addr) : "memory");
+        }
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == kThreads / 32 - 1) {
+            if (lane == 0) done_cnt[b] = 0;
+            if (c + a.nbuf < nchunks) issue(c + a.nbuf, b);
+        }
+    }
+    int pix[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        acc[g] += acc2[g];
+        int ig, jg;
+        sym_pixel(g, i, j, n, ig, jg);
+        pix[g] = (rep && g < ng) ? jg * n + ig : -1;
+    }
+
+    if (a.split > 1) {
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+            if (pix[g] >= 0) a.gpart[(size_t)blockIdx.y * P + pix[g]] = acc[g];
+        if (!last_block(a.tile_cnt + tile, a.split, &last_flag)) return;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            float sum = 0.f;
+            if (pix[g] >= 0)
+                for (int q = 0; q < a.split; ++q) sum += __ldcg(a.gpart + (size_t)q * P + pix[g]);
+            acc[g] = sum;
+        }
+    }
+    if (!EPI) {
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+            if (pix[g] >= 0) a.out[pix[g]] = a.gscale * acc[g];
+        return;
+    }
+    const float* x = (iter & 1) ? a.xb1 : a.xb0;
+    float* xo = (iter & 1) ? a.xb0 : a.xb1;
+    const float eta = (float)a.prm->step[0], lam = (float)a.prm->eta_alpha[0];
+    const float beta = (float)a.prm->beta[0], eps = (float)a.prm->eps;
+    const bool nonneg = a.prm->nonneg != 0;
+    float mx = 0.f, l1 = 0.f;
+    int bad = 0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        const int p = pix[g];
+        if (p < 0) continue;
+        float gr = a.gscale * acc[g];
+        if (beta > 0.f) gr += beta * tv_grad_at<float>(x, p, p % n, p / n, n, n, eps * eps);
+        const float xn = prox<float>(x[p] - eta * gr, lam, nonneg);
+        xo[p] = xn;
+        if (!isfinite(xn)) bad = 1;
+        mx = fmaxf(mx, fabsf(xn));
+        l1 += fabsf(xn);
+    }
+    mx = block_max(mx, red_f);
+    const float l1b = block_sum(l1, red_f);
+    const int badb = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+        double* pp = a.part + 4 * (size_t)tile;
+        pp[0] = mx;
+        pp[1] = l1b;
+        pp[2] = badb;
+    }
+    if (last_block(&a.st->cnt_bp, gridDim.x, &last_flag)) {
+        double m2 = 0.0, s2 = 0.0, b2 = 0.0;
+        for (int q = threadIdx.x; q < (int)gridDim.x; q += kThreads) {
+            const double* pp = a.part + 4 * (size_t)q;
+            m2 = fmax(m2, pp[0]);
+            s2 += pp[1];
+            b2 += pp[2];
+        }
+        m2 = block_max(m2, red_d);
+        s2 = block_sum(s2, red_d);
+        b2 = block_sum(b2, red_d);
+        if (threadIdx.x == 0 && !a.st->fr[0].stopped) {
+            FrameState& fs = a.st->fr[0];
+            fs.maxabs = m2;
+            fs.l1sum = s2;
+            fs.nonfinite = b2 > 0.0 ? 1 : 0;
+            const double scl = (m2 > 0.0 && isfinite(m2)) ? ldexp(1.0, a.bits) / m2 : 0.0;
+            fs.scale64 = scl;
+            fs.scale32 = (float)scl;
+        }
+    }
+}
+
+// ===========================================================================
 // K1 -- back-projector, fp64 validation mode: one pixel per thread, fp64 delay evaluated
 // exactly as the reference (forward.py:157-182), table read through the L1/L2 path.
 // ===========================================================================

@@ -306,3 +306,43 @@ def test_batched_frames_independent_stopping():
     st = status.cpu().numpy()
     assert st[2, 1] == 2 and st[2, 0] < 10  # divergence
     assert all(st[q, 0] == 10 and st[q, 1] == 0 for q in (0, 1, 3))
+
+
+def test_symmetric_and_generic_back_projectors_agree(monkeypatch):
+    """The D4-symmetric back-projector (one delay per 8 pairs) and the generic one give the
+    same products and reconstructions to fp32 rounding."""
+    g, ring, ac, ph, K = scene(128, 128, 1024)
+    rng = np.random.default_rng(3)
+    r = rng.standard_normal(128 * 1024)
+    out = {}
+    for sym in ("1", "0"):
+        monkeypatch.setenv("PK_SYM", sym)
+        pk.clear_plan_cache()
+        op = pk.operator_for(g, ring, ac, F32)
+        assert op.info.symmetric == int(sym)
+        y = pk.forward_project(K, ph, pool=F32)
+        res = pk.iterative_reconstruct(K, y, pk.ReconConfig(iterations=10), pool=F32)
+        out[sym] = (op.adjoint(r).double().cpu().numpy(), res.image.values)
+    pk.clear_plan_cache()
+    assert rel(out["1"][0], out["0"][0]) <= 2e-4
+    assert rel(out["1"][1], out["0"][1]) <= 2e-5
+
+
+@pytest.mark.parametrize("pool", [F32, F64], ids=["f32", "f64"])
+def test_non_symmetric_geometry_vs_oracle(oracle, pool):
+    """Off-centre ring and rectangular grid (generic kernels) against the fp64 oracle."""
+    g = pk.make_grid(96, 64, 1e-4, (-4.8e-3, -3.0e-3))
+    ring = pk.make_ring(60, 1.1e-2, (0.7e-3, -0.4e-3), g)
+    ac = pk.AcousticConfig(c=1500.0, dt=1.6e-7, q_s=160, q_n=160)
+    K = pk.build_time_matrix(g, ring, ac)
+    o = oracle.Operator(*g.axis_vectors(), ring.positions, ac.c, ac.dt, ac.q_s)
+    x = pk.make_vessel_phantom(g, 4).values
+    y = o.forward(x)
+    alpha, beta = oracle.resolve_regularization(o, y)
+    step = oracle.resolve_step(o, beta, 1e-3)
+    ref = oracle.reconstruct(o, y, alpha, beta, step, 10)
+    res = pk.iterative_reconstruct(K, pk.SensorData("time", 60, 160, y),
+                                   pk.ReconConfig(alpha, beta, 10, step), pool=pool)
+    assert pk.operator_for(g, ring, ac, pool).info.symmetric == 0
+    assert res.iterations_run == 10
+    assert rel(res.image.values, ref["image"]) <= IMG_TOL[pool.dtype]
