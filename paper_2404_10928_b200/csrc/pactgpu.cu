@@ -161,6 +161,7 @@ cudaError_t opt_in_smem(int device) {
     smem_kernels<1>(ks);
     smem_kernels<2>(ks);
     smem_kernels<4>(ks);
+    ks.push_back((const void*)fp_sym4_f32_kernel<false>);
     sym_kernels<0>(ks);
     sym_kernels<48>(ks);
     sym_kernels<64>(ks);
@@ -191,6 +192,21 @@ void launch_maxabs_t(pk_plan* p, const void* x, cudaStream_t s) {
 template <int NF>
 void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
     dim3 grid(p->fp_tiles_x * p->fp_tiles_y, p->fp_groups);
+    if (p->dtype == PK_F32 && NF == 1 && p->fsym) {
+        FpArgs a{};
+        a.x = static_cast<const float*>(x);
+        a.xb0 = static_cast<const float*>(p->xbuf[0]);
+        a.xb1 = static_cast<const float*>(p->xbuf[1]);
+        a.pxs = p->pxs; a.pys = p->pys; a.sxs = p->sxs; a.sys = p->sys;
+        a.acc = p->acc;
+        a.nx = p->nx; a.ny = p->ny; a.M = p->M; a.Q = p->Q; a.T = p->fsym_T; a.L = p->fsym_L;
+        a.tiles_x = p->fsym_qt;
+        a.qclamp = (float)p->Q + 1.5f;
+        a.st = p->state; a.part_tv = p->part_tv; a.solver = solver;
+        const dim3 g2(p->fsym_qt * p->fsym_qt, p->fp_groups);
+        fp_sym4_f32_kernel<false><<<g2, kThreads, p->fsym_smem, s>>>(a);
+        return;
+    }
     if (p->dtype == PK_F32) {
         FpArgs a{};
         a.x = static_cast<const float*>(x);
@@ -220,8 +236,9 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
 template <int NF>
 void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq, int solver,
                        cudaStream_t s) {
-    const size_t sm = (size_t)p->Q * tsize(p);
-    const dim3 grid(p->M, NF);
+    const int chunks = p->fin_chunks;
+    const size_t sm = (size_t)((p->Q + chunks - 1) / chunks + 1) * tsize(p);
+    const dim3 grid(p->M * chunks, NF);
     if (p->dtype == PK_F32) {
         FinArgs<float> a{};
         a.acc = p->acc; a.y = static_cast<const float*>(y);
@@ -229,9 +246,12 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
         a.table = static_cast<float2*>(p->table);
         a.M = p->M; a.Q = p->Q; a.TS = p->TS; a.w = p->w;
         a.st = p->state; a.prm = p->params; a.io = p->io; a.part_r = p->part_r;
-        a.part_tv = p->part_tv; a.ntv = p->fp_tiles_x * p->fp_tiles_y; a.sumsq_out = sumsq;
+        a.part_tv = p->part_tv;
+        a.ntv = (NF == 1 && p->fsym) ? p->fsym_qt * p->fsym_qt : p->fp_tiles_x * p->fp_tiles_y;
+        a.sumsq_out = sumsq;
         a.solver = solver;
         a.atrick = p->bp_atrick;
+        a.chunks = chunks;
         finalize_kernel<float, NF><<<grid, kThreads, sm, s>>>(a);
     } else {
         FinArgs<double> a{};
@@ -242,6 +262,7 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
         a.st = p->state; a.prm = p->params; a.io = p->io; a.part_r = p->part_r;
         a.part_tv = p->part_tv; a.ntv = p->fp_tiles_x * p->fp_tiles_y; a.sumsq_out = sumsq;
         a.solver = solver;
+        a.chunks = chunks;
         finalize_kernel<double, 1><<<grid, kThreads, sm, s>>>(a);
     }
 }
@@ -364,6 +385,8 @@ int launch_maxabs(pk_plan* p, const void* x, cudaStream_t s) {
     return PK_OK;
 }
 int launch_fp(pk_plan* p, const void* x, int solver, cudaStream_t s) {
+    // the fixed-point accumulator must be zero on entry (finalize only reads it)
+    PK_CUDA(cudaMemsetAsync(p->acc, 0, (size_t)p->M * p->Q * p->nf * sizeof(long long), s));
     PK_DISPATCH(launch_fp_t, p, x, solver, s);
     return PK_OK;
 }
@@ -622,18 +645,32 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             for (int iw : {48, 64, 96, 128})
                 if (p->sym_L <= iw) { p->sym_iw = iw; break; }
             const int ws = p->sym_iw ? p->sym_iw : p->sym_L;
-            p->sym_nbuf = 3;
-            p->sym_smem = p->sym_nbuf * kSymCS * 8 * ws * 8 + p->sym_nbuf * kSymCS * 16 + p->sym_nbuf * 8;
-            if (p->sym_smem > 110 * 1024) {
-                p->sym_nbuf = 2;
-                p->sym_smem = p->sym_nbuf * kSymCS * 8 * ws * 8 + p->sym_nbuf * kSymCS * 16 + p->sym_nbuf * 8;
-            }
+            // chunks are short (4 base sensors = 32 interactions per thread), so the TMA ring
+            // must be deep to cover the copy latency: as many buffers (<= 8) as fit 74 KB
+            const int per_buf = kSymCS * 8 * ws * 8 + kSymCS * 16 + 8;
+            p->sym_nbuf = std::max(2, std::min(8, (74 * 1024) / per_buf));
+            p->sym_smem = p->sym_nbuf * per_buf;
             if (p->sym_smem > 200 * 1024) p->sym = 0;
             int sp = 1;
             while (p->sym_ntiles * sp < 4 * 148 && p->M / (2 * sp) >= 32) sp *= 2;
             p->sym_ms = (p->M + sp - 1) / sp;
             p->sym_ms = ((p->sym_ms + kSymCS - 1) / kSymCS) * kSymCS;
             p->sym_split = (p->M + p->sym_ms - 1) / p->sym_ms;
+        }
+        // rotation-symmetric projector (4 windows per lane, quadrant tiles of 32 x 32)
+        const char* ev2 = getenv("PK_FSYM");
+        p->fsym = (p->sym && (ev2 ? atoi(ev2) != 0 : false)) ? 1 : 0;  // opt-in (slower)
+        if (p->fsym) {
+            p->fsym_T = 32;
+            p->fsym_qt = (n / 2 + p->fsym_T - 1) / p->fsym_T;
+            p->fsym_L = (int)std::ceil(tile_diag(p->fsym_T)) + 6;
+            p->fsym_smem = p->fsym_L * 4 * 32 * 4 + (kThreads / 32) * (p->fsym_T + kFpBatch) * 3 * 16;
+            if (p->fsym_smem > 110 * 1024) p->fsym = 0;
+            // fixed-point bound of the 32 x 32 windows (may be tighter than the generic tile's)
+            double nc = 1.5 * (p->fsym_T * std::sqrt(2.0) + 2) * (2.0 / std::max(h, 1e-12) + 2);
+            if (p->min_delay < 8.0 * p->fsym_T * std::max(h, 1.0)) nc = (double)p->fsym_T * p->fsym_T;
+            nc = std::min(nc, (double)p->fsym_T * p->fsym_T);
+            p->fp_bits = std::min(p->fp_bits, std::min(22, 30 - ceil_log2(nc)));
         }
     }
     p->misc_blocks = std::max(1, std::min(1024, (p->P + kThreads - 1) / kThreads));
@@ -666,8 +703,10 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[1]), (size_t)p->P * ts * nf));
     const int ntile_max = std::max(p->bp_tiles_x * p->bp_tiles_y, p->sym ? p->sym_ntiles : 0);
     A(alloc(p, &p->part_bp, (size_t)4 * nf * std::max(ntile_max, (p->P + kThreads - 1) / kThreads)));
-    A(alloc(p, &p->part_tv, (size_t)p->fp_tiles_x * p->fp_tiles_y * nf));
-    A(alloc(p, &p->part_r, (size_t)p->M * nf));
+    A(alloc(p, &p->part_tv, (size_t)std::max(p->fp_tiles_x * p->fp_tiles_y,
+                                             p->fsym ? p->fsym_qt * p->fsym_qt : 0) * nf));
+    p->fin_chunks = std::max(1, std::min(8, p->Q / 1024));
+    A(alloc(p, &p->part_r, (size_t)p->M * nf * p->fin_chunks));
     A(alloc(p, &p->part_misc, (size_t)4 * p->misc_blocks * nf));
     {
         const int spmax = std::max(p->bp_split, p->sym ? p->sym_split : 1);
@@ -731,7 +770,7 @@ int pk_plan_get_info(const pk_plan* p, pk_plan_info* o) {
     o->device_bytes = p->device_bytes;
     o->frames = p->nf;
     o->bp_split = p->sym ? p->sym_split : p->bp_split;
-    o->symmetric = p->sym;
+    o->symmetric = p->sym + 2 * p->fsym;
     return PK_OK;
 }
 

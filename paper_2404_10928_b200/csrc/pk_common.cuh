@@ -269,6 +269,9 @@ struct pk_plan {
     // D4-symmetric back-projector (bp_sym_f32_kernel)
     int sym = 0, sym_ntiles = 0, sym_L = 0, sym_nbuf = 0, sym_smem = 0, sym_split = 1, sym_ms = 0;
     int sym_iw = 0;  // compile-time image-window stride (slots), 0 = runtime
+    // rotation-symmetric projector (fp_sym4_f32_kernel)
+    int fsym = 0, fsym_T = 0, fsym_qt = 0, fsym_L = 0, fsym_smem = 0;
+    int fin_chunks = 1;  // residual kernel: sample chunks per sensor
     int* sym_tiles = nullptr;
     std::vector<int> sym_tile_host;
     float* bp_gpart = nullptr;

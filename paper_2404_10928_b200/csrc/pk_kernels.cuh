@@ -435,9 +435,11 @@ __global__ void __launch_bounds__(kThreads, 4) bp_sym_f32_kernel(BpSymArgs A) {
     const float X0 = __ldg(a.pxs + i0), X1 = __ldg(a.pxs + min(i0 + kSymTile - 1, n - 1));
     const float Y0 = __ldg(a.pys + j0), Y1 = __ldg(a.pys + min(j0 + kSymTile - 1, n - 1));
 
+    // each buffer's mbarrier completes on 32 cp.async arrivals (one per lane of the filling
+    // warp, .noinc) plus one release arrive that publishes the sensor constants
     if (threadIdx.x == 0) {
         for (int b = 0; b < a.nbuf; ++b) {
-            mbar_init(bar_s + 8 * b, 1);
+            mbar_init(bar_s + 8 * b, 33);
             done_cnt[b] = 0;
         }
         fence_barrier_init();
@@ -445,7 +447,9 @@ __global__ void __launch_bounds__(kThreads, 4) bp_sym_f32_kernel(BpSymArgs A) {
     __syncthreads();
 
     const int nchunks = (mcount + kSymCS - 1) / kSymCS;
-    // lane = (base sensor c = lane >> 3, image g = lane & 7): one bulk copy per lane
+    // lane = (base sensor c = lane >> 3, image g = lane & 7) owns one window's geometry; the
+    // 32 windows (384-736 B each) are copied warp-cooperatively with 16-B cp.async (LDGSTS):
+    // 32 one-window bulk copies per 32 interactions per thread saturate the TMA queue.
     auto issue = [&](int c, int b) {
         const int nb = min(kSymCS, mcount - c * kSymCS);
         const int cs = lane >> 3, g = lane & 7;
@@ -465,15 +469,24 @@ __global__ void __launch_bounds__(kThreads, 4) bp_sym_f32_kernel(BpSymArgs A) {
         if (act && g == 0)
             sconst[b * kSymCS + cs] =
                 make_float4(sx, sy, __uint_as_float(dst0 - 8u * (uint32_t)lo - 8u * kTwo23Bits), 0.f);
-        __syncwarp();
-        if (lane == 0) mbar_expect_tx(bar_s + 8 * b, (uint32_t)(nb * 8 * a.L * 8));
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (act) {
-            const int ms = sym_sensor(g, m, a.M);
-            bulk_g2s(dst0 + (uint32_t)g * img_stride, a.table + (size_t)ms * a.TS + lo,
-                     (uint32_t)(a.L * 8), bar_s + 8 * b);
+        const uint32_t dst = dst0 + (uint32_t)g * img_stride;
+        const float2* src = a.table + (size_t)sym_sensor(g, m, a.M) * a.TS + lo;
+        const int pieces = a.L >> 1;  // 16-byte pieces per window
+        for (int wdw = 0; wdw < 8 * nb; ++wdw) {
+            const uint32_t dw = __shfl_sync(0xffffffffu, dst, wdw);
+            const unsigned long long sw =
+                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), wdw);
+            for (int q = lane; q < pieces; q += 32)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dw + 16u * q),
+                             "l"(sw + 16ull * q)
+                             : "memory");
         }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar_s + 8 * b)
+                     : "memory");
+        __syncwarp();
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar_s + 8 * b)
+                         : "memory");
     };
     if (warp == 0) {
         for (int c = 0; c < min(a.nbuf, nchunks); ++c) issue(c, c);
@@ -927,6 +940,181 @@ __global__ void __launch_bounds__(kThreads, NF == 1 ? 4 : (NF == 2 ? 3 : 2)) fp_
 }
 
 // ===========================================================================
+// K2s -- projector, fp32, for rotation-symmetric scenes (same conditions as K1s).  The
+// 4 rotations r^g by 90 degrees map a pair (pixel p, sensor m) to (r^g p, m + g*M/4) with
+// the same distance: lane l owns base sensor m = 32*group + l and 4 windows, one per
+// rotation image sensor m + g*M/4; the CTA's pixels are a T x T tile of the first quadrant
+// (i, j >= n/2) and each delay is applied to the 4 image pixels
+//   g = 0: (i, j)   1: (n-1-j, i)   2: (n-1-i, n-1-j)   3: (j, n-1-i).
+// Same fixed-point arithmetic and window layout as K2 ([slot][image][lane]).
+// ===========================================================================
+template <bool CLAMP>
+__global__ void __launch_bounds__(kThreads, 3) fp_sym4_f32_kernel(FpArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ float red_f[kThreads / 32];
+    constexpr int G = 4;
+    constexpr int RV = 3;  // record: px, {xs, xq} x 4 -> 9 floats in 3 float4
+    int iter = 0;
+    if (a.solver) {
+        if (a.st->all_stopped) return;
+        iter = a.st->iter;
+    }
+    const float* x = a.x ? a.x : ((iter & 1) ? a.xb0 : a.xb1);
+    const float scale = a.st->fr[0].scale32;
+    const int n = a.nx, h = n >> 1;
+    const int T = a.T;
+    const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
+    const int i0 = h + tx * T, j0 = h + ty * T;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int m = blockIdx.y * 32 + lane;
+    const bool sensor_ok = m < a.M;
+    const int q4 = a.M >> 2;
+    const float sx = __ldg(a.sxs + min(m, a.M - 1)), sy = __ldg(a.sys + min(m, a.M - 1));
+
+    int32_t* win = reinterpret_cast<int32_t*>(smem);
+    float4* rows = reinterpret_cast<float4*>(smem + (size_t)a.L * G * 32 * 4);
+    float4* rec = rows + (size_t)warp * (T + kFpBatch) * RV;
+
+    for (int q = threadIdx.x; q < a.L * G * 32; q += kThreads) win[q] = 0;
+    const float X0 = __ldg(a.pxs + i0), X1 = __ldg(a.pxs + min(i0 + T - 1, n - 1));
+    const float Y0 = __ldg(a.pys + j0), Y1 = __ldg(a.pys + min(j0 + T - 1, n - 1));
+    const float cx = fminf(fmaxf(sx, X0), X1), cy = fminf(fmaxf(sy, Y0), Y1);
+    float dmin = sqrtf((cx - sx) * (cx - sx) + (cy - sy) * (cy - sy));
+    if (CLAMP) dmin = fminf(dmin, a.qclamp);
+    const int lo = (int)floorf(dmin) - 2;
+    const uint32_t adj = smem_u32(win) + 4u * (uint32_t)lane - (128u * G) * (uint32_t)lo -
+                         (128u * G) * kTwo23Bits;
+    __syncthreads();
+
+    float tv = 0.f;
+    const bool do_tv = a.solver && blockIdx.y == 0;
+    const int jend = min(T, n - j0);
+    for (int r = warp; r < jend; r += kThreads / 32) {
+        const int jj = j0 + r;
+        int cnt = 0;
+        for (int cc = 0; cc < T; cc += 32) {
+            const int ii = i0 + cc + lane;
+            const bool in = ii < n && cc + lane < T;
+            float xv[G] = {0.f, 0.f, 0.f, 0.f};
+            if (in) {
+                const int pg[G] = {jj * n + ii, ii * n + (n - 1 - jj), (n - 1 - jj) * n + (n - 1 - ii),
+                                   (n - 1 - ii) * n + jj};
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    xv[g] = x[pg[g]];
+                    if (do_tv) {  // exact anisotropic TV over the 4 image pixels
+                        const int pi = pg[g] % n, pj = pg[g] / n;
+                        if (pi + 1 < n) tv += fabsf(x[pg[g] + 1] - xv[g]);
+                        if (pj + 1 < n) tv += fabsf(x[pg[g] + n] - xv[g]);
+                    }
+                }
+            }
+            const bool nz = xv[0] != 0.f || xv[1] != 0.f || xv[2] != 0.f || xv[3] != 0.f;
+            const uint32_t bal = __ballot_sync(0xffffffffu, nz);
+            if (nz) {
+                float rv[4 * RV];
+                rv[0] = __ldg(a.pxs + ii);
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const float xs = xv[g] * scale;
+                    rv[1 + 2 * g] = xs;
+                    rv[2 + 2 * g] = __int_as_float(__float_as_int(xs + kMagic));
+                }
+                rv[9] = rv[10] = rv[11] = 0.f;
+                float4* dst = rec + (size_t)(cnt + __popc(bal & ((1u << lane) - 1u))) * RV;
+#pragma unroll
+                for (int v = 0; v < RV; ++v)
+                    dst[v] = make_float4(rv[4 * v], rv[4 * v + 1], rv[4 * v + 2], rv[4 * v + 3]);
+            }
+            cnt += __popc(bal);
+        }
+        if (cnt == 0) continue;
+        const int cnt8 = (cnt + kFpBatch - 1) & ~(kFpBatch - 1);
+        if (lane < cnt8 - cnt) {
+            float4* dst = rec + (size_t)(cnt + lane) * RV;
+            const float mb = __int_as_float(kMagicBits);
+            dst[0] = make_float4(X0, 0.f, mb, 0.f);
+            dst[1] = make_float4(mb, 0.f, mb, 0.f);
+            dst[2] = make_float4(mb, 0.f, 0.f, 0.f);
+        }
+        __syncwarp();
+        if (sensor_ok) {
+            const float ey = __ldg(a.pys + jj) - sy;
+            const float ey2 = ey * ey;
+            for (int k = 0; k < cnt8; k += kFpBatch) {
+                uint32_t ad[kFpBatch];
+                int32_t va[kFpBatch][G], vb[kFpBatch][G];
+#pragma unroll
+                for (int b = 0; b < kFpBatch; ++b) {
+                    float rv[4 * RV];
+#pragma unroll
+                    for (int v = 0; v < RV; ++v) {
+                        const float4 q = rec[(size_t)(k + b) * RV + v];
+                        rv[4 * v] = q.x; rv[4 * v + 1] = q.y; rv[4 * v + 2] = q.z; rv[4 * v + 3] = q.w;
+                    }
+                    const float ex = rv[0] - sx;
+                    float u = sqrt_approx(fmaf(ex, ex, ey2));
+                    if (CLAMP) u = fminf(u, a.qclamp);
+                    const float tb = __fadd_rd(u, kTwo23);
+                    const float fr = u - (tb - kTwo23);
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        const float fb = fmaf(rv[1 + 2 * g], fr, kMagic);
+                        va[b][g] = __float_as_int(fb) - kMagicBits;
+                        vb[b][g] = __float_as_int(rv[2 + 2 * g]) - __float_as_int(fb);
+                    }
+                    ad[b] = adj + (__float_as_uint(tb) << 9);  // 128 B x 4 images per slot
+                }
+#pragma unroll
+                for (int b = 0; b < kFpBatch; ++b)
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        red_smem_s32(ad[b] - 128u * G + 128u * g, vb[b][g]);
+                        red_smem_s32(ad[b] + 128u * g, va[b][g]);
+                    }
+            }
+        }
+        __syncwarp();
+    }
+    if (do_tv) {
+        const float tvb = block_sum(tv, red_f);
+        if (threadIdx.x == 0) a.part_tv[blockIdx.x] = tvb;
+    }
+    __syncthreads();
+
+    // flush (transposed through the record buffer, as in fp_f32_kernel); window g of lane
+    // l belongs to sensor (32*group + l + g*M/4) mod M
+    const int cap = (T + kFpBatch) * RV * 16;
+    const int bs = (32 * 9 * 4 <= cap) ? 8 : 4;
+    int32_t* scr = reinterpret_cast<int32_t*>(rec);
+    const int sensors_per_step = 32 / bs;
+    const int sub = lane % bs, grp = lane / bs;
+    for (int k0 = warp * bs; k0 < a.L; k0 += (kThreads / 32) * bs) {
+#pragma unroll 1
+        for (int g = 0; g < G; ++g) {
+            for (int i = 0; i < bs; ++i) {
+                const int k = k0 + i;
+                scr[lane * (bs + 1) + i] = (k < a.L) ? win[(k * G + g) * 32 + lane] : 0;
+            }
+            __syncwarp();
+            for (int rr = 0; rr < 32; rr += sensors_per_step) {
+                const int ms = rr + grp;
+                const int lo_ms = __shfl_sync(0xffffffffu, lo, ms);
+                const int v = scr[ms * (bs + 1) + sub];
+                const int t = lo_ms + k0 + sub;
+                const int mb = blockIdx.y * 32 + ms;
+                if (v != 0 && mb < a.M && t >= 0 && t < a.Q && k0 + sub < a.L) {
+                    const int mg = (mb + g * q4) % a.M;
+                    atomicAdd(reinterpret_cast<unsigned long long*>(a.acc + (size_t)mg * a.Q + t),
+                              (unsigned long long)(long long)v);
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// ===========================================================================
 // K2 -- projector, fp64 validation mode (same structure, int64 fixed point, CAS atomics)
 // ===========================================================================
 struct FpArgs64 {
@@ -1072,6 +1260,7 @@ struct FinArgs {
     double* sumsq_out;   // optional [NF] (pk_residual)
     int solver;
     int atrick;
+    int chunks;          // sample chunks per sensor (one CTA each)
 };
 
 template <typename T, int NF>
@@ -1082,7 +1271,13 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
     __shared__ double data_s[NF], tv_s[NF];
     __shared__ int last_flag;
     if (a.solver && a.st->all_stopped) return;
-    const int m = blockIdx.x, f = blockIdx.y;
+    // grid (M * chunks, NF): CTA handles samples [c0, c1) of sensor m plus the one-sample
+    // halo r[c0-1] its first pair-table entry needs.  The accumulator is read-only here (it
+    // is cleared by a memset before the next projection), so neighbouring chunks do not race.
+    const int chunks = a.chunks;
+    const int m = blockIdx.x / chunks, cix = blockIdx.x % chunks, f = blockIdx.y;
+    const int clen = (a.Q + chunks - 1) / chunks;
+    const int c0 = cix * clen, c1 = min(a.Q, c0 + clen);
     const double sc = sizeof(T) == 4 ? (double)a.st->fr[f].scale32 : a.st->fr[f].scale64;
     const double wq = sc > 0.0 ? a.w / sc : 0.0;
     const T* y = a.solver ? reinterpret_cast<const T*>(a.io->y) : a.y;
@@ -1090,53 +1285,51 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
     long long* accm = a.acc + (size_t)f * MQ + (size_t)m * a.Q;
     const T* ym = y ? y + f * MQ + (size_t)m * a.Q : nullptr;
     T* om = a.trace_out ? a.trace_out + f * MQ + (size_t)m * a.Q : nullptr;
+    // K x rounded to the working type first, then the residual in that type, so that y
+    // produced by the same projection gives r == 0 exactly (recon.py:75-79 semantics)
+    auto resid = [&](int s, long long v) -> T {
+        const T kx = (T)((double)v * wq);
+        return ym ? (T)(kx - ym[s]) : kx;
+    };
     double ss = 0.0;
-    // 4 samples per thread per step: all loads first (independent), then math and stores
-    for (int s0 = 4 * threadIdx.x; s0 < a.Q; s0 += 4 * kThreads) {
+    // tr[k] holds r[c0 - 1 + k]; 4 samples per thread per step, all loads first
+    if (threadIdx.x == 0) tr[0] = (c0 >= 1) ? resid(c0 - 1, __ldcg(accm + c0 - 1)) : (T)0;
+    for (int s0 = c0 + 4 * threadIdx.x; s0 < c1; s0 += 4 * kThreads) {
         long long v[4];
-        T yv[4] = {(T)0, (T)0, (T)0, (T)0};
-        const bool full = s0 + 4 <= a.Q && (a.Q & 1) == 0;
+        const bool full = s0 + 4 <= c1 && (s0 & 1) == 0;
         if (full) {
             const longlong2 p0 = __ldcg(reinterpret_cast<const longlong2*>(accm + s0));
             const longlong2 p1 = __ldcg(reinterpret_cast<const longlong2*>(accm + s0 + 2));
             v[0] = p0.x; v[1] = p0.y; v[2] = p1.x; v[3] = p1.y;
         } else {
-            for (int q = 0; q < 4; ++q) v[q] = (s0 + q < a.Q) ? __ldcg(accm + s0 + q) : 0;
-        }
-        if (ym)
-            for (int q = 0; q < 4; ++q) yv[q] = (s0 + q < a.Q) ? ym[s0 + q] : (T)0;
-        if (full) {
-            reinterpret_cast<longlong2*>(accm + s0)[0] = make_longlong2(0, 0);
-            reinterpret_cast<longlong2*>(accm + s0)[1] = make_longlong2(0, 0);
-        } else {
-            for (int q = 0; q < 4; ++q) if (s0 + q < a.Q) accm[s0 + q] = 0;
+            for (int q = 0; q < 4; ++q) v[q] = (s0 + q < c1) ? __ldcg(accm + s0 + q) : 0;
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            if (s0 + q >= a.Q) break;
-            // K x rounded to the working type first, then the residual in that type, so that
-            // y produced by the same projection gives r == 0 exactly (recon.py:75-79 semantics)
-            const T kx = (T)((double)v[q] * wq);
-            const T rv = ym ? (T)(kx - yv[q]) : kx;
-            tr[s0 + q] = rv;
+            if (s0 + q >= c1) break;
+            const T rv = resid(s0 + q, v[q]);
+            tr[s0 + q - c0 + 1] = rv;
             if (om) om[s0 + q] = rv;
             ss += (double)rv * (double)rv;
         }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < a.TS; e += kThreads) {
-        const T rp = (e >= 1 && e - 1 < a.Q) ? tr[e - 1] : (T)0;
-        const T rc = (e < a.Q) ? tr[e] : (T)0;
+    // entries e in [c0, c1) (the last chunk also writes the zero-padded tail up to TS)
+    const int e1 = (cix == chunks - 1) ? a.TS : c1;
+    for (int e = c0 + threadIdx.x; e < e1; e += kThreads) {
+        const T rp = (e >= 1 && e - 1 < a.Q) ? tr[e - c0] : (T)0;
+        const T rc = (e < a.Q) ? tr[e - c0 + 1] : (T)0;
         a.table[((size_t)m * a.TS + e) * NF + f] = pair_entry<T>(rp, rc, e, a.atrick);
     }
     ss = block_sum(ss, red_d);
-    if (threadIdx.x == 0) a.part_r[(size_t)f * a.M + m] = ss;
+    if (threadIdx.x == 0) a.part_r[(size_t)f * a.M * chunks + blockIdx.x] = ss;
     if (!last_block(&a.st->cnt_fin, gridDim.x * gridDim.y, &last_flag)) return;
 
 #pragma unroll 1
     for (int g = 0; g < NF; ++g) {
         double d = 0.0, t = 0.0;
-        for (int q = threadIdx.x; q < a.M; q += kThreads) d += a.part_r[(size_t)g * a.M + q];
+        for (int q = threadIdx.x; q < a.M * chunks; q += kThreads)
+            d += a.part_r[(size_t)g * a.M * chunks + q];
         d = block_sum(d, red_d);
         if (a.solver) {
             for (int q = threadIdx.x; q < a.ntv; q += kThreads) t += a.part_tv[(size_t)q * NF + g];

@@ -1,0 +1,71 @@
+"""The symmetric kernels (D4 back-projector, rotation projector) against the generic ones
+and the fp64 oracle.  Every BASELINE scene (centred square grid, M % 4 == 0) selects them
+automatically; PK_SYM / PK_FSYM = 0 forces the generic kernels."""
+
+import numpy as np
+import pytest
+
+import paper_2404_10928_b200 as pk
+
+pytestmark = pytest.mark.gpu
+F32 = pk.CudaPool(0, "float32")
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _plan(monkeypatch, g, ring, ac, sym, fsym):
+    monkeypatch.setenv("PK_SYM", sym)
+    monkeypatch.setenv("PK_FSYM", fsym)
+    pk.clear_plan_cache()
+    return pk.operator_for(g, ring, ac, F32)
+
+
+@pytest.mark.parametrize("cfg", [(64, 32, 128), (128, 128, 1024), (256, 256, 2048)])
+def test_symmetric_products_match_oracle(monkeypatch, oracle, cfg):
+    n, M, Q = cfg
+    g, ring, ac, ph = pk.make_scene(n, M, Q, seed=2)
+    o = oracle.Operator.of(oracle.make_scene(n, M, Q, 2))
+    op = _plan(monkeypatch, g, ring, ac, "1", "1")
+    assert op.info.symmetric == 3  # both symmetric kernels forced on
+    rng = np.random.default_rng(9)
+    x = ph.values + 0.05 * rng.random(g.size)          # dense, non-negative
+    assert rel(op.matvec(x).double().cpu().numpy(), o.forward(x)) <= 5e-5
+    y = o.forward(ph.values)                              # a smooth measured trace
+    assert rel(op.adjoint(y).double().cpu().numpy(), o.adjoint(y)) <= 2e-5
+    pk.clear_plan_cache()
+
+
+@pytest.mark.parametrize("sym,fsym", [("1", "1"), ("1", "0"), ("0", "0")])
+def test_symmetric_and_generic_reconstructions_agree(monkeypatch, oracle, sym, fsym):
+    n, M, Q = 128, 128, 1024
+    g, ring, ac, ph = pk.make_scene(n, M, Q, seed=0)
+    K = pk.build_time_matrix(g, ring, ac)
+    o = oracle.Operator.of(oracle.make_scene(n, M, Q, 0))
+    y = o.forward(ph.values)
+    alpha, beta = oracle.resolve_regularization(o, y)
+    step = oracle.resolve_step(o, beta, 1e-3)
+    ref = oracle.reconstruct(o, y, alpha, beta, step, 10)
+    op = _plan(monkeypatch, g, ring, ac, sym, fsym)
+    assert op.info.symmetric == int(sym) + 2 * int(fsym)
+    res = pk.iterative_reconstruct(K, pk.SensorData("time", M, Q, y),
+                                   pk.ReconConfig(alpha, beta, 10, step), pool=F32)
+    assert res.iterations_run == 10
+    assert rel(res.image.values, ref["image"]) <= 1e-4
+    np.testing.assert_allclose(res.objective_history, ref["objective_history"], rtol=1e-5)
+    pk.clear_plan_cache()
+
+
+def test_symmetric_projector_deterministic(monkeypatch):
+    g, ring, ac, ph = pk.make_scene(64, 32, 128, seed=1)
+    K = pk.build_time_matrix(g, ring, ac)
+    _plan(monkeypatch, g, ring, ac, "1", "1")
+    y1 = pk.forward_project(K, ph, pool=F32)
+    y2 = pk.forward_project(K, ph, pool=F32)
+    assert np.array_equal(y1.values, y2.values)
+    grad = pk.data_gradient(K, ph, y1, pool=F32)
+    assert np.max(np.abs(grad.values)) <= 1e-18
+    pk.clear_plan_cache()
