@@ -82,7 +82,7 @@ typedef struct pk_plan_info {
     int32_t fp_tile, fp_window, fp_bits;              /* projector tiling, fixed-point bits */
     int64_t device_bytes;    /* workspace held by the plan */
     int32_t frames;          /* frames per call */
-    int32_t bp_split;        /* sensor slices per back-projector tile */
+    int32_t bp_split;        /* sensor slices per back-projector tile (symmetric: partial slots) */
     int32_t symmetric;       /* bit 0: D4-symmetric back-projector (one delay per 8 pairs);
                                 bit 1: rotation-symmetric projector (one delay per 4 pairs) */
 } pk_plan_info;

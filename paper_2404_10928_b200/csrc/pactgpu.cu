@@ -110,7 +110,9 @@ void free_plan(pk_plan* p) {
     void* ptrs[] = {p->pxs, p->pys, p->sxs, p->sys, p->px, p->py, p->sx, p->sy, p->table,
                     p->acc, p->xbuf[0], p->xbuf[1], p->ydev, p->y64, p->x64, p->hist_dev,
                     p->status_dev, p->part_bp, p->part_tv, p->part_r, p->part_misc, p->state,
-                    p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt, p->sym_tiles};
+                    p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt, p->sym_tiles,
+                    p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0, p->sym_tile_slot0,
+                    p->sym_part};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
@@ -134,20 +136,25 @@ void smem_kernels(std::vector<const void*>& v) {
     v.push_back((const void*)finalize_kernel<float, NF>);
 }
 
-template <int IW>
-void sym_kernels(std::vector<const void*>& v) {
-    v.push_back((const void*)bp_sym_f32_kernel<true, true, IW>);
-    v.push_back((const void*)bp_sym_f32_kernel<true, false, IW>);
-    v.push_back((const void*)bp_sym_f32_kernel<false, true, IW>);
-    v.push_back((const void*)bp_sym_f32_kernel<false, false, IW>);
-}
+constexpr int kSymIW[] = {64, 96, 128, 192, 256};
+// relative cost of a chunk: diagonal tiles evaluate the same delays for 4 images, not 8
+// (per delay ~8 issue slots of geometry + 3 per image: 20 vs 32)
+constexpr int kSymWDiag = 5, kSymWOff = 8;
 
 template <int IW>
-void launch_sym(const BpSymArgs& A, dim3 grid, int smem, bool epi, bool clamp, cudaStream_t s) {
-    if (epi) { if (clamp) bp_sym_f32_kernel<true, true, IW><<<grid, kThreads, smem, s>>>(A);
-               else bp_sym_f32_kernel<true, false, IW><<<grid, kThreads, smem, s>>>(A); }
-    else { if (clamp) bp_sym_f32_kernel<false, true, IW><<<grid, kThreads, smem, s>>>(A);
-           else bp_sym_f32_kernel<false, false, IW><<<grid, kThreads, smem, s>>>(A); }
+void launch_sym(const BpSymArgs& A, int grid, int smem, cudaStream_t s) {
+    bp_sym_f32_kernel<IW><<<grid, kSymThreads, smem, s>>>(A);
+}
+
+const void* sym_kernel_ptr(int iw) {
+    switch (iw) {
+        case 64: return (const void*)bp_sym_f32_kernel<64>;
+        case 96: return (const void*)bp_sym_f32_kernel<96>;
+        case 128: return (const void*)bp_sym_f32_kernel<128>;
+        case 192: return (const void*)bp_sym_f32_kernel<192>;
+        case 256: return (const void*)bp_sym_f32_kernel<256>;
+        default: return (const void*)bp_sym_f32_kernel<0>;
+    }
 }
 
 cudaError_t opt_in_smem(int device) {
@@ -162,11 +169,8 @@ cudaError_t opt_in_smem(int device) {
     smem_kernels<2>(ks);
     smem_kernels<4>(ks);
     ks.push_back((const void*)fp_sym4_f32_kernel<false>);
-    sym_kernels<0>(ks);
-    sym_kernels<48>(ks);
-    sym_kernels<64>(ks);
-    sym_kernels<96>(ks);
-    sym_kernels<128>(ks);
+    ks.push_back(sym_kernel_ptr(0));
+    for (int iw : kSymIW) ks.push_back(sym_kernel_ptr(iw));
     ks.push_back((const void*)fp_f64_kernel);
     ks.push_back((const void*)finalize_kernel<double, 1>);
     for (const void* k : ks)
@@ -273,27 +277,31 @@ void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_
     const bool clamp = p->max_delay >= (double)p->Q + 0.5;
     if (p->dtype == PK_F32 && NF == 1 && p->sym) {
         BpSymArgs A{};
-        BpArgs& a = A.b;
-        a.table = static_cast<const float2*>(p->table);
-        a.pxs = p->pxs; a.pys = p->pys; a.sxs = p->sxs; a.sys = p->sys;
-        a.nx = p->nx; a.ny = p->ny; a.M = p->M; a.Q = p->Q; a.TS = p->TS; a.L = p->sym_L;
-        a.CS = kSymCS; a.nbuf = p->sym_nbuf; a.tiles_x = 0;
-        a.qclamp = (float)p->Q + 1.5f;
-        a.out = static_cast<float*>(out);
-        a.gscale = (float)(gscale_mult * p->w);
-        a.xb0 = static_cast<float*>(p->xbuf[0]);
-        a.xb1 = static_cast<float*>(p->xbuf[1]);
-        a.prm = p->params; a.st = p->state; a.part = p->part_bp; a.bits = p->fp_bits;
-        a.split = p->sym_split; a.ms = p->sym_ms; a.gpart = p->bp_gpart; a.tile_cnt = p->bp_tile_cnt;
-        A.n = p->nx; A.tile_list = p->sym_tiles;
-        const dim3 grid(p->sym_ntiles, p->sym_split);
+        A.table = static_cast<const float2*>(p->table);
+        A.pxs = p->pxs; A.pys = p->pys; A.sxs = p->sxs; A.sys = p->sys;
+        A.n = p->nx; A.M = p->M; A.TS = p->TS; A.L = p->sym_L; A.nbuf = p->sym_nbuf;
+        A.qclamp = (float)p->Q + 1.5f;
+        A.chunks = p->sym_chunks; A.cta_chunk0 = p->sym_cta_chunk0; A.cta_slot0 = p->sym_cta_slot0;
+        A.tiles = p->sym_tiles; A.part = p->sym_part; A.lanemap = p->sym_lanemap;
+        A.st = epi ? p->state : nullptr;
         switch (p->sym_iw) {
-            case 48: launch_sym<48>(A, grid, p->sym_smem, epi, clamp, s); break;
-            case 64: launch_sym<64>(A, grid, p->sym_smem, epi, clamp, s); break;
-            case 96: launch_sym<96>(A, grid, p->sym_smem, epi, clamp, s); break;
-            case 128: launch_sym<128>(A, grid, p->sym_smem, epi, clamp, s); break;
-            default: launch_sym<0>(A, grid, p->sym_smem, epi, clamp, s); break;
+            case 64: launch_sym<64>(A, p->sym_grid, p->sym_smem, s); break;
+            case 96: launch_sym<96>(A, p->sym_grid, p->sym_smem, s); break;
+            case 128: launch_sym<128>(A, p->sym_grid, p->sym_smem, s); break;
+            case 192: launch_sym<192>(A, p->sym_grid, p->sym_smem, s); break;
+            case 256: launch_sym<256>(A, p->sym_grid, p->sym_smem, s); break;
+            default: launch_sym<0>(A, p->sym_grid, p->sym_smem, s); break;
         }
+        BpSymEpiArgs E{};
+        E.part = p->sym_part; E.tile_slot0 = p->sym_tile_slot0; E.tiles = p->sym_tiles;
+        E.n = p->nx; E.bits = p->fp_bits; E.lanemap = p->sym_lanemap;
+        E.gscale = (float)(gscale_mult * p->w);
+        E.out = static_cast<float*>(out);
+        E.xb0 = static_cast<float*>(p->xbuf[0]);
+        E.xb1 = static_cast<float*>(p->xbuf[1]);
+        E.prm = p->params; E.st = p->state; E.part_bp = p->part_bp;
+        if (epi) bp_sym_epi_kernel<true><<<p->sym_ntiles * 8, kThreads, 0, s>>>(E);
+        else bp_sym_epi_kernel<false><<<p->sym_ntiles * 8, kThreads, 0, s>>>(E);
         return;
     }
     if (p->dtype == PK_F32) {
@@ -633,29 +641,73 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         }
         p->sym = ok ? 1 : 0;
         if (p->sym) {
+            // representative tiles tx >= ty of the quadrant, chunks of kSymCS base sensors
             const int qt = (n / 2 + kSymTile - 1) / kSymTile;
-            std::vector<int> tl;
+            std::vector<int>& tl = p->sym_h[0];
             for (int tx = 0; tx < qt; ++tx)
                 for (int ty = 0; ty <= tx; ++ty) tl.push_back((tx << 16) | ty);
             p->sym_ntiles = (int)tl.size();
-            p->sym_tile_host = tl;
             p->sym_L = ((int)std::ceil(tile_diag(kSymTile)) + 7 + 1) & ~1;
             if (p->sym_L > p->TS) p->sym_L = p->TS;
             p->sym_iw = 0;
-            for (int iw : {48, 64, 96, 128})
+            for (int iw : kSymIW)
                 if (p->sym_L <= iw) { p->sym_iw = iw; break; }
             const int ws = p->sym_iw ? p->sym_iw : p->sym_L;
-            // chunks are short (4 base sensors = 32 interactions per thread), so the TMA ring
-            // must be deep to cover the copy latency: as many buffers (<= 8) as fit 74 KB
-            const int per_buf = kSymCS * 8 * ws * 8 + kSymCS * 16 + 8;
-            p->sym_nbuf = std::max(2, std::min(8, (74 * 1024) / per_buf));
+            // TMA ring as deep as fits ~72 KB (3 CTAs per SM), 2..8 buffers
+            const int per_buf = kSymCS * 8 * ws * 8 + kSymCS * 16 + 16;
+            p->sym_nbuf = std::max(2, std::min(8, (72 * 1024) / per_buf));
+            if (const char* e = getenv("PK_SYM_NBUF")) p->sym_nbuf = std::max(2, std::min(8, atoi(e)));
+            p->sym_lanemap = 1;
+            if (const char* e = getenv("PK_SYM_LANEMAP")) p->sym_lanemap = atoi(e) != 0;
             p->sym_smem = p->sym_nbuf * per_buf;
-            if (p->sym_smem > 200 * 1024) p->sym = 0;
-            int sp = 1;
-            while (p->sym_ntiles * sp < 4 * 148 && p->M / (2 * sp) >= 32) sp *= 2;
-            p->sym_ms = (p->M + sp - 1) / sp;
-            p->sym_ms = ((p->sym_ms + kSymCS - 1) / kSymCS) * kSymCS;
-            p->sym_split = (p->M + p->sym_ms - 1) / p->sym_ms;
+            int occ = 0, sms = 0;
+            if (p->sym_smem > 200 * 1024 || opt_in_smem(p->device) != cudaSuccess ||
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym_kernel_ptr(p->sym_iw), kSymThreads,
+                                                              p->sym_smem) != cudaSuccess ||
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess ||
+                occ < 1) {
+                cudaGetLastError();
+                p->sym = 0;
+            }
+            if (p->sym) {
+                // persistent grid; equal-cost contiguous chunk ranges (off-diagonal chunk = 2)
+                p->sym_grid = occ * sms;
+                if (const char* e = getenv("PK_SYM_GRID")) p->sym_grid = std::max(1, atoi(e));
+                const int nch = (p->M + kSymCS - 1) / kSymCS;
+                std::vector<int>& ch = p->sym_h[1];
+                std::vector<int>& c0 = p->sym_h[2];
+                std::vector<int>& cs0 = p->sym_h[3];
+                std::vector<int>& ts0 = p->sym_h[4];
+                int64_t W = 0;
+                for (int t = 0; t < p->sym_ntiles; ++t)
+                    W += (int64_t)nch * (((tl[t] >> 16) == (tl[t] & 0xffff)) ? kSymWDiag : kSymWOff);
+                const int G = p->sym_grid;
+                c0.assign(G + 1, 0);
+                cs0.assign(G, 0);
+                int64_t cw = 0;
+                int owner_prev = -1, tile_prev = -1, slot = -1;
+                for (int t = 0; t < p->sym_ntiles; ++t) {
+                    const int wt = ((tl[t] >> 16) == (tl[t] & 0xffff)) ? kSymWDiag : kSymWOff;
+                    for (int k = 0; k < nch; ++k) {
+                        const int owner = (int)std::min<int64_t>(G - 1, cw * G / W);
+                        if (owner != owner_prev || t != tile_prev) {
+                            ++slot;
+                            if (t != tile_prev) ts0.push_back(slot);
+                            if (owner != owner_prev) {
+                                for (int b = owner_prev + 1; b <= owner; ++b) c0[b] = (int)ch.size();
+                                cs0[owner] = slot;
+                            }
+                            owner_prev = owner;
+                            tile_prev = t;
+                        }
+                        ch.push_back((t << 16) | k);
+                        cw += wt;
+                    }
+                }
+                for (int b = owner_prev + 1; b <= G; ++b) c0[b] = (int)ch.size();
+                ts0.push_back(slot + 1);
+                p->sym_slots = slot + 1;
+            }
         }
         // rotation-symmetric projector (4 windows per lane, quadrant tiles of 32 x 32)
         const char* ev2 = getenv("PK_FSYM");
@@ -701,19 +753,23 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     A(alloc(p, &p->acc, (size_t)p->M * p->Q * nf));
     A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[0]), (size_t)p->P * ts * nf));
     A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[1]), (size_t)p->P * ts * nf));
-    const int ntile_max = std::max(p->bp_tiles_x * p->bp_tiles_y, p->sym ? p->sym_ntiles : 0);
+    const int ntile_max = std::max(p->bp_tiles_x * p->bp_tiles_y, p->sym ? 8 * p->sym_ntiles : 0);
     A(alloc(p, &p->part_bp, (size_t)4 * nf * std::max(ntile_max, (p->P + kThreads - 1) / kThreads)));
     A(alloc(p, &p->part_tv, (size_t)std::max(p->fp_tiles_x * p->fp_tiles_y,
                                              p->fsym ? p->fsym_qt * p->fsym_qt : 0) * nf));
     p->fin_chunks = std::max(1, std::min(8, p->Q / 1024));
     A(alloc(p, &p->part_r, (size_t)p->M * nf * p->fin_chunks));
     A(alloc(p, &p->part_misc, (size_t)4 * p->misc_blocks * nf));
-    {
-        const int spmax = std::max(p->bp_split, p->sym ? p->sym_split : 1);
-        if (spmax > 1) A(alloc(p, &p->bp_gpart, (size_t)spmax * p->P * nf));
-    }
+    if (p->bp_split > 1) A(alloc(p, &p->bp_gpart, (size_t)p->bp_split * p->P * nf));
     A(alloc(p, &p->bp_tile_cnt, (size_t)ntile_max));
-    if (p->sym) A(alloc(p, &p->sym_tiles, (size_t)p->sym_ntiles));
+    if (p->sym) {
+        A(alloc(p, &p->sym_tiles, p->sym_h[0].size()));
+        A(alloc(p, &p->sym_chunks, p->sym_h[1].size()));
+        A(alloc(p, &p->sym_cta_chunk0, p->sym_h[2].size()));
+        A(alloc(p, &p->sym_cta_slot0, p->sym_h[3].size()));
+        A(alloc(p, &p->sym_tile_slot0, p->sym_h[4].size()));
+        A(alloc(p, &p->sym_part, (size_t)p->sym_slots * 8 * 4 * kThreads));
+    }
     A(alloc(p, &p->state, 1));
     A(alloc(p, &p->params, 1));
     A(alloc(p, &p->io, 1));
@@ -730,9 +786,11 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     if (e == cudaSuccess) e = cudaMemset(p->state, 0, sizeof(DevState));
     if (e == cudaSuccess)
         e = cudaMemset(p->bp_tile_cnt, 0, sizeof(uint32_t) * ntile_max);
-    if (e == cudaSuccess && p->sym)
-        e = cudaMemcpy(p->sym_tiles, p->sym_tile_host.data(), sizeof(int) * p->sym_ntiles,
-                       cudaMemcpyHostToDevice);
+    if (p->sym) {
+        int* dsts[5] = {p->sym_tiles, p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0,
+                        p->sym_tile_slot0};
+        for (int q = 0; q < 5; ++q) up(dsts[q], p->sym_h[q].data(), sizeof(int) * p->sym_h[q].size());
+    }
     if (e == cudaSuccess) e = cudaMemset(p->table, 0, (size_t)p->M * p->TS * 2 * ts * nf);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);
     // opt every dynamic-smem kernel into the device maximum once per device (a per-plan
@@ -769,7 +827,7 @@ int pk_plan_get_info(const pk_plan* p, pk_plan_info* o) {
     o->fp_bits = p->fp_bits;
     o->device_bytes = p->device_bytes;
     o->frames = p->nf;
-    o->bp_split = p->sym ? p->sym_split : p->bp_split;
+    o->bp_split = p->sym ? p->sym_slots : p->bp_split;
     o->symmetric = p->sym + 2 * p->fsym;
     return PK_OK;
 }

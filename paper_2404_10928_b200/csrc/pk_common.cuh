@@ -124,6 +124,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
 }
 
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
 // 1-D bulk copy global -> shared (TMA engine), completion counted on an mbarrier
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
                                          uint32_t bar) {
@@ -266,14 +270,17 @@ struct pk_plan {
     int bp_tiles_x = 0, bp_tiles_y = 0, bp_L = 0, bp_CS = 0, bp_nbuf = 0, bp_smem = 0;
     int bp_split = 1, bp_ms = 0;
     int bp_atrick = 0;  // fp32 pair-table layout {r[s-1] - s*D, D}
-    // D4-symmetric back-projector (bp_sym_f32_kernel)
-    int sym = 0, sym_ntiles = 0, sym_L = 0, sym_nbuf = 0, sym_smem = 0, sym_split = 1, sym_ms = 0;
+    // D4-symmetric back-projector (bp_sym_f32_kernel + bp_sym_epi_kernel)
+    int sym = 0, sym_ntiles = 0, sym_L = 0, sym_nbuf = 0, sym_smem = 0, sym_grid = 0, sym_slots = 0;
     int sym_iw = 0;  // compile-time image-window stride (slots), 0 = runtime
+    int sym_lanemap = 1;
+    int *sym_tiles = nullptr, *sym_chunks = nullptr, *sym_cta_chunk0 = nullptr,
+        *sym_cta_slot0 = nullptr, *sym_tile_slot0 = nullptr;
+    float* sym_part = nullptr;  // [slots][8][4][kThreads] partial sums
+    std::vector<int> sym_h[5];  // host copies: tiles, chunks, cta_chunk0, cta_slot0, tile_slot0
     // rotation-symmetric projector (fp_sym4_f32_kernel)
     int fsym = 0, fsym_T = 0, fsym_qt = 0, fsym_L = 0, fsym_smem = 0;
     int fin_chunks = 1;  // residual kernel: sample chunks per sensor
-    int* sym_tiles = nullptr;
-    std::vector<int> sym_tile_host;
     float* bp_gpart = nullptr;
     uint32_t* bp_tile_cnt = nullptr;
     // projector tiling

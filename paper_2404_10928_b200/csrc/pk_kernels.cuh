@@ -338,25 +338,58 @@ __global__ void __launch_bounds__(kThreads, NF == 1 ? 4 : (NF == 2 ? 3 : 2)) bp_
 // K1s -- back-projector, fp32, for D4-symmetric scenes (square grid centred on the ring
 // centre, n even, M % 4 == 0 -- every BASELINE configuration).  The 8 elements g of the
 // dihedral group map a pair (pixel p, sensor m) to (g p, g m) with the same distance, so
-// one delay evaluation serves 8 pairs: a thread owns a representative pixel of the
-// fundamental triangle (i >= n/2, n/2 <= j <= i) and accumulates its 8 image pixels, each
-// against the image sensor g m.  Per pair: 7/8 geometry + LDS.64 + 2 accumulate ops.
+// one delay evaluation serves up to 8 pairs:
 //   g:      0       1          2              3          4         5       6          7
 //   pixel: (i,j)  (n-1-j,i)  (n-1-i,n-1-j)  (j,n-1-i)  (i,n-1-j)  (j,i)  (n-1-i,j)  (n-1-j,n-1-i)
 //   sensor: m     m+M/4      m+M/2          m+3M/4     -m         M/4-m  M/2-m      3M/4-m
-// Diagonal representatives (i == j) have 4 distinct images (g = 0..3).
-// CTA = 16x16 representative pixels x a slice of the base sensors; chunks of 4 base
-// sensors = 32 image windows, one bulk copy per lane of the issuing warp.
+// Representative pixels are 32x32 tiles (tx, ty), tx >= ty, of the quadrant i, j >= n/2.
+// Off-diagonal tiles (tx > ty) lie strictly below the diagonal and use all 8 images; a
+// diagonal tile is closed under transposition, so all its pixels are representatives of
+// the 4 rotations (g = 0..3) -- no idle lanes.  A thread owns the 4 representatives
+// (i0 + lx + 8k, j0 + 4*warp + ly): every warp instruction covers an 8x4 footprint.
+//
+// Persistent CTAs: the (tile, chunk of kSymCS base sensors) sequence is cut host-side into
+// equal-cost contiguous ranges (off-diagonal chunks cost 2, diagonal 1), one per CTA.  The
+// image windows of a chunk (kSymCS x 8 windows of the pair table) are staged by the TMA
+// engine (one cp.async.bulk per window) into an nbuf-deep ring; the last warp to finish a
+// buffer refills it.  A CTA's partial sums of a tile go to one "slot" of part[]; the
+// epilogue kernel adds a tile's slots in slot order (deterministic) and applies the update.
+// Per pair: LDS.64 + FFMA + FADD, plus 1/NG of the delay (8 issue slots).
 // ===========================================================================
+constexpr int kSymTile = 32;
+constexpr int kSymCS = 2;        // base sensors per chunk (x 8 images = 16 windows)
+constexpr int kSymConsumers = 8; // consumer warps; warp 8 is the TMA producer
+constexpr int kSymThreads = 32 * (kSymConsumers + 1);
+
 struct BpSymArgs {
-    BpArgs b;            // common arguments (table, coordinates, update, split buffers)
-    int n;               // grid side (nx == ny)
-    int qtiles;          // 16x16 tiles per side of the quadrant
-    const int* tile_list;  // [ntiles] packed (tx << 16 | ty) of triangle tiles
+    const float2* table;     // [M][TS] pair table
+    const float* pxs;        // [n] scaled pixel x
+    const float* pys;        // [n]
+    const float* sxs;        // [M]
+    const float* sys;        // [M]
+    int n, M, TS, L, nbuf;
+    int lanemap;             // 1: half-warps own 4x4 blocks of the 8x4 footprint; 0: 8x2 rows
+    float qclamp;            // Q + 1.5
+    const int* chunks;       // [total] (tile << 16) | chunk index within the tile
+    const int* cta_chunk0;   // [grid + 1] chunk range of each CTA
+    const int* cta_slot0;    // [grid] first partial slot of each CTA
+    const int* tiles;        // [ntiles] (tx << 16) | ty
+    float* part;             // [slots][8][4][kThreads]
+    const DevState* st;      // solver mode: early exit once every frame stopped; else null
 };
 
-constexpr int kSymTile = 16;
-constexpr int kSymCS = 4;  // base sensors per chunk (x 8 images = 32 windows)
+// lane -> (column, row) inside a warp's 8x4 footprint.  With lanemap 1 each half-warp
+// covers a 4x4 block (delay span <= ~10 table entries at config 3), which lets the two
+// half-warp phases of an LDS.64 share wavefronts more often than 8x2 rows.
+__device__ __forceinline__ void sym_lane_xy(int lane, int lanemap, int& lx, int& ly) {
+    if (lanemap) {
+        lx = (lane & 3) | ((lane >> 4) << 2);
+        ly = (lane >> 2) & 3;
+    } else {
+        lx = lane & 7;
+        ly = lane >> 3;
+    }
+}
 
 __device__ __forceinline__ void sym_pixel(int g, int i, int j, int n, int& ig, int& jg) {
     const int ri = n - 1 - i, rj = n - 1 - j;
@@ -389,168 +422,226 @@ __device__ __forceinline__ int sym_sensor(int g, int m, int M) {
     return s < 0 ? s + M : s;
 }
 
-// IW > 0: image windows IW slots apart (compile-time, so the 8 image loads use immediate
-// offsets); IW == 0: a.L apart (runtime)
-template <bool EPI, bool CLAMP, int IW>
-__global__ void __launch_bounds__(kThreads, 4) bp_sym_f32_kernel(BpSymArgs A) {
-    const BpArgs& a = A.b;
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ float red_f[kThreads / 32];
-    __shared__ double red_d[kThreads / 32];
-    __shared__ int last_flag;
-    __shared__ uint32_t done_cnt[8];
-
-    int iter = 0;
-    if (EPI) {
-        if (a.st->all_stopped) return;
-        iter = a.st->iter;
-    }
-    const int n = A.n, h = n >> 1;
-    const int tile = blockIdx.x;
-    const int packed = __ldg(A.tile_list + tile);
-    const int i0 = h + (packed >> 16) * kSymTile, j0 = h + (packed & 0xffff) * kSymTile;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int i = i0 + 8 * (warp & 1) + (lane & 7);
-    const int j = j0 + 4 * (warp >> 1) + (lane >> 3);
-    const bool rep = i < n && j < n && j <= i;  // a representative of the fundamental triangle
-    const int ng = (i == j) ? 4 : 8;
-    const int mbase = blockIdx.y * a.ms;
-    const int mcount = min(a.ms, a.M - mbase);
-    const size_t P = (size_t)n * n;
-
-    const float px = __ldg(a.pxs + min(i, n - 1)), py = __ldg(a.pys + min(j, n - 1));
-    float acc[8], acc2[8];
+// one chunk: ns base sensors x 4 representatives x NG images
+template <int NG, int IW>
+__device__ __forceinline__ void sym_chunk(float (&acc)[4][8], const float (&px)[4], float py,
+                                          const float4* sc, int ns, uint32_t img_stride,
+                                          float qclamp) {
+    for (int s = 0; s < ns; ++s) {
+        const float4 q = sc[s];
+        const float ey = py - q.y;
+        const float ey2 = ey * ey;
+        const uint32_t adj = __float_as_uint(q.z);
 #pragma unroll
-    for (int g = 0; g < 8; ++g) acc[g] = acc2[g] = 0.f;
+        for (int k = 0; k < 4; ++k) {
+            const float ex = px[k] - q.x;
+            const float u = fminf(sqrt_approx(fmaf(ex, ex, ey2)), qclamp);
+            const float tb = __fadd_rd(u, kTwo23);  // 2^23 + floor(u)
+            const float f = u - (tb - kTwo23);
+            const uint32_t ad = adj + (__float_as_uint(tb) << 3);
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                const float2 v = lds_f2(ad + (uint32_t)g * (IW > 0 ? (uint32_t)IW * 8u : img_stride));
+                acc[k][g] += fmaf(f, v.y, v.x);  // (1-f) r[s0-1] + f r[s0]
+            }
+        }
+    }
+}
 
-    // windows [nbuf][kSymCS][8][L] float2 | sconst [nbuf][kSymCS] float4 | bars
-    const int WS = IW > 0 ? IW : a.L;  // window stride in slots
-    const size_t win_bytes = (size_t)a.nbuf * kSymCS * 8 * WS * 8;
+template <int IW>
+__global__ void __launch_bounds__(kSymThreads, 3) bp_sym_f32_kernel(BpSymArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (a.st && a.st->all_stopped) return;
+    const int c0 = a.cta_chunk0[blockIdx.x], c1 = a.cta_chunk0[blockIdx.x + 1];
+    if (c0 >= c1) return;
+    const int n = a.n, h = n >> 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    // windows [nbuf][kSymCS][8][WS] float2 | sconst [nbuf][kSymCS] float4 | full [nbuf] | empty [nbuf]
+    const int WS = IW > 0 ? IW : a.L;
+    const uint32_t img_stride = (uint32_t)WS * 8u;
+    const size_t win_bytes = (size_t)a.nbuf * kSymCS * 8 * img_stride;
     float4* sconst = reinterpret_cast<float4*>(smem + win_bytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + win_bytes + (size_t)a.nbuf * kSymCS * 16);
     const uint32_t win_s = smem_u32(smem);
-    const uint32_t bar_s = smem_u32(bars);
-    const uint32_t img_stride = (uint32_t)WS * 8u;  // bytes between the 8 image windows
+    const uint32_t full_s = smem_u32(smem + win_bytes + (size_t)a.nbuf * kSymCS * 16);
+    const uint32_t empty_s = full_s + 8u * a.nbuf;
 
-    const float X0 = __ldg(a.pxs + i0), X1 = __ldg(a.pxs + min(i0 + kSymTile - 1, n - 1));
-    const float Y0 = __ldg(a.pys + j0), Y1 = __ldg(a.pys + min(j0 + kSymTile - 1, n - 1));
-
-    // each buffer's mbarrier completes on 32 cp.async arrivals (one per lane of the filling
-    // warp, .noinc) plus one release arrive that publishes the sensor constants
     if (threadIdx.x == 0) {
         for (int b = 0; b < a.nbuf; ++b) {
-            mbar_init(bar_s + 8 * b, 33);
-            done_cnt[b] = 0;
+            mbar_init(full_s + 8 * b, 1);
+            mbar_init(empty_s + 8 * b, kSymConsumers);
         }
         fence_barrier_init();
     }
     __syncthreads();
 
-    const int nchunks = (mcount + kSymCS - 1) / kSymCS;
-    // lane = (base sensor c = lane >> 3, image g = lane & 7) owns one window's geometry; the
-    // 32 windows (384-736 B each) are copied warp-cooperatively with 16-B cp.async (LDGSTS):
-    // 32 one-window bulk copies per 32 interactions per thread saturate the TMA queue.
-    auto issue = [&](int c, int b) {
-        const int nb = min(kSymCS, mcount - c * kSymCS);
+    if (warp == kSymConsumers) {
+        // ---- producer warp: stage chunk c into buffer b once the consumers released it;
+        // lane = (base sensor cs = lane >> 3, image g = lane & 7) owns one window
         const int cs = lane >> 3, g = lane & 7;
-        const bool act = cs < nb;
-        int lo = 0;
-        const int m = mbase + c * kSymCS + min(cs, nb - 1);
-        const float sx = __ldg(a.sxs + m), sy = __ldg(a.sys + m);
-        {
+        int b = 0;
+        uint32_t phase = 0;
+        for (int c = c0; c < c1; ++c) {
+            if (c - c0 >= a.nbuf) mbar_wait(empty_s + 8 * b, phase ^ 1u);
+            const int packed = __ldg(a.chunks + c);
+            const int tp = __ldg(a.tiles + (packed >> 16));
+            const int tx = tp >> 16, ty = tp & 0xffff;
+            const int ng = (tx == ty) ? 4 : 8;
+            const int i0 = h + kSymTile * tx, j0 = h + kSymTile * ty;
+            const float X0 = __ldg(a.pxs + i0), X1 = __ldg(a.pxs + min(i0 + kSymTile - 1, n - 1));
+            const float Y0 = __ldg(a.pys + j0), Y1 = __ldg(a.pys + min(j0 + kSymTile - 1, n - 1));
+            const int m = (packed & 0xffff) * kSymCS + cs;
+            const bool act = cs < kSymCS && m < a.M && g < ng;
+            const int mm = min(m, a.M - 1);
+            const float sx = __ldg(a.sxs + mm), sy = __ldg(a.sys + mm);
             const float cx = fminf(fmaxf(sx, X0), X1), cy = fminf(fmaxf(sy, Y0), Y1);
-            float dmin = sqrtf((cx - sx) * (cx - sx) + (cy - sy) * (cy - sy));
-            if (CLAMP) dmin = fminf(dmin, a.qclamp);
-            lo = (int)floorf(dmin) - 1;
-            lo = max(lo, 0) & ~1;
-            lo = min(lo, a.TS - a.L);
+            const float dmin = fminf(sqrtf((cx - sx) * (cx - sx) + (cy - sy) * (cy - sy)), a.qclamp);
+            int lo = (int)floorf(dmin) - 1;
+            lo = min(max(lo, 0) & ~1, a.TS - a.L);
+            const uint32_t dst0 =
+                win_s + (uint32_t)((b * kSymCS + min(cs, kSymCS - 1)) * 8) * img_stride;
+            if (cs < kSymCS && g == 0)
+                sconst[b * kSymCS + cs] = make_float4(
+                    sx, sy, __uint_as_float(dst0 - 8u * (uint32_t)lo - 8u * kTwo23Bits), 0.f);
+            const uint32_t nact = __popc(__ballot_sync(0xffffffffu, act));
+            __syncwarp();
+            if (lane == 0) mbar_expect_tx(full_s + 8 * b, nact * (uint32_t)(a.L * 8));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (act)
+                bulk_g2s(dst0 + (uint32_t)g * img_stride,
+                         a.table + (size_t)sym_sensor(g, m, a.M) * a.TS + lo, (uint32_t)(a.L * 8),
+                         full_s + 8 * b);
+            if (++b == a.nbuf) { b = 0; phase ^= 1u; }
         }
-        const uint32_t dst0 = win_s + (uint32_t)((b * kSymCS + cs) * 8) * img_stride;
-        if (act && g == 0)
-            sconst[b * kSymCS + cs] =
-                make_float4(sx, sy, __uint_as_float(dst0 - 8u * (uint32_t)lo - 8u * kTwo23Bits), 0.f);
-        const uint32_t dst = dst0 + (uint32_t)g * img_stride;
-        const float2* src = a.table + (size_t)sym_sensor(g, m, a.M) * a.TS + lo;
-        const int pieces = a.L >> 1;  // 16-byte pieces per window
-        for (int wdw = 0; wdw < 8 * nb; ++wdw) {
-            const uint32_t dw = __shfl_sync(0xffffffffu, dst, wdw);
-            const unsigned long long sw =
-                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), wdw);
-            for (int q = lane; q < pieces; q += 32)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dw + 16u * q),
-                             "l"(sw + 16ull * q)
-                             : "memory");
-        }
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar_s + 8 * b)
-                     : "memory");
-        __syncwarp();
-        if (lane == 0)
-            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar_s + 8 * b)
-                         : "memory");
-    };
-    if (warp == 0) {
-        for (int c = 0; c < min(a.nbuf, nchunks); ++c) issue(c, c);
+        return;
     }
 
-    for (int c = 0; c < nchunks; ++c) {
-        const int b = c % a.nbuf;
-        mbar_wait(bar_s + 8 * b, (uint32_t)((c / a.nbuf) & 1));
-        const int nb = min(kSymCS, mcount - c * kSymCS);
-        const float4* sc = sconst + b * kSymCS;
-        for (int s = 0; s < nb; ++s) {
-            const float4 q = sc[s];
-            const float ey = py - q.y;
-            const float ex = px - q.x;
-            float u = sqrt_approx(fmaf(ex, ex, ey * ey));
-            if (CLAMP) u = fminf(u, a.qclamp);
-            const float tb = __fadd_rd(u, kTwo23);
-            const float f = u - (tb - kTwo23);
-            const uint32_t ad = __float_as_uint(q.z) + (__float_as_uint(tb) << 3);
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                const float2 v = lds_f2(ad + (uint32_t)g * (IW > 0 ? (uint32_t)IW * 8u : img_stride));
-                acc[g] = fmaf(f, v.y, acc[g]);
-                acc2[g] += v.x;
-            }
-        }
-        __syncwarp();
-        uint32_t prev = 0;
-        if (lane == 0) {
-            const uint32_t addr = smem_u32(&done_cnt[b]);
-            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(prev) : "r"(addr) : "memory");
-        }
-        prev = __shfl_sync(0xffffffffu, prev, 0);
-        if (prev == kThreads / 32 - 1) {
-            if (lane == 0) done_cnt[b] = 0;
-            if (c + a.nbuf < nchunks) issue(c + a.nbuf, b);
-        }
-    }
-    int pix[8];
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-        acc[g] += acc2[g];
-        int ig, jg;
-        sym_pixel(g, i, j, n, ig, jg);
-        pix[g] = (rep && g < ng) ? jg * n + ig : -1;
-    }
-
-    if (a.split > 1) {
+    // ---- consumer warps
+    int lx, ly;
+    sym_lane_xy(lane, a.lanemap, lx, ly);
+    float acc[4][8];
+    float px[4], py = 0.f;
+    int cur = -1, slot = a.cta_slot0[blockIdx.x] - 1;
+    bool diag = false;
+    auto flush = [&]() {
+        float* dst = a.part + (size_t)slot * 8 * 4 * kThreads + threadIdx.x;
 #pragma unroll
         for (int g = 0; g < 8; ++g)
-            if (pix[g] >= 0) a.gpart[(size_t)blockIdx.y * P + pix[g]] = acc[g];
-        if (!last_block(a.tile_cnt + tile, a.split, &last_flag)) return;
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-            float sum = 0.f;
-            if (pix[g] >= 0)
-                for (int q = 0; q < a.split; ++q) sum += __ldcg(a.gpart + (size_t)q * P + pix[g]);
-            acc[g] = sum;
+            for (int k = 0; k < 4; ++k)
+                if (g < 4 || !diag) dst[(g * 4 + k) * kThreads] = acc[k][g];
+    };
+    int b = 0;
+    uint32_t phase = 0;
+    for (int c = c0; c < c1; ++c) {
+        const int packed = __ldg(a.chunks + c);
+        const int t = packed >> 16;
+        if (t != cur) {
+            if (cur >= 0) flush();
+            ++slot;
+            cur = t;
+            const int tp = __ldg(a.tiles + t);
+            const int tx = tp >> 16, ty = tp & 0xffff;
+            diag = tx == ty;
+            const int i0 = h + kSymTile * tx, j0 = h + kSymTile * ty;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                px[k] = __ldg(a.pxs + min(i0 + lx + 8 * k, n - 1));
+#pragma unroll
+                for (int g = 0; g < 8; ++g) acc[k][g] = 0.f;
+            }
+            py = __ldg(a.pys + min(j0 + 4 * warp + ly, n - 1));
         }
+        mbar_wait(full_s + 8 * b, phase);
+        const int ns = min(kSymCS, a.M - (packed & 0xffff) * kSymCS);
+        const float4* sc = sconst + b * kSymCS;
+        if (diag) sym_chunk<4, IW>(acc, px, py, sc, ns, img_stride, a.qclamp);
+        else sym_chunk<8, IW>(acc, px, py, sc, ns, img_stride, a.qclamp);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_s + 8 * b);
+        if (++b == a.nbuf) { b = 0; phase ^= 1u; }
+    }
+    flush();
+}
+
+// K1s epilogue: CTA (tile, image g) adds the tile's partial slots in order, maps the
+// representatives to image g, and writes gscale * K^T r (EPI == false) or runs the fused
+// update of recon.py:327-338 with the block statistics of the next projector scale.
+struct BpSymEpiArgs {
+    const float* part;        // [slots][8][4][kThreads]
+    const int* tile_slot0;    // [ntiles + 1]
+    const int* tiles;         // [ntiles]
+    int n, bits, lanemap;
+    float gscale;
+    float* out;               // EPI == false
+    float* xb0;               // EPI == true: x from xb[iter & 1] to xb[(iter + 1) & 1]
+    float* xb1;
+    const DevParams* prm;
+    DevState* st;
+    double* part_bp;          // [grid][4]
+};
+
+template <bool EPI>
+__global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
+    __shared__ float red_f[kThreads / 32];
+    __shared__ double red_d[kThreads / 32];
+    __shared__ int last_flag;
+    int iter = 0;
+    if (EPI) {
+        if (a.st->all_stopped) return;
+        iter = a.st->iter;
+    }
+    const int t = blockIdx.x >> 3, g = blockIdx.x & 7;
+    const int tp = __ldg(a.tiles + t);
+    const int tx = tp >> 16, ty = tp & 0xffff;
+    const bool active = !(tx == ty && g >= 4);
+    const int n = a.n, h = n >> 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int lx, ly;
+    sym_lane_xy(lane, a.lanemap, lx, ly);
+    const int i0 = h + kSymTile * tx, j0 = h + kSymTile * ty;
+    const int j = j0 + 4 * warp + ly;
+    const int s0 = __ldg(a.tile_slot0 + t), s1 = __ldg(a.tile_slot0 + t + 1);
+    // the tile's slots in order; 4 representatives per thread loaded together
+    float sum[4] = {0.f, 0.f, 0.f, 0.f};
+    if (active) {
+        const float* src = a.part + (size_t)g * 4 * kThreads + threadIdx.x;
+        int s = s0;
+        for (; s + 1 < s1; s += 2) {
+            float v[2][4];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    v[u][k] = __ldcg(src + (size_t)(s + u) * 8 * 4 * kThreads + k * kThreads);
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) sum[k] += v[u][k];
+        }
+        if (s < s1) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sum[k] += __ldcg(src + (size_t)s * 8 * 4 * kThreads + k * kThreads);
+        }
+    }
+    float val[4];
+    int pix[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int i = i0 + lx + 8 * k;
+        pix[k] = -1;
+        if (active && i < n && j < n) {
+            int ig, jg;
+            sym_pixel(g, i, j, n, ig, jg);
+            pix[k] = jg * n + ig;
+        }
+        val[k] = a.gscale * sum[k];
     }
     if (!EPI) {
 #pragma unroll
-        for (int g = 0; g < 8; ++g)
-            if (pix[g] >= 0) a.out[pix[g]] = a.gscale * acc[g];
+        for (int k = 0; k < 4; ++k)
+            if (pix[k] >= 0) a.out[pix[k]] = val[k];
         return;
     }
     const float* x = (iter & 1) ? a.xb1 : a.xb0;
@@ -560,23 +651,25 @@ __global__ void __launch_bounds__(kThreads, 4) bp_sym_f32_kernel(BpSymArgs A) {
     const bool nonneg = a.prm->nonneg != 0;
     float mx = 0.f, l1 = 0.f;
     int bad = 0;
+    if (!a.st->fr[0].stopped) {
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
-        const int p = pix[g];
-        if (p < 0) continue;
-        float gr = a.gscale * acc[g];
-        if (beta > 0.f) gr += beta * tv_grad_at<float>(x, p, p % n, p / n, n, n, eps * eps);
-        const float xn = prox<float>(x[p] - eta * gr, lam, nonneg);
-        xo[p] = xn;
-        if (!isfinite(xn)) bad = 1;
-        mx = fmaxf(mx, fabsf(xn));
-        l1 += fabsf(xn);
+        for (int k = 0; k < 4; ++k) {
+            const int p = pix[k];
+            if (p < 0) continue;
+            float gr = val[k];
+            if (beta > 0.f) gr += beta * tv_grad_at<float>(x, p, p % n, p / n, n, n, eps * eps);
+            const float xn = prox<float>(x[p] - eta * gr, lam, nonneg);
+            xo[p] = xn;
+            if (!isfinite(xn)) bad = 1;
+            mx = fmaxf(mx, fabsf(xn));
+            l1 += fabsf(xn);
+        }
     }
     mx = block_max(mx, red_f);
     const float l1b = block_sum(l1, red_f);
     const int badb = __syncthreads_or(bad);
     if (threadIdx.x == 0) {
-        double* pp = a.part + 4 * (size_t)tile;
+        double* pp = a.part_bp + 4 * (size_t)blockIdx.x;
         pp[0] = mx;
         pp[1] = l1b;
         pp[2] = badb;
@@ -584,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 4) bp_sym_f32_kernel(BpSymArgs A) {
     if (last_block(&a.st->cnt_bp, gridDim.x, &last_flag)) {
         double m2 = 0.0, s2 = 0.0, b2 = 0.0;
         for (int q = threadIdx.x; q < (int)gridDim.x; q += kThreads) {
-            const double* pp = a.part + 4 * (size_t)q;
+            const double* pp = a.part_bp + 4 * (size_t)q;
             m2 = fmax(m2, pp[0]);
             s2 += pp[1];
             b2 += pp[2];

@@ -35,7 +35,10 @@ lib = N.load()
 ms = (ctypes.c_float * 3)()
 n = ctypes.c_int32()
 s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+best = [1e30] * 3
 for _ in range(a.reps):
     N.check(lib.pk_profile_iterations(op.handle, ctypes.byref(params), y.data_ptr(), ms, ctypes.byref(n), s))
+    best = [min(b, v) for b, v in zip(best, ms)]
 torch.cuda.synchronize()
-print("per-kernel ms over", a.iterations, "iterations:", list(ms), "launches", n.value)
+us = [1e3 * v / a.iterations for v in best]
+print("per-launch us: K1 %.1f  K2 %.1f  K3 %.1f  (sum %.1f; launches %d)" % (us[0], us[1], us[2], sum(us), n.value))
