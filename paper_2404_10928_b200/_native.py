@@ -15,7 +15,7 @@ import threading
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
-LIB_PATH = os.path.join(_PKG, "libpactgpu.so")
+LIB_PATH = os.environ.get("PK_LIB") or os.path.join(_PKG, "libpactgpu.so")  # PK_LIB: experiment builds
 SOURCES = [
     os.path.join(_PKG, "csrc", "pactgpu.cu"),
     os.path.join(_PKG, "csrc", "pk_kernels.cuh"),
@@ -134,7 +134,7 @@ def nvcc_command(out: str = LIB_PATH) -> list[str]:
         "-gencode", "arch=compute_100a,code=sm_100a",
         "-O3", "-lineinfo", "-std=c++17",
         "-I", os.path.join(_ROOT, "include"),
-        "-shared", "-Xcompiler", "-fPIC",
+        "-shared", "-Xcompiler", "-fPIC", "-lpthread",
         "-o", out,
         os.path.join(_PKG, "csrc", "pactgpu.cu"),
     ]

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "pactgpu.h"
@@ -112,7 +113,7 @@ void free_plan(pk_plan* p) {
                     p->status_dev, p->part_bp, p->part_tv, p->part_r, p->part_misc, p->state,
                     p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt, p->sym_tiles,
                     p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0, p->sym_tile_slot0,
-                    p->sym_part};
+                    p->sym_part, p->fsym_win, p->fsym_lo};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
@@ -168,7 +169,10 @@ cudaError_t opt_in_smem(int device) {
     smem_kernels<1>(ks);
     smem_kernels<2>(ks);
     smem_kernels<4>(ks);
-    ks.push_back((const void*)fp_sym4_f32_kernel<false>);
+    for (const void* k : {(const void*)fp_sym_f32_kernel<96>, (const void*)fp_sym_f32_kernel<128>,
+                          (const void*)fp_sym_f32_kernel<184>, (const void*)fp_sym_f32_kernel<256>,
+                          (const void*)fp_sym_f32_kernel<320>})
+        ks.push_back(k);
     ks.push_back(sym_kernel_ptr(0));
     for (int iw : kSymIW) ks.push_back(sym_kernel_ptr(iw));
     ks.push_back((const void*)fp_f64_kernel);
@@ -197,18 +201,23 @@ template <int NF>
 void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
     dim3 grid(p->fp_tiles_x * p->fp_tiles_y, p->fp_groups);
     if (p->dtype == PK_F32 && NF == 1 && p->fsym) {
-        FpArgs a{};
+        FpSymArgs a{};
         a.x = static_cast<const float*>(x);
         a.xb0 = static_cast<const float*>(p->xbuf[0]);
         a.xb1 = static_cast<const float*>(p->xbuf[1]);
         a.pxs = p->pxs; a.pys = p->pys; a.sxs = p->sxs; a.sys = p->sys;
-        a.acc = p->acc;
-        a.nx = p->nx; a.ny = p->ny; a.M = p->M; a.Q = p->Q; a.T = p->fsym_T; a.L = p->fsym_L;
-        a.tiles_x = p->fsym_qt;
+        a.win = p->fsym_win; a.win_lo = p->fsym_lo;
+        a.n = p->nx; a.M = p->M; a.Q = p->Q; a.groups = p->fp_groups; a.qt = p->fsym_qt;
         a.qclamp = (float)p->Q + 1.5f;
         a.st = p->state; a.part_tv = p->part_tv; a.solver = solver;
-        const dim3 g2(p->fsym_qt * p->fsym_qt, p->fp_groups);
-        fp_sym4_f32_kernel<false><<<g2, kThreads, p->fsym_smem, s>>>(a);
+        const int units = p->fsym_qt * p->fsym_qt * p->fp_groups;
+        switch (p->fsym_L) {
+            case 96: fp_sym_f32_kernel<96><<<units, kFsThreads, p->fsym_smem, s>>>(a); break;
+            case 128: fp_sym_f32_kernel<128><<<units, kFsThreads, p->fsym_smem, s>>>(a); break;
+            case 184: fp_sym_f32_kernel<184><<<units, kFsThreads, p->fsym_smem, s>>>(a); break;
+            case 256: fp_sym_f32_kernel<256><<<units, kFsThreads, p->fsym_smem, s>>>(a); break;
+            default: fp_sym_f32_kernel<320><<<units, kFsThreads, p->fsym_smem, s>>>(a); break;
+        }
         return;
     }
     if (p->dtype == PK_F32) {
@@ -241,7 +250,9 @@ template <int NF>
 void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq, int solver,
                        cudaStream_t s) {
     const int chunks = p->fin_chunks;
-    const size_t sm = (size_t)((p->Q + chunks - 1) / chunks + 1) * tsize(p);
+    const size_t clen1 = (size_t)((p->Q + chunks - 1) / chunks + 1);
+    size_t sm = clen1 * tsize(p);
+    if (NF == 1 && p->fsym) sm = ((sm + 15) & ~(size_t)15) + clen1 * 4;  // gathered window sums
     const dim3 grid(p->M * chunks, NF);
     if (p->dtype == PK_F32) {
         FinArgs<float> a{};
@@ -251,9 +262,14 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
         a.M = p->M; a.Q = p->Q; a.TS = p->TS; a.w = p->w;
         a.st = p->state; a.prm = p->params; a.io = p->io; a.part_r = p->part_r;
         a.part_tv = p->part_tv;
-        a.ntv = (NF == 1 && p->fsym) ? p->fsym_qt * p->fsym_qt : p->fp_tiles_x * p->fp_tiles_y;
+        a.ntv = (NF == 1 && p->fsym) ? p->fsym_qt * p->fsym_qt * p->fp_groups
+                                     : p->fp_tiles_x * p->fp_tiles_y;
         a.sumsq_out = sumsq;
         a.solver = solver;
+        if (NF == 1 && p->fsym) {
+            a.win = p->fsym_win; a.win_lo = p->fsym_lo; a.win_lw = p->fsym_L;
+            a.groups = p->fp_groups; a.ntiles = p->fsym_qt * p->fsym_qt;
+        }
         a.atrick = p->bp_atrick;
         a.chunks = chunks;
         finalize_kernel<float, NF><<<grid, kThreads, sm, s>>>(a);
@@ -393,8 +409,10 @@ int launch_maxabs(pk_plan* p, const void* x, cudaStream_t s) {
     return PK_OK;
 }
 int launch_fp(pk_plan* p, const void* x, int solver, cudaStream_t s) {
-    // the fixed-point accumulator must be zero on entry (finalize only reads it)
-    PK_CUDA(cudaMemsetAsync(p->acc, 0, (size_t)p->M * p->Q * p->nf * sizeof(long long), s));
+    // the fixed-point accumulator must be zero on entry (finalize only reads it); the
+    // symmetric projector writes whole windows instead
+    if (!(p->fsym && p->nf == 1))
+        PK_CUDA(cudaMemsetAsync(p->acc, 0, (size_t)p->M * p->Q * p->nf * sizeof(long long), s));
     PK_DISPATCH(launch_fp_t, p, x, solver, s);
     return PK_OK;
 }
@@ -709,20 +727,60 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 p->sym_slots = slot + 1;
             }
         }
-        // rotation-symmetric projector (4 windows per lane, quadrant tiles of 32 x 32)
+        // rotation-symmetric projector (fp_sym_f32_kernel): one CTA per (64 x 64 quadrant tile,
+        // group of 32 base sensors); used when there are enough units to fill the SMs
         const char* ev2 = getenv("PK_FSYM");
-        p->fsym = (p->sym && (ev2 ? atoi(ev2) != 0 : false)) ? 1 : 0;  // opt-in (slower)
+        p->fsym = (p->sym && (ev2 ? atoi(ev2) != 0 : false)) ? 1 : 0;  // opt-in
         if (p->fsym) {
-            p->fsym_T = 32;
-            p->fsym_qt = (n / 2 + p->fsym_T - 1) / p->fsym_T;
-            p->fsym_L = (int)std::ceil(tile_diag(p->fsym_T)) + 6;
-            p->fsym_smem = p->fsym_L * 4 * 32 * 4 + (kThreads / 32) * (p->fsym_T + kFpBatch) * 3 * 16;
-            if (p->fsym_smem > 110 * 1024) p->fsym = 0;
-            // fixed-point bound of the 32 x 32 windows (may be tighter than the generic tile's)
-            double nc = 1.5 * (p->fsym_T * std::sqrt(2.0) + 2) * (2.0 / std::max(h, 1e-12) + 2);
-            if (p->min_delay < 8.0 * p->fsym_T * std::max(h, 1.0)) nc = (double)p->fsym_T * p->fsym_T;
-            nc = std::min(nc, (double)p->fsym_T * p->fsym_T);
+            p->fsym_T = kFsTile;
+            p->fsym_qt = (n / 2 + kFsTile - 1) / kFsTile;
+            const int need = (int)std::ceil(tile_diag(kFsTile)) + 6;
+            p->fsym_L = 0;
+            for (int lw : {96, 128, 184, 256, 320})
+                if (need <= lw) { p->fsym_L = lw; break; }
+            p->fsym_smem = 4 * p->fsym_L * 32 * 4 + (kFsThreads / 32) * (32 + kFsBatch) * 32;
+            int sms = 0;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+            const int units = p->fsym_qt * p->fsym_qt * p->fp_groups;
+            if (p->fsym_L == 0 || p->fsym_smem > 200 * 1024 ||
+                (units < sms && !(ev2 && atoi(ev2) != 0)))
+                p->fsym = 0;
+        }
+        if (p->fsym) {
+            // fixed-point bound of the 64 x 64 windows (may be tighter than the generic tile's)
+            double nc = 1.5 * (kFsTile * std::sqrt(2.0) + 2) * (2.0 / std::max(h, 1e-12) + 2);
+            if (p->min_delay < 8.0 * kFsTile * std::max(h, 1.0)) nc = (double)kFsTile * kFsTile;
+            nc = std::min(nc, (double)kFsTile * kFsTile);
             p->fp_bits = std::min(p->fp_bits, std::min(22, 30 - ceil_log2(nc)));
+            // the gathered sums are int32: bound the pixels that can reach one sample (s0 in
+            // [s-1, s+2], a one-sample margin for fp32 delays) exactly, from the D4 base
+            // sensors 0..M/8
+            const int mq = std::min(p->M, p->M / 8 + 2);
+            std::vector<int> worst(mq, 0);
+            auto count = [&](int m0, int m1) {
+                std::vector<int> hist(p->Q + 4);
+                for (int m = m0; m < m1; ++m) {
+                    std::fill(hist.begin(), hist.end(), 0);
+                    for (int j = 0; j < p->ny; ++j)
+                        for (int i = 0; i < p->nx; ++i) {
+                            const double u = std::hypot(X[i] - SP[2 * m], Y[j] - SP[2 * m + 1]) / p->cdt;
+                            const long s0 = (long)std::floor(u);
+                            if (s0 >= 0 && s0 <= p->Q + 1) ++hist[s0 + 1];
+                        }
+                    int w = 0;
+                    for (int t = 0; t + 3 < (int)hist.size(); ++t)
+                        w = std::max(w, hist[t] + hist[t + 1] + hist[t + 2] + hist[t + 3]);
+                    worst[m] = w;
+                }
+            };
+            {
+                const int nt = std::max(1, std::min(16, (int)std::thread::hardware_concurrency()));
+                std::vector<std::thread> th;
+                for (int q = 0; q < nt; ++q) th.emplace_back(count, mq * q / nt, mq * (q + 1) / nt);
+                for (auto& t : th) t.join();
+            }
+            const int ncg = *std::max_element(worst.begin(), worst.end());
+            p->fp_bits = std::min(p->fp_bits, 31 - ceil_log2((double)ncg + 1.0));
         }
     }
     p->misc_blocks = std::max(1, std::min(1024, (p->P + kThreads - 1) / kThreads));
@@ -755,8 +813,12 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[1]), (size_t)p->P * ts * nf));
     const int ntile_max = std::max(p->bp_tiles_x * p->bp_tiles_y, p->sym ? 8 * p->sym_ntiles : 0);
     A(alloc(p, &p->part_bp, (size_t)4 * nf * std::max(ntile_max, (p->P + kThreads - 1) / kThreads)));
-    A(alloc(p, &p->part_tv, (size_t)std::max(p->fp_tiles_x * p->fp_tiles_y,
-                                             p->fsym ? p->fsym_qt * p->fsym_qt : 0) * nf));
+    const int fsym_units = p->fsym ? p->fsym_qt * p->fsym_qt * p->fp_groups : 0;
+    A(alloc(p, &p->part_tv, (size_t)std::max(p->fp_tiles_x * p->fp_tiles_y, fsym_units) * nf));
+    if (p->fsym) {
+        A(alloc(p, &p->fsym_win, (size_t)fsym_units * 4 * 32 * p->fsym_L));
+        A(alloc(p, &p->fsym_lo, (size_t)fsym_units * 32));
+    }
     p->fin_chunks = std::max(1, std::min(8, p->Q / 1024));
     A(alloc(p, &p->part_r, (size_t)p->M * nf * p->fin_chunks));
     A(alloc(p, &p->part_misc, (size_t)4 * p->misc_blocks * nf));

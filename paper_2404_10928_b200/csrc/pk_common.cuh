@@ -278,8 +278,10 @@ struct pk_plan {
         *sym_cta_slot0 = nullptr, *sym_tile_slot0 = nullptr;
     float* sym_part = nullptr;  // [slots][8][4][kThreads] partial sums
     std::vector<int> sym_h[5];  // host copies: tiles, chunks, cta_chunk0, cta_slot0, tile_slot0
-    // rotation-symmetric projector (fp_sym4_f32_kernel)
+    // rotation-symmetric projector (fp_sym_f32_kernel)
     int fsym = 0, fsym_T = 0, fsym_qt = 0, fsym_L = 0, fsym_smem = 0;
+    int32_t* fsym_win = nullptr;  // [units][4][32][L] window sums of the last projection
+    int32_t* fsym_lo = nullptr;   // [units][32] first trace index of each window
     int fin_chunks = 1;  // residual kernel: sample chunks per sensor
     float* bp_gpart = nullptr;
     uint32_t* bp_tile_cnt = nullptr;

@@ -597,46 +597,43 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
     const int tx = tp >> 16, ty = tp & 0xffff;
     const bool active = !(tx == ty && g >= 4);
     const int n = a.n, h = n >> 1;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int lx, ly;
-    sym_lane_xy(lane, a.lanemap, lx, ly);
     const int i0 = h + kSymTile * tx, j0 = h + kSymTile * ty;
-    const int j = j0 + 4 * warp + ly;
     const int s0 = __ldg(a.tile_slot0 + t), s1 = __ldg(a.tile_slot0 + t + 1);
-    // the tile's slots in order; 4 representatives per thread loaded together
-    float sum[4] = {0.f, 0.f, 0.f, 0.f};
+    // thread owns elements 4*tid .. 4*tid+3 of the slot vector [k][consumer thread]: one
+    // representative column k, consumer threads ct .. ct+3; every slot is one 16-B load
+    const int k = threadIdx.x >> 6, ct = (threadIdx.x & 63) * 4;
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
     if (active) {
-        const float* src = a.part + (size_t)g * 4 * kThreads + threadIdx.x;
-        int s = s0;
-        for (; s + 1 < s1; s += 2) {
-            float v[2][4];
+        const float4* src = reinterpret_cast<const float4*>(a.part + (size_t)g * 4 * kThreads) + threadIdx.x;
+        const size_t stride = 8 * 4 * kThreads / 4;  // float4s per slot
+        // every slot load in flight at once (a tile has ~ grid / tiles + 1 slots)
+        for (int sb = s0; sb < s1; sb += 16) {
+            float4 v[16];
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
+            for (int u = 0; u < 16; ++u)
+                v[u] = (sb + u < s1) ? __ldcg(src + (size_t)(sb + u) * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    v[u][k] = __ldcg(src + (size_t)(s + u) * 8 * 4 * kThreads + k * kThreads);
-#pragma unroll
-            for (int u = 0; u < 2; ++u)
-#pragma unroll
-                for (int k = 0; k < 4; ++k) sum[k] += v[u][k];
-        }
-        if (s < s1) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) sum[k] += __ldcg(src + (size_t)s * 8 * 4 * kThreads + k * kThreads);
+            for (int u = 0; u < 16; ++u) {
+                sum.x += v[u].x; sum.y += v[u].y; sum.z += v[u].z; sum.w += v[u].w;
+            }
         }
     }
+    const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
     float val[4];
     int pix[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int i = i0 + lx + 8 * k;
-        pix[k] = -1;
+    for (int u = 0; u < 4; ++u) {
+        const int c = ct + u;  // consumer thread of the main kernel
+        int lx, ly;
+        sym_lane_xy(c & 31, a.lanemap, lx, ly);
+        const int i = i0 + lx + 8 * k, j = j0 + 4 * (c >> 5) + ly;
+        pix[u] = -1;
         if (active && i < n && j < n) {
             int ig, jg;
             sym_pixel(g, i, j, n, ig, jg);
-            pix[k] = jg * n + ig;
+            pix[u] = jg * n + ig;
         }
-        val[k] = a.gscale * sum[k];
+        val[u] = a.gscale * sv[u];
     }
     if (!EPI) {
 #pragma unroll
@@ -1033,176 +1030,208 @@ __global__ void __launch_bounds__(kThreads, NF == 1 ? 4 : (NF == 2 ? 3 : 2)) fp_
 }
 
 // ===========================================================================
-// K2s -- projector, fp32, for rotation-symmetric scenes (same conditions as K1s).  The
-// 4 rotations r^g by 90 degrees map a pair (pixel p, sensor m) to (r^g p, m + g*M/4) with
-// the same distance: lane l owns base sensor m = 32*group + l and 4 windows, one per
-// rotation image sensor m + g*M/4; the CTA's pixels are a T x T tile of the first quadrant
-// (i, j >= n/2) and each delay is applied to the 4 image pixels
-//   g = 0: (i, j)   1: (n-1-j, i)   2: (n-1-i, n-1-j)   3: (j, n-1-i).
-// Same fixed-point arithmetic and window layout as K2 ([slot][image][lane]).
+// K2s -- projector, fp32, for D4-symmetric scenes (same conditions as K1s).  The 4
+// rotations r^g by 90 degrees map a pair (pixel p, sensor m) to (r^g p, m + g*M/4) with the
+// same distance, so a delay evaluated for a pixel of the first quadrant (i, j >= n/2) serves
+// its 4 rotation images
+//   g = 0: (i, j)   1: (n-1-j, i)   2: (n-1-i, n-1-j)   3: (j, n-1-i)
+// against the sensors m + g*M/4.  CTA = unit = (64x64 quadrant tile, group of 32 base
+// sensors); lane l owns base sensor m = 32*group + l and 4 windows (one per image sensor) of
+// LW slots; window word (g, slot k, lane) sits at (g*LW + k)*32 + lane, so lane l always hits
+// bank l: the scatter is conflict free.  Contributions are the integers of fp_f32_kernel:
+// xq = rint(x*scale), a = rint(x*scale*f), b = xq - a, added with red.shared.add.s32 at trace
+// index s0 (a) and s0-1 (b).  At the end the unit stores its windows, transposed to
+// [g][sensor][slot], into its own slice of a global window array (plain coalesced stores, no
+// global atomics); the residual kernel gathers, for every trace sample, the windows that cover
+// it in a fixed order (deterministic integer sums).
+// Per pair: 2/4 LDS.128 (broadcast record) + 7/4 delay + FFMA + 2 IADD + 2 ATOMS.
 // ===========================================================================
-template <bool CLAMP>
-__global__ void __launch_bounds__(kThreads, 3) fp_sym4_f32_kernel(FpArgs a) {
+constexpr int kFsTile = 64;      // quadrant tile side (rows are scattered as two 32-pixel pieces)
+constexpr int kFsBatch = 4;      // records per scatter batch (16 independent atomic pairs)
+constexpr int kFsThreads = 512;  // 16 warps share the windows (occupancy at 2 CTAs per SM)
+
+struct FpSymArgs {
+    const float* x;          // standalone input (nullptr: solver mode, xb[(iter+1)&1])
+    const float* xb0;
+    const float* xb1;
+    const float* pxs;
+    const float* pys;
+    const float* sxs;
+    const float* sys;
+    int32_t* win;            // [units][4][32][LW] window sums (unit = tile * groups + group)
+    int32_t* win_lo;         // [units][32] first trace index of each lane's windows
+    int n, M, Q, groups, qt; // groups = ceil(M/32), qt = quadrant tiles per side
+    float qclamp;
+    DevState* st;
+    double* part_tv;         // solver mode: per-unit TV(x) partial (group-0 units, else 0)
+    int solver;
+};
+
+template <int LW>
+__global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ float red_f[kThreads / 32];
-    constexpr int G = 4;
-    constexpr int RV = 3;  // record: px, {xs, xq} x 4 -> 9 floats in 3 float4
+    __shared__ float red_f[kFsThreads / 32];
     int iter = 0;
     if (a.solver) {
         if (a.st->all_stopped) return;
         iter = a.st->iter;
     }
-    const float* x = a.x ? a.x : ((iter & 1) ? a.xb0 : a.xb1);
+    const float* x = a.x ? a.x : ((iter & 1) ? a.xb0 : a.xb1);  // bp wrote xb[(iter+1)&1]
     const float scale = a.st->fr[0].scale32;
-    const int n = a.nx, h = n >> 1;
-    const int T = a.T;
-    const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
-    const int i0 = h + tx * T, j0 = h + ty * T;
+    const int n = a.n, h = n >> 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int m = blockIdx.y * 32 + lane;
-    const bool sensor_ok = m < a.M;
-    const int q4 = a.M >> 2;
-    const float sx = __ldg(a.sxs + min(m, a.M - 1)), sy = __ldg(a.sys + min(m, a.M - 1));
-
+    constexpr int WW = 4 * LW * 32;  // window words
     int32_t* win = reinterpret_cast<int32_t*>(smem);
-    float4* rows = reinterpret_cast<float4*>(smem + (size_t)a.L * G * 32 * 4);
-    float4* rec = rows + (size_t)warp * (T + kFpBatch) * RV;
+    // per-warp record buffer: 2 float4 per pixel {px, xs0, xs1, xs2}, {xs3, xqb0, xqb1, xqb2}
+    float4* rec = reinterpret_cast<float4*>(smem + (size_t)WW * 4) + (size_t)warp * (32 + kFsBatch) * 2;
+    const uint32_t win_s = smem_u32(win);
 
-    for (int q = threadIdx.x; q < a.L * G * 32; q += kThreads) win[q] = 0;
-    const float X0 = __ldg(a.pxs + i0), X1 = __ldg(a.pxs + min(i0 + T - 1, n - 1));
-    const float Y0 = __ldg(a.pys + j0), Y1 = __ldg(a.pys + min(j0 + T - 1, n - 1));
+    const int u = blockIdx.x;
+    const int tile = u / a.groups, grp = u % a.groups;
+    const int i0 = h + kFsTile * (tile % a.qt), j0 = h + kFsTile * (tile / a.qt);
+    const int jend = min(j0 + kFsTile, n);
+    const int m = grp * 32 + lane;
+    const bool sensor_ok = m < a.M;
+    const int mm = min(m, a.M - 1);
+    const float sx = __ldg(a.sxs + mm), sy = __ldg(a.sys + mm);
+    // window: trace indices [lo, lo + LW) of this tile
+    const float X0 = __ldg(a.pxs + i0), X1 = __ldg(a.pxs + min(i0 + kFsTile - 1, n - 1));
+    const float Y0 = __ldg(a.pys + j0), Y1 = __ldg(a.pys + jend - 1);
     const float cx = fminf(fmaxf(sx, X0), X1), cy = fminf(fmaxf(sy, Y0), Y1);
-    float dmin = sqrtf((cx - sx) * (cx - sx) + (cy - sy) * (cy - sy));
-    if (CLAMP) dmin = fminf(dmin, a.qclamp);
+    const float dmin = fminf(sqrtf((cx - sx) * (cx - sx) + (cy - sy) * (cy - sy)), a.qclamp);
     const int lo = (int)floorf(dmin) - 2;
-    const uint32_t adj = smem_u32(win) + 4u * (uint32_t)lane - (128u * G) * (uint32_t)lo -
-                         (128u * G) * kTwo23Bits;
+    // word (g, k, lane) at (g*LW + k)*32 + lane, k = t - lo for trace index t
+    const uint32_t adj = win_s + 4u * (uint32_t)lane - 128u * (uint32_t)lo - 128u * kTwo23Bits;
+    {
+        int4* w4 = reinterpret_cast<int4*>(win);
+        for (int q = threadIdx.x; q < WW / 4; q += kFsThreads) w4[q] = make_int4(0, 0, 0, 0);
+    }
     __syncthreads();
 
     float tv = 0.f;
-    const bool do_tv = a.solver && blockIdx.y == 0;
-    const int jend = min(T, n - j0);
-    for (int r = warp; r < jend; r += kThreads / 32) {
-        const int jj = j0 + r;
-        int cnt = 0;
-        for (int cc = 0; cc < T; cc += 32) {
-            const int ii = i0 + cc + lane;
-            const bool in = ii < n && cc + lane < T;
-            float xv[G] = {0.f, 0.f, 0.f, 0.f};
-            if (in) {
-                const int pg[G] = {jj * n + ii, ii * n + (n - 1 - jj), (n - 1 - jj) * n + (n - 1 - ii),
-                                   (n - 1 - ii) * n + jj};
+    const bool do_tv = a.solver && grp == 0;
+    // pieces pc = (row warp + 16*(pc / P2), 32-pixel piece pc % P2) of this warp; the 4 image
+    // values of the next piece are loaded while the current one scatters
+    constexpr int P2 = kFsTile / 32;
+    constexpr int NW = kFsThreads / 32;
+    auto piece_x = [&](int pc, float (&v)[4]) {
+        const int jj = j0 + warp + NW * (pc / P2);
+        const int ii = i0 + 32 * (pc % P2) + lane;
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    xv[g] = x[pg[g]];
-                    if (do_tv) {  // exact anisotropic TV over the 4 image pixels
-                        const int pi = pg[g] % n, pj = pg[g] / n;
-                        if (pi + 1 < n) tv += fabsf(x[pg[g] + 1] - xv[g]);
-                        if (pj + 1 < n) tv += fabsf(x[pg[g] + n] - xv[g]);
-                    }
-                }
-            }
-            const bool nz = xv[0] != 0.f || xv[1] != 0.f || xv[2] != 0.f || xv[3] != 0.f;
-            const uint32_t bal = __ballot_sync(0xffffffffu, nz);
-            if (nz) {
-                float rv[4 * RV];
-                rv[0] = __ldg(a.pxs + ii);
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const float xs = xv[g] * scale;
-                    rv[1 + 2 * g] = xs;
-                    rv[2 + 2 * g] = __int_as_float(__float_as_int(xs + kMagic));
-                }
-                rv[9] = rv[10] = rv[11] = 0.f;
-                float4* dst = rec + (size_t)(cnt + __popc(bal & ((1u << lane) - 1u))) * RV;
-#pragma unroll
-                for (int v = 0; v < RV; ++v)
-                    dst[v] = make_float4(rv[4 * v], rv[4 * v + 1], rv[4 * v + 2], rv[4 * v + 3]);
-            }
-            cnt += __popc(bal);
+        for (int g = 0; g < 4; ++g) v[g] = 0.f;
+        if (jj < jend && ii < n) {
+            v[0] = x[jj * n + ii];
+            v[1] = x[ii * n + (n - 1 - jj)];
+            v[2] = x[(n - 1 - jj) * n + (n - 1 - ii)];
+            v[3] = x[(n - 1 - ii) * n + jj];
         }
-        if (cnt == 0) continue;
-        const int cnt8 = (cnt + kFpBatch - 1) & ~(kFpBatch - 1);
-        if (lane < cnt8 - cnt) {
-            float4* dst = rec + (size_t)(cnt + lane) * RV;
+    };
+    float xn[4];
+    piece_x(0, xn);
+    for (int pc = 0; j0 + warp + NW * (pc / P2) < jend; ++pc) {
+        const int jj = j0 + warp + NW * (pc / P2);
+        const int ii = i0 + 32 * (pc % P2) + lane;
+        const bool in = ii < n;
+        float xv[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) xv[g] = xn[g];
+        piece_x(pc + 1, xn);
+        if (do_tv && in) {  // exact anisotropic TV over the 4 images (recon.py:169-170)
+            const int pg[4] = {jj * n + ii, ii * n + (n - 1 - jj), (n - 1 - jj) * n + (n - 1 - ii),
+                               (n - 1 - ii) * n + jj};
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                const int pi = pg[g] % n, pj = pg[g] / n;
+                if (pi + 1 < n) tv += fabsf(x[pg[g] + 1] - xv[g]);
+                if (pj + 1 < n) tv += fabsf(x[pg[g] + n] - xv[g]);
+            }
+        }
+        // records of this piece's pixels that are non-zero in any image (compacted)
+        const bool nz = xv[0] != 0.f || xv[1] != 0.f || xv[2] != 0.f || xv[3] != 0.f;
+        const uint32_t bal = __ballot_sync(0xffffffffu, nz);
+        const int cnt = __popc(bal);
+        if (cnt == 0) continue;  // warp-uniform
+        if (nz) {
+            float xs[4];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) xs[g] = xv[g] * scale;
+            float4* dst = rec + 2 * __popc(bal & ((1u << lane) - 1u));
+            dst[0] = make_float4(__ldg(a.pxs + ii), xs[0], xs[1], xs[2]);
+            dst[1] = make_float4(xs[3], __int_as_float(__float_as_int(xs[0] + kMagic)),
+                                 __int_as_float(__float_as_int(xs[1] + kMagic)),
+                                 __int_as_float(__float_as_int(xs[2] + kMagic)));
+        }
+        const int cntb = (cnt + kFsBatch - 1) & ~(kFsBatch - 1);
+        if (lane < cntb - cnt) {  // zero-weight padding (adds 0 at a valid window address)
             const float mb = __int_as_float(kMagicBits);
-            dst[0] = make_float4(X0, 0.f, mb, 0.f);
-            dst[1] = make_float4(mb, 0.f, mb, 0.f);
-            dst[2] = make_float4(mb, 0.f, 0.f, 0.f);
+            float4* dst = rec + 2 * (cnt + lane);
+            dst[0] = make_float4(X0, 0.f, 0.f, 0.f);
+            dst[1] = make_float4(0.f, mb, mb, mb);
         }
         __syncwarp();
         if (sensor_ok) {
             const float ey = __ldg(a.pys + jj) - sy;
             const float ey2 = ey * ey;
-            for (int k = 0; k < cnt8; k += kFpBatch) {
-                uint32_t ad[kFpBatch];
-                int32_t va[kFpBatch][G], vb[kFpBatch][G];
+            for (int k = 0; k < cntb; k += kFsBatch) {
+                uint32_t ad[kFsBatch];
+                int32_t va[kFsBatch][4], vb[kFsBatch][4];
 #pragma unroll
-                for (int b = 0; b < kFpBatch; ++b) {
-                    float rv[4 * RV];
+                for (int b = 0; b < kFsBatch; ++b) {
+                    const float4 r0 = rec[2 * (k + b)], r1 = rec[2 * (k + b) + 1];
+                    const float ex = r0.x - sx;
+                    const float uu = fminf(sqrt_approx(fmaf(ex, ex, ey2)), a.qclamp);
+                    const float tb = __fadd_rd(uu, kTwo23);
+                    const float fr = uu - (tb - kTwo23);
+                    const float xs[4] = {r0.y, r0.z, r0.w, r1.x};
+                    const int32_t xq[4] = {__float_as_int(r1.y), __float_as_int(r1.z),
+                                           __float_as_int(r1.w), __float_as_int(r1.x + kMagic)};
 #pragma unroll
-                    for (int v = 0; v < RV; ++v) {
-                        const float4 q = rec[(size_t)(k + b) * RV + v];
-                        rv[4 * v] = q.x; rv[4 * v + 1] = q.y; rv[4 * v + 2] = q.z; rv[4 * v + 3] = q.w;
+                    for (int g = 0; g < 4; ++g) {
+                        const float fb = fmaf(xs[g], fr, kMagic);
+                        va[b][g] = __float_as_int(fb) - kMagicBits;  // f   -> s0
+                        vb[b][g] = xq[g] - __float_as_int(fb);      // 1-f -> s0-1
                     }
-                    const float ex = rv[0] - sx;
-                    float u = sqrt_approx(fmaf(ex, ex, ey2));
-                    if (CLAMP) u = fminf(u, a.qclamp);
-                    const float tb = __fadd_rd(u, kTwo23);
-                    const float fr = u - (tb - kTwo23);
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const float fb = fmaf(rv[1 + 2 * g], fr, kMagic);
-                        va[b][g] = __float_as_int(fb) - kMagicBits;
-                        vb[b][g] = __float_as_int(rv[2 + 2 * g]) - __float_as_int(fb);
-                    }
-                    ad[b] = adj + (__float_as_uint(tb) << 9);  // 128 B x 4 images per slot
+                    ad[b] = adj + (__float_as_uint(tb) << 7);
                 }
 #pragma unroll
-                for (int b = 0; b < kFpBatch; ++b)
+                for (int b = 0; b < kFsBatch; ++b)
 #pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        red_smem_s32(ad[b] - 128u * G + 128u * g, vb[b][g]);
-                        red_smem_s32(ad[b] + 128u * g, va[b][g]);
+                    for (int g = 0; g < 4; ++g) {
+                        red_smem_s32(ad[b] + (uint32_t)(g * LW * 128) - 128u, vb[b][g]);
+                        red_smem_s32(ad[b] + (uint32_t)(g * LW * 128), va[b][g]);
                     }
             }
         }
-        __syncwarp();
-    }
-    if (do_tv) {
-        const float tvb = block_sum(tv, red_f);
-        if (threadIdx.x == 0) a.part_tv[blockIdx.x] = tvb;
+        __syncwarp();  // rec is rewritten by the next piece
     }
     __syncthreads();
 
-    // flush (transposed through the record buffer, as in fp_f32_kernel); window g of lane
-    // l belongs to sensor (32*group + l + g*M/4) mod M
-    const int cap = (T + kFpBatch) * RV * 16;
-    const int bs = (32 * 9 * 4 <= cap) ? 8 : 4;
-    int32_t* scr = reinterpret_cast<int32_t*>(rec);
-    const int sensors_per_step = 32 / bs;
-    const int sub = lane % bs, grp = lane / bs;
-    for (int k0 = warp * bs; k0 < a.L; k0 += (kThreads / 32) * bs) {
-#pragma unroll 1
-        for (int g = 0; g < G; ++g) {
-            for (int i = 0; i < bs; ++i) {
-                const int k = k0 + i;
-                scr[lane * (bs + 1) + i] = (k < a.L) ? win[(k * G + g) * 32 + lane] : 0;
-            }
-            __syncwarp();
-            for (int rr = 0; rr < 32; rr += sensors_per_step) {
-                const int ms = rr + grp;
-                const int lo_ms = __shfl_sync(0xffffffffu, lo, ms);
-                const int v = scr[ms * (bs + 1) + sub];
-                const int t = lo_ms + k0 + sub;
-                const int mb = blockIdx.y * 32 + ms;
-                if (v != 0 && mb < a.M && t >= 0 && t < a.Q && k0 + sub < a.L) {
-                    const int mg = (mb + g * q4) % a.M;
-                    atomicAdd(reinterpret_cast<unsigned long long*>(a.acc + (size_t)mg * a.Q + t),
-                              (unsigned long long)(long long)v);
-                }
-            }
-            __syncwarp();
+    // store: a warp takes blocks of 8 slots of one image; 8 row reads (lane = sensor,
+    // conflict free) leave lane l holding 8 consecutive slots of its sensor's window, written
+    // as two 16-B stores to win[unit][g][l][k0..k0+7]
+    {
+        constexpr int NB = LW / 8;
+        int32_t* dst0 = a.win + (size_t)u * 4 * 32 * LW + (size_t)lane * LW;
+        for (int blk = warp; blk < 4 * NB; blk += NW) {
+            const int g = blk / NB, k0 = (blk - g * NB) * 8;
+            int v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = win[(g * LW + k0 + i) * 32 + lane];
+            int4* d = reinterpret_cast<int4*>(dst0 + (size_t)g * 32 * LW + k0);
+            __stcg(d, make_int4(v[0], v[1], v[2], v[3]));
+            __stcg(d + 1, make_int4(v[4], v[5], v[6], v[7]));
+        }
+        if (warp == 0) a.win_lo[(size_t)u * 32 + lane] = lo;
+    }
+    if (a.solver) {
+        tv = warp_sum(tv);
+        __syncthreads();
+        if (lane == 0) red_f[warp] = tv;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float tvb = red_f[0];
+            for (int w = 1; w < NW; ++w) tvb += red_f[w];
+            a.part_tv[blockIdx.x] = tvb;
         }
     }
 }
@@ -1352,6 +1381,10 @@ struct FinArgs {
     int ntv;
     double* sumsq_out;   // optional [NF] (pk_residual)
     int solver;
+    // symmetric projector: gather the unit windows instead of reading acc
+    const int32_t* win;  // [units][4][32][LW] (nullptr: acc mode)
+    const int32_t* win_lo;  // [units][32]
+    int win_lw, groups, ntiles;
     int atrick;
     int chunks;          // sample chunks per sensor (one CTA each)
 };
@@ -1384,18 +1417,43 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
         const T kx = (T)((double)v * wq);
         return ym ? (T)(kx - ym[s]) : kx;
     };
+    // symmetric projector: trace m receives, for g = 0..3, the image-g windows of base sensor
+    // m - g*M/4 from every quadrant tile; gather samples [c0 - 1, c1) in that fixed order
+    int32_t* gs = reinterpret_cast<int32_t*>(smem + (((size_t)(clen + 1) * sizeof(T) + 15) & ~(size_t)15));
+    if (a.win) {
+        const int q4 = a.M >> 2, LW = a.win_lw, s_lo = c0 - 1, ns = c1 - s_lo;
+        for (int k = threadIdx.x; k < ns; k += kThreads) gs[k] = 0;
+        __syncthreads();
+        // windows in (g, tile) order; each is added by the whole CTA, one window at a time
+#pragma unroll 1
+        for (int wi = 0; wi < 4 * a.ntiles; ++wi) {
+            const int g = wi / a.ntiles, t = wi - g * a.ntiles;
+            int mb = m - g * q4;
+            if (mb < 0) mb += a.M;
+            const int unit = t * a.groups + (mb >> 5), l = mb & 31;
+            const int lo = __ldg(a.win_lo + unit * 32 + l);
+            const int k0 = max(0, s_lo - lo), k1 = min(LW, c1 - lo);
+            if (k0 >= k1) continue;  // CTA-uniform
+            const int32_t* src = a.win + (((size_t)unit * 4 + g) * 32 + l) * LW;
+            for (int k = k0 + threadIdx.x; k < k1; k += kThreads) gs[lo + k - s_lo] += __ldcg(src + k);
+            __syncthreads();
+        }
+    }
+    auto sample = [&](int s) -> long long {
+        return a.win ? (long long)gs[s - (c0 - 1)] : __ldcg(accm + s);
+    };
     double ss = 0.0;
     // tr[k] holds r[c0 - 1 + k]; 4 samples per thread per step, all loads first
-    if (threadIdx.x == 0) tr[0] = (c0 >= 1) ? resid(c0 - 1, __ldcg(accm + c0 - 1)) : (T)0;
+    if (threadIdx.x == 0) tr[0] = (c0 >= 1) ? resid(c0 - 1, sample(c0 - 1)) : (T)0;
     for (int s0 = c0 + 4 * threadIdx.x; s0 < c1; s0 += 4 * kThreads) {
         long long v[4];
         const bool full = s0 + 4 <= c1 && (s0 & 1) == 0;
-        if (full) {
+        if (full && !a.win) {
             const longlong2 p0 = __ldcg(reinterpret_cast<const longlong2*>(accm + s0));
             const longlong2 p1 = __ldcg(reinterpret_cast<const longlong2*>(accm + s0 + 2));
             v[0] = p0.x; v[1] = p0.y; v[2] = p1.x; v[3] = p1.y;
         } else {
-            for (int q = 0; q < 4; ++q) v[q] = (s0 + q < c1) ? __ldcg(accm + s0 + q) : 0;
+            for (int q = 0; q < 4; ++q) v[q] = (s0 + q < c1) ? sample(s0 + q) : 0;
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {

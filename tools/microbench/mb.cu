@@ -50,6 +50,29 @@ __device__ __forceinline__ int amap(int mode, int lane, int i){
 }
 __global__ void atoms_k(int* out, int iters, int mode, long long* cyc){
   __shared__ int s[64*32];
+  if(mode>=5){ // lane l -> bank l, pseudo-random row (the projector's window pattern)
+    for(int i=threadIdx.x;i<64*32;i+=blockDim.x) s[i]=0;
+    __syncthreads();
+    int lane=threadIdx.x&31; unsigned h=lane*2654435761u+threadIdx.x;
+    long long t0=clock64();
+    for(int i=0;i<iters;i++){
+#pragma unroll
+      for(int k=0;k<8;k++){ h=h*1664525u+1013904223u; int row=(h>>20)&63;
+        int w;
+        if(mode<=6) w=row*32+lane;
+        else if(mode<=10) { int R=1<<(mode-6); w=((row+(lane&(R-1)))&63)*32+lane; }      // R distinct rows
+        else if(mode==11) { // 1-D window, 8x4 pixel footprint, 1.93 slots/px, direction from h
+          float th=(h>>8)*(6.2831853f/16777216.f); int lx=lane&7, ly=lane>>3;
+          w=(int)(1.93f*(lx*__cosf(th)+ly*__sinf(th))+40.f+row); }
+        else { // 1-D window, 32 lanes over 16 consecutive words (2 lanes per word, random order)
+          w=row+((lane*7+k)&15); }
+        asm volatile("red.shared.add.s32 [%0], %1;"::"r"((unsigned)__cvta_generic_to_shared(s+(w&2047))),"r"(k+1)); } }
+    long long t1=clock64();
+    __syncthreads();
+    if(threadIdx.x==0) cyc[blockIdx.x]=t1-t0;
+    out[blockIdx.x*blockDim.x+threadIdx.x]=s[threadIdx.x];
+    return;
+  }
   for(int i=threadIdx.x;i<64*32;i+=blockDim.x) s[i]=0;
   __syncthreads();
   int lane=threadIdx.x&31, w=threadIdx.x>>5;
@@ -128,7 +151,7 @@ int main(){
   cudaEventElapsedTime(&ms,e0,e1); report("DFMA",B,T,it/4*32.0,ms);
   cudaEventRecord(e0); sqrt_k<<<B,T>>>(fo,it/4,cyc); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
   cudaEventElapsedTime(&ms,e0,e1); report("MUFU.SQRT",B,T,it/4*32.0,ms);
-  for(int m=0;m<5;m++){ char nm[64]; snprintf(nm,64,"ATOMS.ADD mode %d",m);
+  for(int m=0;m<13;m++){ char nm[64]; snprintf(nm,64,"ATOMS.ADD mode %d",m);
     cudaEventRecord(e0); atoms_k<<<B,T>>>(io,it/4,m,cyc); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
     cudaEventElapsedTime(&ms,e0,e1); report(nm,B,T,it/4*8.0,ms);}
   for(int m=0;m<8;m++){ char nm[64]; snprintf(nm,64,"LDS.64 mode %d",m);
