@@ -113,7 +113,7 @@ void free_plan(pk_plan* p) {
                     p->status_dev, p->part_bp, p->part_tv, p->part_r, p->part_misc, p->state,
                     p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt, p->sym_tiles,
                     p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0, p->sym_tile_slot0,
-                    p->sym_part, p->fsym_win, p->fsym_lo};
+                    p->sym_part, p->fsym_win, p->fsym_lo, p->fsym_list};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
@@ -206,7 +206,7 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
         a.xb0 = static_cast<const float*>(p->xbuf[0]);
         a.xb1 = static_cast<const float*>(p->xbuf[1]);
         a.pxs = p->pxs; a.pys = p->pys; a.sxs = p->sxs; a.sys = p->sys;
-        a.win = p->fsym_win; a.win_lo = p->fsym_lo;
+        a.win = p->fsym_win;
         a.n = p->nx; a.M = p->M; a.Q = p->Q; a.groups = p->fp_groups; a.qt = p->fsym_qt;
         a.qclamp = (float)p->Q + 1.5f;
         a.st = p->state; a.part_tv = p->part_tv; a.solver = solver;
@@ -267,8 +267,8 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
         a.sumsq_out = sumsq;
         a.solver = solver;
         if (NF == 1 && p->fsym) {
-            a.win = p->fsym_win; a.win_lo = p->fsym_lo; a.win_lw = p->fsym_L;
-            a.groups = p->fp_groups; a.ntiles = p->fsym_qt * p->fsym_qt;
+            a.win = p->fsym_win; a.win_list = p->fsym_list; a.win_lw = p->fsym_L;
+            a.nwin = 4 * p->fsym_qt * p->fsym_qt;
         }
         a.atrick = p->bp_atrick;
         a.chunks = chunks;
@@ -818,6 +818,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     if (p->fsym) {
         A(alloc(p, &p->fsym_win, (size_t)fsym_units * 4 * 32 * p->fsym_L));
         A(alloc(p, &p->fsym_lo, (size_t)fsym_units * 32));
+        A(alloc(p, &p->fsym_list, (size_t)p->M * 4 * p->fsym_qt * p->fsym_qt));
     }
     p->fin_chunks = std::max(1, std::min(8, p->Q / 1024));
     A(alloc(p, &p->part_r, (size_t)p->M * nf * p->fin_chunks));
@@ -852,6 +853,29 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         int* dsts[5] = {p->sym_tiles, p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0,
                         p->sym_tile_slot0};
         for (int q = 0; q < 5; ++q) up(dsts[q], p->sym_h[q].data(), sizeof(int) * p->sym_h[q].size());
+    }
+    if (e == cudaSuccess && p->fsym) {
+        // per-trace window lists of the symmetric projector's gather: trace sg receives, for
+        // g = 0..3, the image-g window of base sensor sg - g*M/4 from every quadrant tile
+        const int ntl = p->fsym_qt * p->fsym_qt, units = ntl * p->fp_groups;
+        fp_sym_lo_kernel<<<units, 32>>>(p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fp_groups,
+                                        p->fsym_qt, (float)p->Q + 1.5f, p->fsym_lo);
+        std::vector<int> lo((size_t)units * 32);
+        e = cudaMemcpy(lo.data(), p->fsym_lo, sizeof(int) * lo.size(), cudaMemcpyDeviceToHost);
+        std::vector<int2> list((size_t)p->M * 4 * ntl);
+        const int q4 = p->M / 4;
+        for (int sg = 0; sg < p->M; ++sg)
+            for (int g = 0; g < 4; ++g) {
+                int mb = sg - g * q4;
+                if (mb < 0) mb += p->M;
+                for (int t = 0; t < ntl; ++t) {
+                    const int unit = t * p->fp_groups + (mb >> 5), l = mb & 31;
+                    list[((size_t)sg * 4 + g) * ntl + t] =
+                        make_int2((int)((((size_t)unit * 4 + g) * 32 + l) * p->fsym_L), lo[(size_t)unit * 32 + l]);
+                }
+            }
+        if (e == cudaSuccess)
+            e = cudaMemcpy(p->fsym_list, list.data(), sizeof(int2) * list.size(), cudaMemcpyHostToDevice);
     }
     if (e == cudaSuccess) e = cudaMemset(p->table, 0, (size_t)p->M * p->TS * 2 * ts * nf);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);

@@ -282,6 +282,7 @@ struct pk_plan {
     int fsym = 0, fsym_T = 0, fsym_qt = 0, fsym_L = 0, fsym_smem = 0;
     int32_t* fsym_win = nullptr;  // [units][4][32][L] window sums of the last projection
     int32_t* fsym_lo = nullptr;   // [units][32] first trace index of each window
+    int2* fsym_list = nullptr;    // [M][4 * tiles] per-trace gather list {window offset, lo}
     int fin_chunks = 1;  // residual kernel: sample chunks per sensor
     float* bp_gpart = nullptr;
     uint32_t* bp_tile_cnt = nullptr;

@@ -1059,13 +1059,32 @@ struct FpSymArgs {
     const float* sxs;
     const float* sys;
     int32_t* win;            // [units][4][32][LW] window sums (unit = tile * groups + group)
-    int32_t* win_lo;         // [units][32] first trace index of each lane's windows
     int n, M, Q, groups, qt; // groups = ceil(M/32), qt = quadrant tiles per side
     float qclamp;
     DevState* st;
     double* part_tv;         // solver mode: per-unit TV(x) partial (group-0 units, else 0)
     int solver;
 };
+
+// first trace index of the window of the 64x64 quadrant tile at (i0, j0) for sensor (sx, sy)
+__device__ __forceinline__ int fp_sym_window_lo(const float* pxs, const float* pys, int n, int i0,
+                                                int j0, float sx, float sy, float qclamp) {
+    const float X0 = __ldg(pxs + i0), X1 = __ldg(pxs + min(i0 + kFsTile - 1, n - 1));
+    const float Y0 = __ldg(pys + j0), Y1 = __ldg(pys + min(j0 + kFsTile - 1, n - 1));
+    const float cx = fminf(fmaxf(sx, X0), X1), cy = fminf(fmaxf(sy, Y0), Y1);
+    const float dmin = fminf(sqrtf((cx - sx) * (cx - sx) + (cy - sy) * (cy - sy)), qclamp);
+    return (int)floorf(dmin) - 2;
+}
+
+// plan setup: lo of every (unit, lane) -- geometry only, identical to the projector's
+__global__ void fp_sym_lo_kernel(const float* pxs, const float* pys, const float* sxs, const float* sys,
+                                 int n, int M, int groups, int qt, float qclamp, int32_t* lo_out) {
+    const int u = blockIdx.x, lane = threadIdx.x;
+    const int tile = u / groups, grp = u % groups, h = n >> 1;
+    const int i0 = h + kFsTile * (tile % qt), j0 = h + kFsTile * (tile / qt);
+    const int mm = min(grp * 32 + lane, M - 1);
+    lo_out[u * 32 + lane] = fp_sym_window_lo(pxs, pys, n, i0, j0, __ldg(sxs + mm), __ldg(sys + mm), qclamp);
+}
 
 template <int LW>
 __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) {
@@ -1094,12 +1113,9 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
     const bool sensor_ok = m < a.M;
     const int mm = min(m, a.M - 1);
     const float sx = __ldg(a.sxs + mm), sy = __ldg(a.sys + mm);
-    // window: trace indices [lo, lo + LW) of this tile
-    const float X0 = __ldg(a.pxs + i0), X1 = __ldg(a.pxs + min(i0 + kFsTile - 1, n - 1));
-    const float Y0 = __ldg(a.pys + j0), Y1 = __ldg(a.pys + jend - 1);
-    const float cx = fminf(fmaxf(sx, X0), X1), cy = fminf(fmaxf(sy, Y0), Y1);
-    const float dmin = fminf(sqrtf((cx - sx) * (cx - sx) + (cy - sy) * (cy - sy)), a.qclamp);
-    const int lo = (int)floorf(dmin) - 2;
+    const float X0 = __ldg(a.pxs + i0);
+    // window: trace indices [lo, lo + LW) of this tile (fp_sym_window_lo)
+    const int lo = fp_sym_window_lo(a.pxs, a.pys, n, i0, j0, sx, sy, a.qclamp);
     // word (g, k, lane) at (g*LW + k)*32 + lane, k = t - lo for trace index t
     const uint32_t adj = win_s + 4u * (uint32_t)lane - 128u * (uint32_t)lo - 128u * kTwo23Bits;
     {
@@ -1221,7 +1237,6 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
             __stcg(d, make_int4(v[0], v[1], v[2], v[3]));
             __stcg(d + 1, make_int4(v[4], v[5], v[6], v[7]));
         }
-        if (warp == 0) a.win_lo[(size_t)u * 32 + lane] = lo;
     }
     if (a.solver) {
         tv = warp_sum(tv);
@@ -1383,8 +1398,8 @@ struct FinArgs {
     int solver;
     // symmetric projector: gather the unit windows instead of reading acc
     const int32_t* win;  // [units][4][32][LW] (nullptr: acc mode)
-    const int32_t* win_lo;  // [units][32]
-    int win_lw, groups, ntiles;
+    const int2* win_list;   // [M][nwin] per trace: {offset of the window in win, its lo}
+    int win_lw, nwin;
     int atrick;
     int chunks;          // sample chunks per sensor (one CTA each)
 };
@@ -1421,23 +1436,22 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
     // m - g*M/4 from every quadrant tile; gather samples [c0 - 1, c1) in that fixed order
     int32_t* gs = reinterpret_cast<int32_t*>(smem + (((size_t)(clen + 1) * sizeof(T) + 15) & ~(size_t)15));
     if (a.win) {
-        const int q4 = a.M >> 2, LW = a.win_lw, s_lo = c0 - 1, ns = c1 - s_lo;
+        const int LW = a.win_lw, s_lo = c0 - 1, ns = c1 - s_lo;
         for (int k = threadIdx.x; k < ns; k += kThreads) gs[k] = 0;
         __syncthreads();
-        // windows in (g, tile) order; each is added by the whole CTA, one window at a time
-#pragma unroll 1
-        for (int wi = 0; wi < 4 * a.ntiles; ++wi) {
-            const int g = wi / a.ntiles, t = wi - g * a.ntiles;
-            int mb = m - g * q4;
-            if (mb < 0) mb += a.M;
-            const int unit = t * a.groups + (mb >> 5), l = mb & 31;
-            const int lo = __ldg(a.win_lo + unit * 32 + l);
-            const int k0 = max(0, s_lo - lo), k1 = min(LW, c1 - lo);
-            if (k0 >= k1) continue;  // CTA-uniform
-            const int32_t* src = a.win + (((size_t)unit * 4 + g) * 32 + l) * LW;
-            for (int k = k0 + threadIdx.x; k < k1; k += kThreads) gs[lo + k - s_lo] += __ldcg(src + k);
-            __syncthreads();
+        // integer shared atomics: the sum does not depend on the order, so every window's
+        // loads can be in flight at once (no barrier between windows)
+        const int2* wl = a.win_list + (size_t)m * a.nwin;
+#pragma unroll 4
+        for (int wi = 0; wi < a.nwin; ++wi) {
+            const int2 d = __ldg(wl + wi);
+            const int k0 = max(0, s_lo - d.y), k1 = min(LW, c1 - d.y);
+            for (int k = k0 + threadIdx.x; k < k1; k += kThreads) {
+                const int v = __ldcg(a.win + d.x + k);
+                if (v != 0) atomicAdd(gs + d.y + k - s_lo, v);
+            }
         }
+        __syncthreads();
     }
     auto sample = [&](int s) -> long long {
         return a.win ? (long long)gs[s - (c0 - 1)] : __ldcg(accm + s);
