@@ -587,6 +587,7 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
     __shared__ float red_f[kThreads / 32];
     __shared__ double red_d[kThreads / 32];
     __shared__ int last_flag;
+    __shared__ float blk[kSymTile * kSymTile];  // the image-g block of the tile, row-major
     int iter = 0;
     if (EPI) {
         if (a.st->all_stopped) return;
@@ -599,14 +600,22 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
     const int n = a.n, h = n >> 1;
     const int i0 = h + kSymTile * tx, j0 = h + kSymTile * ty;
     const int s0 = __ldg(a.tile_slot0 + t), s1 = __ldg(a.tile_slot0 + t + 1);
-    // thread owns elements 4*tid .. 4*tid+3 of the slot vector [k][consumer thread]: one
-    // representative column k, consumer threads ct .. ct+3; every slot is one 16-B load
+    // the tile's image under g is the 32x32 block [bx, bx+32) x [by, by+32) (clipped to the grid)
+    int bx, by;
+    {
+        int ia, ja, ib, jb;
+        sym_pixel(g, i0, j0, n, ia, ja);
+        sym_pixel(g, i0 + kSymTile - 1, j0 + kSymTile - 1, n, ib, jb);
+        bx = min(ia, ib);
+        by = min(ja, jb);
+    }
+    // 1) the tile's slots in order, coalesced: thread owns elements 4*tid .. 4*tid+3 of the
+    //    slot vector [k][consumer thread], every slot is one 16-B load
     const int k = threadIdx.x >> 6, ct = (threadIdx.x & 63) * 4;
     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
     if (active) {
         const float4* src = reinterpret_cast<const float4*>(a.part + (size_t)g * 4 * kThreads) + threadIdx.x;
         const size_t stride = 8 * 4 * kThreads / 4;  // float4s per slot
-        // every slot load in flight at once (a tile has ~ grid / tiles + 1 slots)
         for (int sb = s0; sb < s1; sb += 16) {
             float4 v[16];
 #pragma unroll
@@ -618,27 +627,38 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
             }
         }
     }
-    const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
-    float val[4];
-    int pix[4];
+    // 2) scatter the sums into the image-g block (shared memory transpose)
+    {
+        const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int c = ct + u;  // consumer thread of the main kernel
-        int lx, ly;
-        sym_lane_xy(c & 31, a.lanemap, lx, ly);
-        const int i = i0 + lx + 8 * k, j = j0 + 4 * (c >> 5) + ly;
-        pix[u] = -1;
-        if (active && i < n && j < n) {
+        for (int u = 0; u < 4; ++u) {
+            const int c = ct + u;  // consumer thread of the main kernel
+            int lx, ly;
+            sym_lane_xy(c & 31, a.lanemap, lx, ly);
             int ig, jg;
-            sym_pixel(g, i, j, n, ig, jg);
-            pix[u] = jg * n + ig;
+            sym_pixel(g, i0 + lx + 8 * k, j0 + 4 * (c >> 5) + ly, n, ig, jg);
+            blk[(jg - by) * kSymTile + (ig - bx)] = a.gscale * sv[u];
         }
-        val[u] = a.gscale * sv[u];
+    }
+    __syncthreads();
+    // 3) image-row-major pass over the block: coalesced stencil loads and stores
+    const int bc = threadIdx.x & 31;
+    int pix[4];
+    float val[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int br = (threadIdx.x >> 5) + 8 * q;
+        const int ig = bx + bc, jg = by + br;
+        // a pixel of the block belongs to this CTA iff its representative is in the tile
+        // (row/column beyond the grid edge, or the lower triangle's half of a diagonal
+        // tile under a reflection, are skipped)
+        pix[q] = (active && ig >= 0 && ig < n && jg >= 0 && jg < n) ? jg * n + ig : -1;
+        val[q] = blk[br * kSymTile + bc];
     }
     if (!EPI) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (pix[k] >= 0) a.out[pix[k]] = val[k];
+        for (int q = 0; q < 4; ++q)
+            if (pix[q] >= 0) a.out[pix[q]] = val[q];
         return;
     }
     const float* x = (iter & 1) ? a.xb1 : a.xb0;
@@ -650,10 +670,10 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
     int bad = 0;
     if (!a.st->fr[0].stopped) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int p = pix[k];
+        for (int q = 0; q < 4; ++q) {
+            const int p = pix[q];
             if (p < 0) continue;
-            float gr = val[k];
+            float gr = val[q];
             if (beta > 0.f) gr += beta * tv_grad_at<float>(x, p, p % n, p / n, n, n, eps * eps);
             const float xn = prox<float>(x[p] - eta * gr, lam, nonneg);
             xo[p] = xn;
