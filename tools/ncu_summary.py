@@ -60,8 +60,10 @@ def main(rep, out, label=""):
         kernels.append(k)
     per = {}
     for k in kernels:
-        short = "bp_f32" if "bp_f32" in k["kernel"] else "fp_f32" if "fp_f32" in k["kernel"] else \
-            "finalize" if "finalize" in k["kernel"] else k["kernel"]
+        nm = k["kernel"]
+        short = ("bp_f32" if ("bp_f32" in nm or "bp_sym_f32" in nm) else
+                 "fp_f32" if ("fp_f32" in nm or "fp_sym_f32" in nm) else
+                 "finalize" if "finalize" in nm else nm)
         per.setdefault(short, k["dram_bytes"])
     summary = {"report": rep, "label": label, "kernels": kernels, "dram_bytes_per_launch": per}
     json.dump(summary, open(out + ".json", "w"), indent=1)
