@@ -207,10 +207,10 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
         a.xb1 = static_cast<const float*>(p->xbuf[1]);
         a.pxs = p->pxs; a.pys = p->pys; a.sxs = p->sxs; a.sys = p->sys;
         a.win = p->fsym_win;
-        a.n = p->nx; a.M = p->M; a.Q = p->Q; a.groups = p->fp_groups; a.qt = p->fsym_qt;
+        a.n = p->nx; a.M = p->M; a.Q = p->Q; a.groups = p->fsym_groups; a.qt = p->fsym_qt;
         a.qclamp = (float)p->Q + 1.5f;
         a.st = p->state; a.part_tv = p->part_tv; a.solver = solver;
-        const int units = p->fsym_qt * p->fsym_qt * p->fp_groups;
+        const int units = p->fsym_qt * p->fsym_qt * p->fsym_groups;
         switch (p->fsym_L) {
             case 96: fp_sym_f32_kernel<96><<<units, kFsThreads, p->fsym_smem, s>>>(a); break;
             case 128: fp_sym_f32_kernel<128><<<units, kFsThreads, p->fsym_smem, s>>>(a); break;
@@ -262,7 +262,7 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
         a.M = p->M; a.Q = p->Q; a.TS = p->TS; a.w = p->w;
         a.st = p->state; a.prm = p->params; a.io = p->io; a.part_r = p->part_r;
         a.part_tv = p->part_tv;
-        a.ntv = (NF == 1 && p->fsym) ? p->fsym_qt * p->fsym_qt * p->fp_groups
+        a.ntv = (NF == 1 && p->fsym) ? p->fsym_qt * p->fsym_qt * p->fsym_groups
                                      : p->fp_tiles_x * p->fp_tiles_y;
         a.sumsq_out = sumsq;
         a.solver = solver;
@@ -611,6 +611,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     {
         const int t64 = ((p->nx + 63) / 64) * ((p->ny + 63) / 64);
         p->fp_T = (p->dtype == PK_F32 && nf <= 2 && (int64_t)t64 * p->fp_groups >= 4 * 148) ? 64 : 32;
+        if (const char* e = getenv("PK_FP_T")) p->fp_T = atoi(e) == 64 ? 64 : 32;
     }
     p->fp_tiles_x = (p->nx + p->fp_T - 1) / p->fp_T;
     p->fp_tiles_y = (p->ny + p->fp_T - 1) / p->fp_T;
@@ -741,7 +742,8 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             p->fsym_smem = 4 * p->fsym_L * 32 * 4 + (kFsThreads / 32) * (32 + kFsBatch) * 32;
             int sms = 0;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
-            const int units = p->fsym_qt * p->fsym_qt * p->fp_groups;
+            p->fsym_groups = (p->M + 31) / 32;
+            const int units = p->fsym_qt * p->fsym_qt * p->fsym_groups;
             if (p->fsym_L == 0 || p->fsym_smem > 200 * 1024 ||
                 (units < sms && !(ev2 && atoi(ev2) != 0)))
                 p->fsym = 0;
@@ -813,7 +815,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[1]), (size_t)p->P * ts * nf));
     const int ntile_max = std::max(p->bp_tiles_x * p->bp_tiles_y, p->sym ? 8 * p->sym_ntiles : 0);
     A(alloc(p, &p->part_bp, (size_t)4 * nf * std::max(ntile_max, (p->P + kThreads - 1) / kThreads)));
-    const int fsym_units = p->fsym ? p->fsym_qt * p->fsym_qt * p->fp_groups : 0;
+    const int fsym_units = p->fsym ? p->fsym_qt * p->fsym_qt * p->fsym_groups : 0;
     A(alloc(p, &p->part_tv, (size_t)std::max(p->fp_tiles_x * p->fp_tiles_y, fsym_units) * nf));
     if (p->fsym) {
         A(alloc(p, &p->fsym_win, (size_t)fsym_units * 4 * 32 * p->fsym_L));
@@ -857,8 +859,8 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     if (e == cudaSuccess && p->fsym) {
         // per-trace window lists of the symmetric projector's gather: trace sg receives, for
         // g = 0..3, the image-g window of base sensor sg - g*M/4 from every quadrant tile
-        const int ntl = p->fsym_qt * p->fsym_qt, units = ntl * p->fp_groups;
-        fp_sym_lo_kernel<<<units, 32>>>(p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fp_groups,
+        const int ntl = p->fsym_qt * p->fsym_qt, units = ntl * p->fsym_groups;
+        fp_sym_lo_kernel<<<units, 32>>>(p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups,
                                         p->fsym_qt, (float)p->Q + 1.5f, p->fsym_lo);
         std::vector<int> lo((size_t)units * 32);
         e = cudaMemcpy(lo.data(), p->fsym_lo, sizeof(int) * lo.size(), cudaMemcpyDeviceToHost);
@@ -869,7 +871,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 int mb = sg - g * q4;
                 if (mb < 0) mb += p->M;
                 for (int t = 0; t < ntl; ++t) {
-                    const int unit = t * p->fp_groups + (mb >> 5), l = mb & 31;
+                    const int unit = t * p->fsym_groups + (mb >> 5), l = mb & 31;
                     list[((size_t)sg * 4 + g) * ntl + t] =
                         make_int2((int)((((size_t)unit * 4 + g) * 32 + l) * p->fsym_L), lo[(size_t)unit * 32 + l]);
                 }
