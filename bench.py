@@ -9,9 +9,12 @@ distinct synthetic frames whose measurements together exceed the 126 MB L2.  ``e
 repeats the measurement through the C-ABI host-buffer entry (pk_reconstruct_host):
 pinned fp64 y in, H2D, solve, D2H of the fp64 image, every step.
 
-N > 1 (torchrun, NCCL): ``--shard sensors`` (default; one frame split by sensors with an
-all-reduce of the image-sized gradient per iteration, strong scaling) or
-``--shard frames`` (independent frames per GPU, no collective, weak scaling).
+N > 1 (torchrun, NCCL): ``--shard frames`` (default: independent frames per GPU, no
+collective, weak scaling -- the throughput mode of BASELINE configs 3/4) or ``--shard
+sensors`` (one frame split by sensors with an all-reduce of the image-sized gradient per
+iteration, strong scaling).  In frames mode with N > 1 the JSON line also carries
+``sensor_sharded``: the single-frame latency of the sensor-sharded solve measured in the
+same run (BASELINE config 3's "sensor-sharded with allreduce").
 
 ``--impl reference`` times the reference's CPU algorithm (the matrix-free fp64 C oracle
 restatement, all host threads -- the dense reference cannot hold config 3's 2.2 TB K).
@@ -44,7 +47,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg3", choices=CFG_CHOICES)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--shard", default="sensors", choices=["sensors", "frames"])
+    ap.add_argument("--shard", default="frames", choices=["sensors", "frames"])
+    ap.add_argument("--sensor-frames", type=int, default=5,
+                    help="frames timed through the sensor-sharded solver (N > 1, frames mode)")
     ap.add_argument("--frames", type=int, default=40, help="distinct frames cycled (> L2)")
     ap.add_argument("--streams", type=int, default=4,
                     help="independent plans on concurrent CUDA streams (frames in flight)")
@@ -208,10 +213,16 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; the modulo only matters for functional runs with more ranks than
+    # GPUs (PK_DIST_BACKEND=gloo), never for a measurement
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("PK_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
 
     grid, ring, ac, ph0 = pk.make_scene(cfg.n, cfg.sensors, cfg.samples, seed=0)
@@ -267,7 +278,9 @@ def main():
             N.check(lib.pk_reconstruct(ops[q].handle, params_arr, Ystep[f % n_steps_in].data_ptr(),
                                        x_outs[q].data_ptr(), hists[q].data_ptr(), stats[q].data_ptr(),
                                        ctypes.c_void_p(streams[q].cuda_stream)))
-        launches_per_step = 3 + 3 * cfg.iterations
+        # init + table + copy-out, and per iteration back-projection (+ epilogue kernel for the
+        # symmetric back-projector), projection, residual
+        launches_per_step = 3 + (4 if op.info.symmetric & 1 else 3) * cfg.iterations
 
     frame_base = rank * 7919  # different frames per rank in frames mode
 
@@ -388,11 +401,42 @@ def main():
         ee1.record()
         torch.cuda.synchronize(dev)
         ms_e2e = ee0.elapsed_time(ee1)
-        e2e = {"value": args.steps * B / (ms_e2e * 1e-3) * world, "unit": "frames/s",
+        if world > 1:  # slowest rank, like the device-resident number
+            te = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            ms_e2e = float(te[0])
+        e2e = {"value": args.steps * B * world / (ms_e2e * 1e-3), "unit": "frames/s",
                "h2d_bytes_per_step": B * M * Q * 8,
                "d2h_bytes_per_step": B * (P * 8 + 4 * cfg.iterations * 8 + 8),
                "ms_per_step": ms_e2e / args.steps,
                "path": f"pk_reconstruct_host_async (C ABI, pinned fp64 host buffers, {SS} stream(s))"}
+
+    # ---- sensor-sharded single-frame latency (BASELINE config 3 at N > 1) ----
+    sensor_sharded = None
+    if world > 1 and not sensor_mode and args.sensor_frames > 0:
+        m0, m1 = shard_range(M, rank, world)
+        sops = DeviceShardOps(grid, ring, ac, pk.CudaPool(local, "float32"), m0, m1)
+        ssolver = SensorShardedSolver(sops)
+        Yl = Y[:2, m0 * Q: m1 * Q].contiguous()
+        ssolver.solve(Yl[0], pinned, alpha, beta, step)  # warm-up (plan, NCCL communicators)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for k in range(args.sensor_frames):
+            res = ssolver.solve(Yl[k % 2], pinned, alpha, beta, step)
+        s1.record()
+        torch.cuda.synchronize(dev)
+        ts = torch.tensor([s0.elapsed_time(s1)], device=dev, dtype=torch.float64)
+        dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+        ms_frame = float(ts[0]) / args.sensor_frames
+        sensor_sharded = {
+            "frames_per_s": 1e3 / ms_frame, "ms_per_frame": ms_frame,
+            "ms_per_iteration": ms_frame / cfg.iterations, "frames": args.sensor_frames,
+            "sensors_per_rank": m1 - m0, "iterations_run": res.iterations_run,
+            "allreduce_bytes_per_iteration": P * 4 + 8,
+            "path": "SensorShardedSolver: local K1 -> all_reduce(gradient) -> update -> local K2/K3 "
+                    "-> all_reduce(sum r^2), host-driven loop"}
 
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
@@ -427,6 +471,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
         }
+        if sensor_sharded is not None:
+            line["sensor_sharded"] = sensor_sharded
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
