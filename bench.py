@@ -209,7 +209,7 @@ def main():
 
     import paper_2404_10928_b200 as pk
     from paper_2404_10928_b200 import _native as N
-    from paper_2404_10928_b200.sharded import DeviceShardOps, SensorShardedSolver, shard_range
+    from paper_2404_10928_b200.sharded import DeviceShardOps, SpeculativeShardSolve, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -246,15 +246,18 @@ def main():
     alpha, beta, step = pinned.alpha, pinned.beta, pinned.step
     params = pk.solver.solver_params(pinned, alpha, beta, step)
 
+    capture = os.environ.get("PK_DIST_BACKEND", "nccl") == "nccl"  # gloo cannot be captured
     if sensor_mode:
         m0, m1 = shard_range(M, rank, world)
         ops = DeviceShardOps(grid, ring, ac, pk.CudaPool(local, "float32"), m0, m1)
-        solver = SensorShardedSolver(ops)
+        solver = SpeculativeShardSolve(ops, cfg.iterations, graph=capture)
         Yl = Y[:, m0 * Q : m1 * Q].contiguous()
 
         def one_step(f):
             solver.solve(Yl[f], pinned, alpha, beta, step)
-        launches_per_step = 1 + 3 * cfg.iterations + 3 * cfg.iterations  # residual(3)/bp/update(2)
+        # residual (maxabs, projection, finalize) + N x (back-projection, update + sums,
+        # residual); the all-reduces are NCCL's
+        launches_per_step = 3 + cfg.iterations * (1 + 2 + 3)
     else:
         B = args.batch
         SS = max(1, args.streams)
@@ -416,7 +419,7 @@ def main():
     if world > 1 and not sensor_mode and args.sensor_frames > 0:
         m0, m1 = shard_range(M, rank, world)
         sops = DeviceShardOps(grid, ring, ac, pk.CudaPool(local, "float32"), m0, m1)
-        ssolver = SensorShardedSolver(sops)
+        ssolver = SpeculativeShardSolve(sops, cfg.iterations, graph=capture)
         Yl = Y[:2, m0 * Q: m1 * Q].contiguous()
         ssolver.solve(Yl[0], pinned, alpha, beta, step)  # warm-up (plan, NCCL communicators)
         torch.cuda.synchronize(dev)
@@ -435,8 +438,9 @@ def main():
             "ms_per_iteration": ms_frame / cfg.iterations, "frames": args.sensor_frames,
             "sensors_per_rank": m1 - m0, "iterations_run": res.iterations_run,
             "allreduce_bytes_per_iteration": P * 4 + 8,
-            "path": "SensorShardedSolver: local K1 -> all_reduce(gradient) -> update -> local K2/K3 "
-                    "-> all_reduce(sum r^2), host-driven loop"}
+            "path": "SpeculativeShardSolve: local K1 -> all_reduce(gradient) -> update -> local "
+                    "K2/K3 -> all_reduce(sum r^2), all iterations device-resident"
+                    + (" in one captured CUDA graph (NCCL)" if capture else " (eager)")}
 
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None

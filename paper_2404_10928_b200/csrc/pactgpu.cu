@@ -478,7 +478,12 @@ int upload_params(pk_plan* p, const pk_solver_params* prm, cudaStream_t s) {
     d.tolerance = prm[0].tolerance;
     d.iterations = prm[0].iterations;
     d.nonneg = prm[0].nonneg ? 1 : 0;
+    // unchanged parameters are not re-sent: keeps the sharded entry points free of host
+    // copies, so a solve built from them can be captured into a CUDA graph
+    if (p->params_valid && std::memcmp(&p->params_host, &d, sizeof(d)) == 0) return PK_OK;
     PK_CUDA(cudaMemcpyAsync(p->params, &d, sizeof(d), cudaMemcpyHostToDevice, s));
+    p->params_host = d;
+    p->params_valid = 1;
     return PK_OK;
 }
 

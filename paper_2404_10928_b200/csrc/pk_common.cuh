@@ -296,6 +296,8 @@ struct pk_plan {
     cudaGraphExec_t graph_exec = nullptr;
     cudaStream_t cap_stream = nullptr;
     int graph_iters = -1;
+    pk::DevParams params_host{};  // last uploaded solver parameters
+    int params_valid = 0;
 
     int64_t device_bytes = 0;
 };

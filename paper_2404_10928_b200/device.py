@@ -175,12 +175,25 @@ class DeviceOperator:
                                           ss.data_ptr(), self.stream()))
         return r, ss
 
-    def adjoint_residual(self, scale: float = 1.0):
-        out = self.empty(self.pixels * self.frames)
+    def adjoint_residual(self, scale: float = 1.0, out=None):
+        out = self.empty(self.pixels * self.frames) if out is None else out
         with _torch().cuda.device(self.device):
             N.check(self._lib.pk_adjoint_residual(self._h, out.data_ptr(), float(scale),
                                                   self.stream()))
         return out
+
+    def residual_into(self, x, y, sumsq, r=None):
+        """pk_residual into caller buffers (no allocation: usable under graph capture)."""
+        with _torch().cuda.device(self.device):
+            N.check(self._lib.pk_residual(self._h, x.data_ptr(), y.data_ptr(),
+                                          None if r is None else r.data_ptr(),
+                                          sumsq.data_ptr(), self.stream()))
+
+    def grad_update_into(self, params: "N.SolverParams", x, grad, xo, sums):
+        with _torch().cuda.device(self.device):
+            N.check(self._lib.pk_grad_update(self._h, ctypes.byref(params), x.data_ptr(),
+                                             grad.data_ptr(), xo.data_ptr(), sums.data_ptr(),
+                                             self.stream()))
 
     def grad_update(self, params: "N.SolverParams", x, grad):
         """x_out = prox(x - eta*(grad + beta*tv_grad(x))) and [sum|x_out|, TV(x_out), #nonfinite]."""

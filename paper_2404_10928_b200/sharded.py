@@ -25,7 +25,8 @@ import numpy as np
 from .device import CudaPool, operator_for
 from .solver import DIVERGENCE_STREAK, ReconConfig, solver_params
 
-__all__ = ["shard_range", "DeviceShardOps", "SensorShardedSolver", "FrameShardedSolver"]
+__all__ = ["shard_range", "DeviceShardOps", "SensorShardedSolver", "SpeculativeShardSolve",
+           "FrameShardedSolver", "stop_point"]
 
 
 def shard_range(count: int, rank: int, world: int) -> tuple[int, int]:
@@ -124,6 +125,95 @@ class SensorShardedSolver:
                 break
         img = x.double().cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x, dtype=np.float64)
         return ShardResult(img, np.array(hist, dtype=np.float64).reshape(-1, 4), len(hist), stopped_by)
+
+
+def stop_point(hist_raw, f0: float, alpha: float, beta: float, tolerance: float):
+    """The stopping rules of recon.py:346-363 applied after the fact to per-iteration
+    (data, sum|x|, TV, #nonfinite) rows: returns (iterations_run, stopped_by, history)."""
+    hist = []
+    f_prev, grow = f0, 0
+    for data, l1s, tvs, bad in hist_raw:
+        l1, tvv = alpha * l1s, beta * tvs
+        total = data + l1 + tvv
+        if not math.isfinite(total) or bad > 0:
+            return len(hist), "divergence", hist
+        hist.append((total, data, l1, tvv))
+        grow = grow + 1 if total > f_prev else 0
+        if grow >= DIVERGENCE_STREAK:
+            return len(hist), "divergence", hist
+        rel = abs(total - f_prev) / max(abs(f_prev), 1e-300)
+        f_prev = total
+        if tolerance > 0 and rel < tolerance:
+            return len(hist), "tolerance", hist
+    return len(hist), "max_iterations", hist
+
+
+class SpeculativeShardSolve:
+    """Device-resident sensor-sharded solve: all N iterations are enqueued without a host
+    round trip (iterates kept on the device), the stopping rules are applied afterwards to
+    the recorded objective terms, and the accepted iterate is returned -- the same result as
+    ``SensorShardedSolver.solve``, with iterations past a stop computed but discarded.  With
+    static buffers the whole solve, NCCL all-reduces included, is captured once into a CUDA
+    graph (``graph=True``) and replayed per frame."""
+
+    def __init__(self, ops: "DeviceShardOps", iterations: int, graph: bool = False, group=None):
+        import torch
+
+        self.ops, self.n, self.group = ops, iterations, group
+        op = ops.op
+        P = ops.pixels
+        self.y = torch.zeros(op.sensors * op.samples, device=op.device, dtype=op.tdtype)
+        self.x = torch.zeros(iterations + 1, P, device=op.device, dtype=op.tdtype)
+        self.grad = torch.empty(P, device=op.device, dtype=op.tdtype)
+        self.ss = torch.zeros(iterations + 1, 1, device=op.device, dtype=torch.float64)
+        self.sums = torch.zeros(iterations, 4, device=op.device, dtype=torch.float64)
+        self.graph = None
+        self._use_graph = graph
+        self._params = None
+
+    def _allreduce(self, t):
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            dist.all_reduce(t, group=self.group)
+
+    def _body(self):
+        ops, p = self.ops, self._params
+        ops.op.residual_into(self.x[0], self.y, self.ss[0])  # r0 = -y
+        self._allreduce(self.ss[0])
+        for it in range(self.n):
+            ops.op.adjoint_residual(2.0, out=self.grad)
+            self._allreduce(self.grad)
+            ops.op.grad_update_into(p, self.x[it], self.grad, self.x[it + 1], self.sums[it])
+            ops.op.residual_into(self.x[it + 1], self.y, self.ss[it + 1])
+            self._allreduce(self.ss[it + 1])
+
+    def solve(self, y_local, config: ReconConfig, alpha: float, beta: float, step: float) -> ShardResult:
+        import torch
+
+        params = solver_params(config, alpha, beta, step)
+        key = (params.alpha, params.beta, params.step, params.tv_epsilon, params.nonneg)
+        self.y.copy_(y_local)
+        if self._params is None or self._key != key:
+            self._params, self._key, self.graph = params, key, None
+        if self._use_graph and self.graph is None:
+            self._body()  # warm-up: plan workspaces, parameter upload, NCCL communicators
+            torch.cuda.current_stream().synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._body()
+            self.graph = g
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._body()
+        ss = self.ss[:, 0].cpu().numpy()
+        sums = self.sums.cpu().numpy()
+        rows = [(float(ss[i + 1]), float(sums[i, 0]), float(sums[i, 1]), float(sums[i, 2]))
+                for i in range(self.n)]
+        k, stopped_by, hist = stop_point(rows, float(ss[0]), alpha, beta, config.tolerance)
+        img = self.x[k].double().cpu().numpy()
+        return ShardResult(img, np.array(hist, dtype=np.float64).reshape(-1, 4), k, stopped_by)
 
 
 class FrameShardedSolver:

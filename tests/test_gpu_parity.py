@@ -346,3 +346,31 @@ def test_non_symmetric_geometry_vs_oracle(oracle, pool):
     assert pk.operator_for(g, ring, ac, pool).info.symmetric == 0
     assert res.iterations_run == 10
     assert rel(res.image.values, ref["image"]) <= IMG_TOL[pool.dtype]
+
+
+@pytest.mark.parametrize("graph,tol", [(False, 0.0), (True, 0.0), (True, 1e-3)])
+def test_speculative_shard_solve_matches_device_solver(oracle, graph, tol):
+    """The device-resident sensor-sharded solve (one rank owning every sensor, optionally
+    captured into a CUDA graph) returns the iterate and history of the graph solver."""
+    import torch
+
+    from paper_2404_10928_b200.sharded import DeviceShardOps, SpeculativeShardSolve
+
+    n, M, Q = 64, 32, 128
+    g, ring, ac, ph = pk.make_scene(n, M, Q, seed=3)
+    K = pk.build_time_matrix(g, ring, ac)
+    o = oracle.Operator.of(oracle.make_scene(n, M, Q, 3))
+    y = o.forward(ph.values)
+    alpha, beta = oracle.resolve_regularization(o, y)
+    step = oracle.resolve_step(o, beta, 1e-3)
+    cfg = pk.ReconConfig(alpha, beta, 10, step, tolerance=tol)
+    ref = pk.iterative_reconstruct(K, pk.SensorData("time", M, Q, y), cfg, pool=F32)
+    ops = DeviceShardOps(g, ring, ac, F32, 0, M)
+    solver = SpeculativeShardSolve(ops, cfg.iterations, graph=graph)
+    yt = torch.tensor(y, device="cuda", dtype=torch.float32)
+    for _ in range(2):  # the second call replays the captured graph
+        res = solver.solve(yt, cfg, alpha, beta, step)
+        assert res.iterations_run == ref.iterations_run
+        assert res.stopped_by == ref.stopped_by
+        np.testing.assert_allclose(res.image, ref.image.values, rtol=0, atol=1e-6 * np.abs(ref.image.values).max())
+        np.testing.assert_allclose(res.history[:, 0], ref.objective_history, rtol=1e-5)

@@ -132,3 +132,25 @@ def test_product_does_not_import_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*", "", src).replace("oracle/", ""), f
+
+
+def test_stop_point_rules():
+    """Speculative sharded solve: the stopping rules of recon.py:346-363 applied afterwards."""
+    import math
+
+    from paper_2404_10928_b200.sharded import stop_point
+
+    dec = [(10.0 - i, 0.0, 0.0, 0.0) for i in range(6)]
+    k, why, hist = stop_point(dec, 20.0, 1.0, 1.0, 0.0)
+    assert (k, why, len(hist)) == (6, "max_iterations", 6)
+    bad = dec[:3] + [(math.nan, 0.0, 0.0, 0.0)] + dec[3:]
+    assert stop_point(bad, 20.0, 1.0, 1.0, 0.0)[:2] == (3, "divergence")
+    nonfin = dec[:2] + [(1.0, 0.0, 0.0, 1.0)]
+    assert stop_point(nonfin, 20.0, 1.0, 1.0, 0.0)[:2] == (2, "divergence")
+    grow = [(1.0 + i, 0.0, 0.0, 0.0) for i in range(8)]
+    assert stop_point(grow, 0.5, 1.0, 1.0, 0.0)[:2] == (5, "divergence")
+    flat = [(1.0, 0.0, 0.0, 0.0)] * 4
+    assert stop_point(flat, 2.0, 1.0, 1.0, 1e-6)[:2] == (2, "tolerance")
+    # l1 / tv weights enter the objective
+    k, why, hist = stop_point([(1.0, 2.0, 3.0, 0.0)], 100.0, 0.5, 0.25, 0.0)
+    assert hist[0] == (1.0 + 1.0 + 0.75, 1.0, 1.0, 0.75)
