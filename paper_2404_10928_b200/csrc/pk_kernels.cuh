@@ -1459,16 +1459,40 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
         const int LW = a.win_lw, s_lo = c0 - 1, ns = c1 - s_lo;
         for (int k = threadIdx.x; k < ns; k += kThreads) gs[k] = 0;
         __syncthreads();
-        // integer shared atomics: the sum does not depend on the order, so every window's
-        // loads can be in flight at once (no barrier between windows)
+        // work item = (window, 8 consecutive entries): two 16-B loads; 4 items per thread are
+        // loaded before any is added, and the adds are integer shared atomics (the sum does
+        // not depend on their order: deterministic)
         const int2* wl = a.win_list + (size_t)m * a.nwin;
-#pragma unroll 4
-        for (int wi = 0; wi < a.nwin; ++wi) {
-            const int2 d = __ldg(wl + wi);
-            const int k0 = max(0, s_lo - d.y), k1 = min(LW, c1 - d.y);
-            for (int k = k0 + threadIdx.x; k < k1; k += kThreads) {
-                const int v = __ldcg(a.win + d.x + k);
-                if (v != 0) atomicAdd(gs + d.y + k - s_lo, v);
+        const int per = LW >> 3, items = a.nwin * per;
+        for (int base = threadIdx.x; base < items; base += 4 * kThreads) {
+            int4 v[4][2];
+            int sb[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int it = base + u * kThreads;
+                sb[u] = INT_MIN;
+                v[u][0] = v[u][1] = make_int4(0, 0, 0, 0);
+                if (it < items) {
+                    const int wi = it / per, k = (it - wi * per) * 8;
+                    const int2 d = __ldg(wl + wi);
+                    if (d.y + k + 8 > s_lo && d.y + k < c1) {
+                        const int4* src = reinterpret_cast<const int4*>(a.win + d.x + k);
+                        v[u][0] = __ldcg(src);
+                        v[u][1] = __ldcg(src + 1);
+                        sb[u] = d.y + k - s_lo;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (sb[u] == INT_MIN) continue;
+                const int e[8] = {v[u][0].x, v[u][0].y, v[u][0].z, v[u][0].w,
+                                  v[u][1].x, v[u][1].y, v[u][1].z, v[u][1].w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int j = sb[u] + q;
+                    if (e[q] != 0 && j >= 0 && j < ns) atomicAdd(gs + j, e[q]);
+                }
             }
         }
         __syncthreads();
