@@ -209,6 +209,7 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
         a.win = p->fsym_win;
         a.n = p->nx; a.M = p->M; a.Q = p->Q; a.groups = p->fsym_groups; a.qt = p->fsym_qt;
         a.qclamp = (float)p->Q + 1.5f;
+        a.hx = p->fsym_hx;
         a.st = p->state; a.part_tv = p->part_tv; a.solver = solver;
         const int units = p->fsym_qt * p->fsym_qt * p->fsym_groups;
         switch (p->fsym_L) {
@@ -740,6 +741,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         if (p->fsym) {
             p->fsym_T = kFsTile;
             p->fsym_qt = (n / 2 + kFsTile - 1) / kFsTile;
+            p->fsym_hx = (float)((X[n - 1] - X[0]) / (n - 1) / p->cdt);
             const int need = (int)std::ceil(tile_diag(kFsTile)) + 6;
             p->fsym_L = 0;
             for (int lw : {96, 128, 184, 256, 320})

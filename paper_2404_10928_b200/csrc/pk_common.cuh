@@ -280,6 +280,7 @@ struct pk_plan {
     std::vector<int> sym_h[5];  // host copies: tiles, chunks, cta_chunk0, cta_slot0, tile_slot0
     // rotation-symmetric projector (fp_sym_f32_kernel)
     int fsym = 0, fsym_T = 0, fsym_qt = 0, fsym_L = 0, fsym_smem = 0, fsym_groups = 0;
+    float fsym_hx = 0.f;  // pixel pitch in samples
     int32_t* fsym_win = nullptr;  // [units][4][32][L] window sums of the last projection
     int32_t* fsym_lo = nullptr;   // [units][32] first trace index of each window
     int2* fsym_list = nullptr;    // [M][4 * tiles] per-trace gather list {window offset, lo}

@@ -1081,6 +1081,7 @@ struct FpSymArgs {
     int32_t* win;            // [units][4][32][LW] window sums (unit = tile * groups + group)
     int n, M, Q, groups, qt; // groups = ceil(M/32), qt = quadrant tiles per side
     float qclamp;
+    float hx;                // pixel pitch in samples (pxs[i] ~ pxs[0] + i*hx, fp32)
     DevState* st;
     double* part_tv;         // solver mode: per-unit TV(x) partial (group-0 units, else 0)
     int solver;
@@ -1144,6 +1145,7 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
     }
     __syncthreads();
 
+    if (lane < kFsBatch) rec[32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
     float tv = 0.f;
     const bool do_tv = a.solver && grp == 0;
     // pieces pc = (row warp + 16*(pc / P2), 32-pixel piece pc % P2) of this warp; the 4 image
@@ -1182,50 +1184,35 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
                 if (pj + 1 < n) tv += fabsf(x[pg[g] + n] - xv[g]);
             }
         }
-        // records of this piece's pixels that are non-zero in any image (compacted)
-        const bool nz = xv[0] != 0.f || xv[1] != 0.f || xv[2] != 0.f || xv[3] != 0.f;
-        const uint32_t bal = __ballot_sync(0xffffffffu, nz);
-        const int cnt = __popc(bal);
-        if (cnt == 0) continue;  // warp-uniform
-        if (nz) {
-            float xs[4];
-#pragma unroll
-            for (int g = 0; g < 4; ++g) xs[g] = xv[g] * scale;
-            float4* dst = rec + 2 * __popc(bal & ((1u << lane) - 1u));
-            dst[0] = make_float4(__ldg(a.pxs + ii), xs[0], xs[1], xs[2]);
-            dst[1] = make_float4(xs[3], __int_as_float(__float_as_int(xs[0] + kMagic)),
-                                 __int_as_float(__float_as_int(xs[1] + kMagic)),
-                                 __int_as_float(__float_as_int(xs[2] + kMagic)));
-        }
-        const int cntb = (cnt + kFsBatch - 1) & ~(kFsBatch - 1);
-        if (lane < cntb - cnt) {  // zero-weight padding (adds 0 at a valid window address)
-            const float mb = __int_as_float(kMagicBits);
-            float4* dst = rec + 2 * (cnt + lane);
-            dst[0] = make_float4(X0, 0.f, 0.f, 0.f);
-            dst[1] = make_float4(0.f, mb, mb, mb);
-        }
+        // dense records: lane k writes {xs0, xs1, xs2, xs3} of column i0 + 32*pc + k; the
+        // scatter derives px from k and xq = rint(xs) from xs, so a record is one LDS.128
+        // (the record loads share the shared-memory pipe with the atomics)
+        if (__all_sync(0xffffffffu, xv[0] == 0.f && xv[1] == 0.f && xv[2] == 0.f && xv[3] == 0.f))
+            continue;  // warp-uniform: an all-zero piece
+        rec[lane] = in ? make_float4(xv[0] * scale, xv[1] * scale, xv[2] * scale, xv[3] * scale)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
         __syncwarp();
         if (sensor_ok) {
             const float ey = __ldg(a.pys + jj) - sy;
             const float ey2 = ey * ey;
-            for (int k = 0; k < cntb; k += kFsBatch) {
+            const float pxb = __ldg(a.pxs + i0 + 32 * (pc % P2));  // column k: pxb + k*hx
+            const int kend = min(32, n - (i0 + 32 * (pc % P2)));
+            for (int k = 0; k < kend; k += kFsBatch) {
                 uint32_t ad[kFsBatch];
                 int32_t va[kFsBatch][4], vb[kFsBatch][4];
 #pragma unroll
                 for (int b = 0; b < kFsBatch; ++b) {
-                    const float4 r0 = rec[2 * (k + b)], r1 = rec[2 * (k + b) + 1];
-                    const float ex = r0.x - sx;
+                    const float4 r0 = rec[k + b];  // zero beyond kend (padding entries)
+                    const float ex = fmaf((float)min(k + b, kend - 1), a.hx, pxb) - sx;
                     const float uu = fminf(sqrt_approx(fmaf(ex, ex, ey2)), a.qclamp);
                     const float tb = __fadd_rd(uu, kTwo23);
                     const float fr = uu - (tb - kTwo23);
-                    const float xs[4] = {r0.y, r0.z, r0.w, r1.x};
-                    const int32_t xq[4] = {__float_as_int(r1.y), __float_as_int(r1.z),
-                                           __float_as_int(r1.w), __float_as_int(r1.x + kMagic)};
+                    const float xs[4] = {r0.x, r0.y, r0.z, r0.w};
 #pragma unroll
                     for (int g = 0; g < 4; ++g) {
                         const float fb = fmaf(xs[g], fr, kMagic);
-                        va[b][g] = __float_as_int(fb) - kMagicBits;  // f   -> s0
-                        vb[b][g] = xq[g] - __float_as_int(fb);      // 1-f -> s0-1
+                        va[b][g] = __float_as_int(fb) - kMagicBits;                  // f   -> s0
+                        vb[b][g] = __float_as_int(xs[g] + kMagic) - __float_as_int(fb);  // 1-f -> s0-1
                     }
                     ad[b] = adj + (__float_as_uint(tb) << 7);
                 }
