@@ -113,7 +113,7 @@ void free_plan(pk_plan* p) {
                     p->status_dev, p->part_bp, p->part_tv, p->part_r, p->part_misc, p->state,
                     p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt, p->sym_tiles,
                     p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0, p->sym_tile_slot0,
-                    p->sym_part, p->fsym_win, p->fsym_lo, p->fsym_list};
+                    p->sym_part, p->fsym_win, p->fsym_lo, p->fsym_list, p->fsym_counts};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
@@ -169,9 +169,11 @@ cudaError_t opt_in_smem(int device) {
     smem_kernels<1>(ks);
     smem_kernels<2>(ks);
     smem_kernels<4>(ks);
-    for (const void* k : {(const void*)fp_sym_f32_kernel<96>, (const void*)fp_sym_f32_kernel<128>,
-                          (const void*)fp_sym_f32_kernel<184>, (const void*)fp_sym_f32_kernel<256>,
-                          (const void*)fp_sym_f32_kernel<320>})
+    for (const void* k : {(const void*)fp_sym_f32_kernel<96, false>, (const void*)fp_sym_f32_kernel<128, false>,
+                          (const void*)fp_sym_f32_kernel<184, false>, (const void*)fp_sym_f32_kernel<256, false>,
+                          (const void*)fp_sym_f32_kernel<320, false>, (const void*)fp_sym_f32_kernel<96, true>,
+                          (const void*)fp_sym_f32_kernel<128, true>, (const void*)fp_sym_f32_kernel<184, true>,
+                          (const void*)fp_sym_f32_kernel<256, true>, (const void*)fp_sym_f32_kernel<320, true>})
         ks.push_back(k);
     ks.push_back(sym_kernel_ptr(0));
     for (int iw : kSymIW) ks.push_back(sym_kernel_ptr(iw));
@@ -211,14 +213,19 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
         a.qclamp = (float)p->Q + 1.5f;
         a.hx = p->fsym_hx;
         a.st = p->state; a.part_tv = p->part_tv; a.solver = solver;
+        a.counts = p->fsym_counts;
         const int units = p->fsym_qt * p->fsym_qt * p->fsym_groups;
+        const bool clamp = p->max_delay >= (double)p->Q + 0.5;
+#define PK_FS(LW) (clamp ? fp_sym_f32_kernel<LW, true><<<units, kFsThreads, p->fsym_smem, s>>>(a) \
+                         : fp_sym_f32_kernel<LW, false><<<units, kFsThreads, p->fsym_smem, s>>>(a))
         switch (p->fsym_L) {
-            case 96: fp_sym_f32_kernel<96><<<units, kFsThreads, p->fsym_smem, s>>>(a); break;
-            case 128: fp_sym_f32_kernel<128><<<units, kFsThreads, p->fsym_smem, s>>>(a); break;
-            case 184: fp_sym_f32_kernel<184><<<units, kFsThreads, p->fsym_smem, s>>>(a); break;
-            case 256: fp_sym_f32_kernel<256><<<units, kFsThreads, p->fsym_smem, s>>>(a); break;
-            default: fp_sym_f32_kernel<320><<<units, kFsThreads, p->fsym_smem, s>>>(a); break;
+            case 96: PK_FS(96); break;
+            case 128: PK_FS(128); break;
+            case 184: PK_FS(184); break;
+            case 256: PK_FS(256); break;
+            default: PK_FS(320); break;
         }
+#undef PK_FS
         return;
     }
     if (p->dtype == PK_F32) {
@@ -827,6 +834,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     if (p->fsym) {
         A(alloc(p, &p->fsym_win, (size_t)fsym_units * 4 * 32 * p->fsym_L));
         A(alloc(p, &p->fsym_lo, (size_t)fsym_units * 32));
+        A(alloc(p, &p->fsym_counts, (size_t)fsym_units * 32 * p->fsym_L));
         A(alloc(p, &p->fsym_list, (size_t)p->M * 4 * p->fsym_qt * p->fsym_qt));
     }
     // one CTA per sensor: more, shorter CTAs only add latency (measured 10.3 / 12.8 / 18.2 us
@@ -872,6 +880,17 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         const int ntl = p->fsym_qt * p->fsym_qt, units = ntl * p->fsym_groups;
         fp_sym_lo_kernel<<<units, 32>>>(p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups,
                                         p->fsym_qt, (float)p->Q + 1.5f, p->fsym_lo);
+        {
+            const size_t csm = (size_t)p->fsym_L * 32 * 4;
+            if (p->max_delay >= (double)p->Q + 0.5)
+                fp_sym_count_kernel<true><<<units, kFsThreads, csm>>>(
+                    p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups, p->fsym_qt,
+                    (float)p->Q + 1.5f, p->fsym_hx, p->fsym_L, p->fsym_counts);
+            else
+                fp_sym_count_kernel<false><<<units, kFsThreads, csm>>>(
+                    p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups, p->fsym_qt,
+                    (float)p->Q + 1.5f, p->fsym_hx, p->fsym_L, p->fsym_counts);
+        }
         std::vector<int> lo((size_t)units * 32);
         e = cudaMemcpy(lo.data(), p->fsym_lo, sizeof(int) * lo.size(), cudaMemcpyDeviceToHost);
         std::vector<int2> list((size_t)p->M * 4 * ntl);

@@ -1079,6 +1079,7 @@ struct FpSymArgs {
     const float* sxs;
     const float* sys;
     int32_t* win;            // [units][4][32][LW] window sums (unit = tile * groups + group)
+    const int32_t* counts;   // [units][LW][32] pixels per window slot (fp_sym_count_kernel)
     int n, M, Q, groups, qt; // groups = ceil(M/32), qt = quadrant tiles per side
     float qclamp;
     float hx;                // pixel pitch in samples (pxs[i] ~ pxs[0] + i*hx, fp32)
@@ -1107,7 +1108,60 @@ __global__ void fp_sym_lo_kernel(const float* pxs, const float* pys, const float
     lo_out[u * 32 + lane] = fp_sym_window_lo(pxs, pys, n, i0, j0, __ldg(sxs + mm), __ldg(sys + mm), qclamp);
 }
 
-template <int LW>
+// delay of column k of a 32-pixel piece (pxbs = x of the piece's first column minus the
+// sensor x, in samples) for a sensor at squared row distance ey2: returns 2^23 + s0 (as float)
+// and the fraction fr.  Shared by the projector and its bias-count setup kernel, so both see
+// the same s0 bit for bit.
+template <bool CLAMP>
+__device__ __forceinline__ float fs_delay(float k, float hx, float pxbs, float ey2, float qclamp,
+                                          float& fr) {
+    const float ex = fmaf(k, hx, pxbs);
+    float uu = sqrt_approx(fmaf(ex, ex, ey2));
+    if (CLAMP) uu = fminf(uu, qclamp);
+    const float tb = __fadd_rd(uu, kTwo23);
+    fr = uu - (tb - kTwo23);
+    return tb;
+}
+
+// plan setup: for every (unit, window slot, lane) the number of tile pixels whose delay to
+// the lane's base sensor has s0 = lo + slot.  The projector adds bits(fb) = a + bias (the
+// 1.5*2^23 magic) at s0 and pre-loads each window slot with -count * bias, saving one integer
+// subtract per pair.
+template <bool CLAMP>
+__global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* pxs, const float* pys,
+                                                                  const float* sxs, const float* sys,
+                                                                  int n, int M, int groups, int qt,
+                                                                  float qclamp, float hx, int LW,
+                                                                  int32_t* counts) {
+    extern __shared__ int32_t cnt[];  // [LW][32]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, h = n >> 1;
+    const int u = blockIdx.x, tile = u / groups, grp = u % groups;
+    const int i0 = h + kFsTile * (tile % qt), j0 = h + kFsTile * (tile / qt);
+    const int jend = min(j0 + kFsTile, n);
+    const int mm = min(grp * 32 + lane, M - 1);
+    const float sx = __ldg(sxs + mm), sy = __ldg(sys + mm);
+    const int lo = fp_sym_window_lo(pxs, pys, n, i0, j0, sx, sy, qclamp);
+    for (int q = threadIdx.x; q < LW * 32; q += kFsThreads) cnt[q] = 0;
+    __syncthreads();
+    for (int jj = j0 + warp; jj < jend; jj += kFsThreads / 32) {
+        const float ey = __ldg(pys + jj) - sy;
+        const float ey2 = ey * ey;
+        for (int c0 = i0; c0 < min(i0 + kFsTile, n); c0 += 32) {
+            const float pxbs = __ldg(pxs + c0) - sx;
+            const int kend = min(32, n - c0);
+            for (int k = 0; k < kend; ++k) {
+                float fr;
+                const float tb = fs_delay<CLAMP>((float)k, hx, pxbs, ey2, qclamp, fr);
+                const int slot = (int)(__float_as_uint(tb) - kTwo23Bits) - lo;
+                atomicAdd(cnt + slot * 32 + lane, 1);
+            }
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < LW * 32; q += kFsThreads) counts[(size_t)u * LW * 32 + q] = cnt[q];
+}
+
+template <int LW, bool CLAMP>
 __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ float red_f[kFsThreads / 32];
@@ -1134,14 +1188,19 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
     const bool sensor_ok = m < a.M;
     const int mm = min(m, a.M - 1);
     const float sx = __ldg(a.sxs + mm), sy = __ldg(a.sys + mm);
-    const float X0 = __ldg(a.pxs + i0);
     // window: trace indices [lo, lo + LW) of this tile (fp_sym_window_lo)
     const int lo = fp_sym_window_lo(a.pxs, a.pys, n, i0, j0, sx, sy, a.qclamp);
     // word (g, k, lane) at (g*LW + k)*32 + lane, k = t - lo for trace index t
     const uint32_t adj = win_s + 4u * (uint32_t)lane - 128u * (uint32_t)lo - 128u * kTwo23Bits;
-    {
+    {   // every window slot starts at -count * bias (see fp_sym_count_kernel)
+        const int4* c4 = reinterpret_cast<const int4*>(a.counts + (size_t)u * LW * 32);
         int4* w4 = reinterpret_cast<int4*>(win);
-        for (int q = threadIdx.x; q < WW / 4; q += kFsThreads) w4[q] = make_int4(0, 0, 0, 0);
+        for (int q = threadIdx.x; q < LW * 8; q += kFsThreads) {
+            int4 c = __ldg(c4 + q);
+            c.x *= -kMagicBits; c.y *= -kMagicBits; c.z *= -kMagicBits; c.w *= -kMagicBits;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) w4[g * LW * 8 + q] = c;
+        }
     }
     __syncthreads();
 
@@ -1187,42 +1246,40 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
         // dense records: lane k writes {xs0, xs1, xs2, xs3} of column i0 + 32*pc + k; the
         // scatter derives px from k and xq = rint(xs) from xs, so a record is one LDS.128
         // (the record loads share the shared-memory pipe with the atomics)
-        if (__all_sync(0xffffffffu, xv[0] == 0.f && xv[1] == 0.f && xv[2] == 0.f && xv[3] == 0.f))
-            continue;  // warp-uniform: an all-zero piece
         rec[lane] = in ? make_float4(xv[0] * scale, xv[1] * scale, xv[2] * scale, xv[3] * scale)
                        : make_float4(0.f, 0.f, 0.f, 0.f);
         __syncwarp();
         if (sensor_ok) {
             const float ey = __ldg(a.pys + jj) - sy;
             const float ey2 = ey * ey;
-            const float pxb = __ldg(a.pxs + i0 + 32 * (pc % P2));  // column k: pxb + k*hx
+            // column k of the piece: x = pxs[c0] + k*hx (samples)
+            const float pxbs = __ldg(a.pxs + i0 + 32 * (pc % P2)) - sx;
             const int kend = min(32, n - (i0 + 32 * (pc % P2)));
             for (int k = 0; k < kend; k += kFsBatch) {
                 uint32_t ad[kFsBatch];
                 int32_t va[kFsBatch][4], vb[kFsBatch][4];
 #pragma unroll
                 for (int b = 0; b < kFsBatch; ++b) {
-                    const float4 r0 = rec[k + b];  // zero beyond kend (padding entries)
-                    const float ex = fmaf((float)min(k + b, kend - 1), a.hx, pxb) - sx;
-                    const float uu = fminf(sqrt_approx(fmaf(ex, ex, ey2)), a.qclamp);
-                    const float tb = __fadd_rd(uu, kTwo23);
-                    const float fr = uu - (tb - kTwo23);
+                    const float4 r0 = rec[k + b];
+                    float fr;
+                    const float tb = fs_delay<CLAMP>((float)(k + b), a.hx, pxbs, ey2, a.qclamp, fr);
                     const float xs[4] = {r0.x, r0.y, r0.z, r0.w};
 #pragma unroll
                     for (int g = 0; g < 4; ++g) {
                         const float fb = fmaf(xs[g], fr, kMagic);
-                        va[b][g] = __float_as_int(fb) - kMagicBits;                  // f   -> s0
+                        va[b][g] = __float_as_int(fb);                                   // f -> s0 (+bias)
                         vb[b][g] = __float_as_int(xs[g] + kMagic) - __float_as_int(fb);  // 1-f -> s0-1
                     }
                     ad[b] = adj + (__float_as_uint(tb) << 7);
                 }
 #pragma unroll
                 for (int b = 0; b < kFsBatch; ++b)
+                    if (k + b < kend)  // padding columns beyond the grid add nothing
 #pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                        red_smem_s32(ad[b] + (uint32_t)(g * LW * 128) - 128u, vb[b][g]);
-                        red_smem_s32(ad[b] + (uint32_t)(g * LW * 128), va[b][g]);
-                    }
+                        for (int g = 0; g < 4; ++g) {
+                            red_smem_s32(ad[b] + (uint32_t)(g * LW * 128) - 128u, vb[b][g]);
+                            red_smem_s32(ad[b] + (uint32_t)(g * LW * 128), va[b][g]);
+                        }
             }
         }
         __syncwarp();  // rec is rewritten by the next piece
