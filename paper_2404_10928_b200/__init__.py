@@ -49,6 +49,7 @@ from .solver import (
     tv_gradient,
     tv_value,
 )
+from .fileio import read_matrix, read_signal, write_matrix, write_signal
 from .workloads import CONFIGS, make_scene
 
 __version__ = "1.0.0"
