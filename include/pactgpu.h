@@ -154,6 +154,18 @@ int pk_residual(pk_plan* plan, const void* x_dev, const void* y_dev, void* r_out
 /* out_dev = scale * K_shard^T r for the residual kept by the last pk_residual. */
 int pk_adjoint_residual(pk_plan* plan, void* out_dev, double scale, void* stream);
 
+/* Frequency-domain operator of build_freq_matrix (forward.py:218-234), matrix-free:
+ *   K_f[m*q_n + (n-1), p] = i c k_n exp(-i k_n d_mp) / d_mp,  k_n = 2 pi n / (samples dt c).
+ * Complex buffers are interleaved (re, im) in the plan dtype (complex64 / complex128).
+ * pk_freq_matvec:  y_dev[(m-begin)*q_n + n-1] = (K_f x)[...]   (x real, [P])
+ * pk_freq_adjoint: out_dev[p] = scale * (K_f^H y)[p]           (y complex [M*q_n], out complex [P])
+ * Replaces forward._matvec / _adjoint_matvec for frequency-domain K (forward.py:237-250).
+ * The forward keeps a partial-sum workspace in the plan, allocated on the first call for a
+ * given q_n (the only allocation outside pk_plan_create). */
+int pk_freq_matvec(pk_plan* plan, int32_t q_n, const void* x_dev, void* y_dev, void* stream);
+int pk_freq_adjoint(pk_plan* plan, int32_t q_n, const void* y_dev, void* out_dev, double scale,
+                    void* stream);
+
 /* Index dump (verification): for local sensors [ma, mb) (relative to sensor_begin),
  * s0_dev[(m-ma)*P + p] = floor(hypot(px - sx, py - sy) / (c*dt)) and frac_dev likewise,
  * evaluated in fp64 exactly as forward.py:157-182 (s0 int64, frac double; frac may be NULL). */

@@ -14,7 +14,9 @@ from .measurement import (
     MeasurementMatrix,
     SensorData,
     TruncationWarning,
+    FreqOperator,
     add_noise,
+    build_freq_matrix,
     build_time_matrix,
     forward_project,
 )

@@ -17,6 +17,7 @@
 
 #include "pactgpu.h"
 #include "pk_kernels.cuh"
+#include "pk_freq.cuh"
 
 using namespace pk;
 
@@ -113,7 +114,8 @@ void free_plan(pk_plan* p) {
                     p->status_dev, p->part_bp, p->part_tv, p->part_r, p->part_misc, p->state,
                     p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt, p->sym_tiles,
                     p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0, p->sym_tile_slot0,
-                    p->sym_part, p->fsym_win, p->fsym_lo, p->fsym_list, p->fsym_counts};
+                    p->sym_part, p->fsym_win, p->fsym_lo, p->fsym_list, p->fsym_counts,
+                    p->freq_part};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
@@ -1085,6 +1087,83 @@ int pk_reconstruct_host(pk_plan* p, const pk_solver_params* prm, const double* y
     PK_TRY(pk_reconstruct_host_async(p, prm, y_host, x_out_host, hist_host, status_host, stream));
     DeviceGuard g(p->device);
     PK_CUDA(cudaStreamSynchronize(S(stream)));
+    return PK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// frequency-domain operator (build_freq_matrix, forward.py:218-234), matrix-free
+
+namespace {
+int freq_setup(pk_plan* p, int q_n, FreqArgs& a, int& zblocks) {
+    if (q_n < 1) return fail(PK_ERR_INVALID, "q_n must be >= 1");
+    a.px = p->px; a.py = p->py; a.sx = p->sx; a.sy = p->sy;
+    a.nx = p->nx; a.P = p->P; a.M = p->M; a.Q = p->Q; a.qn = q_n;
+    a.cdt = p->cdt;
+    a.c = p->c;
+    a.kscale = 2.0 * 3.141592653589793 / ((double)p->Q * p->dt * p->c);  // AcousticConfig.k_values
+    zblocks = (q_n + kFreqThreads * kFreqRun - 1) / (kFreqThreads * kFreqRun);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+    a.chunks = std::max(1, std::min(64, (4 * sms + p->M * zblocks - 1) / (p->M * zblocks)));
+    a.chunks = std::min(a.chunks, std::max(1, p->P / kFreqPix));
+    return PK_OK;
+}
+}  // namespace
+
+int pk_freq_matvec(pk_plan* p, int32_t q_n, const void* x, void* y, void* stream) {
+    if (!p || !x || !y) return fail(PK_ERR_INVALID, "NULL argument");
+    if (p->nf != 1) return fail(PK_ERR_UNSUPPORTED, "frequency operator is single-frame");
+    DeviceGuard g(p->device);
+    FreqArgs a{};
+    int zb = 0;
+    PK_TRY(freq_setup(p, q_n, a, zb));
+    const size_t need = (size_t)a.chunks * p->M * q_n * 2 * tsize(p);
+    if (need > p->freq_part_bytes) {  // grows once per (q_n, geometry); not on later calls
+        if (p->freq_part) cudaFree(p->freq_part);
+        p->freq_part = nullptr;
+        p->freq_part_bytes = 0;
+        PK_CUDA(cudaMalloc(&p->freq_part, need));
+        p->freq_part_bytes = need;
+    }
+    a.x = x; a.part = p->freq_part; a.out = y;
+    cudaStream_t s = S(stream);
+    const dim3 grid(p->M, a.chunks, zb);
+    const int sb = (int)std::min<size_t>(148 * 8, ((size_t)p->M * q_n + kThreads - 1) / kThreads);
+    if (p->dtype == PK_F32) {
+        freq_fwd_kernel<float><<<grid, kFreqThreads, 0, s>>>(a);
+        freq_fwd_sum_kernel<float><<<sb, kThreads, 0, s>>>(a);
+    } else {
+        freq_fwd_kernel<double><<<grid, kFreqThreads, 0, s>>>(a);
+        freq_fwd_sum_kernel<double><<<sb, kThreads, 0, s>>>(a);
+    }
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+int pk_freq_adjoint(pk_plan* p, int32_t q_n, const void* y, void* out, double scale, void* stream) {
+    if (!p || !y || !out) return fail(PK_ERR_INVALID, "NULL argument");
+    if (p->nf != 1) return fail(PK_ERR_UNSUPPORTED, "frequency operator is single-frame");
+    DeviceGuard g(p->device);
+    FreqArgs a{};
+    int zb = 0;
+    PK_TRY(freq_setup(p, q_n, a, zb));
+    a.y = y; a.out = out; a.scale = scale;
+    const size_t sm = (size_t)q_n * 2 * tsize(p);
+    if (sm > 200 * 1024) return fail(PK_ERR_UNSUPPORTED, "q_n = %d too large for the adjoint", q_n);
+    cudaStream_t s = S(stream);
+    const int grid = (p->P + kThreads - 1) / kThreads;
+    if (p->dtype == PK_F32) {
+        if (sm > 48 * 1024)
+            PK_CUDA(cudaFuncSetAttribute((const void*)freq_adj_kernel<float>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        freq_adj_kernel<float><<<grid, kThreads, sm, s>>>(a);
+    } else {
+        if (sm > 48 * 1024)
+            PK_CUDA(cudaFuncSetAttribute((const void*)freq_adj_kernel<double>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        freq_adj_kernel<double><<<grid, kThreads, sm, s>>>(a);
+    }
+    PK_CHECK_LAUNCH();
     return PK_OK;
 }
 

@@ -292,6 +292,8 @@ struct pk_plan {
     int fp_T = 0, fp_tiles_x = 0, fp_tiles_y = 0, fp_groups = 0, fp_L = 0, fp_bits = 0,
         fp_smem = 0;
     int misc_blocks = 0;
+    void* freq_part = nullptr;  // frequency-domain forward partials (grown on first use)
+    size_t freq_part_bytes = 0;
 
     // graph cache of pk_reconstruct
     cudaGraph_t graph = nullptr;

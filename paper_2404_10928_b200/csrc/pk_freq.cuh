@@ -1,0 +1,180 @@
+// pk_freq.cuh -- matrix-free frequency-domain operator.
+//
+// The reference builds K_f[m*q_n + (n-1), p] = i c k_n exp(-i k_n d_mp) / d_mp densely
+// (forward.py:218-234, Eq. 7 of the paper), k_n = 2 pi n / (q_s dt c), n = 1..q_n.  With
+// u = d / (c dt) (the delay in samples) the phase is k_n d = 2 pi n f, f = frac(u / q_s), so
+//   forward  y[m, n] = i c k_n  sum_p x_p z_mp^n / d_mp,        z = exp(-2 pi i f)
+//   adjoint  g_p     = sum_m (1/d_mp) sum_n (-i c k_n) y[m, n] conj(z_mp)^n
+// Phases are reduced in fp64 (f and frac(n0 f)), then advanced in the working type by
+// complex multiplication over short runs of n (16 in the forward, 32 in the adjoint) and
+// re-anchored, so the recurrence error stays ~run length x ulp.  Distances come from the fp64
+// coordinates with the reference's hypot (bit-exact u).  Sums over pixels are written as
+// per-chunk partials and added in chunk order (deterministic).
+#pragma once
+#include "pk_common.cuh"
+
+namespace pk {
+
+template <typename T>
+struct Cplx { using type = float2; };
+template <>
+struct Cplx<double> { using type = double2; };
+
+template <typename T>
+__device__ __forceinline__ void sincospi_t(T a, T* s, T* c);
+template <>
+__device__ __forceinline__ void sincospi_t<float>(float a, float* s, float* c) { sincospif(a, s, c); }
+template <>
+__device__ __forceinline__ void sincospi_t<double>(double a, double* s, double* c) { sincospi(a, s, c); }
+
+constexpr int kFreqRun = 16;      // forward: consecutive n per thread
+constexpr int kFreqThreads = 128; // forward: threads per CTA (n-blocks)
+constexpr int kFreqPix = 64;      // forward: pixels staged per smem round
+constexpr int kFreqAdjRun = 32;   // adjoint: Horner run length between exact phase anchors
+
+struct FreqArgs {
+    const double *px, *py, *sx, *sy;  // fp64 coordinates (plan)
+    int nx, P, M, Q, qn;
+    double cdt;
+    int chunks;            // forward: pixel chunks (partials)
+    const void* x;         // forward input [P] (plan dtype)
+    void* part;            // forward partials [chunks][M][qn] complex
+    const void* y;         // adjoint input [M][qn] complex
+    void* out;             // forward: y [M][qn] complex; adjoint: g [P] complex
+    double c, kscale;      // c and 2 pi / (q_s dt c) (k_n = n * kscale)
+    double scale;          // adjoint multiplier
+};
+
+// forward, stage 1: CTA (sensor m, pixel chunk, n-range); thread t owns n = n0 .. n0+15
+template <typename T>
+__global__ void __launch_bounds__(kFreqThreads) freq_fwd_kernel(FreqArgs a) {
+    using C = typename Cplx<T>::type;
+    __shared__ T s_a[kFreqPix];       // x_p / d_mp
+    __shared__ double s_f[kFreqPix];  // frac(u / Q)
+    __shared__ C s_step[kFreqPix];    // exp(-2 pi i f)
+    const int m = blockIdx.x, chunk = blockIdx.y;
+    const int n0 = 1 + (blockIdx.z * kFreqThreads + threadIdx.x) * kFreqRun;
+    const int p0 = (int)((long long)a.P * chunk / a.chunks), p1 = (int)((long long)a.P * (chunk + 1) / a.chunks);
+    const double sxm = a.sx[m], sym = a.sy[m];
+    const T* x = static_cast<const T*>(a.x);
+    T re[kFreqRun], im[kFreqRun];
+#pragma unroll
+    for (int k = 0; k < kFreqRun; ++k) re[k] = im[k] = (T)0;
+    for (int pb = p0; pb < p1; pb += kFreqPix) {
+        __syncthreads();
+        for (int q = threadIdx.x; q < kFreqPix; q += kFreqThreads) {
+            const int p = pb + q;
+            T av = (T)0;
+            double f = 0.0;
+            if (p < p1) {
+                const double d = hypot_libm(__dsub_rn(a.px[p % a.nx], sxm), __dsub_rn(a.py[p / a.nx], sym));
+                const double u = __ddiv_rn(d, a.cdt);
+                const double v = u / a.Q;
+                f = v - floor(v);
+                av = (T)((double)x[p] / d);
+            }
+            T s, c;
+            sincospi_t<T>((T)(-2.0 * f), &s, &c);
+            s_a[q] = av;
+            s_f[q] = f;
+            s_step[q] = C{c, s};
+        }
+        __syncthreads();
+        if (n0 > a.qn) continue;
+        const int np = min(kFreqPix, p1 - pb);
+        for (int q = 0; q < np; ++q) {
+            const double f = s_f[q];
+            const double t0 = (double)n0 * f;
+            T zs, zc;
+            sincospi_t<T>((T)(-2.0 * (t0 - floor(t0))), &zs, &zc);
+            const C st = s_step[q];
+            const T av = s_a[q];
+            T wr = av * zc, wi = av * zs;  // a_p z^n0
+#pragma unroll
+            for (int k = 0; k < kFreqRun; ++k) {
+                re[k] += wr;
+                im[k] += wi;
+                const T nr = wr * st.x - wi * st.y;
+                wi = wr * st.y + wi * st.x;
+                wr = nr;
+            }
+        }
+    }
+    C* part = static_cast<C*>(a.part) + ((size_t)chunk * a.M + m) * a.qn;
+#pragma unroll
+    for (int k = 0; k < kFreqRun; ++k)
+        if (n0 + k <= a.qn) part[n0 + k - 1] = C{re[k], im[k]};
+}
+
+// forward, stage 2: y[m, n] = i c k_n sum_chunks part (chunk order)
+template <typename T>
+__global__ void __launch_bounds__(kThreads) freq_fwd_sum_kernel(FreqArgs a) {
+    using C = typename Cplx<T>::type;
+    const size_t total = (size_t)a.M * a.qn;
+    const C* part = static_cast<const C*>(a.part);
+    C* y = static_cast<C*>(a.out);
+    for (size_t i = (size_t)blockIdx.x * kThreads + threadIdx.x; i < total; i += (size_t)gridDim.x * kThreads) {
+        T sr = 0, si = 0;
+        for (int c = 0; c < a.chunks; ++c) {
+            const C v = part[(size_t)c * total + i];
+            sr += v.x;
+            si += v.y;
+        }
+        const int n = (int)(i % a.qn) + 1;
+        const T w = (T)(a.c * a.kscale * n);  // c k_n
+        y[i] = C{-w * si, w * sr};            // i * w * (sr + i si)
+    }
+}
+
+// adjoint: thread = pixel; per sensor, block-Horner over n with exact phase anchors every
+// kFreqAdjRun wavenumbers.  b_n = -i c k_n y[m, n] * scale staged in shared memory.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) freq_adj_kernel(FreqArgs a) {
+    using C = typename Cplx<T>::type;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* b = reinterpret_cast<C*>(smem_raw);  // [qn]
+    const int p = blockIdx.x * kThreads + threadIdx.x;
+    const bool valid = p < a.P;
+    const double pxv = valid ? a.px[p % a.nx] : 0.0, pyv = valid ? a.py[p / a.nx] : 0.0;
+    const C* y = static_cast<const C*>(a.y);
+    T gr = 0, gi = 0;
+    for (int m = 0; m < a.M; ++m) {
+        __syncthreads();
+        for (int n = threadIdx.x; n < a.qn; n += kThreads) {
+            const C v = y[(size_t)m * a.qn + n];
+            const T w = (T)(a.c * a.kscale * (n + 1) * a.scale);  // c k_n * scale
+            b[n] = C{w * v.y, -w * v.x};                          // -i * w * v
+        }
+        __syncthreads();
+        if (!valid) continue;
+        const double d = hypot_libm(__dsub_rn(pxv, a.sx[m]), __dsub_rn(pyv, a.sy[m]));
+        const double u = __ddiv_rn(d, a.cdt);
+        const double v = u / a.Q;
+        const double f = v - floor(v);
+        T s1, c1;
+        sincospi_t<T>((T)(2.0 * f), &s1, &c1);  // z' = conj(z) = exp(+2 pi i f)
+        T sr = 0, si = 0;
+        for (int nb = 1; nb <= a.qn; nb += kFreqAdjRun) {
+            const int ne = min(a.qn, nb + kFreqAdjRun - 1);
+            // h = sum_{n=nb..ne} b_n z'^(n - nb) by Horner from the top
+            T hr = 0, hi = 0;
+            for (int n = ne; n >= nb; --n) {
+                const C bn = b[n - 1];
+                const T tr = hr * c1 - hi * s1 + bn.x;
+                hi = hr * s1 + hi * c1 + bn.y;
+                hr = tr;
+            }
+            const double t0 = (double)nb * f;
+            T zs, zc;
+            sincospi_t<T>((T)(2.0 * (t0 - floor(t0))), &zs, &zc);  // z'^nb
+            sr += hr * zc - hi * zs;
+            si += hr * zs + hi * zc;
+        }
+        const T inv = (T)(1.0 / d);
+        gr += sr * inv;
+        gi += si * inv;
+    }
+    if (valid) static_cast<C*>(a.out)[p] = C{gr, gi};
+}
+
+}  // namespace pk

@@ -248,6 +248,40 @@ class DeviceOperator:
                 self.stream()))
         return x.reshape(F, self.pixels), hist.reshape(F, 4, n), status.reshape(F, 2)
 
+    # -- frequency-domain operator (build_freq_matrix, forward.py:218-234) ------------
+    @property
+    def cdtype(self):
+        torch = _torch()
+        return torch.complex64 if self.tdtype == torch.float32 else torch.complex128
+
+    def freq_matvec(self, x, q_n: int):
+        """K_f x for a real image x: complex [sensors * q_n] device tensor."""
+        torch = _torch()
+        xt = self.tensor(x)
+        if xt.numel() != self.pixels:
+            raise ValueError(f"matrix has {self.pixels} columns but vector has {xt.numel()}")
+        out = torch.empty(self.sensors * q_n, device=self.device, dtype=self.cdtype)
+        with torch.cuda.device(self.device):
+            N.check(self._lib.pk_freq_matvec(self._h, int(q_n), xt.data_ptr(), out.data_ptr(),
+                                             self.stream()))
+        return out
+
+    def freq_adjoint(self, y, q_n: int, scale: float = 1.0):
+        """scale * K_f^H y for complex y [sensors * q_n]: complex [P] device tensor."""
+        torch = _torch()
+        if isinstance(y, torch.Tensor):
+            yt = y.to(device=self.device, dtype=self.cdtype).contiguous()
+        else:
+            yt = torch.from_numpy(np.ascontiguousarray(y, dtype=np.complex128)).to(
+                device=self.device, dtype=self.cdtype).contiguous()
+        if yt.numel() != self.sensors * q_n:
+            raise ValueError(f"matrix has {self.sensors * q_n} rows but signal has {yt.numel()} values")
+        out = torch.empty(self.pixels, device=self.device, dtype=self.cdtype)
+        with torch.cuda.device(self.device):
+            N.check(self._lib.pk_freq_adjoint(self._h, int(q_n), yt.data_ptr(), out.data_ptr(),
+                                              float(scale), self.stream()))
+        return out
+
     def index_dump(self, ma: int = 0, mb: int | None = None):
         """fp64 (s0, frac) for local sensors [ma, mb) as device tensors [(mb-ma), P]."""
         torch = _torch()

@@ -28,6 +28,8 @@ __all__ = [
     "TruncationWarning",
     "DenseOperator",
     "build_time_matrix",
+    "build_freq_matrix",
+    "FreqOperator",
     "forward_project",
     "add_noise",
     "device_operator",
@@ -163,6 +165,8 @@ class MeasurementMatrix:
         dump (pk_index_dump, the same s0/frac the reference computes) -- small scenes only."""
         if self.entries_ is not None:
             return self.entries_
+        if self.domain == "frequency":
+            return self._freq_entries()
         M, Q = self.ring.count, self.acoustic.q_s
         P = self.grid.size
         if M * Q * P > 64 * 1024 * 1024:
@@ -184,8 +188,62 @@ class MeasurementMatrix:
         return K
 
 
+    def _freq_entries(self) -> np.ndarray:
+        """Dense i c k_n exp(-i k_n d) / d (forward.py:218-234) on the host -- small scenes
+        only; the device products never form it."""
+        M, Qn, P = self.ring.count, self.acoustic.q_n, self.grid.size
+        if M * Qn * P > 16 * 1024 * 1024:
+            raise MemoryError(f"refusing to materialise a {M * Qn} x {P} dense complex matrix")
+        pix = self.grid.pixel_coords()
+        pos = np.asarray(self.ring.positions)
+        d = np.hypot(pix[None, :, 0] - pos[:, 0:1], pix[None, :, 1] - pos[:, 1:2])
+        k = self.acoustic.k_values
+        K = np.empty((M * Qn, P), dtype=np.complex128)
+        for m in range(M):
+            blk = (1j * self.acoustic.c * k)[:, None] * np.exp(-1j * k[:, None] * d[m][None, :])
+            blk /= d[m][None, :]
+            K[m * Qn:(m + 1) * Qn] = blk
+        K.setflags(write=False)
+        object.__setattr__(self, "entries_", K)
+        return K
+
+
 # ---------------------------------------------------------------------------
 # operators
+
+
+class FreqOperator:
+    """Frequency-domain operator (forward.py:218-234) run matrix-free on the device
+    (pk_freq_matvec / pk_freq_adjoint): no (M*q_n, P) complex matrix is formed."""
+
+    def __init__(self, grid, ring, acoustic, pool: CudaPool):
+        self.dev_op = operator_for(grid, ring, acoustic, pool)
+        self.q_n = int(acoustic.q_n)
+        self.pool = pool
+        self.device = self.dev_op.device
+        self.tdtype = self.dev_op.cdtype
+        self.rows, self.cols = ring.count * self.q_n, grid.size
+
+    def tensor(self, a):
+        import torch
+
+        if isinstance(a, torch.Tensor):
+            return a.to(device=self.device, dtype=self.tdtype)
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.complex128)).to(self.device, self.tdtype)
+
+    def matvec(self, x):
+        """K_f x; a complex x is applied as K_f Re(x) + i K_f Im(x)."""
+        import torch
+
+        if isinstance(x, torch.Tensor) and x.is_complex() or (not isinstance(x, torch.Tensor) and np.iscomplexobj(x)):
+            xt = self.tensor(x)
+            re = self.dev_op.freq_matvec(xt.real.contiguous(), self.q_n)
+            im = self.dev_op.freq_matvec(xt.imag.contiguous(), self.q_n)
+            return re + 1j * im
+        return self.dev_op.freq_matvec(x, self.q_n)
+
+    def adjoint(self, y, scale: float = 1.0):
+        return self.dev_op.freq_adjoint(y, self.q_n, scale)
 
 
 class DenseOperator:
@@ -245,6 +303,8 @@ def device_operator(K, pool=None):
     explicit = getattr(K, "entries_", None) if isinstance(K, MeasurementMatrix) else None
     if has_geo and explicit is None and K.domain == "time":
         return operator_for(prov["grid"], prov["ring"], prov["acoustic"], pool)
+    if has_geo and explicit is None and K.domain == "frequency":
+        return FreqOperator(prov["grid"], prov["ring"], prov["acoustic"], pool)
     entries = K.entries if not isinstance(K, np.ndarray) else K
     key = (id(entries), pool)
     op = _dense_cache.get(key)
@@ -324,6 +384,23 @@ def build_time_matrix(grid, ring, acoustic) -> MeasurementMatrix:
         None,
         provenance={"grid": grid, "ring": ring, "acoustic": acoustic, "truncated_pairs": truncated},
     )
+
+
+def build_freq_matrix(grid, ring, acoustic) -> MeasurementMatrix:
+    """Frequency-domain operator of forward.py:218-234 (Eq. 7), geometry-backed: products run
+    matrix-free on the device, the dense complex matrix only forms if ``.entries`` is asked
+    for.  Same validation as the reference (ring encloses the grid, no sensor on a pixel)."""
+    check_enclosure(grid, ring)
+    xs = grid.origin[0] + np.arange(grid.nx) * grid.dx
+    ys = grid.origin[1] + np.arange(grid.ny) * grid.dx
+    pos = np.asarray(ring.positions)
+    hit = np.isin(pos[:, 0], xs) & np.isin(pos[:, 1], ys)
+    if hit.any():
+        m = int(np.flatnonzero(hit)[0])
+        i = int(np.flatnonzero(xs == pos[m, 0])[0])
+        j = int(np.flatnonzero(ys == pos[m, 1])[0])
+        raise GeometryError(f"sensor {m} coincides with pixel index {j * grid.nx + i}")
+    return MeasurementMatrix("frequency", None, provenance={"grid": grid, "ring": ring, "acoustic": acoustic})
 
 
 def _grid_values(x):

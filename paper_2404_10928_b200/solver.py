@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _native as N
 from .device import CudaPool, DeviceOperator
-from .measurement import DenseOperator, SensorData, _as_pool, device_operator
+from .measurement import DenseOperator, FreqOperator, SensorData, _as_pool, device_operator
 from .scene import ImageField
 
 __all__ = [
@@ -220,7 +220,7 @@ def estimate_lipschitz(K, iterations: int = 50, seed: int = 0, pool=None) -> flo
     op = device_operator(K, pool)
     cols = op.pixels if isinstance(op, DeviceOperator) else op.cols
     rng = np.random.default_rng(seed)
-    is_cplx = isinstance(op, DenseOperator) and op.tdtype.is_complex
+    is_cplx = isinstance(op, (DenseOperator, FreqOperator)) and op.tdtype.is_complex
     v = rng.standard_normal(cols) + 1j * rng.standard_normal(cols) if is_cplx else rng.standard_normal(cols)
     nrm = np.linalg.norm(v)
     if nrm == 0:
@@ -301,8 +301,9 @@ def objective(K, x, y, config: ReconConfig, pool=None) -> ObjectiveParts:
 # the solver
 
 
-def _dense_loop(op: DenseOperator, yv, alpha, beta, eta, config, shape):
-    """Explicit-matrix mode: the same loop with cuBLAS GEMV products (host stopping checks)."""
+def _dense_loop(op, yv, alpha, beta, eta, config, shape):
+    """Explicit-matrix (cuBLAS GEMV) and frequency-domain (matrix-free) operators: the same
+    loop with device products and host stopping checks."""
     import torch
 
     dev = op.device

@@ -125,6 +125,28 @@ def small():
         print("wrote scene", n, M, Q, seed, {k: (v.iterations_run, v.stopped_by) for k, v in res.items()})
 
 
+def freq():
+    """Frequency-domain operator (build_freq_matrix, forward.py:218-234): products and a
+    10-iteration reconstruction of the reference on a small scene."""
+    g, ring, ac, ph = pk.make_scene(16, 8, 40, seed=0)
+    ac = pk.AcousticConfig(c=ac.c, dt=ac.dt, q_s=ac.q_s, q_n=12)
+    K = pk.build_freq_matrix(g, ring, ac)
+    y = pk.forward_project(K, ph)
+    rng = np.random.default_rng(21)
+    r = rng.standard_normal(K.rows) + 1j * rng.standard_normal(K.rows)
+    khr = pk.kernels.matvec_adjoint_serial(K.entries, r)
+    cfg = pk.resolve_config(pk.ReconConfig(iterations=10), K, y)
+    out = pk.iterative_reconstruct(K, y, cfg)
+    np.savez_compressed(os.path.join(HERE, "freq_16_8_40_0.npz"),
+                        q_n=np.array(12), y=y.values, r=r, KHr=khr,
+                        pinned=np.array([cfg.alpha, cfg.beta, cfg.step]), image=out.image.values,
+                        hist=np.stack([out.objective_history, out.data_term_history,
+                                       out.l1_history, out.tv_history]),
+                        meta=np.array([out.iterations_run,
+                                       ["max_iterations", "tolerance", "divergence"].index(out.stopped_by)]))
+    print("wrote freq fixture", out.iterations_run, out.stopped_by, cfg)
+
+
 def cfg1():
     t = time.time()
     g, ring, ac, ph = pk.make_scene(128, 128, 1024, seed=0)
@@ -146,9 +168,14 @@ def cfg1():
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg1", action="store_true")
+    ap.add_argument("--only-freq", action="store_true")
     a = ap.parse_args()
+    if a.only_freq:
+        freq()
+        sys.exit(0)
     geometry()
     kat()
     small()
+    freq()
     if a.cfg1:
         cfg1()

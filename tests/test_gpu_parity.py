@@ -374,3 +374,51 @@ def test_speculative_shard_solve_matches_device_solver(oracle, graph, tol):
         assert res.stopped_by == ref.stopped_by
         np.testing.assert_allclose(res.image, ref.image.values, rtol=0, atol=1e-6 * np.abs(ref.image.values).max())
         np.testing.assert_allclose(res.history[:, 0], ref.objective_history, rtol=1e-5)
+
+
+@pytest.mark.parametrize("dtype,tol_p,tol_r", [("float64", 1e-12, 1e-10), ("float32", 2e-5, 1e-4)])
+def test_frequency_operator_vs_reference(dtype, tol_p, tol_r):
+    """Matrix-free frequency-domain products and reconstruction (build_freq_matrix,
+    forward.py:218-234) against the reference's own outputs (tests/golden/freq_16_8_40_0.npz)."""
+    g = np.load(os.path.join(GOLDEN, "freq_16_8_40_0.npz"))
+    grid, ring, ac, ph = pk.make_scene(16, 8, 40, seed=0)
+    ac = pk.AcousticConfig(c=ac.c, dt=ac.dt, q_s=ac.q_s, q_n=int(g["q_n"]))
+    K = pk.build_freq_matrix(grid, ring, ac)
+    pool = pk.CudaPool(0, dtype)
+
+    def rel(a, b):
+        return float(np.linalg.norm(np.asarray(a) - b) / np.linalg.norm(b))
+
+    y = pk.forward_project(K, ph, pool=pool)
+    assert y.domain == "frequency" and rel(y.values, g["y"]) <= tol_p
+    from paper_2404_10928_b200.measurement import device_operator
+
+    khr = device_operator(K, pool).adjoint(g["r"]).cpu().numpy()
+    assert rel(khr, g["KHr"]) <= tol_p
+    alpha, beta, step = (float(v) for v in g["pinned"])
+    ys = pk.SensorData("frequency", ring.count, ac.q_n, g["y"])
+    res = pk.iterative_reconstruct(K, ys, pk.ReconConfig(alpha, beta, 10, step), pool=pool)
+    assert res.iterations_run == int(g["meta"][0])
+    assert rel(res.image.values, g["image"]) <= tol_r
+    np.testing.assert_allclose(res.objective_history, g["hist"][0], rtol=tol_r)
+
+
+def test_frequency_operator_larger_scene_vs_dense():
+    """A scene with several forward chunks / n-blocks: fp32 products against the dense
+    complex128 matrix (materialised on the host)."""
+    grid, ring, ac, ph = pk.make_scene(48, 24, 256, seed=2)
+    ac = pk.AcousticConfig(c=ac.c, dt=ac.dt, q_s=ac.q_s, q_n=200)
+    K = pk.build_freq_matrix(grid, ring, ac)
+    A = K.entries
+    rng = np.random.default_rng(1)
+    x = ph.values + 0.1 * rng.random(grid.size)
+    from paper_2404_10928_b200.measurement import device_operator
+
+    op = device_operator(K, pk.CudaPool(0, "float32"))
+    yd = op.matvec(x).cpu().numpy()
+    yr = A @ x
+    assert np.linalg.norm(yd - yr) / np.linalg.norm(yr) <= 2e-5
+    yy = rng.standard_normal(A.shape[0]) + 1j * rng.standard_normal(A.shape[0])
+    gd = op.adjoint(yy).cpu().numpy()
+    gr = A.conj().T @ yy
+    assert np.linalg.norm(gd - gr) / np.linalg.norm(gr) <= 2e-5

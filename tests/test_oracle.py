@@ -131,3 +131,22 @@ def test_thread_count_independent(oracle):
     assert np.array_equal(a.forward(s.phantom), b.forward(s.phantom))
     r = np.random.default_rng(0).standard_normal(a.rows)
     assert np.array_equal(a.adjoint(r), b.adjoint(r))
+
+
+def test_frequency_operator_matches_reference(oracle):
+    """The frequency-domain oracle (forward.py:218-234) against the reference's own products
+    and 10-iteration reconstruction (tests/golden/freq_16_8_40_0.npz)."""
+    g = np.load(os.path.join(GOLDEN, "freq_16_8_40_0.npz"))
+    s = oracle.make_scene(16, 8, 40, 0)
+    op = oracle.FreqDense(s, int(g["q_n"]))
+    y = op.forward(s.phantom)
+    assert np.max(np.abs(y - g["y"])) <= 1e-14 * np.max(np.abs(g["y"]))
+    khr = op.adjoint(g["r"])
+    assert np.max(np.abs(khr - g["KHr"])) <= 1e-13 * np.max(np.abs(g["KHr"]))
+    alpha, beta, step = g["pinned"]
+    a2, b2 = oracle.resolve_regularization(op, g["y"])
+    assert abs(a2 - alpha) <= 1e-12 * alpha and abs(b2 - beta) <= 1e-12 * beta
+    out = oracle.reconstruct(op, g["y"], alpha, beta, step, 10)
+    assert out["iterations_run"] == int(g["meta"][0])
+    assert oracle.rel_l2(out["image"], g["image"]) <= 1e-12
+    np.testing.assert_allclose(out["objective_history"], g["hist"][0], rtol=1e-12)
