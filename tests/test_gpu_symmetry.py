@@ -91,3 +91,55 @@ def test_symmetric_adjoint_fixed_point_range(monkeypatch, oracle, scale):
     y = scale * rng.standard_normal(M * Q)
     assert rel(op.adjoint(y).double().cpu().numpy(), o.adjoint(y)) <= 2e-4
     pk.clear_plan_cache()
+
+
+@pytest.mark.parametrize("variant", ["nonneg", "tolerance", "divergence"])
+def test_symmetric_kernels_solver_variants(monkeypatch, oracle, variant):
+    """Symmetric back-projector + projector (forced on) through the stopping rules and the
+    non-negativity clamp, on a ring whose sensor count is not a multiple of 32 (a partial
+    sensor group) and a grid whose quadrant is not a multiple of the tiles."""
+    n, M, Q = 96, 36, 512
+    g, ring, ac, ph = pk.make_scene(n, M, Q, seed=5)
+    K = pk.build_time_matrix(g, ring, ac)
+    o = oracle.Operator.of(oracle.make_scene(n, M, Q, 5))
+    y = o.forward(ph.values)
+    alpha, beta = oracle.resolve_regularization(o, y)
+    step = oracle.resolve_step(o, beta, 1e-3)
+    kw = {"nonneg": dict(iterations=10, nonneg=True),
+          "tolerance": dict(iterations=40, tolerance=0.2),
+          "divergence": dict(iterations=50)}[variant]
+    st = 1e9 if variant == "divergence" else step
+    ref = oracle.reconstruct(o, y, alpha, beta, st, **kw)
+    op = _plan(monkeypatch, g, ring, ac, "1", "1")
+    assert op.info.symmetric == 3
+    res = pk.iterative_reconstruct(K, pk.SensorData("time", M, Q, y),
+                                   pk.ReconConfig(alpha, beta, step=st, **kw), pool=F32)
+    assert res.iterations_run == ref["iterations_run"]
+    assert res.stopped_by == ref["stopped_by"]
+    if variant != "divergence":
+        assert rel(res.image.values, ref["image"]) <= 1e-4
+    pk.clear_plan_cache()
+
+
+def test_symmetric_kernels_truncated_window(monkeypatch, oracle):
+    """Delays beyond the acquisition window (TruncationWarning scenes): the clamped paths
+    of both symmetric kernels against the oracle's dropped weights."""
+    import warnings
+
+    n, M = 64, 32
+    s = oracle.make_scene(n, M, 128, 0)
+    Q = 100  # shorter than the farthest delay (~122 samples at 128)
+    g, ring, ac, ph = pk.make_scene(n, M, 128, seed=0)
+    ac = pk.AcousticConfig(c=ac.c, dt=ac.dt, q_s=Q, q_n=Q)
+    o = oracle.Operator(s.xx, s.yy, s.pos, s.c, s.dt, Q)
+    assert o.truncated_pairs() > 0
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        op = _plan(monkeypatch, g, ring, ac, "1", "1")
+    assert op.info.symmetric & 1
+    rng = np.random.default_rng(8)
+    x = ph.values + 0.05 * rng.random(g.size)
+    assert rel(op.matvec(x).double().cpu().numpy(), o.forward(x)) <= 5e-5
+    r = rng.standard_normal(M * Q)
+    assert rel(op.adjoint(r).double().cpu().numpy(), o.adjoint(r)) <= 2e-4
+    pk.clear_plan_cache()
