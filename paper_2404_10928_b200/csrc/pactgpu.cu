@@ -131,6 +131,33 @@ void free_plan(pk_plan* p) {
 
 size_t tsize(const pk_plan* p) { return p->dtype == PK_F32 ? 4 : 8; }
 
+// Programmatic dependent launch (PK_PDL=0 disables): the kernel may be scheduled while its
+// predecessor on the stream drains and waits (griddep_wait) before reading its output.
+// Only kernels that contain that wait are launched this way.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("PK_PDL");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // every (kernel, NF) instantiation the dispatch below can launch
 template <int NF>
 void smem_kernels(std::vector<const void*>& v) {
@@ -153,7 +180,7 @@ constexpr int kSymWDiag = 5, kSymWOff = 8;
 
 template <int IW>
 void launch_sym(const BpSymArgs& A, int grid, int smem, cudaStream_t s) {
-    bp_sym_f32_kernel<IW><<<grid, kSymThreads, smem, s>>>(A);
+    launch_pdl(bp_sym_f32_kernel<IW>, dim3(grid), dim3(kSymThreads), smem, s, A);
 }
 
 const void* sym_kernel_ptr(int iw) {
@@ -225,8 +252,8 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
         a.counts = p->fsym_counts;
         const int units = p->fsym_qt * p->fsym_qt * p->fsym_groups;
         const bool clamp = p->max_delay >= (double)p->Q + 0.5;
-#define PK_FS(LW) (clamp ? fp_sym_f32_kernel<LW, true><<<units, kFsThreads, p->fsym_smem, s>>>(a) \
-                         : fp_sym_f32_kernel<LW, false><<<units, kFsThreads, p->fsym_smem, s>>>(a))
+#define PK_FS(LW) (clamp ? launch_pdl(fp_sym_f32_kernel<LW, true>, dim3(units), dim3(kFsThreads), p->fsym_smem, s, a) \
+                         : launch_pdl(fp_sym_f32_kernel<LW, false>, dim3(units), dim3(kFsThreads), p->fsym_smem, s, a))
         switch (p->fsym_L) {
             case 96: PK_FS(96); break;
             case 128: PK_FS(128); break;
@@ -289,7 +316,7 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
         }
         a.atrick = p->bp_atrick;
         a.chunks = chunks;
-        finalize_kernel<float, NF><<<grid, kThreads, sm, s>>>(a);
+        launch_pdl(finalize_kernel<float, NF>, grid, dim3(kThreads), sm, s, a);
     } else {
         FinArgs<double> a{};
         a.acc = p->acc; a.y = static_cast<const double*>(y);
@@ -333,8 +360,8 @@ void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_
         E.xb0 = static_cast<float*>(p->xbuf[0]);
         E.xb1 = static_cast<float*>(p->xbuf[1]);
         E.prm = p->params; E.st = p->state; E.part_bp = p->part_bp;
-        if (epi) bp_sym_epi_kernel<true><<<p->sym_ntiles * 8, kThreads, 0, s>>>(E);
-        else bp_sym_epi_kernel<false><<<p->sym_ntiles * 8, kThreads, 0, s>>>(E);
+        if (epi) launch_pdl(bp_sym_epi_kernel<true>, dim3(p->sym_ntiles * 8), dim3(kThreads), 0, s, E);
+        else launch_pdl(bp_sym_epi_kernel<false>, dim3(p->sym_ntiles * 8), dim3(kThreads), 0, s, E);
         return;
     }
     if (p->dtype == PK_F32) {

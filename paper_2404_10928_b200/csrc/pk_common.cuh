@@ -142,6 +142,14 @@ __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// programmatic dependent launch: a kernel launched with programmatic stream serialization
+// may start while its predecessor drains; it must wait before touching the predecessor's
+// output.  Both are no-ops for kernels launched without the attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------
 // deterministic block reductions (fixed shuffle tree + fixed warp order)
 template <typename T>

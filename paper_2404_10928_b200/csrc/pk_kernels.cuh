@@ -451,6 +451,7 @@ __device__ __forceinline__ void sym_chunk(float (&acc)[4][8], const float (&px)[
 template <int IW>
 __global__ void __launch_bounds__(kSymThreads, 3) bp_sym_f32_kernel(BpSymArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
+    griddep_wait();  // the pair table and the stop flag come from the residual kernel
     if (a.st && a.st->all_stopped) return;
     const int c0 = a.cta_chunk0[blockIdx.x], c1 = a.cta_chunk0[blockIdx.x + 1];
     if (c0 >= c1) return;
@@ -562,6 +563,7 @@ __global__ void __launch_bounds__(kSymThreads, 3) bp_sym_f32_kernel(BpSymArgs a)
         if (lane == 0) mbar_arrive(empty_s + 8 * b);
         if (++b == a.nbuf) { b = 0; phase ^= 1u; }
     }
+    griddep_launch_dependents();
     flush();
 }
 
@@ -612,6 +614,7 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
     // 1) the tile's slots in order, coalesced: thread owns elements 4*tid .. 4*tid+3 of the
     //    slot vector [k][consumer thread], every slot is one 16-B load
     const int k = threadIdx.x >> 6, ct = (threadIdx.x & 63) * 4;
+    griddep_wait();  // partial slots of the main kernel
     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
     if (active) {
         const float4* src = reinterpret_cast<const float4*>(a.part + (size_t)g * 4 * kThreads) + threadIdx.x;
@@ -682,6 +685,7 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
             l1 += fabsf(xn);
         }
     }
+    griddep_launch_dependents();
     mx = block_max(mx, red_f);
     const float l1b = block_sum(l1, red_f);
     const int badb = __syncthreads_or(bad);
@@ -1171,7 +1175,6 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
         iter = a.st->iter;
     }
     const float* x = a.x ? a.x : ((iter & 1) ? a.xb0 : a.xb1);  // bp wrote xb[(iter+1)&1]
-    const float scale = a.st->fr[0].scale32;
     const int n = a.n, h = n >> 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int WW = 4 * LW * 32;  // window words
@@ -1202,6 +1205,8 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
             for (int g = 0; g < 4; ++g) w4[g * LW * 8 + q] = c;
         }
     }
+    griddep_wait();  // x' and its fixed-point scale come from the back-projector epilogue
+    const float scale = a.st->fr[0].scale32;
     __syncthreads();
 
     if (lane < kFsBatch) rec[32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1284,6 +1289,7 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
         }
         __syncwarp();  // rec is rewritten by the next piece
     }
+    griddep_launch_dependents();
     __syncthreads();
 
     // store: a warp takes blocks of 8 slots of one image; 8 row reads (lane = sensor,
@@ -1476,6 +1482,7 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
     __shared__ double data_s[NF], tv_s[NF];
     __shared__ int last_flag;
     if (a.solver && a.st->all_stopped) return;
+    griddep_wait();  // the projection's accumulator / windows and scale
     // grid (M * chunks, NF): CTA handles samples [c0, c1) of sensor m plus the one-sample
     // halo r[c0-1] its first pair-table entry needs.  The accumulator is read-only here (it
     // is cleared by a memset before the next projection), so neighbouring chunks do not race.
@@ -1574,6 +1581,7 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
         const T rc = (e < a.Q) ? tr[e - c0 + 1] : (T)0;
         a.table[((size_t)m * a.TS + e) * NF + f] = pair_entry<T>(rp, rc, e, a.atrick);
     }
+    griddep_launch_dependents();
     ss = block_sum(ss, red_d);
     if (threadIdx.x == 0) a.part_r[(size_t)f * a.M * chunks + blockIdx.x] = ss;
     if (!last_block(&a.st->cnt_fin, gridDim.x * gridDim.y, &last_flag)) return;
