@@ -362,12 +362,31 @@ def main():
                     ["bp_f32", "fp_f32"][dom])
             except Exception:
                 traffic = None
+        # HBM view of the same kernel: its DRAM traffic (ncu, per launch) over its duration,
+        # against the measured copy bandwidth -- shows the kernel is nowhere near HBM-bound
+        hbm_peak, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
+        mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        if os.path.exists(mp):
+            try:
+                hbm_peak, hbm_src = float(json.load(open(mp))["hbm_gbs"]), "MEASURED_PEAKS.json"
+            except Exception:
+                pass
+        t_dom = per_launch_ms[dom] * 1e-3
         roof = {"bound": "fp32", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                 "frac": achieved / peak.value, "traffic": traffic,
                 "kernel": names[dom],
                 "peak_source": "measured live: FFMA microkernel (pk_measure_fp32_peak); "
                                "MEASURED_PEAKS.json has no FP32 figure",
-                "work": f"12 flops x {M} sensors x {P} pixels per launch"}
+                "work": f"12 flops x {M} sensors x {P} pixels per launch",
+                "why_fp32": "north_star: FP32 pipe utilisation against B200 peaks; the matrix-free "
+                            "operator has ~200 flop/B of compulsory traffic (SURVEY.md 8(d))",
+                "binding_resource": "shared-memory pipe: 2 int32 ATOMS per sensor-pixel pair in the "
+                                    "projector (floor 2 clk / 32 pairs), LDS.64 per pair in the "
+                                    "back-projector (2 wavefronts / 32 pairs)",
+                "smem_floor_us": 2.0 * M * P / 32.0 / (148 * 1.965e3),
+                "hbm": {"achieved_GBs": (traffic / t_dom / 1e9) if traffic else None,
+                        "peak_GBs": hbm_peak, "peak_source": hbm_src,
+                        "frac": (traffic / t_dom / 1e9 / hbm_peak) if traffic else None}}
 
     # ---- end to end through the C-ABI host-buffer entry ----
     e2e = None
