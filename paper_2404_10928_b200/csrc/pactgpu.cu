@@ -1193,17 +1193,37 @@ int pk_freq_adjoint(pk_plan* p, int32_t q_n, const void* y, void* out, double sc
     const size_t sm = (size_t)q_n * 2 * tsize(p);
     if (sm > 200 * 1024) return fail(PK_ERR_UNSUPPORTED, "q_n = %d too large for the adjoint", q_n);
     cudaStream_t s = S(stream);
-    const int grid = (p->P + kThreads - 1) / kThreads;
+    const int blocks = (p->P + kThreads - 1) / kThreads;
+    // sensor chunks so that the grid covers ~4 CTAs per SM; partials summed in chunk order
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+    const int chunks = std::max(1, std::min(p->M, (4 * sms + blocks - 1) / blocks));
+    a.chunks = chunks;
+    if (chunks > 1) {
+        const size_t need = (size_t)chunks * p->P * 2 * tsize(p);
+        if (need > p->freq_part_bytes) {
+            if (p->freq_part) cudaFree(p->freq_part);
+            p->freq_part = nullptr;
+            p->freq_part_bytes = 0;
+            PK_CUDA(cudaMalloc(&p->freq_part, need));
+            p->freq_part_bytes = need;
+        }
+        a.part = p->freq_part;
+    }
+    const dim3 grid(blocks, chunks);
+    const int sb = std::min(148 * 8, blocks);
     if (p->dtype == PK_F32) {
         if (sm > 48 * 1024)
             PK_CUDA(cudaFuncSetAttribute((const void*)freq_adj_kernel<float>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         freq_adj_kernel<float><<<grid, kThreads, sm, s>>>(a);
+        if (chunks > 1) freq_adj_sum_kernel<float><<<sb, kThreads, 0, s>>>(a);
     } else {
         if (sm > 48 * 1024)
             PK_CUDA(cudaFuncSetAttribute((const void*)freq_adj_kernel<double>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         freq_adj_kernel<double><<<grid, kThreads, sm, s>>>(a);
+        if (chunks > 1) freq_adj_sum_kernel<double><<<sb, kThreads, 0, s>>>(a);
     }
     PK_CHECK_LAUNCH();
     return PK_OK;

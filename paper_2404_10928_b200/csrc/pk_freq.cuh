@@ -126,8 +126,10 @@ __global__ void __launch_bounds__(kThreads) freq_fwd_sum_kernel(FreqArgs a) {
     }
 }
 
-// adjoint: thread = pixel; per sensor, block-Horner over n with exact phase anchors every
-// kFreqAdjRun wavenumbers.  b_n = -i c k_n y[m, n] * scale staged in shared memory.
+// adjoint: thread = pixel, CTA = (pixel block, sensor chunk); per sensor, block-Horner over n
+// with exact phase anchors every kFreqAdjRun wavenumbers.  b_n = -i c k_n y[m, n] * scale is
+// staged in shared memory.  Per-chunk partials [chunk][P] are added in chunk order by
+// freq_adj_sum_kernel (deterministic); with one chunk the kernel writes the result directly.
 template <typename T>
 __global__ void __launch_bounds__(kThreads) freq_adj_kernel(FreqArgs a) {
     using C = typename Cplx<T>::type;
@@ -136,9 +138,11 @@ __global__ void __launch_bounds__(kThreads) freq_adj_kernel(FreqArgs a) {
     const int p = blockIdx.x * kThreads + threadIdx.x;
     const bool valid = p < a.P;
     const double pxv = valid ? a.px[p % a.nx] : 0.0, pyv = valid ? a.py[p / a.nx] : 0.0;
+    const int m0 = (int)((long long)a.M * blockIdx.y / gridDim.y);
+    const int m1 = (int)((long long)a.M * (blockIdx.y + 1) / gridDim.y);
     const C* y = static_cast<const C*>(a.y);
     T gr = 0, gi = 0;
-    for (int m = 0; m < a.M; ++m) {
+    for (int m = m0; m < m1; ++m) {
         __syncthreads();
         for (int n = threadIdx.x; n < a.qn; n += kThreads) {
             const C v = y[(size_t)m * a.qn + n];
@@ -174,7 +178,24 @@ __global__ void __launch_bounds__(kThreads) freq_adj_kernel(FreqArgs a) {
         gr += sr * inv;
         gi += si * inv;
     }
-    if (valid) static_cast<C*>(a.out)[p] = C{gr, gi};
+    if (!valid) return;
+    if (gridDim.y == 1) static_cast<C*>(a.out)[p] = C{gr, gi};
+    else static_cast<C*>(a.part)[(size_t)blockIdx.y * a.P + p] = C{gr, gi};
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) freq_adj_sum_kernel(FreqArgs a) {
+    using C = typename Cplx<T>::type;
+    const C* part = static_cast<const C*>(a.part);
+    for (int p = blockIdx.x * kThreads + threadIdx.x; p < a.P; p += gridDim.x * kThreads) {
+        T sr = 0, si = 0;
+        for (int c = 0; c < a.chunks; ++c) {
+            const C v = part[(size_t)c * a.P + p];
+            sr += v.x;
+            si += v.y;
+        }
+        static_cast<C*>(a.out)[p] = C{sr, si};
+    }
 }
 
 }  // namespace pk
