@@ -1260,32 +1260,37 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
             // column k of the piece: x = pxs[c0] + k*hx (samples)
             const float pxbs = __ldg(a.pxs + i0 + 32 * (pc % P2)) - sx;
             const int kend = min(32, n - (i0 + 32 * (pc % P2)));
-            for (int k = 0; k < kend; k += kFsBatch) {
-                uint32_t ad[kFsBatch];
-                int32_t va[kFsBatch][4], vb[kFsBatch][4];
+            auto scatter = [&](auto checked) {
+                constexpr bool CHECK = decltype(checked)::value;
+                for (int k = 0; k < kend; k += kFsBatch) {
+                    uint32_t ad[kFsBatch];
+                    int32_t va[kFsBatch][4], vb[kFsBatch][4];
 #pragma unroll
-                for (int b = 0; b < kFsBatch; ++b) {
-                    const float4 r0 = rec[k + b];
-                    float fr;
-                    const float tb = fs_delay<CLAMP>((float)(k + b), a.hx, pxbs, ey2, a.qclamp, fr);
-                    const float xs[4] = {r0.x, r0.y, r0.z, r0.w};
-#pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                        const float fb = fmaf(xs[g], fr, kMagic);
-                        va[b][g] = __float_as_int(fb);                                   // f -> s0 (+bias)
-                        vb[b][g] = __float_as_int(xs[g] + kMagic) - __float_as_int(fb);  // 1-f -> s0-1
-                    }
-                    ad[b] = adj + (__float_as_uint(tb) << 7);
-                }
-#pragma unroll
-                for (int b = 0; b < kFsBatch; ++b)
-                    if (k + b < kend)  // padding columns beyond the grid add nothing
+                    for (int b = 0; b < kFsBatch; ++b) {
+                        const float4 r0 = rec[k + b];
+                        float fr;
+                        const float tb = fs_delay<CLAMP>((float)(k + b), a.hx, pxbs, ey2, a.qclamp, fr);
+                        const float xs[4] = {r0.x, r0.y, r0.z, r0.w};
 #pragma unroll
                         for (int g = 0; g < 4; ++g) {
-                            red_smem_s32(ad[b] + (uint32_t)(g * LW * 128) - 128u, vb[b][g]);
-                            red_smem_s32(ad[b] + (uint32_t)(g * LW * 128), va[b][g]);
+                            const float fb = fmaf(xs[g], fr, kMagic);
+                            va[b][g] = __float_as_int(fb);                                   // f -> s0 (+bias)
+                            vb[b][g] = __float_as_int(xs[g] + kMagic) - __float_as_int(fb);  // 1-f -> s0-1
                         }
-            }
+                        ad[b] = adj + (__float_as_uint(tb) << 7);
+                    }
+#pragma unroll
+                    for (int b = 0; b < kFsBatch; ++b)
+                        if (!CHECK || k + b < kend)  // padding columns beyond the grid add nothing
+#pragma unroll
+                            for (int g = 0; g < 4; ++g) {
+                                red_smem_s32(ad[b] + (uint32_t)(g * LW * 128) - 128u, vb[b][g]);
+                                red_smem_s32(ad[b] + (uint32_t)(g * LW * 128), va[b][g]);
+                            }
+                }
+            };
+            if (kend == 32) scatter(std::false_type{});  // whole piece: no per-column checks
+            else scatter(std::true_type{});
         }
         __syncwarp();  // rec is rewritten by the next piece
     }
