@@ -250,6 +250,7 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
         a.hx = p->fsym_hx;
         a.st = p->state; a.part_tv = p->part_tv; a.solver = solver;
         a.counts = p->fsym_counts;
+        a.xr = reinterpret_cast<const float4*>(p->fsym_xr);
         const int units = p->fsym_qt * p->fsym_qt * p->fsym_groups;
         const bool clamp = p->max_delay >= (double)p->Q + 0.5;
 #define PK_FS(LW) (clamp ? launch_pdl(fp_sym_f32_kernel<LW, true>, dim3(units), dim3(kFsThreads), p->fsym_smem, s, a) \
@@ -360,6 +361,7 @@ void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_
         E.xb0 = static_cast<float*>(p->xbuf[0]);
         E.xb1 = static_cast<float*>(p->xbuf[1]);
         E.prm = p->params; E.st = p->state; E.part_bp = p->part_bp;
+        E.xr = p->fsym ? p->fsym_xr : nullptr;
         if (epi) launch_pdl(bp_sym_epi_kernel<true>, dim3(p->sym_ntiles * 8), dim3(kThreads), 0, s, E);
         else launch_pdl(bp_sym_epi_kernel<false>, dim3(p->sym_ntiles * 8), dim3(kThreads), 0, s, E);
         return;
@@ -880,6 +882,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         A(alloc(p, &p->fsym_lo, (size_t)fsym_units * 32));
         A(alloc(p, &p->fsym_counts, (size_t)fsym_units * 32 * p->fsym_L));
         A(alloc(p, &p->fsym_list, (size_t)p->M * 4 * p->fsym_qt * p->fsym_qt));
+        A(alloc(p, &p->fsym_xr, (size_t)(p->nx / 2) * (p->nx / 2) * 4));
     }
     // one CTA per sensor: more, shorter CTAs only add latency (measured 10.3 / 12.8 / 18.2 us
     // for 1 / 2 / 4 chunks at config 3)

@@ -289,6 +289,7 @@ struct pk_plan {
     // rotation-symmetric projector (fp_sym_f32_kernel)
     int fsym = 0, fsym_T = 0, fsym_qt = 0, fsym_L = 0, fsym_smem = 0, fsym_groups = 0;
     float fsym_hx = 0.f;  // pixel pitch in samples
+    float* fsym_xr = nullptr;     // [(n/2)^2][4] x' rotation-packed by the epilogue
     int32_t* fsym_win = nullptr;  // [units][4][32][L] window sums of the last projection
     int32_t* fsym_lo = nullptr;   // [units][32] first trace index of each window
     int32_t* fsym_counts = nullptr;  // [units][L][32] pixels per window slot (bias of the adds)

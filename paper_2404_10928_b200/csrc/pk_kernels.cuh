@@ -582,7 +582,25 @@ struct BpSymEpiArgs {
     const DevParams* prm;
     DevState* st;
     double* part_bp;          // [grid][4]
+    float* xr;                // EPI == true, optional: rotation-packed copy of x' for the
+                              // symmetric projector, [(n/2)^2][4] (fp_sym_f32_kernel)
 };
+
+// rotation-packed index of pixel (i, j): the quadrant representative q = (qi, qj) in
+// [h, n)^2 and rotation r with rot^r(q) = (i, j) (the image order of fp_sym_f32_kernel);
+// returns 4 * ((qj - h) * h + (qi - h)) + r
+__device__ __forceinline__ int sym_rot_index(int i, int j, int n) {
+    const int h = n >> 1;
+    int qi, qj, r;
+    if (i >= h) {
+        if (j >= h) { qi = i; qj = j; r = 0; }
+        else { qi = n - 1 - j; qj = i; r = 3; }
+    } else {
+        if (j >= h) { qi = j; qj = n - 1 - i; r = 1; }
+        else { qi = n - 1 - i; qj = n - 1 - j; r = 2; }
+    }
+    return 4 * ((qj - h) * h + (qi - h)) + r;
+}
 
 template <bool EPI>
 __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
@@ -680,6 +698,7 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
             if (beta > 0.f) gr += beta * tv_grad_at<float>(x, p, p % n, p / n, n, n, eps * eps);
             const float xn = prox<float>(x[p] - eta * gr, lam, nonneg);
             xo[p] = xn;
+            if (a.xr) a.xr[sym_rot_index(p % n, p / n, n)] = xn;
             if (!isfinite(xn)) bad = 1;
             mx = fmaxf(mx, fabsf(xn));
             l1 += fabsf(xn);
@@ -1090,6 +1109,7 @@ struct FpSymArgs {
     DevState* st;
     double* part_tv;         // solver mode: per-unit TV(x) partial (group-0 units, else 0)
     int solver;
+    const float4* xr;        // solver mode, optional: x' rotation-packed by the epilogue
 };
 
 // first trace index of the window of the 64x64 quadrant tile at (i0, j0) for sensor (sx, sy)
@@ -1175,6 +1195,7 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
         iter = a.st->iter;
     }
     const float* x = a.x ? a.x : ((iter & 1) ? a.xb0 : a.xb1);  // bp wrote xb[(iter+1)&1]
+    const float4* xr = a.x ? nullptr : a.xr;
     const int n = a.n, h = n >> 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int WW = 4 * LW * 32;  // window words
@@ -1221,7 +1242,10 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
         const int ii = i0 + 32 * (pc % P2) + lane;
 #pragma unroll
         for (int g = 0; g < 4; ++g) v[g] = 0.f;
-        if (jj < jend && ii < n) {
+        if (jj < jend && ii < n && xr) {  // one coalesced 16-B load for the 4 images
+            const float4 q = xr[(jj - h) * h + (ii - h)];
+            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        } else if (jj < jend && ii < n) {
             v[0] = x[jj * n + ii];
             v[1] = x[ii * n + (n - 1 - jj)];
             v[2] = x[(n - 1 - jj) * n + (n - 1 - ii)];
