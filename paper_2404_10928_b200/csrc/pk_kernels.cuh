@@ -1147,10 +1147,10 @@ __device__ __forceinline__ float fs_delay(float k, float hx, float pxbs, float e
     return tb;
 }
 
-// plan setup: for every (unit, window slot, lane) the number of tile pixels whose delay to
-// the lane's base sensor has s0 = lo + slot.  The projector adds bits(fb) = a + bias (the
-// 1.5*2^23 magic) at s0 and pre-loads each window slot with -count * bias, saving one integer
-// subtract per pair.
+// plan setup: for every (unit, window slot, lane) the number of biased words the projector
+// adds to the slot (pixels of the tile whose delay to the lane's base sensor has s0 = lo + slot
+// or lo + slot + 1).  The projector adds bits(fma(xs, f, 1.5*2^23)) = round(xs*f) + bias and
+// pre-loads each window slot with -count * bias, saving the integer conversions per pair.
 template <bool CLAMP>
 __global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* pxs, const float* pys,
                                                                   const float* sxs, const float* sys,
@@ -1182,7 +1182,10 @@ __global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* p
         }
     }
     __syncthreads();
-    for (int q = threadIdx.x; q < LW * 32; q += kFsThreads) counts[(size_t)u * LW * 32 + q] = cnt[q];
+    // slot k receives the f part of pixels with s0 = lo + k and the 1-f part of those with
+    // s0 = lo + k + 1, each word biased by kMagicBits
+    for (int q = threadIdx.x; q < LW * 32; q += kFsThreads)
+        counts[(size_t)u * LW * 32 + q] = cnt[q] + (q + 32 < LW * 32 ? cnt[q + 32] : 0);
 }
 
 template <int LW, bool CLAMP>
@@ -1286,7 +1289,9 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
             const int kend = min(32, n - (i0 + 32 * (pc % P2)));
             auto scatter = [&](auto checked) {
                 constexpr bool CHECK = decltype(checked)::value;
-                for (int k = 0; k < kend; k += kFsBatch) {
+                const int kn = CHECK ? kend : 32;
+#pragma unroll 2
+                for (int k = 0; k < kn; k += kFsBatch) {
                     uint32_t ad[kFsBatch];
                     int32_t va[kFsBatch][4], vb[kFsBatch][4];
 #pragma unroll
@@ -1295,11 +1300,14 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
                         float fr;
                         const float tb = fs_delay<CLAMP>((float)(k + b), a.hx, pxbs, ey2, a.qclamp, fr);
                         const float xs[4] = {r0.x, r0.y, r0.z, r0.w};
+                        const float omf = 1.f - fr;
+                        // both halves rounded independently (the pair's mass is kept to one
+                        // fixed-point unit); each word carries the magic bias, which the
+                        // window pre-load removes (fp_sym_count_kernel)
 #pragma unroll
                         for (int g = 0; g < 4; ++g) {
-                            const float fb = fmaf(xs[g], fr, kMagic);
-                            va[b][g] = __float_as_int(fb);                                   // f -> s0 (+bias)
-                            vb[b][g] = __float_as_int(xs[g] + kMagic) - __float_as_int(fb);  // 1-f -> s0-1
+                            va[b][g] = __float_as_int(fmaf(xs[g], fr, kMagic));   // f -> s0
+                            vb[b][g] = __float_as_int(fmaf(xs[g], omf, kMagic));  // 1-f -> s0-1
                         }
                         ad[b] = adj + (__float_as_uint(tb) << 7);
                     }
