@@ -154,6 +154,37 @@ int pk_residual(pk_plan* plan, const void* x_dev, const void* y_dev, void* r_out
 /* out_dev = scale * K_shard^T r for the residual kept by the last pk_residual. */
 int pk_adjoint_residual(pk_plan* plan, void* out_dev, double scale, void* stream);
 
+/* Peer-memory exchange for sensor-sharded solves: one process (or plan) per GPU
+ * of one node with peer access over NVLink / NVSwitch.  Replaces the all-reduce of the
+ * image-sized gradient between pk_adjoint_residual and pk_grad_update (the NCCL
+ * dist.all_reduce of the gradient in sharded.SensorShardedSolver) with peer loads fused into
+ * the update: every rank reads all ranks' partial gradients in rank order, so x stays bit
+ * identical across ranks.
+ *   pk_peer_handle   allocates the plan's peer-visible block (flags + two gradient slots)
+ *                    and writes its 64-byte handle (cudaIpcMemHandle_t) to handle_out.
+ *   pk_peer_connect  maps the world's blocks (handles[world][64], rank order; handles of
+ *                    plans in this process are resolved without IPC).  All ranks must have
+ *                    connected before any rank's first pk_peer_grad_update (a host barrier).
+ *                    Plans of one process that share a device must each have run every
+ *                    kernel of their solve once before any of them waits in a barrier: a
+ *                    first (lazily loaded) launch waits for the device to drain.
+ *   pk_peer_buffer   device pointer of this rank's gradient slot (0 or 1): the `out_dev` of
+ *                    pk_adjoint_residual.
+ *   pk_peer_grad_update  device barrier of the world (every rank calls it equally often;
+ *                    a device-side epoch makes it graph-capturable), then
+ *                    grad = sum_r slot buffer of rank r, and the update of pk_grad_update.
+ *                    Alternate the slot per iteration (a rank may run one barrier ahead).
+ * A barrier that waits longer than PK_PEER_TIMEOUT_S seconds (default 60; a dead rank) gives
+ * up: the update writes NaN, and pk_peer_status reports timed_out = 1 (synchronous query). */
+#define PK_PEER_MAX 8
+#define PK_PEER_HANDLE_BYTES 64
+int pk_peer_handle(pk_plan* plan, void* handle_out);
+int pk_peer_connect(pk_plan* plan, int32_t world, int32_t rank, const void* handles);
+int pk_peer_buffer(pk_plan* plan, int32_t slot, void** ptr_out);
+int pk_peer_grad_update(pk_plan* plan, const pk_solver_params* params, const void* x_dev,
+                        int32_t slot, void* x_out_dev, double* sums_dev, void* stream);
+int pk_peer_status(pk_plan* plan, int32_t* timed_out);
+
 /* Frequency-domain operator of build_freq_matrix (forward.py:218-234), matrix-free:
  *   K_f[m*q_n + (n-1), p] = i c k_n exp(-i k_n d_mp) / d_mp,  k_n = 2 pi n / (samples dt c).
  * Complex buffers are interleaved (re, im) in the plan dtype (complex64 / complex128).

@@ -30,6 +30,8 @@ PK_ERR_UNSUPPORTED = -3
 PK_ERR_GEOMETRY = -4
 PK_F32 = 0
 PK_F64 = 1
+PK_PEER_MAX = 8
+PK_PEER_HANDLE_BYTES = 64
 STOPPED_BY = {0: "max_iterations", 1: "tolerance", 2: "divergence"}
 
 
@@ -116,6 +118,12 @@ SYMBOLS = [
     ("pk_residual", ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     ("pk_adjoint_residual", ctypes.c_int, [_vp, _vp, ctypes.c_double, _vp]),
     ("pk_index_dump", ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp]),
+    ("pk_peer_handle", ctypes.c_int, [_vp, ctypes.c_char_p]),
+    ("pk_peer_connect", ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_char_p]),
+    ("pk_peer_buffer", ctypes.c_int, [_vp, ctypes.c_int32, ctypes.POINTER(_vp)]),
+    ("pk_peer_grad_update", ctypes.c_int,
+     [_vp, ctypes.POINTER(SolverParams), _vp, ctypes.c_int32, _vp, _vp, _vp]),
+    ("pk_peer_status", ctypes.c_int, [_vp, _ip]),
     ("pk_freq_matvec", ctypes.c_int, [_vp, ctypes.c_int32, _vp, _vp, _vp]),
     ("pk_freq_adjoint", ctypes.c_int, [_vp, ctypes.c_int32, _vp, _vp, ctypes.c_double, _vp]),
     ("pk_profile_iterations", ctypes.c_int,

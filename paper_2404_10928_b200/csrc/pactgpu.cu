@@ -12,6 +12,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -111,6 +114,32 @@ int alloc(pk_plan* p, T** ptr, size_t count) {
     return PK_OK;
 }
 
+// peer blocks exported by plans of this process, by handle bytes: a handle cannot be opened
+// by the process that exported it, so same-process peers are resolved here
+std::mutex g_peer_mu;
+std::map<std::string, unsigned char*> g_peer_registry;
+
+void peer_registry_drop(unsigned char* block) {
+    std::lock_guard<std::mutex> lk(g_peer_mu);
+    for (auto it = g_peer_registry.begin(); it != g_peer_registry.end();)
+        it = it->second == block ? g_peer_registry.erase(it) : std::next(it);
+}
+
+constexpr size_t kPeerHeader = 256;  // int flags[PK_PEER_MAX], int epoch, int timed_out, padding
+
+// barrier wait bound (PK_PEER_TIMEOUT_S, default 60 s)
+long long peer_timeout_ns() {
+    static const long long ns = [] {
+        const char* e = getenv("PK_PEER_TIMEOUT_S");
+        const double sec = e ? atof(e) : 60.0;
+        return (long long)((sec > 0 ? sec : 60.0) * 1e9);
+    }();
+    return ns;
+}
+size_t peer_slot_bytes(const pk_plan* p) {
+    return ((size_t)p->P * (p->dtype == PK_F32 ? 4 : 8) + 255) & ~(size_t)255;
+}
+
 void free_plan(pk_plan* p) {
     if (!p) return;
     DeviceGuard g(p->device);
@@ -125,6 +154,13 @@ void free_plan(pk_plan* p) {
                     p->freq_part};
     for (void* q : ptrs)
         if (q) cudaFree(q);
+    for (void* q : p->peer_opened) cudaIpcCloseMemHandle(q);
+    if (p->peer_block) {
+        peer_registry_drop(p->peer_block);
+        cudaFree(p->peer_block);
+    }
+    if (p->peer_grad_dev) cudaFree(p->peer_grad_dev);
+    if (p->peer_flags_dev) cudaFree(p->peer_flags_dev);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     delete p;
 }
@@ -1054,6 +1090,123 @@ int pk_grad_update(pk_plan* p, const pk_solver_params* prm, const void* x, const
                                                            static_cast<const double*>(grad),
                                                            static_cast<double*>(x_out), p->nx,
                                                            p->ny, p->params);
+        image_sums_kernel<double><<<p->misc_blocks, kThreads, 0, s>>>(
+            static_cast<const double*>(x_out), p->nx, p->ny, p->part_misc, p->state, sums);
+    }
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+int pk_peer_handle(pk_plan* p, void* handle_out) {
+    if (!p || !handle_out) return fail(PK_ERR_INVALID, "NULL argument");
+    if (p->nf != 1) return fail(PK_ERR_UNSUPPORTED, "peer exchange is single-frame");
+    DeviceGuard g(p->device);
+    if (!p->peer_block) {
+        PK_TRY(alloc(p, &p->peer_block, kPeerHeader + 2 * peer_slot_bytes(p)));
+        PK_CUDA(cudaMemset(p->peer_block, 0, kPeerHeader + 2 * peer_slot_bytes(p)));
+    }
+    cudaIpcMemHandle_t h;
+    PK_CUDA(cudaIpcGetMemHandle(&h, p->peer_block));
+    static_assert(sizeof(h) == PK_PEER_HANDLE_BYTES, "cudaIpcMemHandle_t size");
+    std::memcpy(handle_out, &h, sizeof(h));
+    std::lock_guard<std::mutex> lk(g_peer_mu);
+    g_peer_registry[std::string(reinterpret_cast<const char*>(&h), sizeof(h))] = p->peer_block;
+    return PK_OK;
+}
+
+int pk_peer_connect(pk_plan* p, int32_t world, int32_t rank, const void* handles) {
+    if (!p || !handles) return fail(PK_ERR_INVALID, "NULL argument");
+    if (world < 1 || world > PK_PEER_MAX || rank < 0 || rank >= world)
+        return fail(PK_ERR_INVALID, "world %d / rank %d outside 1..%d", world, rank, PK_PEER_MAX);
+    if (!p->peer_block) return fail(PK_ERR_INVALID, "pk_peer_handle must be called first");
+    if (p->peer_world) return fail(PK_ERR_INVALID, "plan is already connected");
+    DeviceGuard g(p->device);
+    std::vector<void*> grads(world);
+    std::vector<int*> flags(world);
+    for (int r = 0; r < world; ++r) {
+        const char* hb = static_cast<const char*>(handles) + (size_t)r * PK_PEER_HANDLE_BYTES;
+        unsigned char* base = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(g_peer_mu);
+            auto it = g_peer_registry.find(std::string(hb, PK_PEER_HANDLE_BYTES));
+            if (it != g_peer_registry.end()) base = it->second;
+        }
+        if (r == rank && base != p->peer_block)
+            return fail(PK_ERR_INVALID, "handles[%d] is not this plan's handle", rank);
+        if (!base) {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, hb, sizeof(h));
+            void* q = nullptr;
+            PK_CUDA(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+            p->peer_opened.push_back(q);
+            base = static_cast<unsigned char*>(q);
+        }
+        grads[r] = base + kPeerHeader;
+        flags[r] = reinterpret_cast<int*>(base);
+    }
+    // load the peer kernels now: under lazy module loading the first launch of a kernel
+    // waits for the device to drain, which never happens while another rank of this process
+    // spins in its barrier (the solve's other kernels are loaded by its warm-up call)
+    {
+        cudaFuncAttributes fa;
+        PK_CUDA(cudaFuncGetAttributes(&fa, peer_barrier_kernel));
+        PK_CUDA(cudaFuncGetAttributes(&fa, peer_grad_update_kernel<float>));
+        PK_CUDA(cudaFuncGetAttributes(&fa, peer_grad_update_kernel<double>));
+        PK_CUDA(cudaFuncGetAttributes(&fa, image_sums_kernel<float>));
+        PK_CUDA(cudaFuncGetAttributes(&fa, image_sums_kernel<double>));
+    }
+    PK_TRY(alloc(p, &p->peer_grad_dev, (size_t)world));
+    PK_TRY(alloc(p, &p->peer_flags_dev, (size_t)world));
+    PK_CUDA(cudaMemcpy(p->peer_grad_dev, grads.data(), world * sizeof(void*), cudaMemcpyHostToDevice));
+    PK_CUDA(cudaMemcpy(p->peer_flags_dev, flags.data(), world * sizeof(int*), cudaMemcpyHostToDevice));
+    p->peer_world = world;
+    p->peer_rank = rank;
+    return PK_OK;
+}
+
+int pk_peer_buffer(pk_plan* p, int32_t slot, void** ptr_out) {
+    if (!p || !ptr_out) return fail(PK_ERR_INVALID, "NULL argument");
+    if (!p->peer_block) return fail(PK_ERR_INVALID, "pk_peer_handle must be called first");
+    if (slot != 0 && slot != 1) return fail(PK_ERR_INVALID, "slot must be 0 or 1");
+    *ptr_out = p->peer_block + kPeerHeader + (size_t)slot * peer_slot_bytes(p);
+    return PK_OK;
+}
+
+int pk_peer_status(pk_plan* p, int32_t* timed_out) {
+    if (!p || !timed_out) return fail(PK_ERR_INVALID, "NULL argument");
+    if (!p->peer_block) return fail(PK_ERR_INVALID, "pk_peer_handle must be called first");
+    DeviceGuard g(p->device);
+    int v = 0;
+    PK_CUDA(cudaMemcpy(&v, reinterpret_cast<int*>(p->peer_block) + PK_PEER_MAX + 1, sizeof(int),
+                       cudaMemcpyDeviceToHost));
+    *timed_out = v;
+    return PK_OK;
+}
+
+int pk_peer_grad_update(pk_plan* p, const pk_solver_params* prm, const void* x, int32_t slot,
+                        void* x_out, double* sums, void* stream) {
+    if (!p || !x || !x_out || !sums) return fail(PK_ERR_INVALID, "NULL argument");
+    if (!p->peer_world) return fail(PK_ERR_INVALID, "plan is not connected (pk_peer_connect)");
+    if (slot != 0 && slot != 1) return fail(PK_ERR_INVALID, "slot must be 0 or 1");
+    PK_TRY(check_params(p, prm));
+    DeviceGuard g(p->device);
+    cudaStream_t s = S(stream);
+    PK_TRY(upload_params(p, prm, s));
+    int* epoch = reinterpret_cast<int*>(p->peer_block) + PK_PEER_MAX;
+    peer_barrier_kernel<<<1, 32, 0, s>>>(epoch, p->peer_flags_dev, p->peer_world, p->peer_rank,
+                                         peer_timeout_ns());
+    const int pb = (p->P + kThreads - 1) / kThreads;
+    const size_t off = (size_t)slot * peer_slot_bytes(p) / tsize(p);
+    if (p->dtype == PK_F32) {
+        peer_grad_update_kernel<float><<<pb, kThreads, 0, s>>>(
+            p->peer_grad_dev, off, p->peer_world, static_cast<const float*>(x),
+            static_cast<float*>(x_out), p->nx, p->ny, p->params, epoch + 1);
+        image_sums_kernel<float><<<p->misc_blocks, kThreads, 0, s>>>(
+            static_cast<const float*>(x_out), p->nx, p->ny, p->part_misc, p->state, sums);
+    } else {
+        peer_grad_update_kernel<double><<<pb, kThreads, 0, s>>>(
+            p->peer_grad_dev, off, p->peer_world, static_cast<const double*>(x),
+            static_cast<double*>(x_out), p->nx, p->ny, p->params, epoch + 1);
         image_sums_kernel<double><<<p->misc_blocks, kThreads, 0, s>>>(
             static_cast<const double*>(x_out), p->nx, p->ny, p->part_misc, p->state, sums);
     }

@@ -304,6 +304,14 @@ struct pk_plan {
     void* freq_part = nullptr;  // frequency-domain forward partials (grown on first use)
     size_t freq_part_bytes = 0;
 
+    // peer exchange of the sensor-sharded gradient (pk_peer_*): the local block holds
+    // int flags[PK_PEER_MAX] (written by the peers), the barrier epoch, and T grad[2][P]
+    unsigned char* peer_block = nullptr;
+    int peer_world = 0, peer_rank = -1;
+    void** peer_grad_dev = nullptr;     // device [world]: grad[0] of every rank (local or mapped)
+    int** peer_flags_dev = nullptr;     // device [world]: flag array of every rank
+    std::vector<void*> peer_opened;     // IPC mappings to close on destroy
+
     // graph cache of pk_reconstruct
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;

@@ -1800,6 +1800,61 @@ __global__ void __launch_bounds__(kThreads) grad_update_kernel(const T* x, const
     xo[p] = prox<T>(x[p] - (T)prm->step[0] * g, (T)prm->eta_alpha[0], prm->nonneg != 0);
 }
 
+// Peer exchange (pk_peer_*).  Barrier of the world: the epoch of this rank is stored into
+// every rank's flag slot [rank] with system-scope release (cumulative over the partial
+// gradient written by the preceding kernel on this stream), then every peer's flag is awaited
+// with acquire.  One warp; launched as its own kernel so that a waiting rank holds one CTA.
+// A peer that has not arrived after timeout_ns (a dead rank) sets the timed-out word
+// (epoch[1]) instead of hanging the device; the update then writes NaN (pk_peer_status).
+__global__ void peer_barrier_kernel(int* epoch, int* const* flags, int world, int rank,
+                                    long long timeout_ns) {
+    const int t = threadIdx.x;
+    int e = 0;
+    if (t == 0) e = ++epoch[0];
+    e = __shfl_sync(0xffffffffu, e, 0);
+    if (t < world) {
+        int* dst = flags[t] + rank;
+        asm volatile("fence.acq_rel.sys;\n\tst.release.sys.global.s32 [%0], %1;" ::"l"(dst), "r"(e) : "memory");
+        const int* src = flags[rank] + t;
+        unsigned long long t0, now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        int v;
+        while (true) {
+            asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(src) : "memory");
+            if (v >= e) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if ((long long)(now - t0) > timeout_ns) {
+                atomicExch(epoch + 1, 1);
+                break;
+            }
+            __nanosleep(200);
+        }
+    }
+    __syncwarp();
+}
+
+// grad = sum over ranks (rank order) of slot `off` of every rank's block, fused with the
+// update of grad_update_kernel.  Peer data is read with ld.global.cv (no stale L1/L2 lines).
+template <typename T>
+__global__ void __launch_bounds__(kThreads) peer_grad_update_kernel(void* const* grads, size_t off,
+                                                                    int world, const T* x, T* xo,
+                                                                    int nx, int ny,
+                                                                    const DevParams* prm,
+                                                                    const int* timed_out) {
+    const int p = blockIdx.x * kThreads + threadIdx.x;
+    if (p >= nx * ny) return;
+    if (*timed_out) {
+        xo[p] = (T)NAN;
+        return;
+    }
+    const int i = p % nx, j = p / nx;
+    T g = (T)0;
+    for (int r = 0; r < world; ++r) g += __ldcv(static_cast<const T*>(grads[r]) + off + p);
+    const T beta = (T)prm->beta[0], eps = (T)prm->eps;
+    if (beta > (T)0) g += beta * tv_grad_at<T>(x, p, i, j, nx, ny, eps * eps);
+    xo[p] = prox<T>(x[p] - (T)prm->step[0] * g, (T)prm->eta_alpha[0], prm->nonneg != 0);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) image_sums_kernel(const T* x, int nx, int ny,
                                                               double* part, DevState* st,

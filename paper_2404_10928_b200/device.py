@@ -195,6 +195,45 @@ class DeviceOperator:
                                              grad.data_ptr(), xo.data_ptr(), sums.data_ptr(),
                                              self.stream()))
 
+    # -- peer exchange of the sensor-sharded gradient (pk_peer_*) --------------------
+    def peer_handle(self) -> bytes:
+        """Allocate the plan's peer-visible block; its 64-byte handle for pk_peer_connect."""
+        buf = ctypes.create_string_buffer(N.PK_PEER_HANDLE_BYTES)
+        with _torch().cuda.device(self.device):
+            N.check(self._lib.pk_peer_handle(self._h, buf))
+        return buf.raw
+
+    def peer_connect(self, world: int, rank: int, handles) -> None:
+        handles = [bytes(h) for h in handles]
+        if len(handles) != world or any(len(h) != N.PK_PEER_HANDLE_BYTES for h in handles):
+            raise ValueError(f"need {world} handles of {N.PK_PEER_HANDLE_BYTES} bytes")
+        with _torch().cuda.device(self.device):
+            N.check(self._lib.pk_peer_connect(self._h, int(world), int(rank), b"".join(handles)))
+
+    def peer_buffer(self, slot: int) -> int:
+        """Device address of this rank's gradient slot (0 or 1)."""
+        ptr = ctypes.c_void_p()
+        N.check(self._lib.pk_peer_buffer(self._h, int(slot), ctypes.byref(ptr)))
+        return int(ptr.value)
+
+    def adjoint_residual_to(self, scale: float, ptr: int) -> None:
+        """scale * K^T r into a raw device address (a peer gradient slot)."""
+        with _torch().cuda.device(self.device):
+            N.check(self._lib.pk_adjoint_residual(self._h, ptr, float(scale), self.stream()))
+
+    def peer_timed_out(self) -> bool:
+        """True once a barrier of this plan gave up waiting for a peer (synchronous)."""
+        v = ctypes.c_int32()
+        N.check(self._lib.pk_peer_status(self._h, ctypes.byref(v)))
+        return bool(v.value)
+
+    def peer_grad_update_into(self, params: "N.SolverParams", x, slot: int, xo, sums) -> None:
+        """World barrier, grad = sum of every rank's slot (rank order), then the update."""
+        with _torch().cuda.device(self.device):
+            N.check(self._lib.pk_peer_grad_update(self._h, ctypes.byref(params), x.data_ptr(),
+                                                  int(slot), xo.data_ptr(), sums.data_ptr(),
+                                                  self.stream()))
+
     def grad_update(self, params: "N.SolverParams", x, grad):
         """x_out = prox(x - eta*(grad + beta*tv_grad(x))) and [sum|x_out|, TV(x_out), #nonfinite]."""
         torch = _torch()

@@ -26,7 +26,7 @@ from .device import CudaPool, operator_for
 from .solver import DIVERGENCE_STREAK, ReconConfig, solver_params
 
 __all__ = ["shard_range", "DeviceShardOps", "SensorShardedSolver", "SpeculativeShardSolve",
-           "FrameShardedSolver", "stop_point"]
+           "PeerShardSolve", "FrameShardedSolver", "stop_point"]
 
 
 def shard_range(count: int, rank: int, world: int) -> tuple[int, int]:
@@ -214,6 +214,141 @@ class SpeculativeShardSolve:
         k, stopped_by, hist = stop_point(rows, float(ss[0]), alpha, beta, config.tolerance)
         img = self.x[k].double().cpu().numpy()
         return ShardResult(img, np.array(hist, dtype=np.float64).reshape(-1, 4), k, stopped_by)
+
+
+class PeerShardSolve:
+    """Sensor-sharded solve with the gradient exchanged over peer memory (NVLink /
+    NVSwitch) instead of an NCCL all-reduce: per iteration
+
+        pk_adjoint_residual  -> this rank's partial 2 K_g^T r_g into its peer slot (it & 1)
+        pk_peer_grad_update  -> device barrier of the world, grad = sum of all ranks' slots in
+                                rank order (peer loads) fused with the TV + prox update
+        pk_residual          -> r_g = K_g x' - y_g and its sum of squares
+
+    so the only collective is fused into the update kernel and x stays bit-identical on every
+    rank.  Like ``SpeculativeShardSolve`` all N iterations are enqueued without a host round
+    trip (optionally as one CUDA graph); the per-rank data terms are summed once at the end
+    and the stopping rules applied afterwards (``stop_point``).
+
+    One instance per rank (process or, for tests, plan on a shared device).  Handles are
+    exchanged with ``connect`` (``handles`` in rank order) or, in a torch.distributed job,
+    with ``connect_distributed``."""
+
+    def __init__(self, grid, ring, acoustic, pool: CudaPool, world: int, rank: int,
+                 iterations: int, graph: bool = False):
+        import torch
+
+        from .device import DeviceOperator
+
+        self.world, self.rank, self.n = int(world), int(rank), int(iterations)
+        self.m0, self.m1 = shard_range(int(ring.count), rank, world)
+        self.op = op = DeviceOperator(grid, ring, acoustic, pool, self.m0, self.m1)
+        P = grid.size
+        self.y = torch.zeros(op.sensors * op.samples, device=op.device, dtype=op.tdtype)
+        self.x = torch.zeros(iterations + 1, P, device=op.device, dtype=op.tdtype)
+        self.ss = torch.zeros(iterations + 1, device=op.device, dtype=torch.float64)
+        self.sums = torch.zeros(iterations, 4, device=op.device, dtype=torch.float64)
+        self.handle = op.peer_handle()
+        self.slots = (op.peer_buffer(0), op.peer_buffer(1))
+        self._use_graph, self.graph, self._key, self._params = graph, None, None, None
+        self._alpha = self._beta = 0.0
+        self._tol = 0.0
+
+    def connect(self, handles) -> None:
+        self.op.peer_connect(self.world, self.rank, handles)
+
+    def connect_distributed(self, group=None) -> None:
+        """Exchange handles with all_gather_object and connect (then a barrier, so no rank
+        signals a peer block before that peer has mapped the world)."""
+        import torch.distributed as dist
+
+        handles = [None] * self.world
+        dist.all_gather_object(handles, self.handle, group=group)
+        self.connect(handles)
+        dist.barrier(group=group)
+
+    def _body(self):
+        op, p = self.op, self._params
+        op.residual_into(self.x[0], self.y, self.ss[0:1])  # r0 = -y
+        for it in range(self.n):
+            slot = it & 1
+            op.adjoint_residual_to(2.0, self.slots[slot])
+            op.peer_grad_update_into(p, self.x[it], slot, self.x[it + 1], self.sums[it])
+            op.residual_into(self.x[it + 1], self.y, self.ss[it + 1:it + 2])
+
+    def prepare(self, config: ReconConfig, alpha: float, beta: float, step: float) -> None:
+        """Upload the solver parameters and (graph mode) capture the solve.  Capturing does
+        not run it, so the barrier epochs advance only on replay, identically on every rank.
+        Ranks sharing one device in one process must all prepare before any launches (the
+        capture synchronises the device)."""
+        import torch
+
+        params = solver_params(config, alpha, beta, step)
+        key = (params.alpha, params.beta, params.step, params.tv_epsilon, params.nonneg)
+        self._alpha, self._beta, self._tol = alpha, beta, config.tolerance
+        if self._key == key:
+            return
+        self._params, self._key, self.graph = params, key, None
+        # parameter upload outside any capture, and one pass over every kernel of the body:
+        # under lazy module loading a first launch waits for the device to drain, which never
+        # happens while another rank of this process spins in its barrier (scratch results)
+        op = self.op
+        op.grad_update_into(params, self.x[0], self.x[0], self.x[1], self.sums[0])
+        op.residual_into(self.x[0], self.y, self.ss[0:1])
+        op.adjoint_residual_to(2.0, self.slots[0])
+        if self._use_graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._body()
+            self.graph = g
+
+    def launch(self, y_local, config: ReconConfig, alpha: float, beta: float, step: float) -> None:
+        """Enqueue the whole solve on the current stream (returns without synchronising)."""
+        import torch
+
+        self.prepare(config, alpha, beta, step)
+        self.y.copy_(torch.as_tensor(y_local).to(self.y.device, self.y.dtype), non_blocking=True)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._body()
+
+    def local_data_terms(self):
+        """This rank's sum r_g^2 after 0..N iterations (synchronises)."""
+        return self.ss.cpu().numpy()
+
+    def finish(self, data_terms=None) -> ShardResult:
+        """Apply the stopping rules.  ``data_terms`` = the world's summed data terms (N+1
+        values); default: all-reduce of the local ones over torch.distributed."""
+        if data_terms is None:
+            data_terms = _allreduce_host(self.local_data_terms())
+        if self.op.peer_timed_out():
+            raise RuntimeError(f"rank {self.rank}: peer barrier timed out (a rank did not arrive)")
+        ss = np.asarray(data_terms, dtype=np.float64)
+        sums = self.sums.cpu().numpy()
+        rows = [(float(ss[i + 1]), float(sums[i, 0]), float(sums[i, 1]), float(sums[i, 2]))
+                for i in range(self.n)]
+        k, stopped_by, hist = stop_point(rows, float(ss[0]), self._alpha, self._beta, self._tol)
+        img = self.x[k].double().cpu().numpy()
+        return ShardResult(img, np.array(hist, dtype=np.float64).reshape(-1, 4), k, stopped_by)
+
+    def solve(self, y_local, config: ReconConfig, alpha: float, beta: float, step: float) -> ShardResult:
+        self.launch(y_local, config, alpha, beta, step)
+        return self.finish()
+
+
+def _allreduce_host(a: np.ndarray) -> np.ndarray:
+    """Sum a small host array over the torch.distributed world (any backend)."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return a
+    t = torch.as_tensor(np.asarray(a, dtype=np.float64))
+    if dist.get_backend() == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t)
+    return t.cpu().numpy()
 
 
 class FrameShardedSolver:
