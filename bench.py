@@ -11,8 +11,9 @@ pinned fp64 y in, H2D, solve, D2H of the fp64 image, every step.
 
 N > 1 (torchrun, NCCL): ``--shard frames`` (default: independent frames per GPU, no
 collective, weak scaling -- the throughput mode of BASELINE configs 3/4) or ``--shard
-sensors`` (one frame split by sensors with an all-reduce of the image-sized gradient per
-iteration, strong scaling).  In frames mode with N > 1 the JSON line also carries
+sensors`` (one frame split by sensors, strong scaling; per iteration the image-sized gradient
+is exchanged over peer memory and summed inside the update kernel, ``--exchange peer``, the
+default, or all-reduced by NCCL, ``--exchange nccl``).  In frames mode with N > 1 the JSON line also carries
 ``sensor_sharded``: the single-frame latency of the sensor-sharded solve measured in the
 same run (BASELINE config 3's "sensor-sharded with allreduce").
 
@@ -48,6 +49,9 @@ def parse():
     ap.add_argument("--config", default="cfg3", choices=CFG_CHOICES)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--shard", default="frames", choices=["sensors", "frames"])
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="sensor shards: gradient exchange over peer memory fused into the update "
+                         "(pk_peer_*) or an NCCL all-reduce")
     ap.add_argument("--sensor-frames", type=int, default=5,
                     help="frames timed through the sensor-sharded solver (N > 1, frames mode)")
     ap.add_argument("--frames", type=int, default=40, help="distinct frames cycled (> L2)")
@@ -209,7 +213,8 @@ def main():
 
     import paper_2404_10928_b200 as pk
     from paper_2404_10928_b200 import _native as N
-    from paper_2404_10928_b200.sharded import DeviceShardOps, SpeculativeShardSolve, shard_range
+    from paper_2404_10928_b200.sharded import (DeviceShardOps, PeerShardSolve, SpeculativeShardSolve,
+                                                shard_range)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -247,17 +252,26 @@ def main():
     params = pk.solver.solver_params(pinned, alpha, beta, step)
 
     capture = os.environ.get("PK_DIST_BACKEND", "nccl") == "nccl"  # gloo cannot be captured
-    if sensor_mode:
+    def make_shard_solver():
         m0, m1 = shard_range(M, rank, world)
+        if args.exchange == "peer":
+            sol = PeerShardSolve(grid, ring, ac, pk.CudaPool(local, "float32"), world, rank,
+                                 cfg.iterations, graph=True)
+            sol.connect_distributed()
+            # residual (maxabs, projection, finalize) + N x (back-projection, barrier, fused
+            # peer-sum update, sums, residual); one all-reduce of N+1 data terms per frame
+            return sol, m0, m1, 3 + cfg.iterations * (1 + 3 + 3)
         ops = DeviceShardOps(grid, ring, ac, pk.CudaPool(local, "float32"), m0, m1)
-        solver = SpeculativeShardSolve(ops, cfg.iterations, graph=capture)
+        # the all-reduces are NCCL's
+        return (SpeculativeShardSolve(ops, cfg.iterations, graph=capture), m0, m1,
+                3 + cfg.iterations * (1 + 2 + 3))
+
+    if sensor_mode:
+        solver, m0, m1, launches_per_step = make_shard_solver()
         Yl = Y[:, m0 * Q : m1 * Q].contiguous()
 
         def one_step(f):
             solver.solve(Yl[f], pinned, alpha, beta, step)
-        # residual (maxabs, projection, finalize) + N x (back-projection, update + sums,
-        # residual); the all-reduces are NCCL's
-        launches_per_step = 3 + cfg.iterations * (1 + 2 + 3)
     else:
         B = args.batch
         SS = max(1, args.streams)
@@ -436,9 +450,7 @@ def main():
     # ---- sensor-sharded single-frame latency (BASELINE config 3 at N > 1) ----
     sensor_sharded = None
     if world > 1 and not sensor_mode and args.sensor_frames > 0:
-        m0, m1 = shard_range(M, rank, world)
-        sops = DeviceShardOps(grid, ring, ac, pk.CudaPool(local, "float32"), m0, m1)
-        ssolver = SpeculativeShardSolve(sops, cfg.iterations, graph=capture)
+        ssolver, m0, m1, _ = make_shard_solver()
         Yl = Y[:2, m0 * Q: m1 * Q].contiguous()
         ssolver.solve(Yl[0], pinned, alpha, beta, step)  # warm-up (plan, NCCL communicators)
         torch.cuda.synchronize(dev)
@@ -456,10 +468,15 @@ def main():
             "frames_per_s": 1e3 / ms_frame, "ms_per_frame": ms_frame,
             "ms_per_iteration": ms_frame / cfg.iterations, "frames": args.sensor_frames,
             "sensors_per_rank": m1 - m0, "iterations_run": res.iterations_run,
-            "allreduce_bytes_per_iteration": P * 4 + 8,
-            "path": "SpeculativeShardSolve: local K1 -> all_reduce(gradient) -> update -> local "
-                    "K2/K3 -> all_reduce(sum r^2), all iterations device-resident"
-                    + (" in one captured CUDA graph (NCCL)" if capture else " (eager)")}
+            "exchange": args.exchange,
+            "exchange_bytes_per_iteration": P * 4 * (world if args.exchange == "peer" else 1),
+            "path": ("PeerShardSolve: local K1 -> device barrier -> update summing every rank's "
+                     "gradient slot over peer memory (rank order) -> local K2/K3; N+1 data terms "
+                     "all-reduced once per frame; all iterations in one captured CUDA graph"
+                     if args.exchange == "peer" else
+                     "SpeculativeShardSolve: local K1 -> all_reduce(gradient) -> update -> local "
+                     "K2/K3 -> all_reduce(sum r^2), all iterations device-resident"
+                     + (" in one captured CUDA graph (NCCL)" if capture else " (eager)"))}
 
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
@@ -483,7 +500,9 @@ def main():
             "config": {"workload": cfg.name, "image": f"{cfg.n}x{cfg.n}", "sensors": M, "samples": Q,
                        "iterations": cfg.iterations, "batch": B,
                        "streams": 1 if sensor_mode else SS,
-                       "parallelism": (f"sensor-shard x{world} + NCCL all-reduce" if sensor_mode
+                       "parallelism": (f"sensor-shard x{world} + "
+                                       + ("peer-memory gradient exchange" if args.exchange == "peer"
+                                          else "NCCL all-reduce") if sensor_mode
                                        else f"frames x{world}" if world > 1 else "single GPU"),
                        "l2": f"{F} distinct frames cycled ({F * M * Q * 4 / 2**20:.0f} MiB of y > 126 MB L2)",
                        "pinned": {"alpha": alpha, "beta": beta, "step": step}},
