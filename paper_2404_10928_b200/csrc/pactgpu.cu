@@ -284,7 +284,7 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
         a.n = p->nx; a.M = p->M; a.Q = p->Q; a.groups = p->fsym_groups; a.qt = p->fsym_qt;
         a.qclamp = (float)p->Q + 1.5f;
         a.hx = p->fsym_hx;
-        a.st = p->state; a.part_tv = p->part_tv; a.solver = solver;
+        a.st = p->state; a.solver = solver;
         a.counts = p->fsym_counts;
         a.xr = reinterpret_cast<const float4*>(p->fsym_xr);
         const int units = p->fsym_qt * p->fsym_qt * p->fsym_groups;
@@ -343,8 +343,13 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
         a.M = p->M; a.Q = p->Q; a.TS = p->TS; a.w = p->w;
         a.st = p->state; a.prm = p->params; a.io = p->io; a.part_r = p->part_r;
         a.part_tv = p->part_tv;
-        a.ntv = (NF == 1 && p->fsym) ? p->fsym_qt * p->fsym_qt * p->fsym_groups
-                                     : p->fp_tiles_x * p->fp_tiles_y;
+        a.ntv = (NF == 1 && p->fsym) ? (int)grid.x : p->fp_tiles_x * p->fp_tiles_y;
+        if (NF == 1 && p->fsym && solver) {
+            a.tv_here = 1;
+            a.xb0 = static_cast<const float*>(p->xbuf[0]);
+            a.xb1 = static_cast<const float*>(p->xbuf[1]);
+            a.n = p->nx;
+        }
         a.sumsq_out = sumsq;
         a.solver = solver;
         if (NF == 1 && p->fsym) {
@@ -912,7 +917,9 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     const int ntile_max = std::max(p->bp_tiles_x * p->bp_tiles_y, p->sym ? 8 * p->sym_ntiles : 0);
     A(alloc(p, &p->part_bp, (size_t)4 * nf * std::max(ntile_max, (p->P + kThreads - 1) / kThreads)));
     const int fsym_units = p->fsym ? p->fsym_qt * p->fsym_qt * p->fsym_groups : 0;
-    A(alloc(p, &p->part_tv, (size_t)std::max(p->fp_tiles_x * p->fp_tiles_y, fsym_units) * nf));
+    // TV partials: per projector tile, or per residual CTA (M x up to 8 chunks) with the
+    // symmetric projector
+    A(alloc(p, &p->part_tv, (size_t)std::max(p->fp_tiles_x * p->fp_tiles_y, p->fsym ? 8 * p->M : 0) * nf));
     if (p->fsym) {
         A(alloc(p, &p->fsym_win, (size_t)fsym_units * 4 * 32 * p->fsym_L));
         A(alloc(p, &p->fsym_lo, (size_t)fsym_units * 32));

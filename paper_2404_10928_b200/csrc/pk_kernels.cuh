@@ -1107,8 +1107,7 @@ struct FpSymArgs {
     float qclamp;
     float hx;                // pixel pitch in samples (pxs[i] ~ pxs[0] + i*hx, fp32)
     DevState* st;
-    double* part_tv;         // solver mode: per-unit TV(x) partial (group-0 units, else 0)
-    int solver;
+    int solver;              // (TV(x') of the iterate is taken by finalize_kernel)
     const float4* xr;        // solver mode, optional: x' rotation-packed by the epilogue
 };
 
@@ -1188,10 +1187,12 @@ __global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* p
         counts[(size_t)u * LW * 32 + q] = cnt[q] + (q + 32 < LW * 32 ? cnt[q + 32] : 0);
 }
 
+#ifndef PK_K2X
+#define PK_K2X 0  // timing experiments only (tools/k2x.sh); 0 = the product
+#endif
 template <int LW, bool CLAMP>
 __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ float red_f[kFsThreads / 32];
     int iter = 0;
     if (a.solver) {
         if (a.st->all_stopped) return;
@@ -1234,8 +1235,9 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
     __syncthreads();
 
     if (lane < kFsBatch) rec[32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-    float tv = 0.f;
-    const bool do_tv = a.solver && grp == 0;
+#if PK_K2X == 1
+    uint32_t k2x_sink = 0;
+#endif
     // pieces pc = (row warp + 16*(pc / P2), 32-pixel piece pc % P2) of this warp; the 4 image
     // values of the next piece are loaded while the current one scatters
     constexpr int P2 = kFsTile / 32;
@@ -1265,16 +1267,6 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
 #pragma unroll
         for (int g = 0; g < 4; ++g) xv[g] = xn[g];
         piece_x(pc + 1, xn);
-        if (do_tv && in) {  // exact anisotropic TV over the 4 images (recon.py:169-170)
-            const int pg[4] = {jj * n + ii, ii * n + (n - 1 - jj), (n - 1 - jj) * n + (n - 1 - ii),
-                               (n - 1 - ii) * n + jj};
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                const int pi = pg[g] % n, pj = pg[g] / n;
-                if (pi + 1 < n) tv += fabsf(x[pg[g] + 1] - xv[g]);
-                if (pj + 1 < n) tv += fabsf(x[pg[g] + n] - xv[g]);
-            }
-        }
         // dense records: lane k writes {xs0, xs1, xs2, xs3} of column i0 + 32*pc + k; the
         // scatter derives px from k and xq = rint(xs) from xs, so a record is one LDS.128
         // (the record loads share the shared-memory pipe with the atomics)
@@ -1296,9 +1288,18 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
                     int32_t va[kFsBatch][4], vb[kFsBatch][4];
 #pragma unroll
                     for (int b = 0; b < kFsBatch; ++b) {
+#if PK_K2X == 2
+                        const float4 r0 = make_float4(xv[0] * (k + b), xv[1], xv[2], xv[3]);
+#else
                         const float4 r0 = rec[k + b];
+#endif
                         float fr;
+#if PK_K2X == 3
+                        const float tb = __fadd_rd(fmaf((float)(k + b), a.hx, pxbs) * 0.25f + ey2 * 0.001f, kTwo23);
+                        fr = 0.3f;
+#else
                         const float tb = fs_delay<CLAMP>((float)(k + b), a.hx, pxbs, ey2, a.qclamp, fr);
+#endif
                         const float xs[4] = {r0.x, r0.y, r0.z, r0.w};
                         const float omf = 1.f - fr;
                         // both halves rounded independently (the pair's mass is kept to one
@@ -1316,8 +1317,14 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
                         if (!CHECK || k + b < kend)  // padding columns beyond the grid add nothing
 #pragma unroll
                             for (int g = 0; g < 4; ++g) {
+#if PK_K2X == 1
+                                k2x_sink += (ad[b] + g) ^ vb[b][g] ^ va[b][g];
+#elif PK_K2X == 4
+                                red_smem_s32(ad[b] + (uint32_t)(g * LW * 128), va[b][g] + vb[b][g]);
+#else
                                 red_smem_s32(ad[b] + (uint32_t)(g * LW * 128) - 128u, vb[b][g]);
                                 red_smem_s32(ad[b] + (uint32_t)(g * LW * 128), va[b][g]);
+#endif
                             }
                 }
             };
@@ -1326,6 +1333,9 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
         }
         __syncwarp();  // rec is rewritten by the next piece
     }
+#if PK_K2X == 1
+    if (k2x_sink == 0x9e3779b9u) win[threadIdx.x] = 1;
+#endif
     griddep_launch_dependents();
     __syncthreads();
 
@@ -1343,17 +1353,6 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
             int4* d = reinterpret_cast<int4*>(dst0 + (size_t)g * 32 * LW + k0);
             __stcg(d, make_int4(v[0], v[1], v[2], v[3]));
             __stcg(d + 1, make_int4(v[4], v[5], v[6], v[7]));
-        }
-    }
-    if (a.solver) {
-        tv = warp_sum(tv);
-        __syncthreads();
-        if (lane == 0) red_f[warp] = tv;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            float tvb = red_f[0];
-            for (int w = 1; w < NW; ++w) tvb += red_f[w];
-            a.part_tv[blockIdx.x] = tvb;
         }
     }
 }
@@ -1499,8 +1498,13 @@ struct FinArgs {
     const DevParams* prm;
     const DevIo* io;
     double* part_r;      // [NF][M]
-    const double* part_tv;  // [tiles][NF]
+    double* part_tv;     // [tiles][NF] (written here when tv_here)
     int ntv;
+    // symmetric projector mode (NF == 1): this kernel also takes TV(x') of the iterate, a
+    // pixel slice per CTA, so that no projector unit carries the strided neighbour loads
+    const T* xb0;
+    const T* xb1;
+    int n, tv_here;
     double* sumsq_out;   // optional [NF] (pk_residual)
     int solver;
     // symmetric projector: gather the unit windows instead of reading acc
@@ -1588,6 +1592,17 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
     auto sample = [&](int s) -> long long {
         return a.win ? (long long)gs[s - (c0 - 1)] : __ldcg(accm + s);
     };
+    double tvp = 0.0;
+    if (a.tv_here) {  // exact anisotropic TV of x' (recon.py:169-170), pixels of this CTA
+        const T* x = (a.st->iter & 1) ? a.xb0 : a.xb1;  // the back-projector wrote xb[(iter+1)&1]
+        const int n = a.n, P = n * n, per = (P + gridDim.x - 1) / gridDim.x;
+        const int p1 = min(P, (int)(blockIdx.x + 1) * per);
+        for (int p = blockIdx.x * per + threadIdx.x; p < p1; p += kThreads) {
+            const T v = x[p];
+            if (p % n + 1 < n) tvp += (double)fabs(x[p + 1] - v);
+            if (p + n < P) tvp += (double)fabs(x[p + n] - v);
+        }
+    }
     double ss = 0.0;
     // tr[k] holds r[c0 - 1 + k]; 4 samples per thread per step, all loads first
     if (threadIdx.x == 0) tr[0] = (c0 >= 1) ? resid(c0 - 1, sample(c0 - 1)) : (T)0;
@@ -1621,6 +1636,10 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
     griddep_launch_dependents();
     ss = block_sum(ss, red_d);
     if (threadIdx.x == 0) a.part_r[(size_t)f * a.M * chunks + blockIdx.x] = ss;
+    if (a.tv_here) {
+        tvp = block_sum(tvp, red_d);
+        if (threadIdx.x == 0) a.part_tv[blockIdx.x] = tvp;
+    }
     if (!last_block(&a.st->cnt_fin, gridDim.x * gridDim.y, &last_flag)) return;
 
 #pragma unroll 1
