@@ -1224,7 +1224,11 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
         const int4* c4 = reinterpret_cast<const int4*>(a.counts + (size_t)u * LW * 32);
         int4* w4 = reinterpret_cast<int4*>(win);
         for (int q = threadIdx.x; q < LW * 8; q += kFsThreads) {
+#if PK_K2X == 7
+            int4 c = make_int4(q, 0, 0, 0);
+#else
             int4 c = __ldg(c4 + q);
+#endif
             c.x *= -kMagicBits; c.y *= -kMagicBits; c.z *= -kMagicBits; c.w *= -kMagicBits;
 #pragma unroll
             for (int g = 0; g < 4; ++g) w4[g * LW * 8 + q] = c;
@@ -1345,6 +1349,9 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
     {
         constexpr int NB = LW / 8;
         int32_t* dst0 = a.win + (size_t)u * 4 * 32 * LW + (size_t)lane * LW;
+#if PK_K2X == 6
+        if (win[threadIdx.x] != 0x12345) return;
+#endif
         for (int blk = warp; blk < 4 * NB; blk += NW) {
             const int g = blk / NB, k0 = (blk - g * NB) * 8;
             int v[8];

@@ -2,7 +2,7 @@
 # Build timing-only variants of the symmetric projector (PK_K2X, pk_kernels.cuh) and print
 # the warm per-launch time of each (K2X_BUILD=1: build here; then run on the GPU box):
 #   0 product, 1 no shared atomics, 2 records from registers (no LDS), 3 no sqrt, 4 one atomic/pair,
-#   (5: TV partial moved to finalize_kernel -- now the product)
+#   6 no window store, 7 no counts load (timings r01d: DESIGN.md, K2s)
 set -e
 cd "$(dirname "$0")/.."
 if [ "$K2X_BUILD" = 1 ]; then
