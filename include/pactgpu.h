@@ -79,7 +79,8 @@ typedef struct pk_plan_info {
     double c_dt;             /* c*dt as the reference forms it (forward.py:180) */
     double weight;           /* 1/(2*pi*c) (forward.py:183) */
     int32_t bp_tile, bp_window, bp_chunk, bp_buffers; /* back-projector tiling */
-    int32_t fp_tile, fp_window, fp_bits;              /* projector tiling, fixed-point bits */
+    int32_t fp_tile, fp_window, fp_bits;              /* projector tiling (symmetric: quadrant
+                                                         tile side, window slots), fixed-point bits */
     int64_t device_bytes;    /* workspace held by the plan */
     int32_t frames;          /* frames per call */
     int32_t bp_split;        /* sensor slices per back-projector tile (symmetric: partial slots) */

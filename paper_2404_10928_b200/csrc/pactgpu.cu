@@ -241,11 +241,14 @@ cudaError_t opt_in_smem(int device) {
     smem_kernels<1>(ks);
     smem_kernels<2>(ks);
     smem_kernels<4>(ks);
-    for (const void* k : {(const void*)fp_sym_f32_kernel<96, false>, (const void*)fp_sym_f32_kernel<128, false>,
-                          (const void*)fp_sym_f32_kernel<184, false>, (const void*)fp_sym_f32_kernel<256, false>,
-                          (const void*)fp_sym_f32_kernel<320, false>, (const void*)fp_sym_f32_kernel<96, true>,
-                          (const void*)fp_sym_f32_kernel<128, true>, (const void*)fp_sym_f32_kernel<184, true>,
-                          (const void*)fp_sym_f32_kernel<256, true>, (const void*)fp_sym_f32_kernel<320, true>})
+    for (const void* k : {(const void*)fp_sym_f32_kernel<96, false, 64>, (const void*)fp_sym_f32_kernel<128, false, 64>,
+                          (const void*)fp_sym_f32_kernel<184, false, 64>, (const void*)fp_sym_f32_kernel<256, false, 64>,
+                          (const void*)fp_sym_f32_kernel<320, false, 64>, (const void*)fp_sym_f32_kernel<96, true, 64>,
+                          (const void*)fp_sym_f32_kernel<128, true, 64>, (const void*)fp_sym_f32_kernel<184, true, 64>,
+                          (const void*)fp_sym_f32_kernel<256, true, 64>, (const void*)fp_sym_f32_kernel<320, true, 64>,
+                          (const void*)fp_sym_f32_kernel<96, false, 32>, (const void*)fp_sym_f32_kernel<128, false, 32>,
+                          (const void*)fp_sym_f32_kernel<184, false, 32>, (const void*)fp_sym_f32_kernel<96, true, 32>,
+                          (const void*)fp_sym_f32_kernel<128, true, 32>, (const void*)fp_sym_f32_kernel<184, true, 32>})
         ks.push_back(k);
     ks.push_back(sym_kernel_ptr(0));
     for (int iw : kSymIW) ks.push_back(sym_kernel_ptr(iw));
@@ -289,14 +292,22 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
         a.xr = reinterpret_cast<const float4*>(p->fsym_xr);
         const int units = p->fsym_qt * p->fsym_qt * p->fsym_groups;
         const bool clamp = p->max_delay >= (double)p->Q + 0.5;
-#define PK_FS(LW) (clamp ? launch_pdl(fp_sym_f32_kernel<LW, true>, dim3(units), dim3(kFsThreads), p->fsym_smem, s, a) \
-                         : launch_pdl(fp_sym_f32_kernel<LW, false>, dim3(units), dim3(kFsThreads), p->fsym_smem, s, a))
-        switch (p->fsym_L) {
-            case 96: PK_FS(96); break;
-            case 128: PK_FS(128); break;
-            case 184: PK_FS(184); break;
-            case 256: PK_FS(256); break;
-            default: PK_FS(320); break;
+#define PK_FS(LW, T) (clamp ? launch_pdl(fp_sym_f32_kernel<LW, true, T>, dim3(units), dim3(kFsThreads), p->fsym_smem, s, a) \
+                            : launch_pdl(fp_sym_f32_kernel<LW, false, T>, dim3(units), dim3(kFsThreads), p->fsym_smem, s, a))
+        if (p->fsym_T == 32) {
+            switch (p->fsym_L) {
+                case 96: PK_FS(96, 32); break;
+                case 128: PK_FS(128, 32); break;
+                default: PK_FS(184, 32); break;
+            }
+        } else {
+            switch (p->fsym_L) {
+                case 96: PK_FS(96, 64); break;
+                case 128: PK_FS(128, 64); break;
+                case 184: PK_FS(184, 64); break;
+                case 256: PK_FS(256, 64); break;
+                default: PK_FS(320, 64); break;
+            }
         }
 #undef PK_FS
         return;
@@ -828,32 +839,42 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 p->sym_slots = slot + 1;
             }
         }
-        // rotation-symmetric projector (fp_sym_f32_kernel): one CTA per (64 x 64 quadrant tile,
-        // group of 32 base sensors); used when there are enough units to fill the SMs
+        // rotation-symmetric projector (fp_sym_f32_kernel): one CTA per (T x T quadrant tile,
+        // group of 32 base sensors).  T = 64 when its window fits (LW <= 320) and there are
+        // enough units to fill the SMs; else T = 32 (window LW <= 184, e.g. config 2's 3.9
+        // samples per pixel) when that gives at least half an SM-count of units.
         const char* ev2 = getenv("PK_FSYM");
+        const bool forced = ev2 && atoi(ev2) != 0;
         p->fsym = (p->sym && (ev2 ? atoi(ev2) != 0 : true)) ? 1 : 0;
         if (p->fsym) {
-            p->fsym_T = kFsTile;
-            p->fsym_qt = (n / 2 + kFsTile - 1) / kFsTile;
-            p->fsym_hx = (float)((X[n - 1] - X[0]) / (n - 1) / p->cdt);
-            const int need = (int)std::ceil(tile_diag(kFsTile)) + 6;
-            p->fsym_L = 0;
-            for (int lw : {96, 128, 184, 256, 320})
-                if (need <= lw) { p->fsym_L = lw; break; }
-            p->fsym_smem = 4 * p->fsym_L * 32 * 4 + (kFsThreads / 32) * (32 + kFsBatch) * 32;
             int sms = 0;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+            p->fsym_hx = (float)((X[n - 1] - X[0]) / (n - 1) / p->cdt);
             p->fsym_groups = (p->M + 31) / 32;
-            const int units = p->fsym_qt * p->fsym_qt * p->fsym_groups;
-            if (p->fsym_L == 0 || p->fsym_smem > 200 * 1024 ||
-                (units < sms && !(ev2 && atoi(ev2) != 0)))
-                p->fsym = 0;
+            p->fsym = 0;
+            for (int T : {64, 32}) {
+                const int need = (int)std::ceil(tile_diag(T)) + 6;
+                int L = 0;
+                for (int lw : {96, 128, 184, 256, 320})
+                    if (need <= lw && (T == 64 || lw <= 184)) { L = lw; break; }
+                const int qt = (n / 2 + T - 1) / T;
+                const int units = qt * qt * p->fsym_groups;
+                const int min_units = T == 64 ? sms : (sms + 1) / 2;
+                if (L == 0 || (units < min_units && !forced)) continue;
+                p->fsym = 1;
+                p->fsym_T = T;
+                p->fsym_qt = qt;
+                p->fsym_L = L;
+                p->fsym_smem = 4 * L * 32 * 4 + (kFsThreads / 32) * (32 + kFsBatch) * 32;
+                break;
+            }
         }
         if (p->fsym) {
             // fixed-point bound of the 64 x 64 windows (may be tighter than the generic tile's)
-            double nc = 1.5 * (kFsTile * std::sqrt(2.0) + 2) * (2.0 / std::max(h, 1e-12) + 2);
-            if (p->min_delay < 8.0 * kFsTile * std::max(h, 1.0)) nc = (double)kFsTile * kFsTile;
-            nc = std::min(nc, (double)kFsTile * kFsTile);
+            const double T = p->fsym_T;
+            double nc = 1.5 * (T * std::sqrt(2.0) + 2) * (2.0 / std::max(h, 1e-12) + 2);
+            if (p->min_delay < 8.0 * T * std::max(h, 1.0)) nc = T * T;
+            nc = std::min(nc, T * T);
             p->fp_bits = std::min(p->fp_bits, std::min(22, 30 - ceil_log2(nc)));
             // the gathered sums are int32: bound the pixels that can reach one sample (s0 in
             // [s-1, s+2], a one-sample margin for fp32 delays) exactly, from the D4 base
@@ -969,17 +990,17 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         // g = 0..3, the image-g window of base sensor sg - g*M/4 from every quadrant tile
         const int ntl = p->fsym_qt * p->fsym_qt, units = ntl * p->fsym_groups;
         fp_sym_lo_kernel<<<units, 32>>>(p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups,
-                                        p->fsym_qt, (float)p->Q + 1.5f, p->fsym_lo);
+                                        p->fsym_qt, (float)p->Q + 1.5f, p->fsym_T, p->fsym_lo);
         {
             const size_t csm = (size_t)p->fsym_L * 32 * 4;
             if (p->max_delay >= (double)p->Q + 0.5)
                 fp_sym_count_kernel<true><<<units, kFsThreads, csm>>>(
                     p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups, p->fsym_qt,
-                    (float)p->Q + 1.5f, p->fsym_hx, p->fsym_L, p->fsym_counts);
+                    (float)p->Q + 1.5f, p->fsym_hx, p->fsym_L, p->fsym_T, p->fsym_counts);
             else
                 fp_sym_count_kernel<false><<<units, kFsThreads, csm>>>(
                     p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups, p->fsym_qt,
-                    (float)p->Q + 1.5f, p->fsym_hx, p->fsym_L, p->fsym_counts);
+                    (float)p->Q + 1.5f, p->fsym_hx, p->fsym_L, p->fsym_T, p->fsym_counts);
         }
         std::vector<int> lo((size_t)units * 32);
         e = cudaMemcpy(lo.data(), p->fsym_lo, sizeof(int) * lo.size(), cudaMemcpyDeviceToHost);
@@ -1029,8 +1050,8 @@ int pk_plan_get_info(const pk_plan* p, pk_plan_info* o) {
     o->bp_window = p->bp_L;
     o->bp_chunk = p->bp_CS;
     o->bp_buffers = p->bp_nbuf;
-    o->fp_tile = p->fp_T;
-    o->fp_window = p->fp_L;
+    o->fp_tile = p->fsym ? p->fsym_T : p->fp_T;   // symmetric projector: quadrant tile side
+    o->fp_window = p->fsym ? p->fsym_L : p->fp_L;
     o->fp_bits = p->fp_bits;
     o->device_bytes = p->device_bytes;
     o->frames = p->nf;

@@ -1078,18 +1078,19 @@ __global__ void __launch_bounds__(kThreads, NF == 1 ? 4 : (NF == 2 ? 3 : 2)) fp_
 // same distance, so a delay evaluated for a pixel of the first quadrant (i, j >= n/2) serves
 // its 4 rotation images
 //   g = 0: (i, j)   1: (n-1-j, i)   2: (n-1-i, n-1-j)   3: (j, n-1-i)
-// against the sensors m + g*M/4.  CTA = unit = (64x64 quadrant tile, group of 32 base
-// sensors); lane l owns base sensor m = 32*group + l and 4 windows (one per image sensor) of
-// LW slots; window word (g, slot k, lane) sits at (g*LW + k)*32 + lane, so lane l always hits
-// bank l: the scatter is conflict free.  Contributions are the integers of fp_f32_kernel:
-// xq = rint(x*scale), a = rint(x*scale*f), b = xq - a, added with red.shared.add.s32 at trace
-// index s0 (a) and s0-1 (b).  At the end the unit stores its windows, transposed to
-// [g][sensor][slot], into its own slice of a global window array (plain coalesced stores, no
-// global atomics); the residual kernel gathers, for every trace sample, the windows that cover
-// it in a fixed order (deterministic integer sums).
-// Per pair: 2/4 LDS.128 (broadcast record) + 7/4 delay + FFMA + 2 IADD + 2 ATOMS.
+// against the sensors m + g*M/4.  CTA = unit = (T x T quadrant tile, T = 64 or 32, group of
+// 32 base sensors); lane l owns base sensor m = 32*group + l and 4 windows (one per image
+// sensor) of LW slots; window word (g, slot k, lane) sits at (g*LW + k)*32 + lane, so lane l
+// always hits bank l: the scatter is conflict free.  Contributions are fixed-point integers:
+// round(xs*f) at trace index s0 and round(xs*(1-f)) at s0-1 (xs = x*scale), added with
+// red.shared.add.s32 as magic-biased float bits (the bias is pre-subtracted per slot).  At the
+// end the unit stores its windows, transposed to [g][sensor][slot], into its own slice of a
+// global window array (no global atomics); the residual kernel gathers, for every trace
+// sample, the windows that cover it (deterministic integer sums).
+// Per record (1 pixel x 32 sensors x 4 images): 1 LDS.128 + ~8 delay + 8 FFMA + 8 ATOMS.
 // ===========================================================================
-constexpr int kFsTile = 64;      // quadrant tile side (rows are scattered as two 32-pixel pieces)
+constexpr int kFsTile = 64;      // quadrant tile side (32 where a 64-tile window does not fit:
+                                 // short c*dt, e.g. BASELINE config 2); rows are 32-pixel pieces
 constexpr int kFsBatch = 4;      // records per scatter batch (16 independent atomic pairs)
 constexpr int kFsThreads = 512;  // 16 warps share the windows (occupancy at 2 CTAs per SM)
 
@@ -1111,11 +1112,11 @@ struct FpSymArgs {
     const float4* xr;        // solver mode, optional: x' rotation-packed by the epilogue
 };
 
-// first trace index of the window of the 64x64 quadrant tile at (i0, j0) for sensor (sx, sy)
+// first trace index of the window of the tile x tile quadrant tile at (i0, j0) for sensor (sx, sy)
 __device__ __forceinline__ int fp_sym_window_lo(const float* pxs, const float* pys, int n, int i0,
-                                                int j0, float sx, float sy, float qclamp) {
-    const float X0 = __ldg(pxs + i0), X1 = __ldg(pxs + min(i0 + kFsTile - 1, n - 1));
-    const float Y0 = __ldg(pys + j0), Y1 = __ldg(pys + min(j0 + kFsTile - 1, n - 1));
+                                                int j0, float sx, float sy, float qclamp, int tile) {
+    const float X0 = __ldg(pxs + i0), X1 = __ldg(pxs + min(i0 + tile - 1, n - 1));
+    const float Y0 = __ldg(pys + j0), Y1 = __ldg(pys + min(j0 + tile - 1, n - 1));
     const float cx = fminf(fmaxf(sx, X0), X1), cy = fminf(fmaxf(sy, Y0), Y1);
     const float dmin = fminf(sqrtf((cx - sx) * (cx - sx) + (cy - sy) * (cy - sy)), qclamp);
     return (int)floorf(dmin) - 2;
@@ -1123,12 +1124,12 @@ __device__ __forceinline__ int fp_sym_window_lo(const float* pxs, const float* p
 
 // plan setup: lo of every (unit, lane) -- geometry only, identical to the projector's
 __global__ void fp_sym_lo_kernel(const float* pxs, const float* pys, const float* sxs, const float* sys,
-                                 int n, int M, int groups, int qt, float qclamp, int32_t* lo_out) {
+                                 int n, int M, int groups, int qt, float qclamp, int T, int32_t* lo_out) {
     const int u = blockIdx.x, lane = threadIdx.x;
     const int tile = u / groups, grp = u % groups, h = n >> 1;
-    const int i0 = h + kFsTile * (tile % qt), j0 = h + kFsTile * (tile / qt);
+    const int i0 = h + T * (tile % qt), j0 = h + T * (tile / qt);
     const int mm = min(grp * 32 + lane, M - 1);
-    lo_out[u * 32 + lane] = fp_sym_window_lo(pxs, pys, n, i0, j0, __ldg(sxs + mm), __ldg(sys + mm), qclamp);
+    lo_out[u * 32 + lane] = fp_sym_window_lo(pxs, pys, n, i0, j0, __ldg(sxs + mm), __ldg(sys + mm), qclamp, T);
 }
 
 // delay of column k of a 32-pixel piece (pxbs = x of the piece's first column minus the
@@ -1155,21 +1156,21 @@ __global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* p
                                                                   const float* sxs, const float* sys,
                                                                   int n, int M, int groups, int qt,
                                                                   float qclamp, float hx, int LW,
-                                                                  int32_t* counts) {
+                                                                  int T, int32_t* counts) {
     extern __shared__ int32_t cnt[];  // [LW][32]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, h = n >> 1;
     const int u = blockIdx.x, tile = u / groups, grp = u % groups;
-    const int i0 = h + kFsTile * (tile % qt), j0 = h + kFsTile * (tile / qt);
-    const int jend = min(j0 + kFsTile, n);
+    const int i0 = h + T * (tile % qt), j0 = h + T * (tile / qt);
+    const int jend = min(j0 + T, n);
     const int mm = min(grp * 32 + lane, M - 1);
     const float sx = __ldg(sxs + mm), sy = __ldg(sys + mm);
-    const int lo = fp_sym_window_lo(pxs, pys, n, i0, j0, sx, sy, qclamp);
+    const int lo = fp_sym_window_lo(pxs, pys, n, i0, j0, sx, sy, qclamp, T);
     for (int q = threadIdx.x; q < LW * 32; q += kFsThreads) cnt[q] = 0;
     __syncthreads();
     for (int jj = j0 + warp; jj < jend; jj += kFsThreads / 32) {
         const float ey = __ldg(pys + jj) - sy;
         const float ey2 = ey * ey;
-        for (int c0 = i0; c0 < min(i0 + kFsTile, n); c0 += 32) {
+        for (int c0 = i0; c0 < min(i0 + T, n); c0 += 32) {
             const float pxbs = __ldg(pxs + c0) - sx;
             const int kend = min(32, n - c0);
             for (int k = 0; k < kend; ++k) {
@@ -1190,7 +1191,7 @@ __global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* p
 #ifndef PK_K2X
 #define PK_K2X 0  // timing experiments only (tools/k2x.sh); 0 = the product
 #endif
-template <int LW, bool CLAMP>
+template <int LW, bool CLAMP, int T>
 __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     int iter = 0;
@@ -1210,14 +1211,14 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
 
     const int u = blockIdx.x;
     const int tile = u / a.groups, grp = u % a.groups;
-    const int i0 = h + kFsTile * (tile % a.qt), j0 = h + kFsTile * (tile / a.qt);
-    const int jend = min(j0 + kFsTile, n);
+    const int i0 = h + T * (tile % a.qt), j0 = h + T * (tile / a.qt);
+    const int jend = min(j0 + T, n);
     const int m = grp * 32 + lane;
     const bool sensor_ok = m < a.M;
     const int mm = min(m, a.M - 1);
     const float sx = __ldg(a.sxs + mm), sy = __ldg(a.sys + mm);
     // window: trace indices [lo, lo + LW) of this tile (fp_sym_window_lo)
-    const int lo = fp_sym_window_lo(a.pxs, a.pys, n, i0, j0, sx, sy, a.qclamp);
+    const int lo = fp_sym_window_lo(a.pxs, a.pys, n, i0, j0, sx, sy, a.qclamp, T);
     // word (g, k, lane) at (g*LW + k)*32 + lane, k = t - lo for trace index t
     const uint32_t adj = win_s + 4u * (uint32_t)lane - 128u * (uint32_t)lo - 128u * kTwo23Bits;
     {   // every window slot starts at -count * bias (see fp_sym_count_kernel)
@@ -1244,7 +1245,7 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
 #endif
     // pieces pc = (row warp + 16*(pc / P2), 32-pixel piece pc % P2) of this warp; the 4 image
     // values of the next piece are loaded while the current one scatters
-    constexpr int P2 = kFsTile / 32;
+    constexpr int P2 = T / 32;
     constexpr int NW = kFsThreads / 32;
     auto piece_x = [&](int pc, float (&v)[4]) {
         const int jj = j0 + warp + NW * (pc / P2);
