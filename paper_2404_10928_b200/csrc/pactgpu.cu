@@ -147,7 +147,7 @@ void free_plan(pk_plan* p) {
     if (p->graph) cudaGraphDestroy(p->graph);
     void* ptrs[] = {p->pxs, p->pys, p->sxs, p->sys, p->px, p->py, p->sx, p->sy, p->table,
                     p->acc, p->xbuf[0], p->xbuf[1], p->ydev, p->y64, p->x64, p->hist_dev,
-                    p->status_dev, p->part_bp, p->part_tv, p->part_r, p->part_misc, p->state,
+                    p->status_dev, p->part_bp, p->part_mx, p->part_l1, p->part_tv, p->part_r, p->part_misc, p->state,
                     p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt, p->sym_tiles,
                     p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0, p->sym_tile_slot0,
                     p->sym_part, p->fsym_win, p->fsym_lo, p->fsym_list, p->fsym_counts,
@@ -290,6 +290,11 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
         a.st = p->state; a.solver = solver;
         a.counts = p->fsym_counts;
         a.xr = reinterpret_cast<const float4*>(p->fsym_xr);
+        if (solver && p->sym) {  // the symmetric epilogue deferred its statistics
+            a.part_mx = p->part_mx;
+            a.nmx = p->sym_ntiles * 32;
+            a.bits = p->fp_bits;
+        }
         const int units = p->fsym_qt * p->fsym_qt * p->fsym_groups;
         const bool clamp = p->max_delay >= (double)p->Q + 0.5;
 #define PK_FS(LW, T) (clamp ? launch_pdl(fp_sym_f32_kernel<LW, true, T>, dim3(units), dim3(kFsThreads), p->fsym_smem, s, a) \
@@ -356,6 +361,7 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
         a.part_tv = p->part_tv;
         a.ntv = (NF == 1 && p->fsym) ? (int)grid.x : p->fp_tiles_x * p->fp_tiles_y;
         if (NF == 1 && p->fsym && solver) {
+            a.part_l1 = p->part_l1;
             a.tv_here = 1;
             a.xb0 = static_cast<const float*>(p->xbuf[0]);
             a.xb1 = static_cast<const float*>(p->xbuf[1]);
@@ -414,8 +420,11 @@ void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_
         E.xb1 = static_cast<float*>(p->xbuf[1]);
         E.prm = p->params; E.st = p->state; E.part_bp = p->part_bp;
         E.xr = p->fsym ? p->fsym_xr : nullptr;
-        if (epi) launch_pdl(bp_sym_epi_kernel<true>, dim3(p->sym_ntiles * 8), dim3(kThreads), 0, s, E);
-        else launch_pdl(bp_sym_epi_kernel<false>, dim3(p->sym_ntiles * 8), dim3(kThreads), 0, s, E);
+        E.part_mx = p->part_mx;
+        const dim3 eg(p->sym_ntiles * 32);
+        if (epi && p->fsym) launch_pdl(bp_sym_epi_kernel<true, true>, eg, dim3(kThreads), 0, s, E);
+        else if (epi) launch_pdl(bp_sym_epi_kernel<true, false>, eg, dim3(kThreads), 0, s, E);
+        else launch_pdl(bp_sym_epi_kernel<false, false>, eg, dim3(kThreads), 0, s, E);
         return;
     }
     if (p->dtype == PK_F32) {
@@ -935,8 +944,10 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     A(alloc(p, &p->acc, (size_t)p->M * p->Q * nf));
     A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[0]), (size_t)p->P * ts * nf));
     A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[1]), (size_t)p->P * ts * nf));
-    const int ntile_max = std::max(p->bp_tiles_x * p->bp_tiles_y, p->sym ? 8 * p->sym_ntiles : 0);
+    const int ntile_max = std::max(p->bp_tiles_x * p->bp_tiles_y, p->sym ? 32 * p->sym_ntiles : 0);
     A(alloc(p, &p->part_bp, (size_t)4 * nf * std::max(ntile_max, (p->P + kThreads - 1) / kThreads)));
+    A(alloc(p, &p->part_mx, (size_t)std::max(1, p->sym ? 32 * p->sym_ntiles : 1)));
+    A(alloc(p, &p->part_l1, (size_t)(p->fsym ? 2 * 8 * p->M : 1)));
     const int fsym_units = p->fsym ? p->fsym_qt * p->fsym_qt * p->fsym_groups : 0;
     // TV partials: per projector tile, or per residual CTA (M x up to 8 chunks) with the
     // symmetric projector

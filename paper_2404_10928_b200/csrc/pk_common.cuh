@@ -165,9 +165,9 @@ __device__ __forceinline__ T warp_max(T v) {
     return v;
 }
 
-// sum over the 256-thread block; result valid in every thread
-template <typename T>
-__device__ __forceinline__ T block_sum(T v, T* red) {
+// sum over the block (NT threads, 256 by default); result valid in every thread
+template <typename T, int NT = kThreads>
+__device__ __forceinline__ T block_sum(T v, T* red) {  // NT = block size (red: NT / 32 slots)
     v = warp_sum(v);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __syncthreads();
@@ -175,10 +175,29 @@ __device__ __forceinline__ T block_sum(T v, T* red) {
     __syncthreads();
     T s = red[0];
 #pragma unroll
-    for (int w = 1; w < kThreads / 32; ++w) s += red[w];
+    for (int w = 1; w < NT / 32; ++w) s += red[w];
     return s;
 }
-template <typename T>
+// four sums in one pass (one pair of barriers); red: 4 * NT / 32 slots
+template <int NT = kThreads>
+__device__ __forceinline__ void block_sum4(double (&v)[4], double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = warp_sum(v[q]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) red[q * (NT / 32) + warp] = v[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        double s = red[q * (NT / 32)];
+#pragma unroll
+        for (int w = 1; w < NT / 32; ++w) s += red[q * (NT / 32) + w];
+        v[q] = s;
+    }
+}
+template <typename T, int NT = kThreads>
 __device__ __forceinline__ T block_max(T v, T* red) {
     v = warp_max(v);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -187,7 +206,7 @@ __device__ __forceinline__ T block_max(T v, T* red) {
     __syncthreads();
     T s = red[0];
 #pragma unroll
-    for (int w = 1; w < kThreads / 32; ++w) s = fmax(s, red[w]);
+    for (int w = 1; w < NT / 32; ++w) s = fmax(s, red[w]);
     return s;
 }
 
@@ -267,6 +286,8 @@ struct pk_plan {
     int hist_cap = 0;
     int32_t* status_dev = nullptr;
     double* part_bp = nullptr;   // [bp blocks * 4]
+    float* part_mx = nullptr;    // [symmetric epilogue CTAs] max |x'| partials (deferred stats)
+    double* part_l1 = nullptr;   // [residual CTAs][2] sum |x'|, non-finite (deferred stats)
     double* part_tv = nullptr;   // [fp tiles]
     double* part_r = nullptr;    // [M]
     double* part_misc = nullptr; // [generic blocks * 4]

@@ -567,9 +567,10 @@ __global__ void __launch_bounds__(kSymThreads, 3) bp_sym_f32_kernel(BpSymArgs a)
     flush();
 }
 
-// K1s epilogue: CTA (tile, image g) adds the tile's partial slots in order, maps the
-// representatives to image g, and writes gscale * K^T r (EPI == false) or runs the fused
-// update of recon.py:327-338 with the block statistics of the next projector scale.
+// K1s epilogue: CTA (tile, image g, 8-column strip) adds the tile's partial slots (4 slot
+// groups in parallel, then in order), maps the representatives to image g, and writes
+// gscale * K^T r (EPI == false) or runs the fused update of recon.py:327-338 with the block
+// statistics of the next projector scale.
 struct BpSymEpiArgs {
     const float* part;        // [slots][8][4][kThreads]
     const int* tile_slot0;    // [ntiles + 1]
@@ -584,6 +585,7 @@ struct BpSymEpiArgs {
     double* part_bp;          // [grid][4]
     float* xr;                // EPI == true, optional: rotation-packed copy of x' for the
                               // symmetric projector, [(n/2)^2][4] (fp_sym_f32_kernel)
+    float* part_mx;           // DEFER: [grid] max |x'| per CTA (the projector reduces them)
 };
 
 // rotation-packed index of pixel (i, j): the quadrant representative q = (qi, qj) in
@@ -602,84 +604,96 @@ __device__ __forceinline__ int sym_rot_index(int i, int j, int n) {
     return 4 * ((qj - h) * h + (qi - h)) + r;
 }
 
-template <bool EPI>
+// DEFER (with the symmetric projector): no last-block reduction here -- the projector's CTAs
+// reduce the max partials into the fixed-point scale and the residual kernel takes sum |x'|
+// and the non-finite count with TV(x'), so no single CTA serialises the end of this kernel.
+template <bool EPI, bool DEFER>
 __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
     __shared__ float red_f[kThreads / 32];
     __shared__ double red_d[kThreads / 32];
     __shared__ int last_flag;
-    __shared__ float blk[kSymTile * kSymTile];  // the image-g block of the tile, row-major
+    __shared__ float4 part4[3][64];            // slot-group partials 1..3
+    __shared__ float blk[8 * kSymTile];        // the strip in image g, row-major (bw x bh)
     int iter = 0;
     if (EPI) {
         if (a.st->all_stopped) return;
         iter = a.st->iter;
     }
-    const int t = blockIdx.x >> 3, g = blockIdx.x & 7;
+    // CTA = (tile, image g, strip k): the main kernel's consumer thread c holds, in slot
+    // element [g][k][c], the sum for representative (i0 + 8k + lx, j0 + 4(c / 32) + ly) -- an
+    // 8-column strip of the tile, 256 pixels
+    const int k = blockIdx.x & 3, g = (blockIdx.x >> 2) & 7, t = blockIdx.x >> 5;
     const int tp = __ldg(a.tiles + t);
     const int tx = tp >> 16, ty = tp & 0xffff;
     const bool active = !(tx == ty && g >= 4);
     const int n = a.n, h = n >> 1;
     const int i0 = h + kSymTile * tx, j0 = h + kSymTile * ty;
     const int s0 = __ldg(a.tile_slot0 + t), s1 = __ldg(a.tile_slot0 + t + 1);
-    // the tile's image under g is the 32x32 block [bx, bx+32) x [by, by+32) (clipped to the grid)
-    int bx, by;
+    // the strip's image under g is the block [bx, bx + bw) x [by, by + bh), bw * bh = 256
+    int bx, by, bw;
     {
         int ia, ja, ib, jb;
-        sym_pixel(g, i0, j0, n, ia, ja);
-        sym_pixel(g, i0 + kSymTile - 1, j0 + kSymTile - 1, n, ib, jb);
+        sym_pixel(g, i0 + 8 * k, j0, n, ia, ja);
+        sym_pixel(g, i0 + 8 * k + 7, j0 + kSymTile - 1, n, ib, jb);
         bx = min(ia, ib);
         by = min(ja, jb);
+        bw = abs(ib - ia) + 1;
     }
-    // 1) the tile's slots in order, coalesced: thread owns elements 4*tid .. 4*tid+3 of the
-    //    slot vector [k][consumer thread], every slot is one 16-B load
-    const int k = threadIdx.x >> 6, ct = (threadIdx.x & 63) * 4;
+    // 1) slot sum: thread (sg, q) adds slots s0 + sg, s0 + sg + 4, ... of consumers 4q..4q+3
+    //    (16-B loads, 8 in flight); the 4 slot groups are then added in order (deterministic)
+    const int sg = threadIdx.x >> 6, q = threadIdx.x & 63;
     griddep_wait();  // partial slots of the main kernel
     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (active) {
-        const float4* src = reinterpret_cast<const float4*>(a.part + (size_t)g * 4 * kThreads) + threadIdx.x;
+#ifndef PK_EPX
+#define PK_EPX 0  // timing experiments only (tools/k2v.sh); 0 = the product
+#endif
+    if (active && PK_EPX != 1) {
+        const float4* src = reinterpret_cast<const float4*>(a.part + (size_t)(g * 4 + k) * kThreads) + q;
         const size_t stride = 8 * 4 * kThreads / 4;  // float4s per slot
-        for (int sb = s0; sb < s1; sb += 16) {
-            float4 v[16];
+        for (int sb = s0 + sg; sb < s1; sb += 32) {
+            float4 v[8];
 #pragma unroll
-            for (int u = 0; u < 16; ++u)
-                v[u] = (sb + u < s1) ? __ldcg(src + (size_t)(sb + u) * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int u = 0; u < 8; ++u)
+                v[u] = (sb + 4 * u < s1) ? __ldcg(src + (size_t)(sb + 4 * u) * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 sum.x += v[u].x; sum.y += v[u].y; sum.z += v[u].z; sum.w += v[u].w;
             }
         }
     }
-    // 2) scatter the sums into the image-g block (shared memory transpose)
-    {
+    if (sg > 0) part4[sg - 1][q] = sum;
+    __syncthreads();
+    // 2) slot group 0 finishes the sums and scatters them into the strip (shared transpose)
+    if (sg == 0) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const float4 o = part4[r][q];
+            sum.x += o.x; sum.y += o.y; sum.z += o.z; sum.w += o.w;
+        }
         const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int c = ct + u;  // consumer thread of the main kernel
+            const int c = 4 * q + u;  // consumer thread of the main kernel
             int lx, ly;
             sym_lane_xy(c & 31, a.lanemap, lx, ly);
             int ig, jg;
             sym_pixel(g, i0 + lx + 8 * k, j0 + 4 * (c >> 5) + ly, n, ig, jg);
-            blk[(jg - by) * kSymTile + (ig - bx)] = a.gscale * sv[u];
+            blk[(jg - by) * bw + (ig - bx)] = a.gscale * sv[u];
         }
     }
     __syncthreads();
-    // 3) image-row-major pass over the block: coalesced stencil loads and stores
-    const int bc = threadIdx.x & 31;
-    int pix[4];
-    float val[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int br = (threadIdx.x >> 5) + 8 * q;
-        const int ig = bx + bc, jg = by + br;
-        // a pixel of the block belongs to this CTA iff its representative is in the tile
-        // (row/column beyond the grid edge, or the lower triangle's half of a diagonal
-        // tile under a reflection, are skipped)
-        pix[q] = (active && ig >= 0 && ig < n && jg >= 0 && jg < n) ? jg * n + ig : -1;
-        val[q] = blk[br * kSymTile + bc];
+    // 3) one pixel per thread in image-row-major order of the strip
+    int pix;
+    float val;
+    {
+        const int ig = bx + threadIdx.x % bw, jg = by + threadIdx.x / bw;
+        // a pixel of the strip belongs to this CTA iff its representative is in the tile (row /
+        // column beyond the grid edge, or the reflections of a diagonal tile, are skipped)
+        pix = (active && ig >= 0 && ig < n && jg >= 0 && jg < n) ? jg * n + ig : -1;
+        val = blk[threadIdx.x];
     }
     if (!EPI) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            if (pix[q] >= 0) a.out[pix[q]] = val[q];
+        if (pix >= 0) a.out[pix] = val;
         return;
     }
     const float* x = (iter & 1) ? a.xb1 : a.xb0;
@@ -689,23 +703,23 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
     const bool nonneg = a.prm->nonneg != 0;
     float mx = 0.f, l1 = 0.f;
     int bad = 0;
-    if (!a.st->fr[0].stopped) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int p = pix[q];
-            if (p < 0) continue;
-            float gr = val[q];
-            if (beta > 0.f) gr += beta * tv_grad_at<float>(x, p, p % n, p / n, n, n, eps * eps);
-            const float xn = prox<float>(x[p] - eta * gr, lam, nonneg);
-            xo[p] = xn;
-            if (a.xr) a.xr[sym_rot_index(p % n, p / n, n)] = xn;
-            if (!isfinite(xn)) bad = 1;
-            mx = fmaxf(mx, fabsf(xn));
-            l1 += fabsf(xn);
-        }
+    if (!a.st->fr[0].stopped && pix >= 0) {
+        const int p = pix;
+        float gr = val;
+        if (beta > 0.f && PK_EPX != 3) gr += beta * tv_grad_at<float>(x, p, p % n, p / n, n, n, eps * eps);
+        const float xn = prox<float>(x[p] - eta * gr, lam, nonneg);
+        xo[p] = xn;
+        if (a.xr) a.xr[sym_rot_index(p % n, p / n, n)] = xn;
+        if (!isfinite(xn)) bad = 1;
+        mx = fabsf(xn);
+        l1 = fabsf(xn);
     }
     griddep_launch_dependents();
     mx = block_max(mx, red_f);
+    if (DEFER) {  // sum |x'| and the non-finite count are taken by the residual kernel
+        if (threadIdx.x == 0) a.part_mx[blockIdx.x] = mx;
+        return;
+    }
     const float l1b = block_sum(l1, red_f);
     const int badb = __syncthreads_or(bad);
     if (threadIdx.x == 0) {
@@ -714,7 +728,7 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
         pp[1] = l1b;
         pp[2] = badb;
     }
-    if (last_block(&a.st->cnt_bp, gridDim.x, &last_flag)) {
+    if (PK_EPX != 2 && last_block(&a.st->cnt_bp, gridDim.x, &last_flag)) {
         double m2 = 0.0, s2 = 0.0, b2 = 0.0;
         for (int q = threadIdx.x; q < (int)gridDim.x; q += kThreads) {
             const double* pp = a.part_bp + 4 * (size_t)q;
@@ -1110,6 +1124,8 @@ struct FpSymArgs {
     DevState* st;
     int solver;              // (TV(x') of the iterate is taken by finalize_kernel)
     const float4* xr;        // solver mode, optional: x' rotation-packed by the epilogue
+    const float* part_mx;    // solver mode, optional: the epilogue's deferred max partials
+    int nmx, bits;           //   (the scale is 2^bits / max, as the epilogue's last block did)
 };
 
 // first trace index of the window of the tile x tile quadrant tile at (i0, j0) for sensor (sx, sy)
@@ -1236,7 +1252,23 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
         }
     }
     griddep_wait();  // x' and its fixed-point scale come from the back-projector epilogue
-    const float scale = a.st->fr[0].scale32;
+    float scale;
+    if (a.part_mx) {  // deferred statistics: every CTA reduces the epilogue's max partials
+        __shared__ float red_f[kFsThreads / 32];
+        float m = 0.f;
+        for (int q = threadIdx.x; q < a.nmx; q += kFsThreads) m = fmaxf(m, __ldcg(a.part_mx + q));
+        m = block_max<float, kFsThreads>(m, red_f);
+        const double scl = (m > 0.f && isfinite(m)) ? ldexp(1.0, a.bits) / (double)m : 0.0;
+        scale = (float)scl;
+        if (blockIdx.x == 0 && threadIdx.x == 0 && !a.st->fr[0].stopped) {
+            FrameState& fs = a.st->fr[0];
+            fs.maxabs = m;
+            fs.scale64 = scl;
+            fs.scale32 = (float)scl;
+        }
+    } else {
+        scale = a.st->fr[0].scale32;
+    }
     __syncthreads();
 
     if (lane < kFsBatch) rec[32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1513,6 +1545,8 @@ struct FinArgs {
     const T* xb0;
     const T* xb1;
     int n, tv_here;
+    double* part_l1;     // tv_here: [grid][2] sum |x'| and non-finite count per CTA (the
+                         // symmetric epilogue deferred them)
     double* sumsq_out;   // optional [NF] (pk_residual)
     int solver;
     // symmetric projector: gather the unit windows instead of reading acc
@@ -1600,13 +1634,15 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
     auto sample = [&](int s) -> long long {
         return a.win ? (long long)gs[s - (c0 - 1)] : __ldcg(accm + s);
     };
-    double tvp = 0.0;
-    if (a.tv_here) {  // exact anisotropic TV of x' (recon.py:169-170), pixels of this CTA
+    double tvp = 0.0, l1p = 0.0, badp = 0.0;
+    if (a.tv_here) {  // exact anisotropic TV of x' (recon.py:169-170), sum |x'| and non-finite
         const T* x = (a.st->iter & 1) ? a.xb0 : a.xb1;  // the back-projector wrote xb[(iter+1)&1]
         const int n = a.n, P = n * n, per = (P + gridDim.x - 1) / gridDim.x;
         const int p1 = min(P, (int)(blockIdx.x + 1) * per);
         for (int p = blockIdx.x * per + threadIdx.x; p < p1; p += kThreads) {
             const T v = x[p];
+            l1p += (double)fabs(v);
+            if (!isfinite(v)) badp += 1.0;
             if (p % n + 1 < n) tvp += (double)fabs(x[p + 1] - v);
             if (p + n < P) tvp += (double)fabs(x[p + n] - v);
         }
@@ -1642,27 +1678,56 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
         a.table[((size_t)m * a.TS + e) * NF + f] = pair_entry<T>(rp, rc, e, a.atrick);
     }
     griddep_launch_dependents();
-    ss = block_sum(ss, red_d);
-    if (threadIdx.x == 0) a.part_r[(size_t)f * a.M * chunks + blockIdx.x] = ss;
     if (a.tv_here) {
-        tvp = block_sum(tvp, red_d);
-        if (threadIdx.x == 0) a.part_tv[blockIdx.x] = tvp;
+        __shared__ double red4[4 * kThreads / 32];
+        double v4[4] = {ss, tvp, l1p, badp};
+        block_sum4(v4, red4);
+        if (threadIdx.x == 0) {
+            a.part_r[(size_t)f * a.M * chunks + blockIdx.x] = v4[0];
+            a.part_tv[blockIdx.x] = v4[1];
+            a.part_l1[2 * (size_t)blockIdx.x] = v4[2];
+            a.part_l1[2 * (size_t)blockIdx.x + 1] = v4[3];
+        }
+    } else {
+        ss = block_sum(ss, red_d);
+        if (threadIdx.x == 0) a.part_r[(size_t)f * a.M * chunks + blockIdx.x] = ss;
     }
     if (!last_block(&a.st->cnt_fin, gridDim.x * gridDim.y, &last_flag)) return;
 
-#pragma unroll 1
-    for (int g = 0; g < NF; ++g) {
-        double d = 0.0, t = 0.0;
-        for (int q = threadIdx.x; q < a.M * chunks; q += kThreads)
-            d += a.part_r[(size_t)g * a.M * chunks + q];
-        d = block_sum(d, red_d);
-        if (a.solver) {
-            for (int q = threadIdx.x; q < a.ntv; q += kThreads) t += a.part_tv[(size_t)q * NF + g];
-            t = block_sum(t, red_d);
+    if (a.tv_here) {  // NF == 1, one pass: data, TV, and the epilogue's deferred sum |x'| and
+                      // non-finite count (the residual CTAs' partials are aligned)
+        __shared__ double red4l[4 * kThreads / 32];
+        double v4[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int q = threadIdx.x; q < a.ntv; q += kThreads) {
+            v4[0] += a.part_r[q];
+            v4[1] += a.part_tv[q];
+            v4[2] += a.part_l1[2 * (size_t)q];
+            v4[3] += a.part_l1[2 * (size_t)q + 1];
         }
+        block_sum4(v4, red4l);
         if (threadIdx.x == 0) {
-            data_s[g] = d;
-            tv_s[g] = t;
+            data_s[0] = v4[0];
+            tv_s[0] = v4[1];
+            if (!a.st->fr[0].stopped) {
+                a.st->fr[0].l1sum = v4[2];
+                a.st->fr[0].nonfinite = v4[3] > 0.0 ? 1 : 0;
+            }
+        }
+    } else {
+#pragma unroll 1
+        for (int g = 0; g < NF; ++g) {
+            double d = 0.0, t = 0.0;
+            for (int q = threadIdx.x; q < a.M * chunks; q += kThreads)
+                d += a.part_r[(size_t)g * a.M * chunks + q];
+            d = block_sum(d, red_d);
+            if (a.solver) {
+                for (int q = threadIdx.x; q < a.ntv; q += kThreads) t += a.part_tv[(size_t)q * NF + g];
+                t = block_sum(t, red_d);
+            }
+            if (threadIdx.x == 0) {
+                data_s[g] = d;
+                tv_s[g] = t;
+            }
         }
     }
     if (threadIdx.x != 0) return;
