@@ -186,17 +186,26 @@ def test_config1_vs_reference(pool):
     np.testing.assert_allclose(res.objective_history, gold["hist"][0], rtol=1e-5)
 
 
-@pytest.mark.parametrize("cfg", [(256, 256, 2048, 20), (512, 512, 2048, 10)])
+@pytest.mark.parametrize("cfg", [(256, 256, 2048, 20), (512, 512, 2048, 10), (1024, 1024, 4096, 3)],
+                         ids=["cfg2", "cfg3", "cfg5-3it"])
 def test_large_config_vs_oracle(oracle, cfg):
-    """Configs 2 and 3 (dense K does not fit): fp32 device vs the fp64 matrix-free oracle."""
+    """Configs 2, 3 and 5 (dense K does not fit): fp32 device vs the fp64 matrix-free oracle
+    (config 5 for 3 of its 50 iterations, the step from the device fp64 calibration: the
+    oracle's 50 power iterations would take minutes there)."""
     n, M, Q, N = cfg
     s = oracle.make_scene(n, M, Q, 0)
     o = oracle.Operator.of(s)
     y = o.forward(s.phantom)
     alpha, beta = oracle.resolve_regularization(o, y)
-    step = oracle.resolve_step(o, beta, 1e-3) if n <= 256 else 333.156  # survey-pinned cfg3 step
-    ref = oracle.reconstruct(o, y, alpha, beta, step, N)
     g, ring, ac, ph, K = scene(n, M, Q)
+    if n <= 256:
+        step = oracle.resolve_step(o, beta, 1e-3)
+    elif n == 512:
+        step = 333.156  # survey-pinned cfg3 step
+    else:
+        step = pk.resolve_config(pk.ReconConfig(alpha, beta, N), K, pk.SensorData("time", M, Q, y),
+                                 pool=F64).step
+    ref = oracle.reconstruct(o, y, alpha, beta, step, N)
     res = pk.iterative_reconstruct(K, pk.SensorData("time", M, Q, y),
                                    pk.ReconConfig(alpha, beta, N, step), pool=F32)
     assert res.iterations_run == ref["iterations_run"]
