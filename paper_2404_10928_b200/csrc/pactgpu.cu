@@ -236,7 +236,7 @@ cudaError_t opt_in_smem(int device) {
     if (done[device]) return cudaSuccess;
     int mx = 0;
     cudaError_t e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-    mx -= 2048;  // headroom for the kernels' static shared memory
+    // (each kernel's own static shared memory is subtracted below)
     std::vector<const void*> ks;
     smem_kernels<1>(ks);
     smem_kernels<2>(ks);
@@ -254,8 +254,13 @@ cudaError_t opt_in_smem(int device) {
     for (int iw : kSymIW) ks.push_back(sym_kernel_ptr(iw));
     ks.push_back((const void*)fp_f64_kernel);
     ks.push_back((const void*)finalize_kernel<double, 1>);
-    for (const void* k : ks)
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    for (const void* k : ks) {
+        cudaFuncAttributes fa{};
+        if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     mx - (int)fa.sharedSizeBytes);
+    }
     if (e == cudaSuccess) done[device] = true;
     return e;
 }
@@ -348,8 +353,9 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
                        cudaStream_t s) {
     const int chunks = p->fin_chunks;
     const size_t clen1 = (size_t)((p->Q + chunks - 1) / chunks + 1);
-    size_t sm = clen1 * tsize(p);
-    if (NF == 1 && p->fsym) sm = ((sm + 15) & ~(size_t)15) + clen1 * 4;  // gathered window sums
+    // residual [clen + 1], staged measurements [clen], gathered window sums [clen + 1]
+    size_t sm = ((clen1 * tsize(p) + 15) & ~(size_t)15) + (((clen1 - 1) * tsize(p) + 15) & ~(size_t)15);
+    if (NF == 1 && p->fsym) sm += clen1 * 4;
     const dim3 grid(p->M * chunks, NF);
     if (p->dtype == PK_F32) {
         FinArgs<float> a{};
@@ -917,7 +923,9 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         }
     }
     p->misc_blocks = std::max(1, std::min(1024, (p->P + kThreads - 1) / kThreads));
-    if ((size_t)p->Q * tsize(p) > 200 * 1024) {
+    // the residual kernel holds a trace, its measurements and (symmetric projector) the
+    // gathered window sums in shared memory
+    if ((size_t)(p->Q + 1) * (2 * tsize(p) + 4) + 64 > 200 * 1024) {
         free_plan(p);
         return fail(PK_ERR_UNSUPPORTED, "trace of %d samples exceeds shared memory", p->Q);
     }

@@ -165,6 +165,15 @@ __device__ __forceinline__ T warp_max(T v) {
     return v;
 }
 
+// LDGSTS: asynchronous 4- / 8-byte global -> shared copy (no register staging)
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem_dst, const void* gmem_src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src),
+                 "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // sum over the block (NT threads, 256 by default); result valid in every thread
 template <typename T, int NT = kThreads>
 __device__ __forceinline__ T block_sum(T v, T* red) {  // NT = block size (red: NT / 32 slots)

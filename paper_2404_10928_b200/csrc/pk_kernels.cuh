@@ -1557,6 +1557,8 @@ struct FinArgs {
     int chunks;          // sample chunks per sensor (one CTA each)
 };
 
+constexpr int kFinListMax = 256;  // per-trace gather lists up to this length are staged in smem
+
 template <typename T, int NF>
 __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1564,8 +1566,8 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
     __shared__ double red_d[kThreads / 32];
     __shared__ double data_s[NF], tv_s[NF];
     __shared__ int last_flag;
+    __shared__ int2 wl_s[kFinListMax];
     if (a.solver && a.st->all_stopped) return;
-    griddep_wait();  // the projection's accumulator / windows and scale
     // grid (M * chunks, NF): CTA handles samples [c0, c1) of sensor m plus the one-sample
     // halo r[c0-1] its first pair-table entry needs.  The accumulator is read-only here (it
     // is cleared by a memset before the next projection), so neighbouring chunks do not race.
@@ -1573,22 +1575,50 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
     const int m = blockIdx.x / chunks, cix = blockIdx.x % chunks, f = blockIdx.y;
     const int clen = (a.Q + chunks - 1) / chunks;
     const int c0 = cix * clen, c1 = min(a.Q, c0 + clen);
-    const double sc = sizeof(T) == 4 ? (double)a.st->fr[f].scale32 : a.st->fr[f].scale64;
-    const double wq = sc > 0.0 ? a.w / sc : 0.0;
     const T* y = a.solver ? reinterpret_cast<const T*>(a.io->y) : a.y;
     const size_t MQ = (size_t)a.M * a.Q;
     long long* accm = a.acc + (size_t)f * MQ + (size_t)m * a.Q;
     const T* ym = y ? y + f * MQ + (size_t)m * a.Q : nullptr;
     T* om = a.trace_out ? a.trace_out + f * MQ + (size_t)m * a.Q : nullptr;
+    // constant inputs are read before waiting for the projection (they overlap its tail under
+    // programmatic dependent launch): the gather list and this thread's first 8 measurements
+    const bool list_s = a.win && a.nwin <= kFinListMax;
+    if (list_s)
+        for (int q = threadIdx.x; q < a.nwin; q += kThreads) wl_s[q] = __ldg(a.win_list + (size_t)m * a.nwin + q);
+    // measurements staged in shared memory by LDGSTS (no registers held across the gather)
+    T* ys = reinterpret_cast<T*>(smem + (((size_t)(clen + 1) * sizeof(T) + 15) & ~(size_t)15));
+    if (ym) {
+        for (int k = threadIdx.x; k < c1 - c0; k += kThreads) cp_async<sizeof(T)>(ys + k, ym + c0 + k);
+        cp_async_commit();
+    }
+    griddep_wait();  // the projection's accumulator / windows and scale
+    const double sc = sizeof(T) == 4 ? (double)a.st->fr[f].scale32 : a.st->fr[f].scale64;
+    const double wq = sc > 0.0 ? a.w / sc : 0.0;
     // K x rounded to the working type first, then the residual in that type, so that y
     // produced by the same projection gives r == 0 exactly (recon.py:75-79 semantics)
-    auto resid = [&](int s, long long v) -> T {
+    auto resid_y = [&](long long v, T yvv) -> T {
         const T kx = (T)((double)v * wq);
-        return ym ? (T)(kx - ym[s]) : kx;
+        return ym ? (T)(kx - yvv) : kx;
     };
+    auto resid = [&](int s, long long v) -> T { return resid_y(v, ym ? ys[s - c0] : (T)0); };
+    double tvp = 0.0, l1p = 0.0, badp = 0.0;
+    auto tv_slice = [&]() {  // exact anisotropic TV of x' (recon.py:169-170), sum |x'|, non-finite
+        const T* x = (a.st->iter & 1) ? a.xb0 : a.xb1;  // the back-projector wrote xb[(iter+1)&1]
+        const int n = a.n, P = n * n, per = (P + gridDim.x - 1) / gridDim.x;
+        const int p1 = min(P, (int)(blockIdx.x + 1) * per);
+        for (int p = blockIdx.x * per + threadIdx.x; p < p1; p += kThreads) {
+            const T v = x[p];
+            l1p += (double)fabs(v);
+            if (!isfinite(v)) badp += 1.0;
+            if (p % n + 1 < n) tvp += (double)fabs(x[p + 1] - v);
+            if (p + n < P) tvp += (double)fabs(x[p + n] - v);
+        }
+    };
+    if (a.tv_here) tv_slice();
     // symmetric projector: trace m receives, for g = 0..3, the image-g windows of base sensor
     // m - g*M/4 from every quadrant tile; gather samples [c0 - 1, c1) in that fixed order
-    int32_t* gs = reinterpret_cast<int32_t*>(smem + (((size_t)(clen + 1) * sizeof(T) + 15) & ~(size_t)15));
+    int32_t* gs = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(ys) +
+                                             (((size_t)clen * sizeof(T) + 15) & ~(size_t)15));
     if (a.win) {
         const int LW = a.win_lw, s_lo = c0 - 1, ns = c1 - s_lo;
         for (int k = threadIdx.x; k < ns; k += kThreads) gs[k] = 0;
@@ -1597,7 +1627,7 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
         // loaded before any is added, and the adds are integer shared atomics (the sum does
         // not depend on their order: deterministic)
         const int2* wl = a.win_list + (size_t)m * a.nwin;
-        const int per = LW >> 3, items = a.nwin * per;
+        const int per = LW >> 3, items = a.nwin * per;  // (wl_s: staged before the barrier above)
         for (int base = threadIdx.x; base < items; base += 4 * kThreads) {
             int4 v[4][2];
             int sb[4];
@@ -1608,7 +1638,7 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
                 v[u][0] = v[u][1] = make_int4(0, 0, 0, 0);
                 if (it < items) {
                     const int wi = it / per, k = (it - wi * per) * 8;
-                    const int2 d = __ldg(wl + wi);
+                    const int2 d = list_s ? wl_s[wi] : __ldg(wl + wi);
                     if (d.y + k + 8 > s_lo && d.y + k < c1) {
                         const int4* src = reinterpret_cast<const int4*>(a.win + d.x + k);
                         v[u][0] = __ldcg(src);
@@ -1634,22 +1664,11 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
     auto sample = [&](int s) -> long long {
         return a.win ? (long long)gs[s - (c0 - 1)] : __ldcg(accm + s);
     };
-    double tvp = 0.0, l1p = 0.0, badp = 0.0;
-    if (a.tv_here) {  // exact anisotropic TV of x' (recon.py:169-170), sum |x'| and non-finite
-        const T* x = (a.st->iter & 1) ? a.xb0 : a.xb1;  // the back-projector wrote xb[(iter+1)&1]
-        const int n = a.n, P = n * n, per = (P + gridDim.x - 1) / gridDim.x;
-        const int p1 = min(P, (int)(blockIdx.x + 1) * per);
-        for (int p = blockIdx.x * per + threadIdx.x; p < p1; p += kThreads) {
-            const T v = x[p];
-            l1p += (double)fabs(v);
-            if (!isfinite(v)) badp += 1.0;
-            if (p % n + 1 < n) tvp += (double)fabs(x[p + 1] - v);
-            if (p + n < P) tvp += (double)fabs(x[p + n] - v);
-        }
-    }
+    if (ym) cp_async_wait_all();
+    __syncthreads();  // ys (and gs)
     double ss = 0.0;
     // tr[k] holds r[c0 - 1 + k]; 4 samples per thread per step, all loads first
-    if (threadIdx.x == 0) tr[0] = (c0 >= 1) ? resid(c0 - 1, sample(c0 - 1)) : (T)0;
+    if (threadIdx.x == 0) tr[0] = (c0 >= 1) ? resid_y(sample(c0 - 1), ym ? ym[c0 - 1] : (T)0) : (T)0;
     for (int s0 = c0 + 4 * threadIdx.x; s0 < c1; s0 += 4 * kThreads) {
         long long v[4];
         const bool full = s0 + 4 <= c1 && (s0 & 1) == 0;
