@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="sensor shards: gradient exchange over peer memory fused into the update "
                          "(pk_peer_*) or an NCCL all-reduce")
+    ap.add_argument("--sensor-streams", type=int, default=2,
+                    help="sensor shards with --exchange peer: frames in flight (one plan/stream each)")
     ap.add_argument("--sensor-frames", type=int, default=5,
                     help="frames timed through the sensor-sharded solver (N > 1, frames mode)")
     ap.add_argument("--frames", type=int, default=40, help="distinct frames cycled (> L2)")
@@ -213,8 +215,8 @@ def main():
 
     import paper_2404_10928_b200 as pk
     from paper_2404_10928_b200 import _native as N
-    from paper_2404_10928_b200.sharded import (DeviceShardOps, PeerShardSolve, SpeculativeShardSolve,
-                                                shard_range)
+    from paper_2404_10928_b200.sharded import (DeviceShardOps, PeerShardSolve, PipelinedShardSolve,
+                                                SpeculativeShardSolve, shard_range)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -267,11 +269,22 @@ def main():
                 3 + cfg.iterations * (1 + 2 + 3))
 
     if sensor_mode:
-        solver, m0, m1, launches_per_step = make_shard_solver()
+        if args.exchange == "peer":
+            # S frames in flight, one PeerShardSolve (plan, peer block, stream) each: one
+            # frame's exchange and barrier waits overlap another frame's kernels
+            made = [make_shard_solver() for _ in range(max(1, args.sensor_streams))]
+            pipe = PipelinedShardSolve([mk[0] for mk in made])
+            _, m0, m1, launches_per_step = made[0]
+        else:
+            solver, m0, m1, launches_per_step = make_shard_solver()
         Yl = Y[:, m0 * Q : m1 * Q].contiguous()
 
-        def one_step(f):
-            solver.solve(Yl[f], pinned, alpha, beta, step)
+        def run_frames(fs):
+            if args.exchange == "peer":
+                pipe.solve_frames([Yl[f] for f in fs], pinned, alpha, beta, step)
+            else:
+                for f in fs:
+                    solver.solve(Yl[f], pinned, alpha, beta, step)
     else:
         B = args.batch
         SS = max(1, args.streams)
@@ -299,22 +312,32 @@ def main():
         # symmetric back-projector), projection, residual
         launches_per_step = 3 + (4 if op.info.symmetric & 1 else 3) * cfg.iterations
 
-    frame_base = rank * 7919  # different frames per rank in frames mode
+        def run_frames(fs):
+            for f in fs:
+                one_step(f)
+
+    frame_base = rank * 7919 if not sensor_mode else 0  # different frames per rank in frames mode
 
     def frame(k):
         return (frame_base + k) % F
 
-    for k in range(args.warmup):
-        one_step(frame(k))
+    t_w = time.perf_counter()
+    run_frames([frame(k) for k in range(args.warmup)])
     torch.cuda.synchronize(dev)
+    t_w = (time.perf_counter() - t_w) / max(1, args.warmup)
 
     clocks = ClockSampler(local)
     clocks.start()
-    # keep the GPU busy while the sampler spins up, then time exactly K steps
-    t_spin = time.perf_counter()
-    while time.perf_counter() - t_spin < 0.3:
-        one_step(frame(0))
-        torch.cuda.synchronize(dev)
+    # keep the GPU busy ~0.3 s while the sampler spins up, then time exactly K steps.  The
+    # spin count is rank 0's (sensor shards run collectives per frame: every rank must run
+    # the same number of frames)
+    n_spin = torch.tensor([max(1, int(0.3 / max(t_w, 1e-4)))], dtype=torch.int64)
+    if world > 1:
+        if dist.get_backend() == "nccl":
+            n_spin = n_spin.to(dev)
+        dist.broadcast(n_spin, 0)
+    run_frames([frame(0)] * int(n_spin.item()))
+    torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -323,8 +346,7 @@ def main():
     side = [] if sensor_mode else streams[1:]
     for st_ in side:  # side streams start after e0 and are joined before e1
         st_.wait_event(e0)
-    for k in range(args.steps):
-        one_step(frame(args.warmup + k))
+    run_frames([frame(args.warmup + k) for k in range(args.steps)])
     for st_ in side:
         torch.cuda.current_stream(dev).wait_stream(st_)
     e1.record()
@@ -499,7 +521,7 @@ def main():
             "data": "synthetic: make_scene vessel phantoms (seed = frame), y = K x by the fp64 device projector",
             "config": {"workload": cfg.name, "image": f"{cfg.n}x{cfg.n}", "sensors": M, "samples": Q,
                        "iterations": cfg.iterations, "batch": B,
-                       "streams": 1 if sensor_mode else SS,
+                       "streams": (args.sensor_streams if args.exchange == "peer" else 1) if sensor_mode else SS,
                        "parallelism": (f"sensor-shard x{world} + "
                                        + ("peer-memory gradient exchange" if args.exchange == "peer"
                                           else "NCCL all-reduce") if sensor_mode

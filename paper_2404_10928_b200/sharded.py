@@ -26,7 +26,7 @@ from .device import CudaPool, operator_for
 from .solver import DIVERGENCE_STREAK, ReconConfig, solver_params
 
 __all__ = ["shard_range", "DeviceShardOps", "SensorShardedSolver", "SpeculativeShardSolve",
-           "PeerShardSolve", "FrameShardedSolver", "stop_point"]
+           "PeerShardSolve", "PipelinedShardSolve", "FrameShardedSolver", "stop_point"]
 
 
 def shard_range(count: int, rank: int, world: int) -> tuple[int, int]:
@@ -251,6 +251,7 @@ class PeerShardSolve:
         self.handle = op.peer_handle()
         self.slots = (op.peer_buffer(0), op.peer_buffer(1))
         self._use_graph, self.graph, self._key, self._params = graph, None, None, None
+        self._stream = None
         self._alpha = self._beta = 0.0
         self._tol = 0.0
 
@@ -307,6 +308,7 @@ class PeerShardSolve:
         import torch
 
         self.prepare(config, alpha, beta, step)
+        self._stream = torch.cuda.current_stream(self.y.device)
         self.y.copy_(torch.as_tensor(y_local).to(self.y.device, self.y.dtype), non_blocking=True)
         if self.graph is not None:
             self.graph.replay()
@@ -314,7 +316,9 @@ class PeerShardSolve:
             self._body()
 
     def local_data_terms(self):
-        """This rank's sum r_g^2 after 0..N iterations (synchronises)."""
+        """This rank's sum r_g^2 after 0..N iterations (waits for the launch's stream)."""
+        if self._stream is not None:
+            self._stream.synchronize()
         return self.ss.cpu().numpy()
 
     def finish(self, data_terms=None) -> ShardResult:
@@ -335,6 +339,39 @@ class PeerShardSolve:
     def solve(self, y_local, config: ReconConfig, alpha: float, beta: float, step: float) -> ShardResult:
         self.launch(y_local, config, alpha, beta, step)
         return self.finish()
+
+
+class PipelinedShardSolve:
+    """Several independent frames of a sensor-sharded solve in flight at once (SURVEY 8(e):
+    one frame's exchange overlaps another frame's compute): S ``PeerShardSolve`` instances,
+    each with its own plan, peer block and CUDA stream; frame f runs on instance f % S, and
+    its result is collected once frame f + S - 1 has been enqueued.  Every rank must call
+    ``solve_frames`` with the same number of frames (the per-frame data-term all-reduces are
+    collectives)."""
+
+    def __init__(self, solvers):
+        import torch
+
+        self.solvers = list(solvers)
+        dev = self.solvers[0].y.device
+        self.streams = [torch.cuda.Stream(dev) for _ in self.solvers]
+
+    def solve_frames(self, ys, config: ReconConfig, alpha: float, beta: float, step: float):
+        import torch
+
+        S, out, pending = len(self.solvers), [], []
+        for s in self.solvers:  # parameter upload / graph capture before anything is in flight
+            s.prepare(config, alpha, beta, step)
+        for f, y in enumerate(ys):
+            q = f % S
+            if len(pending) == S:  # instance q is about to be reused: collect its frame
+                out.append(pending.pop(0).finish())
+            self.streams[q].wait_stream(torch.cuda.current_stream(self.streams[q].device))
+            with torch.cuda.stream(self.streams[q]):
+                self.solvers[q].launch(y, config, alpha, beta, step)
+            pending.append(self.solvers[q])
+        out.extend(s.finish() for s in pending)
+        return out
 
 
 def _allreduce_host(a: np.ndarray) -> np.ndarray:

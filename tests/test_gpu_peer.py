@@ -125,8 +125,16 @@ def _ipc_worker(rank, world, port, y, cfgv, out_dir):
         s = PeerShardSolve(g, ring, ac, F32, world, rank, cfg.iterations)
         s.connect_distributed()
         res = s.solve(y[s.m0 * Q:s.m1 * Q], cfg, alpha, beta, step)
+        # three frames through two pipelined instances (graph-captured), each on its stream
+        from paper_2404_10928_b200.sharded import PipelinedShardSolve
+
+        inst = [PeerShardSolve(g, ring, ac, F32, world, rank, cfg.iterations, graph=True) for _ in range(2)]
+        for q in inst:
+            q.connect_distributed()
+        frames = PipelinedShardSolve(inst).solve_frames([y[s.m0 * Q:s.m1 * Q]] * 3, cfg, alpha, beta, step)
+        same = all(np.array_equal(fr.image, res.image) for fr in frames)
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), image=res.image, hist=res.history,
-                 meta=np.array([res.iterations_run]))
+                 meta=np.array([res.iterations_run, int(same)]))
         dist.barrier()  # keep every block mapped until all ranks are done
     finally:
         dist.destroy_process_group()
@@ -134,7 +142,8 @@ def _ipc_worker(rank, world, port, y, cfgv, out_dir):
 
 def test_peer_shards_two_processes_ipc(oracle, tmp_path):
     """Two processes on cuda:0 map each other's blocks through CUDA IPC (the one-process-
-    per-GPU production layout, here time-sliced on one device); handles go over gloo."""
+    per-GPU production layout, here time-sliced on one device); handles go over gloo.  Each
+    rank then runs three frames through two pipelined, graph-captured instances."""
     import torch.multiprocessing as mp
 
     g, ring, ac, y, alpha, beta, step = _problem(oracle)
@@ -155,6 +164,7 @@ def test_peer_shards_two_processes_ipc(oracle, tmp_path):
     assert codes == [0, 0], codes
     a, b = (np.load(os.path.join(tmp_path, f"rank{r}.npz")) for r in range(2))
     assert np.array_equal(a["image"], b["image"])
+    assert a["meta"][1] == 1 and b["meta"][1] == 1  # pipelined frames == the single solve
     from paper_2404_10928_b200.sharded import ShardResult
 
     _check(ShardResult(a["image"], a["hist"], int(a["meta"][0]), ref.stopped_by), ref)
