@@ -132,9 +132,10 @@ class DeviceOperator:
         torch = _torch()
         if isinstance(a, torch.Tensor):
             return a.to(device=self.device, dtype=self.tdtype).contiguous()
-        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(
-            device=self.device, dtype=self.tdtype
-        ).contiguous()
+        h = np.ascontiguousarray(a, dtype=np.float64)
+        if not h.flags.writeable:  # the reference's containers are read-only (forward.py:145)
+            h = h.copy()
+        return torch.from_numpy(h).to(device=self.device, dtype=self.tdtype).contiguous()
 
     def empty(self, n: int):
         torch = _torch()
