@@ -1238,20 +1238,53 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
     // word (g, k, lane) at (g*LW + k)*32 + lane, k = t - lo for trace index t
     const uint32_t adj = win_s + 4u * (uint32_t)lane - 128u * (uint32_t)lo - 128u * kTwo23Bits;
     {   // every window slot starts at -count * bias (see fp_sym_count_kernel)
+        // all of this thread's count loads are in flight before the first store
         const int4* c4 = reinterpret_cast<const int4*>(a.counts + (size_t)u * LW * 32);
         int4* w4 = reinterpret_cast<int4*>(win);
-        for (int q = threadIdx.x; q < LW * 8; q += kFsThreads) {
-#if PK_K2X == 7
-            int4 c = make_int4(q, 0, 0, 0);
-#else
-            int4 c = __ldg(c4 + q);
-#endif
-            c.x *= -kMagicBits; c.y *= -kMagicBits; c.z *= -kMagicBits; c.w *= -kMagicBits;
+        constexpr int NQ = (LW * 8 + kFsThreads - 1) / kFsThreads;
+        int4 c[NQ];
 #pragma unroll
-            for (int g = 0; g < 4; ++g) w4[g * LW * 8 + q] = c;
+        for (int i = 0; i < NQ; ++i) {
+            const int q = threadIdx.x + i * kFsThreads;
+#if PK_K2X == 7
+            c[i] = make_int4(q, 0, 0, 0);
+#else
+            c[i] = q < LW * 8 ? __ldg(c4 + q) : make_int4(0, 0, 0, 0);
+#endif
+        }
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) {
+            const int q = threadIdx.x + i * kFsThreads;
+            if (q < LW * 8) {
+                int4 v = c[i];
+                v.x *= -kMagicBits; v.y *= -kMagicBits; v.z *= -kMagicBits; v.w *= -kMagicBits;
+#pragma unroll
+                for (int g = 0; g < 4; ++g) w4[g * LW * 8 + q] = v;
+            }
         }
     }
     griddep_wait();  // x' and its fixed-point scale come from the back-projector epilogue
+    // pieces pc = (row warp + 16*(pc / P2), 32-pixel piece pc % P2) of this warp; the 4 image
+    // values of the next piece are loaded while the current one scatters
+    constexpr int P2 = T / 32;
+    constexpr int NW = kFsThreads / 32;
+    auto piece_x = [&](int pc, float (&v)[4]) {
+        const int jj = j0 + warp + NW * (pc / P2);
+        const int ii = i0 + 32 * (pc % P2) + lane;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) v[g] = 0.f;
+        if (jj < jend && ii < n && xr) {  // one coalesced 16-B load for the 4 images
+            const float4 q = xr[(jj - h) * h + (ii - h)];
+            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        } else if (jj < jend && ii < n) {
+            v[0] = x[jj * n + ii];
+            v[1] = x[ii * n + (n - 1 - jj)];
+            v[2] = x[(n - 1 - jj) * n + (n - 1 - ii)];
+            v[3] = x[(n - 1 - ii) * n + jj];
+        }
+    };
+    float xn[4];
+    piece_x(0, xn);  // the first piece's loads overlap the scale reduction below
     float scale;
     if (a.part_mx) {  // deferred statistics: every CTA reduces the epilogue's max partials
         __shared__ float red_f[kFsThreads / 32];
@@ -1275,27 +1308,6 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
 #if PK_K2X == 1
     uint32_t k2x_sink = 0;
 #endif
-    // pieces pc = (row warp + 16*(pc / P2), 32-pixel piece pc % P2) of this warp; the 4 image
-    // values of the next piece are loaded while the current one scatters
-    constexpr int P2 = T / 32;
-    constexpr int NW = kFsThreads / 32;
-    auto piece_x = [&](int pc, float (&v)[4]) {
-        const int jj = j0 + warp + NW * (pc / P2);
-        const int ii = i0 + 32 * (pc % P2) + lane;
-#pragma unroll
-        for (int g = 0; g < 4; ++g) v[g] = 0.f;
-        if (jj < jend && ii < n && xr) {  // one coalesced 16-B load for the 4 images
-            const float4 q = xr[(jj - h) * h + (ii - h)];
-            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-        } else if (jj < jend && ii < n) {
-            v[0] = x[jj * n + ii];
-            v[1] = x[ii * n + (n - 1 - jj)];
-            v[2] = x[(n - 1 - jj) * n + (n - 1 - ii)];
-            v[3] = x[(n - 1 - ii) * n + jj];
-        }
-    };
-    float xn[4];
-    piece_x(0, xn);
     for (int pc = 0; j0 + warp + NW * (pc / P2) < jend; ++pc) {
         const int jj = j0 + warp + NW * (pc / P2);
         const int ii = i0 + 32 * (pc % P2) + lane;
@@ -1376,23 +1388,27 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
     griddep_launch_dependents();
     __syncthreads();
 
-    // store: a warp takes blocks of 8 slots of one image; 8 row reads (lane = sensor,
-    // conflict free) leave lane l holding 8 consecutive slots of its sensor's window, written
-    // as two 16-B stores to win[unit][g][l][k0..k0+7]
+    // store to win[unit][g][sensor][slot]: a warp instruction writes whole 32-B sectors,
+    // 8 slots of 16 sensors (lane l: sensor sh*16 + (l & 15), half l >> 4 of the 8-slot
+    // block; a sensor's window is LW*4 B, a multiple of 32).  Writing 16 B per sensor per
+    // instruction instead left every sector half-written by each of two requests.  The two
+    // lanes of a sensor read the same bank (2-way conflict, a small phase).
     {
+        static_assert(LW % 8 == 0, "window length must be whole 32-B sectors");
         constexpr int NB = LW / 8;
-        int32_t* dst0 = a.win + (size_t)u * 4 * 32 * LW + (size_t)lane * LW;
+        int32_t* dst0 = a.win + (size_t)u * 4 * 32 * LW;
 #if PK_K2X == 6
         if (win[threadIdx.x] != 0x12345) return;
 #endif
-        for (int blk = warp; blk < 4 * NB; blk += NW) {
-            const int g = blk / NB, k0 = (blk - g * NB) * 8;
-            int v[8];
+        const int hf = lane >> 4;
+        for (int blk = warp; blk < 8 * NB; blk += NW) {
+            const int gb = blk >> 1, s = (blk & 1) * 16 + (lane & 15);
+            const int g = gb / NB, k0 = (gb - g * NB) * 8 + 4 * hf;
+            int v[4];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) v[i] = win[(g * LW + k0 + i) * 32 + lane];
-            int4* d = reinterpret_cast<int4*>(dst0 + (size_t)g * 32 * LW + k0);
-            __stcg(d, make_int4(v[0], v[1], v[2], v[3]));
-            __stcg(d + 1, make_int4(v[4], v[5], v[6], v[7]));
+            for (int i = 0; i < 4; ++i) v[i] = win[(g * LW + k0 + i) * 32 + s];
+            __stcg(reinterpret_cast<int4*>(dst0 + ((size_t)g * 32 + s) * LW + k0),
+                   make_int4(v[0], v[1], v[2], v[3]));
         }
     }
 }
