@@ -37,7 +37,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CFG_CHOICES = ["cfg1", "cfg2", "cfg3", "cfg5"]
+CFG_CHOICES = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"]
 METRIC = "frames/s"
 
 
@@ -234,20 +234,29 @@ def main():
 
     grid, ring, ac, ph0 = pk.make_scene(cfg.n, cfg.sensors, cfg.samples, seed=0)
     M, Q, P = cfg.sensors, cfg.samples, cfg.pixels
-    F = max(1, args.frames)
     sensor_mode = world > 1 and args.shard == "sensors"
+    # BASELINE config 4: a dynamic sequence of cfg.frames frames sharded across the ranks (no
+    # collective); a step is one pass over this rank's share, total work fixed (strong scaling)
+    seq = cfg.frames > 1 and not sensor_mode
+    if seq:
+        sq0, sq1 = shard_range(cfg.frames, rank, world)
+        F = sq1 - sq0
+    else:
+        sq0, F = 0, max(1, args.frames)
 
     # synthetic frames: vessel phantoms (seeds = frame index), measurements by the fp64
     # device projector; pinned regularisation from frame 0 (outside timing, bench.py:226)
     op64 = pk.operator_for(grid, ring, ac, pk.CudaPool(local, "float64"))
     Ys = []
-    for f in range(F):
+    for f in range(sq0, sq0 + F):
         phf = ph0 if f == 0 else pk.make_vessel_phantom(grid, f)
         Ys.append(op64.matvec(phf.values).float())
     Y = torch.stack(Ys)  # [F, M*Q] fp32 on the device
     del Ys
     K64 = pk.build_time_matrix(grid, ring, ac)
-    y0 = pk.SensorData("time", M, Q, Y[0].double().cpu().numpy())
+    # the pinned regularisation is frame 0's on every rank
+    y0 = pk.SensorData("time", M, Q, (Y[0] if sq0 == 0 else op64.matvec(ph0.values).float())
+                       .double().cpu().numpy())
     pinned = pk.resolve_config(pk.ReconConfig(iterations=cfg.iterations), K64, y0,
                                pool=pk.CudaPool(local, "float64"))
     alpha, beta, step = pinned.alpha, pinned.beta, pinned.step
@@ -316,15 +325,17 @@ def main():
             for f in fs:
                 one_step(f)
 
-    frame_base = rank * 7919 if not sensor_mode else 0  # different frames per rank in frames mode
+    # different frames per rank in frames mode (seq: each rank owns its share already)
+    frame_base = rank * 7919 if not (sensor_mode or seq) else 0
+    per_step = F if seq else 1  # frames per step and rank
 
     def frame(k):
         return (frame_base + k) % F
 
     t_w = time.perf_counter()
-    run_frames([frame(k) for k in range(args.warmup)])
+    run_frames([frame(k) for k in range(args.warmup * per_step)])
     torch.cuda.synchronize(dev)
-    t_w = (time.perf_counter() - t_w) / max(1, args.warmup)
+    t_w = (time.perf_counter() - t_w) / max(1, args.warmup * per_step)
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -346,7 +357,7 @@ def main():
     side = [] if sensor_mode else streams[1:]
     for st_ in side:  # side streams start after e0 and are joined before e1
         st_.wait_event(e0)
-    run_frames([frame(args.warmup + k) for k in range(args.steps)])
+    run_frames([frame(args.warmup + k) if not seq else k % F for k in range(args.steps * per_step)])
     for st_ in side:
         torch.cuda.current_stream(dev).wait_stream(st_)
     e1.record()
@@ -360,7 +371,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t[0])
     B = 1 if sensor_mode else args.batch
-    frames_total = args.steps * B * (1 if sensor_mode else world)
+    frames_total = (args.steps * cfg.frames if seq
+                    else args.steps * B * (1 if sensor_mode else world))
     fps = frames_total / (ms_max * 1e-3)
     ms_step = ms_max / args.steps
 
@@ -427,7 +439,7 @@ def main():
     # ---- end to end through the C-ABI host-buffer entry ----
     e2e = None
     if not args.no_e2e and not sensor_mode:
-        nF = min(n_steps_in, 4)
+        nF = min(n_steps_in, 64 if seq else 4)
         yh = torch.empty((nF, B * M * Q), dtype=torch.float64, pin_memory=True)
         yh.copy_(Y[:nF * B].reshape(nF, B * M * Q).double().cpu())
         yh_np = yh.numpy()
@@ -452,7 +464,7 @@ def main():
         ee0.record()
         for st_ in streams[1:]:
             st_.wait_event(ee0)
-        for k in range(args.steps):
+        for k in range(args.steps * per_step):
             host_step(k)
         for st_ in streams[1:]:
             torch.cuda.current_stream(dev).wait_stream(st_)
@@ -463,15 +475,19 @@ def main():
             te = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
             ms_e2e = float(te[0])
-        e2e = {"value": args.steps * B * world / (ms_e2e * 1e-3), "unit": "frames/s",
+        e2e = {"value": frames_total / (ms_e2e * 1e-3), "unit": "frames/s",
                "h2d_bytes_per_step": B * M * Q * 8,
                "d2h_bytes_per_step": B * (P * 8 + 4 * cfg.iterations * 8 + 8),
                "ms_per_step": ms_e2e / args.steps,
-               "path": f"pk_reconstruct_host_async (C ABI, pinned fp64 host buffers, {SS} stream(s))"}
+               "path": f"pk_reconstruct_host_async (C ABI, pinned fp64 host buffers, {SS} stream(s))"
+                       + (f"; {nF} host frames cycled, per-frame copies" if seq else "")}
+        if seq:
+            e2e["h2d_bytes_per_step"] *= per_step
+            e2e["d2h_bytes_per_step"] *= per_step
 
     # ---- sensor-sharded single-frame latency (BASELINE config 3 at N > 1) ----
     sensor_sharded = None
-    if world > 1 and not sensor_mode and args.sensor_frames > 0:
+    if world > 1 and not sensor_mode and not seq and args.sensor_frames > 0:
         ssolver, m0, m1, _ = make_shard_solver()
         Yl = Y[:2, m0 * Q: m1 * Q].contiguous()
         ssolver.solve(Yl[0], pinned, alpha, beta, step)  # warm-up (plan, NCCL communicators)
@@ -513,10 +529,10 @@ def main():
         line = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "ms_per_iteration": ms_step / (cfg.iterations * B),  # per frame, amortised over the batch
+            "ms_per_iteration": ms_step / (cfg.iterations * B * per_step),  # per frame, amortised
             "latency_ms_per_step": ms_step,
             "higher_is_better": True,
-            "scaling": "strong" if sensor_mode else ("weak" if world > 1 else "none"),
+            "scaling": "strong" if (sensor_mode or seq) else ("weak" if world > 1 else "none"),
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: make_scene vessel phantoms (seed = frame), y = K x by the fp64 device projector",
             "config": {"workload": cfg.name, "image": f"{cfg.n}x{cfg.n}", "sensors": M, "samples": Q,
@@ -527,9 +543,12 @@ def main():
                                           else "NCCL all-reduce") if sensor_mode
                                        else f"frames x{world}" if world > 1 else "single GPU"),
                        "l2": f"{F} distinct frames cycled ({F * M * Q * 4 / 2**20:.0f} MiB of y > 126 MB L2)",
+                       **({"sequence": f"{cfg.frames} frames (seeds 0..{cfg.frames - 1}) sharded "
+                                       f"{F} per rank; a step is one pass over the rank's share"}
+                          if seq else {}),
                        "pinned": {"alpha": alpha, "beta": beta, "step": step}},
             "clocks": clk,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": launches_per_step * args.steps * per_step,
             "roofline": roof,
             "kernels": kernels,
             "cpu_baseline": cpu,
