@@ -327,7 +327,7 @@ def main():
 
     # different frames per rank in frames mode (seq: each rank owns its share already)
     frame_base = rank * 7919 if not (sensor_mode or seq) else 0
-    per_step = F if seq else 1  # frames per step and rank
+    per_step = max(1, F // args.batch) if seq else 1  # solves (of B frames) per step and rank
 
     def frame(k):
         return (frame_base + k) % F
