@@ -432,6 +432,8 @@ def main():
                                     "projector (floor 2 clk / 32 pairs), LDS.64 per pair in the "
                                     "back-projector (2 wavefronts / 32 pairs)",
                 "smem_floor_us": 2.0 * M * P / 32.0 / (148 * 1.965e3),
+                # the same kernel against its binding resource: the floor above over its time
+                "smem_pipe_frac": (2.0 * M * P / 32.0 / (148 * 1.965e3)) / (per_launch_ms[dom] * 1e3),
                 "hbm": {"achieved_GBs": (traffic / t_dom / 1e9) if traffic else None,
                         "peak_GBs": hbm_peak, "peak_source": hbm_src,
                         "frac": (traffic / t_dom / 1e9 / hbm_peak) if traffic else None}}
