@@ -353,9 +353,9 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
                        cudaStream_t s) {
     const int chunks = p->fin_chunks;
     const size_t clen1 = (size_t)((p->Q + chunks - 1) / chunks + 1);
-    // residual [clen + 1], staged measurements [clen], gathered window sums [clen + 1]
+    // residual [clen + 1], staged measurements [clen], gathered window sums [clen + 1] (padded)
     size_t sm = ((clen1 * tsize(p) + 15) & ~(size_t)15) + (((clen1 - 1) * tsize(p) + 15) & ~(size_t)15);
-    if (NF == 1 && p->fsym) sm += clen1 * 4;
+    if (NF == 1 && p->fsym) sm += (clen1 + clen1 / 8 + 2) * 4;  // padded by one word per 8
     const dim3 grid(p->M * chunks, NF);
     if (p->dtype == PK_F32) {
         FinArgs<float> a{};

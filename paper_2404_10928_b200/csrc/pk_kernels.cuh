@@ -1637,48 +1637,54 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
                                              (((size_t)clen * sizeof(T) + 15) & ~(size_t)15));
     if (a.win) {
         const int LW = a.win_lw, s_lo = c0 - 1, ns = c1 - s_lo;
-        for (int k = threadIdx.x; k < ns; k += kThreads) gs[k] = 0;
+        // gs is padded by one word per 8 entries (index j -> j + j/8): lanes that add entries
+        // 8 apart then hit banks 9 apart (conflict free) instead of 4 banks (8-way conflicts)
+        for (int k = threadIdx.x; k < ns + (ns >> 3) + 1; k += kThreads) gs[k] = 0;
         __syncthreads();
-        // work item = (window, 8 consecutive entries): two 16-B loads; 4 items per thread are
-        // loaded before any is added, and the adds are integer shared atomics (the sum does
-        // not depend on their order: deterministic)
+        // a warp takes whole windows (list order w, w + 8, ...; two at a time so four 16-B loads
+        // per lane are in flight); lane c adds entries 8c..8c+7 of the window.  The window's
+        // start sb is warp-uniform, so the padded address of entry 8c + q is
+        // (sb + q + (sb + q)/8) + 9c: one add per atomic.  Integer adds commute: the sum is
+        // deterministic.  Windows wholly inside the chunk skip the per-entry range checks.
         const int2* wl = a.win_list + (size_t)m * a.nwin;
-        const int per = LW >> 3, items = a.nwin * per;  // (wl_s: staged before the barrier above)
-        for (int base = threadIdx.x; base < items; base += 4 * kThreads) {
-            int4 v[4][2];
-            int sb[4];
+        const int per = LW >> 3;  // (wl_s: staged before the barrier above)
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        constexpr int kW = kThreads / 32;
+        auto add_window = [&](const int4 (&v)[2], int sb, int c) {
+            const int e[8] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y, v[1].z, v[1].w};
+            const bool inside = sb >= 0 && sb + LW <= ns;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int it = base + u * kThreads;
-                sb[u] = INT_MIN;
-                v[u][0] = v[u][1] = make_int4(0, 0, 0, 0);
-                if (it < items) {
-                    const int wi = it / per, k = (it - wi * per) * 8;
-                    const int2 d = list_s ? wl_s[wi] : __ldg(wl + wi);
-                    if (d.y + k + 8 > s_lo && d.y + k < c1) {
-                        const int4* src = reinterpret_cast<const int4*>(a.win + d.x + k);
-                        v[u][0] = __ldcg(src);
-                        v[u][1] = __ldcg(src + 1);
-                        sb[u] = d.y + k - s_lo;
-                    }
-                }
+            for (int q = 0; q < 8; ++q) {
+                const int jq = sb + q;
+                const int jp = jq + (jq >> 3) + 9 * c;  // padded index of entry 8c + q
+                const int j = jq + 8 * c;
+                if (inside || (j >= 0 && j < ns)) atomicAdd(gs + jp, e[q]);
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (sb[u] == INT_MIN) continue;
-                const int e[8] = {v[u][0].x, v[u][0].y, v[u][0].z, v[u][0].w,
-                                  v[u][1].x, v[u][1].y, v[u][1].z, v[u][1].w};
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int j = sb[u] + q;
-                    if (e[q] != 0 && j >= 0 && j < ns) atomicAdd(gs + j, e[q]);
+        };
+        for (int w0 = wid; w0 < a.nwin; w0 += 2 * kW) {
+            const int w1 = w0 + kW;
+            const int2 d0 = list_s ? wl_s[w0] : __ldg(wl + w0);
+            const int2 d1 = w1 < a.nwin ? (list_s ? wl_s[w1] : __ldg(wl + w1)) : make_int2(0, INT_MIN);
+            for (int c = lane; c < per; c += 32) {
+                int4 v0[2], v1[2];
+                const int4* s0p = reinterpret_cast<const int4*>(a.win + d0.x + 8 * c);
+                v0[0] = __ldcg(s0p);
+                v0[1] = __ldcg(s0p + 1);
+                const bool has1 = d1.y != INT_MIN;
+                if (has1) {
+                    const int4* s1p = reinterpret_cast<const int4*>(a.win + d1.x + 8 * c);
+                    v1[0] = __ldcg(s1p);
+                    v1[1] = __ldcg(s1p + 1);
                 }
+                add_window(v0, d0.y - s_lo, c);
+                if (has1) add_window(v1, d1.y - s_lo, c);
             }
         }
         __syncthreads();
     }
     auto sample = [&](int s) -> long long {
-        return a.win ? (long long)gs[s - (c0 - 1)] : __ldcg(accm + s);
+        const int j = s - (c0 - 1);
+        return a.win ? (long long)gs[j + (j >> 3)] : __ldcg(accm + s);
     };
     if (ym) cp_async_wait_all();
     __syncthreads();  // ys (and gs)
