@@ -167,7 +167,8 @@ def test_reconstruction_vs_golden(sc, pool):
             assert rel(res.image.values, gold[f"{name}_image"]) <= IMG_TOL[pool.dtype], name
             h = np.stack([res.objective_history, res.data_term_history, res.l1_history,
                           res.tv_history])
-            np.testing.assert_allclose(h, gold[f"{name}_hist"], rtol=IMG_TOL[pool.dtype] * 10,
+            # histories (F, data, l1, tv) within 1e-4 relative in fp32
+            np.testing.assert_allclose(h, gold[f"{name}_hist"], rtol=IMG_TOL[pool.dtype],
                                        atol=1e-300)
         if name == "nonneg":
             assert res.image.values.min() >= 0.0
@@ -212,7 +213,8 @@ def test_large_config_vs_oracle(oracle, cfg):
     err = rel(res.image.values, ref["image"])
     print(f"cfg {cfg}: fp32 relative L2 image error vs fp64 oracle = {err:.3e}")
     assert err <= 1e-4
-    np.testing.assert_allclose(res.data_term_history, ref["data_term_history"], rtol=1e-4)
+    for key in ("objective_history", "data_term_history", "l1_history", "tv_history"):
+        np.testing.assert_allclose(getattr(res, key), ref[key], rtol=1e-4, err_msg=key)
 
 
 def test_zero_signal_fixed_point():
