@@ -52,6 +52,7 @@ from .solver import (
     tv_value,
 )
 from .fileio import read_matrix, read_signal, write_matrix, write_signal
+from .harness import BenchEntry, BenchReport, bench_recon, profile_breakdown
 from .workloads import CONFIGS, make_scene
 
 __version__ = "1.0.0"

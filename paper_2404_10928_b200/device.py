@@ -13,6 +13,7 @@ plumbing here, the arithmetic is in libpactgpu.so.
 from __future__ import annotations
 
 import ctypes
+import warnings
 import threading
 from dataclasses import dataclass
 
@@ -133,9 +134,12 @@ class DeviceOperator:
         if isinstance(a, torch.Tensor):
             return a.to(device=self.device, dtype=self.tdtype).contiguous()
         h = np.ascontiguousarray(a, dtype=np.float64)
-        if not h.flags.writeable:  # the reference's containers are read-only (forward.py:145)
-            h = h.copy()
-        return torch.from_numpy(h).to(device=self.device, dtype=self.tdtype).contiguous()
+        with warnings.catch_warnings():
+            # the reference's containers are read-only (forward.py:145); the tensor is only
+            # read (copied to the device), so no host copy is made to silence torch
+            warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
+            t = torch.from_numpy(h)
+        return t.to(device=self.device, dtype=self.tdtype).contiguous()
 
     def empty(self, n: int):
         torch = _torch()
@@ -252,7 +256,9 @@ class DeviceOperator:
             params = [params] * self.frames
         if len(params) != self.frames:
             raise ValueError(f"need {self.frames} parameter sets, got {len(params)}")
-        arr = (N.SolverParams * self.frames)(*params)
+        if getattr(self, "_params_t", None) is None:  # one ctypes array type per operator
+            self._params_t = N.SolverParams * self.frames  # (a new type per call is cyclic garbage)
+        arr = self._params_t(*params)
         return arr, int(params[0].iterations)
 
     def reconstruct(self, y, params):
@@ -271,6 +277,19 @@ class DeviceOperator:
             N.check(self._lib.pk_reconstruct(self._h, arr, yt.data_ptr(), x.data_ptr(),
                                              hist.data_ptr(), status.data_ptr(), self.stream()))
         return x.view(F, self.pixels), hist.view(F, 4, n), status.view(F, 2)
+
+    def profile_iterations(self, y, params):
+        """Un-graphed solver kernels with CUDA events around each launch (pk_profile_iterations):
+        summed device seconds of K1 (back-projection with the fused TV/prox update), K2
+        (projection), K3 (residual/objective), and the number of launches."""
+        arr, _ = self._params(params)
+        yt = self.tensor(y)
+        ms = (ctypes.c_float * 3)()
+        n = ctypes.c_int32()
+        with _torch().cuda.device(self.device):
+            N.check(self._lib.pk_profile_iterations(self._h, arr, yt.data_ptr(), ms, ctypes.byref(n),
+                                                    self.stream()))
+        return [v * 1e-3 for v in ms], int(n.value)
 
     def reconstruct_host(self, y_host: np.ndarray, params):
         """The C-ABI host-buffer entry (pk_reconstruct_host): fp64 in, fp64 out, synchronous."""

@@ -1,0 +1,218 @@
+"""The reference's benchmark / profiling harness with the device path plugged in
+(reference ``pactkit/bench.py:44-340``).
+
+``bench_recon`` and ``profile_breakdown`` keep the reference's signatures (plus a ``device``
+argument in place of ``workers``), report types and conventions: wall times are the
+minimum over repetitions of the public API calls (host<->device copies included), every
+timed image carries a content checksum, and the fast result is verified against a slower
+one before its time is reported.  The reference verifies its parallel numba image against
+the serial one (<= 1e-12, ``bench.py:230-234``); here the fp32 production solver is
+verified against the fp64 validation solver on the same device at the north-star tolerance
+(relative L2 <= 1e-4).  There is no CPU path.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .device import CudaPool, operator_for
+from .measurement import build_time_matrix, forward_project
+from .solver import ReconConfig, back_project, iterative_reconstruct, resolve_config, solver_params
+from .workloads import make_scene
+
+__all__ = ["BenchEntry", "BenchReport", "MEASUREMENT_FLOOR_SECONDS", "bench_recon",
+           "profile_breakdown"]
+
+MEASUREMENT_FLOOR_SECONDS = 1e-4  # bench.py:30-31
+# published timings of the 127x127 study the reference's ratio checks are calibrated
+# against (bench.py:33-41); echoed, never asserted
+REFERENCE_TIMES = {"bp_seconds": 2.277, "ir_cpu_seconds": 118.470, "ir_gpu_seconds": 20.062,
+                   "gpu_speedup": 5.9, "gradient_share_percent": 96.7}
+VERIFY_REL_L2 = 1e-4  # north_star: fp32 image within 1e-4 relative L2 of the fp64 result
+
+
+def _sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _best_of(fn, reps: int) -> float:
+    best = float("inf")
+    for _ in range(max(1, reps)):
+        t0 = time.perf_counter()
+        fn()
+        best = min(best, time.perf_counter() - t0)
+    return best
+
+
+def _rel_l2(a: np.ndarray, b: np.ndarray) -> float:
+    nb = float(np.linalg.norm(b))
+    return float(np.linalg.norm(a - b)) / nb if nb > 0 else float(np.linalg.norm(a))
+
+
+@dataclass(frozen=True)
+class BenchEntry:
+    """One timed call (bench.py:64-70)."""
+    label: str
+    wall_seconds: float
+    repetitions: int
+    checksum: str
+    verification: bool | None = None  # None: the baseline an entry is verified against
+
+
+@dataclass
+class BenchReport:
+    """Timings, speed-ups, environment and metrics of one scenario (bench.py:73-125)."""
+    scenario: str
+    entries: list = field(default_factory=list)
+    speedups: list = field(default_factory=list)
+    environment: dict = field(default_factory=dict)
+    metrics: dict = field(default_factory=dict)
+    breakdown: dict = field(default_factory=dict)
+
+    def entry(self, label: str) -> BenchEntry:
+        hit = [e for e in self.entries if e.label == label]
+        if not hit:
+            raise KeyError(f"no entry labelled {label!r}")
+        return hit[0]
+
+    def speedup(self, baseline: str, candidate: str) -> float:
+        hit = [s for s in self.speedups if (s["baseline"], s["candidate"]) == (baseline, candidate)]
+        if not hit:
+            raise KeyError(f"no speedup {baseline!r} -> {candidate!r}")
+        return hit[0]["speedup"]
+
+    def verification_ok(self) -> bool:
+        return not any(e.verification is False for e in self.entries)
+
+    def to_dict(self) -> dict:
+        return {"scenario": self.scenario, "entries": [vars(e) for e in self.entries],
+                "speedups": self.speedups, "environment": self.environment,
+                "metrics": self.metrics, "breakdown": self.breakdown,
+                "verification": self.verification_ok()}
+
+    def to_json(self) -> str:
+        return json.dumps(self.to_dict(), indent=2)
+
+    def to_text(self) -> str:
+        w = max([len(e.label) for e in self.entries] + [8])
+        out = [f"scenario: {self.scenario}", f"{'entry':<{w}}  {'time (s)':>12}  {'reps':>4}  verified"]
+        for e in self.entries:
+            v = "-" if e.verification is None else ("yes" if e.verification else "NO")
+            out.append(f"{e.label:<{w}}  {e.wall_seconds:>12.6f}  {e.repetitions:>4}  {v}")
+        for s in self.speedups:
+            floor = "  (below measurement floor)" if s.get("below_measurement_floor") else ""
+            out.append(f"speedup {s['baseline']} -> {s['candidate']}: {s['speedup']:.2f}x{floor}")
+        for cat, row in self.breakdown.items():
+            out.append(f"{cat}: {row['seconds']:.4f} s  {row['percent']:.1f}%")
+        out += [f"{k}: {v}" for k, v in self.metrics.items()]
+        return "\n".join(out) + "\n"
+
+
+def _environment(device: int, **dims) -> dict:
+    import torch
+
+    prop = torch.cuda.get_device_properties(device)
+    return {"device": prop.name, "multiprocessors": prop.multi_processor_count,
+            "timing_floor_seconds": MEASUREMENT_FLOOR_SECONDS, **dims}
+
+
+def _scene(grid_size, sensors, samples, seed, config, device):
+    grid, ring, ac, phantom = make_scene(grid_size, sensors, samples, seed)
+    K = build_time_matrix(grid, ring, ac)
+    f64 = CudaPool(device, "float64")
+    y = forward_project(K, phantom, pool=f64)  # fp64 device projector (bench.py:222)
+    return grid, ring, ac, phantom, K, y, resolve_config(config, K, y, pool=f64)
+
+
+def bench_recon(grid_size: int, sensors: int, samples: int, config: ReconConfig, reps: int = 5,
+                seed: int = 0, device: int = 0) -> BenchReport:
+    """Back-projection against iterative reconstruction on one scene (bench.py:206-288), on
+    the device: entries back_projection (fp32), iterative_device_f64 (the fp64 validation
+    solver, the baseline) and iterative_device (fp32, verified against it)."""
+    grid, ring, ac, phantom, K, y, config = _scene(grid_size, sensors, samples, seed, config, device)
+    f32, f64 = CudaPool(device, "float32"), CudaPool(device, "float64")
+
+    bp = back_project(K, y, pool=f32)
+    t_bp = _best_of(lambda: back_project(K, y, pool=f32), reps)
+    ir64 = iterative_reconstruct(K, y, config, pool=f64)
+    t_64 = _best_of(lambda: iterative_reconstruct(K, y, config, pool=f64), reps)
+    ir32 = iterative_reconstruct(K, y, config, pool=f32)
+    dev = _rel_l2(ir32.image.values, ir64.image.values)
+    t_32 = _best_of(lambda: iterative_reconstruct(K, y, config, pool=f32), reps)
+
+    truth = phantom.values / max(float(np.max(np.abs(phantom.values))), 1e-300)
+
+    def norm_rmse(v):  # bench.py:243-248
+        peak = float(np.max(np.abs(v)))
+        return float(np.sqrt(np.mean(((v / peak if peak > 0 else v) - truth) ** 2)))
+
+    rep = BenchReport(
+        scenario=f"recon {grid_size}x{grid_size}, {sensors} sensors, {samples} samples",
+        environment=_environment(device, grid=[grid_size, grid_size], sensors=sensors,
+                                 samples=samples, matrix_shape=[K.rows, K.cols],
+                                 scalar_kind="real32 (verified against real64)",
+                                 iterations=config.iterations),
+        metrics={"rmse_bp": norm_rmse(bp.values), "rmse_ir": norm_rmse(ir32.image.values),
+                 "rel_l2_f32_vs_f64": dev, "reference_times": REFERENCE_TIMES})
+    rep.entries += [BenchEntry("back_projection", t_bp, reps, _sha(bp.values)),
+                    BenchEntry("iterative_device_f64", t_64, reps, _sha(ir64.image.values)),
+                    BenchEntry("iterative_device", t_32, reps, _sha(ir32.image.values),
+                               dev <= VERIFY_REL_L2)]
+    for base, cand, tb, tc in (("back_projection", "iterative_device", t_bp, t_32),
+                               ("iterative_device_f64", "iterative_device", t_64, t_32)):
+        rep.speedups.append({"baseline": base, "candidate": cand, "speedup": tb / tc,
+                             "below_measurement_floor": min(tb, tc) < MEASUREMENT_FLOOR_SECONDS})
+    rep.metrics["ir_over_bp_time_ratio"] = t_32 / t_bp
+    return rep
+
+
+def profile_breakdown(grid_size: int, sensors: int, samples: int, config: ReconConfig,
+                      seed: int = 0, device: int = 0) -> BenchReport:
+    """Attribute one iterative run's time to its stages (bench.py:291-340), on the device.
+
+    The total is the wall time of the public ``iterative_reconstruct`` call (best of 3: host
+    copies, the graphed solve, the read-back).  The stage times are device times of the same
+    kernels launched un-graphed with CUDA events around each launch (pk_profile_iterations):
+    gradient_products = back-projection + projection kernels, objective = the
+    residual/objective kernel, other = the rest of the wall time (copies, launch, sync).
+    The TV gradient and the prox have no kernels of their own (they run in the
+    back-projection's epilogue) and are counted in gradient_products.  Percentages sum to
+    100 (over the larger of the wall time and the summed kernel time).
+    """
+    grid, ring, ac, phantom, K, y, config = _scene(grid_size, sensors, samples, seed, config, device)
+    pool = CudaPool(device, "float32")
+    iterative_reconstruct(K, y, config, pool=pool)  # plan, graph capture
+    total, result = float("inf"), None
+    for _ in range(3):
+        stages: dict = {}
+        t0 = time.perf_counter()
+        res = iterative_reconstruct(K, y, config, pool=pool, stage_seconds=stages)
+        dt = time.perf_counter() - t0
+        if dt < total:
+            total, result = dt, res
+
+    op = operator_for(grid, ring, ac, pool)
+    params = solver_params(config, result.alpha_used, result.beta_used, result.step_used)
+    op.profile_iterations(y.values, params)  # warm-up
+    (k1, k2, k3), launches = op.profile_iterations(y.values, params)
+    secs = {"gradient_products": k1 + k2, "tv_gradient": 0.0, "prox": 0.0, "objective": k3}
+    secs["other"] = max(0.0, total - sum(secs.values()))
+    denom = max(total, sum(secs.values()))
+    rep = BenchReport(
+        scenario=f"profile {grid_size}x{grid_size}, {sensors} sensors, {samples} samples",
+        environment=_environment(device, grid=[grid_size, grid_size], sensors=sensors,
+                                 samples=samples, matrix_shape=[K.rows, K.cols],
+                                 scalar_kind="real32", iterations=config.iterations),
+        breakdown={k: {"seconds": v, "percent": 100.0 * v / denom} for k, v in secs.items()},
+        metrics={"iterations_run": result.iterations_run, "stopped_by": result.stopped_by,
+                 "kernel_launches": launches, "back_projection_seconds": k1,
+                 "projection_seconds": k2, "fused": "tv_gradient and prox run in the "
+                 "back-projection epilogue (counted in gradient_products)",
+                 "stage_times": "device, un-graphed kernels with CUDA events"})
+    rep.entries.append(BenchEntry("iterative_run", total, 1, _sha(result.image.values)))
+    return rep
