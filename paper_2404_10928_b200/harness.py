@@ -139,11 +139,11 @@ def bench_recon(grid_size: int, sensors: int, samples: int, config: ReconConfig,
 
     bp = back_project(K, y, pool=f32)
     t_bp = _best_of(lambda: back_project(K, y, pool=f32), reps)
+    ir32 = iterative_reconstruct(K, y, config, pool=f32)
+    t_32 = _best_of(lambda: iterative_reconstruct(K, y, config, pool=f32), reps)
     ir64 = iterative_reconstruct(K, y, config, pool=f64)
     t_64 = _best_of(lambda: iterative_reconstruct(K, y, config, pool=f64), reps)
-    ir32 = iterative_reconstruct(K, y, config, pool=f32)
     dev = _rel_l2(ir32.image.values, ir64.image.values)
-    t_32 = _best_of(lambda: iterative_reconstruct(K, y, config, pool=f32), reps)
 
     truth = phantom.values / max(float(np.max(np.abs(phantom.values))), 1e-300)
 
