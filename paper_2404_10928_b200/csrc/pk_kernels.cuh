@@ -1641,7 +1641,7 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
         // 8 apart then hit banks 9 apart (conflict free) instead of 4 banks (8-way conflicts)
         for (int k = threadIdx.x; k < ns + (ns >> 3) + 1; k += kThreads) gs[k] = 0;
         __syncthreads();
-        // a warp takes whole windows (list order w, w + 8, ...; two at a time so four 16-B loads
+        // a warp takes whole windows (list order w, w + 8, ...; four at a time so eight 16-B loads
         // per lane are in flight); lane c adds entries 8c..8c+7 of the window.  The window's
         // start sb is warp-uniform, so the padded address of entry 8c + q is
         // (sb + q + (sb + q)/8) + 9c: one add per atomic.  Integer adds commute: the sum is
@@ -1661,23 +1661,29 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
                 if (inside || (j >= 0 && j < ns)) atomicAdd(gs + jp, e[q]);
             }
         };
-        for (int w0 = wid; w0 < a.nwin; w0 += 2 * kW) {
-            const int w1 = w0 + kW;
-            const int2 d0 = list_s ? wl_s[w0] : __ldg(wl + w0);
-            const int2 d1 = w1 < a.nwin ? (list_s ? wl_s[w1] : __ldg(wl + w1)) : make_int2(0, INT_MIN);
+#ifndef PK_FIN_WIN
+#define PK_FIN_WIN 2
+#endif
+        constexpr int kWin = PK_FIN_WIN;  // windows per warp whose loads are in flight together
+        for (int w0 = wid; w0 < a.nwin; w0 += kWin * kW) {
+            int2 d[kWin];
+#pragma unroll
+            for (int u = 0; u < kWin; ++u) {
+                const int wi = w0 + u * kW;
+                d[u] = wi < a.nwin ? (list_s ? wl_s[wi] : __ldg(wl + wi)) : make_int2(0, INT_MIN);
+            }
             for (int c = lane; c < per; c += 32) {
-                int4 v0[2], v1[2];
-                const int4* s0p = reinterpret_cast<const int4*>(a.win + d0.x + 8 * c);
-                v0[0] = __ldcg(s0p);
-                v0[1] = __ldcg(s0p + 1);
-                const bool has1 = d1.y != INT_MIN;
-                if (has1) {
-                    const int4* s1p = reinterpret_cast<const int4*>(a.win + d1.x + 8 * c);
-                    v1[0] = __ldcg(s1p);
-                    v1[1] = __ldcg(s1p + 1);
-                }
-                add_window(v0, d0.y - s_lo, c);
-                if (has1) add_window(v1, d1.y - s_lo, c);
+                int4 v[kWin][2];
+#pragma unroll
+                for (int u = 0; u < kWin; ++u)
+                    if (d[u].y != INT_MIN) {
+                        const int4* sp = reinterpret_cast<const int4*>(a.win + d[u].x + 8 * c);
+                        v[u][0] = __ldcg(sp);
+                        v[u][1] = __ldcg(sp + 1);
+                    }
+#pragma unroll
+                for (int u = 0; u < kWin; ++u)
+                    if (d[u].y != INT_MIN) add_window(v[u], d[u].y - s_lo, c);
             }
         }
         __syncthreads();
