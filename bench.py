@@ -489,8 +489,13 @@ def main():
 
     # ---- sensor-sharded single-frame latency (BASELINE config 3 at N > 1) ----
     sensor_sharded = None
+    shard_err = None
     if world > 1 and not sensor_mode and not seq and args.sensor_frames > 0:
-        ssolver, m0, m1, _ = make_shard_solver()
+        try:  # connect failures are raised on every rank together (PeerShardSolve)
+            ssolver, m0, m1, _ = make_shard_solver()
+        except RuntimeError as e:
+            shard_err = str(e)[:300]
+    if world > 1 and not sensor_mode and not seq and args.sensor_frames > 0 and shard_err is None:
         Yl = Y[:2, m0 * Q: m1 * Q].contiguous()
         ssolver.solve(Yl[0], pinned, alpha, beta, step)  # warm-up (plan, NCCL communicators)
         torch.cuda.synchronize(dev)
@@ -558,6 +563,8 @@ def main():
         }
         if sensor_sharded is not None:
             line["sensor_sharded"] = sensor_sharded
+        elif shard_err is not None:
+            line["sensor_sharded"] = {"unavailable": shard_err}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -263,9 +263,23 @@ class PeerShardSolve:
         signals a peer block before that peer has mapped the world)."""
         import torch.distributed as dist
 
+        import torch
+
         handles = [None] * self.world
         dist.all_gather_object(handles, self.handle, group=group)
-        self.connect(handles)
+        err = None
+        try:
+            self.connect(handles)
+        except Exception as e:  # e.g. no peer access between two devices of this node
+            err = e
+        # every rank learns whether any rank failed, so all raise together (none is left
+        # waiting in a collective of a solve the others abandoned)
+        dev = torch.device("cuda", self.op.pool.device) if dist.get_backend(group) == "nccl" else "cpu"
+        bad = torch.tensor([1 if err is not None else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(bad, op=dist.ReduceOp.MAX, group=group)
+        if int(bad.item()):
+            raise RuntimeError(f"peer exchange unavailable on rank {self.rank}: "
+                               f"{err if err is not None else 'another rank failed to connect'}")
         dist.barrier(group=group)
 
     def _body(self):
