@@ -880,7 +880,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 p->fsym_T = T;
                 p->fsym_qt = qt;
                 p->fsym_L = L;
-                p->fsym_smem = 4 * L * 32 * 4 + (kFsThreads / 32) * (32 + kFsBatch) * 32;
+                p->fsym_smem = 4 * L * 32 * 4 + (kFsThreads / 32) * (32 + kFsBatch) * 16;
                 break;
             }
         }

@@ -1221,8 +1221,9 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int WW = 4 * LW * 32;  // window words
     int32_t* win = reinterpret_cast<int32_t*>(smem);
-    // per-warp record buffer: 2 float4 per pixel {px, xs0, xs1, xs2}, {xs3, xqb0, xqb1, xqb2}
-    float4* rec = reinterpret_cast<float4*>(smem + (size_t)WW * 4) + (size_t)warp * (32 + kFsBatch) * 2;
+    // per-warp record buffer: one float4 {xs0, xs1, xs2, xs3} per column of the piece, plus
+    // kFsBatch zero records (padding columns)
+    float4* rec = reinterpret_cast<float4*>(smem + (size_t)WW * 4) + (size_t)warp * (32 + kFsBatch);
     const uint32_t win_s = smem_u32(win);
 
     const int u = blockIdx.x;
