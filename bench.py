@@ -297,7 +297,8 @@ def main():
     else:
         B = args.batch
         SS = max(1, args.streams)
-        ops = [pk.operator_for(grid, ring, ac, pk.CudaPool(local, "float32"), frames=B, slot=q)
+        ops = [pk.operator_for(grid, ring, ac, pk.CudaPool(local, "float32"), frames=B, slot=q,
+                               concurrency=SS)
                for q in range(SS)]
         op = ops[0]
         streams = [torch.cuda.current_stream(dev)] + [torch.cuda.Stream(dev) for _ in range(SS - 1)]
@@ -383,9 +384,12 @@ def main():
         nl = ctypes.c_int32()
         prof_iters = cfg.iterations
         reps = 5
+        # the kernels timed alone on a latency-mode plan (full back-projector grid); the
+        # timed region's plans share the GPU across streams with half that grid
+        prof_op = pk.operator_for(grid, ring, ac, pk.CudaPool(local, "float32"), frames=B, slot=SS)
         tot = np.zeros(3)
         for r_ in range(reps):
-            N.check(lib.pk_profile_iterations(op.handle, params_arr, Ystep[r_ % n_steps_in].data_ptr(),
+            N.check(lib.pk_profile_iterations(prof_op.handle, params_arr, Ystep[r_ % n_steps_in].data_ptr(),
                                               fl, ctypes.byref(nl), stream_ptr()))
             tot += np.array(fl[:])
         per_launch_ms = tot / (reps * prof_iters)
@@ -423,6 +427,9 @@ def main():
         roof = {"bound": "fp32", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                 "frac": achieved / peak.value, "traffic": traffic,
                 "kernel": names[dom],
+                "plan": "kernels timed alone, un-graphed, on a latency-mode plan (full persistent "
+                        "back-projector grid); the timed region runs throughput-mode plans "
+                        "(half that grid) on concurrent streams",
                 "peak_source": "measured live: FFMA microkernel (pk_measure_fp32_peak); "
                                "MEASURED_PEAKS.json has no FP32 figure",
                 "work": f"12 flops x {M} sensors x {P} pixels per launch",

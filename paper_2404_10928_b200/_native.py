@@ -61,6 +61,7 @@ class GeometryDesc(ctypes.Structure):
         ("dtype", ctypes.c_int32),
         ("device", ctypes.c_int32),
         ("frames", ctypes.c_int32),
+        ("concurrency", ctypes.c_int32),
     ]
 
 

@@ -64,7 +64,7 @@ class DeviceOperator:
     """K restricted to sensors [sensor_begin, sensor_end) of a ring, on one device."""
 
     def __init__(self, grid, ring, acoustic, pool: CudaPool, sensor_begin=0, sensor_end=None,
-                 frames: int = 1):
+                 frames: int = 1, concurrency: int = 1):
         _require_cuda(pool.device)
         lib = N.load()
         self.grid, self.ring, self.acoustic, self.pool = grid, ring, acoustic, pool
@@ -84,6 +84,7 @@ class DeviceOperator:
             sensor_begin=self.sensor_begin, sensor_end=self.sensor_end,
             samples=int(acoustic.q_s), c=float(acoustic.c), dt=float(acoustic.dt),
             dtype=pool.pk_dtype, device=pool.device, frames=self.frames,
+            concurrency=int(concurrency),
         )
         handle = ctypes.c_void_p()
         N.check(lib.pk_plan_create(ctypes.byref(desc), ctypes.byref(handle)))
@@ -388,8 +389,8 @@ _cache: dict = {}
 _cache_lock = threading.Lock()
 
 
-def _key(grid, ring, acoustic, pool, m0, m1, frames=1, slot=0):
-    return (int(frames), int(slot),
+def _key(grid, ring, acoustic, pool, m0, m1, frames=1, slot=0, concurrency=1):
+    return (int(frames), int(slot), int(concurrency),
         int(grid.nx), int(grid.ny), float(grid.dx), tuple(float(v) for v in grid.origin),
         int(ring.count), float(ring.radius), tuple(float(v) for v in ring.center),
         float(acoustic.c), float(acoustic.dt), int(acoustic.q_s),
@@ -398,17 +399,18 @@ def _key(grid, ring, acoustic, pool, m0, m1, frames=1, slot=0):
 
 
 def operator_for(grid, ring, acoustic, pool: CudaPool, sensor_begin=0, sensor_end=None,
-                 frames: int = 1, slot: int = 0):
+                 frames: int = 1, slot: int = 0, concurrency: int = 1):
     """Cached DeviceOperator for a geometry (plans are reused across calls and frames).
 
     ``slot`` selects independent plans for the same geometry (one per CUDA stream when
-    frames are streamed concurrently)."""
+    frames are streamed concurrently); ``concurrency`` > 1 plans for that throughput mode
+    (a smaller persistent back-projector grid; rounding-level differences)."""
     m1 = int(ring.count) if sensor_end is None else int(sensor_end)
-    k = _key(grid, ring, acoustic, pool, sensor_begin, m1, frames, slot)
+    k = _key(grid, ring, acoustic, pool, sensor_begin, m1, frames, slot, concurrency)
     with _cache_lock:
         op = _cache.get(k)
         if op is None:
-            op = DeviceOperator(grid, ring, acoustic, pool, sensor_begin, m1, frames)
+            op = DeviceOperator(grid, ring, acoustic, pool, sensor_begin, m1, frames, concurrency)
             _cache[k] = op
         return op
 

@@ -145,3 +145,28 @@ def test_symmetric_kernels_truncated_window(monkeypatch, oracle):
     r = rng.standard_normal(M * Q)
     assert rel(op.adjoint(r).double().cpu().numpy(), o.adjoint(r)) <= 2e-4
     pk.clear_plan_cache()
+
+
+def test_throughput_grid_matches_latency_grid(oracle):
+    """pk_geometry_desc.concurrency > 1 halves the back-projector's persistent grid: the
+    reconstruction agrees with the latency-mode plan to fp32 rounding and with the oracle."""
+    import torch
+
+    n, M, Q, N = 256, 256, 2048, 5
+    s = oracle.make_scene(n, M, Q, 0)
+    o = oracle.Operator.of(s)
+    y = o.forward(s.phantom)
+    alpha, beta = oracle.resolve_regularization(o, y)
+    ref = oracle.reconstruct(o, y, alpha, beta, 2651.3, N)
+    grid, ring, ac, _ = pk.make_scene(n, M, Q, 0)
+    params = pk.solver.solver_params(pk.ReconConfig(alpha, beta, N, 2651.3), alpha, beta, 2651.3)
+    xs = []
+    for conc in (1, 2):
+        op = pk.operator_for(grid, ring, ac, pk.CudaPool(0, "float32"), concurrency=conc)
+        x, hist, status = op.reconstruct(y, params)
+        torch.cuda.synchronize()
+        assert int(status[0, 0]) == N
+        xs.append(x[0].double().cpu().numpy())
+    assert np.linalg.norm(xs[0] - xs[1]) <= 1e-5 * np.linalg.norm(xs[0])
+    for xv in xs:
+        assert np.linalg.norm(xv - ref["image"]) <= 1e-4 * np.linalg.norm(ref["image"])
