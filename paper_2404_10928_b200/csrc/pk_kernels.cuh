@@ -1672,6 +1672,8 @@ __global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
             for (int u = 0; u < kWin; ++u) {
                 const int wi = w0 + u * kW;
                 d[u] = wi < a.nwin ? (list_s ? wl_s[wi] : __ldg(wl + wi)) : make_int2(0, INT_MIN);
+                // windows wholly outside this CTA's sample chunk are not loaded
+                if (d[u].y != INT_MIN && (d[u].y + LW <= s_lo || d[u].y >= c1)) d[u].y = INT_MIN;
             }
             for (int c = lane; c < per; c += 32) {
                 int4 v[kWin][2];
