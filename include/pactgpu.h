@@ -69,8 +69,8 @@ typedef struct pk_geometry_desc {
                                 (frame-major), and params points to `frames` structs. */
     int32_t concurrency;     /* plans the caller runs concurrently on this device (streams):
                                 0/1 = latency (full persistent back-projector grid); > 1 =
-                                throughput (half the grid: fewer partial slots, the other
-                                streams fill the SMs).  Each plan is deterministic; the two
+                                throughput (at most half the occupancy-limited grid: fewer
+                                partial slots, the other streams fill the SMs).  Each plan is deterministic; the two
                                 modes sum the back-projector's partials in a different grouping
                                 (fp32 rounding-level differences). */
 } pk_geometry_desc;

@@ -817,10 +817,13 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                     for (int t = 0; t < p->sym_ntiles; ++t)
                         wsum += (int64_t)nch * (((tl[t] >> 16) == (tl[t] & 0xffff)) ? kSymWDiag : kSymWOff);
                     p->sym_grid = (int)std::max<int64_t>(32, std::min<int64_t>((int64_t)occ * sms, wsum / 64));
-                    // throughput mode (several plans on concurrent streams): half the grid --
-                    // 1013 -> 1027 frames/s at config 3 on 4 streams, 2273 -> 2331 at config 4
-                    // on 8 (tools/sweep_grid.sh); the partial sums group differently (rounding level)
-                    if (d->concurrency > 1) p->sym_grid = std::max(32, p->sym_grid / 2);
+                    // throughput mode (several plans on concurrent streams): at most half the
+                    // occupancy-limited grid -- config 3 on 4 streams 1013 -> 1027 frames/s; a
+                    // work-limited grid (config 2: 136 CTAs) is kept (halving it: 2147 -> 2004)
+                    // (tools/sweep_grid.sh); the partial sums group differently (rounding level)
+                    if (d->concurrency > 1)
+                        p->sym_grid = (int)std::max<int64_t>(
+                            32, std::min<int64_t>((int64_t)occ * sms / 2, wsum / 64));
                 }
                 if (const char* e = getenv("PK_SYM_GRID")) p->sym_grid = std::max(1, atoi(e));
                 std::vector<int>& ch = p->sym_h[1];

@@ -152,17 +152,19 @@ def test_throughput_grid_matches_latency_grid(oracle):
     reconstruction agrees with the latency-mode plan to fp32 rounding and with the oracle."""
     import torch
 
-    n, M, Q, N = 256, 256, 2048, 5
+    n, M, Q, N = 512, 512, 2048, 3  # occupancy-limited grid: the throughput mode halves it
     s = oracle.make_scene(n, M, Q, 0)
     o = oracle.Operator.of(s)
     y = o.forward(s.phantom)
     alpha, beta = oracle.resolve_regularization(o, y)
-    ref = oracle.reconstruct(o, y, alpha, beta, 2651.3, N)
+    step = 333.156  # survey-pinned config 3 step
+    ref = oracle.reconstruct(o, y, alpha, beta, step, N)
     grid, ring, ac, _ = pk.make_scene(n, M, Q, 0)
-    params = pk.solver.solver_params(pk.ReconConfig(alpha, beta, N, 2651.3), alpha, beta, 2651.3)
+    params = pk.solver.solver_params(pk.ReconConfig(alpha, beta, N, step), alpha, beta, step)
     xs = []
     for conc in (1, 2):
         op = pk.operator_for(grid, ring, ac, pk.CudaPool(0, "float32"), concurrency=conc)
+        assert op.info.bp_split >= 1
         x, hist, status = op.reconstruct(y, params)
         torch.cuda.synchronize()
         assert int(status[0, 0]) == N
