@@ -1105,7 +1105,14 @@ __global__ void __launch_bounds__(kThreads, NF == 1 ? 4 : (NF == 2 ? 3 : 2)) fp_
 // ===========================================================================
 constexpr int kFsTile = 64;      // quadrant tile side (32 where a 64-tile window does not fit:
                                  // short c*dt, e.g. BASELINE config 2); rows are 32-pixel pieces
-constexpr int kFsBatch = 4;      // records per scatter batch (16 independent atomic pairs)
+#ifndef PK_FS_BATCH
+#define PK_FS_BATCH 4
+#endif
+#ifndef PK_FS_UNROLL
+#define PK_FS_UNROLL 2
+#endif
+constexpr int kFsBatch = PK_FS_BATCH;  // records per scatter batch (4: 16 independent atomic pairs)
+constexpr int kFsUnroll = PK_FS_UNROLL; // scatter batches unrolled per loop iteration
 constexpr int kFsThreads = 512;  // 16 warps share the windows (occupancy at 2 CTAs per SM)
 
 struct FpSymArgs {
@@ -1332,7 +1339,7 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
             auto scatter = [&](auto checked) {
                 constexpr bool CHECK = decltype(checked)::value;
                 const int kn = CHECK ? kend : 32;
-#pragma unroll 2
+#pragma unroll kFsUnroll
                 for (int k = 0; k < kn; k += kFsBatch) {
                     uint32_t ad[kFsBatch];
                     int32_t va[kFsBatch][4], vb[kFsBatch][4];
