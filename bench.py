@@ -49,9 +49,10 @@ def parse():
     ap.add_argument("--config", default="cfg3", choices=CFG_CHOICES)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--shard", default="frames", choices=["sensors", "frames"])
-    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+    ap.add_argument("--exchange", default=None, choices=["peer", "nccl"],
                     help="sensor shards: gradient exchange over peer memory fused into the update "
-                         "(pk_peer_*) or an NCCL all-reduce")
+                         "(pk_peer_*) or an NCCL all-reduce (default: peer with --shard sensors; "
+                         "nccl for the sensor-sharded extra line of the frames mode)")
     ap.add_argument("--sensor-streams", type=int, default=2,
                     help="sensor shards with --exchange peer: frames in flight (one plan/stream each)")
     ap.add_argument("--sensor-frames", type=int, default=5,
@@ -64,7 +65,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.exchange is None:
+        a.exchange = "peer" if a.shard == "sensors" else "nccl"
+    return a
 
 
 # ---------------------------------------------------------------------------
