@@ -1584,7 +1584,10 @@ struct FinArgs {
 constexpr int kFinListMax = 256;  // per-trace gather lists up to this length are staged in smem
 
 template <typename T, int NF>
-__global__ void __launch_bounds__(kThreads) finalize_kernel(FinArgs<T> a) {
+#ifndef PK_FIN_MINB
+#define PK_FIN_MINB 4  // <= 64 registers: 4 CTAs per SM (more registers cost occupancy: 94 regs -> +6 us)
+#endif
+__global__ void __launch_bounds__(kThreads, PK_FIN_MINB) finalize_kernel(FinArgs<T> a) {
     extern __shared__ __align__(128) unsigned char smem[];
     T* tr = reinterpret_cast<T*>(smem);
     __shared__ double red_d[kThreads / 32];
