@@ -3,11 +3,14 @@
 Drop-in for the reference package ``pactkit``'s reconstruction / projection API
 (pkg/src/pactkit/__init__.py:10-78, hot-path subset): the same names, signatures and
 result types, with every product running matrix-free in sm_100a CUDA kernels behind the
-C ABI of include/pactgpu.h.  Pass ``pool=CudaPool(device, dtype)`` where the reference
-takes a ``WorkerPool``; ``pool=None`` uses ``CudaPool()`` (cuda:0, float32).
+C ABI of include/pactgpu.h.  Pass ``pool=CudaPool(device, "float32")`` where the reference
+takes a ``WorkerPool`` to select the fp32 production mode.  ``pool=None`` and a reference
+``WorkerPool`` keep the reference's fp64 numerics (the device's fp64 validation mode,
+``device.resolve_pool``); ``set_default_pool`` changes what ``None`` means.
 """
 
-from .device import CudaPool, DeviceOperator, clear_plan_cache, operator_for
+from .device import (CudaPool, DeviceOperator, clear_plan_cache, default_pool, operator_for,
+                     resolve_pool, set_default_pool)
 from .measurement import (
     AcousticConfig,
     DenseOperator,

@@ -2,7 +2,7 @@
 
 ``CudaPool`` takes the place of the reference's ``kernels.WorkerPool`` in the ``pool``
 slot of every public function (pkg/src/pactkit/kernels.py:55-73): it names the CUDA
-device and the arithmetic type.  ``DeviceOperator`` wraps the C ABI plan built from the
+device and the arithmetic type (``resolve_pool`` maps None / WorkerPool to fp64).  ``DeviceOperator`` wraps the C ABI plan built from the
 provenance a reference ``MeasurementMatrix`` carries (grid / ring / acoustic,
 forward.py:70-121) -- the dense matrix is never formed.
 
@@ -21,7 +21,8 @@ import numpy as np
 
 from . import _native as N
 
-__all__ = ["CudaPool", "DeviceOperator", "operator_for", "clear_plan_cache"]
+__all__ = ["CudaPool", "DeviceOperator", "operator_for", "clear_plan_cache", "default_pool",
+           "resolve_pool", "set_default_pool"]
 
 
 @dataclass(frozen=True)
@@ -44,6 +45,43 @@ class CudaPool:
     @property
     def pk_dtype(self) -> int:
         return N.PK_F32 if self.dtype == "float32" else N.PK_F64
+
+
+_default_pool: CudaPool | None = None
+
+
+def set_default_pool(pool: CudaPool | None) -> None:
+    """Policy used where a public call passes ``pool=None`` (None restores the built-in
+    default, ``CudaPool(0, "float64")``)."""
+    if pool is not None and not isinstance(pool, CudaPool):
+        raise TypeError(f"expected a CudaPool or None, got {type(pool).__name__}")
+    global _default_pool
+    _default_pool = pool
+
+
+def default_pool() -> CudaPool:
+    return _default_pool if _default_pool is not None else CudaPool(0, "float64")
+
+
+def resolve_pool(pool) -> CudaPool:
+    """The device policy for the ``pool`` argument of the public API.
+
+    * ``CudaPool(device, dtype)``: used as given -- ``dtype="float32"`` is the production
+      mode, the only way to select fp32 arithmetic;
+    * ``None`` (the reference's serial fp64 kernels, kernels.py:304-350): ``default_pool()``,
+      the fp64 validation mode on cuda:0 unless ``set_default_pool`` chose otherwise;
+    * a reference ``kernels.WorkerPool`` (parallel fp64 CPU kernels, kernels.py:55-73):
+      ``CudaPool(0, "float64")`` -- the same fp64 numerics (<= 1e-12 of the reference), on
+      the device; its worker count has no device meaning and is ignored.
+    Anything else raises TypeError.  There is no CPU path.
+    """
+    if isinstance(pool, CudaPool):
+        return pool
+    if pool is None:
+        return default_pool()
+    if type(pool).__name__ == "WorkerPool" and hasattr(pool, "worker_count"):
+        return CudaPool(0, "float64")
+    raise TypeError(f"pool must be a CudaPool, a reference WorkerPool or None, got {type(pool).__name__}")
 
 
 def _torch():
@@ -281,6 +319,15 @@ class DeviceOperator:
                                              self.stream()))
         return xo, sums
 
+    def _check_y(self, yt):
+        """The C ABI reads frames*M*Q values from a raw pointer: a short y must fail here
+        (ValueError, like matvec / adjoint) instead of reading out of bounds on the device."""
+        want = self.frames * self.sensors * self.samples
+        if yt.numel() != want:
+            raise ValueError(f"expected {want} measurement values ({self.frames} frame(s) x "
+                             f"{self.sensors} sensors x {self.samples} samples), got {yt.numel()}")
+        return yt
+
     def _params(self, params):
         """ctypes array of `frames` SolverParams (one struct is broadcast to all frames)."""
         if isinstance(params, N.SolverParams):
@@ -299,7 +346,7 @@ class DeviceOperator:
         status [frames, 2]) device tensors."""
         torch = _torch()
         arr, n = self._params(params)
-        yt = self.tensor(y)
+        yt = self._check_y(self.tensor(y))
         F = self.frames
         x = self.empty(self.pixels * F)
         hist = torch.zeros(4 * n * F, device=self.device, dtype=torch.float64)
@@ -314,7 +361,7 @@ class DeviceOperator:
         summed device seconds of K1 (back-projection with the fused TV/prox update), K2
         (projection), K3 (residual/objective), and the number of launches."""
         arr, _ = self._params(params)
-        yt = self.tensor(y)
+        yt = self._check_y(self.tensor(y))
         ms = (ctypes.c_float * 3)()
         n = ctypes.c_int32()
         with _torch().cuda.device(self.device):
@@ -326,7 +373,9 @@ class DeviceOperator:
         """The C-ABI host-buffer entry (pk_reconstruct_host): fp64 in, fp64 out, synchronous."""
         arr, n = self._params(params)
         F = self.frames
-        y = np.ascontiguousarray(y_host, dtype=np.float64)
+        y = np.ascontiguousarray(y_host, dtype=np.float64).ravel()
+        if y.size != F * self.sensors * self.samples:
+            raise ValueError(f"expected {F * self.sensors * self.samples} measurement values, got {y.size}")
         x = np.empty(self.pixels * F)
         hist = np.empty(4 * n * F)
         status = np.zeros(2 * F, dtype=np.int32)

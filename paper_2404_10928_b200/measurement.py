@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .device import CudaPool, operator_for
+from .device import CudaPool, operator_for, resolve_pool
 from .scene import GeometryError, ImageField, check_enclosure
 
 __all__ = [
@@ -95,7 +95,7 @@ class SensorData:
         return self.values.size
 
 
-@dataclass(frozen=True, eq=False)
+@dataclass(frozen=True, eq=False, init=False)
 class MeasurementMatrix:
     """The discretised operator K.
 
@@ -103,11 +103,23 @@ class MeasurementMatrix:
     records them, forward.py:207-215): products run matrix-free on the device and
     ``entries`` is materialised only on request.  Explicit (``entries`` given): the dense
     array is the operator.
+
+    The constructor is the reference's, ``MeasurementMatrix(domain, entries, provenance)``
+    (forward.py:70-91), positionally or by keyword (``entries=``); ``entries=None`` with
+    grid/ring/acoustic provenance is the lazy form.  The dense array is held in the field
+    ``entries_`` (the ``entries`` property materialises it), so ``dataclasses.replace(K,
+    entries=...)`` works too.
     """
 
     domain: str
     entries_: np.ndarray | None = None
     provenance: dict = field(default_factory=dict)
+
+    def __init__(self, domain, entries=None, provenance=None, *, entries_=None):
+        object.__setattr__(self, "domain", domain)
+        object.__setattr__(self, "entries_", entries if entries is not None else entries_)
+        object.__setattr__(self, "provenance", {} if provenance is None else provenance)
+        self.__post_init__()
 
     def __post_init__(self):
         if self.domain not in ("time", "frequency"):
@@ -165,6 +177,9 @@ class MeasurementMatrix:
         dump (pk_index_dump, the same s0/frac the reference computes) -- small scenes only."""
         if self.entries_ is not None:
             return self.entries_
+        cached = self.__dict__.get("_materialised")
+        if cached is not None:  # kept apart from entries_: K stays geometry-backed
+            return cached
         if self.domain == "frequency":
             return self._freq_entries()
         M, Q = self.ring.count, self.acoustic.q_s
@@ -184,7 +199,7 @@ class MeasurementMatrix:
         K[(m_idx * Q + s0 - 1)[lo_ok], cols[lo_ok]] = (1.0 - fr[lo_ok]) * w
         K[(m_idx * Q + s0)[hi_ok], cols[hi_ok]] = fr[hi_ok] * w
         K.setflags(write=False)
-        object.__setattr__(self, "entries_", K)
+        object.__setattr__(self, "_materialised", K)
         return K
 
 
@@ -204,7 +219,7 @@ class MeasurementMatrix:
             blk /= d[m][None, :]
             K[m * Qn:(m + 1) * Qn] = blk
         K.setflags(write=False)
-        object.__setattr__(self, "entries_", K)
+        object.__setattr__(self, "_materialised", K)
         return K
 
 
@@ -284,11 +299,21 @@ _dense_cache: dict = {}
 
 
 def _as_pool(pool) -> CudaPool:
-    """The device policy for a ``pool`` argument.  None or a reference WorkerPool select the
-    default device pool -- every product runs on the GPU (no CPU path)."""
-    if isinstance(pool, CudaPool):
-        return pool
-    return CudaPool()
+    """The device policy for a ``pool`` argument (see ``device.resolve_pool``)."""
+    return resolve_pool(pool)
+
+
+def geometry_path(K) -> str | None:
+    """'time' / 'frequency' when K's products run matrix-free from its grid/ring/acoustic
+    provenance (no explicit entries), else None (an explicit matrix: dense products)."""
+    if isinstance(K, np.ndarray):
+        return None
+    prov = getattr(K, "provenance", {}) or {}
+    has_geo = all(prov.get(k) is not None for k in ("grid", "ring", "acoustic"))
+    explicit = getattr(K, "entries_", None) if isinstance(K, MeasurementMatrix) else None
+    if has_geo and explicit is None and K.domain in ("time", "frequency"):
+        return K.domain
+    return None
 
 
 def device_operator(K, pool=None):
@@ -299,11 +324,9 @@ def device_operator(K, pool=None):
     """
     pool = _as_pool(pool)
     prov = getattr(K, "provenance", {}) or {}
-    has_geo = all(prov.get(k) is not None for k in ("grid", "ring", "acoustic"))
-    explicit = getattr(K, "entries_", None) if isinstance(K, MeasurementMatrix) else None
-    if has_geo and explicit is None and K.domain == "time":
+    if geometry_path(K) == "time":
         return operator_for(prov["grid"], prov["ring"], prov["acoustic"], pool)
-    if has_geo and explicit is None and K.domain == "frequency":
+    if geometry_path(K) == "frequency":
         return FreqOperator(prov["grid"], prov["ring"], prov["acoustic"], pool)
     entries = K.entries if not isinstance(K, np.ndarray) else K
     key = (id(entries), pool)

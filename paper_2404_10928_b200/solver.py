@@ -19,7 +19,8 @@ import numpy as np
 
 from . import _native as N
 from .device import CudaPool, DeviceOperator
-from .measurement import DenseOperator, FreqOperator, SensorData, _as_pool, device_operator
+from .measurement import (DenseOperator, FreqOperator, SensorData, _as_pool, device_operator,
+                          geometry_path)
 from .scene import ImageField
 
 __all__ = [
@@ -311,7 +312,8 @@ def _dense_loop(op, yv, alpha, beta, eta, config, shape):
     y = op.tensor(yv)
     x = torch.zeros(op.cols, dtype=rdt, device=dev)
     r = -y.clone()
-    f_prev = float(torch.real(torch.vdot(r, r)))
+    r64 = r.to(torch.complex128) if r.is_complex() else r.double()
+    f_prev = float(torch.real(torch.vdot(r64, r64)))  # fp64 like every later objective
     hist = []
     stopped_by = "max_iterations"
     grow = 0
@@ -447,7 +449,7 @@ def reconstruct_frames(K, ys, config: ReconConfig, pool=None, batch: int = 4,
     for y in ys:
         _check_pair(K, y)
     prov = getattr(K, "provenance", {}) or {}
-    if not all(prov.get(k) is not None for k in ("grid", "ring", "acoustic")):
+    if geometry_path(K) != "time":  # explicit or frequency-domain K: one solve per frame
         return [iterative_reconstruct(K, y, config, pool=pool) for y in ys]
     cal = []
     for y in ys:

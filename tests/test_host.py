@@ -185,3 +185,66 @@ def test_pactmat_pactsig_round_trip_and_reference_layout(tmp_path):
         pk.read_signal(tmp_path / "bad")
     with pytest.raises(ValueError):
         pk.read_matrix(tmp_path / "y.sig")
+
+
+def test_measurement_matrix_reference_constructor():
+    """MeasurementMatrix(domain, entries, provenance) as forward.py:70-91 declares it: keyword
+    `entries=` and dataclasses.replace(K, entries=...) work (ADVICE r1)."""
+    import dataclasses
+
+    A = np.arange(12.0).reshape(4, 3)
+    K = pk.MeasurementMatrix(domain="time", entries=A)
+    assert K.rows == 4 and K.cols == 3 and np.array_equal(K.entries, A)
+    assert not K.entries.flags.writeable
+    K2 = dataclasses.replace(K, entries=2 * A)
+    assert np.array_equal(K2.entries, 2 * A) and K2.domain == "time"
+    K3 = pk.MeasurementMatrix("frequency", A + 1j)
+    assert K3.entries.dtype == np.complex128
+    with pytest.raises(ValueError):
+        pk.MeasurementMatrix("time", np.zeros(3))
+    with pytest.raises(ValueError):
+        pk.MeasurementMatrix("time")  # neither entries nor provenance
+    g, ring, ac, _ = pk.make_scene(16, 8, 40)
+    lazy = pk.MeasurementMatrix("time", None, {"grid": g, "ring": ring, "acoustic": ac})
+    assert lazy.geometry_backed and lazy.rows == 320
+
+
+def test_pool_policy_is_explicit():
+    """pool=None and a reference WorkerPool keep the reference's fp64 numerics; fp32 needs
+    an explicit CudaPool (VERDICT r1 weak #10)."""
+    from paper_2404_10928_b200.device import resolve_pool
+
+    class WorkerPool:  # what pactkit.kernels.WorkerPool looks like (kernels.py:55-73)
+        worker_count = 8
+
+    assert resolve_pool(None) == pk.CudaPool(0, "float64")
+    assert resolve_pool(WorkerPool()) == pk.CudaPool(0, "float64")
+    f32 = pk.CudaPool(0, "float32")
+    assert resolve_pool(f32) is f32
+    with pytest.raises(TypeError):
+        resolve_pool("float32")
+    pk.set_default_pool(f32)
+    try:
+        assert resolve_pool(None) is f32
+    finally:
+        pk.set_default_pool(None)
+    assert pk.default_pool().dtype == "float64"
+
+
+def test_reconstruct_frames_routes_non_time_operators_per_frame(monkeypatch):
+    """A frequency-domain (or explicit) K never reaches the time-domain batched plans
+    (ADVICE r1: complex y would be truncated and solved with the wrong operator)."""
+    from paper_2404_10928_b200 import solver
+
+    g, ring, ac, _ = pk.make_scene(16, 8, 40)
+    Kf = pk.build_freq_matrix(g, ring, ac)
+    y = pk.SensorData("frequency", 8, 40, np.ones(320, dtype=complex))
+    seen = []
+    monkeypatch.setattr(solver, "iterative_reconstruct",
+                        lambda K, y, config, pool=None: seen.append(K.domain) or "solved")
+    out = solver.reconstruct_frames(Kf, [y, y], pk.ReconConfig(iterations=2),
+                                    pool=pk.CudaPool(0, "float32"), batch=1)
+    assert out == ["solved", "solved"] and seen == ["frequency", "frequency"]
+    Ke = pk.MeasurementMatrix("time", np.eye(4))
+    assert solver.geometry_path(Ke) is None and solver.geometry_path(Kf) == "frequency"
+    assert solver.geometry_path(pk.build_time_matrix(g, ring, ac)) == "time"
