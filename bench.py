@@ -71,6 +71,17 @@ def parse():
     return a
 
 
+def workload_config(cfg, name):
+    """The `config` object of both arms' JSON lines: the workload only (the same dict for
+    ours and --impl reference); how an arm runs it goes under `arm`."""
+    from paper_2404_10928_b200.workloads import PINNED
+
+    a, b, s = PINNED[name]
+    return {"workload": cfg.name, "image": f"{cfg.n}x{cfg.n}", "sensors": cfg.sensors,
+            "samples": cfg.samples, "iterations": cfg.iterations, "frames": cfg.frames,
+            "pinned": {"alpha": a, "beta": b, "step": s}}
+
+
 # ---------------------------------------------------------------------------
 # CPU baseline (oracle port, test infrastructure; only here and in tests/)
 
@@ -110,6 +121,9 @@ def run_reference(args, cfg):
     per = []
     from oracle import pyoracle as O
 
+    from paper_2404_10928_b200.workloads import PINNED
+
+    alpha, beta, step = PINNED[args.config]
     s = O.make_scene(cfg.n, cfg.sensors, cfg.samples, 0)
     op = O.Operator.of(s)
     y = op.forward(s.phantom)
@@ -117,13 +131,13 @@ def run_reference(args, cfg):
     cores = O.lib().or_max_threads()
     x = np.zeros(s.P)
     r = -y
-    for k in range(W + K):
+    for k in range(W + K):  # recon.py:318-346 with the pinned config, one iteration per step
         t0 = time.perf_counter()
         grad = 2.0 * op.adjoint(r)
-        grad += 1e-5 * O.tv_gradient(x.reshape(shape), 1e-3).reshape(-1)
-        x = O.soft_threshold(x - 1e-3 * grad, 1e-6)
+        grad += beta * O.tv_gradient(x.reshape(shape), 1e-3).reshape(-1)
+        x = O.soft_threshold(x - step * grad, step * alpha)
         r = op.forward(x) - y
-        O.objective_parts(r, x, shape, 1e-3, 1e-5)
+        O.objective_parts(r, x, shape, alpha, beta)
         if k >= W:
             per.append(time.perf_counter() - t0)
     t_it = float(np.mean(per))
@@ -135,8 +149,9 @@ def run_reference(args, cfg):
         "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": t_it * 1e3,
         "ms_per_iteration": t_it * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (make_scene vessel phantom, seed 0)",
-        "config": {"workload": cfg.name, "image": f"{cfg.n}x{cfg.n}", "sensors": cfg.sensors,
-                   "samples": cfg.samples, "iterations": cfg.iterations, "parallelism": "cpu threads"},
+        "config": workload_config(cfg, args.config),
+        "arm": {"parallelism": f"cpu threads ({cores})", "path": "fp64 matrix-free C restatement "
+                "of the reference operator (oracle/pact_oracle.c), iterations of recon.py:318-346"},
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -207,7 +222,7 @@ class ClockSampler:
 
 def main():
     args = parse()
-    from paper_2404_10928_b200.workloads import CONFIGS
+    from paper_2404_10928_b200.workloads import CONFIGS, PINNED
 
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -257,14 +272,16 @@ def main():
         Ys.append(op64.matvec(phf.values).float())
     Y = torch.stack(Ys)  # [F, M*Q] fp32 on the device
     del Ys
-    K64 = pk.build_time_matrix(grid, ring, ac)
-    # the pinned regularisation is frame 0's on every rank
-    y0 = pk.SensorData("time", M, Q, (Y[0] if sq0 == 0 else op64.matvec(ph0.values).float())
-                       .double().cpu().numpy())
-    pinned = pk.resolve_config(pk.ReconConfig(iterations=cfg.iterations), K64, y0,
-                               pool=pk.CudaPool(local, "float64"))
-    alpha, beta, step = pinned.alpha, pinned.beta, pinned.step
+    # frame 0's calibration, pinned once by the fp64 oracle (workloads.PINNED; the reference
+    # arm solves with the same values); cross-checked here against the device's fp64 alpha
+    alpha, beta, step = PINNED[args.config]
+    pinned = pk.ReconConfig(alpha=alpha, beta=beta, iterations=cfg.iterations, step=step)
     params = pk.solver.solver_params(pinned, alpha, beta, step)
+    K64 = pk.build_time_matrix(grid, ring, ac)
+    a_dev, _ = pk.resolve_regularization(pk.ReconConfig(), K64, pk.SensorData(
+        "time", M, Q, op64.matvec(ph0.values).cpu().numpy()), pool=pk.CudaPool(local, "float64"))
+    if abs(a_dev - alpha) > 1e-9 * alpha:
+        raise SystemExit(f"bench: device fp64 alpha {a_dev!r} != pinned {alpha!r}")
 
     capture = os.environ.get("PK_DIST_BACKEND", "nccl") == "nccl"  # gloo cannot be captured
     def make_shard_solver():
@@ -317,10 +334,20 @@ def main():
         lib = N.load()
         import ctypes
 
+        # every timed solve writes its own status row [iterations_run, stopped_by] x B, read
+        # after the timed region: a frame that stopped early or diverged fails the run
+        n_timed = args.steps * (max(1, F // args.batch) if seq else 1)
+        st_timed = torch.full((n_timed, 2 * B), -1, device=dev, dtype=torch.int32)
+        timed = {"on": False, "k": 0}
+
         def one_step(f):
             q = f % SS
+            st_ptr = stats[q].data_ptr()
+            if timed["on"]:
+                st_ptr = st_timed[timed["k"]].data_ptr()
+                timed["k"] += 1
             N.check(lib.pk_reconstruct(ops[q].handle, params_arr, Ystep[f % n_steps_in].data_ptr(),
-                                       x_outs[q].data_ptr(), hists[q].data_ptr(), stats[q].data_ptr(),
+                                       x_outs[q].data_ptr(), hists[q].data_ptr(), st_ptr,
                                        ctypes.c_void_p(streams[q].cuda_stream)))
         # init + table + copy-out, and per iteration back-projection (+ epilogue kernel for the
         # symmetric back-projector), projection, residual
@@ -362,11 +389,22 @@ def main():
     side = [] if sensor_mode else streams[1:]
     for st_ in side:  # side streams start after e0 and are joined before e1
         st_.wait_event(e0)
+    if not sensor_mode:
+        timed["on"] = True
     run_frames([frame(args.warmup + k) if not seq else k % F for k in range(args.steps * per_step)])
     for st_ in side:
         torch.cuda.current_stream(dev).wait_stream(st_)
     e1.record()
     torch.cuda.synchronize(dev)
+    solves_checked = None
+    if not sensor_mode:
+        timed["on"] = False
+        sv = st_timed.cpu().numpy().reshape(-1, 2)
+        bad = np.flatnonzero((sv[:, 0] != cfg.iterations) | (sv[:, 1] != 0))
+        if timed["k"] != n_timed or bad.size:
+            raise SystemExit(f"bench: {bad.size} of {sv.shape[0]} timed frame solves did not run "
+                             f"{cfg.iterations} iterations to max_iterations (status {sv[bad[:4]].tolist()})")
+        solves_checked = int(sv.shape[0])
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -480,6 +518,9 @@ def main():
         hh = [torch.empty(B * 4 * cfg.iterations, dtype=torch.float64, pin_memory=True).numpy()
               for _ in range(SS)]
         sh = [torch.empty(2 * B, dtype=torch.int32, pin_memory=True).numpy() for _ in range(SS)]
+        n_e2e = args.steps * per_step
+        sh_timed = torch.full((n_e2e, 2 * B), -1, dtype=torch.int32, pin_memory=True).numpy()
+        e2e_on = {"on": False}
         dp = ctypes.POINTER(ctypes.c_double)
         ip = ctypes.POINTER(ctypes.c_int32)
 
@@ -487,9 +528,10 @@ def main():
             # one plan per stream: H2D, solve and D2H of consecutive steps overlap across streams
             q = k % SS
             f = k % nF
+            stv = sh_timed[k] if e2e_on["on"] else sh[q]
             N.check(lib.pk_reconstruct_host_async(
                 ops[q].handle, params_arr, yh_np[f].ctypes.data_as(dp), xo[q].ctypes.data_as(dp),
-                hh[q].ctypes.data_as(dp), sh[q].ctypes.data_as(ip), ctypes.c_void_p(streams[q].cuda_stream)))
+                hh[q].ctypes.data_as(dp), stv.ctypes.data_as(ip), ctypes.c_void_p(streams[q].cuda_stream)))
         for k in range(args.warmup):
             host_step(k)
         torch.cuda.synchronize(dev)
@@ -497,12 +539,19 @@ def main():
         ee0.record()
         for st_ in streams[1:]:
             st_.wait_event(ee0)
+        e2e_on["on"] = True
         for k in range(args.steps * per_step):
             host_step(k)
         for st_ in streams[1:]:
             torch.cuda.current_stream(dev).wait_stream(st_)
         ee1.record()
         torch.cuda.synchronize(dev)
+        e2e_on["on"] = False
+        sv = sh_timed.reshape(-1, 2)
+        bad = np.flatnonzero((sv[:, 0] != cfg.iterations) | (sv[:, 1] != 0))
+        if bad.size:
+            raise SystemExit(f"bench e2e: {bad.size} of {sv.shape[0]} timed solves did not run "
+                             f"{cfg.iterations} iterations")
         ms_e2e = ee0.elapsed_time(ee1)
         if world > 1:  # slowest rank, like the device-resident number
             te = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
@@ -512,6 +561,7 @@ def main():
                "h2d_bytes_per_step": B * M * Q * 8,
                "d2h_bytes_per_step": B * (P * 8 + 4 * cfg.iterations * 8 + 8),
                "ms_per_step": ms_e2e / args.steps,
+               "solves_checked": int(sv.shape[0]),
                "path": f"pk_reconstruct_host_async (C ABI, pinned fp64 host buffers, {SS} stream(s))"
                        + (f"; {nF} host frames cycled, per-frame copies" if seq else "")}
         if seq:
@@ -576,8 +626,8 @@ def main():
             "scaling": "strong" if (sensor_mode or seq) else "weak",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: make_scene vessel phantoms (seed = frame), y = K x by the fp64 device projector",
-            "config": {"workload": cfg.name, "image": f"{cfg.n}x{cfg.n}", "sensors": M, "samples": Q,
-                       "iterations": cfg.iterations, "batch": B,
+            "config": workload_config(cfg, args.config),
+            "arm": {"batch": B,
                        "streams": (args.sensor_streams if args.exchange == "peer" else 1) if sensor_mode else SS,
                        "parallelism": (f"sensor-shard x{world} + "
                                        + ("peer-memory gradient exchange" if args.exchange == "peer"
@@ -586,9 +636,11 @@ def main():
                        "l2": f"{F} distinct frames cycled ({F * M * Q * 4 / 2**20:.0f} MiB of y > 126 MB L2)",
                        **({"sequence": f"{cfg.frames} frames (seeds 0..{cfg.frames - 1}) sharded "
                                        f"{F} per rank; a step is one pass over the rank's share"}
-                          if seq else {}),
-                       "pinned": {"alpha": alpha, "beta": beta, "step": step}},
+                          if seq else {})},
             "clocks": clk,
+            # status of every timed solve read back after the timed region (pk_reconstruct's
+            # status_dev): all ran cfg.iterations iterations and stopped by max_iterations
+            "solves_checked": solves_checked,
             "gpu_launches": launches_per_step * args.steps * per_step,
             "roofline": roof,
             "kernels": kernels,

@@ -210,6 +210,14 @@ int pk_freq_adjoint(pk_plan* plan, int32_t q_n, const void* y_dev, void* out_dev
 int pk_index_dump(pk_plan* plan, int32_t ma, int32_t mb, int64_t* s0_dev, double* frac_dev,
                   void* stream);
 
+/* fp32 delay census (verification of the production kernels' index rule): for local sensors
+ * [ma, mb), s0_dev[(m-ma)*P + p] (int32) and frac_dev (float) exactly as the fp32 kernels
+ * evaluate the delay of pair (p, m): rule 0 the generic back-projector / projector, rule 1 the
+ * D4-symmetric back-projector (the representative pair's delay), rule 2 the rotation-symmetric
+ * projector.  s0 + frac is the fp32 delay u; compare with pk_index_dump / np.hypot. */
+int pk_delay_census_f32(pk_plan* plan, int32_t rule, int32_t ma, int32_t mb, int32_t* s0_dev,
+                        float* frac_dev, void* stream);
+
 /* Profiling hook (bench.py roofline): run the solver's kernels un-graphed on `stream`
  * for params->iterations iterations, with CUDA events around every launch.
  * ms_out[0..2] = summed device milliseconds of K1 (fused back-projection update),
@@ -221,6 +229,46 @@ int pk_profile_iterations(pk_plan* plan, const pk_solver_params* params, const v
 /* FP32 roofline denominator: FFMA throughput of `device` measured with a dependent-chain
  * microkernel (8 independent chains per thread, 148*4 CTAs), in TFLOP/s. */
 int pk_measure_fp32_peak(int32_t device, double* tflops_out);
+
+/* Explicit-matrix mode: a MeasurementMatrix given by its entries
+ * (read_matrix / PACTMAT, forward.py:70-121, 297-330) rather than by geometry.  Replaces the
+ * reference's numba GEMV cores for such a K: matvec_parallel / matvec_adjoint_parallel
+ * (kernels.py:195-202, 215-225, 319-350) and iterative_reconstruct's loop (recon.py:286-377).
+ * K is held on the device in the plan dtype (PK_F32 halves the bytes streamed per product);
+ * complex entries (frequency-domain K) are interleaved (re, im).
+ *   pk_dense_create        rows x cols operator; cols must fill whole 16-byte rows
+ *                          (PK_ERR_UNSUPPORTED otherwise)
+ *   pk_dense_set_entries   row-major fp64 (complex128) entries, host (on_device = 0) or
+ *                          device memory; converted to the plan dtype on the device
+ *   pk_dense_matvec        y = K x (x real, or complex if x_complex; y complex iff K or x is)
+ *   pk_dense_adjoint       out = scale K^H y (out complex iff K or y is)
+ *   pk_dense_reconstruct   the whole solve on the device (one captured graph, no host sync):
+ *                          y [rows] plan dtype (complex interleaved for complex K), x_out [nx*ny]
+ *                          real, hist [4][iterations] double, status [2] int32 (as pk_reconstruct).
+ *                          A real PK_F32 operator reads K once per iteration (the residual
+ *                          and the next gradient from one pass); otherwise two passes. */
+typedef struct pk_dense pk_dense;
+typedef struct pk_dense_info {
+    int64_t rows, cols;
+    int32_t dtype, complex_entries;
+    int32_t fused;           /* 1: one pass over K per solver iteration */
+    int32_t splits;          /* row splits of the adjoint's column partials */
+    int64_t device_bytes;
+} pk_dense_info;
+int pk_dense_create(int64_t rows, int64_t cols, int32_t dtype, int32_t complex_entries,
+                    int32_t device, pk_dense** out);
+int pk_dense_destroy(pk_dense* op);
+int pk_dense_get_info(const pk_dense* op, pk_dense_info* out);
+int pk_dense_set_entries(pk_dense* op, const double* entries, int32_t on_device, void* stream);
+/* Dense K of a geometry plan built on the device (build_time_matrix, forward.py:167-194):
+ * fp64 entries bit-identical to the reference's (the plan's fp64 delays), PK_F32 rounded. */
+int pk_dense_from_plan(pk_dense* op, const pk_plan* plan, void* stream);
+int pk_dense_matvec(pk_dense* op, const void* x_dev, int32_t x_complex, void* y_dev, void* stream);
+int pk_dense_adjoint(pk_dense* op, const void* y_dev, int32_t y_complex, void* out_dev, double scale,
+                     void* stream);
+int pk_dense_reconstruct(pk_dense* op, int32_t nx, int32_t ny, const pk_solver_params* params,
+                         const void* y_dev, void* x_out_dev, double* history_dev, int32_t* status_dev,
+                         void* stream);
 
 const char* pk_last_error(void);
 int pk_version(void);

@@ -14,6 +14,7 @@ from .device import (CudaPool, DeviceOperator, clear_plan_cache, default_pool, o
 from .measurement import (
     AcousticConfig,
     DenseOperator,
+    DeviceMatrix,
     MeasurementMatrix,
     SensorData,
     TruncationWarning,
@@ -21,6 +22,7 @@ from .measurement import (
     add_noise,
     build_freq_matrix,
     build_time_matrix,
+    dense_time_matrix,
     forward_project,
 )
 from .scene import (

@@ -20,6 +20,8 @@ SOURCES = [
     os.path.join(_PKG, "csrc", "pactgpu.cu"),
     os.path.join(_PKG, "csrc", "pk_kernels.cuh"),
     os.path.join(_PKG, "csrc", "pk_common.cuh"),
+    os.path.join(_PKG, "csrc", "pk_freq.cuh"),
+    os.path.join(_PKG, "csrc", "pk_dense.cuh"),
     os.path.join(_ROOT, "include", "pactgpu.h"),
 ]
 
@@ -87,6 +89,18 @@ class PlanInfo(ctypes.Structure):
     ]
 
 
+class DenseInfo(ctypes.Structure):
+    _fields_ = [
+        ("rows", ctypes.c_int64),
+        ("cols", ctypes.c_int64),
+        ("dtype", ctypes.c_int32),
+        ("complex_entries", ctypes.c_int32),
+        ("fused", ctypes.c_int32),
+        ("splits", ctypes.c_int32),
+        ("device_bytes", ctypes.c_int64),
+    ]
+
+
 class SolverParams(ctypes.Structure):
     _fields_ = [
         ("alpha", ctypes.c_double),
@@ -119,6 +133,7 @@ SYMBOLS = [
     ("pk_residual", ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     ("pk_adjoint_residual", ctypes.c_int, [_vp, _vp, ctypes.c_double, _vp]),
     ("pk_index_dump", ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp]),
+    ("pk_delay_census_f32", ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp]),
     ("pk_peer_handle", ctypes.c_int, [_vp, ctypes.c_char_p]),
     ("pk_peer_connect", ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_char_p]),
     ("pk_peer_buffer", ctypes.c_int, [_vp, ctypes.c_int32, ctypes.POINTER(_vp)]),
@@ -130,6 +145,16 @@ SYMBOLS = [
     ("pk_profile_iterations", ctypes.c_int,
      [_vp, ctypes.POINTER(SolverParams), _vp, ctypes.POINTER(ctypes.c_float), _ip, _vp]),
     ("pk_measure_fp32_peak", ctypes.c_int, [ctypes.c_int32, _dp]),
+    ("pk_dense_create", ctypes.c_int,
+     [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_vp)]),
+    ("pk_dense_destroy", ctypes.c_int, [_vp]),
+    ("pk_dense_get_info", ctypes.c_int, [_vp, ctypes.POINTER(DenseInfo)]),
+    ("pk_dense_set_entries", ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp]),
+    ("pk_dense_from_plan", ctypes.c_int, [_vp, _vp, _vp]),
+    ("pk_dense_matvec", ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, _vp]),
+    ("pk_dense_adjoint", ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, ctypes.c_double, _vp]),
+    ("pk_dense_reconstruct", ctypes.c_int,
+     [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(SolverParams), _vp, _vp, _vp, _vp, _vp]),
     ("pk_last_error", ctypes.c_char_p, []),
     ("pk_version", ctypes.c_int, []),
 ]

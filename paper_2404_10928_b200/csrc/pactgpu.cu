@@ -21,6 +21,7 @@
 #include "pactgpu.h"
 #include "pk_kernels.cuh"
 #include "pk_freq.cuh"
+#include "pk_dense.cuh"
 
 using namespace pk;
 
@@ -1450,6 +1451,22 @@ int pk_index_dump(pk_plan* p, int32_t ma, int32_t mb, int64_t* s0, double* frac,
     return PK_OK;
 }
 
+int pk_delay_census_f32(pk_plan* p, int32_t rule, int32_t ma, int32_t mb, int32_t* s0, float* frac,
+                        void* stream) {
+    if (!p || !s0 || !frac) return fail(PK_ERR_INVALID, "NULL argument");
+    if (ma < 0 || mb > p->M || ma >= mb) return fail(PK_ERR_INVALID, "bad sensor range");
+    if (rule < 0 || rule > 2) return fail(PK_ERR_INVALID, "rule must be 0, 1 or 2");
+    if (rule == 1 && !p->sym) return fail(PK_ERR_UNSUPPORTED, "plan has no symmetric back-projector");
+    if (rule == 2 && !p->fsym) return fail(PK_ERR_UNSUPPORTED, "plan has no symmetric projector");
+    if (rule > 0 && p->M != p->Mall) return fail(PK_ERR_INVALID, "symmetric rules need all sensors");
+    DeviceGuard g(p->device);
+    delay_census_f32_kernel<<<148 * 8, kThreads, 0, S(stream)>>>(
+        p->pxs, p->pys, p->sxs, p->sys, p->nx, p->P, p->M, ma, mb, rule, (float)p->Q + 1.5f,
+        p->fsym ? p->fsym_hx : 0.f, s0, frac);
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
 int pk_profile_iterations(pk_plan* p, const pk_solver_params* prm, const void* y, float* ms,
                           int32_t* launches, void* stream) {
     if (!p || !y || !ms) return fail(PK_ERR_INVALID, "NULL argument");
@@ -1520,6 +1537,411 @@ int pk_measure_fp32_peak(int32_t device, double* tflops) {
     if (e != cudaSuccess) return fail(PK_ERR_CUDA, "peak kernel failed: %s", cudaGetErrorString(e));
     const double flops = 2.0 * 8.0 * 16.0 * iters * (double)blocks * kThreads;
     *tflops = flops / (ms * 1e-3) / 1e12;
+    return PK_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Explicit-matrix mode (pk_dense_*; kernels in pk_dense.cuh)
+// ===========================================================================
+struct pk_dense {
+    int device = 0, dtype = PK_F32, cplx = 0, fused = 0;
+    int64_t rows = 0, cols = 0;
+    void* K = nullptr;             // rows x cols (x2 if complex), plan dtype, row-major
+    int splits = 1, gemv_grid = 0, fgrid = 0, fnv = 0, init_blocks = 0;
+    void* part = nullptr;          // gemvT partials [splits][cols (x2)]
+    void* fpart = nullptr;         // fused partials [fgrid][cols]
+    double* rpart = nullptr;       // sum |r|^2 partials
+    double* ipart = nullptr;       // [blocks][3] image sums of the stop kernel
+    void* xb[2] = {nullptr, nullptr};
+    void* rb = nullptr;            // residual (two-pass path)
+    void* ybuf = nullptr;          // y (plan dtype) of the captured solve
+    void* xout = nullptr;
+    double* hist = nullptr;
+    int hist_cap = 0;
+    int32_t* status = nullptr;
+    DenseState* st = nullptr;
+    DevParams* prm = nullptr;
+    cudaStream_t cap_stream = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int g_iters = -1, g_nx = -1, g_ny = -1;
+    int64_t device_bytes = 0;
+};
+
+namespace {
+
+template <typename T>
+int dalloc(pk_dense* d, T** ptr, size_t count) {
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(ptr), count * sizeof(T));
+    if (e != cudaSuccess)
+        return fail(PK_ERR_CUDA, "cudaMalloc(%zu) failed: %s", count * sizeof(T), cudaGetErrorString(e));
+    d->device_bytes += (int64_t)(count * sizeof(T));
+    return PK_OK;
+}
+
+size_t dsize(const pk_dense* d) { return d->dtype == PK_F32 ? 4 : 8; }
+int dense_E(const pk_dense* d) { return (int)(16 / (dsize(d) * (d->cplx ? 2 : 1))); }
+
+template <typename R>
+__global__ void narrow_kernel(const double* src, R* dst, size_t n) {
+    for (size_t q = (size_t)blockIdx.x * kThreads + threadIdx.x; q < n; q += (size_t)gridDim.x * kThreads)
+        dst[q] = (R)src[q];
+}
+
+int fused_nv(int64_t cols) {  // float4 groups per thread of the fused kernel
+    const int64_t nv = cols / 4;
+    for (int v : {1, 2, 4, 8, 12})
+        if (nv <= (int64_t)v * kFusedThreads) return v;
+    return 0;
+}
+
+template <typename R>
+int launch_gemv(pk_dense* d, const void* x0, const void* x1, int xc, const void* yobs, void* out0,
+                void* out1, double* part, const DenseState* st, cudaStream_t s) {
+    const R* K = static_cast<const R*>(d->K);
+#define PK_GEMV(KC, XC)                                                                        \
+    dense_gemv_kernel<R, KC, XC><<<d->gemv_grid, kDenseThreads, 0, s>>>(                     \
+        K, d->rows, d->cols, static_cast<const R*>(x0), static_cast<const R*>(x1),           \
+        static_cast<const R*>(yobs), static_cast<R*>(out0), static_cast<R*>(out1), part, st)
+    if (d->cplx) { if (xc) PK_GEMV(true, true); else PK_GEMV(true, false); }
+    else { if (xc) PK_GEMV(false, true); else PK_GEMV(false, false); }
+#undef PK_GEMV
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+template <typename R>
+int launch_gemvt(pk_dense* d, const void* y0, const void* y1, int yc, bool real, double sign,
+                 void* part, const DenseState* st, cudaStream_t s) {
+    const R* K = static_cast<const R*>(d->K);
+    const int64_t nvec = d->cols / dense_E(d);
+    dim3 grid((unsigned)((nvec + kDenseThreads - 1) / kDenseThreads), (unsigned)d->splits);
+#define PK_GEMVT(KC, YC, RE)                                                                  \
+    dense_gemvt_kernel<R, KC, YC, RE><<<grid, kDenseThreads, 0, s>>>(                         \
+        K, d->rows, d->cols, static_cast<const R*>(y0), static_cast<const R*>(y1), (R)sign,   \
+        static_cast<R*>(part), st)
+    if (d->cplx) {
+        if (yc) { if (real) PK_GEMVT(true, true, true); else PK_GEMVT(true, true, false); }
+        else { if (real) PK_GEMVT(true, false, true); else PK_GEMVT(true, false, false); }
+    } else {
+        if (yc) { if (real) PK_GEMVT(false, true, true); else PK_GEMVT(false, true, false); }
+        else PK_GEMVT(false, false, true);
+    }
+#undef PK_GEMVT
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+int fused_smem_attr(pk_dense* d) {  // set once at creation (not during graph capture)
+    const int smem = (int)(2 * d->cols * 4);
+    cudaError_t e = cudaSuccess;
+    switch (d->fnv) {
+        case 1: e = cudaFuncSetAttribute(dense_fused_f32_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+        case 2: e = cudaFuncSetAttribute(dense_fused_f32_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+        case 4: e = cudaFuncSetAttribute(dense_fused_f32_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+        case 8: e = cudaFuncSetAttribute(dense_fused_f32_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+        default: e = cudaFuncSetAttribute(dense_fused_f32_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+    }
+    if (e != cudaSuccess) return fail(PK_ERR_CUDA, "fused kernel attribute: %s", cudaGetErrorString(e));
+    return PK_OK;
+}
+
+int launch_fused(pk_dense* d, int use_state, cudaStream_t s) {
+    const size_t smem = (size_t)2 * d->cols * 4;
+#define PK_FUSED(NV)                                                                              \
+    do {                                                                                          \
+        dense_fused_f32_kernel<NV><<<d->fgrid, kFusedThreads, smem, s>>>(                         \
+            static_cast<const float*>(d->K), d->rows, (int)d->cols,                              \
+            static_cast<const float*>(d->xb[0]), static_cast<const float*>(d->xb[1]),            \
+            static_cast<const float*>(d->ybuf), static_cast<float*>(d->fpart), d->rpart, d->st,  \
+            use_state);                                                                           \
+    } while (0)
+    switch (d->fnv) {
+        case 1: PK_FUSED(1); break;
+        case 2: PK_FUSED(2); break;
+        case 4: PK_FUSED(4); break;
+        case 8: PK_FUSED(8); break;
+        default: PK_FUSED(12); break;
+    }
+#undef PK_FUSED
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+// the whole solve on `s` (captured into a graph by pk_dense_reconstruct)
+template <typename R>
+int record_dense(pk_dense* d, int nx, int ny, int iters, cudaStream_t s) {
+    const int P = nx * ny;
+    const int64_t nr = d->rows * (d->cplx ? 2 : 1);  // residual scalars
+    const int pb = (P + kDenseThreads - 1) / kDenseThreads;
+    const int stop_blocks = std::min(pb, 148 * 2);
+    R* xb0 = static_cast<R*>(d->xb[0]);
+    R* xb1 = static_cast<R*>(d->xb[1]);
+    if (d->fused) {
+        dense_init_kernel<R><<<pb, kDenseThreads, 0, s>>>(xb0, P, d->st, nullptr, nullptr, 0, nullptr);
+        PK_CHECK_LAUNCH();
+        PK_TRY(launch_fused(d, 0, s));  // r0 = -y: gradient partials and sum y^2
+        dense_stop_kernel<R><<<1, kDenseThreads, 0, s>>>(xb0, xb1, nx, ny, d->rpart, d->fgrid,
+                                                         d->ipart, d->prm, d->st, d->hist, d->status, 1);
+        PK_CHECK_LAUNCH();
+        for (int k = 0; k < iters; ++k) {
+            dense_update_kernel<R><<<pb, kDenseThreads, 0, s>>>(xb0, xb1, static_cast<const R*>(d->fpart),
+                                                                d->fgrid, nx, ny, d->prm, d->st);
+            PK_CHECK_LAUNCH();
+            PK_TRY(launch_fused(d, 1, s));
+            dense_stop_kernel<R><<<stop_blocks, kDenseThreads, 0, s>>>(
+                xb0, xb1, nx, ny, d->rpart, d->fgrid, d->ipart, d->prm, d->st, d->hist, d->status, 0);
+            PK_CHECK_LAUNCH();
+        }
+    } else {
+        const int ib = (int)std::max<int64_t>(pb, (nr + kDenseThreads - 1) / kDenseThreads);
+        dense_init_kernel<R><<<ib, kDenseThreads, 0, s>>>(xb0, P, d->st, static_cast<const R*>(d->ybuf),
+                                                          static_cast<R*>(d->rb), nr, d->rpart);
+        PK_CHECK_LAUNCH();
+        dense_stop_kernel<R><<<1, kDenseThreads, 0, s>>>(xb0, xb1, nx, ny, d->rpart, ib, d->ipart,
+                                                         d->prm, d->st, d->hist, d->status, 1);
+        PK_CHECK_LAUNCH();
+        for (int k = 0; k < iters; ++k) {
+            PK_TRY(launch_gemvt<R>(d, d->rb, d->rb, d->cplx, true, 1.0, d->part, d->st, s));
+            dense_update_kernel<R><<<pb, kDenseThreads, 0, s>>>(xb0, xb1, static_cast<const R*>(d->part),
+                                                                d->splits, nx, ny, d->prm, d->st);
+            PK_CHECK_LAUNCH();
+            PK_TRY(launch_gemv<R>(d, xb0, xb1, 0, d->ybuf, d->rb, d->rb, d->rpart, d->st, s));
+            dense_stop_kernel<R><<<stop_blocks, kDenseThreads, 0, s>>>(
+                xb0, xb1, nx, ny, d->rpart, d->gemv_grid, d->ipart, d->prm, d->st, d->hist, d->status, 0);
+            PK_CHECK_LAUNCH();
+        }
+    }
+    dense_copy_out_kernel<R><<<pb, kDenseThreads, 0, s>>>(xb0, xb1, d->st, static_cast<R*>(d->xout), P);
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pk_dense_create(int64_t rows, int64_t cols, int32_t dtype, int32_t complex_entries,
+                    int32_t device, pk_dense** out) {
+    if (!out) return fail(PK_ERR_INVALID, "NULL argument");
+    *out = nullptr;
+    if (rows < 1 || cols < 1) return fail(PK_ERR_INVALID, "matrix must be at least 1 x 1");
+    if (dtype != PK_F32 && dtype != PK_F64) return fail(PK_ERR_INVALID, "bad dtype %d", dtype);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(PK_ERR_CUDA, "no CUDA device available (the B200 kernels have no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(PK_ERR_INVALID, "bad device %d", device);
+    DeviceGuard g(device);
+    pk_dense* d = new pk_dense();
+    d->device = device;
+    d->dtype = dtype;
+    d->cplx = complex_entries ? 1 : 0;
+    d->rows = rows;
+    d->cols = cols;
+    if (cols % dense_E(d) != 0) {
+        delete d;
+        return fail(PK_ERR_UNSUPPORTED, "columns (%lld) must be a multiple of %d (16-byte rows)",
+                    (long long)cols, dense_E(d));
+    }
+    const int sms = 148;
+    d->gemv_grid = sms * 8;
+    const int64_t tiles = (cols / dense_E(d) + kDenseThreads - 1) / kDenseThreads;
+    d->splits = (int)std::max<int64_t>(1, std::min<int64_t>(rows, (4 * sms + tiles - 1) / tiles));
+    d->fnv = fused_nv(cols);
+    d->fused = (dtype == PK_F32 && !d->cplx && cols % 4 == 0 && d->fnv > 0 &&
+                2 * cols * 4 <= 200 * 1024 && !getenv("PK_DENSE_TWOPASS")) ? 1 : 0;
+    d->fgrid = sms;
+    const size_t es = dsize(d) * (d->cplx ? 2 : 1);
+    int rc = PK_OK;
+    auto A = [&](int r) { if (rc == PK_OK) rc = r; };
+    A(dalloc(d, reinterpret_cast<unsigned char**>(&d->K), (size_t)rows * cols * es));
+    A(dalloc(d, reinterpret_cast<unsigned char**>(&d->part), (size_t)d->splits * cols * es));
+    if (d->fused) A(dalloc(d, reinterpret_cast<unsigned char**>(&d->fpart), (size_t)d->fgrid * cols * 4));
+    const int64_t nr = rows * (d->cplx ? 2 : 1);
+    const int64_t rp = std::max<int64_t>({(int64_t)d->gemv_grid, (int64_t)d->fgrid,
+                                          (nr + kDenseThreads - 1) / kDenseThreads,
+                                          (cols + kDenseThreads - 1) / kDenseThreads});
+    A(dalloc(d, &d->rpart, (size_t)rp));
+    A(dalloc(d, reinterpret_cast<unsigned char**>(&d->ybuf), (size_t)rows * es));
+    A(dalloc(d, reinterpret_cast<unsigned char**>(&d->rb), (size_t)rows * es));
+    A(dalloc(d, &d->st, 1));
+    A(dalloc(d, &d->prm, 1));
+    A(dalloc(d, &d->status, 2));
+    if (rc == PK_OK && cudaStreamCreateWithFlags(&d->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+        rc = fail(PK_ERR_CUDA, "stream creation failed");
+    if (rc == PK_OK && d->fused) rc = fused_smem_attr(d);
+    if (rc != PK_OK) {
+        pk_dense_destroy(d);
+        return rc;
+    }
+    *out = d;
+    return PK_OK;
+}
+
+int pk_dense_destroy(pk_dense* d) {
+    if (!d) return PK_OK;
+    DeviceGuard g(d->device);
+    void* ptrs[] = {d->K, d->part, d->fpart, d->rpart, d->ipart, d->xb[0], d->xb[1], d->rb,
+                    d->ybuf, d->xout, d->hist, d->status, d->st, d->prm};
+    for (void* q : ptrs)
+        if (q) cudaFree(q);
+    if (d->exec) cudaGraphExecDestroy(d->exec);
+    if (d->cap_stream) cudaStreamDestroy(d->cap_stream);
+    delete d;
+    return PK_OK;
+}
+
+int pk_dense_get_info(const pk_dense* d, pk_dense_info* o) {
+    if (!d || !o) return fail(PK_ERR_INVALID, "NULL argument");
+    o->rows = d->rows;
+    o->cols = d->cols;
+    o->dtype = d->dtype;
+    o->complex_entries = d->cplx;
+    o->fused = d->fused;
+    o->splits = d->splits;
+    o->device_bytes = d->device_bytes;
+    return PK_OK;
+}
+
+int pk_dense_set_entries(pk_dense* d, const double* entries, int32_t on_device, void* stream) {
+    if (!d || !entries) return fail(PK_ERR_INVALID, "NULL argument");
+    DeviceGuard g(d->device);
+    cudaStream_t s = S(stream);
+    const size_t n = (size_t)d->rows * d->cols * (d->cplx ? 2 : 1);  // scalars
+    if (d->dtype == PK_F64) {
+        PK_CUDA(cudaMemcpyAsync(d->K, entries, n * 8, on_device ? cudaMemcpyDeviceToDevice
+                                                                 : cudaMemcpyHostToDevice, s));
+        return PK_OK;
+    }
+    // fp32 plan: convert in chunks through a device staging buffer
+    const size_t chunk = std::min(n, (size_t)32 << 20);
+    double* stage = nullptr;
+    if (!on_device) PK_CUDA(cudaMallocAsync(&stage, chunk * 8, s));
+    for (size_t off = 0; off < n; off += chunk) {
+        const size_t m = std::min(chunk, n - off);
+        const double* src = entries + off;
+        if (!on_device) {
+            PK_CUDA(cudaMemcpyAsync(stage, src, m * 8, cudaMemcpyHostToDevice, s));
+            src = stage;
+        }
+        narrow_kernel<float><<<148 * 8, kThreads, 0, s>>>(src, static_cast<float*>(d->K) + off, m);
+        PK_CHECK_LAUNCH();
+    }
+    if (stage) PK_CUDA(cudaFreeAsync(stage, s));
+    return PK_OK;
+}
+
+int pk_dense_from_plan(pk_dense* d, const pk_plan* p, void* stream) {
+    if (!d || !p) return fail(PK_ERR_INVALID, "NULL argument");
+    if (d->cplx) return fail(PK_ERR_INVALID, "the time-domain matrix is real");
+    if (p->M != p->Mall || (int64_t)p->M * p->Q != d->rows || (int64_t)p->P != d->cols)
+        return fail(PK_ERR_INVALID, "plan (%d sensors x %d samples, %d pixels) does not match the %lld x %lld matrix",
+                    p->M, p->Q, p->P, (long long)d->rows, (long long)d->cols);
+    if (p->device != d->device) return fail(PK_ERR_INVALID, "plan and matrix live on different devices");
+    DeviceGuard g(d->device);
+    cudaStream_t s = S(stream);
+    PK_CUDA(cudaMemsetAsync(d->K, 0, (size_t)d->rows * d->cols * dsize(d), s));
+    if (d->dtype == PK_F32)
+        dense_from_geometry_kernel<float><<<148 * 8, kDenseThreads, 0, s>>>(
+            p->px, p->py, p->sx, p->sy, p->cdt, p->w, p->nx, p->P, p->M, p->Q, static_cast<float*>(d->K));
+    else
+        dense_from_geometry_kernel<double><<<148 * 8, kDenseThreads, 0, s>>>(
+            p->px, p->py, p->sx, p->sy, p->cdt, p->w, p->nx, p->P, p->M, p->Q, static_cast<double*>(d->K));
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+int pk_dense_matvec(pk_dense* d, const void* x, int32_t x_complex, void* y, void* stream) {
+    if (!d || !x || !y) return fail(PK_ERR_INVALID, "NULL argument");
+    DeviceGuard g(d->device);
+    cudaStream_t s = S(stream);
+    if (d->dtype == PK_F32) return launch_gemv<float>(d, x, x, x_complex, nullptr, y, y, nullptr, nullptr, s);
+    return launch_gemv<double>(d, x, x, x_complex, nullptr, y, y, nullptr, nullptr, s);
+}
+
+int pk_dense_adjoint(pk_dense* d, const void* y, int32_t y_complex, void* out, double scale,
+                     void* stream) {
+    if (!d || !y || !out) return fail(PK_ERR_INVALID, "NULL argument");
+    DeviceGuard g(d->device);
+    cudaStream_t s = S(stream);
+    const bool oc = d->cplx || y_complex;
+    const int64_t n = d->cols * (oc ? 2 : 1);
+    const unsigned blocks = (unsigned)((n + kDenseThreads - 1) / kDenseThreads);
+    if (d->dtype == PK_F32) {
+        PK_TRY(launch_gemvt<float>(d, y, y, y_complex, false, 1.0, d->part, nullptr, s));
+        dense_reduce_kernel<float><<<blocks, kDenseThreads, 0, s>>>(
+            static_cast<const float*>(d->part), d->splits, n, (float)scale, static_cast<float*>(out));
+    } else {
+        PK_TRY(launch_gemvt<double>(d, y, y, y_complex, false, 1.0, d->part, nullptr, s));
+        dense_reduce_kernel<double><<<blocks, kDenseThreads, 0, s>>>(
+            static_cast<const double*>(d->part), d->splits, n, scale, static_cast<double*>(out));
+    }
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+int pk_dense_reconstruct(pk_dense* d, int32_t nx, int32_t ny, const pk_solver_params* prm,
+                         const void* y, void* x_out, double* hist, int32_t* status, void* stream) {
+    if (!d || !prm || !y || !x_out || !hist || !status) return fail(PK_ERR_INVALID, "NULL argument");
+    if (nx < 1 || ny < 1 || (int64_t)nx * ny != d->cols)
+        return fail(PK_ERR_INVALID, "grid %d x %d does not match %lld columns", nx, ny, (long long)d->cols);
+    if (prm->iterations < 1) return fail(PK_ERR_INVALID, "iterations must be >= 1");
+    if (!(prm->tv_epsilon > 0)) return fail(PK_ERR_INVALID, "tv_epsilon must be > 0");
+    if (!(prm->alpha >= 0) || !(prm->beta >= 0)) return fail(PK_ERR_INVALID, "alpha and beta must be >= 0");
+    if (!(prm->step > 0)) return fail(PK_ERR_INVALID, "step must be > 0");
+    DeviceGuard g(d->device);
+    cudaStream_t s = S(stream);
+    const int P = nx * ny;
+    const size_t ts = dsize(d);
+    if (!d->xb[0]) {
+        PK_TRY(dalloc(d, reinterpret_cast<unsigned char**>(&d->xb[0]), (size_t)P * ts));
+        PK_TRY(dalloc(d, reinterpret_cast<unsigned char**>(&d->xb[1]), (size_t)P * ts));
+        PK_TRY(dalloc(d, reinterpret_cast<unsigned char**>(&d->xout), (size_t)P * ts));
+        PK_TRY(dalloc(d, &d->ipart, (size_t)3 * 148 * 2));
+    }
+    if (d->hist_cap < prm->iterations) {
+        if (d->hist) cudaFree(d->hist);
+        d->hist = nullptr;
+        PK_TRY(dalloc(d, &d->hist, (size_t)4 * prm->iterations));
+        d->hist_cap = prm->iterations;
+        if (d->exec) { cudaGraphExecDestroy(d->exec); d->exec = nullptr; }
+        d->g_iters = -1;
+    }
+    DevParams dp{};
+    for (int f = 0; f < kMaxFrames; ++f) {
+        dp.alpha[f] = prm->alpha;
+        dp.beta[f] = prm->beta;
+        dp.step[f] = prm->step;
+        dp.eta_alpha[f] = prm->step * prm->alpha;
+    }
+    dp.eps = prm->tv_epsilon;
+    dp.tolerance = prm->tolerance;
+    dp.iterations = prm->iterations;
+    dp.nonneg = prm->nonneg ? 1 : 0;
+    PK_CUDA(cudaMemcpyAsync(d->prm, &dp, sizeof(dp), cudaMemcpyHostToDevice, s));
+    PK_CUDA(cudaMemcpyAsync(d->ybuf, y, (size_t)d->rows * ts * (d->cplx ? 2 : 1), cudaMemcpyDeviceToDevice, s));
+    if (!d->exec || d->g_iters != prm->iterations || d->g_nx != nx || d->g_ny != ny) {
+        if (d->exec) { cudaGraphExecDestroy(d->exec); d->exec = nullptr; }
+        PK_CUDA(cudaStreamBeginCapture(d->cap_stream, cudaStreamCaptureModeThreadLocal));
+        const int rc = d->dtype == PK_F32 ? record_dense<float>(d, nx, ny, prm->iterations, d->cap_stream)
+                                          : record_dense<double>(d, nx, ny, prm->iterations, d->cap_stream);
+        cudaGraph_t gr = nullptr;
+        cudaError_t e = cudaStreamEndCapture(d->cap_stream, &gr);
+        if (rc != PK_OK) { if (gr) cudaGraphDestroy(gr); return rc; }
+        if (e != cudaSuccess) return fail(PK_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+        e = cudaGraphInstantiate(&d->exec, gr, 0);
+        cudaGraphDestroy(gr);
+        if (e != cudaSuccess) return fail(PK_ERR_CUDA, "graph instantiation failed: %s", cudaGetErrorString(e));
+        d->g_iters = prm->iterations;
+        d->g_nx = nx;
+        d->g_ny = ny;
+    }
+    PK_CUDA(cudaGraphLaunch(d->exec, s));
+    PK_CUDA(cudaMemcpyAsync(x_out, d->xout, (size_t)P * ts, cudaMemcpyDeviceToDevice, s));
+    PK_CUDA(cudaMemcpyAsync(hist, d->hist, (size_t)4 * prm->iterations * 8, cudaMemcpyDeviceToDevice, s));
+    PK_CUDA(cudaMemcpyAsync(status, d->status, 2 * 4, cudaMemcpyDeviceToDevice, s));
     return PK_OK;
 }
 

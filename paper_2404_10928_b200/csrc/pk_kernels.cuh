@@ -2066,6 +2066,70 @@ __global__ void index_dump_kernel(const double* px, const double* py, const doub
     }
 }
 
+// fp32 delay census (verification): the delay s0 / frac the fp32 production kernels use for
+// every pair (p, m) of local sensors [ma, mb), in layout [(m - ma)][p].  rule 0: the generic
+// K1 / K2 delay (pixel and sensor coordinates scaled by 1/(c dt), bp_f32_kernel /
+// fp_f32_kernel); rule 1: K1s -- the delay of the D4 representative pair (tile-level octant of
+// the quadrant, bp_sym_f32_kernel / sym_chunk); rule 2: K2s -- the delay of the rotation
+// representative in the quadrant, column derived from its 32-pixel piece (fs_delay).
+__global__ void delay_census_f32_kernel(const float* pxs, const float* pys, const float* sxs,
+                                        const float* sys, int n_x, int P, int M, int ma, int mb,
+                                        int rule, float qclamp, float hx, int32_t* s0_out,
+                                        float* frac_out) {
+    const size_t total = (size_t)(mb - ma) * P;
+    for (size_t q = (size_t)blockIdx.x * kThreads + threadIdx.x; q < total;
+         q += (size_t)gridDim.x * kThreads) {
+        const int m = ma + (int)(q / P);
+        const int p = (int)(q % P);
+        const int i = p % n_x, j = p / n_x;
+        float tb, fr;
+        if (rule == 0) {
+            const float ex = pxs[i] - sxs[m], ey = pys[j] - sys[m];
+            const float u = fminf(sqrt_approx(fmaf(ex, ex, ey * ey)), qclamp);
+            tb = __fadd_rd(u, kTwo23);
+            fr = u - (tb - kTwo23);
+        } else if (rule == 1) {
+            // the representative c (tile tx >= ty of the quadrant) and the group element g with
+            // sym_pixel(g, c) = p (reflections only for off-diagonal tiles)
+            const int n = n_x, h = n >> 1;
+            int ci = 0, cj = 0, gg = -1;
+            for (int a = 0; a < 8 && gg < 0; ++a) {
+                int oi, oj;
+                sym_pixel(a, i, j, n, oi, oj);  // orbit of p
+                if (oi < h || oj < h) continue;
+                const int tx = (oi - h) / kSymTile, ty = (oj - h) / kSymTile;
+                if (tx < ty) continue;
+                for (int g = 0; g < 8; ++g) {
+                    if (tx == ty && g >= 4) break;
+                    int ri, rj;
+                    sym_pixel(g, oi, oj, n, ri, rj);
+                    if (ri == i && rj == j) { ci = oi; cj = oj; gg = g; break; }
+                }
+            }
+            const int qm = M >> 2;
+            int mbase = gg < 4 ? m - gg * qm : (gg - 4) * qm - m;
+            mbase %= M;
+            if (mbase < 0) mbase += M;
+            const float ex = pxs[ci] - sxs[mbase], ey = pys[cj] - sys[mbase];
+            const float u = fminf(sqrt_approx(fmaf(ex, ex, ey * ey)), qclamp);
+            tb = __fadd_rd(u, kTwo23);
+            fr = u - (tb - kTwo23);
+        } else {
+            const int n = n_x, h = n >> 1;
+            const int ri = sym_rot_index(i, j, n);
+            const int r = ri & 3, qq = ri >> 2;
+            const int qi = h + qq % h, qj = h + qq / h;
+            int mbase = (m - r * (M >> 2)) % M;
+            if (mbase < 0) mbase += M;
+            const int c0 = h + 32 * ((qi - h) / 32);
+            const float ey = pys[qj] - sys[mbase];
+            tb = fs_delay<true>((float)(qi - c0), hx, pxs[c0] - sxs[mbase], ey * ey, qclamp, fr);
+        }
+        s0_out[q] = (int32_t)(__float_as_uint(tb) - kTwo23Bits);
+        frac_out[q] = fr;
+    }
+}
+
 // fp64 -> plan dtype conversion and back (host API)
 template <typename T>
 __global__ void convert_kernel(const double* src, T* dst, size_t n) {

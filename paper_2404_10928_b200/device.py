@@ -421,6 +421,20 @@ class DeviceOperator:
                                               float(scale), self.stream()))
         return out
 
+    def delay_census(self, rule: int, ma: int = 0, mb: int | None = None):
+        """fp32 (s0, frac) of the production kernels' delay rule (0 generic, 1 D4-symmetric
+        back-projector, 2 rotation-symmetric projector) for local sensors [ma, mb), as device
+        tensors [(mb-ma), P] (verification: pk_delay_census_f32)."""
+        torch = _torch()
+        mb = self.sensors if mb is None else mb
+        n = (mb - ma) * self.pixels
+        s0 = torch.empty(n, device=self.device, dtype=torch.int32)
+        fr = torch.empty(n, device=self.device, dtype=torch.float32)
+        with torch.cuda.device(self.device):
+            N.check(self._lib.pk_delay_census_f32(self._h, int(rule), ma, mb, s0.data_ptr(),
+                                                  fr.data_ptr(), self.stream()))
+        return s0.view(mb - ma, self.pixels), fr.view(mb - ma, self.pixels)
+
     def index_dump(self, ma: int = 0, mb: int | None = None):
         """fp64 (s0, frac) for local sensors [ma, mb) as device tensors [(mb-ma), P]."""
         torch = _torch()

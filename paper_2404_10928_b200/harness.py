@@ -34,6 +34,7 @@ MEASUREMENT_FLOOR_SECONDS = 1e-4  # bench.py:30-31
 REFERENCE_TIMES = {"bp_seconds": 2.277, "ir_cpu_seconds": 118.470, "ir_gpu_seconds": 20.062,
                    "gpu_speedup": 5.9, "gradient_share_percent": 96.7}
 VERIFY_REL_L2 = 1e-4  # north_star: fp32 image within 1e-4 relative L2 of the fp64 result
+VERIFY_REL_L2_F64 = 1e-10  # fp64 validation mode against a reference fp64 solver
 
 
 def _sha(a: np.ndarray) -> str:
@@ -130,10 +131,16 @@ def _scene(grid_size, sensors, samples, seed, config, device):
 
 
 def bench_recon(grid_size: int, sensors: int, samples: int, config: ReconConfig, reps: int = 5,
-                seed: int = 0, device: int = 0) -> BenchReport:
+                seed: int = 0, device: int = 0, reference=None) -> BenchReport:
     """Back-projection against iterative reconstruction on one scene (bench.py:206-288), on
     the device: entries back_projection (fp32), iterative_device_f64 (the fp64 validation
-    solver, the baseline) and iterative_device (fp32, verified against it)."""
+    solver) and iterative_device (fp32, verified against the fp64 solver).
+
+    ``reference``, optional, plays the reference's serial kernels (bench.py:230-235): a
+    callable ``reference(K, y, config) -> image values`` run once on the same scene with the
+    pinned config (e.g. the reference package itself, or a CPU restatement of it).  It then
+    becomes the baseline entry ``iterative_reference``: the fp64 device image is verified
+    against it at 1e-10 and the fp32 image at 1e-4 (relative L2)."""
     grid, ring, ac, phantom, K, y, config = _scene(grid_size, sensors, samples, seed, config, device)
     f32, f64 = CudaPool(device, "float32"), CudaPool(device, "float64")
 
@@ -159,10 +166,19 @@ def bench_recon(grid_size: int, sensors: int, samples: int, config: ReconConfig,
                                  iterations=config.iterations),
         metrics={"rmse_bp": norm_rmse(bp.values), "rmse_ir": norm_rmse(ir32.image.values),
                  "rel_l2_f32_vs_f64": dev, "reference_times": REFERENCE_TIMES})
+    ok64 = None
+    ok32 = dev <= VERIFY_REL_L2
+    if reference is not None:
+        t0 = time.perf_counter()
+        ref_img = np.asarray(reference(K, y, config), dtype=np.float64).ravel()
+        t_ref = time.perf_counter() - t0
+        e64, e32 = _rel_l2(ir64.image.values, ref_img), _rel_l2(ir32.image.values, ref_img)
+        ok64, ok32 = e64 <= VERIFY_REL_L2_F64, ok32 and e32 <= VERIFY_REL_L2
+        rep.metrics.update({"rel_l2_f64_vs_reference": e64, "rel_l2_f32_vs_reference": e32})
+        rep.entries.append(BenchEntry("iterative_reference", t_ref, 1, _sha(ref_img)))
     rep.entries += [BenchEntry("back_projection", t_bp, reps, _sha(bp.values)),
-                    BenchEntry("iterative_device_f64", t_64, reps, _sha(ir64.image.values)),
-                    BenchEntry("iterative_device", t_32, reps, _sha(ir32.image.values),
-                               dev <= VERIFY_REL_L2)]
+                    BenchEntry("iterative_device_f64", t_64, reps, _sha(ir64.image.values), ok64),
+                    BenchEntry("iterative_device", t_32, reps, _sha(ir32.image.values), ok32)]
     for base, cand, tb, tc in (("back_projection", "iterative_device", t_bp, t_32),
                                ("iterative_device_f64", "iterative_device", t_64, t_32)):
         rep.speedups.append({"baseline": base, "candidate": cand, "speedup": tb / tc,

@@ -7,8 +7,8 @@ geometry-backed ``MeasurementMatrix`` whose products run matrix-free on the B200
 512^2 x 512 x 2048 -- is only formed if ``.entries`` is explicitly requested.
 
 Explicit matrices (``MeasurementMatrix(domain, entries)`` without provenance, e.g. read
-from a PACTMAT file) are supported through ``DenseOperator`` -- a cuBLAS GEMV on the
-device.
+from a PACTMAT file) are supported through ``DenseOperator`` -- hand-written streaming
+GEMV kernels and a device-resident solver loop (pk_dense_*).
 """
 
 from __future__ import annotations
@@ -33,6 +33,8 @@ __all__ = [
     "forward_project",
     "add_noise",
     "device_operator",
+    "DeviceMatrix",
+    "dense_time_matrix",
 ]
 
 DEFAULT_SOUND_SPEED = 1500.0  # m/s (forward.py:32)
@@ -262,37 +264,167 @@ class FreqOperator:
 
 
 class DenseOperator:
-    """Explicit matrix on the device; products are cuBLAS GEMV (torch.mv)."""
+    """Explicit matrix on the device: the C ABI's pk_dense_* -- K held in
+    HBM in the pool's dtype, hand-written streaming GEMV / GEMV^H kernels, and the whole
+    solver loop on the device (``reconstruct``; one pass over K per iteration for real fp32
+    K).  Replaces the reference's numba GEMV cores for a K given by its entries
+    (kernels.py:195-225, read_matrix forward.py:303-312)."""
 
-    def __init__(self, entries: np.ndarray, pool: CudaPool):
+    def __init__(self, entries: np.ndarray | None, pool: CudaPool, shape=None, cplx: bool = False):
+        import ctypes
+
         import torch
 
+        from . import _native as N
         from .device import _require_cuda
 
         _require_cuda(pool.device)
+        self._N, self._lib = N, N.load()
         self.pool = pool
         self.device = torch.device("cuda", pool.device)
-        cplx = np.iscomplexobj(entries)
+        self.cplx = bool(np.iscomplexobj(entries)) if entries is not None else bool(cplx)
         if pool.dtype == "float32":
-            self.tdtype = torch.complex64 if cplx else torch.float32
+            self.rdtype = torch.float32
+            self.tdtype = torch.complex64 if self.cplx else torch.float32
         else:
-            self.tdtype = torch.complex128 if cplx else torch.float64
-        self.A = torch.from_numpy(np.ascontiguousarray(entries)).to(self.device, self.tdtype)
-        self.rows, self.cols = entries.shape
+            self.rdtype = torch.float64
+            self.tdtype = torch.complex128 if self.cplx else torch.float64
+        self.rows, self.cols = entries.shape if entries is not None else shape
+        h = ctypes.c_void_p()
+        N.check(self._lib.pk_dense_create(self.rows, self.cols, pool.pk_dtype, int(self.cplx),
+                                          pool.device, ctypes.byref(h)))
+        self._h = h
+        if entries is not None:
+            e = np.ascontiguousarray(entries, dtype=np.complex128 if self.cplx else np.float64)
+            with torch.cuda.device(self.device):
+                N.check(self._lib.pk_dense_set_entries(self._h, e.ctypes.data, 0, self._stream()))
+                torch.cuda.current_stream(self.device).synchronize()
+        info = N.DenseInfo()
+        N.check(self._lib.pk_dense_get_info(self._h, ctypes.byref(info)))
+        self.info = info
+
+    @classmethod
+    def from_geometry(cls, grid, ring, acoustic, pool: CudaPool) -> "DenseOperator":
+        """The time-domain K of build_time_matrix (forward.py:167-194) formed on the device
+        (pk_dense_from_plan): fp64 entries bit-identical to the reference's dense K, without a
+        host copy (config 1's K is 17.2 GB)."""
+        import torch
+
+        op = cls(None, pool, shape=(ring.count * acoustic.q_s, grid.size))
+        plan = operator_for(grid, ring, acoustic, CudaPool(pool.device, "float64"))
+        with torch.cuda.device(op.device):
+            op._N.check(op._lib.pk_dense_from_plan(op._h, plan.handle, op._stream()))
+            torch.cuda.current_stream(op.device).synchronize()
+        return op
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.pk_dense_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown ordering
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _stream(self):
+        import ctypes
+
+        import torch
+
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
     def tensor(self, a):
         import torch
 
         if isinstance(a, torch.Tensor):
-            return a.to(device=self.device, dtype=self.tdtype)
+            return a.to(device=self.device, dtype=self.tdtype).contiguous()
         return torch.from_numpy(np.ascontiguousarray(a)).to(self.device, self.tdtype)
 
+    def _vec(self, a, n: int, what: str):
+        """Device vector in the plan's real or complex dtype (complex only if a is complex)."""
+        import torch
+
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+        c = t.is_complex()
+        t = t.to(device=self.device, dtype=(torch.complex64 if self.rdtype == torch.float32
+                                            else torch.complex128) if c else self.rdtype).contiguous()
+        if t.numel() != n:
+            raise ValueError(f"matrix has {n} {what} but vector has {t.numel()} values")
+        return t, c
+
     def matvec(self, x):
-        return self.A @ self.tensor(x)
+        import torch
+
+        xt, xc = self._vec(x, self.cols, "columns")
+        cd = torch.complex64 if self.rdtype == torch.float32 else torch.complex128
+        out = torch.empty(self.rows, device=self.device, dtype=cd if (self.cplx or xc) else self.rdtype)
+        with torch.cuda.device(self.device):
+            self._N.check(self._lib.pk_dense_matvec(self._h, xt.data_ptr(), int(xc), out.data_ptr(),
+                                                    self._stream()))
+        return out
 
     def adjoint(self, y, scale: float = 1.0):
-        out = self.A.conj().T @ self.tensor(y)
-        return out * scale if scale != 1.0 else out
+        import torch
+
+        yt, yc = self._vec(y, self.rows, "rows")
+        oc = self.cplx or yc
+        cd = torch.complex64 if self.rdtype == torch.float32 else torch.complex128
+        out = torch.empty(self.cols, device=self.device, dtype=cd if oc else self.rdtype)
+        with torch.cuda.device(self.device):
+            self._N.check(self._lib.pk_dense_adjoint(self._h, yt.data_ptr(), int(yc), out.data_ptr(),
+                                                     float(scale), self._stream()))
+        return out
+
+    def reconstruct(self, y, params, nx: int, ny: int):
+        """Device-resident solve (pk_dense_reconstruct): (x [P], history [4, N], status [2])."""
+        import ctypes
+
+        import torch
+
+        yt, yc = self._vec(y, self.rows, "rows")
+        if yc != self.cplx:
+            raise ValueError("signal and matrix must both be real or both complex")
+        n = int(params.iterations)
+        x = torch.empty(self.cols, device=self.device, dtype=self.rdtype)
+        hist = torch.zeros(4 * n, device=self.device, dtype=torch.float64)
+        status = torch.zeros(2, device=self.device, dtype=torch.int32)
+        with torch.cuda.device(self.device):
+            self._N.check(self._lib.pk_dense_reconstruct(
+                self._h, int(nx), int(ny), ctypes.byref(params), yt.data_ptr(), x.data_ptr(),
+                hist.data_ptr(), status.data_ptr(), self._stream()))
+        return x, hist.view(4, n), status
+
+
+class DeviceMatrix:
+    """An explicit K resident on the device (its entries are never on the host): the
+    MeasurementMatrix surface the public API reads (domain, rows, cols, grid, layout) over a
+    DenseOperator.  ``dense_time_matrix`` makes one from a geometry."""
+
+    def __init__(self, op: DenseOperator, domain: str, grid=None, layout=None):
+        self.dense_operator = op
+        self.domain = domain
+        self.rows, self.cols = op.rows, op.cols
+        self.provenance = {"grid": grid} if grid is not None else {}
+        self._layout = layout
+
+    @property
+    def grid(self):
+        return self.provenance.get("grid")
+
+    def layout(self) -> tuple[int, int]:
+        if self._layout is None:
+            raise ValueError("matrix has no builder provenance; pass the layout explicitly")
+        return self._layout
+
+
+def dense_time_matrix(grid, ring, acoustic, pool: CudaPool) -> DeviceMatrix:
+    """build_time_matrix's explicit dense K (forward.py:167-215), formed on the device in the
+    pool's dtype; its products and solves run the explicit-matrix kernels (pk_dense_*)."""
+    check_enclosure(grid, ring)
+    op = DenseOperator.from_geometry(grid, ring, acoustic, pool)
+    return DeviceMatrix(op, "time", grid, (ring.count, acoustic.q_s))
 
 
 _dense_cache: dict = {}
@@ -323,6 +455,9 @@ def device_operator(K, pool=None):
     ``pactkit.forward.MeasurementMatrix`` (duck-typed on .provenance / .entries).
     """
     pool = _as_pool(pool)
+    dense = getattr(K, "dense_operator", None)
+    if dense is not None:  # device-resident explicit K (DeviceMatrix)
+        return dense
     prov = getattr(K, "provenance", {}) or {}
     if geometry_path(K) == "time":
         return operator_for(prov["grid"], prov["ring"], prov["acoustic"], pool)

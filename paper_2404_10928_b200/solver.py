@@ -303,8 +303,8 @@ def objective(K, x, y, config: ReconConfig, pool=None) -> ObjectiveParts:
 
 
 def _dense_loop(op, yv, alpha, beta, eta, config, shape):
-    """Explicit-matrix (cuBLAS GEMV) and frequency-domain (matrix-free) operators: the same
-    loop with device products and host stopping checks."""
+    """Frequency-domain (matrix-free) operator: the loop with device products and host
+    stopping checks."""
     import torch
 
     dev = op.device
@@ -383,6 +383,13 @@ def iterative_reconstruct(K, y, config: ReconConfig, grid=None, pool=None,
         h = hist.cpu().numpy()[0][:, :n].T
         stopped_by = N.STOPPED_BY[int(status[1])]
         xv = x[0].double().cpu().numpy()
+    elif isinstance(op, DenseOperator):  # explicit K: the device loop of pk_dense_reconstruct
+        x, hist, status = op.reconstruct(y.values, solver_params(config, alpha, beta, eta), g.nx, g.ny)
+        status = status.cpu().numpy()
+        n = int(status[0])
+        h = hist.cpu().numpy()[:, :n].T
+        stopped_by = N.STOPPED_BY[int(status[1])]
+        xv = x.double().cpu().numpy()
     else:
         xv, h, stopped_by = _dense_loop(op, y.values, alpha, beta, eta, config, (g.ny, g.nx))
         n = h.shape[0]

@@ -50,3 +50,22 @@ def test_profile_breakdown_device():
     assert rep.breakdown["gradient_products"]["seconds"] > 0
     assert rep.metrics["iterations_run"] == 6 and rep.metrics["kernel_launches"] > 0
     assert rep.entry("iterative_run").wall_seconds > 0
+
+
+@pytest.mark.gpu
+def test_bench_recon_verified_against_oracle(oracle):
+    """The harness's verification with the CPU oracle in the reference's serial-kernel role
+    (bench.py:230-235): fp64 device image <= 1e-10, fp32 <= 1e-4 of the oracle's."""
+
+    def ref(K, y, cfg):
+        o = oracle.Operator(*K.grid.axis_vectors(), K.ring.positions, K.acoustic.c,
+                            K.acoustic.dt, K.acoustic.q_s)
+        return oracle.reconstruct(o, y.values, cfg.alpha, cfg.beta, cfg.step, cfg.iterations)["image"]
+
+    rep = pk.bench_recon(64, 32, 128, pk.ReconConfig(iterations=10), reps=1, reference=ref)
+    assert [e.label for e in rep.entries] == ["iterative_reference", "back_projection",
+                                              "iterative_device_f64", "iterative_device"]
+    assert rep.verification_ok(), rep.metrics
+    assert rep.entry("iterative_device_f64").verification is True
+    assert rep.metrics["rel_l2_f64_vs_reference"] <= 1e-10
+    assert rep.metrics["rel_l2_f32_vs_reference"] <= 1e-4

@@ -150,3 +150,14 @@ def test_frequency_operator_matches_reference(oracle):
     assert out["iterations_run"] == int(g["meta"][0])
     assert oracle.rel_l2(out["image"], g["image"]) <= 1e-12
     np.testing.assert_allclose(out["objective_history"], g["hist"][0], rtol=1e-12)
+
+
+@pytest.mark.parametrize("sc", [(64, 32, 128, 1), (128, 128, 1024, 0)])
+def test_c_index_equals_numpy_hypot(oracle, sc):
+    """The C oracle's index rule (glibc hypot, / c dt, floor) is numpy's bit for bit -- it is
+    the reference index of the large-config census (tests/test_gpu_census.py)."""
+    n, M, Q, seed = sc
+    s = oracle.make_scene(n, M, Q, seed)
+    s0, fr = oracle.Operator.of(s).index()
+    ref_s0, ref_fr = oracle.numpy_index(s.xx, s.yy, s.pos, s.c, s.dt)
+    assert np.array_equal(s0, ref_s0) and np.array_equal(fr, ref_fr)
