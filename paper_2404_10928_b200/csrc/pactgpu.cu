@@ -1019,6 +1019,8 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         fp_sym_lo_kernel<<<units, 32>>>(p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups,
                                         p->fsym_qt, (float)p->Q + 1.5f, p->fsym_T, p->fsym_lo);
         {
+            const int zero = 0;
+            if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_counts_overflow, &zero, sizeof(int));
             const size_t csm = (size_t)p->fsym_L * 32 * 4;
             if (p->max_delay >= (double)p->Q + 0.5)
                 fp_sym_count_kernel<true><<<units, kFsThreads, csm>>>(
@@ -1028,6 +1030,12 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 fp_sym_count_kernel<false><<<units, kFsThreads, csm>>>(
                     p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups, p->fsym_qt,
                     (float)p->Q + 1.5f, p->fsym_hx, p->fsym_L, p->fsym_T, p->fsym_counts);
+        }
+        int ovf = 0;
+        if (e == cudaSuccess) e = cudaMemcpyFromSymbol(&ovf, g_counts_overflow, sizeof(int));
+        if (e == cudaSuccess && ovf) {
+            free_plan(p);
+            return fail(PK_ERR_UNSUPPORTED, "projector window slot receives > 65535 pixels (set PK_FSYM=0)");
         }
         std::vector<int> lo((size_t)units * 32);
         e = cudaMemcpy(lo.data(), p->fsym_lo, sizeof(int) * lo.size(), cudaMemcpyDeviceToHost);
@@ -1757,7 +1765,8 @@ int pk_dense_create(int64_t rows, int64_t cols, int32_t dtype, int32_t complex_e
     int rc = PK_OK;
     auto A = [&](int r) { if (rc == PK_OK) rc = r; };
     A(dalloc(d, reinterpret_cast<unsigned char**>(&d->K), (size_t)rows * cols * es));
-    A(dalloc(d, reinterpret_cast<unsigned char**>(&d->part), (size_t)d->splits * cols * es));
+    // (a real K's adjoint of a complex y has complex partials too)
+    A(dalloc(d, reinterpret_cast<unsigned char**>(&d->part), (size_t)d->splits * cols * dsize(d) * 2));
     if (d->fused) A(dalloc(d, reinterpret_cast<unsigned char**>(&d->fpart), (size_t)d->fgrid * cols * 4));
     const int64_t nr = rows * (d->cplx ? 2 : 1);
     const int64_t rp = std::max<int64_t>({(int64_t)d->gemv_grid, (int64_t)d->fgrid,

@@ -329,7 +329,7 @@ struct pk_plan {
     float* fsym_xr = nullptr;     // [(n/2)^2][4] x' rotation-packed by the epilogue
     int32_t* fsym_win = nullptr;  // [units][4][32][L] window sums of the last projection
     int32_t* fsym_lo = nullptr;   // [units][32] first trace index of each window
-    int32_t* fsym_counts = nullptr;  // [units][L][32] pixels per window slot (bias of the adds)
+    uint16_t* fsym_counts = nullptr;  // [units][L][32] biased words per window slot (u16)
     int2* fsym_list = nullptr;    // [M][4 * tiles] per-trace gather list {window offset, lo}
     int fin_chunks = 1;  // residual kernel: sample chunks per sensor
     float* bp_gpart = nullptr;

@@ -1124,7 +1124,7 @@ struct FpSymArgs {
     const float* sxs;
     const float* sys;
     int32_t* win;            // [units][4][32][LW] window sums (unit = tile * groups + group)
-    const int32_t* counts;   // [units][LW][32] pixels per window slot (fp_sym_count_kernel)
+    const uint16_t* counts;  // [units][LW][32] biased words per window slot (fp_sym_count_kernel)
     int n, M, Q, groups, qt; // groups = ceil(M/32), qt = quadrant tiles per side
     float qclamp;
     float hx;                // pixel pitch in samples (pxs[i] ~ pxs[0] + i*hx, fp32)
@@ -1174,12 +1174,15 @@ __device__ __forceinline__ float fs_delay(float k, float hx, float pxbs, float e
 // adds to the slot (pixels of the tile whose delay to the lane's base sensor has s0 = lo + slot
 // or lo + slot + 1).  The projector adds bits(fma(xs, f, 1.5*2^23)) = round(xs*f) + bias and
 // pre-loads each window slot with -count * bias, saving the integer conversions per pair.
+__device__ int g_counts_overflow;
+__device__ __forceinline__ int* counts_overflow_flag() { return &g_counts_overflow; }
+
 template <bool CLAMP>
 __global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* pxs, const float* pys,
                                                                   const float* sxs, const float* sys,
                                                                   int n, int M, int groups, int qt,
                                                                   float qclamp, float hx, int LW,
-                                                                  int T, int32_t* counts) {
+                                                                  int T, uint16_t* counts) {
     extern __shared__ int32_t cnt[];  // [LW][32]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, h = n >> 1;
     const int u = blockIdx.x, tile = u / groups, grp = u % groups;
@@ -1207,8 +1210,13 @@ __global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* p
     __syncthreads();
     // slot k receives the f part of pixels with s0 = lo + k and the 1-f part of those with
     // s0 = lo + k + 1, each word biased by kMagicBits
-    for (int q = threadIdx.x; q < LW * 32; q += kFsThreads)
-        counts[(size_t)u * LW * 32 + q] = cnt[q] + (q + 32 < LW * 32 ? cnt[q + 32] : 0);
+    // (u16: a slot receives at most ~2x the pixels of a one-sample annulus through the tile;
+    // plan setup checks the largest count fits, fp_sym_count_max)
+    for (int q = threadIdx.x; q < LW * 32; q += kFsThreads) {
+        const int c = cnt[q] + (q + 32 < LW * 32 ? cnt[q + 32] : 0);
+        counts[(size_t)u * LW * 32 + q] = (uint16_t)min(c, 65535);
+        if (c > 65535) atomicMax(counts_overflow_flag(), 1);
+    }
 }
 
 #ifndef PK_K2X
@@ -1245,29 +1253,36 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
     const int lo = fp_sym_window_lo(a.pxs, a.pys, n, i0, j0, sx, sy, a.qclamp, T);
     // word (g, k, lane) at (g*LW + k)*32 + lane, k = t - lo for trace index t
     const uint32_t adj = win_s + 4u * (uint32_t)lane - 128u * (uint32_t)lo - 128u * kTwo23Bits;
-    {   // every window slot starts at -count * bias (see fp_sym_count_kernel)
-        // all of this thread's count loads are in flight before the first store
-        const int4* c4 = reinterpret_cast<const int4*>(a.counts + (size_t)u * LW * 32);
+    {   // every window slot starts at -count * bias (see fp_sym_count_kernel); counts are u16,
+        // 8 per 16-B load, all of this thread's loads in flight before the first store
+        const uint4* c8 = reinterpret_cast<const uint4*>(a.counts + (size_t)u * LW * 32);
         int4* w4 = reinterpret_cast<int4*>(win);
-        constexpr int NQ = (LW * 8 + kFsThreads - 1) / kFsThreads;
-        int4 c[NQ];
+        constexpr int NQ = (LW * 4 + kFsThreads - 1) / kFsThreads;
+        uint4 c[NQ];
 #pragma unroll
         for (int i = 0; i < NQ; ++i) {
             const int q = threadIdx.x + i * kFsThreads;
 #if PK_K2X == 7
-            c[i] = make_int4(q, 0, 0, 0);
+            c[i] = make_uint4(q, 0, 0, 0);
 #else
-            c[i] = q < LW * 8 ? __ldg(c4 + q) : make_int4(0, 0, 0, 0);
+            c[i] = q < LW * 4 ? __ldg(c8 + q) : make_uint4(0, 0, 0, 0);
 #endif
         }
 #pragma unroll
         for (int i = 0; i < NQ; ++i) {
             const int q = threadIdx.x + i * kFsThreads;
-            if (q < LW * 8) {
-                int4 v = c[i];
-                v.x *= -kMagicBits; v.y *= -kMagicBits; v.z *= -kMagicBits; v.w *= -kMagicBits;
+            if (q < LW * 4) {
+                const uint32_t wv[4] = {c[i].x, c[i].y, c[i].z, c[i].w};
+                int4 lo, hi;
+                lo.x = -(int)(wv[0] & 0xffffu) * kMagicBits; lo.y = -(int)(wv[0] >> 16) * kMagicBits;
+                lo.z = -(int)(wv[1] & 0xffffu) * kMagicBits; lo.w = -(int)(wv[1] >> 16) * kMagicBits;
+                hi.x = -(int)(wv[2] & 0xffffu) * kMagicBits; hi.y = -(int)(wv[2] >> 16) * kMagicBits;
+                hi.z = -(int)(wv[3] & 0xffffu) * kMagicBits; hi.w = -(int)(wv[3] >> 16) * kMagicBits;
 #pragma unroll
-                for (int g = 0; g < 4; ++g) w4[g * LW * 8 + q] = v;
+                for (int g = 0; g < 4; ++g) {
+                    w4[g * LW * 8 + 2 * q] = lo;
+                    w4[g * LW * 8 + 2 * q + 1] = hi;
+                }
             }
         }
     }
@@ -1338,9 +1353,7 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
             const int kend = min(32, n - (i0 + 32 * (pc % P2)));
             auto scatter = [&](auto checked) {
                 constexpr bool CHECK = decltype(checked)::value;
-                const int kn = CHECK ? kend : 32;
-#pragma unroll kFsUnroll
-                for (int k = 0; k < kn; k += kFsBatch) {
+                auto batch = [&](const int k) {
                     uint32_t ad[kFsBatch];
                     int32_t va[kFsBatch][4], vb[kFsBatch][4];
 #pragma unroll
@@ -1383,6 +1396,15 @@ __global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) 
                                 red_smem_s32(ad[b] + (uint32_t)(g * LW * 128), va[b][g]);
 #endif
                             }
+                };
+                if constexpr (!CHECK) {
+                    // whole piece: fully unrolled, so the column index k + b (and its float) is
+                    // an immediate -- no per-record integer-to-float conversion
+#pragma unroll
+                    for (int k = 0; k < 32; k += kFsBatch) batch(k);
+                } else {
+#pragma unroll kFsUnroll
+                    for (int k = 0; k < kend; k += kFsBatch) batch(k);
                 }
             };
             if (kend == 32) scatter(std::false_type{});  // whole piece: no per-column checks

@@ -346,7 +346,12 @@ class DenseOperator:
         """Device vector in the plan's real or complex dtype (complex only if a is complex)."""
         import torch
 
-        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+        if isinstance(a, torch.Tensor):
+            t = a
+        else:
+            with warnings.catch_warnings():  # read-only reference containers: only copied
+                warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
+                t = torch.from_numpy(np.ascontiguousarray(a))
         c = t.is_complex()
         t = t.to(device=self.device, dtype=(torch.complex64 if self.rdtype == torch.float32
                                             else torch.complex128) if c else self.rdtype).contiguous()
