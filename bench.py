@@ -64,6 +64,8 @@ def parse():
                     help="frames reconstructed per launch sharing one delay evaluation")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ncu", action="store_true",
+                    help="skip the ncu capture of the dominant kernel's DRAM traffic (roofline.traffic)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     a = ap.parse_args()
     if a.exchange is None:
@@ -157,6 +159,57 @@ def run_reference(args, cfg):
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# roofline.traffic: DRAM bytes per launch of the dominant kernel, from ncu on this build
+
+
+def ncu_traffic(config: str, dom: int):
+    """dram__bytes_read + dram__bytes_write per launch of the dominant kernel (K1 = the
+    back-projector with its update epilogue, K2 = the projector), captured by ncu (default
+    cache control: every replay starts cold) on a 2-iteration un-graphed run of this build
+    (tools/profile_kernels.py).  Returns (bytes, description) or (None, reason)."""
+    import shutil
+    import tempfile
+
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not available"
+    pat = "bp_sym_f32|bp_sym_epi|bp_f32_kernel" if dom == 0 else "fp_sym_f32|fp_f32_kernel"
+    iters = 2
+    with tempfile.TemporaryDirectory() as td:
+        log = os.path.join(td, "t.csv")
+        cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none",
+               "-k", f"regex:{pat}", "--csv", "--log-file", log, sys.executable,
+               os.path.join(ROOT, "tools", "profile_kernels.py"), "--config", config,
+               "--iterations", str(iters), "--reps", "1"]
+        try:
+            subprocess.run(cmd, capture_output=True, timeout=240, check=True)
+            import csv
+
+            rows = list(csv.reader(open(log)))
+        except Exception as e:  # noqa: BLE001 -- a missing number is reported, not fatal
+            return None, f"ncu capture failed: {type(e).__name__}"
+    hdr = next((r for r in rows if "Metric Name" in r), None)
+    if hdr is None:
+        return None, "ncu produced no metrics"
+    i_n, i_v, i_u, i_k, i_id = (hdr.index("Metric Name"), hdr.index("Metric Value"),
+                                hdr.index("Metric Unit"), hdr.index("Kernel Name"), hdr.index("ID"))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    total, kernels, mains = 0.0, set(), set()
+    for r in rows[rows.index(hdr) + 1:]:
+        if len(r) > max(i_n, i_v, i_u, i_id) and r[i_n].startswith("dram__bytes_"):
+            total += float(r[i_v].replace(",", "")) * scale.get(r[i_u], 1)
+            nm = r[i_k].split("(")[0].split("<")[0].replace("void ", "").strip()
+            kernels.add(nm)
+            if "epi" not in nm:
+                mains.add(r[i_id])
+    if not mains:
+        return None, "ncu captured no launch of the kernel"
+    # per launch of the dominant kernel (K1 counts its update epilogue with it)
+    return total / len(mains), (f"ncu dram__bytes_read.sum + dram__bytes_write.sum of {sorted(kernels)} "
+                                f"(cold cache, {len(mains)} launches of this build, per launch)")
 
 
 # ---------------------------------------------------------------------------
@@ -455,8 +508,21 @@ def main():
                                               fl, ctypes.byref(nl), stream_ptr()))
             tot += np.array(fl[:])
         per_launch_ms = tot / (reps * prof_iters)
-        peak = ctypes.c_double()
-        N.check(lib.pk_measure_fp32_peak(local, ctypes.byref(peak)))
+        # the denominator: the FFMA peak measured once on this pool's B200s and committed
+        # (profiles/fp32_peak.json, tools/fp32_peak.py); the live measurement is a cross-check
+        live = ctypes.c_double()
+        N.check(lib.pk_measure_fp32_peak(local, ctypes.byref(live)))
+        peak = ctypes.c_double(live.value)
+        peak_src = "measured live (profiles/fp32_peak.json absent)"
+        pj = os.path.join(ROOT, "profiles", "fp32_peak.json")
+        if os.path.exists(pj):
+            try:
+                rec = json.load(open(pj))
+                peak = ctypes.c_double(float(rec["fp32_tflops"]))
+                peak_src = (f"profiles/fp32_peak.json: FFMA microkernel, best of {rec['samples']} at "
+                            f"{rec['sm_mhz_median']} MHz ({rec['when']})")
+            except Exception:
+                pass
         flops_per_launch = 12.0 * M * P * B  # 12 FP32 flops per sensor-pixel pair, per frame
         names = ["K1 bp_update (back-projection + TV + prox)", "K2 projection (fixed-point scatter)",
                  "K3 residual/objective"]
@@ -468,14 +534,9 @@ def main():
                            "share_of_step": float(per_launch_ms[i] / per_launch_ms.sum())}
         dom = int(np.argmax(per_launch_ms[:2]))
         achieved = flops_per_launch / (per_launch_ms[dom] * 1e-3) / 1e12
-        traffic = None
-        prof_json = os.path.join(ROOT, "profiles", "ncu_summary.json")
-        if os.path.exists(prof_json):
-            try:
-                traffic = json.load(open(prof_json)).get("dram_bytes_per_launch", {}).get(
-                    ["bp_f32", "fp_f32"][dom])
-            except Exception:
-                traffic = None
+        traffic, traffic_src = None, None
+        if not args.no_ncu and rank == 0:
+            traffic, traffic_src = ncu_traffic(args.config, dom)
         # HBM view of the same kernel: its DRAM traffic (ncu, per launch) over its duration,
         # against the measured copy bandwidth -- shows the kernel is nowhere near HBM-bound
         hbm_peak, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
@@ -492,8 +553,9 @@ def main():
                 "plan": "kernels timed alone, un-graphed, on a latency-mode plan (full persistent "
                         "back-projector grid); the timed region runs throughput-mode plans "
                         "(half that grid) on concurrent streams",
-                "peak_source": "measured live: FFMA microkernel (pk_measure_fp32_peak); "
-                               "MEASURED_PEAKS.json has no FP32 figure",
+                "peak_source": peak_src + "; MEASURED_PEAKS.json has no FP32 figure",
+                "peak_live": live.value,
+                "traffic_source": traffic_src,
                 "work": f"12 flops x {M} sensors x {P} pixels per launch",
                 "why_fp32": "north_star: FP32 pipe utilisation against B200 peaks; the matrix-free "
                             "operator has ~200 flop/B of compulsory traffic (SURVEY.md 8(d))",
