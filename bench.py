@@ -48,7 +48,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg3", choices=CFG_CHOICES)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--shard", default="frames", choices=["sensors", "frames"])
+    ap.add_argument("--shard", default=None, choices=["sensors", "frames"],
+                    help="N > 1: split one frame's sensors over the GPUs (default for a single-"
+                         "frame configuration: BASELINE config 3 is 'sensor-sharded with "
+                         "allreduce') or give each GPU its own frames (default for config 4's "
+                         "sequence); the other mode is measured as an extra")
     ap.add_argument("--exchange", default=None, choices=["peer", "nccl"],
                     help="sensor shards: gradient exchange over peer memory fused into the update "
                          "(pk_peer_*) or an NCCL all-reduce (default: peer with --shard sensors; "
@@ -68,8 +72,10 @@ def parse():
                     help="skip the ncu capture of the dominant kernel's DRAM traffic (roofline.traffic)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     a = ap.parse_args()
+    if a.shard is None:
+        a.shard = "frames" if a.config == "cfg4" else "sensors"
     if a.exchange is None:
-        a.exchange = "peer" if a.shard == "sensors" else "nccl"
+        a.exchange = "nccl"  # north_star: an NCCL all-reduce of the gradient; --exchange peer
     return a
 
 
@@ -288,7 +294,7 @@ def main():
     import paper_2404_10928_b200 as pk
     from paper_2404_10928_b200 import _native as N
     from paper_2404_10928_b200.sharded import (DeviceShardOps, PeerShardSolve, PipelinedShardSolve,
-                                                SpeculativeShardSolve, shard_range)
+                                                SpeculativeShardSolve, shard_range, shard_sensors)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -338,17 +344,18 @@ def main():
 
     capture = os.environ.get("PK_DIST_BACKEND", "nccl") == "nccl"  # gloo cannot be captured
     def make_shard_solver():
-        m0, m1 = shard_range(M, rank, world)
+        # whole D4 orbits per rank (shard_sensors): every rank runs the symmetric kernels
+        ids = shard_sensors(M, rank, world)
         if args.exchange == "peer":
             sol = PeerShardSolve(grid, ring, ac, pk.CudaPool(local, "float32"), world, rank,
                                  cfg.iterations, graph=True)
             sol.connect_distributed()
             # residual (maxabs, projection, finalize) + N x (back-projection, barrier, fused
             # peer-sum update, sums, residual); one all-reduce of N+1 data terms per frame
-            return sol, m0, m1, 3 + cfg.iterations * (1 + 3 + 3)
-        ops = DeviceShardOps(grid, ring, ac, pk.CudaPool(local, "float32"), m0, m1)
+            return sol, ids, 3 + cfg.iterations * (1 + 3 + 3)
+        ops = DeviceShardOps(grid, ring, ac, pk.CudaPool(local, "float32"), sensors=ids)
         # the all-reduces are NCCL's
-        return (SpeculativeShardSolve(ops, cfg.iterations, graph=capture), m0, m1,
+        return (SpeculativeShardSolve(ops, cfg.iterations, graph=capture), ids,
                 3 + cfg.iterations * (1 + 2 + 3))
 
     if sensor_mode:
@@ -357,10 +364,12 @@ def main():
             # frame's exchange and barrier waits overlap another frame's kernels
             made = [make_shard_solver() for _ in range(max(1, args.sensor_streams))]
             pipe = PipelinedShardSolve([mk[0] for mk in made])
-            _, m0, m1, launches_per_step = made[0]
+            _, ids, launches_per_step = made[0]
         else:
-            solver, m0, m1, launches_per_step = make_shard_solver()
-        Yl = Y[:, m0 * Q : m1 * Q].contiguous()
+            solver, ids, launches_per_step = make_shard_solver()
+        Yl = Y.view(Y.shape[0], M, Q)[:, ids].reshape(Y.shape[0], -1).contiguous()
+        shard_info = {"sensors_per_rank": len(ids), "symmetric": int(
+            (made[0][0] if args.exchange == "peer" else solver.ops).op.info.symmetric)}
 
         def run_frames(fs):
             if args.exchange == "peer":
@@ -635,11 +644,11 @@ def main():
     shard_err = None
     if world > 1 and not sensor_mode and not seq and args.sensor_frames > 0:
         try:  # connect failures are raised on every rank together (PeerShardSolve)
-            ssolver, m0, m1, _ = make_shard_solver()
+            ssolver, ids, _ = make_shard_solver()
         except RuntimeError as e:
             shard_err = str(e)[:300]
     if world > 1 and not sensor_mode and not seq and args.sensor_frames > 0 and shard_err is None:
-        Yl = Y[:2, m0 * Q: m1 * Q].contiguous()
+        Yl = Y[:2].view(2, M, Q)[:, ids].reshape(2, -1).contiguous()
         ssolver.solve(Yl[0], pinned, alpha, beta, step)  # warm-up (plan, NCCL communicators)
         torch.cuda.synchronize(dev)
         dist.barrier()
@@ -655,7 +664,8 @@ def main():
         sensor_sharded = {
             "frames_per_s": 1e3 / ms_frame, "ms_per_frame": ms_frame,
             "ms_per_iteration": ms_frame / cfg.iterations, "frames": args.sensor_frames,
-            "sensors_per_rank": m1 - m0, "iterations_run": res.iterations_run,
+            "sensors_per_rank": len(ids), "iterations_run": res.iterations_run,
+            "shard_layout": "whole D4 orbits (shard_sensors): symmetric kernels on every rank",
             "exchange": args.exchange,
             "exchange_bytes_per_iteration": P * 4 * (world if args.exchange == "peer" else 1),
             "path": ("PeerShardSolve: local K1 -> device barrier -> update summing every rank's "
@@ -665,6 +675,48 @@ def main():
                      "SpeculativeShardSolve: local K1 -> all_reduce(gradient) -> update -> local "
                      "K2/K3 -> all_reduce(sum r^2), all iterations device-resident"
                      + (" in one captured CUDA graph (NCCL)" if capture else " (eager)"))}
+
+    # ---- frames mode as the extra of a sensor-sharded run (independent frames per GPU) ----
+    frames_mode = None
+    if sensor_mode and args.sensor_frames > 0:
+        SSx = max(1, args.streams)
+        fops = [pk.operator_for(grid, ring, ac, pk.CudaPool(local, "float32"), slot=q, concurrency=SSx)
+                for q in range(SSx)]
+        fstreams = [torch.cuda.Stream(dev) for _ in range(SSx)]
+        fx = [torch.empty(P, device=dev, dtype=torch.float32) for _ in range(SSx)]
+        fh = [torch.zeros(4 * cfg.iterations, device=dev, dtype=torch.float64) for _ in range(SSx)]
+        fst = torch.full((max(1, args.steps), 2), -1, device=dev, dtype=torch.int32)
+        fl = N.load()
+        fparams = (N.SolverParams * 1)(params)
+
+        def fstep(k, st_ptr):
+            q = k % SSx
+            N.check(fl.pk_reconstruct(fops[q].handle, fparams, Y[(rank * 7919 + k) % F].data_ptr(),
+                                      fx[q].data_ptr(), fh[q].data_ptr(), st_ptr,
+                                      ctypes.c_void_p(fstreams[q].cuda_stream)))
+        for k in range(max(args.warmup, SSx)):
+            fstep(k, fst[0].data_ptr())
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for st_ in fstreams:
+            st_.wait_event(f0)
+        for k in range(args.steps):
+            fstep(k, fst[k].data_ptr())
+        for st_ in fstreams:
+            torch.cuda.current_stream(dev).wait_stream(st_)
+        f1.record()
+        torch.cuda.synchronize(dev)
+        tf = torch.tensor([f0.elapsed_time(f1)], device=dev, dtype=torch.float64)
+        dist.all_reduce(tf, op=dist.ReduceOp.MAX)
+        sv = fst.cpu().numpy()
+        frames_mode = {"frames_per_s": args.steps * world / (float(tf[0]) * 1e-3),
+                       "ms_per_frame_per_gpu": float(tf[0]) / args.steps, "frames_per_gpu": args.steps,
+                       "streams": SSx, "scaling": "weak",
+                       "all_solves_ran_full": bool(((sv[:, 0] == cfg.iterations) & (sv[:, 1] == 0)).all()),
+                       "path": "independent frames per GPU, pk_reconstruct graphs on concurrent streams, "
+                               "no collective"}
 
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
@@ -709,6 +761,10 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
         }
+        if sensor_mode:
+            line["arm"]["shard"] = shard_info
+        if frames_mode is not None:
+            line["frames_mode"] = frames_mode
         if sensor_sharded is not None:
             line["sensor_sharded"] = sensor_sharded
         elif shard_err is not None:

@@ -73,6 +73,12 @@ typedef struct pk_geometry_desc {
                                 partial slots, the other streams fill the SMs).  Each plan is deterministic; the two
                                 modes sum the back-projector's partials in a different grouping
                                 (fp32 rounding-level differences). */
+    const int32_t* sensor_list; /* optional host [sensor_list_len]: this plan's sensors as a list
+                                of ring indices (strictly increasing) instead of [begin, end);
+                                traces are then stored in list order.  A list closed under the
+                                ring's D4 symmetry (rotation m -> m + M/4, reflection m -> -m)
+                                keeps the symmetric kernels on a sensor shard. */
+    int32_t sensor_list_len;
 } pk_geometry_desc;
 
 typedef struct pk_plan pk_plan;

@@ -64,6 +64,8 @@ class GeometryDesc(ctypes.Structure):
         ("device", ctypes.c_int32),
         ("frames", ctypes.c_int32),
         ("concurrency", ctypes.c_int32),
+        ("sensor_list", ctypes.POINTER(ctypes.c_int32)),
+        ("sensor_list_len", ctypes.c_int32),
     ]
 
 

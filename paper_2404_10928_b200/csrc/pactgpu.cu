@@ -152,7 +152,7 @@ void free_plan(pk_plan* p) {
                     p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt, p->sym_tiles,
                     p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0, p->sym_tile_slot0,
                     p->sym_part, p->fsym_win, p->fsym_lo, p->fsym_list, p->fsym_counts,
-                    p->freq_part};
+                    p->freq_part, p->gid, p->loc};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     for (void* q : p->peer_opened) cudaIpcCloseMemHandle(q);
@@ -410,6 +410,7 @@ void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_
         A.chunks = p->sym_chunks; A.cta_chunk0 = p->sym_cta_chunk0; A.cta_slot0 = p->sym_cta_slot0;
         A.tiles = p->sym_tiles; A.part = p->sym_part; A.lanemap = p->sym_lanemap;
         A.st = epi ? p->state : nullptr;
+        A.gid = p->gid; A.loc = p->loc; A.Mall = p->Mall;
         switch (p->sym_iw) {
             case 64: launch_sym<64>(A, p->sym_grid, p->sym_smem, s); break;
             case 96: launch_sym<96>(A, p->sym_grid, p->sym_smem, s); break;
@@ -628,9 +629,17 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     if (d->sensors < 1) return fail(PK_ERR_INVALID, "sensor count must be >= 1");
     if (d->samples < 1) return fail(PK_ERR_INVALID, "samples must be >= 1");
     if (!(d->c > 0) || !(d->dt > 0)) return fail(PK_ERR_INVALID, "c and dt must be > 0");
-    if (d->sensor_begin < 0 || d->sensor_end > d->sensors || d->sensor_begin >= d->sensor_end)
+    if (d->sensor_list) {
+        if (d->sensor_list_len < 1 || d->sensor_list_len > d->sensors)
+            return fail(PK_ERR_INVALID, "bad sensor list length %d", d->sensor_list_len);
+        for (int l = 0; l < d->sensor_list_len; ++l)
+            if (d->sensor_list[l] < 0 || d->sensor_list[l] >= d->sensors ||
+                (l > 0 && d->sensor_list[l] <= d->sensor_list[l - 1]))
+                return fail(PK_ERR_INVALID, "sensor list must be strictly increasing ring indices");
+    } else if (d->sensor_begin < 0 || d->sensor_end > d->sensors || d->sensor_begin >= d->sensor_end) {
         return fail(PK_ERR_INVALID, "bad sensor shard [%d, %d) of %d", d->sensor_begin,
                     d->sensor_end, d->sensors);
+    }
     if (d->dtype != PK_F32 && d->dtype != PK_F64) return fail(PK_ERR_INVALID, "bad dtype");
     const int nf = d->frames <= 1 ? 1 : d->frames;
     if (nf != 1 && nf != 2 && nf != 4) return fail(PK_ERR_INVALID, "frames must be 1, 2 or 4");
@@ -651,6 +660,15 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     p->nf = nf;
     p->nx = d->nx; p->ny = d->ny; p->P = d->nx * d->ny;
     p->Mall = d->sensors; p->m0 = d->sensor_begin; p->M = d->sensor_end - d->sensor_begin;
+    if (d->sensor_list) {  // a sensor list (e.g. a D4-closed shard) instead of a range
+        p->listed = 1;
+        p->m0 = 0;
+        p->M = d->sensor_list_len;
+        p->gid_h.assign(d->sensor_list, d->sensor_list + d->sensor_list_len);
+    } else {
+        p->gid_h.resize(p->M);
+        for (int l = 0; l < p->M; ++l) p->gid_h[l] = p->m0 + l;
+    }
     p->Q = d->samples;
     p->c = d->c; p->dt = d->dt;
     p->cdt = d->c * d->dt;                          // forward.py:180
@@ -659,7 +677,14 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     // pixel / sensor geometry; delay bounds per sensor from the grid rectangle
     const double* X = d->pixel_x;
     const double* Y = d->pixel_y;
-    const double* SP = d->sensor_xy + 2 * (size_t)d->sensor_begin;
+    std::vector<double> spv(2 * (size_t)std::max(p->M, 1));  // local sensor positions
+    for (int l = 0; l < p->M; ++l) {
+        spv[2 * l] = d->sensor_xy[2 * (size_t)p->gid_h[l]];
+        spv[2 * l + 1] = d->sensor_xy[2 * (size_t)p->gid_h[l] + 1];
+    }
+    const double* SP = spv.data();
+    std::vector<int> loc_h(p->Mall, -1);
+    for (int l = 0; l < p->M; ++l) loc_h[p->gid_h[l]] = l;
     for (int i = 1; i < p->nx; ++i)
         if (!(X[i] > X[i - 1])) { free_plan(p); return fail(PK_ERR_INVALID, "pixel_x must increase"); }
     for (int j = 1; j < p->ny; ++j)
@@ -680,7 +705,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             if (ix != X + p->nx && iy != Y + p->ny) {
                 free_plan(p);
                 return fail(PK_ERR_GEOMETRY, "sensor %d coincides with pixel index %lld",
-                            m + d->sensor_begin, (long long)((iy - Y) * p->nx + (ix - X)));
+                            p->gid_h[m], (long long)((iy - Y) * p->nx + (ix - X)));
             }
         }
     }
@@ -758,8 +783,10 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     // the back-projector then evaluates one delay per 8 sensor-pixel pairs (bp_sym_f32_kernel)
     {
         const char* ev = getenv("PK_SYM");
-        bool ok = (ev ? atoi(ev) != 0 : true) && p->dtype == PK_F32 && nf == 1 && p->M == p->Mall &&
-                  p->nx == p->ny && (p->nx % 2) == 0 && p->nx >= 2 * kSymTile && (p->M % 4) == 0;
+        // the plan's sensors must be closed under the ring's D4 (a whole ring, or a shard
+        // listing whole orbits): every image of a base sensor is then a local trace
+        bool ok = (ev ? atoi(ev) != 0 : true) && p->dtype == PK_F32 && nf == 1 &&
+                  p->nx == p->ny && (p->nx % 2) == 0 && p->nx >= 2 * kSymTile && (p->Mall % 4) == 0;
         const int n = p->nx;
         double scl = 0.0;
         for (int i = 0; ok && i < n; ++i) scl = std::max(scl, std::fabs(X[i]));
@@ -770,9 +797,10 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         for (int m = 0; ok && m < p->M; ++m) R = std::max(R, std::hypot(SP[2 * m], SP[2 * m + 1]));
         const double tols = 1e-9 * std::max(R, 1e-300);
         for (int m = 0; ok && m < p->M; ++m) {
-            const int q = p->M / 4;
+            const int q = p->Mall / 4, gm = p->gid_h[m];
             const double sx = SP[2 * m], sy = SP[2 * m + 1];
-            const int mr = (m + q) % p->M, mf = (p->M - m) % p->M;
+            const int mr = loc_h[(gm + q) % p->Mall], mf = loc_h[(p->Mall - gm) % p->Mall];
+            if (mr < 0 || mf < 0) { ok = false; break; }  // not closed under D4
             // rotation by 90 degrees (x, y) -> (-y, x) and reflection (x, y) -> (x, -y)
             if (std::fabs(SP[2 * mr] + sy) > tols || std::fabs(SP[2 * mr + 1] - sx) > tols) ok = false;
             if (std::fabs(SP[2 * mf] - sx) > tols || std::fabs(SP[2 * mf + 1] + sy) > tols) ok = false;
@@ -902,22 +930,35 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             // the gathered sums are int32: bound the pixels that can reach one sample (s0 in
             // [s-1, s+2], a one-sample margin for fp32 delays) exactly, from the D4 base
             // sensors 0..M/8
-            const int mq = std::min(p->M, p->M / 8 + 2);
+            // (a sensor's count equals its D4 representative's in [0, Mall/8]: the ring
+            // positions of the representatives present in this plan's list)
+            std::vector<int> reps;
+            {
+                std::vector<char> seen(p->Mall / 8 + 2, 0);
+                const int q = p->Mall / 4;
+                for (int l = 0; l < p->M; ++l) {
+                    const int r = p->gid_h[l] % q, rep = std::min(r, q - r);
+                    if (rep < (int)seen.size() && !seen[rep]) { seen[rep] = 1; reps.push_back(rep); }
+                }
+            }
+            const int mq = (int)reps.size();
+            const double* RP = d->sensor_xy;
             std::vector<int> worst(mq, 0);
             auto count = [&](int m0, int m1) {
                 std::vector<int> hist(p->Q + 4);
-                for (int m = m0; m < m1; ++m) {
+                for (int k = m0; k < m1; ++k) {
+                    const int m = reps[k];
                     std::fill(hist.begin(), hist.end(), 0);
                     for (int j = 0; j < p->ny; ++j)
                         for (int i = 0; i < p->nx; ++i) {
-                            const double u = std::hypot(X[i] - SP[2 * m], Y[j] - SP[2 * m + 1]) / p->cdt;
+                            const double u = std::hypot(X[i] - RP[2 * m], Y[j] - RP[2 * m + 1]) / p->cdt;
                             const long s0 = (long)std::floor(u);
                             if (s0 >= 0 && s0 <= p->Q + 1) ++hist[s0 + 1];
                         }
                     int w = 0;
                     for (int t = 0; t + 3 < (int)hist.size(); ++t)
                         w = std::max(w, hist[t] + hist[t + 1] + hist[t + 2] + hist[t + 3]);
-                    worst[m] = w;
+                    worst[k] = w;
                 }
             };
             {
@@ -951,6 +992,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         fsx[m] = (float)(SP[2 * m] / p->cdt);
         fsy[m] = (float)(SP[2 * m + 1] / p->cdt);
     }
+    A(alloc(p, &p->gid, p->M)); A(alloc(p, &p->loc, p->Mall));
     A(alloc(p, &p->pxs, p->nx)); A(alloc(p, &p->pys, p->ny));
     A(alloc(p, &p->sxs, p->M)); A(alloc(p, &p->sys, p->M));
     A(alloc(p, &p->px, p->nx)); A(alloc(p, &p->py, p->ny));
@@ -999,6 +1041,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     auto up = [&](void* dst, const void* src, size_t n) {
         if (e == cudaSuccess) e = cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
     };
+    up(p->gid, p->gid_h.data(), sizeof(int) * p->M); up(p->loc, loc_h.data(), sizeof(int) * p->Mall);
     up(p->pxs, fx.data(), p->nx * 4); up(p->pys, fy.data(), p->ny * 4);
     up(p->sxs, fsx.data(), p->M * 4); up(p->sys, fsy.data(), p->M * 4);
     up(p->px, X, p->nx * 8); up(p->py, Y, p->ny * 8);
@@ -1040,11 +1083,12 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         std::vector<int> lo((size_t)units * 32);
         e = cudaMemcpy(lo.data(), p->fsym_lo, sizeof(int) * lo.size(), cudaMemcpyDeviceToHost);
         std::vector<int2> list((size_t)p->M * 4 * ntl);
-        const int q4 = p->M / 4;
+        const int q4 = p->Mall / 4;
         for (int sg = 0; sg < p->M; ++sg)
             for (int g = 0; g < 4; ++g) {
-                int mb = sg - g * q4;
-                if (mb < 0) mb += p->M;
+                int gb = p->gid_h[sg] - g * q4;  // ring index of the base sensor of image g
+                if (gb < 0) gb += p->Mall;
+                const int mb = loc_h[gb];        // (local: the plan's sensors are D4-closed)
                 for (int t = 0; t < ntl; ++t) {
                     const int unit = t * p->fsym_groups + (mb >> 5), l = mb & 31;
                     list[((size_t)sg * 4 + g) * ntl + t] =

@@ -283,6 +283,13 @@ struct pk_plan {
     int may_truncate = 0;
     double min_delay = 0, max_delay = 0;  // in samples, host-computed bounds
 
+    // local sensors: gid[l] = ring index of local sensor l (m0 + l, or the sensor list);
+    // loc[ring index] = local index or -1 (device copies for the symmetric kernels)
+    std::vector<int> gid_h;
+    int* gid = nullptr;
+    int* loc = nullptr;
+    int listed = 0;  // the plan was made from a sensor list
+
     // geometry on the device
     float *pxs = nullptr, *pys = nullptr, *sxs = nullptr, *sys = nullptr;  // scaled by 1/cdt
     double *px = nullptr, *py = nullptr, *sx = nullptr, *sy = nullptr;    // original fp64

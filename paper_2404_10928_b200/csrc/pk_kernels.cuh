@@ -376,6 +376,9 @@ struct BpSymArgs {
     const int* tiles;        // [ntiles] (tx << 16) | ty
     float* part;             // [slots][8][4][kThreads]
     const DevState* st;      // solver mode: early exit once every frame stopped; else null
+    const int* gid;          // [M] ring index of local sensor (base sensors are local)
+    const int* loc;          // [Mall] local index of a ring sensor (the images of a base)
+    int Mall;                // ring size (the D4 images are ring indices)
 };
 
 // lane -> (column, row) inside a warp's 8x4 footprint.  With lanemap 1 each half-warp
@@ -511,7 +514,8 @@ __global__ void __launch_bounds__(kSymThreads, 3) bp_sym_f32_kernel(BpSymArgs a)
             __syncwarp();
             if (act)
                 bulk_g2s(dst0 + (uint32_t)g * img_stride,
-                         a.table + (size_t)sym_sensor(g, m, a.M) * a.TS + lo, (uint32_t)(a.L * 8),
+                         a.table + (size_t)__ldg(a.loc + sym_sensor(g, __ldg(a.gid + mm), a.Mall)) * a.TS + lo,
+                         (uint32_t)(a.L * 8),
                          full_s + 8 * b);
             if (++b == a.nbuf) { b = 0; phase ^= 1u; }
         }

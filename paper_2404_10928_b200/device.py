@@ -102,14 +102,16 @@ class DeviceOperator:
     """K restricted to sensors [sensor_begin, sensor_end) of a ring, on one device."""
 
     def __init__(self, grid, ring, acoustic, pool: CudaPool, sensor_begin=0, sensor_end=None,
-                 frames: int = 1, concurrency: int = 1):
+                 frames: int = 1, concurrency: int = 1, sensor_list=None):
         _require_cuda(pool.device)
         lib = N.load()
         self.grid, self.ring, self.acoustic, self.pool = grid, ring, acoustic, pool
         self.frames = int(frames)
         M = int(ring.count)
-        self.sensor_begin = int(sensor_begin)
-        self.sensor_end = M if sensor_end is None else int(sensor_end)
+        self.sensor_list = None if sensor_list is None else [int(v) for v in sensor_list]
+        self.sensor_begin = int(sensor_begin) if self.sensor_list is None else 0
+        self.sensor_end = (M if sensor_end is None else int(sensor_end)) if self.sensor_list is None \
+            else len(self.sensor_list)
         xx = np.ascontiguousarray(grid.origin[0] + np.arange(grid.nx) * grid.dx, dtype=np.float64)
         yy = np.ascontiguousarray(grid.origin[1] + np.arange(grid.ny) * grid.dx, dtype=np.float64)
         pos = np.ascontiguousarray(ring.positions, dtype=np.float64)
@@ -124,6 +126,11 @@ class DeviceOperator:
             dtype=pool.pk_dtype, device=pool.device, frames=self.frames,
             concurrency=int(concurrency),
         )
+        if self.sensor_list is not None:
+            lst = np.ascontiguousarray(self.sensor_list, dtype=np.int32)
+            self._keep = self._keep + (lst,)
+            desc.sensor_list = lst.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+            desc.sensor_list_len = int(lst.size)
         handle = ctypes.c_void_p()
         N.check(lib.pk_plan_create(ctypes.byref(desc), ctypes.byref(handle)))
         self._h = handle
@@ -144,6 +151,13 @@ class DeviceOperator:
     @property
     def sensors(self) -> int:
         return self.sensor_end - self.sensor_begin
+
+    @property
+    def sensor_ids(self) -> list[int]:
+        """Ring indices of this operator's traces, in trace order."""
+        if self.sensor_list is not None:
+            return list(self.sensor_list)
+        return list(range(self.sensor_begin, self.sensor_end))
 
     @property
     def samples(self) -> int:
@@ -452,8 +466,9 @@ _cache: dict = {}
 _cache_lock = threading.Lock()
 
 
-def _key(grid, ring, acoustic, pool, m0, m1, frames=1, slot=0, concurrency=1):
+def _key(grid, ring, acoustic, pool, m0, m1, frames=1, slot=0, concurrency=1, sensor_list=None):
     return (int(frames), int(slot), int(concurrency),
+        None if sensor_list is None else tuple(int(v) for v in sensor_list),
         int(grid.nx), int(grid.ny), float(grid.dx), tuple(float(v) for v in grid.origin),
         int(ring.count), float(ring.radius), tuple(float(v) for v in ring.center),
         float(acoustic.c), float(acoustic.dt), int(acoustic.q_s),
@@ -462,18 +477,19 @@ def _key(grid, ring, acoustic, pool, m0, m1, frames=1, slot=0, concurrency=1):
 
 
 def operator_for(grid, ring, acoustic, pool: CudaPool, sensor_begin=0, sensor_end=None,
-                 frames: int = 1, slot: int = 0, concurrency: int = 1):
+                 frames: int = 1, slot: int = 0, concurrency: int = 1, sensor_list=None):
     """Cached DeviceOperator for a geometry (plans are reused across calls and frames).
 
     ``slot`` selects independent plans for the same geometry (one per CUDA stream when
     frames are streamed concurrently); ``concurrency`` > 1 plans for that throughput mode
     (a smaller persistent back-projector grid; rounding-level differences)."""
     m1 = int(ring.count) if sensor_end is None else int(sensor_end)
-    k = _key(grid, ring, acoustic, pool, sensor_begin, m1, frames, slot, concurrency)
+    k = _key(grid, ring, acoustic, pool, sensor_begin, m1, frames, slot, concurrency, sensor_list)
     with _cache_lock:
         op = _cache.get(k)
         if op is None:
-            op = DeviceOperator(grid, ring, acoustic, pool, sensor_begin, m1, frames, concurrency)
+            op = DeviceOperator(grid, ring, acoustic, pool, sensor_begin, m1, frames, concurrency,
+                                sensor_list=sensor_list)
             _cache[k] = op
         return op
 

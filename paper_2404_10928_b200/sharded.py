@@ -25,7 +25,7 @@ import numpy as np
 from .device import CudaPool, operator_for
 from .solver import DIVERGENCE_STREAK, ReconConfig, solver_params
 
-__all__ = ["shard_range", "DeviceShardOps", "SensorShardedSolver", "SpeculativeShardSolve",
+__all__ = ["shard_range", "shard_sensors", "d4_orbits", "local_traces", "DeviceShardOps", "SensorShardedSolver", "SpeculativeShardSolve",
            "PeerShardSolve", "PipelinedShardSolve", "FrameShardedSolver", "stop_point"]
 
 
@@ -40,12 +40,65 @@ def shard_range(count: int, rank: int, world: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
-class DeviceShardOps:
-    """Per-rank kernels (C ABI) for a sensor shard."""
+def d4_orbits(count: int) -> list[list[int]]:
+    """Orbits of the ring indices under the ring's D4 symmetry (rotation m -> m + M/4,
+    reflection m -> -m), sorted by their smallest member; M % 4 == 0."""
+    if count % 4:
+        raise ValueError(f"a ring of {count} sensors has no D4 symmetry")
+    q = count // 4
+    return [sorted({(sgn * b + k * q) % count for sgn in (1, -1) for k in range(4)})
+            for b in range(q // 2 + 1)]
 
-    def __init__(self, grid, ring, acoustic, pool: CudaPool, m0: int, m1: int):
-        self.op = operator_for(grid, ring, acoustic, pool, m0, m1)
+
+def shard_sensors(count: int, rank: int, world: int) -> list[int]:
+    """Rank `rank`'s sensors when the ring is split into whole D4 orbits (rotation-closed and
+    reflection-closed shards), balanced by sensor count: each rank's plan keeps the symmetric
+    back-projector and projector (one delay per 8 / 4 pairs), with every rank's traces a
+    list of ring indices (pk_geometry_desc.sensor_list).  Orbits go, largest first, to the
+    rank with the fewest sensors (ties: lowest rank) -- deterministic on every rank.  A ring
+    without D4 symmetry (M % 4 != 0) falls back to the contiguous shard_range."""
+    if not (0 <= rank < world):
+        raise ValueError(f"rank {rank} outside world of {world}")
+    if count % 4:
+        lo, hi = shard_range(count, rank, world)
+        return list(range(lo, hi))
+    orbits = d4_orbits(count)
+    if len(orbits) < world:
+        raise ValueError(f"cannot split {len(orbits)} D4 orbits over {world} ranks")
+    load, own = [0] * world, [[] for _ in range(world)]
+    for orb in sorted(orbits, key=lambda o: (-len(o), o[0])):
+        r = min(range(world), key=lambda k: (load[k], k))
+        own[r].extend(orb)
+        load[r] += len(orb)
+    return sorted(own[rank])
+
+
+def local_traces(y_full, sensor_ids, samples: int):
+    """Rows `sensor_ids` (ring indices, in order) of a whole-ring trace vector [M*Q]: a
+    contiguous slice for a range shard, a gather for a D4-orbit shard (tensor or array)."""
+    ids = list(sensor_ids)
+    if ids == list(range(ids[0], ids[0] + len(ids))):
+        return y_full[ids[0] * samples:(ids[-1] + 1) * samples]
+    try:
+        import torch
+
+        if isinstance(y_full, torch.Tensor):
+            idx = torch.tensor(ids, device=y_full.device)
+            return y_full.view(-1, samples).index_select(0, idx).reshape(-1).contiguous()
+    except ImportError:  # pragma: no cover
+        pass
+    return np.asarray(y_full).reshape(-1, samples)[ids].reshape(-1)
+
+
+class DeviceShardOps:
+    """Per-rank kernels (C ABI) for a sensor shard: a contiguous range [m0, m1) or, with
+    ``sensors``, a list of ring indices (e.g. shard_sensors' D4-closed shards)."""
+
+    def __init__(self, grid, ring, acoustic, pool: CudaPool, m0: int = 0, m1: int | None = None,
+                 sensors=None):
+        self.op = operator_for(grid, ring, acoustic, pool, m0, m1, sensor_list=sensors)
         self.pixels = grid.size
+        self.sensor_ids = self.op.sensor_ids
 
     def zeros_image(self):
         import torch
@@ -235,14 +288,26 @@ class PeerShardSolve:
     with ``connect_distributed``."""
 
     def __init__(self, grid, ring, acoustic, pool: CudaPool, world: int, rank: int,
-                 iterations: int, graph: bool = False):
+                 iterations: int, graph: bool = False, layout: str = "orbits", op=None):
         import torch
 
         from .device import DeviceOperator
 
         self.world, self.rank, self.n = int(world), int(rank), int(iterations)
-        self.m0, self.m1 = shard_range(int(ring.count), rank, world)
-        self.op = op = DeviceOperator(grid, ring, acoustic, pool, self.m0, self.m1)
+        M = int(ring.count)
+        if op is not None:  # an operator with the same interface (tests: a CPU stand-in)
+            self.op = op
+            self.sensor_ids = list(op.sensor_ids)
+        elif layout == "orbits":  # whole D4 orbits: the shard keeps the symmetric kernels
+            self.sensor_ids = shard_sensors(M, rank, world)
+            self.op = op = DeviceOperator(grid, ring, acoustic, pool, sensor_list=self.sensor_ids)
+        elif layout == "contiguous":
+            m0, m1 = shard_range(M, rank, world)
+            self.sensor_ids = list(range(m0, m1))
+            self.op = op = DeviceOperator(grid, ring, acoustic, pool, m0, m1)
+        else:
+            raise ValueError(f"layout must be 'orbits' or 'contiguous', got {layout!r}")
+        op = self.op
         P = grid.size
         self.y = torch.zeros(op.sensors * op.samples, device=op.device, dtype=op.tdtype)
         self.x = torch.zeros(iterations + 1, P, device=op.device, dtype=op.tdtype)
@@ -254,6 +319,10 @@ class PeerShardSolve:
         self._stream = None
         self._alpha = self._beta = 0.0
         self._tol = 0.0
+
+    def local_y(self, y_full):
+        """This rank's traces of a whole-ring measurement [M*Q] (trace order of the plan)."""
+        return local_traces(y_full, self.sensor_ids, self.op.samples)
 
     def connect(self, handles) -> None:
         self.op.peer_connect(self.world, self.rank, handles)
@@ -322,7 +391,7 @@ class PeerShardSolve:
         import torch
 
         self.prepare(config, alpha, beta, step)
-        self._stream = torch.cuda.current_stream(self.y.device)
+        self._stream = torch.cuda.current_stream(self.y.device) if self.y.is_cuda else None
         self.y.copy_(torch.as_tensor(y_local).to(self.y.device, self.y.dtype), non_blocking=True)
         if self.graph is not None:
             self.graph.replay()

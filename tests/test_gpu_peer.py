@@ -62,7 +62,7 @@ def test_peer_shards_in_process(oracle, world, graph):
     for rep in range(2):  # epochs keep advancing across solves (and graph replays)
         for r, s in zip(ranks, streams):
             with torch.cuda.stream(s):
-                r.launch(yt[r.m0 * Q:r.m1 * Q], cfg, alpha, beta, step)
+                r.launch(r.local_y(yt), cfg, alpha, beta, step)
         torch.cuda.synchronize()
         data = sum(r.local_data_terms() for r in ranks)
         res = [r.finish(data) for r in ranks]
@@ -124,14 +124,14 @@ def _ipc_worker(rank, world, port, y, cfgv, out_dir):
         cfg = pk.ReconConfig(alpha, beta, 10, step)
         s = PeerShardSolve(g, ring, ac, F32, world, rank, cfg.iterations)
         s.connect_distributed()
-        res = s.solve(y[s.m0 * Q:s.m1 * Q], cfg, alpha, beta, step)
+        res = s.solve(s.local_y(y), cfg, alpha, beta, step)
         # three frames through two pipelined instances (graph-captured), each on its stream
         from paper_2404_10928_b200.sharded import PipelinedShardSolve
 
         inst = [PeerShardSolve(g, ring, ac, F32, world, rank, cfg.iterations, graph=True) for _ in range(2)]
         for q in inst:
             q.connect_distributed()
-        frames = PipelinedShardSolve(inst).solve_frames([y[s.m0 * Q:s.m1 * Q]] * 3, cfg, alpha, beta, step)
+        frames = PipelinedShardSolve(inst).solve_frames([s.local_y(y)] * 3, cfg, alpha, beta, step)
         same = all(np.array_equal(fr.image, res.image) for fr in frames)
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), image=res.image, hist=res.history,
                  meta=np.array([res.iterations_run, int(same)]))
@@ -209,3 +209,49 @@ def test_peer_barrier_times_out_without_hanging():
     r = subprocess.run([sys.executable, "-c", _TIMEOUT_SCRIPT, root], env=env, capture_output=True,
                        text=True, timeout=240)
     assert r.returncode == 0 and "TIMEOUT-OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_orbit_shards_run_symmetric_kernels(oracle, world, monkeypatch):
+    """Sensor shards of whole D4 orbits (shard_sensors, pk_geometry_desc.sensor_list) keep the
+    D4 back-projector and the rotation-symmetric projector on every rank (info.symmetric == 3);
+    at 2 / 4 / 8 in-process ranks x stays bit-identical across ranks and the solve matches
+    the fp64 oracle's reconstruction (recon.py:286-377) within the fp32 tolerance."""
+    import torch
+
+    from paper_2404_10928_b200.sharded import PeerShardSolve
+
+    monkeypatch.setenv("PK_FSYM", "1")  # (small shards: the projector's unit count is low)
+    pk.clear_plan_cache()
+    n, M, Q, seed = 128, 64, 512, 2
+    g, ring, ac, ph = pk.make_scene(n, M, Q, seed=seed)
+    o = oracle.Operator.of(oracle.make_scene(n, M, Q, seed))
+    y = o.forward(ph.values)
+    alpha, beta = oracle.resolve_regularization(o, y)
+    step = oracle.resolve_step(o, beta, 1e-3)
+    cfg = pk.ReconConfig(alpha, beta, 10, step)
+    ref = oracle.reconstruct(o, y, alpha, beta, step, 10)
+    ranks = [PeerShardSolve(g, ring, ac, F32, world, r, cfg.iterations, graph=True) for r in range(world)]
+    assert sorted(sum((r.sensor_ids for r in ranks), [])) == list(range(M))
+    assert all(r.op.info.symmetric == 3 for r in ranks), [r.op.info.symmetric for r in ranks]
+    handles = [r.handle for r in ranks]
+    for r in ranks:
+        r.connect(handles)
+    for r in ranks:
+        r.prepare(cfg, alpha, beta, step)
+    streams = [torch.cuda.Stream() for _ in ranks]
+    yt = torch.tensor(y, device="cuda", dtype=torch.float32)
+    for r, s in zip(ranks, streams):
+        with torch.cuda.stream(s):
+            r.launch(r.local_y(yt), cfg, alpha, beta, step)
+    torch.cuda.synchronize()
+    data = sum(r.local_data_terms() for r in ranks)
+    res = [r.finish(data) for r in ranks]
+    for q in res[1:]:
+        assert np.array_equal(q.image, res[0].image)
+    assert res[0].iterations_run == 10
+    err = float(np.linalg.norm(res[0].image - ref["image"]) / np.linalg.norm(ref["image"]))
+    print(f"{world} orbit shards: rel L2 vs oracle {err:.3e}")
+    assert err <= 1e-4
+    np.testing.assert_allclose(res[0].history[:, 0], ref["objective_history"], rtol=1e-4)
+    pk.clear_plan_cache()

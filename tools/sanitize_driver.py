@@ -12,6 +12,8 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+os.environ.setdefault("PK_FSYM", "1")  # the rotation-symmetric projector even at this small size
+
 import paper_2404_10928_b200 as pk  # noqa: E402
 from paper_2404_10928_b200 import measurement as meas  # noqa: E402
 
@@ -62,4 +64,21 @@ for r, s in enumerate(solvers):
         s.launch(yl[r], cfg, cfg.alpha, cfg.beta, cfg.step)
 torch.cuda.synchronize()
 print("peer data terms", [float(s.local_data_terms()[0]) for s in solvers])
+# shards listing whole D4 orbits keep the symmetric kernels (pk_geometry_desc.sensor_list)
+from paper_2404_10928_b200.sharded import shard_sensors  # noqa: E402
+
+for r in range(2):
+    lst = shard_sensors(64, r, 2)
+    op = pk.DeviceOperator(g, ring, ac, F32, sensor_list=lst)
+    print("shard", r, "symmetric flags", op.info.symmetric)
+    rr = torch.tensor(np.random.default_rng(r).standard_normal(len(lst) * 512), device="cuda",
+                      dtype=torch.float32)
+    op.adjoint(rr)
+    op.matvec(ph.values)
+    op.close()
+for s in solvers:
+    s.op.close()
+pk.clear_plan_cache()
+meas._dense_cache.clear()
+torch.cuda.synchronize()
 print("sanitize driver done")
