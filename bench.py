@@ -394,7 +394,6 @@ def main():
         Ystep = [Y[B * t: B * t + B].reshape(-1) for t in range(n_steps_in)]
         stream_ptr = lambda: __import__("ctypes").c_void_p(torch.cuda.current_stream(dev).cuda_stream)
         lib = N.load()
-        import ctypes
 
         # every timed solve writes its own status row [iterations_run, stopped_by] x B, read
         # after the timed region: a frame that stopped early or diverged fails the run

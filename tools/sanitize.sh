@@ -8,8 +8,9 @@ TAG=${1:-r02}
 cd "$(dirname "$0")/.."
 CS=compute-sanitizer
 for tool in memcheck racecheck synccheck; do
+  # (no --leak-check: torch's caching allocator keeps its blocks until exit, which a leak
+  # check reports as leaks; memcheck still reports every invalid or misaligned access)
   extra=""
-  [ "$tool" = "memcheck" ] && extra="--leak-check full"
   timeout 900 $CS --tool $tool $extra --error-exitcode 99 --print-limit 50 \
     python tools/sanitize_driver.py > gpurun_out/sanitize_${TAG}_$tool.log 2>&1
   echo "$tool rc=$?" >> gpurun_out/sanitize_${TAG}_$tool.log
