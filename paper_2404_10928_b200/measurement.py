@@ -433,6 +433,7 @@ def dense_time_matrix(grid, ring, acoustic, pool: CudaPool) -> DeviceMatrix:
 
 
 _dense_cache: dict = {}
+_freq_cache: dict = {}
 
 
 def _as_pool(pool) -> CudaPool:
@@ -467,7 +468,12 @@ def device_operator(K, pool=None):
     if geometry_path(K) == "time":
         return operator_for(prov["grid"], prov["ring"], prov["acoustic"], pool)
     if geometry_path(K) == "frequency":
-        return FreqOperator(prov["grid"], prov["ring"], prov["acoustic"], pool)
+        fk = (id(operator_for(prov["grid"], prov["ring"], prov["acoustic"], pool)), int(prov["acoustic"].q_n))
+        fo = _freq_cache.get(fk)
+        if fo is None or fo.dev_op is not operator_for(prov["grid"], prov["ring"], prov["acoustic"], pool):
+            fo = FreqOperator(prov["grid"], prov["ring"], prov["acoustic"], pool)
+            _freq_cache[fk] = fo
+        return fo
     entries = K.entries if not isinstance(K, np.ndarray) else K
     key = (id(entries), pool)
     op = _dense_cache.get(key)
