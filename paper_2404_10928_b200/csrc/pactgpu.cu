@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -151,7 +152,8 @@ void free_plan(pk_plan* p) {
                     p->status_dev, p->part_bp, p->part_mx, p->part_l1, p->part_tv, p->part_r, p->part_misc, p->state,
                     p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt, p->sym_tiles,
                     p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0, p->sym_tile_slot0,
-                    p->sym_part, p->fsym_win, p->fsym_lo, p->fsym_list, p->fsym_counts,
+                    p->sym_part, p->fsym_acc, p->fsym_trace, p->fsym_counts,
+                    p->fsym_segs, p->fsym_cta_seg0,
                     p->freq_part, p->gid, p->loc};
     for (void* q : ptrs)
         if (q) cudaFree(q);
@@ -231,6 +233,15 @@ const void* sym_kernel_ptr(int iw) {
     }
 }
 
+template <int NW>
+void fsym_kernels(std::vector<const void*>& ks) {
+#define PK_FSK(LW, T) ks.push_back((const void*)fp_sym_f32_kernel<LW, false, T, NW>); \
+                      ks.push_back((const void*)fp_sym_f32_kernel<LW, true, T, NW>);
+    PK_FSK(96, 64) PK_FSK(128, 64) PK_FSK(184, 64) PK_FSK(256, 64) PK_FSK(320, 64)
+    PK_FSK(96, 32) PK_FSK(128, 32) PK_FSK(184, 32) PK_FSK(256, 32)
+#undef PK_FSK
+}
+
 cudaError_t opt_in_smem(int device) {
     static bool done[64] = {};
     if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
@@ -242,14 +253,9 @@ cudaError_t opt_in_smem(int device) {
     smem_kernels<1>(ks);
     smem_kernels<2>(ks);
     smem_kernels<4>(ks);
-    for (const void* k : {(const void*)fp_sym_f32_kernel<96, false, 64>, (const void*)fp_sym_f32_kernel<128, false, 64>,
-                          (const void*)fp_sym_f32_kernel<184, false, 64>, (const void*)fp_sym_f32_kernel<256, false, 64>,
-                          (const void*)fp_sym_f32_kernel<320, false, 64>, (const void*)fp_sym_f32_kernel<96, true, 64>,
-                          (const void*)fp_sym_f32_kernel<128, true, 64>, (const void*)fp_sym_f32_kernel<184, true, 64>,
-                          (const void*)fp_sym_f32_kernel<256, true, 64>, (const void*)fp_sym_f32_kernel<320, true, 64>,
-                          (const void*)fp_sym_f32_kernel<96, false, 32>, (const void*)fp_sym_f32_kernel<128, false, 32>,
-                          (const void*)fp_sym_f32_kernel<184, false, 32>, (const void*)fp_sym_f32_kernel<96, true, 32>,
-                          (const void*)fp_sym_f32_kernel<128, true, 32>, (const void*)fp_sym_f32_kernel<184, true, 32>})
+    fsym_kernels<16>(ks);
+    fsym_kernels<32>(ks);
+    for (const void* k : std::vector<const void*>{})
         ks.push_back(k);
     ks.push_back(sym_kernel_ptr(0));
     for (int iw : kSymIW) ks.push_back(sym_kernel_ptr(iw));
@@ -289,8 +295,9 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
         a.xb0 = static_cast<const float*>(p->xbuf[0]);
         a.xb1 = static_cast<const float*>(p->xbuf[1]);
         a.pxs = p->pxs; a.pys = p->pys; a.sxs = p->sxs; a.sys = p->sys;
-        a.win = p->fsym_win;
-        a.n = p->nx; a.M = p->M; a.Q = p->Q; a.groups = p->fsym_groups; a.qt = p->fsym_qt;
+        a.acc = p->fsym_acc; a.acc_ld = p->fsym_acc_ld; a.trace_of = p->fsym_trace;
+        a.n = p->nx; a.M = p->M; a.Q = p->Q;
+        a.segs = p->fsym_segs; a.cta_seg0 = p->fsym_cta_seg0;
         a.qclamp = (float)p->Q + 1.5f;
         a.hx = p->fsym_hx;
         a.st = p->state; a.solver = solver;
@@ -301,15 +308,17 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
             a.nmx = p->sym_ntiles * 32;
             a.bits = p->fp_bits;
         }
-        const int units = p->fsym_qt * p->fsym_qt * p->fsym_groups;
         const bool clamp = p->max_delay >= (double)p->Q + 0.5;
-#define PK_FS(LW, T) (clamp ? launch_pdl(fp_sym_f32_kernel<LW, true, T>, dim3(units), dim3(kFsThreads), p->fsym_smem, s, a) \
-                            : launch_pdl(fp_sym_f32_kernel<LW, false, T>, dim3(units), dim3(kFsThreads), p->fsym_smem, s, a))
+        const dim3 grid(p->fsym_grid), block(p->fsym_nw * 32);
+#define PK_FS3(LW, T, NW) (clamp ? launch_pdl(fp_sym_f32_kernel<LW, true, T, NW>, grid, block, p->fsym_smem, s, a) \
+                                 : launch_pdl(fp_sym_f32_kernel<LW, false, T, NW>, grid, block, p->fsym_smem, s, a))
+#define PK_FS(LW, T) (p->fsym_nw == 32 ? PK_FS3(LW, T, 32) : PK_FS3(LW, T, 16))
         if (p->fsym_T == 32) {
             switch (p->fsym_L) {
                 case 96: PK_FS(96, 32); break;
                 case 128: PK_FS(128, 32); break;
-                default: PK_FS(184, 32); break;
+                case 184: PK_FS(184, 32); break;
+                default: PK_FS(256, 32); break;
             }
         } else {
             switch (p->fsym_L) {
@@ -320,6 +329,7 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
                 default: PK_FS(320, 64); break;
             }
         }
+#undef PK_FS3
 #undef PK_FS
         return;
     }
@@ -354,9 +364,8 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
                        cudaStream_t s) {
     const int chunks = p->fin_chunks;
     const size_t clen1 = (size_t)((p->Q + chunks - 1) / chunks + 1);
-    // residual [clen + 1], staged measurements [clen], gathered window sums [clen + 1] (padded)
+    // residual [clen + 1], staged measurements [clen]
     size_t sm = ((clen1 * tsize(p) + 15) & ~(size_t)15) + (((clen1 - 1) * tsize(p) + 15) & ~(size_t)15);
-    if (NF == 1 && p->fsym) sm += (clen1 + clen1 / 8 + 2) * 4;  // padded by one word per 8
     const dim3 grid(p->M * chunks, NF);
     if (p->dtype == PK_F32) {
         FinArgs<float> a{};
@@ -377,8 +386,8 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
         a.sumsq_out = sumsq;
         a.solver = solver;
         if (NF == 1 && p->fsym) {
-            a.win = p->fsym_win; a.win_list = p->fsym_list; a.win_lw = p->fsym_L;
-            a.nwin = 4 * p->fsym_qt * p->fsym_qt;
+            a.acc32 = p->fsym_acc;
+            a.acc32_ld = p->fsym_acc_ld;
         }
         a.atrick = p->bp_atrick;
         a.chunks = chunks;
@@ -890,12 +899,13 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 p->sym_slots = slot + 1;
             }
         }
-        // rotation-symmetric projector (fp_sym_f32_kernel): one CTA per (T x T quadrant tile,
-        // group of 32 base sensors).  T = 64 when its window fits (LW <= 320) and there are
-        // enough units to fill the SMs; else T = 32 (window LW <= 184, e.g. config 2's 3.9
-        // samples per pixel) when that gives at least half an SM-count of units.
+        // rotation-symmetric projector (fp_sym_f32_kernel): persistent CTAs, every one resident
+        // (one per SM with 32 warps, or two with 16: PK_FSYM_NW), each taking an equal
+        // contiguous range of the (group of 32 base sensors, T-column quadrant strip, row)
+        // sequence, cut into segments of at most hs rows inside one (group, strip).  The strip
+        // width T (64 or 32) and the window length LW (the segment rectangle's delay span) are
+        // chosen for the fewest window words stored per projection.
         const char* ev2 = getenv("PK_FSYM");
-        const bool forced = ev2 && atoi(ev2) != 0;
         p->fsym = (p->sym && (ev2 ? atoi(ev2) != 0 : true)) ? 1 : 0;
         if (p->fsym) {
             int sms = 0;
@@ -903,29 +913,81 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             p->fsym_hx = (float)((X[n - 1] - X[0]) / (n - 1) / p->cdt);
             p->fsym_groups = (p->M + 31) / 32;
             p->fsym = 0;
+            const int nw = (getenv("PK_FSYM_NW") && atoi(getenv("PK_FSYM_NW")) == 16) ? 16 : 32;
+            const int per_sm = 32 / nw, G = std::max(1, sms) * per_sm;
+            const int hq = n / 2;
+            auto region_diag = [&](int T, int H) {
+                const double ex = std::min(T - 1, hq - 1) * hx, ey = std::min(H - 1, hq - 1) * hy;
+                return std::sqrt(ex * ex + ey * ey);
+            };
+            auto segment = [&](int T, int hs, std::vector<int4>* sg, std::vector<int>* c0) {
+                const int qt = (hq + T - 1) / T;
+                const long long R = (long long)p->fsym_groups * qt * hq;
+                int cnt = 0;
+                std::vector<int> per_group(p->fsym_groups, 0);
+                for (int c = 0; c < G; ++c) {
+                    long long r0 = R * c / G;
+                    const long long r1 = R * (c + 1) / G;
+                    if (c0) c0->push_back(cnt);
+                    while (r0 < r1) {
+                        const long long gs = r0 / hq;
+                        const long long end = std::min({r1, (gs + 1) * hq, r0 + hs});
+                        const int grp = (int)(gs / qt), strip = (int)(gs % qt);
+                        if (sg) sg->push_back(make_int4(grp, strip, hq + (int)(r0 - gs * hq),
+                                                        hq + (int)(end - gs * hq)));
+                        ++per_group[grp];
+                        ++cnt;
+                        r0 = end;
+                    }
+                }
+                if (c0) c0->push_back(cnt);
+                return std::make_pair(cnt, *std::max_element(per_group.begin(), per_group.end()));
+            };
+            const char* evt = getenv("PK_FSYM_T");
+            long long best = -1;
             for (int T : {64, 32}) {
-                const int need = (int)std::ceil(tile_diag(T)) + 6;
-                int L = 0;
-                for (int lw : {96, 128, 184, 256, 320})
-                    if (need <= lw && (T == 64 || lw <= 184)) { L = lw; break; }
-                const int qt = (n / 2 + T - 1) / T;
-                const int units = qt * qt * p->fsym_groups;
-                const int min_units = T == 64 ? sms : (sms + 1) / 2;
-                if (L == 0 || (units < min_units && !forced)) continue;
-                p->fsym = 1;
-                p->fsym_T = T;
-                p->fsym_qt = qt;
-                p->fsym_L = L;
-                p->fsym_smem = 4 * L * 32 * 4 + (kFsThreads / 32) * (32 + kFsBatch) * 16;
-                break;
+                if (evt && atoi(evt) != T) continue;
+                const int qt = (hq + T - 1) / T;
+                const long long R = (long long)p->fsym_groups * qt * hq;
+                const int rows_per = (int)((R + G - 1) / G);
+                for (int lw : {96, 128, 184, 256, 320}) {
+                    if (T == 32 && lw > 256) continue;
+                    if (fs_ngr(lw, nw) == 0) continue;  // windows + one staged image must fit
+                    const int sm = fs_smem(lw, nw);
+                    // window span: the rectangle's delay spread + the slot margins + 3 for the
+                    // 16-B alignment of the window start (fp_sym_window_lo)
+                    int hs = 0;
+                    while (hs < hq && (int)std::ceil(region_diag(T, hs + 1)) + 9 <= lw) ++hs;
+                    hs = std::min(hs, rows_per);
+                    if (hs == 0) continue;
+                    const long long words = (long long)segment(T, hs, nullptr, nullptr).first * lw;
+                    if (best < 0 || words < best) {
+                        best = words;
+                        p->fsym = 1;
+                        p->fsym_T = T;
+                        p->fsym_qt = qt;
+                        p->fsym_L = lw;
+                        p->fsym_hs = hs;
+                        p->fsym_smem = sm;
+                    }
+                }
+            }
+            if (p->fsym) {
+                p->fsym_nw = nw;
+                p->fsym_grid = G;
+                p->fsym_segs_h.clear();
+                p->fsym_cta_seg0_h.clear();
+                const auto sc = segment(p->fsym_T, p->fsym_hs, &p->fsym_segs_h, &p->fsym_cta_seg0_h);
+                p->fsym_nseg = sc.first;
+                p->fsym_acc_ld = ((kAccFront + p->Q + p->fsym_L + 4) + 3) & ~3;
             }
         }
         if (p->fsym) {
-            // fixed-point bound of the 64 x 64 windows (may be tighter than the generic tile's)
-            const double T = p->fsym_T;
-            double nc = 1.5 * (T * std::sqrt(2.0) + 2) * (2.0 / std::max(h, 1e-12) + 2);
-            if (p->min_delay < 8.0 * T * std::max(h, 1.0)) nc = T * T;
-            nc = std::min(nc, T * T);
+            // fixed-point bound of the segment windows (may be tighter than the generic tile's)
+            const double T = p->fsym_T, H = p->fsym_hs;
+            double nc = 1.5 * (std::hypot(T, H) + 2) * (2.0 / std::max(h, 1e-12) + 2);
+            if (p->min_delay < 8.0 * std::max(T, H) * std::max(h, 1.0)) nc = T * H;
+            nc = std::min(nc, T * H);
             p->fp_bits = std::min(p->fp_bits, std::min(22, 30 - ceil_log2(nc)));
             // the gathered sums are int32: bound the pixels that can reach one sample (s0 in
             // [s-1, s+2], a one-sample margin for fp32 delays) exactly, from the D4 base
@@ -1006,21 +1068,23 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     A(alloc(p, &p->part_bp, (size_t)4 * nf * std::max(ntile_max, (p->P + kThreads - 1) / kThreads)));
     A(alloc(p, &p->part_mx, (size_t)std::max(1, p->sym ? 32 * p->sym_ntiles : 1)));
     A(alloc(p, &p->part_l1, (size_t)(p->fsym ? 2 * 8 * p->M : 1)));
-    const int fsym_units = p->fsym ? p->fsym_qt * p->fsym_qt * p->fsym_groups : 0;
+    const int fsym_units = p->fsym ? p->fsym_nseg : 0;
     // TV partials: per projector tile, or per residual CTA (M x up to 8 chunks) with the
     // symmetric projector
     A(alloc(p, &p->part_tv, (size_t)std::max(p->fp_tiles_x * p->fp_tiles_y, p->fsym ? 8 * p->M : 0) * nf));
     if (p->fsym) {
-        A(alloc(p, &p->fsym_win, (size_t)fsym_units * 4 * 32 * p->fsym_L));
-        A(alloc(p, &p->fsym_lo, (size_t)fsym_units * 32));
+        A(alloc(p, &p->fsym_acc, (size_t)p->M * p->fsym_acc_ld));
+        A(alloc(p, &p->fsym_trace, (size_t)p->fsym_groups * 32 * 4));
         A(alloc(p, &p->fsym_counts, (size_t)fsym_units * 32 * p->fsym_L));
-        A(alloc(p, &p->fsym_list, (size_t)p->M * 4 * p->fsym_qt * p->fsym_qt));
+        A(alloc(p, &p->fsym_segs, p->fsym_segs_h.size()));
+        A(alloc(p, &p->fsym_cta_seg0, p->fsym_cta_seg0_h.size()));
         A(alloc(p, &p->fsym_xr, (size_t)(p->nx / 2) * (p->nx / 2) * 4));
     }
     // one CTA per sensor: more, shorter CTAs only add latency (measured 10.3 / 12.8 / 18.2 us
     // for 1 / 2 / 4 chunks at config 3)
     p->fin_chunks = 1;
     if (const char* e = getenv("PK_FIN_CHUNKS")) p->fin_chunks = std::max(1, std::min(8, atoi(e)));
+    if (p->fsym) p->fin_chunks = 1;  // the residual CTA of a trace clears its accumulator row
     A(alloc(p, &p->part_r, (size_t)p->M * nf * p->fin_chunks));
     A(alloc(p, &p->part_misc, (size_t)4 * p->misc_blocks * nf));
     if (p->bp_split > 1) A(alloc(p, &p->bp_gpart, (size_t)p->bp_split * p->P * nf));
@@ -1056,23 +1120,27 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         for (int q = 0; q < 5; ++q) up(dsts[q], p->sym_h[q].data(), sizeof(int) * p->sym_h[q].size());
     }
     if (e == cudaSuccess && p->fsym) {
-        // per-trace window lists of the symmetric projector's gather: trace sg receives, for
-        // g = 0..3, the image-g window of base sensor sg - g*M/4 from every quadrant tile
-        const int ntl = p->fsym_qt * p->fsym_qt, units = ntl * p->fsym_groups;
-        fp_sym_lo_kernel<<<units, 32>>>(p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups,
-                                        p->fsym_qt, (float)p->Q + 1.5f, p->fsym_T, p->fsym_lo);
+        // segments, bias counts, the cleared accumulator, and the local trace of every (base
+        // sensor, image): image g of base sensor b is ring sensor gid(b) + g*M/4
+        const int nseg = p->fsym_nseg;
+        up(p->fsym_segs, p->fsym_segs_h.data(), sizeof(int4) * nseg);
+        up(p->fsym_cta_seg0, p->fsym_cta_seg0_h.data(), sizeof(int) * p->fsym_cta_seg0_h.size());
+        if (e == cudaSuccess) e = cudaMemset(p->fsym_acc, 0, sizeof(int32_t) * (size_t)p->M * p->fsym_acc_ld);
         {
             const int zero = 0;
             if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_counts_overflow, &zero, sizeof(int));
             const size_t csm = (size_t)p->fsym_L * 32 * 4;
-            if (p->max_delay >= (double)p->Q + 0.5)
-                fp_sym_count_kernel<true><<<units, kFsThreads, csm>>>(
-                    p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups, p->fsym_qt,
-                    (float)p->Q + 1.5f, p->fsym_hx, p->fsym_L, p->fsym_T, p->fsym_counts);
-            else
-                fp_sym_count_kernel<false><<<units, kFsThreads, csm>>>(
-                    p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups, p->fsym_qt,
-                    (float)p->Q + 1.5f, p->fsym_hx, p->fsym_L, p->fsym_T, p->fsym_counts);
+            if (e == cudaSuccess) {
+                if (p->max_delay >= (double)p->Q + 0.5)
+                    fp_sym_count_kernel<true><<<nseg, kFsThreads, csm>>>(
+                        p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_segs, (float)p->Q + 1.5f,
+                        p->fsym_hx, p->fsym_L, p->fsym_T, p->fsym_counts);
+                else
+                    fp_sym_count_kernel<false><<<nseg, kFsThreads, csm>>>(
+                        p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_segs, (float)p->Q + 1.5f,
+                        p->fsym_hx, p->fsym_L, p->fsym_T, p->fsym_counts);
+                e = cudaGetLastError();
+            }
         }
         int ovf = 0;
         if (e == cudaSuccess) e = cudaMemcpyFromSymbol(&ovf, g_counts_overflow, sizeof(int));
@@ -1080,23 +1148,11 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             free_plan(p);
             return fail(PK_ERR_UNSUPPORTED, "projector window slot receives > 65535 pixels (set PK_FSYM=0)");
         }
-        std::vector<int> lo((size_t)units * 32);
-        e = cudaMemcpy(lo.data(), p->fsym_lo, sizeof(int) * lo.size(), cudaMemcpyDeviceToHost);
-        std::vector<int2> list((size_t)p->M * 4 * ntl);
+        std::vector<int> tro((size_t)p->fsym_groups * 32 * 4, -1);
         const int q4 = p->Mall / 4;
-        for (int sg = 0; sg < p->M; ++sg)
-            for (int g = 0; g < 4; ++g) {
-                int gb = p->gid_h[sg] - g * q4;  // ring index of the base sensor of image g
-                if (gb < 0) gb += p->Mall;
-                const int mb = loc_h[gb];        // (local: the plan's sensors are D4-closed)
-                for (int t = 0; t < ntl; ++t) {
-                    const int unit = t * p->fsym_groups + (mb >> 5), l = mb & 31;
-                    list[((size_t)sg * 4 + g) * ntl + t] =
-                        make_int2((int)((((size_t)unit * 4 + g) * 32 + l) * p->fsym_L), lo[(size_t)unit * 32 + l]);
-                }
-            }
-        if (e == cudaSuccess)
-            e = cudaMemcpy(p->fsym_list, list.data(), sizeof(int2) * list.size(), cudaMemcpyHostToDevice);
+        for (int b = 0; b < p->M; ++b)
+            for (int g = 0; g < 4; ++g) tro[4 * b + g] = loc_h[(p->gid_h[b] + g * q4) % p->Mall];
+        up(p->fsym_trace, tro.data(), sizeof(int) * tro.size());
     }
     if (e == cudaSuccess) e = cudaMemset(p->table, 0, (size_t)p->M * p->TS * 2 * ts * nf);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);

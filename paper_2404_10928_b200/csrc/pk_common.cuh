@@ -138,6 +138,26 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
         : "memory");
 }
 
+// 1-D bulk reduction shared -> global (TMA engine): dst[i] += src[i] as 32-bit integers,
+// performed at L2 (order independent); bytes and both addresses multiples of 16.  Tracked by
+// the issuing thread's bulk groups.
+__device__ __forceinline__ void bulk_reduce_add_u32(void* dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u32 [%0], [%1], %2;" ::"l"(dst),
+                 "r"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the shared-memory sources of this thread's bulk groups may be overwritten
+__device__ __forceinline__ void bulk_wait_read_all() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// this thread's bulk groups are complete (their global writes performed)
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// generic-proxy shared-memory writes made visible to the async proxy (TMA) before a barrier
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -332,12 +352,20 @@ struct pk_plan {
     std::vector<int> sym_h[5];  // host copies: tiles, chunks, cta_chunk0, cta_slot0, tile_slot0
     // rotation-symmetric projector (fp_sym_f32_kernel)
     int fsym = 0, fsym_T = 0, fsym_qt = 0, fsym_L = 0, fsym_smem = 0, fsym_groups = 0;
+    int fsym_nw = 0;      // warps per CTA (16: two CTAs per SM, 32: one)
+    int fsym_grid = 0;    // persistent CTAs (every one resident)
+    int fsym_nseg = 0;    // segments (window sets) per projection
+    int fsym_hs = 0;      // rows per segment at most
+    int fsym_acc_ld = 0;  // accumulator row length (words)
     float fsym_hx = 0.f;  // pixel pitch in samples
     float* fsym_xr = nullptr;     // [(n/2)^2][4] x' rotation-packed by the epilogue
-    int32_t* fsym_win = nullptr;  // [units][4][32][L] window sums of the last projection
-    int32_t* fsym_lo = nullptr;   // [units][32] first trace index of each window
-    uint16_t* fsym_counts = nullptr;  // [units][L][32] biased words per window slot (u16)
-    int2* fsym_list = nullptr;    // [M][4 * tiles] per-trace gather list {window offset, lo}
+    int32_t* fsym_acc = nullptr;  // [M][acc_ld] int32 trace accumulator (windows reduce-added)
+    int* fsym_trace = nullptr;    // [groups * 32][4] local trace of (base sensor, image)
+    uint16_t* fsym_counts = nullptr;  // [segments][L][32] biased words per window slot (u16)
+    int4* fsym_segs = nullptr;    // [segments] {group, strip, first row, end row}
+    int* fsym_cta_seg0 = nullptr; // [grid + 1]
+    std::vector<int4> fsym_segs_h;
+    std::vector<int> fsym_cta_seg0_h;
     int fin_chunks = 1;  // residual kernel: sample chunks per sensor
     float* bp_gpart = nullptr;
     uint32_t* bp_tile_cnt = nullptr;

@@ -1096,19 +1096,26 @@ __global__ void __launch_bounds__(kThreads, NF == 1 ? 4 : (NF == 2 ? 3 : 2)) fp_
 // same distance, so a delay evaluated for a pixel of the first quadrant (i, j >= n/2) serves
 // its 4 rotation images
 //   g = 0: (i, j)   1: (n-1-j, i)   2: (n-1-i, n-1-j)   3: (j, n-1-i)
-// against the sensors m + g*M/4.  CTA = unit = (T x T quadrant tile, T = 64 or 32, group of
-// 32 base sensors); lane l owns base sensor m = 32*group + l and 4 windows (one per image
-// sensor) of LW slots; window word (g, slot k, lane) sits at (g*LW + k)*32 + lane, so lane l
-// always hits bank l: the scatter is conflict free.  Contributions are fixed-point integers:
-// round(xs*f) at trace index s0 and round(xs*(1-f)) at s0-1 (xs = x*scale), added with
-// red.shared.add.s32 as magic-biased float bits (the bias is pre-subtracted per slot).  At the
-// end the unit stores its windows, transposed to [g][sensor][slot], into its own slice of a
-// global window array (no global atomics); the residual kernel gathers, for every trace
-// sample, the windows that cover it (deterministic integer sums).
+// against the sensors m + g*M/4.
+//
+// Work = rows of (group of 32 base sensors, T-column strip of the quadrant, quadrant row),
+// flattened in that order and cut host-side into one equal contiguous range per persistent
+// CTA (grid = CTAs resident on the GPU, so every SM carries the same number of rows: no
+// partly idle SMs).  A CTA's range is split into segments, each inside one (group, strip) and
+// at most Hs rows high; per segment lane l owns base sensor m = 32*group + l and 4 windows (one
+// per image sensor) of LW slots covering the delays of the segment's T x rows rectangle;
+// window word (g, slot k, lane) sits at (g*LW + k)*32 + lane, so lane l always hits bank l: the
+// scatter is conflict free.  Contributions are fixed-point integers: round(xs*f) at trace index
+// s0 and round(xs*(1-f)) at s0-1 (xs = x*scale), added with red.shared.add.s32 as magic-biased
+// float bits (the bias is pre-subtracted per slot).  At the end of a segment the CTA stores its
+// windows, transposed to [g][sensor][slot], into the segment's slice of a global window array
+// (no global atomics); the residual kernel gathers, for every trace sample, the windows that
+// cover it (deterministic integer sums).
 // Per record (1 pixel x 32 sensors x 4 images): 1 LDS.128 + ~8 delay + 8 FFMA + 8 ATOMS.
 // ===========================================================================
-constexpr int kFsTile = 64;      // quadrant tile side (32 where a 64-tile window does not fit:
-                                 // short c*dt, e.g. BASELINE config 2); rows are 32-pixel pieces
+constexpr int kFsTile = 64;      // quadrant strip width (32 where the window per pixel of a
+                                 // 64 strip is larger, e.g. BASELINE config 2); rows are
+                                 // 32-pixel pieces
 #ifndef PK_FS_BATCH
 #define PK_FS_BATCH 4
 #endif
@@ -1117,7 +1124,7 @@ constexpr int kFsTile = 64;      // quadrant tile side (32 where a 64-tile windo
 #endif
 constexpr int kFsBatch = PK_FS_BATCH;  // records per scatter batch (4: 16 independent atomic pairs)
 constexpr int kFsUnroll = PK_FS_UNROLL; // scatter batches unrolled per loop iteration
-constexpr int kFsThreads = 512;  // 16 warps share the windows (occupancy at 2 CTAs per SM)
+constexpr int kFsThreads = 512;  // threads of the plan-setup count kernel
 
 struct FpSymArgs {
     const float* x;          // standalone input (nullptr: solver mode, xb[(iter+1)&1])
@@ -1127,9 +1134,15 @@ struct FpSymArgs {
     const float* pys;
     const float* sxs;
     const float* sys;
-    int32_t* win;            // [units][4][32][LW] window sums (unit = tile * groups + group)
-    const uint16_t* counts;  // [units][LW][32] biased words per window slot (fp_sym_count_kernel)
-    int n, M, Q, groups, qt; // groups = ceil(M/32), qt = quadrant tiles per side
+    int32_t* acc;            // [M][acc_ld] int32 trace accumulator (row offset kAccFront);
+                             //   the windows are reduce-added into it, the residual kernel
+                             //   reads and clears it
+    int acc_ld;
+    const int* trace_of;     // [groups * 32][4] local trace of (base sensor, image), -1: none
+    const uint16_t* counts;  // [segments][LW][32] biased words per window slot (fp_sym_count_kernel)
+    const int4* segs;        // [segments] {group, strip, first row, end row} (rows absolute)
+    const int* cta_seg0;     // [grid + 1] first segment of each CTA
+    int n, M, Q;
     float qclamp;
     float hx;                // pixel pitch in samples (pxs[i] ~ pxs[0] + i*hx, fp32)
     DevState* st;
@@ -1139,24 +1152,29 @@ struct FpSymArgs {
     int nmx, bits;           //   (the scale is 2^bits / max, as the epilogue's last block did)
 };
 
-// first trace index of the window of the tile x tile quadrant tile at (i0, j0) for sensor (sx, sy)
+constexpr int kAccFront = 4;  // words before sample 0 in an accumulator row (windows may start at -4)
+// shared memory of the projector: windows [4][LW][32], the transposed staging of ngr images
+// [ngr][32][LW + 4] for the bulk reductions, and the per-warp records
+__host__ __device__ constexpr int fs_smem_cap(int nw) { return (nw == 32 ? 226 : 112) * 1024; }
+__host__ __device__ constexpr int fs_base_smem(int lw, int nw) { return 4 * lw * 32 * 4 + nw * (32 + kFsBatch) * 16; }
+__host__ __device__ constexpr int fs_ngr(int lw, int nw) {
+    return fs_base_smem(lw, nw) + 4 * 32 * (lw + 4) * 4 <= fs_smem_cap(nw) ? 4
+         : fs_base_smem(lw, nw) + 2 * 32 * (lw + 4) * 4 <= fs_smem_cap(nw) ? 2
+         : fs_base_smem(lw, nw) + 32 * (lw + 4) * 4 <= fs_smem_cap(nw) ? 1 : 0;
+}
+__host__ __device__ constexpr int fs_smem(int lw, int nw) { return fs_base_smem(lw, nw) + fs_ngr(lw, nw) * 32 * (lw + 4) * 4; }
+
+// first trace index of the window of the quadrant rectangle [i0, i0 + T) x [j0, j1) for
+// sensor (sx, sy): floor of the distance to the nearest point of the rectangle, minus 2,
+// rounded down to a multiple of 4 (the bulk reductions need 16-B aligned rows)
 __device__ __forceinline__ int fp_sym_window_lo(const float* pxs, const float* pys, int n, int i0,
-                                                int j0, float sx, float sy, float qclamp, int tile) {
+                                                int j0, int j1, float sx, float sy, float qclamp,
+                                                int tile) {
     const float X0 = __ldg(pxs + i0), X1 = __ldg(pxs + min(i0 + tile - 1, n - 1));
-    const float Y0 = __ldg(pys + j0), Y1 = __ldg(pys + min(j0 + tile - 1, n - 1));
+    const float Y0 = __ldg(pys + j0), Y1 = __ldg(pys + min(j1 - 1, n - 1));
     const float cx = fminf(fmaxf(sx, X0), X1), cy = fminf(fmaxf(sy, Y0), Y1);
     const float dmin = fminf(sqrtf((cx - sx) * (cx - sx) + (cy - sy) * (cy - sy)), qclamp);
-    return (int)floorf(dmin) - 2;
-}
-
-// plan setup: lo of every (unit, lane) -- geometry only, identical to the projector's
-__global__ void fp_sym_lo_kernel(const float* pxs, const float* pys, const float* sxs, const float* sys,
-                                 int n, int M, int groups, int qt, float qclamp, int T, int32_t* lo_out) {
-    const int u = blockIdx.x, lane = threadIdx.x;
-    const int tile = u / groups, grp = u % groups, h = n >> 1;
-    const int i0 = h + T * (tile % qt), j0 = h + T * (tile / qt);
-    const int mm = min(grp * 32 + lane, M - 1);
-    lo_out[u * 32 + lane] = fp_sym_window_lo(pxs, pys, n, i0, j0, __ldg(sxs + mm), __ldg(sys + mm), qclamp, T);
+    return ((int)floorf(dmin) - 2) & ~3;
 }
 
 // delay of column k of a 32-pixel piece (pxbs = x of the piece's first column minus the
@@ -1174,8 +1192,8 @@ __device__ __forceinline__ float fs_delay(float k, float hx, float pxbs, float e
     return tb;
 }
 
-// plan setup: for every (unit, window slot, lane) the number of biased words the projector
-// adds to the slot (pixels of the tile whose delay to the lane's base sensor has s0 = lo + slot
+// plan setup: for every (segment, window slot, lane) the number of biased words the projector
+// adds to the slot (pixels of the segment whose delay to the lane's base sensor has s0 = lo + slot
 // or lo + slot + 1).  The projector adds bits(fma(xs, f, 1.5*2^23)) = round(xs*f) + bias and
 // pre-loads each window slot with -count * bias, saving the integer conversions per pair.
 __device__ int g_counts_overflow;
@@ -1184,20 +1202,20 @@ __device__ __forceinline__ int* counts_overflow_flag() { return &g_counts_overfl
 template <bool CLAMP>
 __global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* pxs, const float* pys,
                                                                   const float* sxs, const float* sys,
-                                                                  int n, int M, int groups, int qt,
+                                                                  int n, int M, const int4* segs,
                                                                   float qclamp, float hx, int LW,
                                                                   int T, uint16_t* counts) {
     extern __shared__ int32_t cnt[];  // [LW][32]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, h = n >> 1;
-    const int u = blockIdx.x, tile = u / groups, grp = u % groups;
-    const int i0 = h + T * (tile % qt), j0 = h + T * (tile / qt);
-    const int jend = min(j0 + T, n);
-    const int mm = min(grp * 32 + lane, M - 1);
+    const int u = blockIdx.x;
+    const int4 sg = segs[u];
+    const int i0 = h + T * sg.y;
+    const int mm = min(sg.x * 32 + lane, M - 1);
     const float sx = __ldg(sxs + mm), sy = __ldg(sys + mm);
-    const int lo = fp_sym_window_lo(pxs, pys, n, i0, j0, sx, sy, qclamp, T);
+    const int lo = fp_sym_window_lo(pxs, pys, n, i0, sg.z, sg.w, sx, sy, qclamp, T);
     for (int q = threadIdx.x; q < LW * 32; q += kFsThreads) cnt[q] = 0;
     __syncthreads();
-    for (int jj = j0 + warp; jj < jend; jj += kFsThreads / 32) {
+    for (int jj = sg.z + warp; jj < sg.w; jj += kFsThreads / 32) {
         const float ey = __ldg(pys + jj) - sy;
         const float ey2 = ey * ey;
         for (int c0 = i0; c0 < min(i0 + T, n); c0 += 32) {
@@ -1214,8 +1232,8 @@ __global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* p
     __syncthreads();
     // slot k receives the f part of pixels with s0 = lo + k and the 1-f part of those with
     // s0 = lo + k + 1, each word biased by kMagicBits
-    // (u16: a slot receives at most ~2x the pixels of a one-sample annulus through the tile;
-    // plan setup checks the largest count fits, fp_sym_count_max)
+    // (u16: a slot receives at most ~2x the pixels of a one-sample annulus through the segment;
+    // plan setup checks the largest count fits)
     for (int q = threadIdx.x; q < LW * 32; q += kFsThreads) {
         const int c = cnt[q] + (q + 32 < LW * 32 ? cnt[q + 32] : 0);
         counts[(size_t)u * LW * 32 + q] = (uint16_t)min(c, 65535);
@@ -1223,228 +1241,239 @@ __global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* p
     }
 }
 
-#ifndef PK_K2X
-#define PK_K2X 0  // timing experiments only (tools/k2x.sh); 0 = the product
-#endif
-template <int LW, bool CLAMP, int T>
-__global__ void __launch_bounds__(kFsThreads, 2) fp_sym_f32_kernel(FpSymArgs a) {
+template <int LW, bool CLAMP, int T, int NW>
+__global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int NT = NW * 32;
     int iter = 0;
     if (a.solver) {
         if (a.st->all_stopped) return;
         iter = a.st->iter;
     }
+    const int k0 = a.cta_seg0[blockIdx.x], k1 = a.cta_seg0[blockIdx.x + 1];
+    if (k0 >= k1 && !(blockIdx.x == 0 && a.part_mx)) return;  // (CTA 0 records the scale)
     const float* x = a.x ? a.x : ((iter & 1) ? a.xb0 : a.xb1);  // bp wrote xb[(iter+1)&1]
     const float4* xr = a.x ? nullptr : a.xr;
     const int n = a.n, h = n >> 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int WW = 4 * LW * 32;  // window words
+    // images per staging round (plans never launch an instantiation whose windows do not fit:
+    // fs_ngr == 0), staging row stride
+    constexpr int NGR = fs_ngr(LW, NW) > 0 ? fs_ngr(LW, NW) : 1, LWS = LW + 4;
     int32_t* win = reinterpret_cast<int32_t*>(smem);
     // per-warp record buffer: one float4 {xs0, xs1, xs2, xs3} per column of the piece, plus
     // kFsBatch zero records (padding columns)
     float4* rec = reinterpret_cast<float4*>(smem + (size_t)WW * 4) + (size_t)warp * (32 + kFsBatch);
-    const uint32_t win_s = smem_u32(win);
+    int32_t* stg = reinterpret_cast<int32_t*>(smem + (size_t)WW * 4 + (size_t)NW * (32 + kFsBatch) * 16);
+    const uint32_t win_s = smem_u32(win), stg_s = smem_u32(stg);
+    bool pending = false;  // this thread has bulk reductions in flight
+    constexpr int P2 = T / 32;  // 32-column pieces per row
 
-    const int u = blockIdx.x;
-    const int tile = u / a.groups, grp = u % a.groups;
-    const int i0 = h + T * (tile % a.qt), j0 = h + T * (tile / a.qt);
-    const int jend = min(j0 + T, n);
-    const int m = grp * 32 + lane;
-    const bool sensor_ok = m < a.M;
-    const int mm = min(m, a.M - 1);
-    const float sx = __ldg(a.sxs + mm), sy = __ldg(a.sys + mm);
-    // window: trace indices [lo, lo + LW) of this tile (fp_sym_window_lo)
-    const int lo = fp_sym_window_lo(a.pxs, a.pys, n, i0, j0, sx, sy, a.qclamp, T);
-    // word (g, k, lane) at (g*LW + k)*32 + lane, k = t - lo for trace index t
-    const uint32_t adj = win_s + 4u * (uint32_t)lane - 128u * (uint32_t)lo - 128u * kTwo23Bits;
-    {   // every window slot starts at -count * bias (see fp_sym_count_kernel); counts are u16,
-        // 8 per 16-B load, all of this thread's loads in flight before the first store
-        const uint4* c8 = reinterpret_cast<const uint4*>(a.counts + (size_t)u * LW * 32);
-        int4* w4 = reinterpret_cast<int4*>(win);
-        constexpr int NQ = (LW * 4 + kFsThreads - 1) / kFsThreads;
-        uint4 c[NQ];
-#pragma unroll
-        for (int i = 0; i < NQ; ++i) {
-            const int q = threadIdx.x + i * kFsThreads;
-#if PK_K2X == 7
-            c[i] = make_uint4(q, 0, 0, 0);
-#else
-            c[i] = q < LW * 4 ? __ldg(c8 + q) : make_uint4(0, 0, 0, 0);
-#endif
-        }
-#pragma unroll
-        for (int i = 0; i < NQ; ++i) {
-            const int q = threadIdx.x + i * kFsThreads;
-            if (q < LW * 4) {
-                const uint32_t wv[4] = {c[i].x, c[i].y, c[i].z, c[i].w};
-                int4 lo, hi;
-                lo.x = -(int)(wv[0] & 0xffffu) * kMagicBits; lo.y = -(int)(wv[0] >> 16) * kMagicBits;
-                lo.z = -(int)(wv[1] & 0xffffu) * kMagicBits; lo.w = -(int)(wv[1] >> 16) * kMagicBits;
-                hi.x = -(int)(wv[2] & 0xffffu) * kMagicBits; hi.y = -(int)(wv[2] >> 16) * kMagicBits;
-                hi.z = -(int)(wv[3] & 0xffffu) * kMagicBits; hi.w = -(int)(wv[3] >> 16) * kMagicBits;
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    w4[g * LW * 8 + 2 * q] = lo;
-                    w4[g * LW * 8 + 2 * q + 1] = hi;
-                }
-            }
-        }
-    }
-    griddep_wait();  // x' and its fixed-point scale come from the back-projector epilogue
-    // pieces pc = (row warp + 16*(pc / P2), 32-pixel piece pc % P2) of this warp; the 4 image
-    // values of the next piece are loaded while the current one scatters
-    constexpr int P2 = T / 32;
-    constexpr int NW = kFsThreads / 32;
-    auto piece_x = [&](int pc, float (&v)[4]) {
-        const int jj = j0 + warp + NW * (pc / P2);
-        const int ii = i0 + 32 * (pc % P2) + lane;
+    // the 4 image values of piece q of segment (i0, j0): row j0 + q / P2, columns
+    // i0 + 32 * (q % P2) + lane
+    auto piece_x = [&](int i0, int j0, int j1, int q, float (&v)[4]) {
+        const int jj = j0 + q / P2;
+        const int ii = i0 + 32 * (q % P2) + lane;
 #pragma unroll
         for (int g = 0; g < 4; ++g) v[g] = 0.f;
-        if (jj < jend && ii < n && xr) {  // one coalesced 16-B load for the 4 images
-            const float4 q = xr[(jj - h) * h + (ii - h)];
-            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-        } else if (jj < jend && ii < n) {
+        if (jj < j1 && ii < n && xr) {  // one coalesced 16-B load for the 4 images
+            const float4 r = xr[(jj - h) * h + (ii - h)];
+            v[0] = r.x; v[1] = r.y; v[2] = r.z; v[3] = r.w;
+        } else if (jj < j1 && ii < n) {
             v[0] = x[jj * n + ii];
             v[1] = x[ii * n + (n - 1 - jj)];
             v[2] = x[(n - 1 - jj) * n + (n - 1 - ii)];
             v[3] = x[(n - 1 - ii) * n + jj];
         }
     };
-    float xn[4];
-    piece_x(0, xn);  // the first piece's loads overlap the scale reduction below
-    float scale;
-    if (a.part_mx) {  // deferred statistics: every CTA reduces the epilogue's max partials
-        __shared__ float red_f[kFsThreads / 32];
-        float m = 0.f;
-        for (int q = threadIdx.x; q < a.nmx; q += kFsThreads) m = fmaxf(m, __ldcg(a.part_mx + q));
-        m = block_max<float, kFsThreads>(m, red_f);
-        const double scl = (m > 0.f && isfinite(m)) ? ldexp(1.0, a.bits) / (double)m : 0.0;
-        scale = (float)scl;
-        if (blockIdx.x == 0 && threadIdx.x == 0 && !a.st->fr[0].stopped) {
-            FrameState& fs = a.st->fr[0];
-            fs.maxabs = m;
-            fs.scale64 = scl;
-            fs.scale32 = (float)scl;
-        }
-    } else {
-        scale = a.st->fr[0].scale32;
-    }
-    __syncthreads();
-
     if (lane < kFsBatch) rec[32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-#if PK_K2X == 1
-    uint32_t k2x_sink = 0;
-#endif
-    for (int pc = 0; j0 + warp + NW * (pc / P2) < jend; ++pc) {
-        const int jj = j0 + warp + NW * (pc / P2);
-        const int ii = i0 + 32 * (pc % P2) + lane;
-        const bool in = ii < n;
-        float xv[4];
+    float scale = 0.f;
+    // the fixed-point scale: deferred statistics (every CTA reduces the epilogue's max
+    // partials; CTA 0 records it for the residual kernel) or the plan state
+    auto reduce_scale = [&]() {
+        if (a.part_mx) {
+            __shared__ float red_f[NW];
+            float mx = 0.f;
+            for (int q = threadIdx.x; q < a.nmx; q += NT) mx = fmaxf(mx, __ldcg(a.part_mx + q));
+            mx = block_max<float, NT>(mx, red_f);
+            const double scl = (mx > 0.f && isfinite(mx)) ? ldexp(1.0, a.bits) / (double)mx : 0.0;
+            scale = (float)scl;
+            if (blockIdx.x == 0 && threadIdx.x == 0 && !a.st->fr[0].stopped) {
+                FrameState& fs = a.st->fr[0];
+                fs.maxabs = mx;
+                fs.scale64 = scl;
+                fs.scale32 = (float)scl;
+            }
+        } else {
+            scale = a.st->fr[0].scale32;
+        }
+    };
+    if (k0 >= k1) {  // CTA 0 without rows (tiny grids)
+        griddep_wait();
+        reduce_scale();
+        return;
+    }
+    for (int k = k0; k < k1; ++k) {
+        const int4 sg = __ldg(a.segs + k);
+        const int i0 = h + T * sg.y, j0 = sg.z, j1 = sg.w;
+        const int m = sg.x * 32 + lane;
+        const bool sensor_ok = m < a.M;
+        const int mm = min(m, a.M - 1);
+        const float sx = __ldg(a.sxs + mm), sy = __ldg(a.sys + mm);
+        // window: trace indices [lo, lo + LW) of this segment (fp_sym_window_lo)
+        const int lo = fp_sym_window_lo(a.pxs, a.pys, n, i0, j0, j1, sx, sy, a.qclamp, T);
+        // word (g, k, lane) at (g*LW + k)*32 + lane, k = t - lo for trace index t
+        const uint32_t adj = win_s + 4u * (uint32_t)lane - 128u * (uint32_t)lo - 128u * kTwo23Bits;
+        {   // every window slot starts at -count * bias (see fp_sym_count_kernel); counts are u16,
+            // 8 per 16-B load, all of this thread's loads in flight before the first store
+            const uint4* c8 = reinterpret_cast<const uint4*>(a.counts + (size_t)k * LW * 32);
+            int4* w4 = reinterpret_cast<int4*>(win);
+            constexpr int NQ = (LW * 4 + NT - 1) / NT;
+            uint4 c[NQ];
 #pragma unroll
-        for (int g = 0; g < 4; ++g) xv[g] = xn[g];
-        piece_x(pc + 1, xn);
-        // dense records: lane k writes {xs0, xs1, xs2, xs3} of column i0 + 32*pc + k; the
-        // scatter derives px from k and xq = rint(xs) from xs, so a record is one LDS.128
-        // (the record loads share the shared-memory pipe with the atomics)
-        rec[lane] = in ? make_float4(xv[0] * scale, xv[1] * scale, xv[2] * scale, xv[3] * scale)
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
-        __syncwarp();
-        if (sensor_ok) {
-            const float ey = __ldg(a.pys + jj) - sy;
-            const float ey2 = ey * ey;
-            // column k of the piece: x = pxs[c0] + k*hx (samples)
-            const float pxbs = __ldg(a.pxs + i0 + 32 * (pc % P2)) - sx;
-            const int kend = min(32, n - (i0 + 32 * (pc % P2)));
-            auto scatter = [&](auto checked) {
-                constexpr bool CHECK = decltype(checked)::value;
-                auto batch = [&](const int k) {
-                    uint32_t ad[kFsBatch];
-                    int32_t va[kFsBatch][4], vb[kFsBatch][4];
+            for (int i = 0; i < NQ; ++i) {
+                const int q = threadIdx.x + i * NT;
+                c[i] = q < LW * 4 ? __ldg(c8 + q) : make_uint4(0, 0, 0, 0);
+            }
 #pragma unroll
-                    for (int b = 0; b < kFsBatch; ++b) {
-#if PK_K2X == 2
-                        const float4 r0 = make_float4(xv[0] * (k + b), xv[1], xv[2], xv[3]);
-#else
-                        const float4 r0 = rec[k + b];
-#endif
-                        float fr;
-#if PK_K2X == 3
-                        const float tb = __fadd_rd(fmaf((float)(k + b), a.hx, pxbs) * 0.25f + ey2 * 0.001f, kTwo23);
-                        fr = 0.3f;
-#else
-                        const float tb = fs_delay<CLAMP>((float)(k + b), a.hx, pxbs, ey2, a.qclamp, fr);
-#endif
-                        const float xs[4] = {r0.x, r0.y, r0.z, r0.w};
-                        const float omf = 1.f - fr;
-                        // both halves rounded independently (the pair's mass is kept to one
-                        // fixed-point unit); each word carries the magic bias, which the
-                        // window pre-load removes (fp_sym_count_kernel)
+            for (int i = 0; i < NQ; ++i) {
+                const int q = threadIdx.x + i * NT;
+                if (q < LW * 4) {
+                    const uint32_t wv[4] = {c[i].x, c[i].y, c[i].z, c[i].w};
+                    int4 l4, h4;
+                    l4.x = -(int)(wv[0] & 0xffffu) * kMagicBits; l4.y = -(int)(wv[0] >> 16) * kMagicBits;
+                    l4.z = -(int)(wv[1] & 0xffffu) * kMagicBits; l4.w = -(int)(wv[1] >> 16) * kMagicBits;
+                    h4.x = -(int)(wv[2] & 0xffffu) * kMagicBits; h4.y = -(int)(wv[2] >> 16) * kMagicBits;
+                    h4.z = -(int)(wv[3] & 0xffffu) * kMagicBits; h4.w = -(int)(wv[3] >> 16) * kMagicBits;
 #pragma unroll
-                        for (int g = 0; g < 4; ++g) {
-                            va[b][g] = __float_as_int(fmaf(xs[g], fr, kMagic));   // f -> s0
-                            vb[b][g] = __float_as_int(fmaf(xs[g], omf, kMagic));  // 1-f -> s0-1
-                        }
-                        ad[b] = adj + (__float_as_uint(tb) << 7);
+                    for (int g = 0; g < 4; ++g) {
+                        w4[g * LW * 8 + 2 * q] = l4;
+                        w4[g * LW * 8 + 2 * q + 1] = h4;
                     }
+                }
+            }
+        }
+        // pieces q = warp, warp + NW, ... of the segment (row j0 + q / P2, column piece q % P2);
+        // the 4 image values of the next piece are loaded while the current one scatters
+        const int npc = (j1 - j0) * P2;
+        float xn[4];
+        if (k == k0) {
+            griddep_wait();  // x' and its fixed-point scale come from the back-projector epilogue
+            piece_x(i0, j0, j1, warp, xn);  // the first piece's loads overlap the scale reduction
+            reduce_scale();
+        } else {
+            piece_x(i0, j0, j1, warp, xn);
+        }
+        __syncthreads();  // windows initialised (and the previous segment's store done)
+
+        for (int q = warp; q < npc; q += NW) {
+            const int jj = j0 + q / P2;
+            const int c0 = i0 + 32 * (q % P2);
+            const bool in = c0 + lane < n;
+            float xv[4];
 #pragma unroll
-                    for (int b = 0; b < kFsBatch; ++b)
-                        if (!CHECK || k + b < kend)  // padding columns beyond the grid add nothing
+            for (int g = 0; g < 4; ++g) xv[g] = xn[g];
+            piece_x(i0, j0, j1, q + NW, xn);
+            // dense records: lane k writes {xs0, xs1, xs2, xs3} of column c0 + k; the scatter
+            // derives px from k and xq = rint(xs) from xs, so a record is one LDS.128 (the
+            // record loads share the shared-memory pipe with the atomics)
+            rec[lane] = in ? make_float4(xv[0] * scale, xv[1] * scale, xv[2] * scale, xv[3] * scale)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            __syncwarp();
+            if (sensor_ok && c0 < n) {
+                const float ey = __ldg(a.pys + jj) - sy;
+                const float ey2 = ey * ey;
+                // column k of the piece: x = pxs[c0] + k*hx (samples)
+                const float pxbs = __ldg(a.pxs + c0) - sx;
+                const int kend = min(32, n - c0);
+                auto scatter = [&](auto checked) {
+                    constexpr bool CHECK = decltype(checked)::value;
+                    auto batch = [&](const int kk) {
+                        uint32_t ad[kFsBatch];
+                        int32_t va[kFsBatch][4], vb[kFsBatch][4];
+#pragma unroll
+                        for (int b = 0; b < kFsBatch; ++b) {
+                            const float4 r0 = rec[kk + b];
+                            float fr;
+                            const float tb = fs_delay<CLAMP>((float)(kk + b), a.hx, pxbs, ey2, a.qclamp, fr);
+                            const float xs[4] = {r0.x, r0.y, r0.z, r0.w};
+                            const float omf = 1.f - fr;
+                            // both halves rounded independently (the pair's mass is kept to one
+                            // fixed-point unit); each word carries the magic bias, which the
+                            // window pre-load removes (fp_sym_count_kernel)
 #pragma unroll
                             for (int g = 0; g < 4; ++g) {
-#if PK_K2X == 1
-                                k2x_sink += (ad[b] + g) ^ vb[b][g] ^ va[b][g];
-#elif PK_K2X == 4
-                                red_smem_s32(ad[b] + (uint32_t)(g * LW * 128), va[b][g] + vb[b][g]);
-#else
-                                red_smem_s32(ad[b] + (uint32_t)(g * LW * 128) - 128u, vb[b][g]);
-                                red_smem_s32(ad[b] + (uint32_t)(g * LW * 128), va[b][g]);
-#endif
+                                va[b][g] = __float_as_int(fmaf(xs[g], fr, kMagic));   // f -> s0
+                                vb[b][g] = __float_as_int(fmaf(xs[g], omf, kMagic));  // 1-f -> s0-1
                             }
-                };
-                if constexpr (!CHECK) {
-                    // whole piece: fully unrolled, so the column index k + b (and its float) is
-                    // an immediate -- no per-record integer-to-float conversion
+                            ad[b] = adj + (__float_as_uint(tb) << 7);
+                        }
 #pragma unroll
-                    for (int k = 0; k < 32; k += kFsBatch) batch(k);
-                } else {
+                        for (int b = 0; b < kFsBatch; ++b)
+                            if (!CHECK || kk + b < kend)  // padding columns beyond the grid add nothing
+#pragma unroll
+                                for (int g = 0; g < 4; ++g) {
+                                    red_smem_s32(ad[b] + (uint32_t)(g * LW * 128) - 128u, vb[b][g]);
+                                    red_smem_s32(ad[b] + (uint32_t)(g * LW * 128), va[b][g]);
+                                }
+                    };
+                    if constexpr (!CHECK) {
+                        // whole piece: fully unrolled, so the column index kk + b (and its float)
+                        // is an immediate -- no per-record integer-to-float conversion
+#pragma unroll
+                        for (int kk = 0; kk < 32; kk += kFsBatch) batch(kk);
+                    } else {
 #pragma unroll kFsUnroll
-                    for (int k = 0; k < kend; k += kFsBatch) batch(k);
-                }
-            };
-            if (kend == 32) scatter(std::false_type{});  // whole piece: no per-column checks
-            else scatter(std::true_type{});
+                        for (int kk = 0; kk < kend; kk += kFsBatch) batch(kk);
+                    }
+                };
+                if (kend == 32) scatter(std::false_type{});  // whole piece: no per-column checks
+                else scatter(std::true_type{});
+            }
+            __syncwarp();  // rec is rewritten by the next piece
         }
-        __syncwarp();  // rec is rewritten by the next piece
-    }
-#if PK_K2X == 1
-    if (k2x_sink == 0x9e3779b9u) win[threadIdx.x] = 1;
-#endif
-    griddep_launch_dependents();
-    __syncthreads();
+        if (k == k1 - 1) griddep_launch_dependents();
+        __syncthreads();
 
-    // store to win[unit][g][sensor][slot]: a warp instruction writes whole 32-B sectors,
-    // 8 slots of 16 sensors (lane l: sensor sh*16 + (l & 15), half l >> 4 of the 8-slot
-    // block; a sensor's window is LW*4 B, a multiple of 32).  Writing 16 B per sensor per
-    // instruction instead left every sector half-written by each of two requests.  The two
-    // lanes of a sensor read the same bank (2-way conflict, a small phase).
-    {
+        // reduce-add the windows into the trace accumulator: per round, NGR images are
+        // transposed to staging rows [image][lane][slot] (lane l's window is LW contiguous
+        // words, the accumulator row segment it adds to), then thread (image, lane) issues one
+        // bulk reduction of LW words (TMA engine, integer adds at L2: order independent)
         static_assert(LW % 8 == 0, "window length must be whole 32-B sectors");
-        constexpr int NB = LW / 8;
-        int32_t* dst0 = a.win + (size_t)u * 4 * 32 * LW;
-#if PK_K2X == 6
-        if (win[threadIdx.x] != 0x12345) return;
-#endif
-        const int hf = lane >> 4;
-        for (int blk = warp; blk < 8 * NB; blk += NW) {
-            const int gb = blk >> 1, s = (blk & 1) * 16 + (lane & 15);
-            const int g = gb / NB, k0 = (gb - g * NB) * 8 + 4 * hf;
-            int v[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) v[i] = win[(g * LW + k0 + i) * 32 + s];
-            __stcg(reinterpret_cast<int4*>(dst0 + ((size_t)g * 32 + s) * LW + k0),
-                   make_int4(v[0], v[1], v[2], v[3]));
+        for (int g0 = 0; g0 < 4; g0 += NGR) {
+            if (pending) bulk_wait_read_all();  // the staging rows were read by the engine
+            pending = false;
+            if (g0 > 0 || k > k0) __syncthreads();
+            // thread -> (image gl, lane l, 4 slots): 4 conflict-free LDS (bank l), one STS.128
+            // (row stride LW + 4 words: 8 lanes of a phase hit 8 distinct 16-B bank groups)
+            for (int q = threadIdx.x; q < NGR * 32 * (LW / 4); q += NT) {
+                const int l = q & 31, r = q >> 5;
+                const int gl = r / (LW / 4), sl = (r - gl * (LW / 4)) * 4;
+                const int32_t* src = win + ((g0 + gl) * LW + sl) * 32 + l;
+                int4 v;
+                v.x = src[0]; v.y = src[32]; v.z = src[64]; v.w = src[96];
+                *reinterpret_cast<int4*>(stg + (gl * 32 + l) * LWS + sl) = v;
+            }
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (threadIdx.x < NGR * 32) {
+                const int gl = threadIdx.x >> 5, l = threadIdx.x & 31;
+                const int b = sg.x * 32 + l;
+                const int tr = b < a.M ? __ldg(a.trace_of + 4 * b + g0 + gl) : -1;
+                if (tr >= 0) {
+                    const int lol = fp_sym_window_lo(a.pxs, a.pys, n, i0, j0, j1, __ldg(a.sxs + b),
+                                                     __ldg(a.sys + b), a.qclamp, T);
+                    bulk_reduce_add_u32(a.acc + (size_t)tr * a.acc_ld + kAccFront + lol,
+                                        stg_s + 4u * (uint32_t)((gl * 32 + l) * LWS), LW * 4);
+                    bulk_commit();
+                    pending = true;
+                }
+            }
         }
+        // (the last round's barrier also ends every read of the windows: the next segment may
+        // re-initialise them)
     }
+    if (pending) bulk_wait_all();  // the reductions are performed before the CTA retires
 }
 
 // ===========================================================================
@@ -1599,15 +1628,13 @@ struct FinArgs {
                          // symmetric epilogue deferred them)
     double* sumsq_out;   // optional [NF] (pk_residual)
     int solver;
-    // symmetric projector: gather the unit windows instead of reading acc
-    const int32_t* win;  // [units][4][32][LW] (nullptr: acc mode)
-    const int2* win_list;   // [M][nwin] per trace: {offset of the window in win, its lo}
-    int win_lw, nwin;
+    // symmetric projector: the int32 accumulator its windows were reduce-added into (row m
+    // at acc32 + m * acc32_ld + kAccFront); read and cleared here (one CTA per trace)
+    int32_t* acc32;      // (nullptr: acc mode)
+    int acc32_ld;
     int atrick;
     int chunks;          // sample chunks per sensor (one CTA each)
 };
-
-constexpr int kFinListMax = 256;  // per-trace gather lists up to this length are staged in smem
 
 template <typename T, int NF>
 #ifndef PK_FIN_MINB
@@ -1619,7 +1646,6 @@ __global__ void __launch_bounds__(kThreads, PK_FIN_MINB) finalize_kernel(FinArgs
     __shared__ double red_d[kThreads / 32];
     __shared__ double data_s[NF], tv_s[NF];
     __shared__ int last_flag;
-    __shared__ int2 wl_s[kFinListMax];
     if (a.solver && a.st->all_stopped) return;
     // grid (M * chunks, NF): CTA handles samples [c0, c1) of sensor m plus the one-sample
     // halo r[c0-1] its first pair-table entry needs.  The accumulator is read-only here (it
@@ -1633,11 +1659,7 @@ __global__ void __launch_bounds__(kThreads, PK_FIN_MINB) finalize_kernel(FinArgs
     long long* accm = a.acc + (size_t)f * MQ + (size_t)m * a.Q;
     const T* ym = y ? y + f * MQ + (size_t)m * a.Q : nullptr;
     T* om = a.trace_out ? a.trace_out + f * MQ + (size_t)m * a.Q : nullptr;
-    // constant inputs are read before waiting for the projection (they overlap its tail under
-    // programmatic dependent launch): the gather list and this thread's first 8 measurements
-    const bool list_s = a.win && a.nwin <= kFinListMax;
-    if (list_s)
-        for (int q = threadIdx.x; q < a.nwin; q += kThreads) wl_s[q] = __ldg(a.win_list + (size_t)m * a.nwin + q);
+    int32_t* accr = a.acc32 ? a.acc32 + (size_t)m * a.acc32_ld + kAccFront : nullptr;
     // measurements staged in shared memory by LDGSTS (no registers held across the gather)
     T* ys = reinterpret_cast<T*>(smem + (((size_t)(clen + 1) * sizeof(T) + 15) & ~(size_t)15));
     if (ym) {
@@ -1668,78 +1690,19 @@ __global__ void __launch_bounds__(kThreads, PK_FIN_MINB) finalize_kernel(FinArgs
         }
     };
     if (a.tv_here) tv_slice();
-    // symmetric projector: trace m receives, for g = 0..3, the image-g windows of base sensor
-    // m - g*M/4 from every quadrant tile; gather samples [c0 - 1, c1) in that fixed order
-    int32_t* gs = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(ys) +
-                                             (((size_t)clen * sizeof(T) + 15) & ~(size_t)15));
-    if (a.win) {
-        const int LW = a.win_lw, s_lo = c0 - 1, ns = c1 - s_lo;
-        // gs is padded by one word per 8 entries (index j -> j + j/8): lanes that add entries
-        // 8 apart then hit banks 9 apart (conflict free) instead of 4 banks (8-way conflicts)
-        for (int k = threadIdx.x; k < ns + (ns >> 3) + 1; k += kThreads) gs[k] = 0;
-        __syncthreads();
-        // a warp takes whole windows (list order w, w + 8, ...; four at a time so eight 16-B loads
-        // per lane are in flight); lane c adds entries 8c..8c+7 of the window.  The window's
-        // start sb is warp-uniform, so the padded address of entry 8c + q is
-        // (sb + q + (sb + q)/8) + 9c: one add per atomic.  Integer adds commute: the sum is
-        // deterministic.  Windows wholly inside the chunk skip the per-entry range checks.
-        const int2* wl = a.win_list + (size_t)m * a.nwin;
-        const int per = LW >> 3;  // (wl_s: staged before the barrier above)
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        constexpr int kW = kThreads / 32;
-        auto add_window = [&](const int4 (&v)[2], int sb, int c) {
-            const int e[8] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y, v[1].z, v[1].w};
-            const bool inside = sb >= 0 && sb + LW <= ns;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int jq = sb + q;
-                const int jp = jq + (jq >> 3) + 9 * c;  // padded index of entry 8c + q
-                const int j = jq + 8 * c;
-                if (inside || (j >= 0 && j < ns)) atomicAdd(gs + jp, e[q]);
-            }
-        };
-#ifndef PK_FIN_WIN
-#define PK_FIN_WIN 2
-#endif
-        constexpr int kWin = PK_FIN_WIN;  // windows per warp whose loads are in flight together
-        for (int w0 = wid; w0 < a.nwin; w0 += kWin * kW) {
-            int2 d[kWin];
-#pragma unroll
-            for (int u = 0; u < kWin; ++u) {
-                const int wi = w0 + u * kW;
-                d[u] = wi < a.nwin ? (list_s ? wl_s[wi] : __ldg(wl + wi)) : make_int2(0, INT_MIN);
-                // windows wholly outside this CTA's sample chunk are not loaded
-                if (d[u].y != INT_MIN && (d[u].y + LW <= s_lo || d[u].y >= c1)) d[u].y = INT_MIN;
-            }
-            for (int c = lane; c < per; c += 32) {
-                int4 v[kWin][2];
-#pragma unroll
-                for (int u = 0; u < kWin; ++u)
-                    if (d[u].y != INT_MIN) {
-                        const int4* sp = reinterpret_cast<const int4*>(a.win + d[u].x + 8 * c);
-                        v[u][0] = __ldcg(sp);
-                        v[u][1] = __ldcg(sp + 1);
-                    }
-#pragma unroll
-                for (int u = 0; u < kWin; ++u)
-                    if (d[u].y != INT_MIN) add_window(v[u], d[u].y - s_lo, c);
-            }
-        }
-        __syncthreads();
-    }
-    auto sample = [&](int s) -> long long {
-        const int j = s - (c0 - 1);
-        return a.win ? (long long)gs[j + (j >> 3)] : __ldcg(accm + s);
-    };
+    auto sample = [&](int s) -> long long { return accr ? (long long)__ldcg(accr + s) : __ldcg(accm + s); };
     if (ym) cp_async_wait_all();
-    __syncthreads();  // ys (and gs)
+    __syncthreads();  // ys
     double ss = 0.0;
     // tr[k] holds r[c0 - 1 + k]; 4 samples per thread per step, all loads first
     if (threadIdx.x == 0) tr[0] = (c0 >= 1) ? resid_y(sample(c0 - 1), ym ? ym[c0 - 1] : (T)0) : (T)0;
     for (int s0 = c0 + 4 * threadIdx.x; s0 < c1; s0 += 4 * kThreads) {
         long long v[4];
         const bool full = s0 + 4 <= c1 && (s0 & 1) == 0;
-        if (full && !a.win) {
+        if (full && accr && (s0 & 3) == 0) {
+            const int4 p4 = __ldcg(reinterpret_cast<const int4*>(accr + s0));
+            v[0] = p4.x; v[1] = p4.y; v[2] = p4.z; v[3] = p4.w;
+        } else if (full && !accr) {
             const longlong2 p0 = __ldcg(reinterpret_cast<const longlong2*>(accm + s0));
             const longlong2 p1 = __ldcg(reinterpret_cast<const longlong2*>(accm + s0 + 2));
             v[0] = p0.x; v[1] = p0.y; v[2] = p1.x; v[3] = p1.y;
@@ -1756,6 +1719,11 @@ __global__ void __launch_bounds__(kThreads, PK_FIN_MINB) finalize_kernel(FinArgs
         }
     }
     __syncthreads();
+    if (accr) {  // every sample of the row was read (one CTA per trace): clear it, pads included,
+                 // for the next projection's reductions
+        int4* row4 = reinterpret_cast<int4*>(accr - kAccFront);
+        for (int q = threadIdx.x; q < a.acc32_ld / 4; q += kThreads) row4[q] = make_int4(0, 0, 0, 0);
+    }
     // entries e in [c0, c1) (the last chunk also writes the zero-padded tail up to TS)
     const int e1 = (cix == chunks - 1) ? a.TS : c1;
     for (int e = c0 + threadIdx.x; e < e1; e += kThreads) {
