@@ -150,7 +150,7 @@ void free_plan(pk_plan* p) {
     void* ptrs[] = {p->pxs, p->pys, p->sxs, p->sys, p->px, p->py, p->sx, p->sy, p->table,
                     p->acc, p->xbuf[0], p->xbuf[1], p->ydev, p->y64, p->x64, p->hist_dev,
                     p->status_dev, p->part_bp, p->part_mx, p->part_l1, p->part_tv, p->part_r, p->part_misc, p->state,
-                    p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt, p->sym_tiles,
+                    p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt, p->sym_sync, p->sym_tiles,
                     p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0, p->sym_tile_slot0,
                     p->sym_part, p->fsym_acc, p->fsym_trace, p->fsym_counts,
                     p->fsym_segs, p->fsym_cta_seg0,
@@ -420,14 +420,6 @@ void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_
         A.tiles = p->sym_tiles; A.part = p->sym_part; A.lanemap = p->sym_lanemap;
         A.st = epi ? p->state : nullptr;
         A.gid = p->gid; A.loc = p->loc; A.Mall = p->Mall;
-        switch (p->sym_iw) {
-            case 64: launch_sym<64>(A, p->sym_grid, p->sym_smem, s); break;
-            case 96: launch_sym<96>(A, p->sym_grid, p->sym_smem, s); break;
-            case 128: launch_sym<128>(A, p->sym_grid, p->sym_smem, s); break;
-            case 192: launch_sym<192>(A, p->sym_grid, p->sym_smem, s); break;
-            case 256: launch_sym<256>(A, p->sym_grid, p->sym_smem, s); break;
-            default: launch_sym<0>(A, p->sym_grid, p->sym_smem, s); break;
-        }
         BpSymEpiArgs E{};
         E.part = p->sym_part; E.tile_slot0 = p->sym_tile_slot0; E.tiles = p->sym_tiles;
         E.n = p->nx; E.bits = p->fp_bits; E.lanemap = p->sym_lanemap;
@@ -438,7 +430,24 @@ void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_
         E.prm = p->params; E.st = p->state; E.part_bp = p->part_bp;
         E.xr = p->fsym ? p->fsym_xr : nullptr;
         E.part_mx = p->part_mx;
+        // solver mode with the symmetric projector: the update runs in the back-projector's
+        // tail (no epilogue launch); PK_SYM_FUSE=0 keeps the separate epilogue kernel
+        A.fuse = (epi && p->fsym && p->sym_fuse) ? 1 : 0;
+        A.epi = E;
+        A.tile_cnt = p->sym_sync;
+        A.tile_units = p->sym_sync + p->sym_ntiles;
+        A.tile_done = p->sym_sync + 2 * p->sym_ntiles;
+        A.spin_ns = p->sym_spin_ns;
+        switch (p->sym_iw) {
+            case 64: launch_sym<64>(A, p->sym_grid, p->sym_smem, s); break;
+            case 96: launch_sym<96>(A, p->sym_grid, p->sym_smem, s); break;
+            case 128: launch_sym<128>(A, p->sym_grid, p->sym_smem, s); break;
+            case 192: launch_sym<192>(A, p->sym_grid, p->sym_smem, s); break;
+            case 256: launch_sym<256>(A, p->sym_grid, p->sym_smem, s); break;
+            default: launch_sym<0>(A, p->sym_grid, p->sym_smem, s); break;
+        }
         const dim3 eg(p->sym_ntiles * 32);
+        if (A.fuse) return;
         if (epi && p->fsym) launch_pdl(bp_sym_epi_kernel<true, true>, eg, dim3(kThreads), 0, s, E);
         else if (epi) launch_pdl(bp_sym_epi_kernel<true, false>, eg, dim3(kThreads), 0, s, E);
         else launch_pdl(bp_sym_epi_kernel<false, false>, eg, dim3(kThreads), 0, s, E);
@@ -833,6 +842,11 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             p->sym_nbuf = std::max(2, std::min(8, (72 * 1024) / per_buf));
             if (const char* e = getenv("PK_SYM_NBUF")) p->sym_nbuf = std::max(2, std::min(8, atoi(e)));
             p->sym_lanemap = 1;
+            // update fused into the back-projector's tail: opt-in (measured slower at config 3:
+            // 57.0 us vs 41.1 + 9.7 us for the separate epilogue)
+            p->sym_fuse = 0;
+            if (const char* e = getenv("PK_SYM_FUSE")) p->sym_fuse = atoi(e) != 0;
+            if (const char* e = getenv("PK_SYM_SPIN_NS")) p->sym_spin_ns = std::max(0LL, atoll(e));
             if (const char* e = getenv("PK_SYM_LANEMAP")) p->sym_lanemap = atoi(e) != 0;
             p->sym_smem = p->sym_nbuf * per_buf;
             int occ = 0, sms = 0;
@@ -950,8 +964,10 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 const int qt = (hq + T - 1) / T;
                 const long long R = (long long)p->fsym_groups * qt * hq;
                 const int rows_per = (int)((R + G - 1) / G);
+                const char* evl = getenv("PK_FSYM_LW");
                 for (int lw : {96, 128, 184, 256, 320}) {
                     if (T == 32 && lw > 256) continue;
+                    if (evl && atoi(evl) != lw) continue;
                     if (fs_ngr(lw, nw) == 0) continue;  // windows + one staged image must fit
                     const int sm = fs_smem(lw, nw);
                     // window span: the rectangle's delay spread + the slot margins + 3 for the
@@ -1089,6 +1105,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     A(alloc(p, &p->part_misc, (size_t)4 * p->misc_blocks * nf));
     if (p->bp_split > 1) A(alloc(p, &p->bp_gpart, (size_t)p->bp_split * p->P * nf));
     A(alloc(p, &p->bp_tile_cnt, (size_t)ntile_max));
+    if (p->sym) A(alloc(p, &p->sym_sync, (size_t)3 * p->sym_ntiles));
     if (p->sym) {
         A(alloc(p, &p->sym_tiles, p->sym_h[0].size()));
         A(alloc(p, &p->sym_chunks, p->sym_h[1].size()));
@@ -1114,6 +1131,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     if (e == cudaSuccess) e = cudaMemset(p->state, 0, sizeof(DevState));
     if (e == cudaSuccess)
         e = cudaMemset(p->bp_tile_cnt, 0, sizeof(uint32_t) * ntile_max);
+    if (e == cudaSuccess && p->sym) e = cudaMemset(p->sym_sync, 0, sizeof(uint32_t) * 3 * p->sym_ntiles);
     if (p->sym) {
         int* dsts[5] = {p->sym_tiles, p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0,
                         p->sym_tile_slot0};

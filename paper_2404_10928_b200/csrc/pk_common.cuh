@@ -47,7 +47,8 @@ struct FrameState {
 struct DevState {
     int32_t iter;        // iterations attempted so far (shared by the frames)
     int32_t all_stopped; // every frame stopped (or iteration cap): kernels early-exit
-    int32_t pad0, pad1;
+    int32_t epoch;       // solves started on this plan (init_kernel): launch ids of the fused update
+    int32_t pad1;
     // last-block counters (reset by the last block itself)
     uint32_t cnt_bp, cnt_fp, cnt_fin, cnt_misc;
     double sums[4];      // scalars of the sharded / standalone entry points
@@ -153,6 +154,14 @@ __device__ __forceinline__ void bulk_wait_read_all() {
 }
 // this thread's bulk groups are complete (their global writes performed)
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 // generic-proxy shared-memory writes made visible to the async proxy (TMA) before a barrier
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -346,6 +355,7 @@ struct pk_plan {
     int sym = 0, sym_ntiles = 0, sym_L = 0, sym_nbuf = 0, sym_smem = 0, sym_grid = 0, sym_slots = 0;
     int sym_iw = 0;  // compile-time image-window stride (slots), 0 = runtime
     int sym_lanemap = 1;
+    int sym_fuse = 0;     // update fused into the back-projector's tail (solver mode, opt-in)
     int *sym_tiles = nullptr, *sym_chunks = nullptr, *sym_cta_chunk0 = nullptr,
         *sym_cta_slot0 = nullptr, *sym_tile_slot0 = nullptr;
     float* sym_part = nullptr;  // [slots][8][4][kThreads] partial sums
@@ -369,6 +379,8 @@ struct pk_plan {
     int fin_chunks = 1;  // residual kernel: sample chunks per sensor
     float* bp_gpart = nullptr;
     uint32_t* bp_tile_cnt = nullptr;
+    uint32_t* sym_sync = nullptr;  // [3][ntiles] fused-update arrival / unit / publication words
+    long long sym_spin_ns = 20000;
     // projector tiling
     int fp_T = 0, fp_tiles_x = 0, fp_tiles_y = 0, fp_groups = 0, fp_L = 0, fp_bits = 0,
         fp_smem = 0;

@@ -361,6 +361,43 @@ constexpr int kSymCS = 2;        // base sensors per chunk (x 8 images = 16 wind
 constexpr int kSymConsumers = 8; // consumer warps; warp 8 is the TMA producer
 constexpr int kSymThreads = 32 * (kSymConsumers + 1);
 
+// K1s epilogue: CTA (tile, image g, 8-column strip) adds the tile's partial slots (4 slot
+// groups in parallel, then in order), maps the representatives to image g, and writes
+// gscale * K^T r (EPI == false) or runs the fused update of recon.py:327-338 with the block
+// statistics of the next projector scale.
+struct BpSymEpiArgs {
+    const float* part;        // [slots][8][4][kThreads]
+    const int* tile_slot0;    // [ntiles + 1]
+    const int* tiles;         // [ntiles]
+    int n, bits, lanemap;
+    float gscale;
+    float* out;               // EPI == false
+    float* xb0;               // EPI == true: x from xb[iter & 1] to xb[(iter + 1) & 1]
+    float* xb1;
+    const DevParams* prm;
+    DevState* st;
+    double* part_bp;          // [grid][4]
+    float* xr;                // EPI == true, optional: rotation-packed copy of x' for the
+                              // symmetric projector, [(n/2)^2][4] (fp_sym_f32_kernel)
+    float* part_mx;           // DEFER: [grid] max |x'| per CTA (the projector reduces them)
+};
+
+// rotation-packed index of pixel (i, j): the quadrant representative q = (qi, qj) in
+// [h, n)^2 and rotation r with rot^r(q) = (i, j) (the image order of fp_sym_f32_kernel);
+// returns 4 * ((qj - h) * h + (qi - h)) + r
+__device__ __forceinline__ int sym_rot_index(int i, int j, int n) {
+    const int h = n >> 1;
+    int qi, qj, r;
+    if (i >= h) {
+        if (j >= h) { qi = i; qj = j; r = 0; }
+        else { qi = n - 1 - j; qj = i; r = 3; }
+    } else {
+        if (j >= h) { qi = j; qj = n - 1 - i; r = 1; }
+        else { qi = n - 1 - i; qj = n - 1 - j; r = 2; }
+    }
+    return 4 * ((qj - h) * h + (qi - h)) + r;
+}
+
 struct BpSymArgs {
     const float2* table;     // [M][TS] pair table
     const float* pxs;        // [n] scaled pixel x
@@ -379,6 +416,16 @@ struct BpSymArgs {
     const int* gid;          // [M] ring index of local sensor (base sensors are local)
     const int* loc;          // [Mall] local index of a ring sensor (the images of a base)
     int Mall;                // ring size (the D4 images are ring indices)
+    // fused update (solver mode with the symmetric projector): the CTAs whose last tile is t
+    // run the update of t once all of its partial slots are in (per-tile arrival counter);
+    // the final arriver publishes the tile, waiting CTAs join within a bounded spin, and the 32
+    // (image, 8-column strip) units of the tile are claimed one at a time
+    int fuse;
+    BpSymEpiArgs epi;
+    uint32_t* tile_cnt;      // [ntiles] partial slots arrived (reset by the final arriver)
+    uint32_t* tile_units;    // [ntiles] units claimed
+    uint32_t* tile_done;     // [ntiles] launch id of the last publication
+    long long spin_ns;       // how long a CTA waits for its last tile before leaving it
 };
 
 // lane -> (column, row) inside a warp's 8x4 footprint.  With lanemap 1 each half-warp
@@ -449,6 +496,121 @@ __device__ __forceinline__ void sym_chunk(float (&acc)[4][8], const float (&px)[
             }
         }
     }
+}
+
+// units of the symmetric update (solver mode, deferred statistics): tile t, image g, 8-column
+// strip k (unit index u = 4g + k), U units [u0, u0 + U) at once (every load of the U units in
+// flight together) -- the tile's partial slots summed in slot order, mapped to image g, then
+// TV gradient + prox + non-negativity (recon.py:327-338), x' written twice (image order and
+// rotation-packed for the projector) and each unit's max |x'| partial.  256 threads; sync() is
+// their barrier.  Shared scratch: part4 [U][3][64] float4, blk [U][256] float, red [U][8] float.
+template <int U, typename Sync>
+__device__ __forceinline__ void sym_epi_units(const BpSymEpiArgs& a, int t, int u0, int iter,
+                                              float4* part4, float* blk, float* red, Sync sync) {
+    const int tid = threadIdx.x;
+    const int tp = __ldg(a.tiles + t);
+    const int tx = tp >> 16, ty = tp & 0xffff;
+    const int n = a.n, h = n >> 1;
+    const int i0 = h + kSymTile * tx, j0 = h + kSymTile * ty;
+    const int s0 = __ldg(a.tile_slot0 + t), s1 = __ldg(a.tile_slot0 + t + 1);
+    const int sg = tid >> 6, q = tid & 63;
+    int bx[U], by[U], bw[U];
+    bool active[U];
+#pragma unroll
+    for (int v = 0; v < U; ++v) {
+        const int u = u0 + v, k = u & 3, g = u >> 2;
+        active[v] = u < 32 && !(tx == ty && g >= 4);
+        int ia, ja, ib, jb;
+        sym_pixel(g & 7, i0 + 8 * k, j0, n, ia, ja);
+        sym_pixel(g & 7, i0 + 8 * k + 7, j0 + kSymTile - 1, n, ib, jb);
+        bx[v] = min(ia, ib);
+        by[v] = min(ja, jb);
+        bw[v] = abs(ib - ia) + 1;
+    }
+    // the iterate and its TV neighbours are independent of the slot sums: loads first
+    const float* x = (iter & 1) ? a.xb1 : a.xb0;
+    float* xo = (iter & 1) ? a.xb0 : a.xb1;
+    const float eta = (float)a.prm->step[0], lam = (float)a.prm->eta_alpha[0];
+    const float beta = (float)a.prm->beta[0], eps = (float)a.prm->eps;
+    const bool run = !a.st->fr[0].stopped;
+    int pix[U];
+    float xv[U], tvg[U];
+#pragma unroll
+    for (int v = 0; v < U; ++v) {
+        const int ig = bx[v] + tid % bw[v], jg = by[v] + tid / bw[v];
+        pix[v] = (run && active[v] && ig >= 0 && ig < n && jg >= 0 && jg < n) ? jg * n + ig : -1;
+        xv[v] = pix[v] >= 0 ? x[pix[v]] : 0.f;
+        tvg[v] = (pix[v] >= 0 && beta > 0.f) ? tv_grad_at<float>(x, pix[v], ig, jg, n, n, eps * eps) : 0.f;
+    }
+    float4 sum[U];
+#pragma unroll
+    for (int v = 0; v < U; ++v) sum[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const size_t stride = 8 * 4 * kThreads / 4;  // float4s per slot
+    for (int sb = s0 + sg; sb < s1; sb += 16) {
+        float4 w4[U][4];
+#pragma unroll
+        for (int v = 0; v < U; ++v) {
+            const int u = u0 + v;
+            const float4* src = reinterpret_cast<const float4*>(a.part + (size_t)(u & 31) * kThreads) + q;
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+                w4[v][w] = (active[v] && sb + 4 * w < s1) ? __ldcg(src + (size_t)(sb + 4 * w) * stride)
+                                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int v = 0; v < U; ++v)
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                sum[v].x += w4[v][w].x; sum[v].y += w4[v][w].y; sum[v].z += w4[v][w].z; sum[v].w += w4[v][w].w;
+            }
+    }
+    if (sg > 0)
+#pragma unroll
+        for (int v = 0; v < U; ++v) part4[(v * 3 + sg - 1) * 64 + q] = sum[v];
+    sync();
+    if (sg == 0)
+#pragma unroll
+        for (int v = 0; v < U; ++v) {
+            float4 sm = sum[v];
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                const float4 o = part4[(v * 3 + r) * 64 + q];
+                sm.x += o.x; sm.y += o.y; sm.z += o.z; sm.w += o.w;
+            }
+            const float sv[4] = {sm.x, sm.y, sm.z, sm.w};
+            const int u = u0 + v, k = u & 3, g = (u >> 2) & 7;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const int c = 4 * q + w;
+                int lx, ly;
+                sym_lane_xy(c & 31, a.lanemap, lx, ly);
+                int ig, jg;
+                sym_pixel(g, i0 + lx + 8 * k, j0 + 4 * (c >> 5) + ly, n, ig, jg);
+                blk[v * 256 + (jg - by[v]) * bw[v] + (ig - bx[v])] = a.gscale * sv[w];
+            }
+        }
+    sync();
+    float mx[U];
+#pragma unroll
+    for (int v = 0; v < U; ++v) {
+        mx[v] = 0.f;
+        if (pix[v] >= 0) {
+            const float xn = prox<float>(xv[v] - eta * (blk[v * 256 + tid] + beta * tvg[v]), lam, a.prm->nonneg != 0);
+            xo[pix[v]] = xn;
+            if (a.xr) a.xr[sym_rot_index(pix[v] % n, pix[v] / n, n)] = xn;
+            mx[v] = fabsf(xn);
+        }
+        mx[v] = warp_max(mx[v]);
+        if ((tid & 31) == 0) red[v * 8 + (tid >> 5)] = mx[v];
+    }
+    sync();
+    if (tid < U && u0 + tid < 32) {
+        float m = red[tid * 8];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) m = fmaxf(m, red[tid * 8 + w]);
+        a.part_mx[t * 32 + u0 + tid] = m;
+    }
+    sync();  // the scratch is reused by the next claim
 }
 
 template <int IW>
@@ -537,13 +699,32 @@ __global__ void __launch_bounds__(kSymThreads, 3) bp_sym_f32_kernel(BpSymArgs a)
             for (int k = 0; k < 4; ++k)
                 if (g < 4 || !diag) dst[(g * 4 + k) * kThreads] = acc[k][g];
     };
+    // fused update: consumer-only barrier (the producer warp has left), tiles this CTA was
+    // the final arriver of
+    auto cbar = []() { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+    __shared__ int fin_s;
+    int owe0 = -1, owe1 = -1;
+    auto arrive = [&](int t) {  // after the flush of tile t: count the slot in
+        cbar();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const uint32_t old = atomicAdd(a.tile_cnt + t, 1u);
+            const int ns = __ldg(a.epi.tile_slot0 + t + 1) - __ldg(a.epi.tile_slot0 + t);
+            fin_s = (old + 1u == (uint32_t)ns) ? 1 : 0;
+        }
+        cbar();
+        if (fin_s) { if (owe0 < 0) owe0 = t; else owe1 = t; }
+    };
     int b = 0;
     uint32_t phase = 0;
     for (int c = c0; c < c1; ++c) {
         const int packed = __ldg(a.chunks + c);
         const int t = packed >> 16;
         if (t != cur) {
-            if (cur >= 0) flush();
+            if (cur >= 0) {
+                flush();
+                if (a.fuse) arrive(cur);
+            }
             ++slot;
             cur = t;
             const int tp = __ldg(a.tiles + t);
@@ -569,43 +750,54 @@ __global__ void __launch_bounds__(kSymThreads, 3) bp_sym_f32_kernel(BpSymArgs a)
     }
     griddep_launch_dependents();
     flush();
-}
-
-// K1s epilogue: CTA (tile, image g, 8-column strip) adds the tile's partial slots (4 slot
-// groups in parallel, then in order), maps the representatives to image g, and writes
-// gscale * K^T r (EPI == false) or runs the fused update of recon.py:327-338 with the block
-// statistics of the next projector scale.
-struct BpSymEpiArgs {
-    const float* part;        // [slots][8][4][kThreads]
-    const int* tile_slot0;    // [ntiles + 1]
-    const int* tiles;         // [ntiles]
-    int n, bits, lanemap;
-    float gscale;
-    float* out;               // EPI == false
-    float* xb0;               // EPI == true: x from xb[iter & 1] to xb[(iter + 1) & 1]
-    float* xb1;
-    const DevParams* prm;
-    DevState* st;
-    double* part_bp;          // [grid][4]
-    float* xr;                // EPI == true, optional: rotation-packed copy of x' for the
-                              // symmetric projector, [(n/2)^2][4] (fp_sym_f32_kernel)
-    float* part_mx;           // DEFER: [grid] max |x'| per CTA (the projector reduces them)
-};
-
-// rotation-packed index of pixel (i, j): the quadrant representative q = (qi, qj) in
-// [h, n)^2 and rotation r with rot^r(q) = (i, j) (the image order of fp_sym_f32_kernel);
-// returns 4 * ((qj - h) * h + (qi - h)) + r
-__device__ __forceinline__ int sym_rot_index(int i, int j, int n) {
-    const int h = n >> 1;
-    int qi, qj, r;
-    if (i >= h) {
-        if (j >= h) { qi = i; qj = j; r = 0; }
-        else { qi = n - 1 - j; qj = i; r = 3; }
-    } else {
-        if (j >= h) { qi = j; qj = n - 1 - i; r = 1; }
-        else { qi = n - 1 - i; qj = n - 1 - j; r = 2; }
+    if (!a.fuse) return;
+    arrive(cur);
+    // publish the tiles this CTA completed (counters reset for the next launch first), wait a
+    // bounded time for its last tile otherwise, then claim units of those tiles
+    const int iter = a.st->iter;
+    const uint32_t lid = (((uint32_t)a.st->epoch << 10) | (uint32_t)(iter & 1023)) + 1u;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 2; ++q) {
+            const int t = q == 0 ? owe0 : owe1;
+            if (t < 0) continue;
+            a.tile_cnt[t] = 0u;
+            a.tile_units[t] = 0u;
+            __threadfence();
+            st_release_u32(a.tile_done + t, lid);
+        }
+        int join = (owe0 == cur || owe1 == cur) ? 1 : 0;
+        if (!join) {
+            long long t0, now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            for (;;) {
+                if (ld_acquire_u32(a.tile_done + cur) == lid) { join = 1; break; }
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                if (now - t0 > a.spin_ns) break;
+                __nanosleep(64);
+            }
+        }
+        fin_s = join;
     }
-    return 4 * ((qj - h) * h + (qi - h)) + r;
+    cbar();
+    const int joined = fin_s;
+    // scratch for the units: the (idle) TMA ring
+    constexpr int kU = 4;  // units per claim
+    float4* part4 = reinterpret_cast<float4*>(smem);
+    float* blk = reinterpret_cast<float*>(smem + kU * 3 * 64 * 16);
+    float* red = blk + kU * 256;
+    __shared__ int unit_s;
+    for (int q = 0; q < 3; ++q) {
+        const int t = q == 0 ? owe0 : (q == 1 ? owe1 : (joined && owe0 != cur && owe1 != cur ? cur : -1));
+        if (t < 0) continue;
+        for (;;) {
+            cbar();  // every thread has read the previous claim
+            if (threadIdx.x == 0) unit_s = (int)atomicAdd(a.tile_units + t, (uint32_t)kU);
+            cbar();
+            const int u0 = unit_s;
+            if (u0 >= 32) break;
+            sym_epi_units<kU>(a.epi, t, u0, iter, part4, blk, red, cbar);
+        }
+    }
 }
 
 // DEFER (with the symmetric projector): no last-block reduction here -- the projector's CTAs
@@ -1875,6 +2067,7 @@ __global__ void init_kernel(T* xb0, int P, DevState* st, const DevIo* io) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         st->iter = 0;
         st->all_stopped = 0;
+        st->epoch += 1;
         for (int g = 0; g < NF; ++g) {
             FrameState& fs = st->fr[g];
             fs.accepted = 0;

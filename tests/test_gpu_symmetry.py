@@ -172,3 +172,29 @@ def test_throughput_grid_matches_latency_grid(oracle):
     assert np.linalg.norm(xs[0] - xs[1]) <= 1e-5 * np.linalg.norm(xs[0])
     for xv in xs:
         assert np.linalg.norm(xv - ref["image"]) <= 1e-4 * np.linalg.norm(ref["image"])
+
+
+@pytest.mark.parametrize("spin", ["20000", "0"])
+def test_fused_update_matches_epilogue_kernel(monkeypatch, oracle, spin):
+    """PK_SYM_FUSE=1 runs the update in the back-projector's tail (per-tile arrival counters,
+    bounded wait, claimed units); the image, history and status are bitwise those of the
+    separate epilogue kernel, with waiting CTAs (spin) or the final arrivers alone (0)."""
+    n, M, Q = 256, 256, 2048
+    g, ring, ac, ph = pk.make_scene(n, M, Q, seed=4)
+    K = pk.build_time_matrix(g, ring, ac)
+    o = oracle.Operator.of(oracle.make_scene(n, M, Q, 4))
+    y = o.forward(ph.values)
+    alpha, beta = oracle.resolve_regularization(o, y)
+    cfg = pk.ReconConfig(alpha, beta, 6, 2651.3)
+    out = {}
+    for fuse in ("0", "1"):
+        monkeypatch.setenv("PK_SYM_FUSE", fuse)
+        monkeypatch.setenv("PK_SYM_SPIN_NS", spin)
+        pk.clear_plan_cache()
+        res = [pk.iterative_reconstruct(K, pk.SensorData("time", M, Q, y), cfg, pool=F32) for _ in range(2)]
+        assert np.array_equal(res[0].image.values, res[1].image.values)  # graph replay
+        out[fuse] = res[1]
+    pk.clear_plan_cache()
+    assert np.array_equal(out["0"].image.values, out["1"].image.values)
+    assert np.array_equal(out["0"].objective_history, out["1"].objective_history)
+    assert out["1"].iterations_run == 6
