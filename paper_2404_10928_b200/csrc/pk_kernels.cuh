@@ -1448,17 +1448,20 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
     const float4* xr = a.x ? nullptr : a.xr;
     const int n = a.n, h = n >> 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // shared memory: records [NW][32 + kFsBatch] float4 | windows [4][LW][32] | staging
+    // [NGR][32][LW + 4] (round 0; a later round stages into the window rows the previous
+    // rounds have transposed, starting NGR * 512 B early inside the record area, so no round
+    // waits for the engine to finish reading an earlier one)
     constexpr int WW = 4 * LW * 32;  // window words
-    // images per staging round (plans never launch an instantiation whose windows do not fit:
-    // fs_ngr == 0), staging row stride
     constexpr int NGR = fs_ngr(LW, NW) > 0 ? fs_ngr(LW, NW) : 1, LWS = LW + 4;
-    int32_t* win = reinterpret_cast<int32_t*>(smem);
-    // per-warp record buffer: one float4 {xs0, xs1, xs2, xs3} per column of the piece, plus
-    // kFsBatch zero records (padding columns)
-    float4* rec = reinterpret_cast<float4*>(smem + (size_t)WW * 4) + (size_t)warp * (32 + kFsBatch);
-    int32_t* stg = reinterpret_cast<int32_t*>(smem + (size_t)WW * 4 + (size_t)NW * (32 + kFsBatch) * 16);
-    const uint32_t win_s = smem_u32(win), stg_s = smem_u32(stg);
-    bool pending = false;  // this thread has bulk reductions in flight
+    constexpr int REC = NW * (32 + kFsBatch) * 16;
+    static_assert(REC >= NGR * 512, "record area must cover the staging overhang");
+    float4* rec = reinterpret_cast<float4*>(smem) + (size_t)warp * (32 + kFsBatch);
+    int32_t* win = reinterpret_cast<int32_t*>(smem + REC);
+    int32_t* stg0 = reinterpret_cast<int32_t*>(smem + REC + (size_t)WW * 4);
+    const uint32_t win_s = smem_u32(win);
+    __shared__ int piece_s[2];  // dynamic piece counter (double-buffered by segment parity)
+    bool pending = false;       // this thread has bulk reductions in flight
     constexpr int P2 = T / 32;  // 32-column pieces per row
 
     // the 4 image values of piece q of segment (i0, j0): row j0 + q / P2, columns
@@ -1476,6 +1479,37 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
             v[1] = x[ii * n + (n - 1 - jj)];
             v[2] = x[(n - 1 - jj) * n + (n - 1 - ii)];
             v[3] = x[(n - 1 - ii) * n + jj];
+        }
+    };
+    // bias counts of segment k: u16, 8 per 16-B load
+    constexpr int NQ = (LW * 4 + NT - 1) / NT;
+    auto load_counts = [&](int k, uint4 (&c)[NQ]) {
+        const uint4* c8 = reinterpret_cast<const uint4*>(a.counts + (size_t)k * LW * 32);
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) {
+            const int q = threadIdx.x + i * NT;
+            c[i] = q < LW * 4 ? __ldg(c8 + q) : make_uint4(0, 0, 0, 0);
+        }
+    };
+    // every window slot starts at -count * bias (see fp_sym_count_kernel)
+    auto init_windows = [&](const uint4 (&c)[NQ]) {
+        int4* w4 = reinterpret_cast<int4*>(win);
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) {
+            const int q = threadIdx.x + i * NT;
+            if (q < LW * 4) {
+                const uint32_t wv[4] = {c[i].x, c[i].y, c[i].z, c[i].w};
+                int4 l4, h4;
+                l4.x = -(int)(wv[0] & 0xffffu) * kMagicBits; l4.y = -(int)(wv[0] >> 16) * kMagicBits;
+                l4.z = -(int)(wv[1] & 0xffffu) * kMagicBits; l4.w = -(int)(wv[1] >> 16) * kMagicBits;
+                h4.x = -(int)(wv[2] & 0xffffu) * kMagicBits; h4.y = -(int)(wv[2] >> 16) * kMagicBits;
+                h4.z = -(int)(wv[3] & 0xffffu) * kMagicBits; h4.w = -(int)(wv[3] >> 16) * kMagicBits;
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    w4[g * LW * 8 + 2 * q] = l4;
+                    w4[g * LW * 8 + 2 * q + 1] = h4;
+                }
+            }
         }
     };
     if (lane < kFsBatch) rec[32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1505,6 +1539,14 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
         reduce_scale();
         return;
     }
+    {   // first segment: windows initialised before the wait for the epilogue (constant data)
+        uint4 c[NQ];
+        load_counts(k0, c);
+        init_windows(c);
+        if (threadIdx.x == 0) piece_s[k0 & 1] = NW;
+    }
+    griddep_wait();  // x' and its fixed-point scale come from the back-projector epilogue
+    reduce_scale();  // (ends with a barrier: the windows are initialised)
     for (int k = k0; k < k1; ++k) {
         const int4 sg = __ldg(a.segs + k);
         const int i0 = h + T * sg.y, j0 = sg.z, j1 = sg.w;
@@ -1516,56 +1558,27 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
         const int lo = fp_sym_window_lo(a.pxs, a.pys, n, i0, j0, j1, sx, sy, a.qclamp, T);
         // word (g, k, lane) at (g*LW + k)*32 + lane, k = t - lo for trace index t
         const uint32_t adj = win_s + 4u * (uint32_t)lane - 128u * (uint32_t)lo - 128u * kTwo23Bits;
-        {   // every window slot starts at -count * bias (see fp_sym_count_kernel); counts are u16,
-            // 8 per 16-B load, all of this thread's loads in flight before the first store
-            const uint4* c8 = reinterpret_cast<const uint4*>(a.counts + (size_t)k * LW * 32);
-            int4* w4 = reinterpret_cast<int4*>(win);
-            constexpr int NQ = (LW * 4 + NT - 1) / NT;
-            uint4 c[NQ];
-#pragma unroll
-            for (int i = 0; i < NQ; ++i) {
-                const int q = threadIdx.x + i * NT;
-                c[i] = q < LW * 4 ? __ldg(c8 + q) : make_uint4(0, 0, 0, 0);
-            }
-#pragma unroll
-            for (int i = 0; i < NQ; ++i) {
-                const int q = threadIdx.x + i * NT;
-                if (q < LW * 4) {
-                    const uint32_t wv[4] = {c[i].x, c[i].y, c[i].z, c[i].w};
-                    int4 l4, h4;
-                    l4.x = -(int)(wv[0] & 0xffffu) * kMagicBits; l4.y = -(int)(wv[0] >> 16) * kMagicBits;
-                    l4.z = -(int)(wv[1] & 0xffffu) * kMagicBits; l4.w = -(int)(wv[1] >> 16) * kMagicBits;
-                    h4.x = -(int)(wv[2] & 0xffffu) * kMagicBits; h4.y = -(int)(wv[2] >> 16) * kMagicBits;
-                    h4.z = -(int)(wv[3] & 0xffffu) * kMagicBits; h4.w = -(int)(wv[3] >> 16) * kMagicBits;
-#pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                        w4[g * LW * 8 + 2 * q] = l4;
-                        w4[g * LW * 8 + 2 * q + 1] = h4;
-                    }
-                }
-            }
-        }
-        // pieces q = warp, warp + NW, ... of the segment (row j0 + q / P2, column piece q % P2);
-        // the 4 image values of the next piece are loaded while the current one scatters
+        // pieces (row j0 + q / P2, column piece q % P2) claimed dynamically (the first NW
+        // statically, one per warp); the 4 image values of the next piece are loaded while the
+        // current one scatters
         const int npc = (j1 - j0) * P2;
+        int q = warp;
+        auto claim = [&]() {
+            int v = 0;
+            if (lane == 0) v = atomicAdd(piece_s + (k & 1), 1);
+            return __shfl_sync(0xffffffffu, v, 0);
+        };
         float xn[4];
-        if (k == k0) {
-            griddep_wait();  // x' and its fixed-point scale come from the back-projector epilogue
-            piece_x(i0, j0, j1, warp, xn);  // the first piece's loads overlap the scale reduction
-            reduce_scale();
-        } else {
-            piece_x(i0, j0, j1, warp, xn);
-        }
-        __syncthreads();  // windows initialised (and the previous segment's store done)
-
-        for (int q = warp; q < npc; q += NW) {
+        piece_x(i0, j0, j1, q, xn);
+        while (q < npc) {
             const int jj = j0 + q / P2;
             const int c0 = i0 + 32 * (q % P2);
             const bool in = c0 + lane < n;
             float xv[4];
 #pragma unroll
             for (int g = 0; g < 4; ++g) xv[g] = xn[g];
-            piece_x(i0, j0, j1, q + NW, xn);
+            const int qn = claim();
+            piece_x(i0, j0, j1, qn, xn);
             // dense records: lane k writes {xs0, xs1, xs2, xs3} of column c0 + k; the scatter
             // derives px from k and xq = rint(xs) from xs, so a record is one LDS.128 (the
             // record loads share the shared-memory pipe with the atomics)
@@ -1623,9 +1636,13 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
                 else scatter(std::true_type{});
             }
             __syncwarp();  // rec is rewritten by the next piece
+            q = qn;
         }
+        // the next segment's bias counts are in flight during the barrier and the reduction
+        uint4 cn[NQ];
+        if (k + 1 < k1) load_counts(k + 1, cn);
         if (k == k1 - 1) griddep_launch_dependents();
-        __syncthreads();
+        __syncthreads();  // the segment's windows are complete
 
         // reduce-add the windows into the trace accumulator: per round, NGR images are
         // transposed to staging rows [image][lane][slot] (lane l's window is LW contiguous
@@ -1633,13 +1650,11 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
         // bulk reduction of LW words (TMA engine, integer adds at L2: order independent)
         static_assert(LW % 8 == 0, "window length must be whole 32-B sectors");
         for (int g0 = 0; g0 < 4; g0 += NGR) {
-            if (pending) bulk_wait_read_all();  // the staging rows were read by the engine
-            pending = false;
-            if (g0 > 0 || k > k0) __syncthreads();
+            int32_t* stg = g0 == 0 ? stg0 : win + (g0 - NGR) * LW * 32 - NGR * 128;
             // thread -> (image gl, lane l, 4 slots): 4 conflict-free LDS (bank l), one STS.128
             // (row stride LW + 4 words: 8 lanes of a phase hit 8 distinct 16-B bank groups)
-            for (int q = threadIdx.x; q < NGR * 32 * (LW / 4); q += NT) {
-                const int l = q & 31, r = q >> 5;
+            for (int qq = threadIdx.x; qq < NGR * 32 * (LW / 4); qq += NT) {
+                const int l = qq & 31, r = qq >> 5;
                 const int gl = r / (LW / 4), sl = (r - gl * (LW / 4)) * 4;
                 const int32_t* src = win + ((g0 + gl) * LW + sl) * 32 + l;
                 int4 v;
@@ -1656,16 +1671,24 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
                     const int lol = fp_sym_window_lo(a.pxs, a.pys, n, i0, j0, j1, __ldg(a.sxs + b),
                                                      __ldg(a.sys + b), a.qclamp, T);
                     bulk_reduce_add_u32(a.acc + (size_t)tr * a.acc_ld + kAccFront + lol,
-                                        stg_s + 4u * (uint32_t)((gl * 32 + l) * LWS), LW * 4);
+                                        smem_u32(stg + (gl * 32 + l) * LWS), LW * 4);
                     bulk_commit();
                     pending = true;
                 }
             }
         }
-        // (the last round's barrier also ends every read of the windows: the next segment may
-        // re-initialise them)
+        if (k + 1 < k1) {
+            // the staging rows (windows and records included) were read by the engine
+            if (pending) bulk_wait_read_all();
+            pending = false;
+            if (threadIdx.x == 0) piece_s[(k + 1) & 1] = NW;
+            __syncthreads();
+            init_windows(cn);
+            if (lane < kFsBatch) rec[32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);  // (staged over)
+            __syncthreads();
+        }
     }
-    if (pending) bulk_wait_all();  // the reductions are performed before the CTA retires
+    if (pending) bulk_wait_read_all();  // the staging must outlive the engine's reads
 }
 
 // ===========================================================================
