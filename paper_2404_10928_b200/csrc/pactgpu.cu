@@ -391,7 +391,10 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
         }
         a.atrick = p->bp_atrick;
         a.chunks = chunks;
-        launch_pdl(finalize_kernel<float, NF>, grid, dim3(kThreads), sm, s, a);
+        if (NF == 1 && p->fsym && p->Q <= kFinSymMax && chunks == 1)
+            launch_pdl(finalize_sym_kernel, grid, dim3(kThreads), 0, s, a);
+        else
+            launch_pdl(finalize_kernel<float, NF>, grid, dim3(kThreads), sm, s, a);
     } else {
         FinArgs<double> a{};
         a.acc = p->acc; a.y = static_cast<const double*>(y);
@@ -928,7 +931,14 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             p->fsym_groups = (p->M + 31) / 32;
             p->fsym = 0;
             const int nw = (getenv("PK_FSYM_NW") && atoi(getenv("PK_FSYM_NW")) == 16) ? 16 : 32;
-            const int per_sm = 32 / nw, G = std::max(1, sms) * per_sm;
+            // throughput mode (several plans on concurrent streams): the persistent grid is
+            // divided by concurrency / 2 so that other streams' kernels share the SMs (measured
+            // share 1 / 2 / 4: cfg4 on 8 streams 1963 / 2182 / 2293 frames/s, cfg3 on 4 streams
+            // 961 / 991 / 978, tools/r2_share.sh); PK_FSYM_SHARE overrides
+            int share = std::max(1, d->concurrency / 2);
+            if (d->concurrency > 1)
+                if (const char* e = getenv("PK_FSYM_SHARE")) share = std::max(1, atoi(e));
+            const int per_sm = 32 / nw, G = std::max(1, std::max(1, sms) * per_sm / share);
             const int hq = n / 2;
             auto region_diag = [&](int T, int H) {
                 const double ex = std::min(T - 1, hq - 1) * hx, ey = std::min(H - 1, hq - 1) * hy;

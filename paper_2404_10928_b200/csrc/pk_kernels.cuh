@@ -1851,6 +1851,97 @@ struct FinArgs {
     int chunks;          // sample chunks per sensor (one CTA each)
 };
 
+// the last residual CTA: objective terms from the per-CTA partials and the stopping rules of
+// every frame (recon.py:346-363); data_s / tv_s: block-shared scratch [NF]
+template <typename T, int NF>
+__device__ __forceinline__ void finalize_objective(const FinArgs<T>& a, int chunks, double* data_s,
+                                                   double* tv_s, double* red_d) {
+
+    if (a.tv_here) {  // NF == 1, one pass: data, TV, and the epilogue's deferred sum |x'| and
+                      // non-finite count (the residual CTAs' partials are aligned)
+        __shared__ double red4l[4 * kThreads / 32];
+        double v4[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int q = threadIdx.x; q < a.ntv; q += kThreads) {
+            v4[0] += a.part_r[q];
+            v4[1] += a.part_tv[q];
+            v4[2] += a.part_l1[2 * (size_t)q];
+            v4[3] += a.part_l1[2 * (size_t)q + 1];
+        }
+        block_sum4(v4, red4l);
+        if (threadIdx.x == 0) {
+            data_s[0] = v4[0];
+            tv_s[0] = v4[1];
+            if (!a.st->fr[0].stopped) {
+                a.st->fr[0].l1sum = v4[2];
+                a.st->fr[0].nonfinite = v4[3] > 0.0 ? 1 : 0;
+            }
+        }
+    } else {
+#pragma unroll 1
+        for (int g = 0; g < NF; ++g) {
+            double d = 0.0, t = 0.0;
+            for (int q = threadIdx.x; q < a.M * chunks; q += kThreads)
+                d += a.part_r[(size_t)g * a.M * chunks + q];
+            d = block_sum(d, red_d);
+            if (a.solver) {
+                for (int q = threadIdx.x; q < a.ntv; q += kThreads) t += a.part_tv[(size_t)q * NF + g];
+                t = block_sum(t, red_d);
+            }
+            if (threadIdx.x == 0) {
+                data_s[g] = d;
+                tv_s[g] = t;
+            }
+        }
+    }
+    if (threadIdx.x != 0) return;
+    if (a.sumsq_out)
+        for (int g = 0; g < NF; ++g) a.sumsq_out[g] = data_s[g];
+    if (!a.solver) return;
+    // objective and stopping per frame (recon.py:346-363)
+    DevState* st = a.st;
+    const DevParams* prm = a.prm;
+    const int it = st->iter;
+    const int N = prm->iterations;
+    int all = 1;
+    for (int g = 0; g < NF; ++g) {
+        FrameState& fs = st->fr[g];
+        if (!fs.stopped) {
+            const double data = data_s[g];
+            const double l1 = prm->alpha[g] * fs.l1sum;
+            const double tv = prm->beta[g] * tv_s[g];
+            const double total = data + l1 + tv;
+            if (!isfinite(total) || fs.nonfinite) {
+                fs.stopped = 1;
+                fs.stopped_by = PK_STOP_DIVERGENCE;
+            } else {
+                double* h = a.io->hist + (size_t)g * 4 * N;
+                h[it] = total;
+                h[N + it] = data;
+                h[2 * N + it] = l1;
+                h[3 * N + it] = tv;
+                fs.accepted = it + 1;
+                fs.grow = total > fs.f_prev ? fs.grow + 1 : 0;
+                if (fs.grow >= kDivergenceStreak) {
+                    fs.stopped = 1;
+                    fs.stopped_by = PK_STOP_DIVERGENCE;
+                } else {
+                    const double rel = fabs(total - fs.f_prev) / fmax(fabs(fs.f_prev), 1e-300);
+                    fs.f_prev = total;
+                    if (prm->tolerance > 0.0 && rel < prm->tolerance) {
+                        fs.stopped = 1;
+                        fs.stopped_by = PK_STOP_TOLERANCE;
+                    }
+                }
+            }
+        }
+        all &= fs.stopped;
+        a.io->status[2 * g] = fs.accepted;
+        a.io->status[2 * g + 1] = fs.stopped_by;
+    }
+    st->iter = it + 1;
+    st->all_stopped = (all || st->iter >= N) ? 1 : 0;
+}
+
 template <typename T, int NF>
 #ifndef PK_FIN_MINB
 #define PK_FIN_MINB 4  // <= 64 registers: 4 CTAs per SM (more registers cost occupancy: 94 regs -> +6 us)
@@ -1962,90 +2053,127 @@ __global__ void __launch_bounds__(kThreads, PK_FIN_MINB) finalize_kernel(FinArgs
         if (threadIdx.x == 0) a.part_r[(size_t)f * a.M * chunks + blockIdx.x] = ss;
     }
     if (!last_block(&a.st->cnt_fin, gridDim.x * gridDim.y, &last_flag)) return;
+    finalize_objective<T, NF>(a, chunks, data_s, tv_s, red_d);
+}
 
-    if (a.tv_here) {  // NF == 1, one pass: data, TV, and the epilogue's deferred sum |x'| and
-                      // non-finite count (the residual CTAs' partials are aligned)
-        __shared__ double red4l[4 * kThreads / 32];
-        double v4[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int q = threadIdx.x; q < a.ntv; q += kThreads) {
-            v4[0] += a.part_r[q];
-            v4[1] += a.part_tv[q];
-            v4[2] += a.part_l1[2 * (size_t)q];
-            v4[3] += a.part_l1[2 * (size_t)q + 1];
+// K3 for the symmetric projector (fp32, one frame): one CTA of 256 threads per trace, every
+// load issued up front -- TV(x') of the iterate (its slice) and the measurements before the
+// wait for the projection (both final by then), then the int32 accumulator row (read once,
+// then cleared for the next projection's reductions); r = w*acc/scale - y rounded as
+// finalize_kernel does, the pair table and the sums.  Q <= kFinSymMax.
+constexpr int kFinSymG = 4;                       // int4 groups per thread
+constexpr int kFinSymMax = 4 * kThreads * kFinSymG;  // 4096 samples
+__global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float> a) {
+    __shared__ float tr[kFinSymMax + 8];           // tr[1 + s] = r[s], tr[0] = 0
+    __shared__ __align__(16) float ys[kFinSymMax];  // measurements (LDGSTS: no registers held)
+    __shared__ double red_d[kThreads / 32];
+    __shared__ double red4[4 * kThreads / 32];
+    __shared__ double data_s[1], tv_s[1];
+    __shared__ int last_flag;
+    if (a.solver && a.st->all_stopped) return;
+    const int m = blockIdx.x, tid = threadIdx.x, Q = a.Q;
+    const float* ym = a.solver ? reinterpret_cast<const float*>(a.io->y) : a.y;
+    if (ym) ym += (size_t)m * Q;
+    float* om = a.trace_out ? a.trace_out + (size_t)m * Q : nullptr;
+    int32_t* accr = a.acc32 + (size_t)m * a.acc32_ld + kAccFront;
+    // measurements (constant): staged before the wait
+    if (ym) {
+        for (int k = tid; k < Q; k += kThreads) cp_async<4>(ys + k, ym + k);
+        cp_async_commit();
+    }
+    double tvp = 0.0, l1p = 0.0, badp = 0.0;
+    if (a.tv_here) {  // exact anisotropic TV of x' (recon.py:169-170), sum |x'|, non-finite
+        const float* x = (a.st->iter & 1) ? a.xb0 : a.xb1;  // the back-projector wrote xb[(iter+1)&1]
+        const int n = a.n, P = n * n, per = (P + gridDim.x - 1) / gridDim.x;
+        const int p1 = min(P, (int)(blockIdx.x + 1) * per);
+        for (int p = blockIdx.x * per + tid; p < p1; p += kThreads) {
+            const float v = x[p];
+            const float xr = (p % n + 1 < n) ? x[p + 1] : v;
+            const float xd = (p + n < P) ? x[p + n] : v;
+            l1p += (double)fabsf(v);
+            if (!isfinite(v)) badp += 1.0;
+            if (p % n + 1 < n) tvp += (double)fabsf(xr - v);
+            if (p + n < P) tvp += (double)fabsf(xd - v);
         }
-        block_sum4(v4, red4l);
-        if (threadIdx.x == 0) {
-            data_s[0] = v4[0];
-            tv_s[0] = v4[1];
-            if (!a.st->fr[0].stopped) {
-                a.st->fr[0].l1sum = v4[2];
-                a.st->fr[0].nonfinite = v4[3] > 0.0 ? 1 : 0;
+    }
+    griddep_wait();  // the projection's accumulator and scale
+    int4 v4[kFinSymG];
+#pragma unroll
+    for (int i = 0; i < kFinSymG; ++i) {
+        const int s0 = 4 * (tid + i * kThreads);
+        v4[i] = s0 < Q ? __ldcg(reinterpret_cast<const int4*>(accr + s0)) : make_int4(0, 0, 0, 0);
+    }
+    const double sc = (double)a.st->fr[0].scale32;
+    const double wq = sc > 0.0 ? a.w / sc : 0.0;
+    double ss = 0.0;
+    if (tid == 0) tr[0] = 0.f;
+    if (ym) cp_async_wait_all();
+    __syncthreads();  // ys
+#pragma unroll
+    for (int i = 0; i < kFinSymG; ++i) {
+        const int s0 = 4 * (tid + i * kThreads);
+        const int vv[4] = {v4[i].x, v4[i].y, v4[i].z, v4[i].w};
+        float yy[4];
+        if (ym && s0 + 4 <= Q) {
+            const float4 y4 = *reinterpret_cast<const float4*>(ys + s0);
+            yy[0] = y4.x; yy[1] = y4.y; yy[2] = y4.z; yy[3] = y4.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) yy[q] = (ym && s0 + q < Q) ? ys[s0 + q] : 0.f;
+        }
+        float rr[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            // K x rounded to fp32 first, then the residual (recon.py:75-79 semantics)
+            const float kx = (float)((double)vv[q] * wq);
+            rr[q] = ym ? kx - yy[q] : kx;
+            if (s0 + q < Q) {
+                tr[1 + s0 + q] = rr[q];
+                ss += (double)rr[q] * (double)rr[q];
             }
+        }
+        if (om && s0 < Q) {
+            if (s0 + 4 <= Q && ((reinterpret_cast<uintptr_t>(om) & 15) == 0))
+                *reinterpret_cast<float4*>(om + s0) = make_float4(rr[0], rr[1], rr[2], rr[3]);
+            else
+                for (int q = 0; q < 4 && s0 + q < Q; ++q) om[s0 + q] = rr[q];
+        }
+    }
+    __syncthreads();  // tr; every sample of the accumulator row was read
+    {   // clear the row, pads included, for the next projection's reductions
+        int4* row4 = reinterpret_cast<int4*>(accr - kAccFront);
+        for (int q = tid; q < a.acc32_ld / 4; q += kThreads) row4[q] = make_int4(0, 0, 0, 0);
+    }
+    // pair table entries e in [0, TS): {r[e-1], r[e] - r[e-1]}, zero padded beyond Q
+    float2* tab = a.table + (size_t)m * a.TS;
+    for (int e0 = 2 * tid; e0 < a.TS; e0 += 2 * kThreads) {
+        float2 p2[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int e = e0 + q;
+            const float rp = (e >= 1 && e - 1 < Q) ? tr[e] : 0.f;
+            const float rc = (e < Q) ? tr[e + 1] : 0.f;
+            p2[q] = pair_entry<float>(rp, rc, e, a.atrick);
+        }
+        if (e0 + 1 < a.TS) *reinterpret_cast<float4*>(tab + e0) = make_float4(p2[0].x, p2[0].y, p2[1].x, p2[1].y);
+        else tab[e0] = p2[0];
+    }
+    griddep_launch_dependents();
+    if (a.tv_here) {
+        double w4[4] = {ss, tvp, l1p, badp};
+        block_sum4(w4, red4);
+        if (tid == 0) {
+            a.part_r[blockIdx.x] = w4[0];
+            a.part_tv[blockIdx.x] = w4[1];
+            a.part_l1[2 * (size_t)blockIdx.x] = w4[2];
+            a.part_l1[2 * (size_t)blockIdx.x + 1] = w4[3];
         }
     } else {
-#pragma unroll 1
-        for (int g = 0; g < NF; ++g) {
-            double d = 0.0, t = 0.0;
-            for (int q = threadIdx.x; q < a.M * chunks; q += kThreads)
-                d += a.part_r[(size_t)g * a.M * chunks + q];
-            d = block_sum(d, red_d);
-            if (a.solver) {
-                for (int q = threadIdx.x; q < a.ntv; q += kThreads) t += a.part_tv[(size_t)q * NF + g];
-                t = block_sum(t, red_d);
-            }
-            if (threadIdx.x == 0) {
-                data_s[g] = d;
-                tv_s[g] = t;
-            }
-        }
+        ss = block_sum(ss, red_d);
+        if (tid == 0) a.part_r[blockIdx.x] = ss;
     }
-    if (threadIdx.x != 0) return;
-    if (a.sumsq_out)
-        for (int g = 0; g < NF; ++g) a.sumsq_out[g] = data_s[g];
-    if (!a.solver) return;
-    // objective and stopping per frame (recon.py:346-363)
-    DevState* st = a.st;
-    const DevParams* prm = a.prm;
-    const int it = st->iter;
-    const int N = prm->iterations;
-    int all = 1;
-    for (int g = 0; g < NF; ++g) {
-        FrameState& fs = st->fr[g];
-        if (!fs.stopped) {
-            const double data = data_s[g];
-            const double l1 = prm->alpha[g] * fs.l1sum;
-            const double tv = prm->beta[g] * tv_s[g];
-            const double total = data + l1 + tv;
-            if (!isfinite(total) || fs.nonfinite) {
-                fs.stopped = 1;
-                fs.stopped_by = PK_STOP_DIVERGENCE;
-            } else {
-                double* h = a.io->hist + (size_t)g * 4 * N;
-                h[it] = total;
-                h[N + it] = data;
-                h[2 * N + it] = l1;
-                h[3 * N + it] = tv;
-                fs.accepted = it + 1;
-                fs.grow = total > fs.f_prev ? fs.grow + 1 : 0;
-                if (fs.grow >= kDivergenceStreak) {
-                    fs.stopped = 1;
-                    fs.stopped_by = PK_STOP_DIVERGENCE;
-                } else {
-                    const double rel = fabs(total - fs.f_prev) / fmax(fabs(fs.f_prev), 1e-300);
-                    fs.f_prev = total;
-                    if (prm->tolerance > 0.0 && rel < prm->tolerance) {
-                        fs.stopped = 1;
-                        fs.stopped_by = PK_STOP_TOLERANCE;
-                    }
-                }
-            }
-        }
-        all &= fs.stopped;
-        a.io->status[2 * g] = fs.accepted;
-        a.io->status[2 * g + 1] = fs.stopped_by;
-    }
-    st->iter = it + 1;
-    st->all_stopped = (all || st->iter >= N) ? 1 : 0;
+    if (!last_block(&a.st->cnt_fin, gridDim.x, &last_flag)) return;
+    finalize_objective<float, 1>(a, 1, data_s, tv_s, red_d);
 }
 
 // ===========================================================================
