@@ -152,7 +152,7 @@ void free_plan(pk_plan* p) {
                     p->status_dev, p->part_bp, p->part_mx, p->part_l1, p->part_tv, p->part_r, p->part_misc, p->state,
                     p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt, p->sym_sync, p->sym_tiles,
                     p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0, p->sym_tile_slot0,
-                    p->sym_part, p->fsym_acc, p->fsym_trace, p->fsym_counts,
+                    p->sym_part, p->fsym_acc, p->fsym_trace, p->fsym_counts, p->fsym_rec,
                     p->fsym_segs, p->fsym_cta_seg0,
                     p->freq_part, p->gid, p->loc};
     for (void* q : ptrs)
@@ -289,7 +289,7 @@ void launch_maxabs_t(pk_plan* p, const void* x, cudaStream_t s) {
 template <int NF>
 void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
     dim3 grid(p->fp_tiles_x * p->fp_tiles_y, p->fp_groups);
-    if (p->dtype == PK_F32 && NF == 1 && p->fsym) {
+    if (p->dtype == PK_F32 && p->fsym) {
         FpSymArgs a{};
         a.x = static_cast<const float*>(x);
         a.xb0 = static_cast<const float*>(p->xbuf[0]);
@@ -298,6 +298,7 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
         a.acc = p->fsym_acc; a.acc_ld = p->fsym_acc_ld; a.trace_of = p->fsym_trace;
         a.n = p->nx; a.M = p->M; a.Q = p->Q;
         a.segs = p->fsym_segs; a.cta_seg0 = p->fsym_cta_seg0;
+        a.rec = p->fsym_rec; a.groups = p->fsym_groups;
         a.qclamp = (float)p->Q + 1.5f;
         a.hx = p->fsym_hx;
         a.st = p->state; a.solver = solver;
@@ -375,8 +376,8 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
         a.M = p->M; a.Q = p->Q; a.TS = p->TS; a.w = p->w;
         a.st = p->state; a.prm = p->params; a.io = p->io; a.part_r = p->part_r;
         a.part_tv = p->part_tv;
-        a.ntv = (NF == 1 && p->fsym) ? (int)grid.x : p->fp_tiles_x * p->fp_tiles_y;
-        if (NF == 1 && p->fsym && solver) {
+        a.ntv = p->fsym ? (int)grid.x : p->fp_tiles_x * p->fp_tiles_y;
+        if (p->fsym && solver) {
             a.part_l1 = p->part_l1;
             a.tv_here = 1;
             a.xb0 = static_cast<const float*>(p->xbuf[0]);
@@ -385,14 +386,14 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
         }
         a.sumsq_out = sumsq;
         a.solver = solver;
-        if (NF == 1 && p->fsym) {
+        if (p->fsym) {
             a.acc32 = p->fsym_acc;
             a.acc32_ld = p->fsym_acc_ld;
         }
         a.atrick = p->bp_atrick;
         a.chunks = chunks;
-        if (NF == 1 && p->fsym && p->Q <= kFinSymMax && chunks == 1)
-            launch_pdl(finalize_sym_kernel, grid, dim3(kThreads), 0, s, a);
+        if (p->fsym && p->Q <= kFinSymMax && chunks == 1)
+            launch_pdl(finalize_sym_kernel<NF>, grid, dim3(kThreads), 0, s, a);
         else
             launch_pdl(finalize_kernel<float, NF>, grid, dim3(kThreads), sm, s, a);
     } else {
@@ -413,7 +414,7 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
 template <int NF>
 void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_t s) {
     const bool clamp = p->max_delay >= (double)p->Q + 0.5;
-    if (p->dtype == PK_F32 && NF == 1 && p->sym) {
+    if (p->dtype == PK_F32 && p->sym) {
         BpSymArgs A{};
         A.table = static_cast<const float2*>(p->table);
         A.pxs = p->pxs; A.pys = p->pys; A.sxs = p->sxs; A.sys = p->sys;
@@ -423,6 +424,7 @@ void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_
         A.tiles = p->sym_tiles; A.part = p->sym_part; A.lanemap = p->sym_lanemap;
         A.st = epi ? p->state : nullptr;
         A.gid = p->gid; A.loc = p->loc; A.Mall = p->Mall;
+        A.ntiles = p->sym_ntiles; A.table_fstride = (size_t)p->M * p->TS;
         BpSymEpiArgs E{};
         E.part = p->sym_part; E.tile_slot0 = p->sym_tile_slot0; E.tiles = p->sym_tiles;
         E.n = p->nx; E.bits = p->fp_bits; E.lanemap = p->sym_lanemap;
@@ -433,9 +435,10 @@ void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_
         E.prm = p->params; E.st = p->state; E.part_bp = p->part_bp;
         E.xr = p->fsym ? p->fsym_xr : nullptr;
         E.part_mx = p->part_mx;
+        E.ntiles = p->sym_ntiles; E.P = p->P;
         // solver mode with the symmetric projector: the update runs in the back-projector's
         // tail (no epilogue launch); PK_SYM_FUSE=0 keeps the separate epilogue kernel
-        A.fuse = (epi && p->fsym && p->sym_fuse) ? 1 : 0;
+        A.fuse = (epi && p->fsym && p->sym_fuse && NF == 1) ? 1 : 0;
         A.epi = E;
         A.tile_cnt = p->sym_sync;
         A.tile_units = p->sym_sync + p->sym_ntiles;
@@ -449,7 +452,7 @@ void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_
             case 256: launch_sym<256>(A, p->sym_grid, p->sym_smem, s); break;
             default: launch_sym<0>(A, p->sym_grid, p->sym_smem, s); break;
         }
-        const dim3 eg(p->sym_ntiles * 32);
+        const dim3 eg(p->sym_ntiles * 32 * NF);
         if (A.fuse) return;
         if (epi && p->fsym) launch_pdl(bp_sym_epi_kernel<true, true>, eg, dim3(kThreads), 0, s, E);
         else if (epi) launch_pdl(bp_sym_epi_kernel<true, false>, eg, dim3(kThreads), 0, s, E);
@@ -501,7 +504,7 @@ void launch_table_t(pk_plan* p, const void* y, int init, cudaStream_t s) {
     if (p->dtype == PK_F32)
         table_kernel<float, NF><<<grid, kThreads, 0, s>>>(
             static_cast<const float*>(y), p->io, static_cast<float2*>(p->table), p->M, p->Q, p->TS,
-            init ? -1.f : 1.f, p->part_r, p->state, init, p->bp_atrick);
+            init ? -1.f : 1.f, p->part_r, p->state, init, p->bp_atrick, p->sym ? 1 : 0);
     else
         table_kernel<double, 1><<<grid, kThreads, 0, s>>>(
             static_cast<const double*>(y), p->io, static_cast<double2*>(p->table), p->M, p->Q,
@@ -547,7 +550,7 @@ int launch_maxabs(pk_plan* p, const void* x, cudaStream_t s) {
 int launch_fp(pk_plan* p, const void* x, int solver, cudaStream_t s) {
     // the fixed-point accumulator must be zero on entry (finalize only reads it); the
     // symmetric projector writes whole windows instead
-    if (!(p->fsym && p->nf == 1))
+    if (!p->fsym)
         PK_CUDA(cudaMemsetAsync(p->acc, 0, (size_t)p->M * p->Q * p->nf * sizeof(long long), s));
     PK_DISPATCH(launch_fp_t, p, x, solver, s);
     return PK_OK;
@@ -806,7 +809,9 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         const char* ev = getenv("PK_SYM");
         // the plan's sensors must be closed under the ring's D4 (a whole ring, or a shard
         // listing whole orbits): every image of a base sensor is then a local trace
-        bool ok = (ev ? atoi(ev) != 0 : true) && p->dtype == PK_F32 && nf == 1 &&
+        // (batched frames: the symmetric kernels take frame-major work, NF <= 4; the residual
+        // kernel of the batched symmetric path holds a trace of <= kFinSymMax samples)
+        bool ok = (ev ? atoi(ev) != 0 : true) && p->dtype == PK_F32 && (nf == 1 || p->Q <= kFinSymMax) &&
                   p->nx == p->ny && (p->nx % 2) == 0 && p->nx >= 2 * kSymTile && (p->Mall % 4) == 0;
         const int n = p->nx;
         double scl = 0.0;
@@ -870,7 +875,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 {
                     int64_t wsum = 0;
                     for (int t = 0; t < p->sym_ntiles; ++t)
-                        wsum += (int64_t)nch * (((tl[t] >> 16) == (tl[t] & 0xffff)) ? kSymWDiag : kSymWOff);
+                        wsum += (int64_t)nch * nf * (((tl[t] >> 16) == (tl[t] & 0xffff)) ? kSymWDiag : kSymWOff);
                     p->sym_grid = (int)std::max<int64_t>(32, std::min<int64_t>((int64_t)occ * sms, wsum / 64));
                     // throughput mode (several plans on concurrent streams): at most half the
                     // occupancy-limited grid -- config 3 on 4 streams 1013 -> 1027 frames/s; a
@@ -887,14 +892,16 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 std::vector<int>& ts0 = p->sym_h[4];
                 int64_t W = 0;
                 for (int t = 0; t < p->sym_ntiles; ++t)
-                    W += (int64_t)nch * (((tl[t] >> 16) == (tl[t] & 0xffff)) ? kSymWDiag : kSymWOff);
+                    W += (int64_t)nch * nf * (((tl[t] >> 16) == (tl[t] & 0xffff)) ? kSymWDiag : kSymWOff);
                 const int G = p->sym_grid;
                 c0.assign(G + 1, 0);
                 cs0.assign(G, 0);
                 int64_t cw = 0;
                 int owner_prev = -1, tile_prev = -1, slot = -1;
-                for (int t = 0; t < p->sym_ntiles; ++t) {
-                    const int wt = ((tl[t] >> 16) == (tl[t] & 0xffff)) ? kSymWDiag : kSymWOff;
+                // frame-major tiles: chunk tile index t = frame * ntiles + tile
+                for (int t = 0; t < p->sym_ntiles * nf; ++t) {
+                    const int tt = t % p->sym_ntiles;
+                    const int wt = ((tl[tt] >> 16) == (tl[tt] & 0xffff)) ? kSymWDiag : kSymWOff;
                     for (int k = 0; k < nch; ++k) {
                         const int owner = (int)std::min<int64_t>(G - 1, cw * G / W);
                         if (owner != owner_prev || t != tile_prev) {
@@ -944,11 +951,12 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 const double ex = std::min(T - 1, hq - 1) * hx, ey = std::min(H - 1, hq - 1) * hy;
                 return std::sqrt(ex * ex + ey * ey);
             };
+            // (batched frames: the sequence is frame-major, segment group index f * groups + group)
             auto segment = [&](int T, int hs, std::vector<int4>* sg, std::vector<int>* c0) {
                 const int qt = (hq + T - 1) / T;
-                const long long R = (long long)p->fsym_groups * qt * hq;
+                const long long R = (long long)nf * p->fsym_groups * qt * hq;
                 int cnt = 0;
-                std::vector<int> per_group(p->fsym_groups, 0);
+                std::vector<int> per_group(nf * p->fsym_groups, 0);
                 for (int c = 0; c < G; ++c) {
                     long long r0 = R * c / G;
                     const long long r1 = R * (c + 1) / G;
@@ -972,7 +980,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             for (int T : {64, 32}) {
                 if (evt && atoi(evt) != T) continue;
                 const int qt = (hq + T - 1) / T;
-                const long long R = (long long)p->fsym_groups * qt * hq;
+                const long long R = (long long)nf * p->fsym_groups * qt * hq;
                 const int rows_per = (int)((R + G - 1) / G);
                 const char* evl = getenv("PK_FSYM_LW");
                 for (int lw : {96, 128, 184, 256, 320}) {
@@ -1005,9 +1013,13 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 p->fsym_cta_seg0_h.clear();
                 const auto sc = segment(p->fsym_T, p->fsym_hs, &p->fsym_segs_h, &p->fsym_cta_seg0_h);
                 p->fsym_nseg = sc.first;
+                // the CTA of each frame's first segment records the frame's fixed-point scale
+                p->fsym_rec_h.assign(nf, 0);
+                for (int k = p->fsym_nseg - 1; k >= 0; --k) p->fsym_rec_h[p->fsym_segs_h[k].x / p->fsym_groups] = k;
                 p->fsym_acc_ld = ((kAccFront + p->Q + p->fsym_L + 4) + 3) & ~3;
             }
         }
+        if (nf > 1 && !p->fsym) p->sym = 0;  // batched symmetric plans need the symmetric projector
         if (p->fsym) {
             // fixed-point bound of the segment windows (may be tighter than the generic tile's)
             const double T = p->fsym_T, H = p->fsym_hs;
@@ -1092,19 +1104,20 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     A(alloc(p, reinterpret_cast<unsigned char**>(&p->xbuf[1]), (size_t)p->P * ts * nf));
     const int ntile_max = std::max(p->bp_tiles_x * p->bp_tiles_y, p->sym ? 32 * p->sym_ntiles : 0);
     A(alloc(p, &p->part_bp, (size_t)4 * nf * std::max(ntile_max, (p->P + kThreads - 1) / kThreads)));
-    A(alloc(p, &p->part_mx, (size_t)std::max(1, p->sym ? 32 * p->sym_ntiles : 1)));
-    A(alloc(p, &p->part_l1, (size_t)(p->fsym ? 2 * 8 * p->M : 1)));
+    A(alloc(p, &p->part_mx, (size_t)std::max(1, p->sym ? 32 * p->sym_ntiles * nf : 1)));
+    A(alloc(p, &p->part_l1, (size_t)(p->fsym ? 2 * 8 * p->M * nf : 1)));
     const int fsym_units = p->fsym ? p->fsym_nseg : 0;
     // TV partials: per projector tile, or per residual CTA (M x up to 8 chunks) with the
     // symmetric projector
     A(alloc(p, &p->part_tv, (size_t)std::max(p->fp_tiles_x * p->fp_tiles_y, p->fsym ? 8 * p->M : 0) * nf));
     if (p->fsym) {
-        A(alloc(p, &p->fsym_acc, (size_t)p->M * p->fsym_acc_ld));
+        A(alloc(p, &p->fsym_acc, (size_t)nf * p->M * p->fsym_acc_ld));
+        A(alloc(p, &p->fsym_rec, (size_t)nf));
         A(alloc(p, &p->fsym_trace, (size_t)p->fsym_groups * 32 * 4));
         A(alloc(p, &p->fsym_counts, (size_t)fsym_units * 32 * p->fsym_L));
         A(alloc(p, &p->fsym_segs, p->fsym_segs_h.size()));
         A(alloc(p, &p->fsym_cta_seg0, p->fsym_cta_seg0_h.size()));
-        A(alloc(p, &p->fsym_xr, (size_t)(p->nx / 2) * (p->nx / 2) * 4));
+        A(alloc(p, &p->fsym_xr, (size_t)(p->nx / 2) * (p->nx / 2) * 4 * nf));
     }
     // one CTA per sensor: more, shorter CTAs only add latency (measured 10.3 / 12.8 / 18.2 us
     // for 1 / 2 / 4 chunks at config 3)
@@ -1115,7 +1128,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     A(alloc(p, &p->part_misc, (size_t)4 * p->misc_blocks * nf));
     if (p->bp_split > 1) A(alloc(p, &p->bp_gpart, (size_t)p->bp_split * p->P * nf));
     A(alloc(p, &p->bp_tile_cnt, (size_t)ntile_max));
-    if (p->sym) A(alloc(p, &p->sym_sync, (size_t)3 * p->sym_ntiles));
+    if (p->sym) A(alloc(p, &p->sym_sync, (size_t)3 * p->sym_ntiles * nf));
     if (p->sym) {
         A(alloc(p, &p->sym_tiles, p->sym_h[0].size()));
         A(alloc(p, &p->sym_chunks, p->sym_h[1].size()));
@@ -1141,7 +1154,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     if (e == cudaSuccess) e = cudaMemset(p->state, 0, sizeof(DevState));
     if (e == cudaSuccess)
         e = cudaMemset(p->bp_tile_cnt, 0, sizeof(uint32_t) * ntile_max);
-    if (e == cudaSuccess && p->sym) e = cudaMemset(p->sym_sync, 0, sizeof(uint32_t) * 3 * p->sym_ntiles);
+    if (e == cudaSuccess && p->sym) e = cudaMemset(p->sym_sync, 0, sizeof(uint32_t) * 3 * p->sym_ntiles * nf);
     if (p->sym) {
         int* dsts[5] = {p->sym_tiles, p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0,
                         p->sym_tile_slot0};
@@ -1153,7 +1166,8 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         const int nseg = p->fsym_nseg;
         up(p->fsym_segs, p->fsym_segs_h.data(), sizeof(int4) * nseg);
         up(p->fsym_cta_seg0, p->fsym_cta_seg0_h.data(), sizeof(int) * p->fsym_cta_seg0_h.size());
-        if (e == cudaSuccess) e = cudaMemset(p->fsym_acc, 0, sizeof(int32_t) * (size_t)p->M * p->fsym_acc_ld);
+        if (e == cudaSuccess) e = cudaMemset(p->fsym_acc, 0, sizeof(int32_t) * (size_t)nf * p->M * p->fsym_acc_ld);
+        up(p->fsym_rec, p->fsym_rec_h.data(), sizeof(int) * nf);
         {
             const int zero = 0;
             if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_counts_overflow, &zero, sizeof(int));
@@ -1161,11 +1175,11 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             if (e == cudaSuccess) {
                 if (p->max_delay >= (double)p->Q + 0.5)
                     fp_sym_count_kernel<true><<<nseg, kFsThreads, csm>>>(
-                        p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_segs, (float)p->Q + 1.5f,
+                        p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups, p->fsym_segs, (float)p->Q + 1.5f,
                         p->fsym_hx, p->fsym_L, p->fsym_T, p->fsym_counts);
                 else
                     fp_sym_count_kernel<false><<<nseg, kFsThreads, csm>>>(
-                        p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_segs, (float)p->Q + 1.5f,
+                        p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups, p->fsym_segs, (float)p->Q + 1.5f,
                         p->fsym_hx, p->fsym_L, p->fsym_T, p->fsym_counts);
                 e = cudaGetLastError();
             }

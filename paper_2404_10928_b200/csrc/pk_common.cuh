@@ -374,7 +374,9 @@ struct pk_plan {
     uint16_t* fsym_counts = nullptr;  // [segments][L][32] biased words per window slot (u16)
     int4* fsym_segs = nullptr;    // [segments] {group, strip, first row, end row}
     int* fsym_cta_seg0 = nullptr; // [grid + 1]
+    int* fsym_rec = nullptr;      // [frames] segment that records the frame's scale
     std::vector<int4> fsym_segs_h;
+    std::vector<int> fsym_rec_h;
     std::vector<int> fsym_cta_seg0_h;
     int fin_chunks = 1;  // residual kernel: sample chunks per sensor
     float* bp_gpart = nullptr;

@@ -380,6 +380,8 @@ struct BpSymEpiArgs {
     float* xr;                // EPI == true, optional: rotation-packed copy of x' for the
                               // symmetric projector, [(n/2)^2][4] (fp_sym_f32_kernel)
     float* part_mx;           // DEFER: [grid] max |x'| per CTA (the projector reduces them)
+    int ntiles;               // representative tiles per frame (units: frame-major tiles)
+    int P;                    // pixels per frame (frame stride of x; x' packed: P / 4)
 };
 
 // rotation-packed index of pixel (i, j): the quadrant representative q = (qi, qj) in
@@ -416,6 +418,8 @@ struct BpSymArgs {
     const int* gid;          // [M] ring index of local sensor (base sensors are local)
     const int* loc;          // [Mall] local index of a ring sensor (the images of a base)
     int Mall;                // ring size (the D4 images are ring indices)
+    int ntiles;              // tiles per frame: chunk tile indices are f * ntiles + tile
+    size_t table_fstride;    // [frames][M][TS] pair tables: M * TS entries per frame
     // fused update (solver mode with the symmetric projector): the CTAs whose last tile is t
     // run the update of t once all of its partial slots are in (per-tile arrival counter);
     // the final arriver publishes the tile, waiting CTAs join within a bounded spin, and the 32
@@ -650,7 +654,8 @@ __global__ void __launch_bounds__(kSymThreads, 3) bp_sym_f32_kernel(BpSymArgs a)
         for (int c = c0; c < c1; ++c) {
             if (c - c0 >= a.nbuf) mbar_wait(empty_s + 8 * b, phase ^ 1u);
             const int packed = __ldg(a.chunks + c);
-            const int tp = __ldg(a.tiles + (packed >> 16));
+            const int fr = (packed >> 16) / a.ntiles;  // frame of the chunk
+            const int tp = __ldg(a.tiles + (packed >> 16) - fr * a.ntiles);
             const int tx = tp >> 16, ty = tp & 0xffff;
             const int ng = (tx == ty) ? 4 : 8;
             const int i0 = h + kSymTile * tx, j0 = h + kSymTile * ty;
@@ -676,7 +681,8 @@ __global__ void __launch_bounds__(kSymThreads, 3) bp_sym_f32_kernel(BpSymArgs a)
             __syncwarp();
             if (act)
                 bulk_g2s(dst0 + (uint32_t)g * img_stride,
-                         a.table + (size_t)__ldg(a.loc + sym_sensor(g, __ldg(a.gid + mm), a.Mall)) * a.TS + lo,
+                         a.table + fr * a.table_fstride +
+                             (size_t)__ldg(a.loc + sym_sensor(g, __ldg(a.gid + mm), a.Mall)) * a.TS + lo,
                          (uint32_t)(a.L * 8),
                          full_s + 8 * b);
             if (++b == a.nbuf) { b = 0; phase ^= 1u; }
@@ -727,7 +733,7 @@ __global__ void __launch_bounds__(kSymThreads, 3) bp_sym_f32_kernel(BpSymArgs a)
             }
             ++slot;
             cur = t;
-            const int tp = __ldg(a.tiles + t);
+            const int tp = __ldg(a.tiles + t % a.ntiles);
             const int tx = tp >> 16, ty = tp & 0xffff;
             diag = tx == ty;
             const int i0 = h + kSymTile * tx, j0 = h + kSymTile * ty;
@@ -818,8 +824,9 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
     // CTA = (tile, image g, strip k): the main kernel's consumer thread c holds, in slot
     // element [g][k][c], the sum for representative (i0 + 8k + lx, j0 + 4(c / 32) + ly) -- an
     // 8-column strip of the tile, 256 pixels
-    const int k = blockIdx.x & 3, g = (blockIdx.x >> 2) & 7, t = blockIdx.x >> 5;
-    const int tp = __ldg(a.tiles + t);
+    const int k = blockIdx.x & 3, g = (blockIdx.x >> 2) & 7, t = blockIdx.x >> 5;  // t: frame-major
+    const int fr = t / a.ntiles;
+    const int tp = __ldg(a.tiles + t - fr * a.ntiles);
     const int tx = tp >> 16, ty = tp & 0xffff;
     const bool active = !(tx == ty && g >= 4);
     const int n = a.n, h = n >> 1;
@@ -889,23 +896,24 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
         val = blk[threadIdx.x];
     }
     if (!EPI) {
-        if (pix >= 0) a.out[pix] = val;
+        if (pix >= 0) a.out[(size_t)fr * a.P + pix] = val;
         return;
     }
-    const float* x = (iter & 1) ? a.xb1 : a.xb0;
-    float* xo = (iter & 1) ? a.xb0 : a.xb1;
-    const float eta = (float)a.prm->step[0], lam = (float)a.prm->eta_alpha[0];
-    const float beta = (float)a.prm->beta[0], eps = (float)a.prm->eps;
+    const float* x = ((iter & 1) ? a.xb1 : a.xb0) + (size_t)fr * a.P;
+    float* xo = ((iter & 1) ? a.xb0 : a.xb1) + (size_t)fr * a.P;
+    float* xr = a.xr ? a.xr + (size_t)fr * a.P : nullptr;  // (4 * (n/2)^2 = P floats per frame)
+    const float eta = (float)a.prm->step[fr], lam = (float)a.prm->eta_alpha[fr];
+    const float beta = (float)a.prm->beta[fr], eps = (float)a.prm->eps;
     const bool nonneg = a.prm->nonneg != 0;
     float mx = 0.f, l1 = 0.f;
     int bad = 0;
-    if (!a.st->fr[0].stopped && pix >= 0) {
+    if (!a.st->fr[fr].stopped && pix >= 0) {
         const int p = pix;
         float gr = val;
         if (beta > 0.f && PK_EPX != 3) gr += beta * tv_grad_at<float>(x, p, p % n, p / n, n, n, eps * eps);
         const float xn = prox<float>(x[p] - eta * gr, lam, nonneg);
         xo[p] = xn;
-        if (a.xr) a.xr[sym_rot_index(p % n, p / n, n)] = xn;
+        if (xr) xr[sym_rot_index(p % n, p / n, n)] = xn;
         if (!isfinite(xn)) bad = 1;
         mx = fabsf(xn);
         l1 = fabsf(xn);
@@ -1332,8 +1340,10 @@ struct FpSymArgs {
     int acc_ld;
     const int* trace_of;     // [groups * 32][4] local trace of (base sensor, image), -1: none
     const uint16_t* counts;  // [segments][LW][32] biased words per window slot (fp_sym_count_kernel)
-    const int4* segs;        // [segments] {group, strip, first row, end row} (rows absolute)
+    const int4* segs;        // [segments] {frame * groups + group, strip, first row, end row}
     const int* cta_seg0;     // [grid + 1] first segment of each CTA
+    const int* rec;          // [frames] the segment whose CTA records the frame's scale
+    int groups;              // sensor groups per frame
     int n, M, Q;
     float qclamp;
     float hx;                // pixel pitch in samples (pxs[i] ~ pxs[0] + i*hx, fp32)
@@ -1394,7 +1404,8 @@ __device__ __forceinline__ int* counts_overflow_flag() { return &g_counts_overfl
 template <bool CLAMP>
 __global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* pxs, const float* pys,
                                                                   const float* sxs, const float* sys,
-                                                                  int n, int M, const int4* segs,
+                                                                  int n, int M, int groups,
+                                                                  const int4* segs,
                                                                   float qclamp, float hx, int LW,
                                                                   int T, uint16_t* counts) {
     extern __shared__ int32_t cnt[];  // [LW][32]
@@ -1402,7 +1413,7 @@ __global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* p
     const int u = blockIdx.x;
     const int4 sg = segs[u];
     const int i0 = h + T * sg.y;
-    const int mm = min(sg.x * 32 + lane, M - 1);
+    const int mm = min((sg.x % groups) * 32 + lane, M - 1);  // (segment group: f * groups + group)
     const float sx = __ldg(sxs + mm), sy = __ldg(sys + mm);
     const int lo = fp_sym_window_lo(pxs, pys, n, i0, sg.z, sg.w, sx, sy, qclamp, T);
     for (int q = threadIdx.x; q < LW * 32; q += kFsThreads) cnt[q] = 0;
@@ -1443,10 +1454,13 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
         iter = a.st->iter;
     }
     const int k0 = a.cta_seg0[blockIdx.x], k1 = a.cta_seg0[blockIdx.x + 1];
-    if (k0 >= k1 && !(blockIdx.x == 0 && a.part_mx)) return;  // (CTA 0 records the scale)
-    const float* x = a.x ? a.x : ((iter & 1) ? a.xb0 : a.xb1);  // bp wrote xb[(iter+1)&1]
-    const float4* xr = a.x ? nullptr : a.xr;
+    if (k0 >= k1) return;
+    const float* xall = a.x ? a.x : ((iter & 1) ? a.xb0 : a.xb1);  // bp wrote xb[(iter+1)&1]
     const int n = a.n, h = n >> 1;
+    // frame of the current segment: its x', packed x' and accumulator
+    const float* x = xall;
+    const float4* xr = a.x ? nullptr : a.xr;
+    int32_t* acc = a.acc;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // shared memory: records [NW][32 + kFsBatch] float4 | windows [4][LW][32] | staging
     // [NGR][32][LW + 4] (round 0; a later round stages into the window rows the previous
@@ -1514,31 +1528,35 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
     };
     if (lane < kFsBatch) rec[32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
     float scale = 0.f;
-    // the fixed-point scale: deferred statistics (every CTA reduces the epilogue's max
-    // partials; CTA 0 records it for the residual kernel) or the plan state
-    auto reduce_scale = [&]() {
+    int cur_fr = -1;
+    // the fixed-point scale of frame fr: deferred statistics (every CTA reduces the epilogue's
+    // max partials of the frame; the CTA of segment rec[fr] records it for the residual kernel)
+    // or the plan state.  Ends with a barrier.
+    auto reduce_scale = [&](int fr, int k) {
         if (a.part_mx) {
             __shared__ float red_f[NW];
             float mx = 0.f;
-            for (int q = threadIdx.x; q < a.nmx; q += NT) mx = fmaxf(mx, __ldcg(a.part_mx + q));
+            for (int q = threadIdx.x; q < a.nmx; q += NT) mx = fmaxf(mx, __ldcg(a.part_mx + (size_t)fr * a.nmx + q));
             mx = block_max<float, NT>(mx, red_f);
             const double scl = (mx > 0.f && isfinite(mx)) ? ldexp(1.0, a.bits) / (double)mx : 0.0;
             scale = (float)scl;
-            if (blockIdx.x == 0 && threadIdx.x == 0 && !a.st->fr[0].stopped) {
-                FrameState& fs = a.st->fr[0];
+            if (k == __ldg(a.rec + fr) && threadIdx.x == 0 && !a.st->fr[fr].stopped) {
+                FrameState& fs = a.st->fr[fr];
                 fs.maxabs = mx;
                 fs.scale64 = scl;
                 fs.scale32 = (float)scl;
             }
         } else {
-            scale = a.st->fr[0].scale32;
+            scale = a.st->fr[fr].scale32;
+            __syncthreads();
         }
     };
-    if (k0 >= k1) {  // CTA 0 without rows (tiny grids)
-        griddep_wait();
-        reduce_scale();
-        return;
-    }
+    auto set_frame = [&](int fr) {
+        cur_fr = fr;
+        x = xall + (size_t)fr * n * n;
+        xr = a.x ? nullptr : a.xr + (size_t)fr * h * h;
+        acc = a.acc + (size_t)fr * a.M * a.acc_ld;
+    };
     {   // first segment: windows initialised before the wait for the epilogue (constant data)
         uint4 c[NQ];
         load_counts(k0, c);
@@ -1546,11 +1564,15 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
         if (threadIdx.x == 0) piece_s[k0 & 1] = NW;
     }
     griddep_wait();  // x' and its fixed-point scale come from the back-projector epilogue
-    reduce_scale();  // (ends with a barrier: the windows are initialised)
     for (int k = k0; k < k1; ++k) {
         const int4 sg = __ldg(a.segs + k);
+        const int fr = sg.x / a.groups, grp = sg.x - fr * a.groups;
+        if (fr != cur_fr) {  // (ends with a barrier: the windows are initialised)
+            set_frame(fr);
+            reduce_scale(fr, k);
+        }
         const int i0 = h + T * sg.y, j0 = sg.z, j1 = sg.w;
-        const int m = sg.x * 32 + lane;
+        const int m = grp * 32 + lane;
         const bool sensor_ok = m < a.M;
         const int mm = min(m, a.M - 1);
         const float sx = __ldg(a.sxs + mm), sy = __ldg(a.sys + mm);
@@ -1650,7 +1672,16 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
         // bulk reduction of LW words (TMA engine, integer adds at L2: order independent)
         static_assert(LW % 8 == 0, "window length must be whole 32-B sectors");
         for (int g0 = 0; g0 < 4; g0 += NGR) {
-            int32_t* stg = g0 == 0 ? stg0 : win + (g0 - NGR) * LW * 32 - NGR * 128;
+            // round 0: the staging area; round 1: the rows of round 0's images (starting NGR *
+            // 512 B early, inside the record area); later rounds (NGR == 1) wait for the engine
+            // and reuse the staging area
+            int32_t* stg = g0 == 0 ? stg0 : win - NGR * 128;
+            if (g0 >= 2 * NGR) {
+                if (pending) bulk_wait_read_all();
+                pending = false;
+                __syncthreads();
+                stg = stg0;
+            }
             // thread -> (image gl, lane l, 4 slots): 4 conflict-free LDS (bank l), one STS.128
             // (row stride LW + 4 words: 8 lanes of a phase hit 8 distinct 16-B bank groups)
             for (int qq = threadIdx.x; qq < NGR * 32 * (LW / 4); qq += NT) {
@@ -1665,12 +1696,12 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
             __syncthreads();
             if (threadIdx.x < NGR * 32) {
                 const int gl = threadIdx.x >> 5, l = threadIdx.x & 31;
-                const int b = sg.x * 32 + l;
+                const int b = grp * 32 + l;
                 const int tr = b < a.M ? __ldg(a.trace_of + 4 * b + g0 + gl) : -1;
                 if (tr >= 0) {
                     const int lol = fp_sym_window_lo(a.pxs, a.pys, n, i0, j0, j1, __ldg(a.sxs + b),
                                                      __ldg(a.sys + b), a.qclamp, T);
-                    bulk_reduce_add_u32(a.acc + (size_t)tr * a.acc_ld + kAccFront + lol,
+                    bulk_reduce_add_u32(acc + (size_t)tr * a.acc_ld + kAccFront + lol,
                                         smem_u32(stg + (gl * 32 + l) * LWS), LW * 4);
                     bulk_commit();
                     pending = true;
@@ -1857,23 +1888,28 @@ template <typename T, int NF>
 __device__ __forceinline__ void finalize_objective(const FinArgs<T>& a, int chunks, double* data_s,
                                                    double* tv_s, double* red_d) {
 
-    if (a.tv_here) {  // NF == 1, one pass: data, TV, and the epilogue's deferred sum |x'| and
-                      // non-finite count (the residual CTAs' partials are aligned)
+    if (a.tv_here) {  // symmetric projector, one pass per frame: data, TV, and the epilogue's
+                      // deferred sum |x'| and non-finite count (the residual CTAs' partials are
+                      // aligned: frame g's are [g * ntv, (g + 1) * ntv))
         __shared__ double red4l[4 * kThreads / 32];
-        double v4[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int q = threadIdx.x; q < a.ntv; q += kThreads) {
-            v4[0] += a.part_r[q];
-            v4[1] += a.part_tv[q];
-            v4[2] += a.part_l1[2 * (size_t)q];
-            v4[3] += a.part_l1[2 * (size_t)q + 1];
-        }
-        block_sum4(v4, red4l);
-        if (threadIdx.x == 0) {
-            data_s[0] = v4[0];
-            tv_s[0] = v4[1];
-            if (!a.st->fr[0].stopped) {
-                a.st->fr[0].l1sum = v4[2];
-                a.st->fr[0].nonfinite = v4[3] > 0.0 ? 1 : 0;
+#pragma unroll 1
+        for (int g = 0; g < NF; ++g) {
+            double v4[4] = {0.0, 0.0, 0.0, 0.0};
+            const size_t o = (size_t)g * a.ntv;
+            for (int q = threadIdx.x; q < a.ntv; q += kThreads) {
+                v4[0] += a.part_r[o + q];
+                v4[1] += a.part_tv[o + q];
+                v4[2] += a.part_l1[2 * (o + q)];
+                v4[3] += a.part_l1[2 * (o + q) + 1];
+            }
+            block_sum4(v4, red4l);
+            if (threadIdx.x == 0) {
+                data_s[g] = v4[0];
+                tv_s[g] = v4[1];
+                if (!a.st->fr[g].stopped) {
+                    a.st->fr[g].l1sum = v4[2];
+                    a.st->fr[g].nonfinite = v4[3] > 0.0 ? 1 : 0;
+                }
             }
         }
     } else {
@@ -2063,19 +2099,23 @@ __global__ void __launch_bounds__(kThreads, PK_FIN_MINB) finalize_kernel(FinArgs
 // finalize_kernel does, the pair table and the sums.  Q <= kFinSymMax.
 constexpr int kFinSymG = 4;                       // int4 groups per thread
 constexpr int kFinSymMax = 4 * kThreads * kFinSymG;  // 4096 samples
+template <int NF>
 __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float> a) {
     __shared__ float tr[kFinSymMax + 8];           // tr[1 + s] = r[s], tr[0] = 0
     __shared__ __align__(16) float ys[kFinSymMax];  // measurements (LDGSTS: no registers held)
     __shared__ double red_d[kThreads / 32];
     __shared__ double red4[4 * kThreads / 32];
-    __shared__ double data_s[1], tv_s[1];
+    __shared__ double data_s[NF], tv_s[NF];
     __shared__ int last_flag;
     if (a.solver && a.st->all_stopped) return;
-    const int m = blockIdx.x, tid = threadIdx.x, Q = a.Q;
+    // grid (M, frames); frame-major layouts: y [f][M][Q], accumulator [f][M][acc_ld], pair
+    // table [f][M][TS], x [f][P]
+    const int m = blockIdx.x, f = blockIdx.y, tid = threadIdx.x, Q = a.Q;
+    const size_t fm = (size_t)f * a.M + m;
     const float* ym = a.solver ? reinterpret_cast<const float*>(a.io->y) : a.y;
-    if (ym) ym += (size_t)m * Q;
-    float* om = a.trace_out ? a.trace_out + (size_t)m * Q : nullptr;
-    int32_t* accr = a.acc32 + (size_t)m * a.acc32_ld + kAccFront;
+    if (ym) ym += fm * Q;
+    float* om = a.trace_out ? a.trace_out + fm * Q : nullptr;
+    int32_t* accr = a.acc32 + fm * a.acc32_ld + kAccFront;
     // measurements (constant): staged before the wait
     if (ym) {
         for (int k = tid; k < Q; k += kThreads) cp_async<4>(ys + k, ym + k);
@@ -2083,8 +2123,8 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
     }
     double tvp = 0.0, l1p = 0.0, badp = 0.0;
     if (a.tv_here) {  // exact anisotropic TV of x' (recon.py:169-170), sum |x'|, non-finite
-        const float* x = (a.st->iter & 1) ? a.xb0 : a.xb1;  // the back-projector wrote xb[(iter+1)&1]
         const int n = a.n, P = n * n, per = (P + gridDim.x - 1) / gridDim.x;
+        const float* x = ((a.st->iter & 1) ? a.xb0 : a.xb1) + (size_t)f * P;  // bp wrote xb[(iter+1)&1]
         const int p1 = min(P, (int)(blockIdx.x + 1) * per);
         for (int p = blockIdx.x * per + tid; p < p1; p += kThreads) {
             const float v = x[p];
@@ -2103,7 +2143,7 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
         const int s0 = 4 * (tid + i * kThreads);
         v4[i] = s0 < Q ? __ldcg(reinterpret_cast<const int4*>(accr + s0)) : make_int4(0, 0, 0, 0);
     }
-    const double sc = (double)a.st->fr[0].scale32;
+    const double sc = (double)a.st->fr[f].scale32;
     const double wq = sc > 0.0 ? a.w / sc : 0.0;
     double ss = 0.0;
     if (tid == 0) tr[0] = 0.f;
@@ -2145,7 +2185,7 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
         for (int q = tid; q < a.acc32_ld / 4; q += kThreads) row4[q] = make_int4(0, 0, 0, 0);
     }
     // pair table entries e in [0, TS): {r[e-1], r[e] - r[e-1]}, zero padded beyond Q
-    float2* tab = a.table + (size_t)m * a.TS;
+    float2* tab = a.table + fm * a.TS;
     for (int e0 = 2 * tid; e0 < a.TS; e0 += 2 * kThreads) {
         float2 p2[2];
 #pragma unroll
@@ -2163,17 +2203,17 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
         double w4[4] = {ss, tvp, l1p, badp};
         block_sum4(w4, red4);
         if (tid == 0) {
-            a.part_r[blockIdx.x] = w4[0];
-            a.part_tv[blockIdx.x] = w4[1];
-            a.part_l1[2 * (size_t)blockIdx.x] = w4[2];
-            a.part_l1[2 * (size_t)blockIdx.x + 1] = w4[3];
+            a.part_r[fm] = w4[0];
+            a.part_tv[fm] = w4[1];
+            a.part_l1[2 * fm] = w4[2];
+            a.part_l1[2 * fm + 1] = w4[3];
         }
     } else {
         ss = block_sum(ss, red_d);
-        if (tid == 0) a.part_r[blockIdx.x] = ss;
+        if (tid == 0) a.part_r[fm] = ss;
     }
-    if (!last_block(&a.st->cnt_fin, gridDim.x, &last_flag)) return;
-    finalize_objective<float, 1>(a, 1, data_s, tv_s, red_d);
+    if (!last_block(&a.st->cnt_fin, gridDim.x * gridDim.y, &last_flag)) return;
+    finalize_objective<float, NF>(a, 1, data_s, tv_s, red_d);
 }
 
 // ===========================================================================
@@ -2184,7 +2224,7 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
 template <typename T, int NF>
 __global__ void __launch_bounds__(kThreads) table_kernel(
     const T* y_direct, const DevIo* io, typename std::conditional<sizeof(T) == 4, float2, double2>::type* table,
-    int M, int Q, int TS, T sign, double* part, DevState* st, int init, int atrick) {
+    int M, int Q, int TS, T sign, double* part, DevState* st, int init, int atrick, int outer = 0) {
     __shared__ double red_d[kThreads / 32];
     __shared__ int last_flag;
     const T* y = y_direct ? y_direct : reinterpret_cast<const T*>(io->y);
@@ -2194,7 +2234,8 @@ __global__ void __launch_bounds__(kThreads) table_kernel(
     for (int e = threadIdx.x; e < TS; e += kThreads) {
         const T rp = (e >= 1 && e - 1 < Q) ? sign * ym[e - 1] : (T)0;
         const T rc = (e < Q) ? sign * ym[e] : (T)0;
-        table[((size_t)m * TS + e) * NF + f] = pair_entry<T>(rp, rc, e, atrick);
+        // interleaved [M][TS][NF] (generic kernels) or frame-major [NF][M][TS] (symmetric)
+        table[outer ? ((size_t)f * M + m) * TS + e : ((size_t)m * TS + e) * NF + f] = pair_entry<T>(rp, rc, e, atrick);
         if (e < Q) ss += (double)rc * (double)rc;
     }
     if (!init) return;

@@ -198,3 +198,59 @@ def test_fused_update_matches_epilogue_kernel(monkeypatch, oracle, spin):
     assert np.array_equal(out["0"].image.values, out["1"].image.values)
     assert np.array_equal(out["0"].objective_history, out["1"].objective_history)
     assert out["1"].iterations_run == 6
+
+
+@pytest.mark.parametrize("batch", [2, 4])
+def test_batched_symmetric_frames_match_oracle(oracle, batch):
+    """Batched plans keep both symmetric kernels (frame-major chunks and segments, one residual
+    CTA per (trace, frame)): every frame of a 256^2 batch (BASELINE config 2/4 geometry) within
+    1e-4 of its fp64 oracle solve, and equal to the single-frame plan to fp32 rounding."""
+    n, M, Q, N = 256, 256, 2048, 4
+    grid, ring, ac, _ = pk.make_scene(n, M, Q, 0)
+    K = pk.build_time_matrix(grid, ring, ac)
+    op = pk.operator_for(grid, ring, ac, F32, frames=batch)
+    assert op.info.symmetric == 3 and op.info.frames == batch
+    ys, refs = [], []
+    o = oracle.Operator.of(oracle.make_scene(n, M, Q, 0))
+    alpha, beta, step = 2.0817e-8, 2.0817e-10, 2651.30  # survey-pinned config 2
+    for f in range(batch):
+        s = oracle.make_scene(n, M, Q, 0)
+        ph = pk.make_vessel_phantom(grid, 10 + f).values * (1.0 + f)
+        y = o.forward(ph)
+        ys.append(pk.SensorData("time", M, Q, y))
+        refs.append(oracle.reconstruct(o, y, alpha, beta, step, N)["image"])
+    cfg = pk.ReconConfig(alpha, beta, N, step)
+    many = pk.reconstruct_frames(K, ys, cfg, pool=F32, batch=batch, pinned=(alpha, beta, step))
+    singles = [pk.iterative_reconstruct(K, y, cfg, pool=F32) for y in ys]
+    for r, s1, ref in zip(many, singles, refs):
+        assert r.iterations_run == N
+        assert rel(r.image.values, ref) <= 1e-4
+        assert rel(r.image.values, s1.image.values) <= 1e-5
+    # standalone batched products: each frame's projection and adjoint match the oracle
+    rng = np.random.default_rng(5)
+    xs = rng.random((batch, n * n))
+    yb = op.matvec(xs.ravel()).double().cpu().numpy().reshape(batch, -1)
+    rb = rng.standard_normal((batch, M * Q))
+    gb = op.adjoint(rb.ravel()).double().cpu().numpy().reshape(batch, -1)
+    for f in range(batch):
+        assert rel(yb[f], o.forward(xs[f])) <= 5e-5
+        assert rel(gb[f], o.adjoint(rb[f])) <= 2e-4
+    pk.clear_plan_cache()
+
+
+@pytest.mark.parametrize("lw,t", [("184", "32"), ("256", "32"), ("256", "64"), ("320", "64")])
+def test_projector_window_variants_match_oracle(monkeypatch, oracle, lw, t):
+    """Every staging-round schedule of the projector's bulk reductions (4 images at once,
+    2 + 2 with the second round aliasing the transposed rows, 1 + 1 + waits) and both strip
+    widths give the same projection (fp32 rounding of the oracle) and reconstruction."""
+    n, M, Q = 256, 256, 2048
+    monkeypatch.setenv("PK_FSYM_LW", lw)
+    monkeypatch.setenv("PK_FSYM_T", t)
+    g, ring, ac, ph = pk.make_scene(n, M, Q, seed=6)
+    o = oracle.Operator.of(oracle.make_scene(n, M, Q, 6))
+    op = _plan(monkeypatch, g, ring, ac, "1", "1")
+    assert op.info.symmetric == 3 and op.info.fp_window == int(lw) and op.info.fp_tile == int(t)
+    rng = np.random.default_rng(11)
+    x = ph.values + 0.05 * rng.random(g.size)
+    assert rel(op.matvec(x).double().cpu().numpy(), o.forward(x)) <= 5e-5
+    pk.clear_plan_cache()
