@@ -938,6 +938,9 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             p->fsym_groups = (p->M + 31) / 32;
             p->fsym = 0;
             const int nw = (getenv("PK_FSYM_NW") && atoi(getenv("PK_FSYM_NW")) == 16) ? 16 : 32;
+            // (one 16-warp CTA per SM measured no faster: cfg3 62.9 vs 61.7 us, cfg2 x 4 frames
+            // 48.2 vs 48.6 us)
+            const int persm = 32 / nw, cap = fs_cap(nw);
             // throughput mode (several plans on concurrent streams): the persistent grid is
             // divided by concurrency / 2 so that other streams' kernels share the SMs (measured
             // share 1 / 2 / 4: cfg4 on 8 streams 1963 / 2182 / 2293 frames/s, cfg3 on 4 streams
@@ -945,7 +948,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             int share = std::max(1, d->concurrency / 2);
             if (d->concurrency > 1)
                 if (const char* e = getenv("PK_FSYM_SHARE")) share = std::max(1, atoi(e));
-            const int per_sm = 32 / nw, G = std::max(1, std::max(1, sms) * per_sm / share);
+            const int G = std::max(1, std::max(1, sms) * persm / share);
             const int hq = n / 2;
             auto region_diag = [&](int T, int H) {
                 const double ex = std::min(T - 1, hq - 1) * hx, ey = std::min(H - 1, hq - 1) * hy;
@@ -975,36 +978,46 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 if (c0) c0->push_back(cnt);
                 return std::make_pair(cnt, *std::max_element(per_group.begin(), per_group.end()));
             };
+            // candidates (T, LW): the segment height hs whose rectangle fits the window; the
+            // fewest window words per projection wins, among windows that stage >= 2 images
+            // per round when any does (one image per round waits for the engine between rounds:
+            // cfg2 batched 4 frames T 32 / LW 256 48.9 us, T 64 / LW 320 55.2 us)
             const char* evt = getenv("PK_FSYM_T");
-            long long best = -1;
+            const char* evl = getenv("PK_FSYM_LW");
+            struct Cand { int T, lw, hs, qt; long long words; int ngr; };
+            std::vector<Cand> cands;
             for (int T : {64, 32}) {
                 if (evt && atoi(evt) != T) continue;
                 const int qt = (hq + T - 1) / T;
                 const long long R = (long long)nf * p->fsym_groups * qt * hq;
                 const int rows_per = (int)((R + G - 1) / G);
-                const char* evl = getenv("PK_FSYM_LW");
                 for (int lw : {96, 128, 184, 256, 320}) {
                     if (T == 32 && lw > 256) continue;
                     if (evl && atoi(evl) != lw) continue;
-                    if (fs_ngr(lw, nw) == 0) continue;  // windows + one staged image must fit
-                    const int sm = fs_smem(lw, nw);
+                    if (fs_ngr(lw, nw, cap) == 0) continue;  // windows + one staged image must fit
                     // window span: the rectangle's delay spread + the slot margins + 3 for the
                     // 16-B alignment of the window start (fp_sym_window_lo)
                     int hs = 0;
                     while (hs < hq && (int)std::ceil(region_diag(T, hs + 1)) + 9 <= lw) ++hs;
                     hs = std::min(hs, rows_per);
                     if (hs == 0) continue;
-                    const long long words = (long long)segment(T, hs, nullptr, nullptr).first * lw;
-                    if (best < 0 || words < best) {
-                        best = words;
-                        p->fsym = 1;
-                        p->fsym_T = T;
-                        p->fsym_qt = qt;
-                        p->fsym_L = lw;
-                        p->fsym_hs = hs;
-                        p->fsym_smem = sm;
-                    }
+                    cands.push_back({T, lw, hs, qt, (long long)segment(T, hs, nullptr, nullptr).first * lw,
+                                     fs_ngr(lw, nw, cap)});
                 }
+            }
+            const bool multi = std::any_of(cands.begin(), cands.end(), [](const Cand& c) { return c.ngr >= 2; });
+            long long best = -1;
+            for (const Cand& c : cands) {
+                if (multi && c.ngr < 2) continue;
+                if (best >= 0 && c.words >= best) continue;
+                best = c.words;
+                p->fsym = 1;
+                p->fsym_T = c.T;
+                p->fsym_qt = c.qt;
+                p->fsym_L = c.lw;
+                p->fsym_hs = c.hs;
+                p->fsym_smem = fs_smem(c.lw, nw, cap);
+                p->fsym_ngr = c.ngr;
             }
             if (p->fsym) {
                 p->fsym_nw = nw;

@@ -363,6 +363,7 @@ struct pk_plan {
     // rotation-symmetric projector (fp_sym_f32_kernel)
     int fsym = 0, fsym_T = 0, fsym_qt = 0, fsym_L = 0, fsym_smem = 0, fsym_groups = 0;
     int fsym_nw = 0;      // warps per CTA (16: two CTAs per SM, 32: one)
+    int fsym_ngr = 4;     // images per staging round of the bulk reductions
     int fsym_grid = 0;    // persistent CTAs (every one resident)
     int fsym_nseg = 0;    // segments (window sets) per projection
     int fsym_hs = 0;      // rows per segment at most

@@ -1357,14 +1357,18 @@ struct FpSymArgs {
 constexpr int kAccFront = 4;  // words before sample 0 in an accumulator row (windows may start at -4)
 // shared memory of the projector: windows [4][LW][32], the transposed staging of ngr images
 // [ngr][32][LW + 4] for the bulk reductions, and the per-warp records
-__host__ __device__ constexpr int fs_smem_cap(int nw) { return (nw == 32 ? 226 : 112) * 1024; }
+// (cap: the dynamic shared memory one CTA may take -- 226 KB at one 32-warp CTA per SM, 112 KB
+// at two 16-warp CTAs)
+__host__ __device__ constexpr int fs_cap(int nw) { return (nw == 32 ? 226 : 112) * 1024; }
 __host__ __device__ constexpr int fs_base_smem(int lw, int nw) { return 4 * lw * 32 * 4 + nw * (32 + kFsBatch) * 16; }
-__host__ __device__ constexpr int fs_ngr(int lw, int nw) {
-    return fs_base_smem(lw, nw) + 4 * 32 * (lw + 4) * 4 <= fs_smem_cap(nw) ? 4
-         : fs_base_smem(lw, nw) + 2 * 32 * (lw + 4) * 4 <= fs_smem_cap(nw) ? 2
-         : fs_base_smem(lw, nw) + 32 * (lw + 4) * 4 <= fs_smem_cap(nw) ? 1 : 0;
+__host__ __device__ constexpr int fs_ngr(int lw, int nw, int cap) {
+    return fs_base_smem(lw, nw) + 4 * 32 * (lw + 4) * 4 <= cap ? 4
+         : fs_base_smem(lw, nw) + 2 * 32 * (lw + 4) * 4 <= cap ? 2
+         : fs_base_smem(lw, nw) + 32 * (lw + 4) * 4 <= cap ? 1 : 0;
 }
-__host__ __device__ constexpr int fs_smem(int lw, int nw) { return fs_base_smem(lw, nw) + fs_ngr(lw, nw) * 32 * (lw + 4) * 4; }
+__host__ __device__ constexpr int fs_smem(int lw, int nw, int cap) {
+    return fs_base_smem(lw, nw) + fs_ngr(lw, nw, cap) * 32 * (lw + 4) * 4;
+}
 
 // first trace index of the window of the quadrant rectangle [i0, i0 + T) x [j0, j1) for
 // sensor (sx, sy): floor of the distance to the nearest point of the rectangle, minus 2,
@@ -1457,17 +1461,15 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
     if (k0 >= k1) return;
     const float* xall = a.x ? a.x : ((iter & 1) ? a.xb0 : a.xb1);  // bp wrote xb[(iter+1)&1]
     const int n = a.n, h = n >> 1;
-    // frame of the current segment: its x', packed x' and accumulator
-    const float* x = xall;
-    const float4* xr = a.x ? nullptr : a.xr;
-    int32_t* acc = a.acc;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // shared memory: records [NW][32 + kFsBatch] float4 | windows [4][LW][32] | staging
     // [NGR][32][LW + 4] (round 0; a later round stages into the window rows the previous
     // rounds have transposed, starting NGR * 512 B early inside the record area, so no round
     // waits for the engine to finish reading an earlier one)
     constexpr int WW = 4 * LW * 32;  // window words
-    constexpr int NGR = fs_ngr(LW, NW) > 0 ? fs_ngr(LW, NW) : 1, LWS = LW + 4;
+    // images per staging round (plans never launch an instantiation whose windows do not fit:
+    // fs_ngr == 0), staging row stride
+    constexpr int NGR = fs_ngr(LW, NW, fs_cap(NW)) > 0 ? fs_ngr(LW, NW, fs_cap(NW)) : 1, LWS = LW + 4;
     constexpr int REC = NW * (32 + kFsBatch) * 16;
     static_assert(REC >= NGR * 512, "record area must cover the staging overhang");
     float4* rec = reinterpret_cast<float4*>(smem) + (size_t)warp * (32 + kFsBatch);
@@ -1480,7 +1482,8 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
 
     // the 4 image values of piece q of segment (i0, j0): row j0 + q / P2, columns
     // i0 + 32 * (q % P2) + lane
-    auto piece_x = [&](int i0, int j0, int j1, int q, float (&v)[4]) {
+    // (x, xr: the segment frame's x' and rotation-packed x', passed by value)
+    auto piece_x = [&](const float* x, const float4* xr, int i0, int j0, int j1, int q, float (&v)[4]) {
         const int jj = j0 + q / P2;
         const int ii = i0 + 32 * (q % P2) + lane;
 #pragma unroll
@@ -1551,12 +1554,6 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
             __syncthreads();
         }
     };
-    auto set_frame = [&](int fr) {
-        cur_fr = fr;
-        x = xall + (size_t)fr * n * n;
-        xr = a.x ? nullptr : a.xr + (size_t)fr * h * h;
-        acc = a.acc + (size_t)fr * a.M * a.acc_ld;
-    };
     {   // first segment: windows initialised before the wait for the epilogue (constant data)
         uint4 c[NQ];
         load_counts(k0, c);
@@ -1568,9 +1565,12 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
         const int4 sg = __ldg(a.segs + k);
         const int fr = sg.x / a.groups, grp = sg.x - fr * a.groups;
         if (fr != cur_fr) {  // (ends with a barrier: the windows are initialised)
-            set_frame(fr);
+            cur_fr = fr;
             reduce_scale(fr, k);
         }
+        const float* x = xall + (size_t)fr * n * n;
+        const float4* xr = a.x ? nullptr : a.xr + (size_t)fr * h * h;
+        int32_t* acc = a.acc + (size_t)fr * a.M * a.acc_ld;
         const int i0 = h + T * sg.y, j0 = sg.z, j1 = sg.w;
         const int m = grp * 32 + lane;
         const bool sensor_ok = m < a.M;
@@ -1591,7 +1591,7 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
             return __shfl_sync(0xffffffffu, v, 0);
         };
         float xn[4];
-        piece_x(i0, j0, j1, q, xn);
+        piece_x(x, xr, i0, j0, j1, q, xn);
         while (q < npc) {
             const int jj = j0 + q / P2;
             const int c0 = i0 + 32 * (q % P2);
@@ -1600,7 +1600,7 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
 #pragma unroll
             for (int g = 0; g < 4; ++g) xv[g] = xn[g];
             const int qn = claim();
-            piece_x(i0, j0, j1, qn, xn);
+            piece_x(x, xr, i0, j0, j1, qn, xn);
             // dense records: lane k writes {xs0, xs1, xs2, xs3} of column c0 + k; the scatter
             // derives px from k and xq = rint(xs) from xs, so a record is one LDS.128 (the
             // record loads share the shared-memory pipe with the atomics)

@@ -13,6 +13,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2404_10928_b200 as pk  # noqa: E402
@@ -24,20 +25,22 @@ ap.add_argument("--config", default="cfg3")
 ap.add_argument("--iterations", type=int, default=2)
 ap.add_argument("--dtype", default="float32")
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--frames", type=int, default=1, help="batched plan (1, 2, 4 frames per launch)")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 grid, ring, ac, ph = pk.make_scene(cfg.n, cfg.sensors, cfg.samples, seed=0)
-op = pk.operator_for(grid, ring, ac, pk.CudaPool(0, a.dtype))
-y = op.matvec(ph.values)
-params = N.SolverParams(alpha=8.8e-8, beta=8.8e-10, step=333.0, tv_epsilon=1e-3, tolerance=0.0,
+op = pk.operator_for(grid, ring, ac, pk.CudaPool(0, a.dtype), frames=a.frames)
+y = op.matvec(np.tile(ph.values, a.frames))
+params1 = N.SolverParams(alpha=8.8e-8, beta=8.8e-10, step=333.0, tv_epsilon=1e-3, tolerance=0.0,
                         iterations=a.iterations, nonneg=0)
+params = (N.SolverParams * a.frames)(*([params1] * a.frames))
 lib = N.load()
 ms = (ctypes.c_float * 3)()
 n = ctypes.c_int32()
 s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 best = [1e30] * 3
 for _ in range(a.reps):
-    N.check(lib.pk_profile_iterations(op.handle, ctypes.byref(params), y.data_ptr(), ms, ctypes.byref(n), s))
+    N.check(lib.pk_profile_iterations(op.handle, params, y.data_ptr(), ms, ctypes.byref(n), s))
     best = [min(b, v) for b, v in zip(best, ms)]
 torch.cuda.synchronize()
 us = [1e3 * v / a.iterations for v in best]
