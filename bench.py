@@ -62,10 +62,11 @@ def parse():
     ap.add_argument("--sensor-frames", type=int, default=5,
                     help="frames timed through the sensor-sharded solver (N > 1, frames mode)")
     ap.add_argument("--frames", type=int, default=40, help="distinct frames cycled (> L2)")
-    ap.add_argument("--streams", type=int, default=4,
-                    help="independent plans on concurrent CUDA streams (frames in flight)")
-    ap.add_argument("--batch", type=int, default=1, choices=[1, 2, 4],
-                    help="frames reconstructed per launch sharing one delay evaluation")
+    ap.add_argument("--streams", type=int, default=None,
+                    help="independent plans on concurrent CUDA streams (default 8 for the cfg4 "
+                         "sequence, else 4)")
+    ap.add_argument("--batch", type=int, default=None, choices=[1, 2, 4],
+                    help="frames reconstructed per launch (default 4 for the cfg4 sequence, else 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ncu", action="store_true",
@@ -76,6 +77,12 @@ def parse():
         a.shard = "frames" if a.config == "cfg4" else "sensors"
     if a.exchange is None:
         a.exchange = "nccl"  # north_star: an NCCL all-reduce of the gradient; --exchange peer
+    # the cfg4 sequence: 4 frames per launch on the symmetric kernels, 8 plans in flight
+    # (tools/r2_cfg4_sweep.sh); single frames otherwise
+    if a.batch is None:
+        a.batch = 4 if a.config == "cfg4" else 1
+    if a.streams is None:
+        a.streams = 8 if a.config == "cfg4" else 4
     return a
 
 
