@@ -566,20 +566,23 @@ def main():
                 "frac": achieved / peak.value, "traffic": traffic,
                 "kernel": names[dom],
                 "plan": "kernels timed alone, un-graphed, on a latency-mode plan (full persistent "
-                        "back-projector grid); the timed region runs throughput-mode plans "
-                        "(half that grid) on concurrent streams",
+                        "grids); the timed region runs throughput-mode plans on concurrent "
+                        "streams (back-projector grid halved, projector grid / (streams / 2))",
                 "peak_source": peak_src + "; MEASURED_PEAKS.json has no FP32 figure",
                 "peak_live": live.value,
                 "traffic_source": traffic_src,
                 "work": f"12 flops x {M} sensors x {P} pixels per launch",
                 "why_fp32": "north_star: FP32 pipe utilisation against B200 peaks; the matrix-free "
                             "operator has ~200 flop/B of compulsory traffic (SURVEY.md 8(d))",
-                "binding_resource": "shared-memory pipe: 2 int32 ATOMS per sensor-pixel pair in the "
-                                    "projector (floor 2 clk / 32 pairs), LDS.64 per pair in the "
-                                    "back-projector (2 wavefronts / 32 pairs)",
-                "smem_floor_us": 2.0 * M * P / 32.0 / (148 * 1.965e3),
+                "binding_resource": "shared-memory (L1 data) pipe: per sensor-pixel pair the "
+                                    "projector issues 2 int32 ATOMS plus a quarter of a broadcast "
+                                    "LDS.128 record (2 wavefronts per 4 images): 2.5 wavefronts / "
+                                    "32 pairs; the back-projector one LDS.64 (2 wavefronts / 32 "
+                                    "pairs) -- tools/microbench/mio.cu",
+                "smem_floor_us": (2.5 if "K2" in names[dom] else 2.0) * M * P / 32.0 / (148 * 1.965e3),
                 # the same kernel against its binding resource: the floor above over its time
-                "smem_pipe_frac": (2.0 * M * P / 32.0 / (148 * 1.965e3)) / (per_launch_ms[dom] * 1e3),
+                "smem_pipe_frac": ((2.5 if "K2" in names[dom] else 2.0) * M * P / 32.0 / (148 * 1.965e3))
+                                  / (per_launch_ms[dom] * 1e3),
                 "hbm": {"achieved_GBs": (traffic / t_dom / 1e9) if traffic else None,
                         "peak_GBs": hbm_peak, "peak_source": hbm_src,
                         "frac": (traffic / t_dom / 1e9 / hbm_peak) if traffic else None}}
@@ -609,7 +612,8 @@ def main():
             N.check(lib.pk_reconstruct_host_async(
                 ops[q].handle, params_arr, yh_np[f].ctypes.data_as(dp), xo[q].ctypes.data_as(dp),
                 hh[q].ctypes.data_as(dp), stv.ctypes.data_as(ip), ctypes.c_void_p(streams[q].cuda_stream)))
-        for k in range(args.warmup):
+        # every plan's host-buffer path warmed (its pinned staging buffer is created on first use)
+        for k in range(max(args.warmup, SS)):
             host_step(k)
         torch.cuda.synchronize(dev)
         ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -9,7 +9,7 @@ import statistics
 import sys
 from collections import defaultdict
 
-SOLVER = ("fp_sym_f32", "bp_sym_f32", "bp_sym_epi", "finalize_kernel<float", "table_kernel<float",
+SOLVER = ("fp_sym_f32", "bp_sym_f32", "bp_sym_epi", "finalize_kernel<float", "finalize_sym_kernel", "table_kernel<float",
           "init_kernel<float", "copy_out_kernel<float", "fp_f32_kernel", "bp_f32_kernel")
 
 
