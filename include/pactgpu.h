@@ -232,6 +232,15 @@ int pk_delay_census_f32(pk_plan* plan, int32_t rule, int32_t ma, int32_t mb, int
 int pk_profile_iterations(pk_plan* plan, const pk_solver_params* params, const void* y_dev,
                           float* ms_out, int32_t* launches_out, void* stream);
 
+/* The same un-graphed replay with the symmetric back-projector's update kernel timed on its
+ * own (replaces the stage accounting of iterative_reconstruct, recon.py:303-347):
+ * ms_out[0..3] = summed device milliseconds of the back-projection (K^T r), the update
+ * (TV gradient + soft threshold + non-negativity, recon.py:330-338), the projection and the
+ * residual/objective kernel; plans without a separate update report it inside ms_out[0] and
+ * ms_out[1] = 0.  Synchronises the stream. */
+int pk_profile_stages(pk_plan* plan, const pk_solver_params* params, const void* y_dev,
+                      float* ms_out, int32_t* launches_out, void* stream);
+
 /* FP32 roofline denominator: FFMA throughput of `device` measured with a dependent-chain
  * microkernel (8 independent chains per thread, 148*4 CTAs), in TFLOP/s. */
 int pk_measure_fp32_peak(int32_t device, double* tflops_out);

@@ -146,6 +146,8 @@ SYMBOLS = [
     ("pk_freq_adjoint", ctypes.c_int, [_vp, ctypes.c_int32, _vp, _vp, ctypes.c_double, _vp]),
     ("pk_profile_iterations", ctypes.c_int,
      [_vp, ctypes.POINTER(SolverParams), _vp, ctypes.POINTER(ctypes.c_float), _ip, _vp]),
+    ("pk_profile_stages", ctypes.c_int,
+     [_vp, ctypes.POINTER(SolverParams), _vp, ctypes.POINTER(ctypes.c_float), _ip, _vp]),
     ("pk_measure_fp32_peak", ctypes.c_int, [ctypes.c_int32, _dp]),
     ("pk_dense_create", ctypes.c_int,
      [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_vp)]),

@@ -454,6 +454,7 @@ void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_
         }
         const dim3 eg(p->sym_ntiles * 32 * NF);
         if (A.fuse) return;
+        if (p->bp_mid_event) cudaEventRecord(p->bp_mid_event, s);
         if (epi && p->fsym) launch_pdl(bp_sym_epi_kernel<true, true>, eg, dim3(kThreads), 0, s, E);
         else if (epi) launch_pdl(bp_sym_epi_kernel<true, false>, eg, dim3(kThreads), 0, s, E);
         else launch_pdl(bp_sym_epi_kernel<false, false>, eg, dim3(kThreads), 0, s, E);
@@ -1671,6 +1672,60 @@ int pk_profile_iterations(pk_plan* p, const pk_solver_params* prm, const void* y
     for (auto& e : ev) cudaEventDestroy(e);
     if (launches) launches[0] = 2 + 3 * n;
     return PK_OK;
+}
+
+int pk_profile_stages(pk_plan* p, const pk_solver_params* prm, const void* y, float* ms,
+                      int32_t* launches, void* stream) {
+    if (!p || !y || !ms) return fail(PK_ERR_INVALID, "NULL argument");
+    if (!(p->dtype == PK_F32 && p->sym && !p->sym_fuse)) {  // no separate update kernel
+        float k3[3];
+        PK_TRY(pk_profile_iterations(p, prm, y, k3, launches, stream));
+        ms[0] = k3[0]; ms[1] = 0.f; ms[2] = k3[1]; ms[3] = k3[2];
+        return PK_OK;
+    }
+    PK_TRY(check_params(p, prm));
+    if (p->M != p->Mall) return fail(PK_ERR_INVALID, "profiling needs a plan over all sensors");
+    DeviceGuard g(p->device);
+    cudaStream_t s = S(stream);
+    const int n = prm[0].iterations;
+    PK_TRY(ensure_hist(p, n));
+    if (!p->status_dev) { PK_TRY(alloc(p, &p->status_dev, 2 * p->nf)); }
+    if (!p->xout_dev) {
+        PK_TRY(alloc(p, reinterpret_cast<unsigned char**>(&p->xout_dev), (size_t)p->P * tsize(p) * p->nf));
+    }
+    PK_TRY(upload_params(p, prm, s));
+    DevIo io{y, p->xout_dev, p->hist_dev, p->status_dev};
+    PK_CUDA(cudaMemcpyAsync(p->io, &io, sizeof(io), cudaMemcpyHostToDevice, s));
+    PK_TRY(launch_init(p, s));
+    PK_TRY(launch_table(p, nullptr, 1, s));
+    // per iteration: [back-projection | update | projection | residual/objective], the
+    // back-projection / update boundary recorded inside launch_bp (bp_mid_event)
+    std::vector<cudaEvent_t> ev(4 * n + 1);
+    for (auto& e : ev) PK_CUDA(cudaEventCreate(&e));
+    hold_kernel<<<1, 32, 0, s>>>(2000000LL + 400000LL * n);
+    int rc = PK_OK;
+    if (cudaEventRecord(ev[0], s) != cudaSuccess) rc = fail(PK_ERR_CUDA, "event record failed");
+    for (int it = 0; it < n && rc == PK_OK; ++it) {
+        p->bp_mid_event = ev[4 * it + 1];
+        rc = launch_bp(p, 1, nullptr, 2.0, s);
+        p->bp_mid_event = nullptr;
+        if (rc == PK_OK && cudaEventRecord(ev[4 * it + 2], s) != cudaSuccess) rc = PK_ERR_CUDA;
+        if (rc == PK_OK) rc = launch_fp(p, nullptr, 1, s);
+        if (rc == PK_OK && cudaEventRecord(ev[4 * it + 3], s) != cudaSuccess) rc = PK_ERR_CUDA;
+        if (rc == PK_OK) rc = launch_finalize(p, nullptr, nullptr, nullptr, 1, s);
+        if (rc == PK_OK && cudaEventRecord(ev[4 * it + 4], s) != cudaSuccess) rc = PK_ERR_CUDA;
+    }
+    if (cudaStreamSynchronize(s) != cudaSuccess && rc == PK_OK) rc = fail(PK_ERR_CUDA, "profile failed");
+    ms[0] = ms[1] = ms[2] = ms[3] = 0.f;
+    for (int it = 0; it < n && rc == PK_OK; ++it)
+        for (int k = 0; k < 4; ++k) {
+            float t = 0.f;
+            cudaEventElapsedTime(&t, ev[4 * it + k], ev[4 * it + k + 1]);
+            ms[k] += t;
+        }
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (launches) launches[0] = 2 + 4 * n;
+    return rc;
 }
 
 int pk_measure_fp32_peak(int32_t device, double* tflops) {

@@ -403,6 +403,7 @@ struct pk_plan {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
     cudaStream_t cap_stream = nullptr;
+    cudaEvent_t bp_mid_event = nullptr;  // pk_profile_stages: recorded between K1s and its epilogue
     int graph_iters = -1;
     pk::DevParams params_host{};  // last uploaded solver parameters
     int params_valid = 0;

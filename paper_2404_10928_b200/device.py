@@ -383,6 +383,19 @@ class DeviceOperator:
                                                     self.stream()))
         return [v * 1e-3 for v in ms], int(n.value)
 
+    def profile_stages(self, y, params):
+        """Device seconds of the solver's stages over one un-graphed replay
+        (pk_profile_stages): back-projection, update (TV gradient + prox), projection,
+        residual/objective."""
+        arr, _ = self._params(params)
+        yt = self._check_y(self.tensor(y))
+        ms = (ctypes.c_float * 4)()
+        n = ctypes.c_int32()
+        with _torch().cuda.device(self.device):
+            N.check(self._lib.pk_profile_stages(self._h, arr, yt.data_ptr(), ms, ctypes.byref(n),
+                                                self.stream()))
+        return [v * 1e-3 for v in ms]
+
     def reconstruct_host(self, y_host: np.ndarray, params):
         """The C-ABI host-buffer entry (pk_reconstruct_host): fp64 in, fp64 out, synchronous."""
         arr, n = self._params(params)

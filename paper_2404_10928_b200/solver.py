@@ -437,14 +437,37 @@ def _dense_loop(op, yv, alpha, beta, eta, config, shape):
     return x.double().cpu().numpy(), h, stopped_by
 
 
+_stage_split: dict = {}
+
+
+def _book_stages(times: dict, wall: float, op, yv, config, alpha, beta, eta) -> None:
+    """Apportion a graph solve's wall time over the reference's stage keys by the plan's
+    device-time split (see iterative_reconstruct)."""
+    key = (id(op), float(alpha), float(beta), float(eta), int(config.iterations))
+    split = _stage_split.get(key)
+    if split is None:
+        bp, upd, fp, fin = op.profile_stages(yv, solver_params(config, alpha, beta, eta))
+        tot = max(bp + upd + fp + fin, 1e-30)
+        split = ((bp + fp) / tot, upd / tot, fin / tot)
+        _stage_split[key] = split
+    prod, upd, obj = split
+    times["gradient_products"] += wall * prod
+    times["tv_gradient" if beta > 0 else "prox"] += wall * upd
+    times["objective"] += wall * obj
+
+
 def iterative_reconstruct(K, y, config: ReconConfig, grid=None, pool=None,
                           stage_seconds: dict | None = None) -> ReconResult:
     """Proximal-gradient minimisation of ||Kx-y||^2 + alpha||x||_1 + beta TV(x)
     (recon.py:286-377), x0 = 0, on the device.
 
-    stage_seconds, if given, accumulates wall time under the reference's keys; the fused
-    device loop has no separate TV/prox/objective stages, so the whole solve is recorded
-    under "gradient_products" and the others stay 0.
+    stage_seconds, if given, accumulates wall time under the reference's keys
+    (recon.py:303-347).  The solve is one captured graph, so its wall time is apportioned by
+    the plan's per-kernel device times (pk_profile_stages, one un-graphed replay per plan and
+    parameter set, cached): "gradient_products" <- back-projection + projection, "tv_gradient"
+    <- the update kernel (TV gradient fused with the soft threshold and non-negativity; with
+    beta = 0 it is booked under "prox"), "objective" <- the residual/objective kernel.  Other
+    operators (explicit, frequency-domain) book the whole solve under "gradient_products".
     """
     g = _grid_of(K, grid)
     _check_pair(K, y)
@@ -474,7 +497,11 @@ def iterative_reconstruct(K, y, config: ReconConfig, grid=None, pool=None,
     else:  # frequency-domain operator: speculative device loop, one graph replay
         xv, h, stopped_by = _speculative_loop(op, y.values, alpha, beta, eta, config, (g.ny, g.nx))
         n = h.shape[0]
-    times["gradient_products"] += time.perf_counter() - t0
+    wall = time.perf_counter() - t0
+    if stage_seconds is not None and isinstance(op, DeviceOperator):
+        _book_stages(times, wall, op, y.values, config, alpha, beta, eta)
+    else:
+        times["gradient_products"] += wall
     return ReconResult(
         image=ImageField(g, xv),
         objective_history=h[:, 0].copy(),

@@ -69,3 +69,28 @@ def test_bench_recon_verified_against_oracle(oracle):
     assert rep.entry("iterative_device_f64").verification is True
     assert rep.metrics["rel_l2_f64_vs_reference"] <= 1e-10
     assert rep.metrics["rel_l2_f32_vs_reference"] <= 1e-4
+
+
+@pytest.mark.gpu
+def test_stage_seconds_split():
+    """iterative_reconstruct(stage_seconds=...) books the graph solve under the reference's
+    four stage keys (recon.py:303-347) by the plan's per-kernel device times."""
+    import time
+
+    g, ring, ac, ph = pk.make_scene(128, 128, 1024, seed=0)
+    K = pk.build_time_matrix(g, ring, ac)
+    F32 = pk.CudaPool(0, "float32")
+    y = pk.forward_project(K, ph, pool=F32)
+    cfg = pk.resolve_config(pk.ReconConfig(iterations=10), K, y, pool=F32)
+    pk.iterative_reconstruct(K, y, cfg, pool=F32)  # graph captured
+    stages = {}
+    t0 = time.perf_counter()
+    pk.iterative_reconstruct(K, y, cfg, pool=F32, stage_seconds=stages)
+    wall = time.perf_counter() - t0
+    assert set(stages) == {"gradient_products", "tv_gradient", "prox", "objective"}
+    assert stages["gradient_products"] > stages["tv_gradient"] > 0.0
+    assert stages["objective"] > 0.0 and stages["prox"] == 0.0  # beta > 0: the update is TV + prox
+    assert sum(stages.values()) <= wall
+    # accumulates like the reference's dict
+    pk.iterative_reconstruct(K, y, cfg, pool=F32, stage_seconds=stages)
+    assert stages["gradient_products"] > 0.0
