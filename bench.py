@@ -180,7 +180,7 @@ def run_reference(args, cfg):
 
 def ncu_traffic(config: str, dom: int):
     """dram__bytes_read + dram__bytes_write per launch of the dominant kernel (K1 = the
-    back-projector with its update epilogue, K2 = the projector), captured by ncu (default
+    back-projector, K2 = the projector), captured by ncu (default
     cache control: every replay starts cold) on a 2-iteration un-graphed run of this build
     (tools/profile_kernels.py).  Returns (bytes, description) or (None, reason)."""
     import shutil
@@ -189,7 +189,7 @@ def ncu_traffic(config: str, dom: int):
     ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
     if not os.path.exists(ncu):
         return None, "ncu not available"
-    pat = "bp_sym_f32|bp_sym_epi|bp_f32_kernel" if dom == 0 else "fp_sym_f32|fp_f32_kernel"
+    pat = "bp_sym_f32|bp_f32_kernel" if dom == 0 else "fp_sym_f32|fp_f32_kernel"
     iters = 2
     with tempfile.TemporaryDirectory() as td:
         log = os.path.join(td, "t.csv")
@@ -513,16 +513,20 @@ def main():
     # ---- roofline of the dominant kernel (CUDA events around each launch) ----
     roof, kernels = None, None
     if not sensor_mode:
-        fl = (ctypes.c_float * 3)()
+        # per-stage device times (pk_profile_stages): back-projection, its update kernel
+        # (TV gradient + prox), projection, residual/objective
+        fl = (ctypes.c_float * 4)()
         nl = ctypes.c_int32()
         prof_iters = cfg.iterations
         reps = 5
-        tot = np.zeros(3)
+        tot = np.zeros(4)
         for r_ in range(reps):
-            N.check(lib.pk_profile_iterations(prof_op.handle, params_arr, Ystep[r_ % n_steps_in].data_ptr(),
-                                              fl, ctypes.byref(nl), stream_ptr()))
+            N.check(lib.pk_profile_stages(prof_op.handle, params_arr, Ystep[r_ % n_steps_in].data_ptr(),
+                                          fl, ctypes.byref(nl), stream_ptr()))
             tot += np.array(fl[:])
-        per_launch_ms = tot / (reps * prof_iters)
+        st_ms = tot / (reps * prof_iters)
+        # products first: [back-projection, projection, update, residual/objective]
+        per_launch_ms = np.array([st_ms[0], st_ms[2], st_ms[1], st_ms[3]])
         # the denominator: the FFMA peak measured once on this pool's B200s and committed
         # (profiles/fp32_peak.json, tools/fp32_peak.py); the live measurement is a cross-check
         live = ctypes.c_double()
@@ -539,7 +543,8 @@ def main():
             except Exception:
                 pass
         flops_per_launch = 12.0 * M * P * B  # 12 FP32 flops per sensor-pixel pair, per frame
-        names = ["K1 bp_update (back-projection + TV + prox)", "K2 projection (fixed-point scatter)",
+        names = ["K1 back-projection", "K2 projection (fixed-point scatter)",
+                 "K1u update (TV gradient + prox, separate kernel; 0 when fused into K1)",
                  "K3 residual/objective"]
         kernels = {}
         for i, nm in enumerate(names):

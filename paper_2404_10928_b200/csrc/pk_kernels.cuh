@@ -617,8 +617,11 @@ __device__ __forceinline__ void sym_epi_units(const BpSymEpiArgs& a, int t, int 
     sync();  // the scratch is reused by the next claim
 }
 
+#ifndef PK_SYM_MINB
+#define PK_SYM_MINB 3  // CTAs per SM the back-projector's registers are capped for (build knob)
+#endif
 template <int IW>
-__global__ void __launch_bounds__(kSymThreads, 3) bp_sym_f32_kernel(BpSymArgs a) {
+__global__ void __launch_bounds__(kSymThreads, PK_SYM_MINB) bp_sym_f32_kernel(BpSymArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     griddep_wait();  // the pair table and the stop flag come from the residual kernel
     if (a.st && a.st->all_stopped) return;
