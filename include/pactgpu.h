@@ -275,6 +275,14 @@ int pk_dense_create(int64_t rows, int64_t cols, int32_t dtype, int32_t complex_e
 int pk_dense_destroy(pk_dense* op);
 int pk_dense_get_info(const pk_dense* op, pk_dense_info* out);
 int pk_dense_set_entries(pk_dense* op, const double* entries, int32_t on_device, void* stream);
+/* Multi-frame products on the tensor cores (tcgen05 kind::tf32, 3xTF32 split: fp32
+ * accuracy, ~2e-6 relative), real fp32 matrices: y[f] = K x[f] (x [frames][cols], y
+ * [frames][rows]) and g[f] = K^T y[f] (g [frames][cols]; K^T is built in HBM on the first
+ * call), 1 <= frames <= 128, cols (and rows, for the adjoint) multiples of 4.  The
+ * reference's per-frame GEMV cores (kernels.py:195-225) applied to a frame batch. */
+int pk_dense_matmat(pk_dense* dense, int32_t frames, const void* x_dev, void* y_dev, void* stream);
+int pk_dense_rmatmat(pk_dense* dense, int32_t frames, const void* y_dev, void* g_dev, void* stream);
+
 /* Dense K of a geometry plan built on the device (build_time_matrix, forward.py:167-194):
  * fp64 entries bit-identical to the reference's (the plan's fp64 delays), PK_F32 rounded. */
 int pk_dense_from_plan(pk_dense* op, const pk_plan* plan, void* stream);

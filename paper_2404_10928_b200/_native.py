@@ -157,6 +157,8 @@ SYMBOLS = [
     ("pk_dense_from_plan", ctypes.c_int, [_vp, _vp, _vp]),
     ("pk_dense_matvec", ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, _vp]),
     ("pk_dense_adjoint", ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, ctypes.c_double, _vp]),
+    ("pk_dense_matmat", ctypes.c_int, [_vp, ctypes.c_int32, _vp, _vp, _vp]),
+    ("pk_dense_rmatmat", ctypes.c_int, [_vp, ctypes.c_int32, _vp, _vp, _vp]),
     ("pk_dense_reconstruct", ctypes.c_int,
      [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(SolverParams), _vp, _vp, _vp, _vp, _vp]),
     ("pk_last_error", ctypes.c_char_p, []),

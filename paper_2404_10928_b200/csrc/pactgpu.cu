@@ -23,6 +23,7 @@
 #include "pk_kernels.cuh"
 #include "pk_freq.cuh"
 #include "pk_dense.cuh"
+#include "pk_tc.cuh"
 
 using namespace pk;
 
@@ -1785,6 +1786,12 @@ struct pk_dense {
     cudaGraphExec_t exec = nullptr;
     int g_iters = -1, g_nx = -1, g_ny = -1;
     int64_t device_bytes = 0;
+    // multi-frame products on the tensor cores (pk_dense_matmat / pk_dense_rmatmat)
+    void* Kt = nullptr;            // cols x rows transpose of K (built on the first K^T Y)
+    float* bhi = nullptr;          // frames operand split hi / lo [frames][k]
+    float* blo = nullptr;
+    float* tcpart = nullptr;       // split-K partials
+    size_t b_cap = 0, part_cap = 0;
 };
 
 namespace {
@@ -2003,7 +2010,8 @@ int pk_dense_destroy(pk_dense* d) {
     if (!d) return PK_OK;
     DeviceGuard g(d->device);
     void* ptrs[] = {d->K, d->part, d->fpart, d->rpart, d->ipart, d->xb[0], d->xb[1], d->rb,
-                    d->ybuf, d->xout, d->hist, d->status, d->st, d->prm};
+                    d->ybuf, d->xout, d->hist, d->status, d->st, d->prm, d->Kt, d->bhi, d->blo,
+                    d->tcpart};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (d->exec) cudaGraphExecDestroy(d->exec);
@@ -2099,6 +2107,128 @@ int pk_dense_adjoint(pk_dense* d, const void* y, int32_t y_complex, void* out, d
     }
     PK_CHECK_LAUNCH();
     return PK_OK;
+}
+
+// ---- multi-frame products on the tensor cores (pk_tc.cuh) ----
+namespace {
+
+typedef CUresult (*TmapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                 CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                 CUtensorMapFloatOOBfill);
+
+TmapEncodeFn tmap_encode() {
+    static TmapEncodeFn fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<TmapEncodeFn>(f);
+    }
+    return fn;
+}
+
+// fp32 [rows][cols] row-major, 32-column x box_rows boxes, 128-B swizzle (pk_tc.cuh)
+int tc_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int box_rows) {
+    TmapEncodeFn enc = tmap_encode();
+    if (!enc) return fail(PK_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+    cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return fail(PK_ERR_INVALID, "tensor map rejected (%lld x %lld)", (long long)rows, (long long)cols);
+    return PK_OK;
+}
+
+cudaError_t tc_opt_in() {
+    static bool done = false;
+    if (done) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes(32));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tc_gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes(64));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tc_gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes(128));
+    done = e == cudaSuccess;
+    return e;
+}
+
+// C[f][r] = sum_k A[r][k] B[f][k] for f < frames (A fp32 [R][Kd] in HBM, B fp32 [frames][Kd])
+int tc_products(pk_dense* d, const float* A, int64_t R, int64_t Kd, int frames, const float* B, float* C,
+                cudaStream_t s) {
+    if (frames < 1 || frames > 128) return fail(PK_ERR_INVALID, "frames must be 1..128, got %d", frames);
+    if (Kd % 4 || R > INT_MAX || Kd > INT_MAX) return fail(PK_ERR_UNSUPPORTED, "matrix shape unsupported by the tensor-core path");
+    const int N = frames <= 32 ? 32 : (frames <= 64 ? 64 : 128);
+    const size_t nb = (size_t)frames * Kd;
+    if (d->b_cap < nb) {
+        if (d->bhi) cudaFree(d->bhi);
+        if (d->blo) cudaFree(d->blo);
+        d->bhi = d->blo = nullptr;
+        d->b_cap = 0;
+        PK_TRY(dalloc(d, &d->bhi, nb));
+        PK_TRY(dalloc(d, &d->blo, nb));
+        d->b_cap = nb;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
+    const int tiles = (int)((R + kTcBM - 1) / kTcBM);
+    const int nkb = (int)((Kd + kTcBK - 1) / kTcBK);
+    // split K until the grid covers the GPU twice (at least 64 K blocks per split)
+    int splits = 1;
+    while (tiles * splits < 2 * sms && nkb / (2 * splits) >= 64 && splits < 16) splits *= 2;
+    if (splits > 1 && d->part_cap < (size_t)splits * N * R) {
+        if (d->tcpart) cudaFree(d->tcpart);
+        d->tcpart = nullptr;
+        d->part_cap = 0;
+        PK_TRY(dalloc(d, &d->tcpart, (size_t)splits * N * R));
+        d->part_cap = (size_t)splits * N * R;
+    }
+    CUtensorMap ma, mbh, mbl;
+    PK_TRY(tc_map(&ma, A, R, Kd, kTcBM));
+    PK_TRY(tc_map(&mbh, d->bhi, frames, Kd, N));
+    PK_TRY(tc_map(&mbl, d->blo, frames, Kd, N));
+    PK_CUDA(tc_opt_in());
+    tc_split_kernel<<<2 * sms, 256, 0, s>>>(B, d->bhi, d->blo, nb);
+    float* out = splits > 1 ? d->tcpart : C;
+    const dim3 grid(tiles, splits);
+    // (rows of frames >= `frames` read as zeros: out-of-bounds box rows; only the first
+    //  `frames` frames of C / the partials are written)
+    switch (N) {
+        case 32: tc_gemm_kernel<32><<<grid, kTcThreads, tc_smem_bytes(32), s>>>(ma, mbh, mbl, out, (int)R, (int)Kd, splits, frames); break;
+        case 64: tc_gemm_kernel<64><<<grid, kTcThreads, tc_smem_bytes(64), s>>>(ma, mbh, mbl, out, (int)R, (int)Kd, splits, frames); break;
+        default: tc_gemm_kernel<128><<<grid, kTcThreads, tc_smem_bytes(128), s>>>(ma, mbh, mbl, out, (int)R, (int)Kd, splits, frames); break;
+    }
+    if (splits > 1) tc_split_sum_kernel<<<2 * sms, 256, 0, s>>>(d->tcpart, C, (size_t)frames * R, splits, (size_t)N * R);
+    PK_CHECK_LAUNCH();
+    return PK_OK;
+}
+
+}  // namespace
+
+int pk_dense_matmat(pk_dense* d, int32_t frames, const void* x, void* y, void* stream) {
+    if (!d || !x || !y) return fail(PK_ERR_INVALID, "NULL argument");
+    if (d->dtype != PK_F32 || d->cplx) return fail(PK_ERR_UNSUPPORTED, "tensor-core products need a real fp32 matrix");
+    DeviceGuard g(d->device);
+    return tc_products(d, static_cast<const float*>(d->K), d->rows, d->cols, frames, static_cast<const float*>(x),
+                       static_cast<float*>(y), S(stream));
+}
+
+int pk_dense_rmatmat(pk_dense* d, int32_t frames, const void* y, void* g_out, void* stream) {
+    if (!d || !y || !g_out) return fail(PK_ERR_INVALID, "NULL argument");
+    if (d->dtype != PK_F32 || d->cplx) return fail(PK_ERR_UNSUPPORTED, "tensor-core products need a real fp32 matrix");
+    DeviceGuard g(d->device);
+    cudaStream_t s = S(stream);
+    if (!d->Kt) {  // K^T, once: both tensor-core operands stay K-major
+        PK_TRY(dalloc(d, reinterpret_cast<float**>(&d->Kt), (size_t)d->rows * d->cols));
+        d->device_bytes += d->rows * d->cols * 4;
+        const dim3 blk(32, 8), grd((unsigned)((d->cols + 31) / 32), (unsigned)((d->rows + 31) / 32));
+        dense_transpose_kernel<<<grd, blk, 0, s>>>(static_cast<const float*>(d->K), static_cast<float*>(d->Kt),
+                                                    d->rows, d->cols);
+        PK_CHECK_LAUNCH();
+    }
+    return tc_products(d, static_cast<const float*>(d->Kt), d->cols, d->rows, frames, static_cast<const float*>(y),
+                       static_cast<float*>(g_out), s);
 }
 
 int pk_dense_reconstruct(pk_dense* d, int32_t nx, int32_t ny, const pk_solver_params* prm,

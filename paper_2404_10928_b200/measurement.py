@@ -359,6 +359,43 @@ class DenseOperator:
             raise ValueError(f"matrix has {n} {what} but vector has {t.numel()} values")
         return t, c
 
+    def _frames(self, a, n: int, what: str):
+        """[frames, n] real fp32 device matrix of a frame batch (tensor-core products)."""
+        import torch
+
+        if self.cplx or self.rdtype != torch.float32:
+            raise ValueError("frame-batched products need a real float32 matrix")
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+        if t.is_complex():
+            raise ValueError("frame-batched products take real frames")
+        t = t.to(device=self.device, dtype=torch.float32).reshape(-1, n).contiguous() if t.numel() % n == 0 else None
+        if t is None or not 1 <= t.shape[0] <= 128:
+            raise ValueError(f"expected 1..128 frames of {n} {what}")
+        return t
+
+    def matmat(self, xs):
+        """K x for a batch of frames, xs [frames, cols] -> [frames, rows] (pk_dense_matmat:
+        tcgen05 tensor cores, 3xTF32, fp32 accuracy)."""
+        import torch
+
+        xt = self._frames(xs, self.cols, "columns")
+        out = torch.empty((xt.shape[0], self.rows), device=self.device, dtype=torch.float32)
+        with torch.cuda.device(self.device):
+            self._N.check(self._lib.pk_dense_matmat(self._h, xt.shape[0], xt.data_ptr(), out.data_ptr(),
+                                                    self._stream()))
+        return out
+
+    def rmatmat(self, ys):
+        """K^T y for a batch of frames, ys [frames, rows] -> [frames, cols] (pk_dense_rmatmat)."""
+        import torch
+
+        yt = self._frames(ys, self.rows, "rows")
+        out = torch.empty((yt.shape[0], self.cols), device=self.device, dtype=torch.float32)
+        with torch.cuda.device(self.device):
+            self._N.check(self._lib.pk_dense_rmatmat(self._h, yt.shape[0], yt.data_ptr(), out.data_ptr(),
+                                                     self._stream()))
+        return out
+
     def matvec(self, x):
         import torch
 
