@@ -153,7 +153,7 @@ void free_plan(pk_plan* p) {
                     p->status_dev, p->part_bp, p->part_mx, p->part_l1, p->part_tv, p->part_r, p->part_misc, p->state,
                     p->params, p->io, p->xout_dev, p->bp_gpart, p->bp_tile_cnt, p->sym_sync, p->sym_tiles,
                     p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0, p->sym_tile_slot0,
-                    p->sym_part, p->fsym_acc, p->fsym_trace, p->fsym_counts, p->fsym_rec,
+                    p->sym_part, p->fsym_acc, p->fsym_trace, p->fsym_bias, p->fsym_rec,
                     p->fsym_segs, p->fsym_cta_seg0,
                     p->freq_part, p->gid, p->loc};
     for (void* q : ptrs)
@@ -303,7 +303,6 @@ void launch_fp_t(pk_plan* p, const void* x, int solver, cudaStream_t s) {
         a.qclamp = (float)p->Q + 1.5f;
         a.hx = p->fsym_hx;
         a.st = p->state; a.solver = solver;
-        a.counts = p->fsym_counts;
         a.xr = reinterpret_cast<const float4*>(p->fsym_xr);
         if (solver && p->sym) {  // the symmetric epilogue deferred its statistics
             a.part_mx = p->part_mx;
@@ -390,6 +389,7 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
         if (p->fsym) {
             a.acc32 = p->fsym_acc;
             a.acc32_ld = p->fsym_acc_ld;
+            a.bias16 = p->fsym_bias;
         }
         a.atrick = p->bp_atrick;
         a.chunks = chunks;
@@ -956,15 +956,64 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 const double ex = std::min(T - 1, hq - 1) * hx, ey = std::min(H - 1, hq - 1) * hy;
                 return std::sqrt(ex * ex + ey * ey);
             };
+            // cuts of the row sequence [0, R) into G contiguous CTA ranges that minimise the
+            // largest cost, cost = rows + cs * (segments - 1): a range that crosses a (group,
+            // strip) boundary (or the hs limit) starts a second segment, whose window set-up,
+            // staging and scatter ramp cost a CTA as much as ~cs rows (measured r02c, config 3:
+            // 1-segment CTAs 47.8 us, 2-segment 56.5 us for the same rows).  Greedy fill per
+            // budget, binary search on the budget.
+            auto balanced_cuts = [&](long long R, int hs, long long cs) {
+                auto fill = [&](long long B, std::vector<long long>* cut) {
+                    long long pos = 0;
+                    int used = 0;
+                    while (pos < R && used < G) {
+                        if (cut) cut->push_back(pos);
+                        ++used;
+                        long long budget = B;
+                        bool first = true;
+                        while (pos < R) {
+                            if (!first) {
+                                if (budget <= cs) break;
+                                budget -= cs;
+                            }
+                            const long long send = std::min({(pos / hq + 1) * hq, pos + hs, R});
+                            const long long take = std::min(send - pos, budget);
+                            pos += take;
+                            budget -= take;
+                            first = false;
+                            if (pos < send) break;  // budget spent inside the segment
+                        }
+                    }
+                    if (cut) { while ((int)cut->size() < G) cut->push_back(pos); cut->push_back(R); }
+                    return pos >= R;
+                };
+                long long lo = std::max(1LL, (R + G - 1) / G), hi = lo + 2 * cs + hs + 1;
+                while (!fill(hi, nullptr)) hi *= 2;
+                while (lo < hi) {
+                    const long long mid = (lo + hi) / 2;
+                    if (fill(mid, nullptr)) hi = mid; else lo = mid + 1;
+                }
+                std::vector<long long> cut;
+                fill(lo, &cut);
+                return cut;
+            };
+            const char* evc = getenv("PK_FSYM_SEGCOST");  // (sweeps: cost of a segment, in rows)
+            // a row of T columns scatters 10 shared-memory wavefronts per column (8 atomics, one
+            // broadcast LDS.128); an extra segment costs ~7.5 us of SM time
+            auto seg_cost = [&](int T) {
+                return evc ? (long long)std::max(0, atoi(evc))
+                           : (long long)std::lround(7.5 / (T * 10.0 / 1965.0 * 1.15));
+            };
             // (batched frames: the sequence is frame-major, segment group index f * groups + group)
             auto segment = [&](int T, int hs, std::vector<int4>* sg, std::vector<int>* c0) {
                 const int qt = (hq + T - 1) / T;
                 const long long R = (long long)nf * p->fsym_groups * qt * hq;
+                const std::vector<long long> cut = balanced_cuts(R, hs, seg_cost(T));
                 int cnt = 0;
                 std::vector<int> per_group(nf * p->fsym_groups, 0);
                 for (int c = 0; c < G; ++c) {
-                    long long r0 = R * c / G;
-                    const long long r1 = R * (c + 1) / G;
+                    long long r0 = cut[c];
+                    const long long r1 = cut[c + 1];
                     if (c0) c0->push_back(cnt);
                     while (r0 < r1) {
                         const long long gs = r0 / hq;
@@ -1001,7 +1050,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                     // 16-B alignment of the window start (fp_sym_window_lo)
                     int hs = 0;
                     while (hs < hq && (int)std::ceil(region_diag(T, hs + 1)) + 9 <= lw) ++hs;
-                    hs = std::min(hs, rows_per);
+                    hs = std::min<long long>(hs, rows_per + seg_cost(T));  // (balanced ranges exceed R / G)
                     if (hs == 0) continue;
                     cands.push_back({T, lw, hs, qt, (long long)segment(T, hs, nullptr, nullptr).first * lw,
                                      fs_ngr(lw, nw, cap)});
@@ -1121,7 +1170,6 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     A(alloc(p, &p->part_bp, (size_t)4 * nf * std::max(ntile_max, (p->P + kThreads - 1) / kThreads)));
     A(alloc(p, &p->part_mx, (size_t)std::max(1, p->sym ? 32 * p->sym_ntiles * nf : 1)));
     A(alloc(p, &p->part_l1, (size_t)(p->fsym ? 2 * 8 * p->M * nf : 1)));
-    const int fsym_units = p->fsym ? p->fsym_nseg : 0;
     // TV partials: per projector tile, or per residual CTA (M x up to 8 chunks) with the
     // symmetric projector
     A(alloc(p, &p->part_tv, (size_t)std::max(p->fp_tiles_x * p->fp_tiles_y, p->fsym ? 8 * p->M : 0) * nf));
@@ -1129,7 +1177,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         A(alloc(p, &p->fsym_acc, (size_t)nf * p->M * p->fsym_acc_ld));
         A(alloc(p, &p->fsym_rec, (size_t)nf));
         A(alloc(p, &p->fsym_trace, (size_t)p->fsym_groups * 32 * 4));
-        A(alloc(p, &p->fsym_counts, (size_t)fsym_units * 32 * p->fsym_L));
+        A(alloc(p, &p->fsym_bias, (size_t)p->M * p->fsym_acc_ld));
         A(alloc(p, &p->fsym_segs, p->fsym_segs_h.size()));
         A(alloc(p, &p->fsym_cta_seg0, p->fsym_cta_seg0_h.size()));
         A(alloc(p, &p->fsym_xr, (size_t)(p->nx / 2) * (p->nx / 2) * 4 * nf));
@@ -1181,35 +1229,44 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         const int nseg = p->fsym_nseg;
         up(p->fsym_segs, p->fsym_segs_h.data(), sizeof(int4) * nseg);
         up(p->fsym_cta_seg0, p->fsym_cta_seg0_h.data(), sizeof(int) * p->fsym_cta_seg0_h.size());
-        if (e == cudaSuccess) e = cudaMemset(p->fsym_acc, 0, sizeof(int32_t) * (size_t)nf * p->M * p->fsym_acc_ld);
-        up(p->fsym_rec, p->fsym_rec_h.data(), sizeof(int) * nf);
-        {
-            const int zero = 0;
-            if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_counts_overflow, &zero, sizeof(int));
-            const size_t csm = (size_t)p->fsym_L * 32 * 4;
-            if (e == cudaSuccess) {
-                if (p->max_delay >= (double)p->Q + 0.5)
-                    fp_sym_count_kernel<true><<<nseg, kFsThreads, csm>>>(
-                        p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups, p->fsym_segs, (float)p->Q + 1.5f,
-                        p->fsym_hx, p->fsym_L, p->fsym_T, p->fsym_counts);
-                else
-                    fp_sym_count_kernel<false><<<nseg, kFsThreads, csm>>>(
-                        p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups, p->fsym_segs, (float)p->Q + 1.5f,
-                        p->fsym_hx, p->fsym_L, p->fsym_T, p->fsym_counts);
-                e = cudaGetLastError();
-            }
-        }
-        int ovf = 0;
-        if (e == cudaSuccess) e = cudaMemcpyFromSymbol(&ovf, g_counts_overflow, sizeof(int));
-        if (e == cudaSuccess && ovf) {
-            free_plan(p);
-            return fail(PK_ERR_UNSUPPORTED, "projector window slot receives > 65535 pixels (set PK_FSYM=0)");
-        }
         std::vector<int> tro((size_t)p->fsym_groups * 32 * 4, -1);
         const int q4 = p->Mall / 4;
         for (int b = 0; b < p->M; ++b)
             for (int g = 0; g < 4; ++g) tro[4 * b + g] = loc_h[(p->gid_h[b] + g * q4) % p->Mall];
         up(p->fsym_trace, tro.data(), sizeof(int) * tro.size());
+        up(p->fsym_rec, p->fsym_rec_h.data(), sizeof(int) * nf);
+        {   // bias counts of every accumulator position (frame 0's segments), the rows' start values
+            const int zero = 0;
+            const size_t words = (size_t)p->M * p->fsym_acc_ld;
+            int* cnt = nullptr;
+            if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_counts_overflow, &zero, sizeof(int));
+            if (e == cudaSuccess) e = cudaMalloc(&cnt, sizeof(int) * words);
+            if (e == cudaSuccess) e = cudaMemset(cnt, 0, sizeof(int) * words);
+            const size_t csm = (size_t)p->fsym_L * 32 * 4;
+            if (e == cudaSuccess) {
+                if (p->max_delay >= (double)p->Q + 0.5)
+                    fp_sym_count_kernel<true><<<nseg, kFsThreads, csm>>>(
+                        p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups, p->fsym_segs, (float)p->Q + 1.5f,
+                        p->fsym_hx, p->fsym_L, p->fsym_T, p->fsym_trace, p->fsym_acc_ld, cnt);
+                else
+                    fp_sym_count_kernel<false><<<nseg, kFsThreads, csm>>>(
+                        p->pxs, p->pys, p->sxs, p->sys, p->nx, p->M, p->fsym_groups, p->fsym_segs, (float)p->Q + 1.5f,
+                        p->fsym_hx, p->fsym_L, p->fsym_T, p->fsym_trace, p->fsym_acc_ld, cnt);
+                e = cudaGetLastError();
+            }
+            if (e == cudaSuccess) {
+                fp_sym_bias_init_kernel<<<1024, 256>>>(cnt, p->fsym_bias, p->fsym_acc, words, nf);
+                e = cudaGetLastError();
+            }
+            if (e == cudaSuccess) e = cudaDeviceSynchronize();
+            if (cnt) cudaFree(cnt);
+        }
+        int ovf = 0;
+        if (e == cudaSuccess) e = cudaMemcpyFromSymbol(&ovf, g_counts_overflow, sizeof(int));
+        if (e == cudaSuccess && ovf) {
+            free_plan(p);
+            return fail(PK_ERR_UNSUPPORTED, "projector accumulator position receives > 65535 pixels (set PK_FSYM=0)");
+        }
     }
     if (e == cudaSuccess) e = cudaMemset(p->table, 0, (size_t)p->M * p->TS * 2 * ts * nf);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);
@@ -1631,6 +1688,14 @@ int pk_delay_census_f32(pk_plan* p, int32_t rule, int32_t ma, int32_t mb, int32_
     PK_CHECK_LAUNCH();
     return PK_OK;
 }
+
+#if PK_FS_TRACE
+// timing experiments only (-DPK_FS_TRACE=1): copy the projector's phase trace of the last launch
+int pk_debug_fs_trace(void* host, int64_t bytes) {
+    const int64_t n = std::min<int64_t>(bytes, sizeof(long long) * 1024 * kFsTraceSlots);
+    return cudaMemcpyFromSymbol(host, g_fs_trace, n) == cudaSuccess ? PK_OK : PK_ERR_CUDA;
+}
+#endif
 
 int pk_profile_iterations(pk_plan* p, const pk_solver_params* prm, const void* y, float* ms,
                           int32_t* launches, void* stream) {

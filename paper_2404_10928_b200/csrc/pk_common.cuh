@@ -372,7 +372,7 @@ struct pk_plan {
     float* fsym_xr = nullptr;     // [(n/2)^2][4] x' rotation-packed by the epilogue
     int32_t* fsym_acc = nullptr;  // [M][acc_ld] int32 trace accumulator (windows reduce-added)
     int* fsym_trace = nullptr;    // [groups * 32][4] local trace of (base sensor, image)
-    uint16_t* fsym_counts = nullptr;  // [segments][L][32] biased words per window slot (u16)
+    uint16_t* fsym_bias = nullptr;  // [M][acc_ld] biased words per accumulator position (u16)
     int4* fsym_segs = nullptr;    // [segments] {group, strip, first row, end row}
     int* fsym_cta_seg0 = nullptr; // [grid + 1]
     int* fsym_rec = nullptr;      // [frames] segment that records the frame's scale

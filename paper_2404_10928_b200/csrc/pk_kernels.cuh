@@ -1342,7 +1342,8 @@ struct FpSymArgs {
                              //   reads and clears it
     int acc_ld;
     const int* trace_of;     // [groups * 32][4] local trace of (base sensor, image), -1: none
-    const uint16_t* counts;  // [segments][LW][32] biased words per window slot (fp_sym_count_kernel)
+    // (every word the scatter adds carries the magic bias kMagicBits; the accumulator rows
+    // start at -count * kMagicBits per position, fp_sym_bias_kernel / the residual kernel)
     const int4* segs;        // [segments] {frame * groups + group, strip, first row, end row}
     const int* cta_seg0;     // [grid + 1] first segment of each CTA
     const int* rec;          // [frames] the segment whose CTA records the frame's scale
@@ -1401,10 +1402,14 @@ __device__ __forceinline__ float fs_delay(float k, float hx, float pxbs, float e
     return tb;
 }
 
-// plan setup: for every (segment, window slot, lane) the number of biased words the projector
-// adds to the slot (pixels of the segment whose delay to the lane's base sensor has s0 = lo + slot
-// or lo + slot + 1).  The projector adds bits(fma(xs, f, 1.5*2^23)) = round(xs*f) + bias and
-// pre-loads each window slot with -count * bias, saving the integer conversions per pair.
+// plan setup: the number of biased words the projector adds at every accumulator position of
+// every local trace (pixels whose delay to the trace's sensor has s0 = t or t + 1).  The
+// projector adds bits(fma(xs, f, 1.5*2^23)) = round(xs*f) + bias, so an accumulator row that
+// starts at -count * bias holds the exact fixed-point sum after the reductions; the residual
+// kernel restores that start when it clears a row it has read.  Per segment (of frame 0: every
+// frame adds the same words) the counts are histogrammed per window slot in shared memory with
+// the projector's own delay code (same s0, bit for bit), then added to the 4 image traces of
+// each lane's base sensor.
 __device__ int g_counts_overflow;
 __device__ __forceinline__ int* counts_overflow_flag() { return &g_counts_overflow; }
 
@@ -1414,11 +1419,13 @@ __global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* p
                                                                   int n, int M, int groups,
                                                                   const int4* segs,
                                                                   float qclamp, float hx, int LW,
-                                                                  int T, uint16_t* counts) {
+                                                                  int T, const int* trace_of,
+                                                                  int acc_ld, int* counts) {
     extern __shared__ int32_t cnt[];  // [LW][32]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, h = n >> 1;
     const int u = blockIdx.x;
     const int4 sg = segs[u];
+    if (sg.x >= groups) return;  // frames > 0 repeat frame 0's words
     const int i0 = h + T * sg.y;
     const int mm = min((sg.x % groups) * 32 + lane, M - 1);  // (segment group: f * groups + group)
     const float sx = __ldg(sxs + mm), sy = __ldg(sys + mm);
@@ -1442,14 +1449,43 @@ __global__ void __launch_bounds__(kFsThreads) fp_sym_count_kernel(const float* p
     __syncthreads();
     // slot k receives the f part of pixels with s0 = lo + k and the 1-f part of those with
     // s0 = lo + k + 1, each word biased by kMagicBits
-    // (u16: a slot receives at most ~2x the pixels of a one-sample annulus through the segment;
-    // plan setup checks the largest count fits)
+    const int b = sg.x * 32 + lane;
+    const int4 tr = b < M ? __ldg(reinterpret_cast<const int4*>(trace_of) + b) : make_int4(-1, -1, -1, -1);
     for (int q = threadIdx.x; q < LW * 32; q += kFsThreads) {
         const int c = cnt[q] + (q + 32 < LW * 32 ? cnt[q + 32] : 0);
-        counts[(size_t)u * LW * 32 + q] = (uint16_t)min(c, 65535);
-        if (c > 65535) atomicMax(counts_overflow_flag(), 1);
+        if (c == 0 || b >= M) continue;  // (lane of q is lane: q % 32 == threadIdx.x % 32)
+        const int pos = kAccFront + lo + (q >> 5);
+        if (tr.x >= 0) atomicAdd(counts + (size_t)tr.x * acc_ld + pos, c);
+        if (tr.y >= 0) atomicAdd(counts + (size_t)tr.y * acc_ld + pos, c);
+        if (tr.z >= 0) atomicAdd(counts + (size_t)tr.z * acc_ld + pos, c);
+        if (tr.w >= 0) atomicAdd(counts + (size_t)tr.w * acc_ld + pos, c);
     }
 }
+
+// plan setup: u16 bias counts of every accumulator position (checked to fit), and every
+// frame's accumulator rows set to their start value -count * kMagicBits
+__global__ void fp_sym_bias_init_kernel(const int* counts, uint16_t* bias, int32_t* acc, size_t words,
+                                        int nf) {
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < words; q += (size_t)gridDim.x * blockDim.x) {
+        const int c = counts[q];
+        if (c > 65535) atomicMax(counts_overflow_flag(), 1);
+        bias[q] = (uint16_t)min(c, 65535);
+        for (int f = 0; f < nf; ++f) acc[(size_t)f * words + q] = -c * kMagicBits;
+    }
+}
+
+// phase trace of the projector (timing experiments only: -DPK_FS_TRACE=1, tools/k2_trace.py):
+// per CTA, clock64 stamps of its phases (slot 0: globaltimer at entry)
+#ifndef PK_FS_TRACE
+#define PK_FS_TRACE 0
+#endif
+constexpr int kFsTraceSlots = 64;
+#if PK_FS_TRACE
+__device__ long long g_fs_trace[1024][kFsTraceSlots];
+#define FS_T(i) do { if (threadIdx.x == 0 && (i) < kFsTraceSlots) g_fs_trace[blockIdx.x][(i)] = clock64(); } while (0)
+#else
+#define FS_T(i) do { } while (0)
+#endif
 
 template <int LW, bool CLAMP, int T, int NW>
 __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs a) {
@@ -1462,19 +1498,27 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
     }
     const int k0 = a.cta_seg0[blockIdx.x], k1 = a.cta_seg0[blockIdx.x + 1];
     if (k0 >= k1) return;
+#if PK_FS_TRACE
+    __shared__ long long wend_s[2];
+    if (threadIdx.x == 0) {
+        long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        g_fs_trace[blockIdx.x][0] = gt;
+        g_fs_trace[blockIdx.x][1] = clock64();
+        g_fs_trace[blockIdx.x][2] = k1 - k0;
+        wend_s[0] = 0x7fffffffffffffffLL; wend_s[1] = 0;
+    }
+#endif
     const float* xall = a.x ? a.x : ((iter & 1) ? a.xb0 : a.xb1);  // bp wrote xb[(iter+1)&1]
     const int n = a.n, h = n >> 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // shared memory: records [NW][32 + kFsBatch] float4 | windows [4][LW][32] | staging
-    // [NGR][32][LW + 4] (round 0; a later round stages into the window rows the previous
-    // rounds have transposed, starting NGR * 512 B early inside the record area, so no round
-    // waits for the engine to finish reading an earlier one)
+    // [NGR][32][LW + 4] (4 / NGR rounds per segment)
     constexpr int WW = 4 * LW * 32;  // window words
     // images per staging round (plans never launch an instantiation whose windows do not fit:
     // fs_ngr == 0), staging row stride
     constexpr int NGR = fs_ngr(LW, NW, fs_cap(NW)) > 0 ? fs_ngr(LW, NW, fs_cap(NW)) : 1, LWS = LW + 4;
     constexpr int REC = NW * (32 + kFsBatch) * 16;
-    static_assert(REC >= NGR * 512, "record area must cover the staging overhang");
     float4* rec = reinterpret_cast<float4*>(smem) + (size_t)warp * (32 + kFsBatch);
     int32_t* win = reinterpret_cast<int32_t*>(smem + REC);
     int32_t* stg0 = reinterpret_cast<int32_t*>(smem + REC + (size_t)WW * 4);
@@ -1486,6 +1530,8 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
     // the 4 image values of piece q of segment (i0, j0): row j0 + q / P2, columns
     // i0 + 32 * (q % P2) + lane
     // (x, xr: the segment frame's x' and rotation-packed x', passed by value)
+    // (claiming the last pieces of a segment as 8-column quarters, so the warps leave the
+    // scatter together, measured no faster: the pipe stays saturated through the tail)
     auto piece_x = [&](const float* x, const float4* xr, int i0, int j0, int j1, int q, float (&v)[4]) {
         const int jj = j0 + q / P2;
         const int ii = i0 + 32 * (q % P2) + lane;
@@ -1499,37 +1545,6 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
             v[1] = x[ii * n + (n - 1 - jj)];
             v[2] = x[(n - 1 - jj) * n + (n - 1 - ii)];
             v[3] = x[(n - 1 - ii) * n + jj];
-        }
-    };
-    // bias counts of segment k: u16, 8 per 16-B load
-    constexpr int NQ = (LW * 4 + NT - 1) / NT;
-    auto load_counts = [&](int k, uint4 (&c)[NQ]) {
-        const uint4* c8 = reinterpret_cast<const uint4*>(a.counts + (size_t)k * LW * 32);
-#pragma unroll
-        for (int i = 0; i < NQ; ++i) {
-            const int q = threadIdx.x + i * NT;
-            c[i] = q < LW * 4 ? __ldg(c8 + q) : make_uint4(0, 0, 0, 0);
-        }
-    };
-    // every window slot starts at -count * bias (see fp_sym_count_kernel)
-    auto init_windows = [&](const uint4 (&c)[NQ]) {
-        int4* w4 = reinterpret_cast<int4*>(win);
-#pragma unroll
-        for (int i = 0; i < NQ; ++i) {
-            const int q = threadIdx.x + i * NT;
-            if (q < LW * 4) {
-                const uint32_t wv[4] = {c[i].x, c[i].y, c[i].z, c[i].w};
-                int4 l4, h4;
-                l4.x = -(int)(wv[0] & 0xffffu) * kMagicBits; l4.y = -(int)(wv[0] >> 16) * kMagicBits;
-                l4.z = -(int)(wv[1] & 0xffffu) * kMagicBits; l4.w = -(int)(wv[1] >> 16) * kMagicBits;
-                h4.x = -(int)(wv[2] & 0xffffu) * kMagicBits; h4.y = -(int)(wv[2] >> 16) * kMagicBits;
-                h4.z = -(int)(wv[3] & 0xffffu) * kMagicBits; h4.w = -(int)(wv[3] >> 16) * kMagicBits;
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    w4[g * LW * 8 + 2 * q] = l4;
-                    w4[g * LW * 8 + 2 * q + 1] = h4;
-                }
-            }
         }
     };
     if (lane < kFsBatch) rec[32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1557,13 +1572,14 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
             __syncthreads();
         }
     };
-    {   // first segment: windows initialised before the wait for the epilogue (constant data)
-        uint4 c[NQ];
-        load_counts(k0, c);
-        init_windows(c);
+    {   // windows start at zero (every staging round zeroes the words it has read, so later
+        // segments find them zeroed), before the wait for the epilogue
+        int4* w4 = reinterpret_cast<int4*>(win);
+        for (int q = threadIdx.x; q < WW / 4; q += NT) w4[q] = make_int4(0, 0, 0, 0);
         if (threadIdx.x == 0) piece_s[k0 & 1] = NW;
     }
     griddep_wait();  // x' and its fixed-point scale come from the back-projector epilogue
+    FS_T(3);
     for (int k = k0; k < k1; ++k) {
         const int4 sg = __ldg(a.segs + k);
         const int fr = sg.x / a.groups, grp = sg.x - fr * a.groups;
@@ -1571,6 +1587,7 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
             cur_fr = fr;
             reduce_scale(fr, k);
         }
+        FS_T(4 + 8 * (k - k0));
         const float* x = xall + (size_t)fr * n * n;
         const float4* xr = a.x ? nullptr : a.xr + (size_t)fr * h * h;
         int32_t* acc = a.acc + (size_t)fr * a.M * a.acc_ld;
@@ -1583,9 +1600,15 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
         const int lo = fp_sym_window_lo(a.pxs, a.pys, n, i0, j0, j1, sx, sy, a.qclamp, T);
         // word (g, k, lane) at (g*LW + k)*32 + lane, k = t - lo for trace index t
         const uint32_t adj = win_s + 4u * (uint32_t)lane - 128u * (uint32_t)lo - 128u * kTwo23Bits;
-        // pieces (row j0 + q / P2, column piece q % P2) claimed dynamically (the first NW
-        // statically, one per warp); the 4 image values of the next piece are loaded while the
-        // current one scatters
+        // the bulk reductions' destinations (trace of each image of this lane's base sensor;
+        // the window start is lo), loaded while the segment scatters
+        // (double-buffered by segment parity: warp 0 may start the next segment while the
+        // issuing warps still read this one's)
+        __shared__ int4 trv_s[2][32];
+        if (warp == 0) trv_s[k & 1][lane] = sensor_ok ? __ldg(reinterpret_cast<const int4*>(a.trace_of) + m)
+                                                      : make_int4(-1, -1, -1, -1);
+        // pieces claimed dynamically (the first NW statically, one per warp); the 4 image
+        // values of the next piece are loaded while the current one scatters
         const int npc = (j1 - j0) * P2;
         int q = warp;
         auto claim = [&]() {
@@ -1663,11 +1686,27 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
             __syncwarp();  // rec is rewritten by the next piece
             q = qn;
         }
-        // the next segment's bias counts are in flight during the barrier and the reduction
-        uint4 cn[NQ];
-        if (k + 1 < k1) load_counts(k + 1, cn);
+#if PK_FS_TRACE
+        if (lane == 0) {
+            const long long t = clock64();
+            atomicMin((unsigned long long*)&wend_s[0], (unsigned long long)t);
+            atomicMax((unsigned long long*)&wend_s[1], (unsigned long long)t);
+        }
+#endif
+        // the staging area is rewritten below: the engine must have read the previous
+        // segment's last round
+        if (pending) bulk_wait_read_all();
+        pending = false;
         if (k == k1 - 1) griddep_launch_dependents();
         __syncthreads();  // the segment's windows are complete
+#if PK_FS_TRACE
+        if (threadIdx.x == 0 && 4 + 8 * (k - k0) + 7 < kFsTraceSlots) {
+            g_fs_trace[blockIdx.x][4 + 8 * (k - k0) + 1] = wend_s[0];
+            g_fs_trace[blockIdx.x][4 + 8 * (k - k0) + 2] = wend_s[1];
+            wend_s[0] = 0x7fffffffffffffffLL; wend_s[1] = 0;
+        }
+#endif
+        FS_T(4 + 8 * (k - k0) + 3);
 
         // reduce-add the windows into the trace accumulator: per round, NGR images are
         // transposed to staging rows [image][lane][slot] (lane l's window is LW contiguous
@@ -1675,54 +1714,59 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
         // bulk reduction of LW words (TMA engine, integer adds at L2: order independent)
         static_assert(LW % 8 == 0, "window length must be whole 32-B sectors");
         for (int g0 = 0; g0 < 4; g0 += NGR) {
-            // round 0: the staging area; round 1: the rows of round 0's images (starting NGR *
-            // 512 B early, inside the record area); later rounds (NGR == 1) wait for the engine
-            // and reuse the staging area
-            int32_t* stg = g0 == 0 ? stg0 : win - NGR * 128;
-            if (g0 >= 2 * NGR) {
+            // every round stages into the staging area (a later round first waits for the
+            // engine to read the earlier one), so the window rows are never staging: the
+            // transposition zeroes each word it reads, and the next segment scatters into the
+            // window as soon as the last round is issued
+            if (g0 > 0) {
                 if (pending) bulk_wait_read_all();
                 pending = false;
                 __syncthreads();
-                stg = stg0;
             }
             // thread -> (image gl, lane l, 4 slots): 4 conflict-free LDS (bank l), one STS.128
             // (row stride LW + 4 words: 8 lanes of a phase hit 8 distinct 16-B bank groups)
-            for (int qq = threadIdx.x; qq < NGR * 32 * (LW / 4); qq += NT) {
-                const int l = qq & 31, r = qq >> 5;
-                const int gl = r / (LW / 4), sl = (r - gl * (LW / 4)) * 4;
-                const int32_t* src = win + ((g0 + gl) * LW + sl) * 32 + l;
-                int4 v;
-                v.x = src[0]; v.y = src[32]; v.z = src[64]; v.w = src[96];
-                *reinterpret_cast<int4*>(stg + (gl * 32 + l) * LWS + sl) = v;
+            constexpr int NTR = NGR * 32 * (LW / 4);  // 4-slot transposition units per round
+            constexpr int TU = (NTR + NT - 1) / NT;
+            {
+                int4 v[TU];
+#pragma unroll
+                for (int u = 0; u < TU; ++u) {  // all loads first (independent), then the stores
+                    const int qq = threadIdx.x + u * NT;
+                    const int l = qq & 31, r = qq >> 5;
+                    const int gl = r / (LW / 4), sl = (r - gl * (LW / 4)) * 4;
+                    int32_t* src = win + ((g0 + gl) * LW + sl) * 32 + l;
+                    if (NTR % NT == 0 || qq < NTR) {
+                        v[u].x = src[0]; v[u].y = src[32]; v[u].z = src[64]; v[u].w = src[96];
+                        src[0] = 0; src[32] = 0; src[64] = 0; src[96] = 0;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < TU; ++u) {
+                    const int qq = threadIdx.x + u * NT;
+                    const int l = qq & 31, r = qq >> 5;
+                    const int gl = r / (LW / 4), sl = (r - gl * (LW / 4)) * 4;
+                    if (NTR % NT == 0 || qq < NTR) *reinterpret_cast<int4*>(stg0 + (gl * 32 + l) * LWS + sl) = v[u];
+                }
             }
+            if (g0 + NGR >= 4 && threadIdx.x == 0) piece_s[(k + 1) & 1] = NW;  // next segment's claims
             fence_proxy_async_smem();
             __syncthreads();
             if (threadIdx.x < NGR * 32) {
                 const int gl = threadIdx.x >> 5, l = threadIdx.x & 31;
-                const int b = grp * 32 + l;
-                const int tr = b < a.M ? __ldg(a.trace_of + 4 * b + g0 + gl) : -1;
-                if (tr >= 0) {
-                    const int lol = fp_sym_window_lo(a.pxs, a.pys, n, i0, j0, j1, __ldg(a.sxs + b),
-                                                     __ldg(a.sys + b), a.qclamp, T);
-                    bulk_reduce_add_u32(acc + (size_t)tr * a.acc_ld + kAccFront + lol,
-                                        smem_u32(stg + (gl * 32 + l) * LWS), LW * 4);
+                const int gi = g0 + gl;
+                const int tr = reinterpret_cast<const int*>(trv_s[k & 1])[4 * l + gi];
+                if (tr >= 0) {  // (lane l of warp gl: base sensor grp * 32 + l, window start lo)
+                    bulk_reduce_add_u32(acc + (size_t)tr * a.acc_ld + kAccFront + lo,
+                                        smem_u32(stg0 + (gl * 32 + l) * LWS), LW * 4);
                     bulk_commit();
                     pending = true;
                 }
             }
-        }
-        if (k + 1 < k1) {
-            // the staging rows (windows and records included) were read by the engine
-            if (pending) bulk_wait_read_all();
-            pending = false;
-            if (threadIdx.x == 0) piece_s[(k + 1) & 1] = NW;
-            __syncthreads();
-            init_windows(cn);
-            if (lane < kFsBatch) rec[32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);  // (staged over)
-            __syncthreads();
+            FS_T(4 + 8 * (k - k0) + 4 + g0 / NGR);
         }
     }
     if (pending) bulk_wait_read_all();  // the staging must outlive the engine's reads
+    FS_T(kFsTraceSlots - 1);
 }
 
 // ===========================================================================
@@ -1854,6 +1898,12 @@ pair_entry(T rp, T rc, int s, int atrick) {
 // pair table, sum r^2; solver mode: the last CTA evaluates the objective and the stopping
 // rules of every frame.
 // ===========================================================================
+// start value of 4 accumulator words from their u16 bias counts
+__device__ __forceinline__ int4 bias_start4(uint2 c) {
+    return make_int4(-(int)(c.x & 0xffffu) * kMagicBits, -(int)(c.x >> 16) * kMagicBits,
+                     -(int)(c.y & 0xffffu) * kMagicBits, -(int)(c.y >> 16) * kMagicBits);
+}
+
 template <typename T>
 struct FinArgs {
     long long* acc;      // [NF][M][Q]
@@ -1881,6 +1931,8 @@ struct FinArgs {
     // at acc32 + m * acc32_ld + kAccFront); read and cleared here (one CTA per trace)
     int32_t* acc32;      // (nullptr: acc mode)
     int acc32_ld;
+    const uint16_t* bias16;  // [M][acc32_ld] biased words per accumulator position (row start
+                             //   value -count * kMagicBits, fp_sym_count_kernel)
     int atrick;
     int chunks;          // sample chunks per sensor (one CTA each)
 };
@@ -2064,10 +2116,11 @@ __global__ void __launch_bounds__(kThreads, PK_FIN_MINB) finalize_kernel(FinArgs
         }
     }
     __syncthreads();
-    if (accr) {  // every sample of the row was read (one CTA per trace): clear it, pads included,
-                 // for the next projection's reductions
+    if (accr) {  // every sample of the row was read (one CTA per trace): reset it, pads included,
+                 // to its start value for the next projection's reductions
         int4* row4 = reinterpret_cast<int4*>(accr - kAccFront);
-        for (int q = threadIdx.x; q < a.acc32_ld / 4; q += kThreads) row4[q] = make_int4(0, 0, 0, 0);
+        const uint2* b4 = reinterpret_cast<const uint2*>(a.bias16 + (size_t)m * a.acc32_ld);
+        for (int q = threadIdx.x; q < a.acc32_ld / 4; q += kThreads) row4[q] = bias_start4(__ldg(b4 + q));
     }
     // entries e in [c0, c1) (the last chunk also writes the zero-padded tail up to TS)
     const int e1 = (cix == chunks - 1) ? a.TS : c1;
@@ -2183,9 +2236,10 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
         }
     }
     __syncthreads();  // tr; every sample of the accumulator row was read
-    {   // clear the row, pads included, for the next projection's reductions
+    {   // reset the row, pads included, to its start value for the next projection's reductions
         int4* row4 = reinterpret_cast<int4*>(accr - kAccFront);
-        for (int q = tid; q < a.acc32_ld / 4; q += kThreads) row4[q] = make_int4(0, 0, 0, 0);
+        const uint2* b4 = reinterpret_cast<const uint2*>(a.bias16 + (size_t)m * a.acc32_ld);
+        for (int q = tid; q < a.acc32_ld / 4; q += kThreads) row4[q] = bias_start4(__ldg(b4 + q));
     }
     // pair table entries e in [0, TS): {r[e-1], r[e] - r[e-1]}, zero padded beyond Q
     float2* tab = a.table + fm * a.TS;
