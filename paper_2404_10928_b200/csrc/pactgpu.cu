@@ -892,6 +892,9 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 std::vector<int>& c0 = p->sym_h[2];
                 std::vector<int>& cs0 = p->sym_h[3];
                 std::vector<int>& ts0 = p->sym_h[4];
+                // (a per-chunk model of the LDS.64 bank-pair conflicts of each half-warp block,
+                // used as cut weights, measured slower: config 3 44.0 -> 47.3 us, config 2
+                // 18.0 -> 22.1 us; the flat 8 / 5 weights stay)
                 int64_t W = 0;
                 for (int t = 0; t < p->sym_ntiles; ++t)
                     W += (int64_t)nch * nf * (((tl[t] >> 16) == (tl[t] & 0xffff)) ? kSymWDiag : kSymWOff);
@@ -1689,6 +1692,25 @@ int pk_delay_census_f32(pk_plan* p, int32_t rule, int32_t ma, int32_t mb, int32_
     return PK_OK;
 }
 
+#if PK_BP_TRACE
+// timing experiments only (-DPK_BP_TRACE=1): the back-projector's phase trace of the last launch
+int pk_debug_bp_trace(void* host, int64_t bytes) {
+    const int64_t n = std::min<int64_t>(bytes, sizeof(long long) * 1536 * 16);
+    return cudaMemcpyFromSymbol(host, g_bp_trace, n) == cudaSuccess ? PK_OK : PK_ERR_CUDA;
+}
+int pk_debug_bp_chunks(void* host, int64_t bytes) {
+    const int64_t n = std::min<int64_t>(bytes, sizeof(int) * 1536 * 64);
+    return cudaMemcpyFromSymbol(host, g_bp_chunk_clk, n) == cudaSuccess ? PK_OK : PK_ERR_CUDA;
+}
+int pk_debug_bp_plan(const pk_plan* p, int* chunks, int* cta_chunk0, int* tiles, int cap) {
+    const size_t n1 = p->sym_h[1].size(), n2 = p->sym_h[2].size(), n0 = p->sym_h[0].size();
+    if ((int)std::max({n0, n1, n2}) > cap) return -1;
+    std::copy(p->sym_h[1].begin(), p->sym_h[1].end(), chunks);
+    std::copy(p->sym_h[2].begin(), p->sym_h[2].end(), cta_chunk0);
+    std::copy(p->sym_h[0].begin(), p->sym_h[0].end(), tiles);
+    return (int)n1;
+}
+#endif
 #if PK_FS_TRACE
 // timing experiments only (-DPK_FS_TRACE=1): copy the projector's phase trace of the last launch
 int pk_debug_fs_trace(void* host, int64_t bytes) {

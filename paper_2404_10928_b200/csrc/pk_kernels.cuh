@@ -617,16 +617,38 @@ __device__ __forceinline__ void sym_epi_units(const BpSymEpiArgs& a, int t, int 
     sync();  // the scratch is reused by the next claim
 }
 
+// phase trace of the back-projector (timing experiments only: -DPK_BP_TRACE=1, tools/k1_trace.py)
+#ifndef PK_BP_TRACE
+#define PK_BP_TRACE 0
+#endif
+#if PK_BP_TRACE
+__device__ long long g_bp_trace[1536][16];
+__device__ int g_bp_chunk_clk[1536][64];   // consumer warp 0: clocks per chunk (first 64)
+#define BP_T(i, v) do { if (threadIdx.x == 0) g_bp_trace[blockIdx.x][(i)] = (v); } while (0)
+#else
+#define BP_T(i, v) do { } while (0)
+#endif
+
 #ifndef PK_SYM_MINB
 #define PK_SYM_MINB 3  // CTAs per SM the back-projector's registers are capped for (build knob)
 #endif
 template <int IW>
 __global__ void __launch_bounds__(kSymThreads, PK_SYM_MINB) bp_sym_f32_kernel(BpSymArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    griddep_wait();  // the pair table and the stop flag come from the residual kernel
-    if (a.st && a.st->all_stopped) return;
+#if PK_BP_TRACE
+    if (threadIdx.x == 0) {
+        long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        g_bp_trace[blockIdx.x][0] = gt;
+        g_bp_trace[blockIdx.x][1] = clock64();
+    }
+#endif
+    // (the pair table and the stop flag come from the residual kernel: griddepcontrol.wait
+    // comes after the constant-data prologue -- the producer's first chunk set-up included --
+    // and before the first read of either)
     const int c0 = a.cta_chunk0[blockIdx.x], c1 = a.cta_chunk0[blockIdx.x + 1];
     if (c0 >= c1) return;
+    BP_T(3, c1 - c0);
     const int n = a.n, h = n >> 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
@@ -656,6 +678,8 @@ __global__ void __launch_bounds__(kSymThreads, PK_SYM_MINB) bp_sym_f32_kernel(Bp
         uint32_t phase = 0;
         for (int c = c0; c < c1; ++c) {
             if (c - c0 >= a.nbuf) mbar_wait(empty_s + 8 * b, phase ^ 1u);
+            // (chunk c0: everything below but the copy is constant geometry, set up before
+            // the wait for the residual kernel)
             const int packed = __ldg(a.chunks + c);
             const int fr = (packed >> 16) / a.ntiles;  // frame of the chunk
             const int tp = __ldg(a.tiles + (packed >> 16) - fr * a.ntiles);
@@ -678,22 +702,27 @@ __global__ void __launch_bounds__(kSymThreads, PK_SYM_MINB) bp_sym_f32_kernel(Bp
                 sconst[b * kSymCS + cs] = make_float4(
                     sx, sy, __uint_as_float(dst0 - 8u * (uint32_t)lo - 8u * kTwo23Bits), 0.f);
             const uint32_t nact = __popc(__ballot_sync(0xffffffffu, act));
+            const size_t src_row = (size_t)__ldg(a.loc + sym_sensor(g, __ldg(a.gid + mm), a.Mall)) * a.TS + lo;
+            if (c == c0) {
+                griddep_wait();
+                if (a.st && a.st->all_stopped) return;
+            }
             __syncwarp();
             if (lane == 0) mbar_expect_tx(full_s + 8 * b, nact * (uint32_t)(a.L * 8));
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (act)
-                bulk_g2s(dst0 + (uint32_t)g * img_stride,
-                         a.table + fr * a.table_fstride +
-                             (size_t)__ldg(a.loc + sym_sensor(g, __ldg(a.gid + mm), a.Mall)) * a.TS + lo,
-                         (uint32_t)(a.L * 8),
-                         full_s + 8 * b);
+                bulk_g2s(dst0 + (uint32_t)g * img_stride, a.table + fr * a.table_fstride + src_row,
+                         (uint32_t)(a.L * 8), full_s + 8 * b);
             if (++b == a.nbuf) { b = 0; phase ^= 1u; }
         }
         return;
     }
 
     // ---- consumer warps
+    griddep_wait();
+    BP_T(2, clock64());
+    if (a.st && a.st->all_stopped) return;
     int lx, ly;
     sym_lane_xy(lane, a.lanemap, lx, ly);
     float acc[4][8];
@@ -749,16 +778,33 @@ __global__ void __launch_bounds__(kSymThreads, PK_SYM_MINB) bp_sym_f32_kernel(Bp
             py = __ldg(a.pys + min(j0 + 4 * warp + ly, n - 1));
         }
         mbar_wait(full_s + 8 * b, phase);
+#if PK_BP_TRACE
+        if (c == c0) BP_T(4, clock64());
+#endif
         const int ns = min(kSymCS, a.M - (packed & 0xffff) * kSymCS);
         const float4* sc = sconst + b * kSymCS;
+#if PK_BP_TRACE
+        const long long tc0 = clock64();
+#endif
         if (diag) sym_chunk<4, IW>(acc, px, py, sc, ns, img_stride, a.qclamp);
         else sym_chunk<8, IW>(acc, px, py, sc, ns, img_stride, a.qclamp);
         __syncwarp();
+#if PK_BP_TRACE
+        if (threadIdx.x == 0 && c - c0 < 64) {
+            float s = 0.f;  // (a dependency on the accumulators, so the clock reads after them)
+#pragma unroll
+            for (int g = 0; g < 8; ++g) s += acc[0][g];
+            g_bp_chunk_clk[blockIdx.x][c - c0] = (int)(clock64() - tc0) + (s == 12345.f ? 1 : 0);
+        }
+#endif
         if (lane == 0) mbar_arrive(empty_s + 8 * b);
         if (++b == a.nbuf) { b = 0; phase ^= 1u; }
     }
+    BP_T(5, clock64());
     griddep_launch_dependents();
     flush();
+    BP_T(6, clock64());
+    BP_T(7, slot - a.cta_slot0[blockIdx.x] + 1);
     if (!a.fuse) return;
     arrive(cur);
     // publish the tiles this CTA completed (counters reset for the next launch first), wait a
