@@ -80,7 +80,9 @@ def parse():
     # the cfg4 sequence: 4 frames per launch on the symmetric kernels, 8 plans in flight
     # (tools/r2_cfg4_sweep.sh); single frames otherwise
     if a.batch is None:
-        a.batch = 4 if a.config == "cfg4" else 1
+        # 4 frames per launch on the symmetric kernels except the 1024^2 stress frame (r02, 4
+        # streams: cfg2 batch 1 2199 / batch 4 2602 frames/s, cfg3 1030 / 1079)
+        a.batch = 1 if a.config == "cfg5" else 4
     if a.streams is None:
         a.streams = 8 if a.config == "cfg4" else 4
     return a
@@ -492,13 +494,17 @@ def main():
     # across streams with a smaller one).  The roofline block below times its kernels too.
     latency_ms = None
     if not sensor_mode:
+        # (the latency is always one frame per launch; the roofline plan below has the timed
+        # region's B frames per launch)
         prof_op = pk.operator_for(grid, ring, ac, pk.CudaPool(local, "float32"), frames=B, slot=SS)
-        xl = torch.empty(B * P, device=dev, dtype=torch.float32)
-        hl = torch.zeros(B * 4 * cfg.iterations, device=dev, dtype=torch.float64)
-        sl = torch.zeros(2 * B, device=dev, dtype=torch.int32)
+        lat_op = prof_op if B == 1 else pk.operator_for(grid, ring, ac, pk.CudaPool(local, "float32"),
+                                                       frames=1, slot=SS + 1)
+        xl = torch.empty(P, device=dev, dtype=torch.float32)
+        hl = torch.zeros(4 * cfg.iterations, device=dev, dtype=torch.float64)
+        sl = torch.zeros(2, device=dev, dtype=torch.int32)
 
         def lat_step(f):
-            N.check(lib.pk_reconstruct(prof_op.handle, params_arr, Ystep[f % n_steps_in].data_ptr(),
+            N.check(lib.pk_reconstruct(lat_op.handle, params_arr, Ystep[f % n_steps_in].data_ptr(),
                                        xl.data_ptr(), hl.data_ptr(), sl.data_ptr(), stream_ptr()))
         l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         nlat = 10
@@ -576,7 +582,7 @@ def main():
                 "peak_source": peak_src + "; MEASURED_PEAKS.json has no FP32 figure",
                 "peak_live": live.value,
                 "traffic_source": traffic_src,
-                "work": f"12 flops x {M} sensors x {P} pixels per launch",
+                "work": f"12 flops x {M} sensors x {P} pixels x {B} frame(s) per launch",
                 "why_fp32": "north_star: FP32 pipe utilisation against B200 peaks; the matrix-free "
                             "operator has ~200 flop/B of compulsory traffic (SURVEY.md 8(d))",
                 "binding_resource": "shared-memory (L1 data) pipe: per sensor-pixel pair the "
@@ -584,9 +590,9 @@ def main():
                                     "LDS.128 record (2 wavefronts per 4 images): 2.5 wavefronts / "
                                     "32 pairs; the back-projector one LDS.64 (2 wavefronts / 32 "
                                     "pairs) -- tools/microbench/mio.cu",
-                "smem_floor_us": (2.5 if "K2" in names[dom] else 2.0) * M * P / 32.0 / (148 * 1.965e3),
+                "smem_floor_us": (2.5 if "K2" in names[dom] else 2.0) * M * P * B / 32.0 / (148 * 1.965e3),
                 # the same kernel against its binding resource: the floor above over its time
-                "smem_pipe_frac": ((2.5 if "K2" in names[dom] else 2.0) * M * P / 32.0 / (148 * 1.965e3))
+                "smem_pipe_frac": ((2.5 if "K2" in names[dom] else 2.0) * M * P * B / 32.0 / (148 * 1.965e3))
                                   / (per_launch_ms[dom] * 1e3),
                 "hbm": {"achieved_GBs": (traffic / t_dom / 1e9) if traffic else None,
                         "peak_GBs": hbm_peak, "peak_source": hbm_src,

@@ -393,8 +393,11 @@ void launch_finalize_t(pk_plan* p, const void* y, void* trace_out, double* sumsq
         }
         a.atrick = p->bp_atrick;
         a.chunks = chunks;
-        if (p->fsym && p->Q <= kFinSymMax && chunks == 1)
-            launch_pdl(finalize_sym_kernel<NF>, grid, dim3(kThreads), 0, s, a);
+        if (p->fsym && p->Q <= kFinSymMax && chunks == 1) {
+            if (p->Q <= 4 * kThreads) launch_pdl(finalize_sym_kernel<NF, 1>, grid, dim3(kThreads), 0, s, a);
+            else if (p->Q <= 8 * kThreads) launch_pdl(finalize_sym_kernel<NF, 2>, grid, dim3(kThreads), 0, s, a);
+            else launch_pdl(finalize_sym_kernel<NF, 4>, grid, dim3(kThreads), 0, s, a);
+        }
         else
             launch_pdl(finalize_kernel<float, NF>, grid, dim3(kThreads), sm, s, a);
     } else {

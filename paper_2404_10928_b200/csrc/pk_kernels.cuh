@@ -858,6 +858,9 @@ __global__ void __launch_bounds__(kSymThreads, PK_SYM_MINB) bp_sym_f32_kernel(Bp
 // DEFER (with the symmetric projector): no last-block reduction here -- the projector's CTAs
 // reduce the max partials into the fixed-point scale and the residual kernel takes sum |x'|
 // and the non-finite count with TV(x'), so no single CTA serialises the end of this kernel.
+#ifndef PK_EPX
+#define PK_EPX 0  // timing experiments only (tools/k2v.sh); 0 = the product
+#endif
 template <bool EPI, bool DEFER>
 __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
     __shared__ float red_f[kThreads / 32];
@@ -891,14 +894,29 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
         by = min(ja, jb);
         bw = abs(ib - ia) + 1;
     }
+    // 0) one pixel per thread in image-row-major order of the strip; a pixel of the strip
+    //    belongs to this CTA iff its representative is in the tile (row / column beyond the
+    //    grid edge, or the reflections of a diagonal tile, are skipped).  Solver mode: its
+    //    iterate value and TV gradient (final since the previous iteration) are loaded
+    //    before the wait for the main kernel
+    int pix;
+    {
+        const int ig = bx + threadIdx.x % bw, jg = by + threadIdx.x / bw;
+        pix = (active && ig >= 0 && ig < n && jg >= 0 && jg < n) ? jg * n + ig : -1;
+    }
+    const float* x = EPI ? ((iter & 1) ? a.xb1 : a.xb0) + (size_t)fr * a.P : nullptr;
+    const bool run = EPI && pix >= 0 && !a.st->fr[fr].stopped;
+    float xv = 0.f, tvg = 0.f;
+    if (run) {
+        xv = x[pix];
+        const float beta = (float)a.prm->beta[fr], eps = (float)a.prm->eps;
+        if (beta > 0.f && PK_EPX != 3) tvg = tv_grad_at<float>(x, pix, pix % n, pix / n, n, n, eps * eps);
+    }
     // 1) slot sum: thread (sg, q) adds slots s0 + sg, s0 + sg + 4, ... of consumers 4q..4q+3
     //    (16-B loads, 8 in flight); the 4 slot groups are then added in order (deterministic)
     const int sg = threadIdx.x >> 6, q = threadIdx.x & 63;
     griddep_wait();  // partial slots of the main kernel
     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-#ifndef PK_EPX
-#define PK_EPX 0  // timing experiments only (tools/k2v.sh); 0 = the product
-#endif
     if (active && PK_EPX != 1) {
         const float4* src = reinterpret_cast<const float4*>(a.part + (size_t)(g * 4 + k) * kThreads) + q;
         const size_t stride = 8 * 4 * kThreads / 4;  // float4s per slot
@@ -934,33 +952,24 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
         }
     }
     __syncthreads();
-    // 3) one pixel per thread in image-row-major order of the strip
-    int pix;
-    float val;
-    {
-        const int ig = bx + threadIdx.x % bw, jg = by + threadIdx.x / bw;
-        // a pixel of the strip belongs to this CTA iff its representative is in the tile (row /
-        // column beyond the grid edge, or the reflections of a diagonal tile, are skipped)
-        pix = (active && ig >= 0 && ig < n && jg >= 0 && jg < n) ? jg * n + ig : -1;
-        val = blk[threadIdx.x];
-    }
+    // 3) the update of this thread's pixel
+    const float val = blk[threadIdx.x];
     if (!EPI) {
         if (pix >= 0) a.out[(size_t)fr * a.P + pix] = val;
         return;
     }
-    const float* x = ((iter & 1) ? a.xb1 : a.xb0) + (size_t)fr * a.P;
     float* xo = ((iter & 1) ? a.xb0 : a.xb1) + (size_t)fr * a.P;
     float* xr = a.xr ? a.xr + (size_t)fr * a.P : nullptr;  // (4 * (n/2)^2 = P floats per frame)
     const float eta = (float)a.prm->step[fr], lam = (float)a.prm->eta_alpha[fr];
-    const float beta = (float)a.prm->beta[fr], eps = (float)a.prm->eps;
+    const float beta = (float)a.prm->beta[fr];
     const bool nonneg = a.prm->nonneg != 0;
     float mx = 0.f, l1 = 0.f;
     int bad = 0;
-    if (!a.st->fr[fr].stopped && pix >= 0) {
+    if (run) {
         const int p = pix;
         float gr = val;
-        if (beta > 0.f && PK_EPX != 3) gr += beta * tv_grad_at<float>(x, p, p % n, p / n, n, n, eps * eps);
-        const float xn = prox<float>(x[p] - eta * gr, lam, nonneg);
+        if (beta > 0.f && PK_EPX != 3) gr += beta * tvg;
+        const float xn = prox<float>(xv - eta * gr, lam, nonneg);
         xo[p] = xn;
         if (xr) xr[sym_rot_index(p % n, p / n, n)] = xn;
         if (!isfinite(xn)) bad = 1;
@@ -2194,17 +2203,19 @@ __global__ void __launch_bounds__(kThreads, PK_FIN_MINB) finalize_kernel(FinArgs
     finalize_objective<T, NF>(a, chunks, data_s, tv_s, red_d);
 }
 
-// K3 for the symmetric projector (fp32, one frame): one CTA of 256 threads per trace, every
-// load issued up front -- TV(x') of the iterate (its slice) and the measurements before the
-// wait for the projection (both final by then), then the int32 accumulator row (read once,
-// then cleared for the next projection's reductions); r = w*acc/scale - y rounded as
-// finalize_kernel does, the pair table and the sums.  Q <= kFinSymMax.
-constexpr int kFinSymG = 4;                       // int4 groups per thread
+// K3 for the symmetric projector (fp32): one CTA of 256 threads per (trace, frame), every
+// load issued up front -- TV(x') of the iterate (its slice) before the wait for the projection
+// (final by then), then per thread groups of 4 samples: the int32 accumulator words and the
+// measurements of the group and of the sample before it (so the pair-table entries of the
+// group need no exchange between threads: no shared-memory staging, one barrier -- the sums'),
+// r = w*acc/scale - y rounded as finalize_kernel does, the pair table, the sums; the row is
+// reset to its start value after the barrier (every read of it is done).  Q <= kFinSymMax.
+// G: 4-sample groups per thread (1, 2 or 4: the smallest with 4 * 256 * G >= Q; the pair-table
+// entries past the groups are a short tail loop)
+constexpr int kFinSymG = 4;
 constexpr int kFinSymMax = 4 * kThreads * kFinSymG;  // 4096 samples
-template <int NF>
+template <int NF, int G>
 __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float> a) {
-    __shared__ float tr[kFinSymMax + 8];           // tr[1 + s] = r[s], tr[0] = 0
-    __shared__ __align__(16) float ys[kFinSymMax];  // measurements (LDGSTS: no registers held)
     __shared__ double red_d[kThreads / 32];
     __shared__ double red4[4 * kThreads / 32];
     __shared__ double data_s[NF], tv_s[NF];
@@ -2218,11 +2229,6 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
     if (ym) ym += fm * Q;
     float* om = a.trace_out ? a.trace_out + fm * Q : nullptr;
     int32_t* accr = a.acc32 + fm * a.acc32_ld + kAccFront;
-    // measurements (constant): staged before the wait
-    if (ym) {
-        for (int k = tid; k < Q; k += kThreads) cp_async<4>(ys + k, ym + k);
-        cp_async_commit();
-    }
     double tvp = 0.0, l1p = 0.0, badp = 0.0;
     if (a.tv_here) {  // exact anisotropic TV of x' (recon.py:169-170), sum |x'|, non-finite
         const int n = a.n, P = n * n, per = (P + gridDim.x - 1) / gridDim.x;
@@ -2238,41 +2244,60 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
             if (p + n < P) tvp += (double)fabsf(xd - v);
         }
     }
-    griddep_wait();  // the projection's accumulator and scale
-    int4 v4[kFinSymG];
+    // measurements (constant): loaded before the wait (G = 4: after it, with the accumulator
+    // words -- 64 registers do not hold both sets across the wait)
+    const bool y4ok = ym && (Q & 3) == 0;
+    float4 y4[G];
+    float yp[G];
+    auto load_y = [&]() {
 #pragma unroll
-    for (int i = 0; i < kFinSymG; ++i) {
+    for (int i = 0; i < G; ++i) {
+        const int s0 = 4 * (tid + i * kThreads);
+        y4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        yp[i] = 0.f;
+        if (ym && s0 < Q) {
+            if (y4ok) y4[i] = __ldg(reinterpret_cast<const float4*>(ym + s0));
+            else {
+                y4[i].x = __ldg(ym + s0);
+                if (s0 + 1 < Q) y4[i].y = __ldg(ym + s0 + 1);
+                if (s0 + 2 < Q) y4[i].z = __ldg(ym + s0 + 2);
+                if (s0 + 3 < Q) y4[i].w = __ldg(ym + s0 + 3);
+            }
+        }
+        if (ym && s0 >= 1 && s0 - 1 < Q) yp[i] = __ldg(ym + s0 - 1);
+    }
+    };
+    if (G <= 2) load_y();
+    griddep_wait();  // the projection's accumulator and scale
+    if (G > 2) load_y();
+    int4 v4[G];
+    int32_t vp[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
         const int s0 = 4 * (tid + i * kThreads);
         v4[i] = s0 < Q ? __ldcg(reinterpret_cast<const int4*>(accr + s0)) : make_int4(0, 0, 0, 0);
+        vp[i] = (s0 >= 1 && s0 - 1 < Q) ? __ldcg(accr + s0 - 1) : 0;
     }
     const double sc = (double)a.st->fr[f].scale32;
     const double wq = sc > 0.0 ? a.w / sc : 0.0;
+    // K x rounded to fp32 first, then the residual (recon.py:75-79 semantics)
+    auto resid = [&](int32_t v, float yv) -> float {
+        const float kx = (float)((double)v * wq);
+        return ym ? kx - yv : kx;
+    };
     double ss = 0.0;
-    if (tid == 0) tr[0] = 0.f;
-    if (ym) cp_async_wait_all();
-    __syncthreads();  // ys
+    float2* tab = a.table + fm * a.TS;
 #pragma unroll
-    for (int i = 0; i < kFinSymG; ++i) {
+    for (int i = 0; i < G; ++i) {
         const int s0 = 4 * (tid + i * kThreads);
+        if (s0 >= a.TS) continue;
         const int vv[4] = {v4[i].x, v4[i].y, v4[i].z, v4[i].w};
-        float yy[4];
-        if (ym && s0 + 4 <= Q) {
-            const float4 y4 = *reinterpret_cast<const float4*>(ys + s0);
-            yy[0] = y4.x; yy[1] = y4.y; yy[2] = y4.z; yy[3] = y4.w;
-        } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) yy[q] = (ym && s0 + q < Q) ? ys[s0 + q] : 0.f;
-        }
+        const float yy[4] = {y4[i].x, y4[i].y, y4[i].z, y4[i].w};
         float rr[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            // K x rounded to fp32 first, then the residual (recon.py:75-79 semantics)
-            const float kx = (float)((double)vv[q] * wq);
-            rr[q] = ym ? kx - yy[q] : kx;
-            if (s0 + q < Q) {
-                tr[1 + s0 + q] = rr[q];
-                ss += (double)rr[q] * (double)rr[q];
-            }
+            rr[q] = (s0 + q < Q) ? resid(vv[q], yy[q]) : 0.f;
+            if (s0 + q < Q) ss += (double)rr[q] * (double)rr[q];
         }
         if (om && s0 < Q) {
             if (s0 + 4 <= Q && ((reinterpret_cast<uintptr_t>(om) & 15) == 0))
@@ -2280,26 +2305,19 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
             else
                 for (int q = 0; q < 4 && s0 + q < Q; ++q) om[s0 + q] = rr[q];
         }
+        // pair table entries e = s0 .. s0 + 3: {r[e-1], r[e] - r[e-1]}, zero padded beyond Q
+        const float rprev = (s0 >= 1 && s0 - 1 < Q) ? resid(vp[i], yp[i]) : 0.f;
+        const float2 p0 = pair_entry<float>(rprev, rr[0], s0, a.atrick);
+        const float2 p1 = pair_entry<float>(rr[0], rr[1], s0 + 1, a.atrick);
+        const float2 p2 = pair_entry<float>(rr[1], rr[2], s0 + 2, a.atrick);
+        const float2 p3 = pair_entry<float>(rr[2], rr[3], s0 + 3, a.atrick);
+        *reinterpret_cast<float4*>(tab + s0) = make_float4(p0.x, p0.y, p1.x, p1.y);  // (TS even)
+        if (s0 + 2 < a.TS) *reinterpret_cast<float4*>(tab + s0 + 2) = make_float4(p2.x, p2.y, p3.x, p3.y);
     }
-    __syncthreads();  // tr; every sample of the accumulator row was read
-    {   // reset the row, pads included, to its start value for the next projection's reductions
-        int4* row4 = reinterpret_cast<int4*>(accr - kAccFront);
-        const uint2* b4 = reinterpret_cast<const uint2*>(a.bias16 + (size_t)m * a.acc32_ld);
-        for (int q = tid; q < a.acc32_ld / 4; q += kThreads) row4[q] = bias_start4(__ldg(b4 + q));
-    }
-    // pair table entries e in [0, TS): {r[e-1], r[e] - r[e-1]}, zero padded beyond Q
-    float2* tab = a.table + fm * a.TS;
-    for (int e0 = 2 * tid; e0 < a.TS; e0 += 2 * kThreads) {
-        float2 p2[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int e = e0 + q;
-            const float rp = (e >= 1 && e - 1 < Q) ? tr[e] : 0.f;
-            const float rc = (e < Q) ? tr[e + 1] : 0.f;
-            p2[q] = pair_entry<float>(rp, rc, e, a.atrick);
-        }
-        if (e0 + 1 < a.TS) *reinterpret_cast<float4*>(tab + e0) = make_float4(p2[0].x, p2[0].y, p2[1].x, p2[1].y);
-        else tab[e0] = p2[0];
+    // entries past the groups (e.g. Q = 2048: e = 2048, 2049)
+    for (int e = 4 * kThreads * G + tid; e < a.TS; e += kThreads) {
+        auto rat = [&](int s) { return (s >= 0 && s < Q) ? resid(__ldcg(accr + s), ym ? __ldg(ym + s) : 0.f) : 0.f; };
+        tab[e] = pair_entry<float>(rat(e - 1), rat(e), e, a.atrick);
     }
     griddep_launch_dependents();
     if (a.tv_here) {
@@ -2314,6 +2332,12 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
     } else {
         ss = block_sum(ss, red_d);
         if (tid == 0) a.part_r[fm] = ss;
+    }
+    {   // (after the sums' barrier: every read of the row is done) reset the row, pads
+        // included, to its start value for the next projection's reductions
+        int4* row4 = reinterpret_cast<int4*>(accr - kAccFront);
+        const uint2* b4 = reinterpret_cast<const uint2*>(a.bias16 + (size_t)m * a.acc32_ld);
+        for (int q = tid; q < a.acc32_ld / 4; q += kThreads) row4[q] = bias_start4(__ldg(b4 + q));
     }
     if (!last_block(&a.st->cnt_fin, gridDim.x * gridDim.y, &last_flag)) return;
     finalize_objective<float, NF>(a, 1, data_s, tv_s, red_d);

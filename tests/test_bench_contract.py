@@ -48,6 +48,7 @@ def test_our_arm_line_gpu():
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["value"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
-    assert d["solves_checked"] == 20 and e2e["solves_checked"] == 20  # every timed solve ran 10 it
+    B = d["arm"]["batch"]  # frames per launch: every timed frame solve ran 10 iterations
+    assert d["solves_checked"] == 20 * B and e2e["solves_checked"] == 20 * B
     ref = run_bench("--impl", "reference", "--config", "cfg1", "--steps", "1", "--warmup", "1")
     assert ref["config"] == d["config"]  # the two arms describe the same workload

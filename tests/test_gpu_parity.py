@@ -526,9 +526,11 @@ def test_back_project_vs_oracle(oracle, pool):
 
 
 def test_throughput_plans_concurrent_vs_oracle(oracle):
-    """The bench's timed configuration: config 3, four throughput-mode plans (concurrency 4,
-    the bench's default) on four streams, 10 iterations each, every frame against the fp64
-    oracle's reconstruction (recon.py:286-377) with the bench's pinned parameters."""
+    """The bench's timed configurations at config 3: four throughput-mode plans (concurrency
+    4, the bench's default) on four streams with one frame per launch, and two batched plans
+    of four frames per launch (the bench's default batch since r02) on two streams, 10
+    iterations each; every frame against the fp64 oracle's reconstruction (recon.py:286-377)
+    with the bench's pinned parameters."""
     import torch
 
     n, M, Q, N = 512, 512, 2048, 10
@@ -537,25 +539,31 @@ def test_throughput_plans_concurrent_vs_oracle(oracle):
     ys = [o.forward((ph0 if f == 0 else pk.make_vessel_phantom(g, f)).values) for f in range(4)]
     alpha, beta = oracle.resolve_regularization(o, ys[0])
     step = 333.156  # survey-pinned cfg3 step (as test_large_config_vs_oracle)
-    params = pk.solver.solver_params(pk.ReconConfig(alpha, beta, N, step), alpha, beta, step)
-    ops = [pk.operator_for(g, ring, ac, F32, slot=q, concurrency=4) for q in range(4)]
-    assert all(op.info.symmetric == 3 for op in ops)
-    streams = [torch.cuda.Stream() for _ in range(4)]
-    yd = [torch.tensor(y, device="cuda", dtype=torch.float32) for y in ys]
-    torch.cuda.synchronize()
-    outs = []
-    for q in range(4):
-        with torch.cuda.stream(streams[q]):
-            outs.append(ops[q].reconstruct(yd[q], params))
-    torch.cuda.synchronize()
-    for q in range(4):
-        ref = oracle.reconstruct(o, ys[q], alpha, beta, step, N)
-        x, hist, status = (t.cpu().numpy() for t in outs[q])
-        assert status[0, 0] == N and status[0, 1] == 0
-        err = rel(x[0], ref["image"])
-        print(f"frame {q}: rel L2 {err:.3e}")
-        assert err <= 1e-4
-        np.testing.assert_allclose(hist[0][0], ref["objective_history"], rtol=1e-4)
+    refs = [oracle.reconstruct(o, y, alpha, beta, step, N) for y in ys]
+    for batch, nplans in ((1, 4), (4, 2)):
+        params = pk.solver.solver_params(pk.ReconConfig(alpha, beta, N, step), alpha, beta, step)
+        ops = [pk.operator_for(g, ring, ac, F32, slot=q, concurrency=4, frames=batch) for q in range(nplans)]
+        assert all(op.info.symmetric == 3 and op.info.frames == batch for op in ops)
+        streams = [torch.cuda.Stream() for _ in range(nplans)]
+        # plan q solves frames (q * batch + b) % 4, b < batch
+        fidx = [[(q * batch + b) % 4 for b in range(batch)] for q in range(nplans)]
+        yd = [torch.tensor(np.concatenate([ys[f] for f in fidx[q]]), device="cuda", dtype=torch.float32)
+              for q in range(nplans)]
+        torch.cuda.synchronize()
+        outs = []
+        for q in range(nplans):
+            with torch.cuda.stream(streams[q]):
+                outs.append(ops[q].reconstruct(yd[q], params))
+        torch.cuda.synchronize()
+        for q in range(nplans):
+            x, hist, status = (t.cpu().numpy() for t in outs[q])
+            for b, f in enumerate(fidx[q]):
+                ref = refs[f]
+                assert status[b, 0] == N and status[b, 1] == 0
+                err = rel(x[b], ref["image"])
+                print(f"batch {batch} plan {q} frame {f}: rel L2 {err:.3e}")
+                assert err <= 1e-4
+                np.testing.assert_allclose(hist[b][0], ref["objective_history"], rtol=1e-4)
 
 
 def test_bp_artifacts_outside_support():
