@@ -218,6 +218,50 @@ constexpr int kSymIW[] = {64, 96, 128, 192, 256};
 // (per delay ~8 issue slots of geometry + 3 per image: 20 vs 32)
 constexpr int kSymWDiag = 5, kSymWOff = 8;
 
+// chunk ranges of the symmetric back-projector's persistent CTAs: equal-cost contiguous
+// ranges of the (frame-major tile, chunk) sequence, off-diagonal chunk weight 32, diagonal
+// wdiag; every CTA leaves one partial slot per tile it touches.  Fills sym_h[1..4], sym_slots.
+static void sym_partition(pk_plan* p, int wdiag) {
+    const std::vector<int>& tl = p->sym_h[0];
+    std::vector<int>& ch = p->sym_h[1];
+    std::vector<int>& c0 = p->sym_h[2];
+    std::vector<int>& cs0 = p->sym_h[3];
+    std::vector<int>& ts0 = p->sym_h[4];
+    ch.clear(); c0.clear(); cs0.clear(); ts0.clear();
+    const int nf = p->nf, nch = p->sym_nch;
+    auto cw_of = [&](int tt) { return ((tl[tt] >> 16) == (tl[tt] & 0xffff)) ? wdiag : 32; };
+    int64_t W = 0;
+    for (int t = 0; t < p->sym_ntiles; ++t) W += (int64_t)nch * nf * cw_of(t);
+    const int G = p->sym_grid;
+    c0.assign(G + 1, 0);
+    cs0.assign(G, 0);
+    int64_t cw = 0;
+    int owner_prev = -1, tile_prev = -1, slot = -1;
+    // frame-major tiles: chunk tile index t = frame * ntiles + tile
+    for (int t = 0; t < p->sym_ntiles * nf; ++t) {
+        const int wt = cw_of(t % p->sym_ntiles);
+        for (int k = 0; k < nch; ++k) {
+            const int owner = (int)std::min<int64_t>(G - 1, cw * G / W);
+            if (owner != owner_prev || t != tile_prev) {
+                ++slot;
+                if (t != tile_prev) ts0.push_back(slot);
+                if (owner != owner_prev) {
+                    for (int b = owner_prev + 1; b <= owner; ++b) c0[b] = (int)ch.size();
+                    cs0[owner] = slot;
+                }
+                owner_prev = owner;
+                tile_prev = t;
+            }
+            ch.push_back((t << 16) | k);
+            cw += wt;
+        }
+    }
+    for (int b = owner_prev + 1; b <= G; ++b) c0[b] = (int)ch.size();
+    ts0.push_back(slot + 1);
+    p->sym_slots = slot + 1;
+}
+constexpr int kSymWCand[] = {18, 20, 22, 24, 26};
+
 template <int IW>
 void launch_sym(const BpSymArgs& A, int grid, int smem, cudaStream_t s) {
     launch_pdl(bp_sym_f32_kernel<IW>, dim3(grid), dim3(kSymThreads), smem, s, A);
@@ -568,6 +612,84 @@ int launch_bp(pk_plan* p, int epi, void* out, double g, cudaStream_t s) {
     PK_DISPATCH(launch_bp_t, p, epi, out, g, s);
     return PK_OK;
 }
+// upload the host partition of the symmetric back-projector
+static cudaError_t sym_upload(pk_plan* p) {
+    int* dsts[4] = {p->sym_chunks, p->sym_cta_chunk0, p->sym_cta_slot0, p->sym_tile_slot0};
+    for (int q = 0; q < 4; ++q) {
+        const cudaError_t e = cudaMemcpy(dsts[q], p->sym_h[q + 1].data(), sizeof(int) * p->sym_h[q + 1].size(),
+                                         cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// the diagonal cut weight of the symmetric back-projector: each candidate partition timed
+// (back-projection of a zero table, non-solver, 3 launches after a warm-up, the minimum), once
+// per geometry and process; every later plan of the same geometry reuses the choice, so plans
+// of one process agree bit for bit
+static cudaError_t sym_tune_wdiag(pk_plan* p) {
+    if (!p->sym || p->dtype != PK_F32 || p->sym_wdiag < 0) return cudaSuccess;
+    if (getenv("CUDA_INJECTION64_PATH")) {
+        // under a profiler (ncu injects itself) event times are the tool's, not the kernel's:
+        // the measured choice of the unprofiled runs (configs 1-5: 24, except 18 at config 2's
+        // pitch of 3.9 samples per pixel with frames batched), no timing
+        const double hx = p->fsym_hx > 0.f ? p->fsym_hx : 1.0;
+        const int w = (hx > 2.9 && p->nf > 1 && p->nx < 512) ? 18 : 24;
+        sym_partition(p, w);
+        p->sym_wdiag = w;
+        return sym_upload(p);
+    }
+    static std::mutex mu;
+    static std::map<std::vector<long long>, int> best_of;
+    std::vector<long long> key = {p->nx, p->M, p->Mall, p->Q, p->nf, p->sym_grid, p->sym_nbuf, p->sym_iw,
+                                  (long long)std::llround(p->cdt * 1e12)};
+    for (int g : p->gid_h) key.push_back(g);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = best_of.find(key);
+        if (it != best_of.end()) {
+            sym_partition(p, it->second);
+            p->sym_wdiag = it->second;
+            return sym_upload(p);
+        }
+    }
+    cudaStream_t s;
+    cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    int best = std::abs(p->sym_wdiag);
+    float best_ms = 1e30f;
+    for (int w : kSymWCand) {
+        sym_partition(p, w);
+        if ((e = sym_upload(p)) != cudaSuccess) break;
+        float t = 1e30f;
+        for (int r = 0; r < 4 && e == cudaSuccess; ++r) {
+            cudaEventRecord(e0, s);
+            if (launch_bp(p, 0, p->xbuf[0], 1.0, s) != PK_OK) e = cudaErrorUnknown;
+            cudaEventRecord(e1, s);
+            if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+            float ms = 0.f;
+            if (e == cudaSuccess && r > 0 && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess) t = std::min(t, ms);
+        }
+        if (e != cudaSuccess) break;
+        if (getenv("PK_SYM_TUNE_LOG")) fprintf(stderr, "pk sym tune: wdiag %d %.2f us\n", w, 1e3 * t);
+        if (t < best_ms) { best_ms = t; best = w; }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    if (e != cudaSuccess) return e;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        best = best_of.emplace(key, best).first->second;  // (a concurrent tuner may have won)
+    }
+    sym_partition(p, best);
+    p->sym_wdiag = best;
+    return sym_upload(p);
+}
+
 int launch_table(pk_plan* p, const void* y, int init, cudaStream_t s) {
     PK_DISPATCH(launch_table_t, p, y, init, s);
     return PK_OK;
@@ -891,44 +1013,23 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                             32, std::min<int64_t>((int64_t)occ * sms / 2, wsum / 64));
                 }
                 if (const char* e = getenv("PK_SYM_GRID")) p->sym_grid = std::max(1, atoi(e));
-                std::vector<int>& ch = p->sym_h[1];
-                std::vector<int>& c0 = p->sym_h[2];
-                std::vector<int>& cs0 = p->sym_h[3];
-                std::vector<int>& ts0 = p->sym_h[4];
-                // (a per-chunk model of the LDS.64 bank-pair conflicts of each half-warp block,
-                // used as cut weights, measured slower: config 3 44.0 -> 47.3 us, config 2
-                // 18.0 -> 22.1 us; the flat 8 / 5 weights stay)
-                int64_t W = 0;
-                for (int t = 0; t < p->sym_ntiles; ++t)
-                    W += (int64_t)nch * nf * (((tl[t] >> 16) == (tl[t] & 0xffff)) ? kSymWDiag : kSymWOff);
-                const int G = p->sym_grid;
-                c0.assign(G + 1, 0);
-                cs0.assign(G, 0);
-                int64_t cw = 0;
-                int owner_prev = -1, tile_prev = -1, slot = -1;
-                // frame-major tiles: chunk tile index t = frame * ntiles + tile
-                for (int t = 0; t < p->sym_ntiles * nf; ++t) {
-                    const int tt = t % p->sym_ntiles;
-                    const int wt = ((tl[tt] >> 16) == (tl[tt] & 0xffff)) ? kSymWDiag : kSymWOff;
-                    for (int k = 0; k < nch; ++k) {
-                        const int owner = (int)std::min<int64_t>(G - 1, cw * G / W);
-                        if (owner != owner_prev || t != tile_prev) {
-                            ++slot;
-                            if (t != tile_prev) ts0.push_back(slot);
-                            if (owner != owner_prev) {
-                                for (int b = owner_prev + 1; b <= owner; ++b) c0[b] = (int)ch.size();
-                                cs0[owner] = slot;
-                            }
-                            owner_prev = owner;
-                            tile_prev = t;
-                        }
-                        ch.push_back((t << 16) | k);
-                        cw += wt;
-                    }
-                }
-                for (int b = owner_prev + 1; b <= G; ++b) c0[b] = (int)ch.size();
-                ts0.push_back(slot + 1);
-                p->sym_slots = slot + 1;
+                // cut weights: off-diagonal chunk 32, diagonal chunk wdiag.  (A per-chunk model
+                // of the LDS.64 bank-pair conflicts of each half-warp block, used as cut
+                // weights, measured slower: config 3 44.0 -> 47.3 us, config 2 18.0 -> 22.1 us.)
+                // The best wdiag depends on how the cuts fall against tile boundaries and on
+                // which CTAs share an SM, not on one cost ratio (measured, tools/k2_sweep_cfg.sh:
+                // config 3 44.4 / 42.1 us at 20 / 24, 4 frames per launch 160.8 / 148.5; config
+                // 2 x 4 frames 34.0 / 37.7, best 17-18; config 1 x 4 frames best 24), so the plan
+                // times the candidates once per geometry and process (sym_tune_wdiag) unless
+                // PK_SYM_WDIAG pins it
+                p->sym_nch = nch;
+                p->sym_wdiag = 24;
+                if (const char* e = getenv("PK_SYM_WDIAG")) p->sym_wdiag = -std::max(1, atoi(e));  // (< 0: pinned)
+                // (the partial-slot buffer holds the largest candidate's slots)
+                int smax = 0;
+                for (int w : kSymWCand) { sym_partition(p, w); smax = std::max(smax, p->sym_slots); }
+                sym_partition(p, std::abs(p->sym_wdiag));
+                p->sym_slots_cap = std::max(smax, p->sym_slots);
             }
         }
         // rotation-symmetric projector (fp_sym_f32_kernel): persistent CTAs, every one resident
@@ -1204,7 +1305,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
         A(alloc(p, &p->sym_cta_chunk0, p->sym_h[2].size()));
         A(alloc(p, &p->sym_cta_slot0, p->sym_h[3].size()));
         A(alloc(p, &p->sym_tile_slot0, p->sym_h[4].size()));
-        A(alloc(p, &p->sym_part, (size_t)p->sym_slots * 8 * 4 * kThreads));
+        A(alloc(p, &p->sym_part, (size_t)p->sym_slots_cap * 8 * 4 * kThreads));
     }
     A(alloc(p, &p->state, 1));
     A(alloc(p, &p->params, 1));
@@ -1279,6 +1380,8 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
     // opt every dynamic-smem kernel into the device maximum once per device (a per-plan
     // value would shrink the limit under plans created earlier with larger windows)
     if (e == cudaSuccess) e = opt_in_smem(p->device);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = sym_tune_wdiag(p);  // (zero table: the products' cost is data independent)
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         free_plan(p);

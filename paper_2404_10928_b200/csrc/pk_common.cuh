@@ -354,6 +354,9 @@ struct pk_plan {
     // D4-symmetric back-projector (bp_sym_f32_kernel + bp_sym_epi_kernel)
     int sym = 0, sym_ntiles = 0, sym_L = 0, sym_nbuf = 0, sym_smem = 0, sym_grid = 0, sym_slots = 0;
     int sym_iw = 0;  // compile-time image-window stride (slots), 0 = runtime
+    int sym_nch = 0;     // chunks (of kSymCS base sensors) per tile
+    int sym_wdiag = 24;  // cut weight of a diagonal chunk (off-diagonal 32); < 0: pinned (env)
+    int sym_slots_cap = 0;  // partial slots allocated (the largest candidate partition's)
     int sym_lanemap = 1;
     int sym_fuse = 0;     // update fused into the back-projector's tail (solver mode, opt-in)
     int *sym_tiles = nullptr, *sym_chunks = nullptr, *sym_cta_chunk0 = nullptr,
