@@ -643,9 +643,9 @@ __global__ void __launch_bounds__(kSymThreads, PK_SYM_MINB) bp_sym_f32_kernel(Bp
         g_bp_trace[blockIdx.x][1] = clock64();
     }
 #endif
-    // (the pair table and the stop flag come from the residual kernel: griddepcontrol.wait
-    // comes after the constant-data prologue -- the producer's first chunk set-up included --
-    // and before the first read of either)
+    griddep_wait();  // the pair table and the stop flag come from the residual kernel
+    BP_T(2, clock64());
+    if (a.st && a.st->all_stopped) return;
     const int c0 = a.cta_chunk0[blockIdx.x], c1 = a.cta_chunk0[blockIdx.x + 1];
     if (c0 >= c1) return;
     BP_T(3, c1 - c0);
@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(kSymThreads, PK_SYM_MINB) bp_sym_f32_kernel(Bp
     if (threadIdx.x == 0) {
         for (int b = 0; b < a.nbuf; ++b) {
             mbar_init(full_s + 8 * b, 1);
-            mbar_init(empty_s + 8 * b, kSymConsumers);
+            mbar_init(empty_s + 8 * b, kSymConsumers * 32);  // every consumer thread releases
         }
         fence_barrier_init();
     }
@@ -678,8 +678,6 @@ __global__ void __launch_bounds__(kSymThreads, PK_SYM_MINB) bp_sym_f32_kernel(Bp
         uint32_t phase = 0;
         for (int c = c0; c < c1; ++c) {
             if (c - c0 >= a.nbuf) mbar_wait(empty_s + 8 * b, phase ^ 1u);
-            // (chunk c0: everything below but the copy is constant geometry, set up before
-            // the wait for the residual kernel)
             const int packed = __ldg(a.chunks + c);
             const int fr = (packed >> 16) / a.ntiles;  // frame of the chunk
             const int tp = __ldg(a.tiles + (packed >> 16) - fr * a.ntiles);
@@ -703,10 +701,6 @@ __global__ void __launch_bounds__(kSymThreads, PK_SYM_MINB) bp_sym_f32_kernel(Bp
                     sx, sy, __uint_as_float(dst0 - 8u * (uint32_t)lo - 8u * kTwo23Bits), 0.f);
             const uint32_t nact = __popc(__ballot_sync(0xffffffffu, act));
             const size_t src_row = (size_t)__ldg(a.loc + sym_sensor(g, __ldg(a.gid + mm), a.Mall)) * a.TS + lo;
-            if (c == c0) {
-                griddep_wait();
-                if (a.st && a.st->all_stopped) return;
-            }
             __syncwarp();
             if (lane == 0) mbar_expect_tx(full_s + 8 * b, nact * (uint32_t)(a.L * 8));
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -720,9 +714,6 @@ __global__ void __launch_bounds__(kSymThreads, PK_SYM_MINB) bp_sym_f32_kernel(Bp
     }
 
     // ---- consumer warps
-    griddep_wait();
-    BP_T(2, clock64());
-    if (a.st && a.st->all_stopped) return;
     int lx, ly;
     sym_lane_xy(lane, a.lanemap, lx, ly);
     float acc[4][8];
@@ -788,7 +779,6 @@ __global__ void __launch_bounds__(kSymThreads, PK_SYM_MINB) bp_sym_f32_kernel(Bp
 #endif
         if (diag) sym_chunk<4, IW>(acc, px, py, sc, ns, img_stride, a.qclamp);
         else sym_chunk<8, IW>(acc, px, py, sc, ns, img_stride, a.qclamp);
-        __syncwarp();
 #if PK_BP_TRACE
         if (threadIdx.x == 0 && c - c0 < 64) {
             float s = 0.f;  // (a dependency on the accumulators, so the clock reads after them)
@@ -797,7 +787,10 @@ __global__ void __launch_bounds__(kSymThreads, PK_SYM_MINB) bp_sym_f32_kernel(Bp
             g_bp_chunk_clk[blockIdx.x][c - c0] = (int)(clock64() - tc0) + (s == 12345.f ? 1 : 0);
         }
 #endif
-        if (lane == 0) mbar_arrive(empty_s + 8 * b);
+        // every thread releases the buffer after its own reads of it (release semantics per
+        // thread: the producer's acquire then orders its refill after all of them, without
+        // relying on a warp barrier before a single arrival)
+        mbar_arrive(empty_s + 8 * b);
         if (++b == a.nbuf) { b = 0; phase ^= 1u; }
     }
     BP_T(5, clock64());

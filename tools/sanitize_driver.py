@@ -30,6 +30,14 @@ for pool in (F32, F64):
     res = pk.iterative_reconstruct(K, y, cfg, pool=pool)  # graph replay
     op.profile_iterations(y.values, pk.solver.solver_params(cfg, cfg.alpha, cfg.beta, cfg.step))
     print(pool.dtype, "iterations", res.iterations_run)
+# batched symmetric plan (2 frames per launch): frame-major chunks, segments, residual CTAs
+opb = pk.operator_for(g, ring, ac, F32, frames=2)
+pb = pk.solver.solver_params(cfg, cfg.alpha, cfg.beta, cfg.step)
+yb = np.concatenate([y.values, 0.5 * y.values])
+for _ in range(2):
+    opb.reconstruct(yb, pb)
+torch.cuda.synchronize()
+print("batched symmetric flags", opb.info.symmetric, "frames", opb.info.frames)
 # generic (non-symmetric) kernels: off-centre ring
 g2 = pk.make_grid(48, 40, 1e-4, (-2.4e-3, -2.0e-3))
 ring2 = pk.make_ring(24, 6e-3, (0.3e-3, -0.2e-3), g2)
