@@ -1685,7 +1685,10 @@ int freq_setup(pk_plan* p, int q_n, FreqArgs& a, int& zblocks) {
     a.cdt = p->cdt;
     a.c = p->c;
     a.kscale = 2.0 * 3.141592653589793 / ((double)p->Q * p->dt * p->c);  // AcousticConfig.k_values
-    zblocks = (q_n + kFreqThreads * kFreqRun - 1) / (kFreqThreads * kFreqRun);
+    // fp32: freq_fwd_f32_kernel, 32 lanes x R wavenumbers per CTA (R = 32 above q_n = 512,
+    // else 16); fp64: freq_fwd_kernel, 128 threads x kFreqRun
+    const int span = p->dtype == PK_F32 ? 32 * (q_n > 512 ? 32 : 16) : kFreqThreads * kFreqRun;
+    zblocks = (q_n + span - 1) / span;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
     a.chunks = std::max(1, std::min(64, (4 * sms + p->M * zblocks - 1) / (p->M * zblocks)));
@@ -1714,7 +1717,8 @@ int pk_freq_matvec(pk_plan* p, int32_t q_n, const void* x, void* y, void* stream
     const dim3 grid(p->M, a.chunks, zb);
     const int sb = (int)std::min<size_t>(148 * 8, ((size_t)p->M * q_n + kThreads - 1) / kThreads);
     if (p->dtype == PK_F32) {
-        freq_fwd_kernel<float><<<grid, kFreqThreads, 0, s>>>(a);
+        if (q_n > 512) freq_fwd_f32_kernel<32><<<grid, 128, 0, s>>>(a);
+        else freq_fwd_f32_kernel<16><<<grid, 128, 0, s>>>(a);
         freq_fwd_sum_kernel<float><<<sb, kThreads, 0, s>>>(a);
     } else {
         freq_fwd_kernel<double><<<grid, kFreqThreads, 0, s>>>(a);
