@@ -1080,7 +1080,9 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                         bool first = true;
                         while (pos < R) {
                             if (!first) {
-                                if (budget <= cs) break;
+                                // a further segment only if it gets at least cs / 2 rows (a
+                                // sliver of a segment pays the whole staging for a few rows)
+                                if (budget < cs + std::max(1LL, cs / 2)) break;
                                 budget -= cs;
                             }
                             const long long send = std::min({(pos / hq + 1) * hq, pos + hs, R});
