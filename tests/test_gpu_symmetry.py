@@ -254,3 +254,36 @@ def test_projector_window_variants_match_oracle(monkeypatch, oracle, lw, t):
     x = ph.values + 0.05 * rng.random(g.size)
     assert rel(op.matvec(x).double().cpu().numpy(), o.forward(x)) <= 5e-5
     pk.clear_plan_cache()
+
+
+def test_tuned_chunk_ranges_agree(monkeypatch, oracle):
+    """The back-projector's diagonal cut weight is timed once per geometry and process: a
+    second plan of the same geometry reuses the choice (bitwise equal solves), and pinned
+    weights (PK_SYM_WDIAG) at both ends of the candidate range give the same image to fp32
+    rounding and the oracle's to 1e-4."""
+    n, M, Q, N = 128, 128, 1024, 6
+    g, ring, ac, ph = pk.make_scene(n, M, Q, seed=3)
+    K = pk.build_time_matrix(g, ring, ac)
+    o = oracle.Operator.of(oracle.make_scene(n, M, Q, 3))
+    y = o.forward(ph.values)
+    alpha, beta = oracle.resolve_regularization(o, y)
+    step = oracle.resolve_step(o, beta, 1e-3)
+    ref = oracle.reconstruct(o, y, alpha, beta, step, N)["image"]
+    cfg = pk.ReconConfig(alpha, beta, N, step)
+    sd = pk.SensorData("time", M, Q, y)
+    pk.clear_plan_cache()
+    a = pk.iterative_reconstruct(K, sd, cfg, pool=F32)
+    split_a = pk.operator_for(g, ring, ac, F32).info.bp_split
+    pk.clear_plan_cache()
+    b = pk.iterative_reconstruct(K, sd, cfg, pool=F32)
+    assert pk.operator_for(g, ring, ac, F32).info.bp_split == split_a
+    assert np.array_equal(a.image.values, b.image.values)
+    imgs = []
+    for w in ("18", "26"):
+        monkeypatch.setenv("PK_SYM_WDIAG", w)
+        pk.clear_plan_cache()
+        imgs.append(pk.iterative_reconstruct(K, sd, cfg, pool=F32).image.values)
+    pk.clear_plan_cache()
+    assert rel(imgs[0], imgs[1]) <= 1e-5
+    for im in imgs + [a.image.values]:
+        assert rel(im, ref) <= 1e-4
