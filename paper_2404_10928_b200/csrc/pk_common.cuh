@@ -42,6 +42,8 @@ struct FrameState {
     int32_t stopped;
     int32_t stopped_by;
     int32_t grow;
+    uint32_t mxw;      // max |x'| of the symmetric epilogue's CTAs as float bits (atomicMax of
+                       //   non-negative floats; reset by the residual kernel and init)
 };
 
 struct DevState {

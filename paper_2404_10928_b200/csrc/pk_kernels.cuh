@@ -613,6 +613,7 @@ __device__ __forceinline__ void sym_epi_units(const BpSymEpiArgs& a, int t, int 
 #pragma unroll
         for (int w = 1; w < 8; ++w) m = fmaxf(m, red[tid * 8 + w]);
         a.part_mx[t * 32 + u0 + tid] = m;
+        if (m > 0.f) atomicMax(&a.st->fr[t / a.ntiles].mxw, __float_as_uint(m));
     }
     sync();  // the scratch is reused by the next claim
 }
@@ -972,7 +973,12 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
     griddep_launch_dependents();
     mx = block_max(mx, red_f);
     if (DEFER) {  // sum |x'| and the non-finite count are taken by the residual kernel
-        if (threadIdx.x == 0) a.part_mx[blockIdx.x] = mx;
+        if (threadIdx.x == 0) {
+            a.part_mx[blockIdx.x] = mx;
+            // (NaN skipped as fmaxf over the partials does; non-finite iterates are caught by
+            // the residual kernel's count)
+            if (mx > 0.f) atomicMax(&a.st->fr[fr].mxw, __float_as_uint(mx));
+        }
         return;
     }
     const float l1b = block_sum(l1, red_f);
@@ -1603,10 +1609,10 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
     // or the plan state.  Ends with a barrier.
     auto reduce_scale = [&](int fr, int k) {
         if (a.part_mx) {
-            __shared__ float red_f[NW];
-            float mx = 0.f;
-            for (int q = threadIdx.x; q < a.nmx; q += NT) mx = fmaxf(mx, __ldcg(a.part_mx + (size_t)fr * a.nmx + q));
-            mx = block_max<float, NT>(mx, red_f);
+            // the epilogue's CTAs atomicMax their max |x'| into one word per frame (equal to
+            // the maximum over its partials, part_mx, which the round-2b projector reduced here)
+            const float mx = __uint_as_float(__ldcg(&a.st->fr[fr].mxw));
+            __syncthreads();  // (callers rely on a barrier: the windows are initialised)
             const double scl = (mx > 0.f && isfinite(mx)) ? ldexp(1.0, a.bits) / (double)mx : 0.0;
             scale = (float)scl;
             if (k == __ldg(a.rec + fr) && threadIdx.x == 0 && !a.st->fr[fr].stopped) {
@@ -1799,6 +1805,7 @@ __global__ void __launch_bounds__(NW * 32, 32 / NW) fp_sym_f32_kernel(FpSymArgs 
             if (g0 + NGR >= 4 && threadIdx.x == 0) piece_s[(k + 1) & 1] = NW;  // next segment's claims
             fence_proxy_async_smem();
             __syncthreads();
+            if (g0 == 0) FS_T(4 + 8 * (k - k0) + 6);  // (transposed; the bulk issue follows)
             if (threadIdx.x < NGR * 32) {
                 const int gl = threadIdx.x >> 5, l = threadIdx.x & 31;
                 const int gi = g0 + gl;
@@ -2262,6 +2269,7 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
     };
     if (G <= 2) load_y();
     griddep_wait();  // the projection's accumulator and scale
+    if (a.solver && blockIdx.x == 0 && tid == 0) a.st->fr[f].mxw = 0u;  // (read by the projector: done)
     if (G > 2) load_y();
     int4 v4[G];
     int32_t vp[G];
@@ -2387,6 +2395,7 @@ __global__ void init_kernel(T* xb0, int P, DevState* st, const DevIo* io) {
             fs.stopped_by = PK_STOP_MAX_ITERATIONS;
             fs.grow = 0;
             fs.nonfinite = 0;
+            fs.mxw = 0u;
             io->status[2 * g] = 0;
             io->status[2 * g + 1] = PK_STOP_MAX_ITERATIONS;
         }
