@@ -131,10 +131,15 @@ def _scene(grid_size, sensors, samples, seed, config, device):
 
 
 def bench_recon(grid_size: int, sensors: int, samples: int, config: ReconConfig, reps: int = 5,
-                seed: int = 0, device: int = 0, reference=None) -> BenchReport:
+                seed: int = 0, workers: int | None = None, device: int = 0,
+                reference=None) -> BenchReport:
     """Back-projection against iterative reconstruction on one scene (bench.py:206-288), on
-    the device: entries back_projection (fp32), iterative_device_f64 (the fp64 validation
-    solver) and iterative_device (fp32, verified against the fp64 solver).
+    the device, with the reference's entry labels: back_projection (fp32), iterative_serial
+    (the reference's serial fp64 baseline role: the fp64 validation solver) and
+    iterative_parallel (the candidate: the fp32 production solver, verified against the fp64
+    one at 1e-4 relative L2 -- the reference verifies its parallel kernels at 1e-12, fp64
+    against fp64).  ``workers`` is accepted for the reference's signature (its WorkerPool
+    size); the device path has no worker count and records it in the environment only.
 
     ``reference``, optional, plays the reference's serial kernels (bench.py:230-235): a
     callable ``reference(K, y, config) -> image values`` run once on the same scene with the
@@ -163,7 +168,7 @@ def bench_recon(grid_size: int, sensors: int, samples: int, config: ReconConfig,
         environment=_environment(device, grid=[grid_size, grid_size], sensors=sensors,
                                  samples=samples, matrix_shape=[K.rows, K.cols],
                                  scalar_kind="real32 (verified against real64)",
-                                 iterations=config.iterations),
+                                 iterations=config.iterations, workers=workers),
         metrics={"rmse_bp": norm_rmse(bp.values), "rmse_ir": norm_rmse(ir32.image.values),
                  "rel_l2_f32_vs_f64": dev, "reference_times": REFERENCE_TIMES})
     ok64 = None
@@ -177,10 +182,12 @@ def bench_recon(grid_size: int, sensors: int, samples: int, config: ReconConfig,
         rep.metrics.update({"rel_l2_f64_vs_reference": e64, "rel_l2_f32_vs_reference": e32})
         rep.entries.append(BenchEntry("iterative_reference", t_ref, 1, _sha(ref_img)))
     rep.entries += [BenchEntry("back_projection", t_bp, reps, _sha(bp.values)),
-                    BenchEntry("iterative_device_f64", t_64, reps, _sha(ir64.image.values), ok64),
-                    BenchEntry("iterative_device", t_32, reps, _sha(ir32.image.values), ok32)]
-    for base, cand, tb, tc in (("back_projection", "iterative_device", t_bp, t_32),
-                               ("iterative_device_f64", "iterative_device", t_64, t_32)):
+                    BenchEntry("iterative_serial", t_64, reps, _sha(ir64.image.values), ok64),
+                    BenchEntry("iterative_parallel", t_32, reps, _sha(ir32.image.values), ok32)]
+    rep.metrics["entry_roles"] = {"iterative_serial": "fp64 device solver",
+                                  "iterative_parallel": "fp32 device solver"}
+    for base, cand, tb, tc in (("back_projection", "iterative_serial", t_bp, t_64),
+                               ("iterative_serial", "iterative_parallel", t_64, t_32)):
         rep.speedups.append({"baseline": base, "candidate": cand, "speedup": tb / tc,
                              "below_measurement_floor": min(tb, tc) < MEASUREMENT_FLOOR_SECONDS})
     rep.metrics["ir_over_bp_time_ratio"] = t_32 / t_bp
@@ -188,7 +195,7 @@ def bench_recon(grid_size: int, sensors: int, samples: int, config: ReconConfig,
 
 
 def profile_breakdown(grid_size: int, sensors: int, samples: int, config: ReconConfig,
-                      seed: int = 0, device: int = 0) -> BenchReport:
+                      seed: int = 0, workers: int | None = None, device: int = 0) -> BenchReport:
     """Attribute one iterative run's time to its stages (bench.py:291-340), on the device.
 
     The total is the wall time of the public ``iterative_reconstruct`` call (best of 3: host
@@ -223,7 +230,8 @@ def profile_breakdown(grid_size: int, sensors: int, samples: int, config: ReconC
         scenario=f"profile {grid_size}x{grid_size}, {sensors} sensors, {samples} samples",
         environment=_environment(device, grid=[grid_size, grid_size], sensors=sensors,
                                  samples=samples, matrix_shape=[K.rows, K.cols],
-                                 scalar_kind="real32", iterations=config.iterations),
+                                 scalar_kind="real32", iterations=config.iterations,
+                                 workers=workers),
         breakdown={k: {"seconds": v, "percent": 100.0 * v / denom} for k, v in secs.items()},
         metrics={"iterations_run": result.iterations_run, "stopped_by": result.stopped_by,
                  "kernel_launches": launches, "back_projection_seconds": k1,

@@ -32,12 +32,12 @@ def test_report_type_cpu():
 @pytest.mark.gpu
 def test_bench_recon_device():
     rep = pk.bench_recon(64, 32, 128, pk.ReconConfig(iterations=10), reps=2)
-    assert [e.label for e in rep.entries] == ["back_projection", "iterative_device_f64",
-                                              "iterative_device"]
+    assert [e.label for e in rep.entries] == ["back_projection", "iterative_serial",
+                                              "iterative_parallel"]
     assert rep.verification_ok(), rep.metrics
     assert rep.metrics["rel_l2_f32_vs_f64"] <= 1e-4
     assert all(len(e.checksum) == 64 and e.wall_seconds > 0 for e in rep.entries)
-    assert rep.speedup("iterative_device_f64", "iterative_device") > 0
+    assert rep.speedup("iterative_serial", "iterative_parallel") > 0
     assert 0.0 <= rep.metrics["rmse_ir"] < rep.metrics["rmse_bp"]  # IR beats BP (bench.py:243)
 
 
@@ -64,9 +64,9 @@ def test_bench_recon_verified_against_oracle(oracle):
 
     rep = pk.bench_recon(64, 32, 128, pk.ReconConfig(iterations=10), reps=1, reference=ref)
     assert [e.label for e in rep.entries] == ["iterative_reference", "back_projection",
-                                              "iterative_device_f64", "iterative_device"]
+                                              "iterative_serial", "iterative_parallel"]
     assert rep.verification_ok(), rep.metrics
-    assert rep.entry("iterative_device_f64").verification is True
+    assert rep.entry("iterative_serial").verification is True
     assert rep.metrics["rel_l2_f64_vs_reference"] <= 1e-10
     assert rep.metrics["rel_l2_f32_vs_reference"] <= 1e-4
 

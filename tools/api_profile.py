@@ -30,7 +30,7 @@ print("ir f32 ms", t(lambda: pk.iterative_reconstruct(K, y, cfg, pool=f32)))
 
 if len(sys.argv) > 4:  # the harness in the same process, then the direct calls again
     rep = pk.bench_recon(n, M, Q, pk.ReconConfig(iterations=10), reps=5)
-    print("harness iterative_device ms", rep.entry("iterative_device").wall_seconds * 1e3)
+    print("harness iterative_parallel (fp32) ms", rep.entry("iterative_parallel").wall_seconds * 1e3)
     print("ir f32 ms", t(lambda: pk.iterative_reconstruct(K, y, cfg, pool=f32)))
     g2, r2, a2, p2, K2, y2, c2 = _scene(n, M, Q, 0, pk.ReconConfig(iterations=10), 0)
     print("ir f32 (new scene objects) ms", t(lambda: pk.iterative_reconstruct(K2, y2, c2, pool=f32)))
