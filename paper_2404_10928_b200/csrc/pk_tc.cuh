@@ -32,6 +32,11 @@
 
 namespace pk {
 
+#ifndef PK_TC_RAWHI
+// 1: the MMAs read the raw fp32 A tile as its tf32 hi part (kind::tf32 ignores the low 13
+// mantissa bits), so the split warps only write the lo part
+#define PK_TC_RAWHI 1
+#endif
 constexpr int kTcBM = 128;      // rows per CTA (UMMA M)
 constexpr int kTcBK = 32;       // fp32 per 128-B swizzle row (one TMA box row)
 constexpr int kTcLo = 2;        // A lo-part ring depth
@@ -139,7 +144,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     const int nkb = (Kd + kTcBK - 1) / kTcBK;
     const int kb0 = (int)((long long)nkb * blockIdx.y / splits), kb1 = (int)((long long)nkb * (blockIdx.y + 1) / splits);
     const int nk = kb1 - kb0, nch = (nk + kTcChunk - 1) / kTcChunk;
-    constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : (2 * N <= 64 ? 64 : (2 * N <= 128 ? 128 : 256));
+    // two chunk buffers of 2N columns: [0, N) = A_hi (B_hi) + A_lo B_hi, [N, 2N) = A_hi B_lo
+    constexpr int TMEM_COLS = 4 * N;
+    static_assert(TMEM_COLS == 128 || TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM allocation: power of 2");
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < HI; ++s) {
@@ -177,20 +184,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         }
     } else if (warp == 1) {
         if (lane == 0) {  // MMA issuer
-            constexpr uint32_t idesc = tc_idesc(N);
+            constexpr uint32_t idesc = tc_idesc(N), idesc2 = tc_idesc(2 * N);
             for (int i = 0; i < nk; ++i) {
                 const int s = i % HI, l = i % kTcLo, ch = i / kTcChunk, buf = ch & 1;
                 if (i % kTcChunk == 0 && ch >= 2) mbar_wait(cfree0 + 8 * buf, ((ch / 2) - 1) & 1);
                 mbar_wait(split0 + 8 * s, (i / HI) & 1);
                 tc_fence_after();
-                const uint32_t d = tmem + (uint32_t)(buf * N);
+                const uint32_t d = tmem + (uint32_t)(buf * 2 * N);
                 const uint32_t ah = smem_u32(a_hi(s)), al = smem_u32(a_lo(l));
-                const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
+                const uint32_t bh = smem_u32(b_hi(s));
 #pragma unroll
                 for (int k = 0; k < kTcBK / 8; ++k) {  // K 8 tf32 = 32 B per MMA
                     const uint32_t o = 32u * k;
-                    tc_mma(d, tc_desc(ah + o), tc_desc(bh + o), idesc, (i % kTcChunk > 0 || k > 0) ? 1u : 0u);
-                    tc_mma(d, tc_desc(ah + o), tc_desc(bl + o), idesc, 1u);
+                    // A_hi against B_hi and B_lo in one MMA of N' = 2N (the two frame tiles are
+                    // adjacent 128-B-swizzled row blocks of the stage): A_hi is read once
+                    tc_mma(d, tc_desc(ah + o), tc_desc(bh + o), idesc2, (i % kTcChunk > 0 || k > 0) ? 1u : 0u);
                     tc_mma(d, tc_desc(al + o), tc_desc(bh + o), idesc, 1u);
                 }
                 tc_commit(empty0 + 8 * s);  // stage s and A lo stage l are free after these MMAs
@@ -213,10 +221,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
             tc_fence_after();
 #pragma unroll
             for (int n0 = 0; n0 < NH; n0 += 16) {
-                float v[16];
-                tc_ld16(tmem + ((uint32_t)(32 * sub) << 16) + (uint32_t)(buf * N + half * NH + n0), v);
+                float v[16], w[16];
+                const uint32_t col = tmem + ((uint32_t)(32 * sub) << 16) + (uint32_t)(buf * 2 * N + half * NH + n0);
+                tc_ld16(col, v);          // A_hi B_hi + A_lo B_hi
+                tc_ld16(col + N, w);      // A_hi B_lo
 #pragma unroll
-                for (int j = 0; j < 16; ++j) acc[n0 + j] += v[j];
+                for (int j = 0; j < 16; ++j) acc[n0 + j] += v[j] + w[j];
             }
             tc_fence_before();
             __syncwarp();
@@ -238,7 +248,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 q.y = __uint_as_float(v.y) - __uint_as_float(h.y);
                 q.z = __uint_as_float(v.z) - __uint_as_float(h.z);
                 q.w = __uint_as_float(v.w) - __uint_as_float(h.w);
+#if !PK_TC_RAWHI
                 *reinterpret_cast<uint4*>(hi + o) = h;
+#endif
                 *reinterpret_cast<float4*>(lo + o) = q;
             }
             fence_proxy_async_smem();  // generic writes -> the tensor cores' (async proxy) reads
