@@ -2025,6 +2025,8 @@ template <typename R>
 int launch_gemv(pk_dense* d, const void* x0, const void* x1, int xc, const void* yobs, void* out0,
                 void* out1, double* part, const DenseState* st, cudaStream_t s) {
     const R* K = static_cast<const R*>(d->K);
+    if (!d->cplx && !xc && ((reinterpret_cast<uintptr_t>(x0) | reinterpret_cast<uintptr_t>(x1)) & 15))
+        return fail(PK_ERR_INVALID, "x must be 16-byte aligned (read in 16-byte vectors)");
 #define PK_GEMV(KC, XC)                                                                        \
     dense_gemv_kernel<R, KC, XC><<<d->gemv_grid, kDenseThreads, 0, s>>>(                     \
         K, d->rows, d->cols, static_cast<const R*>(x0), static_cast<const R*>(x1),           \

@@ -31,6 +31,18 @@ struct DVec {
     static constexpr int E = 16 / (int)(sizeof(R) * (C ? 2 : 1));
 };
 
+// 16 B of x (re-read by every row: cached, read-only path)
+template <typename R>
+__device__ __forceinline__ void ldx16(const R* p, R (&o)[16 / sizeof(R)]) {
+    if constexpr (sizeof(R) == 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    } else {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+        o[0] = v.x; o[1] = v.y;
+    }
+}
+
 template <typename R>
 __device__ __forceinline__ void ld16(const R* p, R (&o)[16 / sizeof(R)]) {
     if constexpr (sizeof(R) == 4) {
@@ -79,6 +91,13 @@ __global__ void __launch_bounds__(kDenseThreads) dense_gemv_kernel(
           R b[NU][W];
 #pragma unroll
           for (int u = 0; u < NU; ++u) ld16(row + (v0 + 32 * u) * W, b[u]);
+          // real K and x: x in the same 16-B vectors as the row (one L1 wavefront per 32
+          // lanes x 16 B instead of four scalar loads at a 16-B stride)
+          R xv[NU][W];
+          if constexpr (!KC && !XC) {
+#pragma unroll
+            for (int u = 0; u < NU; ++u) ldx16(x + (v0 + 32 * u) * W, xv[u]);
+          }
 #pragma unroll
           for (int u = 0; u < NU; ++u) {
             const int64_t v = v0 + 32 * u;
@@ -87,7 +106,7 @@ __global__ void __launch_bounds__(kDenseThreads) dense_gemv_kernel(
             for (int e = 0; e < E; ++e) {
                 const int64_t c = v * E + e;
                 if constexpr (!KC && !XC) {
-                    sr = fma(a[e], __ldg(x + c), sr);
+                    sr = fma(a[e], xv[u][e], sr);
                 } else if constexpr (!KC && XC) {
                     sr = fma(a[e], __ldg(x + 2 * c), sr);
                     si = fma(a[e], __ldg(x + 2 * c + 1), si);
