@@ -1680,6 +1680,11 @@ int pk_reconstruct_host(pk_plan* p, const pk_solver_params* prm, const double* y
 // frequency-domain operator (build_freq_matrix, forward.py:218-234), matrix-free
 
 namespace {
+// wavenumbers per lane of the fp32 forward (PK_FREQ_R: 16 or 32 for sweeps)
+int freq_run(int q_n) {
+    if (const char* e = getenv("PK_FREQ_R")) return atoi(e) == 16 ? 16 : 32;
+    return q_n > 512 ? 32 : 16;
+}
 int freq_setup(pk_plan* p, int q_n, FreqArgs& a, int& zblocks) {
     if (q_n < 1) return fail(PK_ERR_INVALID, "q_n must be >= 1");
     a.px = p->px; a.py = p->py; a.sx = p->sx; a.sy = p->sy;
@@ -1689,7 +1694,7 @@ int freq_setup(pk_plan* p, int q_n, FreqArgs& a, int& zblocks) {
     a.kscale = 2.0 * 3.141592653589793 / ((double)p->Q * p->dt * p->c);  // AcousticConfig.k_values
     // fp32: freq_fwd_f32_kernel, 32 lanes x R wavenumbers per CTA (R = 32 above q_n = 512,
     // else 16); fp64: freq_fwd_kernel, 128 threads x kFreqRun
-    const int span = p->dtype == PK_F32 ? 32 * (q_n > 512 ? 32 : 16) : kFreqThreads * kFreqRun;
+    const int span = p->dtype == PK_F32 ? 32 * freq_run(q_n) : kFreqThreads * kFreqRun;
     zblocks = (q_n + span - 1) / span;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
@@ -1719,7 +1724,7 @@ int pk_freq_matvec(pk_plan* p, int32_t q_n, const void* x, void* y, void* stream
     const dim3 grid(p->M, a.chunks, zb);
     const int sb = (int)std::min<size_t>(148 * 8, ((size_t)p->M * q_n + kThreads - 1) / kThreads);
     if (p->dtype == PK_F32) {
-        if (q_n > 512) freq_fwd_f32_kernel<32><<<grid, 128, 0, s>>>(a);
+        if (freq_run(q_n) == 32) freq_fwd_f32_kernel<32><<<grid, 128, 0, s>>>(a);
         else freq_fwd_f32_kernel<16><<<grid, 128, 0, s>>>(a);
         freq_fwd_sum_kernel<float><<<sb, kThreads, 0, s>>>(a);
     } else {
