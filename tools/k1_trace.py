@@ -74,6 +74,8 @@ cap = 1 << 20
 chunks = np.zeros(cap, np.int32); c0 = np.zeros(cap, np.int32); tiles = np.zeros(cap, np.int32)
 lib.pk_debug_bp_plan.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
 nch = lib.pk_debug_bp_plan(op.handle, chunks.ctypes.data, c0.ctypes.data, tiles.ctypes.data, cap)
+qt = (cfg.n // 2 + 31) // 32
+ntiles = qt * (qt + 1) // 2
 recs = []
 for cta in range(len(rows)):
     a0, a1 = c0[cta], c0[cta + 1]
@@ -81,7 +83,7 @@ for cta in range(len(rows)):
         if c == a0:
             continue  # (the first chunk includes the pipeline fill)
         t = chunks[c] >> 16; k = chunks[c] & 0xffff
-        tp = tiles[t % max(1, len(set(tiles[:4096]))) if False else t]
+        tp = tiles[t % ntiles]
         tx, ty = tp >> 16, tp & 0xffff
         recs.append((cc[cta, c - a0], tx, ty, k))
 recs = np.array(recs)
@@ -98,3 +100,15 @@ for lo_ in range(0, 360, 45):
     sel = (ang >= lo_) & (ang < lo_ + 45)
     if sel.any():
         print(f"  sensor angle {lo_:3d}-{lo_ + 45:3d}: us per chunk {off[sel, 0].mean() * us:.3f}")
+
+# per tile (off-diagonal and diagonal) mean cost, and per sensor angle (16 bins) per tile class
+print("per tile: (tx, ty) us per chunk")
+for (tx, ty) in sorted(set((int(r[1]), int(r[2])) for r in recs)):
+    sel = (recs[:, 1] == tx) & (recs[:, 2] == ty)
+    print(f"  ({tx},{ty}) {recs[sel, 0].mean() * us:.3f} (n {sel.sum()})")
+for name, sel0 in (("off-diagonal", ~diag), ("diagonal", diag)):
+    r = recs[sel0]
+    ang = (r[:, 3] * 2 / M * 360.0)
+    line = " ".join(f"{r[(ang >= a0) & (ang < a0 + 22.5), 0].mean() * us:.2f}" if ((ang >= a0) & (ang < a0 + 22.5)).any() else "-"
+                    for a0 in np.arange(0, 360, 22.5))
+    print(f"{name} by sensor angle (22.5 deg bins): {line}")

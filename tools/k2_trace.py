@@ -62,12 +62,10 @@ for c in range(a.ctas):
         b = 4 + 8 * k
         st, wmin, wmax, bar = t[b], t[b + 1], t[b + 2], t[b + 3]
         rounds = [x for x in t[b + 4:b + 6] if x > 0 and x >= bar]
-        if k + 1 < nseg and t[b + 6] > 0:
-            tot_w = tot_extra.setdefault("bulk_wait", 0.0)
-            tot_extra["bulk_wait"] = tot_w + (t[b + 6] - rounds[-1]) * us
-            tot_extra["bar_after_wait"] = tot_extra.get("bar_after_wait", 0.0) + (t[b + 7] - t[b + 6]) * us
-            tot_extra["init"] = tot_extra.get("init", 0.0) + (t[b + 8] - t[b + 7]) * us
-            tot_extra["n"] = tot_extra.get("n", 0) + 1
+        if t[b + 6] > 0 and t[b + 6] >= bar and rounds:
+            tot_extra["transpose0"] = tot_extra.get("transpose0", 0.0) + (t[b + 6] - bar) * us
+            tot_extra["issue0"] = tot_extra.get("issue0", 0.0) + (rounds[0] - t[b + 6]) * us
+            tot_extra["nt"] = tot_extra.get("nt", 0) + 1
         if len(rounds) == 2:
             tot_extra["round0"] = tot_extra.get("round0", 0.0) + (rounds[0] - bar) * us
             tot_extra["round1"] = tot_extra.get("round1", 0.0) + (rounds[1] - rounds[0]) * us
@@ -98,9 +96,9 @@ for r in rows:
     tot["post"] = tot.get("post", 0.0) + r["post"]
 for key, v in tot.items():
     print(f"  {key:14s} per CTA {v / len(rows):7.2f} us")
-if tot_extra.get("n"):
-    print("segment boundary (per boundary): bulk wait %.2f  barrier %.2f  init+barrier %.2f us" % (
-        tot_extra["bulk_wait"] / tot_extra["n"], tot_extra["bar_after_wait"] / tot_extra["n"], tot_extra["init"] / tot_extra["n"]))
+if tot_extra.get("nt"):
+    print("round 0 (per segment): transposition + fence + barrier %.2f  bulk issue %.2f us" % (
+        tot_extra["transpose0"] / tot_extra["nt"], tot_extra["issue0"] / tot_extra["nt"]))
 if tot_extra.get("nr"):
     print("staging rounds (per segment): round0 %.2f  round1 %.2f us" % (tot_extra["round0"] / tot_extra["nr"], tot_extra["round1"] / tot_extra["nr"]))
 order = np.argsort(ends)
