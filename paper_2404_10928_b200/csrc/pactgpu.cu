@@ -1069,7 +1069,56 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             // staging and scatter ramp cost a CTA as much as ~cs rows (measured r02c, config 3:
             // 1-segment CTAs 47.8 us, 2-segment 56.5 us for the same rows).  Greedy fill per
             // budget, binary search on the budget.
-            auto balanced_cuts = [&](long long R, int hs, long long cs) {
+            // per (group, strip, start row): the most rows a segment starting there can have so
+            // that its rectangle's delays fit the window for every lane (fp64 distances from the
+            // lanes' own sensors: spread = farthest corner - nearest point, + 10 slots of margin
+            // for the window's alignment, the two interpolation slots and fp32 delays).  Round
+            // 2b used one height for all, from the rectangle's diagonal (the worst direction);
+            // a group whose sensors look along the strip gets much taller segments.  Heights are
+            // capped at hcap (the fixed-point bound of fp_bits); empty if a row cannot fit.
+            const double qcl = (double)p->Q + 1.5;
+            const bool clampd = p->max_delay >= (double)p->Q + 0.5;
+            auto make_hmax = [&](int T, int lw, int hcap) {
+                const int qt = (hq + T - 1) / T;
+                std::vector<int> tab((size_t)p->fsym_groups * qt * hq, 0);
+                for (int grp = 0; grp < p->fsym_groups; ++grp)
+                    for (int strip = 0; strip < qt; ++strip) {
+                        const int i0 = hq + T * strip, i1 = std::min(i0 + T, n) - 1;
+                        const double xa = std::min(X[i0], X[i1]) / p->cdt, xb = std::max(X[i0], X[i1]) / p->cdt;
+                        auto fits = [&](int r, int e) {  // rows [r, e) of the quadrant
+                            const double ya = std::min(Y[hq + r], Y[hq + e - 1]) / p->cdt;
+                            const double yb = std::max(Y[hq + r], Y[hq + e - 1]) / p->cdt;
+                            for (int l = 0; l < 32; ++l) {
+                                const int m = grp * 32 + l;
+                                if (m >= p->M) break;
+                                const double sx = SP[2 * m] / p->cdt, sy = SP[2 * m + 1] / p->cdt;
+                                const double cx = std::min(std::max(sx, xa), xb), cy = std::min(std::max(sy, ya), yb);
+                                double dmin = std::hypot(cx - sx, cy - sy);
+                                double dmax = std::max(std::max(std::hypot(xa - sx, ya - sy), std::hypot(xa - sx, yb - sy)),
+                                                       std::max(std::hypot(xb - sx, ya - sy), std::hypot(xb - sx, yb - sy)));
+                                if (clampd) { dmin = std::min(dmin, qcl); dmax = std::min(dmax, qcl); }
+                                if ((int)std::ceil(dmax - dmin) + 10 > lw) return false;
+                            }
+                            return true;
+                        };
+                        int e = 0;
+                        for (int r = 0; r < hq; ++r) {
+                            e = std::max(e, r);
+                            while (e < hq && e - r < hcap && fits(r, e + 1)) ++e;
+                            if (e == r) return std::vector<int>();  // not even one row fits
+                            tab[((size_t)grp * qt + strip) * hq + r] = e - r;
+                        }
+                    }
+                return tab;
+            };
+            std::vector<int> hm_tab;  // the table segment() and balanced_cuts() cut with
+            int hm_qt = 1;
+            auto hm_at = [&](long long pos) -> long long {
+                const long long gs = pos / hq;
+                const int grp = (int)((gs / hm_qt) % p->fsym_groups), strip = (int)(gs % hm_qt);
+                return hm_tab[((size_t)grp * hm_qt + strip) * hq + (pos - gs * hq)];
+            };
+            auto balanced_cuts = [&](long long R, long long cs) {
                 auto fill = [&](long long B, std::vector<long long>* cut) {
                     long long pos = 0;
                     int used = 0;
@@ -1085,7 +1134,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                                 if (budget < cs + std::max(1LL, cs / 2)) break;
                                 budget -= cs;
                             }
-                            const long long send = std::min({(pos / hq + 1) * hq, pos + hs, R});
+                            const long long send = std::min({(pos / hq + 1) * hq, pos + hm_at(pos), R});
                             const long long take = std::min(send - pos, budget);
                             pos += take;
                             budget -= take;
@@ -1096,7 +1145,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                     if (cut) { while ((int)cut->size() < G) cut->push_back(pos); cut->push_back(R); }
                     return pos >= R;
                 };
-                long long lo = std::max(1LL, (R + G - 1) / G), hi = lo + 2 * cs + hs + 1;
+                long long lo = std::max(1LL, (R + G - 1) / G), hi = lo + 2 * cs + hq + 1;
                 while (!fill(hi, nullptr)) hi *= 2;
                 while (lo < hi) {
                     const long long mid = (lo + hi) / 2;
@@ -1114,10 +1163,10 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                            : (long long)std::lround(7.5 / (T * 10.0 / 1965.0 * 1.15));
             };
             // (batched frames: the sequence is frame-major, segment group index f * groups + group)
-            auto segment = [&](int T, int hs, std::vector<int4>* sg, std::vector<int>* c0) {
+            auto segment = [&](int T, std::vector<int4>* sg, std::vector<int>* c0) {
                 const int qt = (hq + T - 1) / T;
                 const long long R = (long long)nf * p->fsym_groups * qt * hq;
-                const std::vector<long long> cut = balanced_cuts(R, hs, seg_cost(T));
+                const std::vector<long long> cut = balanced_cuts(R, seg_cost(T));
                 int cnt = 0;
                 std::vector<int> per_group(nf * p->fsym_groups, 0);
                 for (int c = 0; c < G; ++c) {
@@ -1126,7 +1175,7 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                     if (c0) c0->push_back(cnt);
                     while (r0 < r1) {
                         const long long gs = r0 / hq;
-                        const long long end = std::min({r1, (gs + 1) * hq, r0 + hs});
+                        const long long end = std::min({r1, (gs + 1) * hq, r0 + hm_at(r0)});
                         const int grp = (int)(gs / qt), strip = (int)(gs % qt);
                         if (sg) sg->push_back(make_int4(grp, strip, hq + (int)(r0 - gs * hq),
                                                         hq + (int)(end - gs * hq)));
@@ -1144,8 +1193,15 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             // cfg2 batched 4 frames T 32 / LW 256 48.9 us, T 64 / LW 320 55.2 us)
             const char* evt = getenv("PK_FSYM_T");
             const char* evl = getenv("PK_FSYM_LW");
-            struct Cand { int T, lw, hs, qt; long long words; int ngr; };
+            struct Cand { int T, lw, hs, qt; long long words; int ngr; std::vector<int> tab; };
             std::vector<Cand> cands;
+            // the fixed-point bound's contributions-per-slot estimate of a T x H rectangle (as
+            // the fp_bits rule below)
+            auto nc_of = [&](double T, double H) {
+                double nc = 1.5 * (std::hypot(T, H) + 2) * (2.0 / std::max(h, 1e-12) + 2);
+                if (p->min_delay < 8.0 * std::max(T, H) * std::max(h, 1.0)) nc = T * H;
+                return std::min(nc, T * H);
+            };
             for (int T : {64, 32}) {
                 if (evt && atoi(evt) != T) continue;
                 const int qt = (hq + T - 1) / T;
@@ -1161,8 +1217,17 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                     while (hs < hq && (int)std::ceil(region_diag(T, hs + 1)) + 9 <= lw) ++hs;
                     hs = std::min<long long>(hs, rows_per + seg_cost(T));  // (balanced ranges exceed R / G)
                     if (hs == 0) continue;
-                    cands.push_back({T, lw, hs, qt, (long long)segment(T, hs, nullptr, nullptr).first * lw,
-                                     fs_ngr(lw, nw, cap)});
+                    // direction-aware heights, capped where the fixed-point bound would lose a bit
+                    // against the uniform height's (PK_FSYM_UNIFORM=1: the uniform height)
+                    int hcap = hs;
+                    if (!getenv("PK_FSYM_UNIFORM") || atoi(getenv("PK_FSYM_UNIFORM")) == 0)
+                        while (hcap < hq && ceil_log2(nc_of(T, hcap + 1)) <= ceil_log2(nc_of(T, hs))) ++hcap;
+                    std::vector<int> tab = make_hmax(T, lw, hcap);
+                    if (tab.empty()) continue;
+                    hm_tab = tab;
+                    hm_qt = qt;
+                    cands.push_back({T, lw, hs, qt, (long long)segment(T, nullptr, nullptr).first * lw,
+                                     fs_ngr(lw, nw, cap), std::move(tab)});
                 }
             }
             const bool multi = std::any_of(cands.begin(), cands.end(), [](const Cand& c) { return c.ngr >= 2; });
@@ -1178,14 +1243,19 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
                 p->fsym_hs = c.hs;
                 p->fsym_smem = fs_smem(c.lw, nw, cap);
                 p->fsym_ngr = c.ngr;
+                hm_tab = c.tab;
+                hm_qt = c.qt;
             }
             if (p->fsym) {
                 p->fsym_nw = nw;
                 p->fsym_grid = G;
                 p->fsym_segs_h.clear();
                 p->fsym_cta_seg0_h.clear();
-                const auto sc = segment(p->fsym_T, p->fsym_hs, &p->fsym_segs_h, &p->fsym_cta_seg0_h);
+                const auto sc = segment(p->fsym_T, &p->fsym_segs_h, &p->fsym_cta_seg0_h);
                 p->fsym_nseg = sc.first;
+                // the tallest segment cut (the fixed-point bound below)
+                p->fsym_hs = 1;
+                for (const int4& q : p->fsym_segs_h) p->fsym_hs = std::max(p->fsym_hs, q.w - q.z);
                 // the CTA of each frame's first segment records the frame's fixed-point scale
                 p->fsym_rec_h.assign(nf, 0);
                 for (int k = p->fsym_nseg - 1; k >= 0; --k) p->fsym_rec_h[p->fsym_segs_h[k].x / p->fsym_groups] = k;
