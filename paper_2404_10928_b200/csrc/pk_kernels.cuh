@@ -2214,6 +2214,7 @@ __global__ void __launch_bounds__(kThreads, PK_FIN_MINB) finalize_kernel(FinArgs
 // entries past the groups are a short tail loop)
 constexpr int kFinSymG = 4;
 constexpr int kFinSymMax = 4 * kThreads * kFinSymG;  // 4096 samples
+constexpr int kFinSymB = 3;  // start-value words (uint2 = 4 samples) per thread held in registers
 template <int NF, int G>
 __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float> a) {
     __shared__ double red_d[kThreads / 32];
@@ -2267,10 +2268,23 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
         if (ym && s0 >= 1 && s0 - 1 < Q) yp[i] = __ldg(ym + s0 - 1);
     }
     };
-    if (G <= 2) load_y();
+    // the row's start values (geometry constants): loaded with the measurements, so the row
+    // reset after the sums' barrier is stores only (no further round trip at the CTA's tail)
+    const int nb4 = a.acc32_ld / 4;
+    const uint2* b4 = reinterpret_cast<const uint2*>(a.bias16 + (size_t)m * a.acc32_ld);
+    constexpr int B = G <= 2 ? kFinSymB : 0;  // (G = 4: no registers to spare; a loop at the tail)
+    uint2 bw[B > 0 ? B : 1];
+    auto load_b = [&]() {
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            const int q = tid + i * kThreads;
+            bw[i] = q < nb4 ? __ldg(b4 + q) : make_uint2(0u, 0u);
+        }
+    };
+    if (G <= 2) { load_y(); load_b(); }
     griddep_wait();  // the projection's accumulator and scale
     if (a.solver && blockIdx.x == 0 && tid == 0) a.st->fr[f].mxw = 0u;  // (read by the projector: done)
-    if (G > 2) load_y();
+    if (G > 2) { load_y(); load_b(); }
     int4 v4[G];
     int32_t vp[G];
 #pragma unroll
@@ -2314,11 +2328,13 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
         const float2 p3 = pair_entry<float>(rr[2], rr[3], s0 + 3, a.atrick);
         *reinterpret_cast<float4*>(tab + s0) = make_float4(p0.x, p0.y, p1.x, p1.y);  // (TS even)
         if (s0 + 2 < a.TS) *reinterpret_cast<float4*>(tab + s0 + 2) = make_float4(p2.x, p2.y, p3.x, p3.y);
-    }
-    // entries past the groups (e.g. Q = 2048: e = 2048, 2049)
-    for (int e = 4 * kThreads * G + tid; e < a.TS; e += kThreads) {
-        auto rat = [&](int s) { return (s >= 0 && s < Q) ? resid(__ldcg(accr + s), ym ? __ldg(ym + s) : 0.f) : 0.f; };
-        tab[e] = pair_entry<float>(rat(e - 1), rat(e), e, a.atrick);
+        // entries past the groups (e.g. Q = 2048: e = 2048, 2049): r[e] = 0 there (Q <= 4 *
+        // kThreads * G), so only e = Q = 4 * kThreads * G needs a sample -- r[Q - 1], held by
+        // the thread of the last group, which writes them all (no extra load round trip)
+        if (s0 + 4 == 4 * kThreads * G) {
+            const float rl = (s0 + 3 < Q) ? rr[3] : 0.f;
+            for (int e = s0 + 4; e < a.TS; ++e) tab[e] = pair_entry<float>(e == Q ? rl : 0.f, 0.f, e, a.atrick);
+        }
     }
     griddep_launch_dependents();
     if (a.tv_here) {
@@ -2337,8 +2353,12 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
     {   // (after the sums' barrier: every read of the row is done) reset the row, pads
         // included, to its start value for the next projection's reductions
         int4* row4 = reinterpret_cast<int4*>(accr - kAccFront);
-        const uint2* b4 = reinterpret_cast<const uint2*>(a.bias16 + (size_t)m * a.acc32_ld);
-        for (int q = tid; q < a.acc32_ld / 4; q += kThreads) row4[q] = bias_start4(__ldg(b4 + q));
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            const int q = tid + i * kThreads;
+            if (q < nb4) row4[q] = bias_start4(bw[i]);
+        }
+        for (int q = tid + B * kThreads; q < nb4; q += kThreads) row4[q] = bias_start4(__ldg(b4 + q));
     }
     if (!last_block(&a.st->cnt_fin, gridDim.x * gridDim.y, &last_flag)) return;
     finalize_objective<float, NF>(a, 1, data_s, tv_s, red_d);
