@@ -862,9 +862,12 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
     __shared__ int last_flag;
     __shared__ float4 part4[3][64];            // slot-group partials 1..3
     __shared__ float blk[8 * kSymTile];        // the strip in image g, row-major (bw x bh)
+    // state words issued together with the tile loads (one round trip; the stop test waits on
+    // it, then the iterate loads)
     int iter = 0;
+    bool all_st = false;
     if (EPI) {
-        if (a.st->all_stopped) return;
+        all_st = a.st->all_stopped;
         iter = a.st->iter;
     }
     // CTA = (tile, image g, strip k): the main kernel's consumer thread c holds, in slot
@@ -878,6 +881,10 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
     const int n = a.n, h = n >> 1;
     const int i0 = h + kSymTile * tx, j0 = h + kSymTile * ty;
     const int s0 = __ldg(a.tile_slot0 + t), s1 = __ldg(a.tile_slot0 + t + 1);
+    const bool fr_stopped = EPI ? (bool)a.st->fr[fr].stopped : true;
+    float beta_tv = 0.f, eps_tv = 0.f;
+    if (EPI) { beta_tv = (float)a.prm->beta[fr]; eps_tv = (float)a.prm->eps; }
+    if (all_st) return;
     // the strip's image under g is the block [bx, bx + bw) x [by, by + bh), bw * bh = 256
     int bx, by, bw;
     {
@@ -899,12 +906,11 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
         pix = (active && ig >= 0 && ig < n && jg >= 0 && jg < n) ? jg * n + ig : -1;
     }
     const float* x = EPI ? ((iter & 1) ? a.xb1 : a.xb0) + (size_t)fr * a.P : nullptr;
-    const bool run = EPI && pix >= 0 && !a.st->fr[fr].stopped;
+    const bool run = EPI && pix >= 0 && !fr_stopped;
     float xv = 0.f, tvg = 0.f;
     if (run) {
         xv = x[pix];
-        const float beta = (float)a.prm->beta[fr], eps = (float)a.prm->eps;
-        if (beta > 0.f && PK_EPX != 3) tvg = tv_grad_at<float>(x, pix, pix % n, pix / n, n, n, eps * eps);
+        if (beta_tv > 0.f && PK_EPX != 3) tvg = tv_grad_at<float>(x, pix, pix % n, pix / n, n, n, eps_tv * eps_tv);
     }
     // 1) slot sum: thread (sg, q) adds slots s0 + sg, s0 + sg + 4, ... of consumers 4q..4q+3
     //    (16-B loads, 8 in flight); the 4 slot groups are then added in order (deterministic)
@@ -2221,7 +2227,10 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
     __shared__ double red4[4 * kThreads / 32];
     __shared__ double data_s[NF], tv_s[NF];
     __shared__ int last_flag;
-    if (a.solver && a.st->all_stopped) return;
+    // state words first (one round trip with the constant loads below; the stop test and the
+    // iterate's buffer parity wait on it, the measurement / start-value loads do not)
+    const bool stopped = a.solver && a.st->all_stopped;
+    const int it_par = a.tv_here ? (a.st->iter & 1) : 0;
     // grid (M, frames); frame-major layouts: y [f][M][Q], accumulator [f][M][acc_ld], pair
     // table [f][M][TS], x [f][P]
     const int m = blockIdx.x, f = blockIdx.y, tid = threadIdx.x, Q = a.Q;
@@ -2230,21 +2239,6 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
     if (ym) ym += fm * Q;
     float* om = a.trace_out ? a.trace_out + fm * Q : nullptr;
     int32_t* accr = a.acc32 + fm * a.acc32_ld + kAccFront;
-    double tvp = 0.0, l1p = 0.0, badp = 0.0;
-    if (a.tv_here) {  // exact anisotropic TV of x' (recon.py:169-170), sum |x'|, non-finite
-        const int n = a.n, P = n * n, per = (P + gridDim.x - 1) / gridDim.x;
-        const float* x = ((a.st->iter & 1) ? a.xb0 : a.xb1) + (size_t)f * P;  // bp wrote xb[(iter+1)&1]
-        const int p1 = min(P, (int)(blockIdx.x + 1) * per);
-        for (int p = blockIdx.x * per + tid; p < p1; p += kThreads) {
-            const float v = x[p];
-            const float xr = (p % n + 1 < n) ? x[p + 1] : v;
-            const float xd = (p + n < P) ? x[p + n] : v;
-            l1p += (double)fabsf(v);
-            if (!isfinite(v)) badp += 1.0;
-            if (p % n + 1 < n) tvp += (double)fabsf(xr - v);
-            if (p + n < P) tvp += (double)fabsf(xd - v);
-        }
-    }
     // measurements (constant): loaded before the wait (G = 4: after it, with the accumulator
     // words -- 64 registers do not hold both sets across the wait)
     const bool y4ok = ym && (Q & 3) == 0;
@@ -2282,6 +2276,36 @@ __global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float
         }
     };
     if (G <= 2) { load_y(); load_b(); }
+    if (stopped) return;
+    double tvp = 0.0, l1p = 0.0, badp = 0.0;
+    if (a.tv_here) {  // exact anisotropic TV of x' (recon.py:169-170), sum |x'|, non-finite
+        const int n = a.n, P = n * n, per = (P + gridDim.x - 1) / gridDim.x;
+        const float* x = (it_par ? a.xb0 : a.xb1) + (size_t)f * P;  // bp wrote xb[(iter+1)&1]
+        const int p1 = min(P, (int)(blockIdx.x + 1) * per);
+        // two pixels per thread per pass: their 6 loads in flight together
+        for (int pb = blockIdx.x * per + tid; pb < p1; pb += 2 * kThreads) {
+            float v[2], xr[2], xd[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int p = pb + u * kThreads;
+                v[u] = xr[u] = xd[u] = 0.f;
+                if (p < p1) {
+                    v[u] = x[p];
+                    if (p % n + 1 < n) xr[u] = x[p + 1];
+                    if (p + n < P) xd[u] = x[p + n];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int p = pb + u * kThreads;
+                if (p >= p1) break;
+                l1p += (double)fabsf(v[u]);
+                if (!isfinite(v[u])) badp += 1.0;
+                if (p % n + 1 < n) tvp += (double)fabsf(xr[u] - v[u]);
+                if (p + n < P) tvp += (double)fabsf(xd[u] - v[u]);
+            }
+        }
+    }
     griddep_wait();  // the projection's accumulator and scale
     if (a.solver && blockIdx.x == 0 && tid == 0) a.st->fr[f].mxw = 0u;  // (read by the projector: done)
     if (G > 2) { load_y(); load_b(); }
