@@ -1,0 +1,12 @@
+#!/bin/bash
+# GPU suite, default bench, config 2 / 4 bench lines (TAG)
+cd "$(dirname "$0")/.."
+TAG=${1:-e4}
+timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/gputests_$TAG.log 2>&1; echo "tests rc=$?" >> gpurun_out/gputests_$TAG.log
+tail -3 gpurun_out/gputests_$TAG.log
+timeout 300 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
+python tools/bsum.py gpurun_out/bench_$TAG.json
+for c in cfg4 cfg2; do
+  timeout 300 python bench.py --config $c --no-cpu --steps 30 > gpurun_out/bench_${TAG}_$c.json 2>/dev/null
+  python tools/bsum.py gpurun_out/bench_${TAG}_$c.json
+done
