@@ -2139,6 +2139,8 @@ struct FinArgs {
 template <typename T, int NF>
 __device__ __forceinline__ void finalize_objective(const FinArgs<T>& a, int chunks, double* data_s,
                                                    double* tv_s, double* red_d) {
+    __shared__ double l1_s[NF];  // (tv_here) this pass's sum |x'| and non-finite flag per frame
+    __shared__ int nf_s[NF];
 
     if (a.tv_here) {  // symmetric projector, one pass per frame: data, TV, and the epilogue's
                       // deferred sum |x'| and non-finite count (the residual CTAs' partials are
@@ -2158,6 +2160,8 @@ __device__ __forceinline__ void finalize_objective(const FinArgs<T>& a, int chun
             if (threadIdx.x == 0) {
                 data_s[g] = v4[0];
                 tv_s[g] = v4[1];
+                l1_s[g] = v4[2];
+                nf_s[g] = v4[3] > 0.0 ? 1 : 0;
                 if (!a.st->fr[g].stopped) {
                     a.st->fr[g].l1sum = v4[2];
                     a.st->fr[g].nonfinite = v4[3] > 0.0 ? 1 : 0;
@@ -2181,53 +2185,71 @@ __device__ __forceinline__ void finalize_objective(const FinArgs<T>& a, int chun
             }
         }
     }
-    if (threadIdx.x != 0) return;
-    if (a.sumsq_out)
+    // objective and stopping rules: lane g of warp 0 takes frame g (recon.py:346-363), every
+    // state / parameter word it reads loaded up front -- one round trip per launch instead of
+    // a chain of dependent loads per frame behind the history stores
+    if (threadIdx.x >= 32) return;
+    __syncwarp();  // thread 0's shared / global writes above are visible to the warp
+    if (threadIdx.x == 0 && a.sumsq_out)
         for (int g = 0; g < NF; ++g) a.sumsq_out[g] = data_s[g];
     if (!a.solver) return;
-    // objective and stopping per frame (recon.py:346-363)
     DevState* st = a.st;
     const DevParams* prm = a.prm;
     const int it = st->iter;
     const int N = prm->iterations;
-    int all = 1;
-    for (int g = 0; g < NF; ++g) {
+    const int g = threadIdx.x;
+    int stopped_g = 1;
+    if (g < NF) {
         FrameState& fs = st->fr[g];
-        if (!fs.stopped) {
+        const FrameState f = fs;  // every field, before any store of this frame
+        const double alpha = prm->alpha[g], beta = prm->beta[g], tol = prm->tolerance;
+        const double l1sum = a.tv_here ? l1_s[g] : f.l1sum;
+        const int nonfinite = a.tv_here ? nf_s[g] : f.nonfinite;
+        int stopped = f.stopped, stopped_by = f.stopped_by, accepted = f.accepted;
+        if (!stopped) {
             const double data = data_s[g];
-            const double l1 = prm->alpha[g] * fs.l1sum;
-            const double tv = prm->beta[g] * tv_s[g];
+            const double l1 = alpha * l1sum;
+            const double tv = beta * tv_s[g];
             const double total = data + l1 + tv;
-            if (!isfinite(total) || fs.nonfinite) {
-                fs.stopped = 1;
-                fs.stopped_by = PK_STOP_DIVERGENCE;
+            if (!isfinite(total) || nonfinite) {
+                stopped = 1;
+                stopped_by = PK_STOP_DIVERGENCE;
             } else {
                 double* h = a.io->hist + (size_t)g * 4 * N;
                 h[it] = total;
                 h[N + it] = data;
                 h[2 * N + it] = l1;
                 h[3 * N + it] = tv;
-                fs.accepted = it + 1;
-                fs.grow = total > fs.f_prev ? fs.grow + 1 : 0;
-                if (fs.grow >= kDivergenceStreak) {
-                    fs.stopped = 1;
-                    fs.stopped_by = PK_STOP_DIVERGENCE;
+                accepted = it + 1;
+                fs.accepted = accepted;
+                const int grow = total > f.f_prev ? f.grow + 1 : 0;
+                fs.grow = grow;
+                if (grow >= kDivergenceStreak) {
+                    stopped = 1;
+                    stopped_by = PK_STOP_DIVERGENCE;
                 } else {
-                    const double rel = fabs(total - fs.f_prev) / fmax(fabs(fs.f_prev), 1e-300);
+                    const double rel = fabs(total - f.f_prev) / fmax(fabs(f.f_prev), 1e-300);
                     fs.f_prev = total;
-                    if (prm->tolerance > 0.0 && rel < prm->tolerance) {
-                        fs.stopped = 1;
-                        fs.stopped_by = PK_STOP_TOLERANCE;
+                    if (tol > 0.0 && rel < tol) {
+                        stopped = 1;
+                        stopped_by = PK_STOP_TOLERANCE;
                     }
                 }
             }
+            if (stopped) {
+                fs.stopped = 1;
+                fs.stopped_by = stopped_by;
+            }
         }
-        all &= fs.stopped;
-        a.io->status[2 * g] = fs.accepted;
-        a.io->status[2 * g + 1] = fs.stopped_by;
+        stopped_g = stopped;
+        a.io->status[2 * g] = accepted;
+        a.io->status[2 * g + 1] = stopped_by;
     }
-    st->iter = it + 1;
-    st->all_stopped = (all || st->iter >= N) ? 1 : 0;
+    const bool all = __all_sync(0xffffffffu, stopped_g != 0);
+    if (g == 0) {
+        st->iter = it + 1;
+        st->all_stopped = (all || it + 1 >= N) ? 1 : 0;
+    }
 }
 
 template <typename T, int NF>
