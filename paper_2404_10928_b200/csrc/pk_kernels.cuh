@@ -2146,25 +2146,36 @@ __device__ __forceinline__ void finalize_objective(const FinArgs<T>& a, int chun
                       // deferred sum |x'| and non-finite count (the residual CTAs' partials are
                       // aligned: frame g's are [g * ntv, (g + 1) * ntv))
         __shared__ double red4l[4 * kThreads / 32];
-#pragma unroll 1
+        // every frame's partials loaded in one pass (one round trip, not one per frame); per
+        // frame the same per-thread order and block reduction as frame by frame
+        double v[NF][4];
+        int stp[NF];
+#pragma unroll
         for (int g = 0; g < NF; ++g) {
-            double v4[4] = {0.0, 0.0, 0.0, 0.0};
-            const size_t o = (size_t)g * a.ntv;
-            for (int q = threadIdx.x; q < a.ntv; q += kThreads) {
-                v4[0] += a.part_r[o + q];
-                v4[1] += a.part_tv[o + q];
-                v4[2] += a.part_l1[2 * (o + q)];
-                v4[3] += a.part_l1[2 * (o + q) + 1];
+            v[g][0] = v[g][1] = v[g][2] = v[g][3] = 0.0;
+            stp[g] = threadIdx.x == 0 ? a.st->fr[g].stopped : 1;
+        }
+        for (int q = threadIdx.x; q < a.ntv; q += kThreads) {
+#pragma unroll
+            for (int g = 0; g < NF; ++g) {
+                const size_t o = (size_t)g * a.ntv + q;
+                v[g][0] += a.part_r[o];
+                v[g][1] += a.part_tv[o];
+                v[g][2] += a.part_l1[2 * o];
+                v[g][3] += a.part_l1[2 * o + 1];
             }
-            block_sum4(v4, red4l);
+        }
+#pragma unroll
+        for (int g = 0; g < NF; ++g) {
+            block_sum4(v[g], red4l);
             if (threadIdx.x == 0) {
-                data_s[g] = v4[0];
-                tv_s[g] = v4[1];
-                l1_s[g] = v4[2];
-                nf_s[g] = v4[3] > 0.0 ? 1 : 0;
-                if (!a.st->fr[g].stopped) {
-                    a.st->fr[g].l1sum = v4[2];
-                    a.st->fr[g].nonfinite = v4[3] > 0.0 ? 1 : 0;
+                data_s[g] = v[g][0];
+                tv_s[g] = v[g][1];
+                l1_s[g] = v[g][2];
+                nf_s[g] = v[g][3] > 0.0 ? 1 : 0;
+                if (!stp[g]) {
+                    a.st->fr[g].l1sum = v[g][2];
+                    a.st->fr[g].nonfinite = v[g][3] > 0.0 ? 1 : 0;
                 }
             }
         }
