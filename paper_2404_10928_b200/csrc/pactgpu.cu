@@ -503,10 +503,14 @@ void launch_bp_t(pk_plan* p, int epi, void* out, double gscale_mult, cudaStream_
         const dim3 eg(p->sym_ntiles * 32 * NF);
         if (A.fuse) return;
         if (p->bp_mid_event) cudaEventRecord(p->bp_mid_event, s);
-        // batched plans: the 4-strip epilogue (4 frames, config 3: 26.9 -> 23.8 us); one frame
-        // per launch keeps the one-strip kernel (11.6 vs 10.8 us: 13 slots per tile, 288 CTAs)
-        if (epi && p->fsym && p->sym_epi4 && NF > 1)
-            launch_pdl(bp_sym_epi4_kernel, dim3(p->sym_ntiles * 8 * NF), dim3(kThreads), 0, s, E);
+        // strips per epilogue CTA (config 3, warm, one / four frames per launch): 1 strip 10.6 /
+        // 27.1 us, 2 strips 9.2 / 22.9, 4 strips 11.8 / 23.7 (too few CTAs at one frame, ~13
+        // slots per tile); PK_SYM_EPIK forces 1 (the one-strip kernel), 2 or 4
+        const int ks = p->sym_epik > 0 ? p->sym_epik : 2;
+        if (epi && p->fsym && ks == 4)
+            launch_pdl(bp_sym_epik_kernel<4>, dim3(p->sym_ntiles * 8 * NF), dim3(kThreads), 0, s, E);
+        else if (epi && p->fsym && ks == 2)
+            launch_pdl(bp_sym_epik_kernel<2>, dim3(p->sym_ntiles * 16 * NF), dim3(kThreads), 0, s, E);
         else if (epi && p->fsym) launch_pdl(bp_sym_epi_kernel<true, true>, eg, dim3(kThreads), 0, s, E);
         else if (epi) launch_pdl(bp_sym_epi_kernel<true, false>, eg, dim3(kThreads), 0, s, E);
         else launch_pdl(bp_sym_epi_kernel<false, false>, eg, dim3(kThreads), 0, s, E);
@@ -985,8 +989,11 @@ int pk_plan_create(const pk_geometry_desc* d, pk_plan** out) {
             // 57.0 us vs 41.1 + 9.7 us for the separate epilogue)
             p->sym_fuse = 0;
             if (const char* e = getenv("PK_SYM_FUSE")) p->sym_fuse = atoi(e) != 0;
-            p->sym_epi4 = 1;
-            if (const char* e = getenv("PK_SYM_EPI4")) p->sym_epi4 = atoi(e) != 0;
+            p->sym_epik = 0;  // (0: by frames per launch)
+            if (const char* e = getenv("PK_SYM_EPIK")) {
+                const int v = atoi(e);
+                p->sym_epik = (v == 1 || v == 2 || v == 4) ? v : 0;
+            }
             if (const char* e = getenv("PK_SYM_SPIN_NS")) p->sym_spin_ns = std::max(0LL, atoll(e));
             if (const char* e = getenv("PK_SYM_LANEMAP")) p->sym_lanemap = atoi(e) != 0;
             p->sym_smem = p->sym_nbuf * per_buf;

@@ -361,7 +361,7 @@ struct pk_plan {
     int sym_slots_cap = 0;  // partial slots allocated (the largest candidate partition's)
     int sym_lanemap = 1;
     int sym_fuse = 0;     // update fused into the back-projector's tail (solver mode, opt-in)
-    int sym_epi4 = 1;     // batched solver epilogue (deferred stats): one CTA per (tile, image), 4 strips
+    int sym_epik = 0;     // solver epilogue strips per CTA (deferred stats): 0 = default (2), 1, 2, 4
     int *sym_tiles = nullptr, *sym_chunks = nullptr, *sym_cta_chunk0 = nullptr,
         *sym_cta_slot0 = nullptr, *sym_tile_slot0 = nullptr;
     float* sym_part = nullptr;  // [slots][8][4][kThreads] partial sums

@@ -1019,22 +1019,27 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi_kernel(BpSymEpiArgs a) {
 }
 
 // Solver-mode epilogue with deferred statistics (the bench's path), one CTA per (tile, image
-// g) doing all 4 strips of bp_sym_epi_kernel<true, true>'s (tile, image, strip) CTAs: the
-// strips' loads (iterate, TV gradient before the PDL wait; partial slots after it) are in
+// g, block of KS strips) doing KS of bp_sym_epi_kernel<true, true>'s (tile, image, strip) CTAs:
+// the strips' loads (iterate, TV gradient before the PDL wait; partial slots after it) are in
 // flight together and the per-CTA fixed costs (state loads, barriers, max reduction, atomic)
-// are paid once per 4 strips.  Per pixel the same arithmetic and the same slot order (slot
+// are paid once per KS strips.  Per pixel the same arithmetic and the same slot order (slot
 // group sg adds slots s0 + sg, s0 + sg + 4, ... in increasing order, then the groups 0..3 in
 // order), so the result is bitwise that of bp_sym_epi_kernel: the zero padding of its 8-wide
 // slot batches is skipped, and adding +0.0f to a sum that starts at +0.0f is exact (such a sum
-// is never -0.0f).  Batched plans only (NF > 1); PK_SYM_EPI4=0 restores the one-strip kernel.
-__global__ void __launch_bounds__(kThreads) bp_sym_epi4_kernel(BpSymEpiArgs a) {
+// is never -0.0f).  KS = 2 by default (config 3: 9.2 / 22.9 us at one / four frames per
+// launch against 10.6 / 27.1 for one strip and 11.8 / 23.7 for four); PK_SYM_EPIK=1 restores
+// the one-strip kernel (2 / 4 force KS).
+template <int KS>
+__global__ void __launch_bounds__(kThreads) bp_sym_epik_kernel(BpSymEpiArgs a) {
     __shared__ float red_f[kThreads / 32];
-    __shared__ float4 part4[4][3][64];         // [strip][slot group 1..3][consumer quad]
-    __shared__ float blk[4][8 * kSymTile];     // strip k in image g, row-major (bw x bh)
+    __shared__ float4 part4[KS][3][64];        // [strip][slot group 1..3][consumer quad]
+    __shared__ float blk[KS][8 * kSymTile];    // strip k0 + k in image g, row-major (bw x bh)
     // state words with the tile loads (one round trip)
     const bool all_st = a.st->all_stopped;
     const int iter = a.st->iter;
-    const int g = blockIdx.x & 7, t = blockIdx.x >> 3;  // t: frame-major tile
+    constexpr int NB = 4 / KS;  // strip blocks per (tile, image)
+    const int kb = blockIdx.x % NB, g = (blockIdx.x / NB) & 7, t = blockIdx.x / (8 * NB);  // t: frame-major
+    const int k0 = kb * KS;
     const int fr = t / a.ntiles;
     const int tp = __ldg(a.tiles + t - fr * a.ntiles);
     const int s0 = __ldg(a.tile_slot0 + t), s1 = __ldg(a.tile_slot0 + t + 1);
@@ -1046,11 +1051,11 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi4_kernel(BpSymEpiArgs a) {
     if (all_st || (tx == ty && g >= 4)) return;  // (reflections of a diagonal tile: no pixels)
     const int n = a.n, h = n >> 1;
     const int i0 = h + kSymTile * tx, j0 = h + kSymTile * ty;
-    // strip k's image under g: the block [bx, bx + bw) x [by, by + bh), bw * bh = 256
+    // strip k0 + k's image under g: the block [bx, bx + bw) x [by, by + bh), bw * bh = 256
     auto strip_box = [&](int k, int& bx, int& by, int& bw) {
         int ia, ja, ib, jb;
-        sym_pixel(g, i0 + 8 * k, j0, n, ia, ja);
-        sym_pixel(g, i0 + 8 * k + 7, j0 + kSymTile - 1, n, ib, jb);
+        sym_pixel(g, i0 + 8 * (k0 + k), j0, n, ia, ja);
+        sym_pixel(g, i0 + 8 * (k0 + k) + 7, j0 + kSymTile - 1, n, ib, jb);
         bx = min(ia, ib);
         by = min(ja, jb);
         bw = abs(ib - ia) + 1;
@@ -1058,10 +1063,10 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi4_kernel(BpSymEpiArgs a) {
     // one pixel per thread and strip (image-row-major order of the strip); iterate value and
     // TV gradient loaded before the wait (final since the previous iteration)
     const float* x = ((iter & 1) ? a.xb1 : a.xb0) + (size_t)fr * a.P;
-    int pix[4];
-    float xv[4], tvg[4];
+    int pix[KS];
+    float xv[KS], tvg[KS];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < KS; ++k) {
         int bx, by, bw;
         strip_box(k, bx, by, bw);
         const int ig = bx + threadIdx.x % bw, jg = by + threadIdx.x / bw;
@@ -1074,28 +1079,28 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi4_kernel(BpSymEpiArgs a) {
         }
     }
     // slot sums: thread (sg, q) adds slots s0 + sg, s0 + sg + 4, ... of consumers 4q..4q+3 of
-    // every strip (two slots x 4 strips = 8 16-B loads in flight per pass)
+    // every strip (two slots x KS strips of 16-B loads in flight per pass)
     const int sg = threadIdx.x >> 6, q = threadIdx.x & 63;
     griddep_wait();  // partial slots of the main kernel
-    float4 sum[4];
+    float4 sum[KS];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) sum[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < KS; ++k) sum[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     {
-        const float4* src = reinterpret_cast<const float4*>(a.part + (size_t)(g * 4) * kThreads) + q;
+        const float4* src = reinterpret_cast<const float4*>(a.part + (size_t)(g * 4 + k0) * kThreads) + q;
         const size_t stride = 8 * 4 * kThreads / 4;  // float4s per slot
         for (int sb = s0 + sg; sb < s1; sb += 8) {
-            float4 v[2][4];
+            float4 v[2][KS];
 #pragma unroll
             for (int u = 0; u < 2; ++u)
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
+                for (int k = 0; k < KS; ++k)
                     v[u][k] = (sb + 4 * u < s1) ? __ldcg(src + k * (kThreads / 4) + (size_t)(sb + 4 * u) * stride)
                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 if (sb + 4 * u >= s1) break;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < KS; ++k) {
                     sum[k].x += v[u][k].x; sum[k].y += v[u][k].y; sum[k].z += v[u][k].z; sum[k].w += v[u][k].w;
                 }
             }
@@ -1103,13 +1108,13 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi4_kernel(BpSymEpiArgs a) {
     }
     if (sg > 0) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) part4[k][sg - 1][q] = sum[k];
+        for (int k = 0; k < KS; ++k) part4[k][sg - 1][q] = sum[k];
     }
     __syncthreads();
     // slot group 0 finishes the sums and scatters them into the strips (shared transpose)
     if (sg == 0) {
-#pragma unroll 1
-        for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int k = 0; k < KS; ++k) {
             float4 sm = sum[k];
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
@@ -1125,7 +1130,7 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi4_kernel(BpSymEpiArgs a) {
                 int lx, ly;
                 sym_lane_xy(c & 31, a.lanemap, lx, ly);
                 int ig, jg;
-                sym_pixel(g, i0 + lx + 8 * k, j0 + 4 * (c >> 5) + ly, n, ig, jg);
+                sym_pixel(g, i0 + lx + 8 * (k0 + k), j0 + 4 * (c >> 5) + ly, n, ig, jg);
                 blk[k][(jg - by) * bw + (ig - bx)] = a.gscale * sv[u];
             }
         }
@@ -1136,7 +1141,7 @@ __global__ void __launch_bounds__(kThreads) bp_sym_epi4_kernel(BpSymEpiArgs a) {
     float* xr = a.xr ? a.xr + (size_t)fr * a.P : nullptr;
     float mx = 0.f;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < KS; ++k) {
         const int p = pix[k];
         if (p < 0) continue;
         float gr = blk[k][threadIdx.x];

@@ -289,19 +289,19 @@ def test_tuned_chunk_ranges_agree(monkeypatch, oracle):
         assert rel(im, ref) <= 1e-4
 
 
-@pytest.mark.parametrize("frames", [2, 4])
-def test_four_strip_epilogue_matches_one_strip_kernel(monkeypatch, frames):
-    """The solver epilogue with one CTA per (tile, image) doing 4 strips (bp_sym_epi4_kernel,
-    the default of batched plans) is bitwise the one-strip kernel (PK_SYM_EPI4=0): same slot
-    order per pixel, the skipped zero padding is exact.  Image, history and status of 2- and
-    4-frame batches."""
+@pytest.mark.parametrize("frames", [1, 2, 4])
+def test_multi_strip_epilogue_matches_one_strip_kernel(monkeypatch, frames):
+    """The solver epilogue with one CTA per (tile, image, block of 2 or 4 strips)
+    (bp_sym_epik_kernel; 2 strips by default) is bitwise
+    the one-strip kernel (PK_SYM_EPIK=1): same slot order per pixel, the skipped zero padding
+    is exact.  Image, history and status, one frame and 2- and 4-frame batches."""
     n, M, Q, N = 256, 256, 2048, 6
     grid, ring, ac, ph = pk.make_scene(n, M, Q, 5)
     alpha, beta, step = 2.0817e-8, 2.0817e-10, 2651.30  # survey-pinned config 2
     params = pk.solver.solver_params(pk.ReconConfig(alpha, beta, N, step), alpha, beta, step)
     out = {}
-    for e4 in ("0", "1"):
-        monkeypatch.setenv("PK_SYM_EPI4", e4)
+    for ks in ("1", "2", "4"):
+        monkeypatch.setenv("PK_SYM_EPIK", ks)
         pk.clear_plan_cache()
         op = pk.operator_for(grid, ring, ac, F32, frames=frames)
         assert op.info.symmetric == 3
@@ -309,8 +309,9 @@ def test_four_strip_epilogue_matches_one_strip_kernel(monkeypatch, frames):
         runs = [[t.cpu().numpy() for t in op.reconstruct(y, params)] for _ in range(2)]
         for a_, b_ in zip(runs[0], runs[1]):
             assert np.array_equal(a_, b_)  # graph replay
-        out[e4] = runs[1]
+        out[ks] = runs[1]
     pk.clear_plan_cache()
     assert (out["1"][2][:, 0] == N).all()
-    for a_, b_ in zip(out["0"], out["1"]):
-        assert np.array_equal(a_, b_)
+    for ks in ("2", "4"):
+        for a_, b_ in zip(out["1"], out[ks]):
+            assert np.array_equal(a_, b_)
