@@ -69,6 +69,8 @@ def parse():
                     help="frames reconstructed per launch (default 4 for the cfg4 sequence, else 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true",
+                    help="skip the fp64-mode line (the reference's arithmetic on the device)")
     ap.add_argument("--no-ncu", action="store_true",
                     help="skip the ncu capture of the dominant kernel's DRAM traffic (roofline.traffic)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -516,6 +518,34 @@ def main():
         torch.cuda.synchronize(dev)
         latency_ms = l0.elapsed_time(l1) / nlat
 
+    # ---- fp64 validation mode (the reference's arithmetic, fp64 kernels): one frame per
+    # launch on the fp64 plan, the same pinned parameters; outside the timed region ----
+    fp64_mode = None
+    if not sensor_mode and not args.no_fp64 and args.config != "cfg5":
+        y64 = op64.matvec(ph0.values).contiguous()
+        x64 = torch.empty(P, device=dev, dtype=torch.float64)
+        h64 = torch.zeros(4 * cfg.iterations, device=dev, dtype=torch.float64)
+        s64 = torch.zeros(2, device=dev, dtype=torch.int32)
+        p64 = (N.SolverParams * 1)(params)
+
+        def step64():
+            N.check(lib.pk_reconstruct(op64.handle, p64, y64.data_ptr(), x64.data_ptr(),
+                                       h64.data_ptr(), s64.data_ptr(), stream_ptr()))
+        step64()  # plan warm-up (graph capture)
+        n64 = 3
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(n64):
+            step64()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms64 = e0.elapsed_time(e1) / n64
+        if int(s64[0]) != cfg.iterations:
+            raise SystemExit(f"bench: fp64 solve ran {int(s64[0])} of {cfg.iterations} iterations")
+        fp64_mode = {"frames_per_s": 1e3 / ms64, "ms_per_frame": ms64, "frames_timed": n64,
+                     "path": "pk_reconstruct on an fp64 plan (CudaPool float64: fp64 delays, "
+                             "int64 fixed-point projector), frame 0, one frame per launch"}
+
     # ---- roofline of the dominant kernel (CUDA events around each launch) ----
     roof, kernels = None, None
     if not sensor_mode:
@@ -756,6 +786,7 @@ def main():
             # one frame at a time on one stream, latency-mode plan (the timed region keeps SS
             # frames in flight on throughput-mode plans)
             "latency_ms_per_frame": latency_ms if latency_ms is not None else ms_step,
+            "fp64_mode": fp64_mode,
             "higher_is_better": True,
             # frames mode: each rank reconstructs its own frames (per-GPU work fixed as N grows)
             "scaling": "strong" if (sensor_mode or seq) else "weak",
