@@ -2395,8 +2395,11 @@ __global__ void __launch_bounds__(kThreads, PK_FIN_MINB) finalize_kernel(FinArgs
 constexpr int kFinSymG = 4;
 constexpr int kFinSymMax = 4 * kThreads * kFinSymG;  // 4096 samples
 constexpr int kFinSymB = 3;  // start-value words (uint2 = 4 samples) per thread held in registers
+#ifndef PK_FINSYM_MINB
+#define PK_FINSYM_MINB 4  // CTAs per SM the residual kernel is compiled for (timing sweeps: 3)
+#endif
 template <int NF, int G>
-__global__ void __launch_bounds__(kThreads, 4) finalize_sym_kernel(FinArgs<float> a) {
+__global__ void __launch_bounds__(kThreads, PK_FINSYM_MINB) finalize_sym_kernel(FinArgs<float> a) {
     __shared__ double red_d[kThreads / 32];
     __shared__ double red4[4 * kThreads / 32];
     __shared__ double data_s[NF], tv_s[NF];
